@@ -1,0 +1,219 @@
+/* gapa_cuda.h — C ABI of the B200 (sm_100a) implementation of GAPA's
+ * data-parallel hot path: per-generation batched fitness evaluation of a GA
+ * population over perturbed graphs, plus the genetic operators around it.
+ *
+ * This is the drop-in boundary.  Every entry point replaces one interface of
+ * the reference C++ library (citations are file:line under
+ * /root/reference/proj); host C++ (paper_2412_20980_b200/host/) and the Python
+ * driver bind exactly these symbols, and nothing else crosses the boundary:
+ * plain pointers and sizes, no STL, no exceptions, no torch types.
+ *
+ * Conventions
+ *   - every function returns an int status: 0 = ok, otherwise a GAPA_CUDA_E_*
+ *     code; gapa_cuda_last_error() returns the message for the calling thread
+ *     (the host adapters turn a non-zero status into `throw gapa::Error`,
+ *     include/gapa/error.hpp:9-30).
+ *   - "host" pointers are ordinary CPU memory; "_device" entry points take
+ *     device pointers valid on the context's GPU and a cudaStream_t passed as
+ *     void* (NULL = the legacy default stream).  They enqueue work and
+ *     return; the caller synchronises the stream (gapa_cuda_stream_sync).
+ *   - gene matrices are row-major int32 [rows x cols] (population.hpp:12-40);
+ *     fitness vectors are double[rows] (population.hpp:62).
+ *   - there is NO CPU fallback: without a CUDA device every call fails with
+ *     GAPA_CUDA_E_CUDA.
+ */
+#ifndef GAPA_CUDA_H
+#define GAPA_CUDA_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GAPA_CUDA_ABI_VERSION 1
+
+enum {
+    GAPA_CUDA_OK = 0,
+    GAPA_CUDA_E_INVALID = 1,  /* bad argument / shape / wrong pool kind (fitness.cpp:50-57)   */
+    GAPA_CUDA_E_RANGE = 2,    /* gene id outside the pool (gene_pool.cpp:104-108)             */
+    GAPA_CUDA_E_NAN = 3,      /* NaN / non-finite fitness (ga_ops.cpp:56-57, :189-192)        */
+    GAPA_CUDA_E_CUDA = 4,     /* CUDA runtime failure, or no device                           */
+    GAPA_CUDA_E_NOMEM = 5
+};
+
+/* fitness tasks — the four objectives of fitness.hpp:33-52 */
+enum {
+    GAPA_TASK_PC = 0,  /* pairwise connectivity, pc_fitness        (fitness.cpp:28-33)  */
+    GAPA_TASK_MCN = 1, /* largest component, sixdst_fitness(Exact) (fitness.cpp:18-26)  */
+    GAPA_TASK_CDA = 2, /* modularity of the greedy detector        (fitness.cpp:35-41)  */
+    GAPA_TASK_LPA = 3  /* AUC of the RA predictor                  (fitness.cpp:43-48)  */
+};
+
+/* PoolKind, gene_pool.hpp:14 (same order) */
+enum { GAPA_POOL_EDGE_REMOVAL = 0, GAPA_POOL_EDGE_ADDITION = 1, GAPA_POOL_NODE_REMOVAL = 2 };
+
+/* StreamRole, rng.hpp:41-47 */
+enum { GAPA_ROLE_INIT = 1, GAPA_ROLE_SELECT = 2, GAPA_ROLE_CROSSOVER_MASK = 3,
+       GAPA_ROLE_MUTATION_MASK = 4, GAPA_ROLE_MUTATION_INDEX = 5 };
+
+typedef struct gapa_cuda_ctx gapa_cuda_ctx; /* graph + pool + split on one GPU */
+
+const char* gapa_cuda_last_error(void);
+int gapa_cuda_abi_version(void);
+int gapa_cuda_device_count(int* count);
+
+/* ---- graph / pool / split ------------------------------------------------------
+ * gapa_cuda_graph_create replaces Graph::adjacency() (graph.cpp:47-54) and the
+ * per-objective BitMatrix copies (fitness.cpp:94-113): ONE read-only CSR per GPU,
+ * shared by every individual, never copied.  `uv` holds m canonical edges
+ * (Graph::edges(), graph.hpp:26; either endpoint order accepted, loops and
+ * duplicates rejected like graph.cpp:26-31). */
+int gapa_cuda_graph_create(int32_t n, int64_t m, const int32_t* uv, int device, gapa_cuda_ctx** out);
+/* Same, from a ready CSR (row_ptr[n+1], col_idx[2m] ascending per row, symmetric). */
+int gapa_cuda_graph_create_csr(int32_t n, int64_t m, const int32_t* row_ptr, const int32_t* col_idx,
+                               int device, gapa_cuda_ctx** out);
+int gapa_cuda_destroy(gapa_cuda_ctx* ctx);
+int gapa_cuda_graph_info(const gapa_cuda_ctx* ctx, int32_t* n, int64_t* m, int* device);
+
+/* GenePool (gene_pool.hpp:32-52).  kind NODE_REMOVAL: u[i] = node of gene i
+ * (u == NULL means the identity pool of build_gene_pool, gene_pool.cpp:89-92),
+ * v ignored.  kind EDGE_REMOVAL: (u[i], v[i]) must be edges of the graph
+ * (u == NULL means build_gene_pool's (u,v)-sorted order, gene_pool.cpp:73-79).
+ * EDGE_ADDITION is not on this path yet and returns GAPA_CUDA_E_INVALID. */
+int gapa_cuda_pool_set(gapa_cuda_ctx* ctx, int kind, int32_t n_genes, const int32_t* u, const int32_t* v);
+int gapa_cuda_pool_info(const gapa_cuda_ctx* ctx, int* kind, int32_t* n_genes);
+
+/* LinkPredictionSplit (link_prediction.hpp:16-21): the context's graph is
+ * split.train; test_uv / probe_uv are T and P (u,v) pairs. */
+int gapa_cuda_lp_split_set(gapa_cuda_ctx* ctx, int32_t T, const int32_t* test_uv, int32_t P,
+                           const int32_t* probe_uv);
+
+/* ---- fitness: FitnessFunction::evaluate_batch (fitness.hpp:17-27) ----------------
+ * out[i] = fitness of row i, identical to the reference's evaluate_one on
+ * that row (fitness.cpp:10-14).  cols may be 0 (empty perturbation), rows may be 0.
+ * Host form: H2D of genes + kernels + D2H of out, synchronous. */
+int gapa_cuda_eval_batch(gapa_cuda_ctx* ctx, int task, const int32_t* genes_host, int rows, int cols,
+                         double* out_host);
+/* Device form: genes and out live in HBM; synchronises `stream` before returning
+ * only as far as needed to report status (gene range / NaN). */
+int gapa_cuda_eval_batch_device(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, int cols,
+                                double* out_dev, void* stream);
+
+/* ---- genetic operators on HBM-resident populations (ga_ops.hpp:30-93) ------------
+ * All keyed by (seed, generation, role, GLOBAL row) exactly like rng.hpp:59-65,
+ * so any row partition reproduces the same matrices. */
+
+/* init_population_block (ga_ops.cpp:19-29): out_dev[row_count x budget] */
+int gapa_cuda_ga_init_device(int32_t pool_size, int row_first, int row_count, int budget, uint64_t seed,
+                             uint64_t generation, int32_t* out_dev, void* stream);
+/* roulette_select in index form (ga_ops.cpp:54-82,105-128): rank weights with
+ * tie-span averaging -> cumulative -> one Select draw per row -> partner row.
+ * weights_dev / scratch may be NULL.  Non-finite fitness -> GAPA_CUDA_E_NAN. */
+int gapa_cuda_ga_select_device(const double* fitness_dev, int s, int minimize, uint64_t seed,
+                               uint64_t generation, int32_t* partner_dev, double* weights_dev, void* stream);
+/* crossover (ga_ops.cpp:130-144) fused with mutate_block (ga_ops.cpp:164-178) for
+ * rows [row_first, row_first+row_count) of the population; pop_dev is the FULL
+ * s x k matrix, partner_dev the full partner vector, out_dev the block. */
+int gapa_cuda_ga_crossover_mutate_device(const int32_t* pop_dev, const int32_t* partner_dev, int s, int k,
+                                         int row_first, int row_count, double pc, double pm,
+                                         int32_t pool_size, uint64_t seed, uint64_t generation,
+                                         int32_t* out_dev, void* stream);
+/* mutate_block alone (used after eda_sample, modes.cpp:167-173) */
+int gapa_cuda_ga_mutate_device(const int32_t* block_dev, int rows, int k, int row_offset, double pm,
+                               int32_t pool_size, uint64_t seed, uint64_t generation, int32_t* out_dev,
+                               void* stream);
+/* eda_sample (ga_ops.cpp:214-238) */
+int gapa_cuda_ga_eda_device(const int32_t* elite_dev, int s, int k, int elite_count, int32_t pool_size,
+                            uint64_t seed, uint64_t generation, int smoothing, int32_t* out_dev, void* stream);
+/* elitism (ga_ops.cpp:180-212): stable best-first order of the 2s stacked rows,
+ * originals before mutated on ties; next_dev must not alias pop_dev / m_pop_dev. */
+int gapa_cuda_ga_elitism_device(const int32_t* pop_dev, const int32_t* m_pop_dev, int s, int k,
+                                const double* fit_dev, const double* fit_m_dev, int minimize,
+                                int32_t* next_dev, double* next_fit_dev, void* stream);
+
+/* Host-buffer forms of the same operators (H2D, kernel, D2H, synchronous) — the
+ * exact shapes of the reference free functions, used by the host adapters and
+ * the parity tests.  `device` selects the GPU. */
+int gapa_cuda_ga_init(int device, int32_t pool_size, int row_first, int row_count, int budget, uint64_t seed,
+                      uint64_t generation, int32_t* out);
+int gapa_cuda_ga_selection_weights(int device, const double* fitness, int s, int minimize, double* weights);
+int gapa_cuda_ga_select(int device, const double* fitness, int s, int minimize, uint64_t seed,
+                        uint64_t generation, int32_t* partner_index);
+int gapa_cuda_ga_crossover_mutate(int device, const int32_t* pop, const int32_t* partner_index, int s, int k,
+                                  int row_first, int row_count, double pc, double pm, int32_t pool_size,
+                                  uint64_t seed, uint64_t generation, int32_t* out);
+int gapa_cuda_ga_mutate(int device, const int32_t* block, int rows, int k, int row_offset, double pm,
+                        int32_t pool_size, uint64_t seed, uint64_t generation, int32_t* out);
+int gapa_cuda_ga_eda(int device, const int32_t* elite, int s, int k, int elite_count, int32_t pool_size,
+                     uint64_t seed, uint64_t generation, int smoothing, int32_t* out);
+int gapa_cuda_ga_elitism(int device, const int32_t* pop, const int32_t* m_pop, int s, int k, const double* fit,
+                         const double* fit_m, int minimize, int32_t* next, double* next_fit);
+/* first `count` raw draws of RngPolicy(seed).stream(generation, role, row)
+ * (rng.hpp:21) computed ON THE DEVICE — the known-answer hook for the RNG twin */
+int gapa_cuda_rng_draws(int device, uint64_t seed, uint64_t generation, uint64_t role, uint64_t row, int count,
+                        uint64_t* out);
+
+/* ---- generation loop (modes.cpp:132-178 == run_serial :359-418) ------------------ */
+typedef struct gapa_cuda_run_params {
+    double pc, pm;          /* GAParams, ga_ops.hpp:12-23 */
+    int32_t pop_size;       /* s >= 2  */
+    int32_t budget;         /* k >= 1  */
+    int32_t iterations;     /* >= 1 (modes.cpp:26-29) */
+    int32_t minimize;       /* Direction */
+    int32_t eda_interval;   /* 0 = none */
+    int32_t task;           /* GAPA_TASK_* */
+    uint64_t seed;
+    /* population sharding (modes.cpp:506-516): this process evaluates block
+     * `rank` of partition_rows(s, world); 0/1 = single GPU. */
+    int32_t rank, world;
+} gapa_cuda_run_params;
+
+/* Exchange hook for world > 1: must fill fit_full_dev[s] from every rank's
+ * block fit_full_dev[lo..hi) (an all-gather; NCCL over NVLink in the Python
+ * driver).  `padded_block` = ceil(s/world).  NULL when world == 1. */
+typedef int (*gapa_cuda_allgather_fn)(void* user, double* fit_full_dev, int s, int padded_block, void* stream);
+
+typedef struct gapa_cuda_run_result {
+    double* history_best;      /* [iterations]  GenerationStats::best  (modes.hpp:63-71) */
+    double* history_mean;      /* [iterations]  GenerationStats::mean                    */
+    int32_t* final_population; /* [s x k]       RunResult::final_population (best first) */
+    double* final_fitness;     /* [s]                                                    */
+    uint64_t fitness_batch_calls;
+    double total_wall_seconds; /* generation loop only */
+    double eval_seconds;       /* device time inside fitness kernels (CUDA events)        */
+} gapa_cuda_run_result;
+
+int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* params, gapa_cuda_allgather_fn exchange,
+                  void* exchange_user, gapa_cuda_run_result* result);
+
+/* ---- host-side problem setup (CPU, once per experiment — inputs to the path) --------
+ * Deterministic generators with the reference's draw sequences (generators.cpp) and
+ * the link-prediction split builder (link_prediction.cpp:11-53).  `uv` receives
+ * canonical (u < v) pairs in insertion order; pass uv == NULL to query *m first. */
+int gapa_host_barabasi_albert(int32_t n, int32_t attach, uint64_t seed, int32_t* uv, int64_t capacity, int64_t* m);
+int gapa_host_erdos_renyi(int32_t n, double p, uint64_t seed, int32_t* uv, int64_t capacity, int64_t* m);
+int gapa_host_planted_partition(int32_t blocks, int32_t block_size, double p_in, double p_out, uint64_t seed,
+                                int32_t* uv, int64_t capacity, int64_t* m);
+/* train_uv[(m-T) x 2], test_uv[T x 2], probe_uv[T x 2]; null outputs = query T */
+int gapa_host_lp_split(int32_t n, int64_t m, const int32_t* edges, double fraction, uint64_t seed,
+                       int32_t* train_uv, int32_t* test_uv, int32_t* probe_uv, int32_t* test_count);
+/* perturbation_budget (gene_pool.cpp:98-102): k = max(1, ceil(rate * basis)) */
+int gapa_host_budget(int64_t basis, double rate, int32_t* k);
+
+/* ---- plumbing for hosts without a CUDA runtime of their own ---------------------- */
+int gapa_cuda_malloc(int device, uint64_t bytes, void** out_dev);
+int gapa_cuda_free(int device, void* dev);
+int gapa_cuda_memcpy_h2d(int device, void* dst_dev, const void* src_host, uint64_t bytes);
+int gapa_cuda_memcpy_d2h(int device, void* dst_host, const void* src_dev, uint64_t bytes);
+int gapa_cuda_stream_sync(int device, void* stream);
+/* launch counter: kernels launched by this library since load (bench.py's gpu_launches) */
+uint64_t gapa_cuda_launch_count(void);
+/* timing of the last eval on a context: device milliseconds between CUDA events
+ * recorded on the eval stream around the kernels only (no copies). */
+int gapa_cuda_last_eval_ms(const gapa_cuda_ctx* ctx, float* ms);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GAPA_CUDA_H */

@@ -1,0 +1,385 @@
+// Context management and the fitness entry points of include/gapa_cuda.h.
+//
+// One gapa_cuda_ctx = one GPU's copy of the read-only problem: the CSR that
+// replaces the reference's dense BitMatrix (graph.cpp:47-54), the gene pool
+// (gene_pool.cpp:69-96) and, for the link-prediction task, the split
+// (link_prediction.hpp:16-21).
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <numeric>
+
+#include "internal.cuh"
+
+namespace gapa_b200 {
+
+static thread_local std::string t_error;
+std::atomic<uint64_t> g_launches{0};
+
+int fail(int code, const char* fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof(buf), fmt, ap);
+    va_end(ap);
+    t_error = buf;
+    return code;
+}
+
+uint64_t bernoulli_threshold(double p) {
+    if (!(p > 0.0)) return 0;
+    if (p >= 1.0) return 1ull << 53;
+    return static_cast<uint64_t>(std::ceil(p * 9007199254740992.0));  // exact scaling by 2^53
+}
+
+static int upload_i32(const std::vector<int32_t>& h, int32_t** d) {
+    GAPA_CUDA_TRY(cudaMalloc(d, sizeof(int32_t) * std::max<size_t>(h.size(), 1)));
+    if (!h.empty()) GAPA_CUDA_TRY(cudaMemcpy(*d, h.data(), sizeof(int32_t) * h.size(), cudaMemcpyHostToDevice));
+    return GAPA_CUDA_OK;
+}
+
+// Edge rank of {u, v} in the (u,v)-sorted edge list, or -1.
+static int32_t edge_rank(const gapa_cuda_ctx* c, int32_t u, int32_t v) {
+    if (u < 0 || v < 0 || u >= c->n || v >= c->n || u == v) return -1;
+    const int32_t* b = c->h_col_idx.data() + c->h_row_ptr[u];
+    const int32_t* e = c->h_col_idx.data() + c->h_row_ptr[u + 1];
+    const int32_t* it = std::lower_bound(b, e, v);
+    if (it == e || *it != v) return -1;
+    return c->h_edge_id[it - c->h_col_idx.data()];
+}
+
+static int finish_create(gapa_cuda_ctx* c, int device, gapa_cuda_ctx** out) {
+    const int32_t n = c->n;
+    const int64_t m = c->m;
+    // edge ranks: (u, v), u < v, in row-major CSR order == lexicographic order
+    c->h_edge_id.assign(static_cast<size_t>(2 * m), 0);
+    std::vector<int32_t> eu(static_cast<size_t>(m)), ev(static_cast<size_t>(m));
+    int32_t next = 0;
+    for (int32_t u = 0; u < n; ++u)
+        for (int32_t i = c->h_row_ptr[u]; i < c->h_row_ptr[u + 1]; ++i) {
+            const int32_t v = c->h_col_idx[i];
+            if (v > u) {
+                c->h_edge_id[i] = next;
+                eu[next] = u;
+                ev[next] = v;
+                ++next;
+            }
+        }
+    if (next != m) {
+        delete c;
+        return fail(GAPA_CUDA_E_INVALID, "graph: CSR is not symmetric (found %d forward edges, expected %lld)", next,
+                    static_cast<long long>(m));
+    }
+    for (int32_t u = 0; u < n; ++u)
+        for (int32_t i = c->h_row_ptr[u]; i < c->h_row_ptr[u + 1]; ++i) {
+            const int32_t v = c->h_col_idx[i];
+            if (v < u) {
+                const int32_t* b = c->h_col_idx.data() + c->h_row_ptr[v];
+                const int32_t* e = c->h_col_idx.data() + c->h_row_ptr[v + 1];
+                const int32_t* it = std::lower_bound(b, e, u);
+                if (it == e || *it != u) {
+                    delete c;
+                    return fail(GAPA_CUDA_E_INVALID, "graph: CSR is not symmetric at (%d, %d)", u, v);
+                }
+                c->h_edge_id[i] = c->h_edge_id[it - c->h_col_idx.data()];
+            }
+        }
+    // BFS source candidates: vertices by descending degree, ties by id
+    std::vector<int32_t> by_degree(static_cast<size_t>(n));
+    std::iota(by_degree.begin(), by_degree.end(), 0);
+    std::stable_sort(by_degree.begin(), by_degree.end(), [&](int32_t a, int32_t b) {
+        return c->h_row_ptr[a + 1] - c->h_row_ptr[a] > c->h_row_ptr[b + 1] - c->h_row_ptr[b];
+    });
+
+    int count = 0;
+    if (cudaGetDeviceCount(&count) != cudaSuccess || count <= 0) {
+        delete c;
+        return fail(GAPA_CUDA_E_CUDA, "no CUDA device available (this library has no CPU fallback)");
+    }
+    if (device < 0 || device >= count) {
+        delete c;
+        return fail(GAPA_CUDA_E_INVALID, "device %d out of range (%d visible)", device, count);
+    }
+    c->device = device;
+    int rc = GAPA_CUDA_OK;
+    auto body = [&]() -> int {
+        GAPA_CUDA_TRY(cudaSetDevice(device));
+        GAPA_CUDA_TRY(cudaDeviceGetAttribute(&c->sm_count, cudaDevAttrMultiProcessorCount, device));
+        GAPA_TRY(upload_i32(c->h_row_ptr, &c->d_row_ptr));
+        GAPA_TRY(upload_i32(c->h_col_idx, &c->d_col_idx));
+        GAPA_TRY(upload_i32(c->h_edge_id, &c->d_edge_id));
+        GAPA_TRY(upload_i32(eu, &c->d_edge_u));
+        GAPA_TRY(upload_i32(ev, &c->d_edge_v));
+        GAPA_TRY(upload_i32(by_degree, &c->d_by_degree));
+        GAPA_CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        GAPA_CUDA_TRY(cudaEventCreate(&c->ev_start));
+        GAPA_CUDA_TRY(cudaEventCreate(&c->ev_stop));
+        GAPA_CUDA_TRY(cudaMallocHost(&c->h_status, 64 * sizeof(int32_t)));
+        GAPA_TRY(c->status_buf.ensure(64 * sizeof(int32_t)));
+        return GAPA_CUDA_OK;
+    };
+    rc = body();
+    if (rc != GAPA_CUDA_OK) {
+        gapa_cuda_destroy(c);
+        return rc;
+    }
+    // default pool: node removal, identity (build_gene_pool NodeRemoval, gene_pool.cpp:89-92)
+    c->pool_kind = GAPA_POOL_NODE_REMOVAL;
+    c->pool_size = n;
+    c->pool_identity = true;
+    *out = c;
+    return GAPA_CUDA_OK;
+}
+
+}  // namespace gapa_b200
+
+using namespace gapa_b200;
+
+extern "C" {
+
+const char* gapa_cuda_last_error(void) { return t_error.c_str(); }
+int gapa_cuda_abi_version(void) { return GAPA_CUDA_ABI_VERSION; }
+uint64_t gapa_cuda_launch_count(void) { return g_launches.load(); }
+
+int gapa_cuda_device_count(int* count) {
+    if (!count) return fail(GAPA_CUDA_E_INVALID, "device_count: null output");
+    *count = 0;
+    GAPA_CUDA_TRY(cudaGetDeviceCount(count));
+    return GAPA_CUDA_OK;
+}
+
+int gapa_cuda_graph_create(int32_t n, int64_t m, const int32_t* uv, int device, gapa_cuda_ctx** out) {
+    if (!out) return fail(GAPA_CUDA_E_INVALID, "graph_create: null output");
+    *out = nullptr;
+    if (n < 0 || m < 0 || (m > 0 && !uv)) return fail(GAPA_CUDA_E_INVALID, "graph_create: bad sizes");
+    if (2 * m > INT32_MAX) return fail(GAPA_CUDA_E_INVALID, "graph_create: 2m exceeds int32 CSR offsets");
+    auto* c = new gapa_cuda_ctx();
+    c->n = n;
+    c->m = m;
+    c->h_row_ptr.assign(static_cast<size_t>(n) + 1, 0);
+    for (int64_t e = 0; e < m; ++e) {
+        const int32_t u = uv[2 * e], v = uv[2 * e + 1];
+        if (u == v) { delete c; return fail(GAPA_CUDA_E_INVALID, "graph: self-loop rejected"); }
+        if (u < 0 || v < 0 || u >= n || v >= n) { delete c; return fail(GAPA_CUDA_E_INVALID, "graph: edge endpoint out of range"); }
+        c->h_row_ptr[u + 1]++;
+        c->h_row_ptr[v + 1]++;
+    }
+    for (int32_t u = 0; u < n; ++u) c->h_row_ptr[u + 1] += c->h_row_ptr[u];
+    c->h_col_idx.assign(static_cast<size_t>(2 * m), 0);
+    std::vector<int32_t> fill(c->h_row_ptr.begin(), c->h_row_ptr.end() - 1);
+    for (int64_t e = 0; e < m; ++e) {
+        const int32_t u = uv[2 * e], v = uv[2 * e + 1];
+        c->h_col_idx[fill[u]++] = v;
+        c->h_col_idx[fill[v]++] = u;
+    }
+    for (int32_t u = 0; u < n; ++u) {
+        auto b = c->h_col_idx.begin() + c->h_row_ptr[u], e = c->h_col_idx.begin() + c->h_row_ptr[u + 1];
+        std::sort(b, e);
+        if (std::adjacent_find(b, e) != e) { delete c; return fail(GAPA_CUDA_E_INVALID, "graph: duplicate edge rejected"); }
+    }
+    return finish_create(c, device, out);
+}
+
+int gapa_cuda_graph_create_csr(int32_t n, int64_t m, const int32_t* row_ptr, const int32_t* col_idx, int device,
+                               gapa_cuda_ctx** out) {
+    if (!out) return fail(GAPA_CUDA_E_INVALID, "graph_create_csr: null output");
+    *out = nullptr;
+    if (n < 0 || m < 0 || !row_ptr || (m > 0 && !col_idx)) return fail(GAPA_CUDA_E_INVALID, "graph_create_csr: bad sizes");
+    if (2 * m > INT32_MAX) return fail(GAPA_CUDA_E_INVALID, "graph_create_csr: 2m exceeds int32 CSR offsets");
+    if (row_ptr[0] != 0 || row_ptr[n] != 2 * m) return fail(GAPA_CUDA_E_INVALID, "graph_create_csr: row_ptr does not span 2m slots");
+    auto* c = new gapa_cuda_ctx();
+    c->n = n;
+    c->m = m;
+    c->h_row_ptr.assign(row_ptr, row_ptr + n + 1);
+    c->h_col_idx.assign(col_idx, col_idx + 2 * m);
+    for (int32_t u = 0; u < n; ++u) {
+        if (row_ptr[u + 1] < row_ptr[u]) { delete c; return fail(GAPA_CUDA_E_INVALID, "graph_create_csr: row_ptr not monotone"); }
+        for (int32_t i = row_ptr[u]; i < row_ptr[u + 1]; ++i) {
+            const int32_t v = col_idx[i];
+            if (v < 0 || v >= n || v == u || (i > row_ptr[u] && col_idx[i - 1] >= v)) {
+                delete c;
+                return fail(GAPA_CUDA_E_INVALID, "graph_create_csr: row %d is not a strictly ascending loop-free list", u);
+            }
+        }
+    }
+    return finish_create(c, device, out);
+}
+
+int gapa_cuda_destroy(gapa_cuda_ctx* c) {
+    if (!c) return GAPA_CUDA_OK;
+    cudaSetDevice(c->device);
+    pc_free(c);
+    lpa_free(c);
+    cda_free(c);
+    for (int32_t* p : {c->d_row_ptr, c->d_col_idx, c->d_edge_id, c->d_edge_u, c->d_edge_v, c->d_by_degree,
+                       c->d_pool_map, c->d_pairs})
+        if (p) cudaFree(p);
+    c->genes_stage.release();
+    c->out_stage.release();
+    c->status_buf.release();
+    if (c->h_status) cudaFreeHost(c->h_status);
+    if (c->ev_start) cudaEventDestroy(c->ev_start);
+    if (c->ev_stop) cudaEventDestroy(c->ev_stop);
+    if (c->stream) cudaStreamDestroy(c->stream);
+    delete c;
+    return GAPA_CUDA_OK;
+}
+
+int gapa_cuda_graph_info(const gapa_cuda_ctx* c, int32_t* n, int64_t* m, int* device) {
+    if (!c) return fail(GAPA_CUDA_E_INVALID, "graph_info: null context");
+    if (n) *n = c->n;
+    if (m) *m = c->m;
+    if (device) *device = c->device;
+    return GAPA_CUDA_OK;
+}
+
+int gapa_cuda_pool_set(gapa_cuda_ctx* c, int kind, int32_t n_genes, const int32_t* u, const int32_t* v) {
+    if (!c) return fail(GAPA_CUDA_E_INVALID, "pool_set: null context");
+    if (kind == GAPA_POOL_EDGE_ADDITION)
+        return fail(GAPA_CUDA_E_INVALID, "pool_set: edge-addition pools are not on the CUDA path yet");
+    if (kind != GAPA_POOL_NODE_REMOVAL && kind != GAPA_POOL_EDGE_REMOVAL)
+        return fail(GAPA_CUDA_E_INVALID, "pool_set: unknown pool kind %d", kind);
+    if (c->n == 0) return fail(GAPA_CUDA_E_INVALID, "gene pool: graph is empty");  // gene_pool.cpp:70
+    const int32_t full = kind == GAPA_POOL_NODE_REMOVAL ? c->n : static_cast<int32_t>(c->m);
+    if (!u) n_genes = full;
+    if (n_genes < 0) return fail(GAPA_CUDA_E_INVALID, "pool_set: negative size");
+    std::vector<int32_t> map(static_cast<size_t>(n_genes));
+    bool identity = true;
+    for (int32_t i = 0; i < n_genes; ++i) {
+        int32_t target;
+        if (!u) target = i;
+        else if (kind == GAPA_POOL_NODE_REMOVAL) {
+            target = u[i];
+            if (target < 0 || target >= c->n) return fail(GAPA_CUDA_E_INVALID, "pool_set: node %d out of range", target);
+        } else {
+            if (!v) return fail(GAPA_CUDA_E_INVALID, "pool_set: edge pool needs both endpoint arrays");
+            target = edge_rank(c, u[i], v[i]);
+            if (target < 0) return fail(GAPA_CUDA_E_INVALID, "pool_set: (%d, %d) is not an edge of the graph", u[i], v[i]);
+        }
+        map[i] = target;
+        identity &= (target == i);
+    }
+    GAPA_CUDA_TRY(cudaSetDevice(c->device));
+    if (c->d_pool_map) { cudaFree(c->d_pool_map); c->d_pool_map = nullptr; }
+    if (!identity) GAPA_TRY(upload_i32(map, &c->d_pool_map));
+    c->pool_kind = kind;
+    c->pool_size = n_genes;
+    c->pool_identity = identity;
+    return GAPA_CUDA_OK;
+}
+
+int gapa_cuda_pool_info(const gapa_cuda_ctx* c, int* kind, int32_t* n_genes) {
+    if (!c) return fail(GAPA_CUDA_E_INVALID, "pool_info: null context");
+    if (kind) *kind = c->pool_kind;
+    if (n_genes) *n_genes = c->pool_size;
+    return GAPA_CUDA_OK;
+}
+
+int gapa_cuda_lp_split_set(gapa_cuda_ctx* c, int32_t T, const int32_t* test_uv, int32_t P, const int32_t* probe_uv) {
+    if (!c) return fail(GAPA_CUDA_E_INVALID, "lp_split_set: null context");
+    if (T < 1 || P < 0 || !test_uv || (P > 0 && !probe_uv))
+        return fail(GAPA_CUDA_E_INVALID, "lp_auc_precision: empty test set");  // link_prediction.cpp:82
+    std::vector<int32_t> pairs(static_cast<size_t>(2) * (T + P));
+    std::memcpy(pairs.data(), test_uv, sizeof(int32_t) * 2 * T);
+    if (P) std::memcpy(pairs.data() + 2 * T, probe_uv, sizeof(int32_t) * 2 * P);
+    for (int32_t x : pairs)
+        if (x < 0 || x >= c->n) return fail(GAPA_CUDA_E_INVALID, "lp_split_set: pair endpoint out of range");
+    GAPA_CUDA_TRY(cudaSetDevice(c->device));
+    if (c->d_pairs) { cudaFree(c->d_pairs); c->d_pairs = nullptr; }
+    GAPA_TRY(upload_i32(pairs, &c->d_pairs));
+    c->T = T;
+    c->P = P;
+    return GAPA_CUDA_OK;
+}
+
+static int check_task(const gapa_cuda_ctx* c, int task) {
+    switch (task) {
+        case GAPA_TASK_PC:
+        case GAPA_TASK_MCN:
+            if (c->pool_kind != GAPA_POOL_NODE_REMOVAL)
+                return fail(GAPA_CUDA_E_INVALID, "%s: incompatible gene pool kind", task == GAPA_TASK_PC ? "pc_fitness" : "sixdst_fitness");
+            return GAPA_CUDA_OK;
+        case GAPA_TASK_CDA:
+            if (c->pool_kind == GAPA_POOL_NODE_REMOVAL) return fail(GAPA_CUDA_E_INVALID, "cda_fitness: incompatible gene pool kind");
+            return GAPA_CUDA_OK;
+        case GAPA_TASK_LPA:
+            if (c->pool_kind != GAPA_POOL_EDGE_REMOVAL) return fail(GAPA_CUDA_E_INVALID, "lpa_fitness: incompatible gene pool kind");
+            if (c->T < 1) return fail(GAPA_CUDA_E_INVALID, "lpa_fitness: no link-prediction split set");
+            return GAPA_CUDA_OK;
+    }
+    return fail(GAPA_CUDA_E_INVALID, "unknown fitness task %d", task);
+}
+
+int gapa_cuda_eval_batch_device(gapa_cuda_ctx* c, int task, const int32_t* genes_dev, int rows, int cols,
+                                double* out_dev, void* stream) {
+    if (!c) return fail(GAPA_CUDA_E_INVALID, "eval_batch: null context");
+    GAPA_TRY(check_task(c, task));
+    if (rows < 0 || cols < 0) return fail(GAPA_CUDA_E_INVALID, "eval_batch: negative shape");
+    if (rows == 0) return GAPA_CUDA_OK;
+    if (!out_dev || (cols > 0 && !genes_dev)) return fail(GAPA_CUDA_E_INVALID, "eval_batch: null buffer");
+    GAPA_CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    GAPA_CUDA_TRY(cudaEventRecord(c->ev_start, s));
+    int rc;
+    if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) rc = pc_eval(c, task, genes_dev, rows, cols, out_dev, s);
+    else if (task == GAPA_TASK_CDA) rc = cda_eval(c, genes_dev, rows, cols, out_dev, s);
+    else rc = lpa_eval(c, genes_dev, rows, cols, out_dev, s);
+    if (rc != GAPA_CUDA_OK) return rc;
+    GAPA_CUDA_TRY(cudaEventRecord(c->ev_stop, s));
+    GAPA_CUDA_TRY(cudaEventSynchronize(c->ev_stop));
+    GAPA_CUDA_TRY(cudaEventElapsedTime(&c->last_eval_ms, c->ev_start, c->ev_stop));
+    return GAPA_CUDA_OK;
+}
+
+int gapa_cuda_eval_batch(gapa_cuda_ctx* c, int task, const int32_t* genes_host, int rows, int cols, double* out_host) {
+    if (!c) return fail(GAPA_CUDA_E_INVALID, "eval_batch: null context");
+    GAPA_TRY(check_task(c, task));
+    if (rows < 0 || cols < 0) return fail(GAPA_CUDA_E_INVALID, "eval_batch: negative shape");
+    if (rows == 0) return GAPA_CUDA_OK;
+    if (!out_host || (cols > 0 && !genes_host)) return fail(GAPA_CUDA_E_INVALID, "eval_batch: null buffer");
+    GAPA_CUDA_TRY(cudaSetDevice(c->device));
+    const size_t cells = static_cast<size_t>(rows) * cols;
+    GAPA_TRY(c->genes_stage.ensure(sizeof(int32_t) * std::max<size_t>(cells, 1)));
+    GAPA_TRY(c->out_stage.ensure(sizeof(double) * rows));
+    if (cells)
+        GAPA_CUDA_TRY(cudaMemcpyAsync(c->genes_stage.ptr, genes_host, sizeof(int32_t) * cells, cudaMemcpyHostToDevice, c->stream));
+    GAPA_TRY(gapa_cuda_eval_batch_device(c, task, c->genes_stage.as<int32_t>(), rows, cols, c->out_stage.as<double>(), c->stream));
+    GAPA_CUDA_TRY(cudaMemcpyAsync(out_host, c->out_stage.ptr, sizeof(double) * rows, cudaMemcpyDeviceToHost, c->stream));
+    GAPA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return GAPA_CUDA_OK;
+}
+
+int gapa_cuda_last_eval_ms(const gapa_cuda_ctx* c, float* ms) {
+    if (!c || !ms) return fail(GAPA_CUDA_E_INVALID, "last_eval_ms: null argument");
+    *ms = c->last_eval_ms;
+    return GAPA_CUDA_OK;
+}
+
+int gapa_cuda_malloc(int device, uint64_t bytes, void** out_dev) {
+    if (!out_dev) return fail(GAPA_CUDA_E_INVALID, "malloc: null output");
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    GAPA_CUDA_TRY(cudaMalloc(out_dev, std::max<uint64_t>(bytes, 1)));
+    return GAPA_CUDA_OK;
+}
+int gapa_cuda_free(int device, void* dev) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    if (dev) GAPA_CUDA_TRY(cudaFree(dev));
+    return GAPA_CUDA_OK;
+}
+int gapa_cuda_memcpy_h2d(int device, void* dst_dev, const void* src_host, uint64_t bytes) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    if (bytes) GAPA_CUDA_TRY(cudaMemcpy(dst_dev, src_host, bytes, cudaMemcpyHostToDevice));
+    return GAPA_CUDA_OK;
+}
+int gapa_cuda_memcpy_d2h(int device, void* dst_host, const void* src_dev, uint64_t bytes) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    if (bytes) GAPA_CUDA_TRY(cudaMemcpy(dst_host, src_dev, bytes, cudaMemcpyDeviceToHost));
+    return GAPA_CUDA_OK;
+}
+int gapa_cuda_stream_sync(int device, void* stream) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    GAPA_CUDA_TRY(cudaStreamSynchronize(static_cast<cudaStream_t>(stream)));
+    return GAPA_CUDA_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,471 @@
+// Genetic operators on HBM-resident populations — device twins of
+// /root/reference/proj/src/ga_ops.cpp, keyed by the same counter-based streams
+// (include/gapa/rng.hpp), so every matrix equals the reference's bit for bit.
+//
+// Because draw j of a stream is mix64(key + C*j) (rng.hpp:21), element (row, col)
+// needs only the row's key and j = col + 1: one thread per gene, no sequential
+// state, any row partition gives the same result.
+#include <algorithm>
+#include <cmath>
+
+#include "internal.cuh"
+
+namespace gapa_b200 {
+
+static constexpr int kGaThreads = 256;
+
+// ---- init_population_block (ga_ops.cpp:19-29) ----------------------------------------
+__global__ void __launch_bounds__(kGaThreads) k_ga_init(uint32_t pool_size, int row_first, int budget, uint64_t seed,
+                                                        uint64_t generation, int32_t* __restrict__ out) {
+    __shared__ uint64_t key;
+    const int row = blockIdx.y;
+    if (threadIdx.x == 0) key = stream_key(seed, generation, GAPA_ROLE_INIT, static_cast<uint64_t>(row_first + row));
+    __syncthreads();
+    const uint64_t k = key;
+    int32_t* dst = out + static_cast<size_t>(row) * budget;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < budget; j += gridDim.x * blockDim.x)
+        dst[j] = static_cast<int32_t>(draw_index(k, static_cast<uint64_t>(j) + 1, pool_size));
+}
+
+// ---- crossover (ga_ops.cpp:130-144) fused with mutate_block (:164-178) -------------------
+// out(i,j) = RM(i,j) ? fresh(i,j) : (RC(i,j) ? pop(partner_i, j) : pop(i, j)).
+// All three draws are random-access, so a flipped gene skips the crossover draw
+// and both loads; the result is unchanged.
+__global__ void __launch_bounds__(kGaThreads) k_ga_crossover_mutate(
+    const int32_t* __restrict__ pop, const int32_t* __restrict__ partner, int k, int row_first, uint64_t pc_thr,
+    uint64_t pm_thr, uint32_t pool_size, uint64_t seed, uint64_t generation, int32_t* __restrict__ out) {
+    __shared__ uint64_t keys[3];
+    const int row = row_first + blockIdx.y;
+    if (threadIdx.x < 3)
+        keys[threadIdx.x] = stream_key(seed, generation, GAPA_ROLE_CROSSOVER_MASK + threadIdx.x, static_cast<uint64_t>(row));
+    __syncthreads();
+    const uint64_t kc = keys[0], km = keys[1], ki = keys[2];
+    const int32_t* mine = pop + static_cast<size_t>(row) * k;
+    const int32_t* theirs = pop + static_cast<size_t>(partner[row]) * k;
+    int32_t* dst = out + static_cast<size_t>(blockIdx.y) * k;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+        const uint64_t d = static_cast<uint64_t>(j) + 1;
+        int32_t g;
+        if (draw_bernoulli(km, d, pm_thr)) g = static_cast<int32_t>(draw_index(ki, d, pool_size));
+        else g = draw_bernoulli(kc, d, pc_thr) ? theirs[j] : mine[j];
+        dst[j] = g;
+    }
+}
+
+// ---- mutate_block alone (ga_ops.cpp:164-178) ------------------------------------------------
+__global__ void __launch_bounds__(kGaThreads) k_ga_mutate(const int32_t* __restrict__ block, int k, int row_offset,
+                                                          uint64_t pm_thr, uint32_t pool_size, uint64_t seed,
+                                                          uint64_t generation, int32_t* __restrict__ out) {
+    __shared__ uint64_t keys[2];
+    const int row = row_offset + blockIdx.y;
+    if (threadIdx.x < 2)
+        keys[threadIdx.x] = stream_key(seed, generation, GAPA_ROLE_MUTATION_MASK + threadIdx.x, static_cast<uint64_t>(row));
+    __syncthreads();
+    const uint64_t km = keys[0], ki = keys[1];
+    const int32_t* src = block + static_cast<size_t>(blockIdx.y) * k;
+    int32_t* dst = out + static_cast<size_t>(blockIdx.y) * k;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+        const uint64_t d = static_cast<uint64_t>(j) + 1;
+        dst[j] = draw_bernoulli(km, d, pm_thr) ? static_cast<int32_t>(draw_index(ki, d, pool_size)) : src[j];
+    }
+}
+
+// ---- eda_sample (ga_ops.cpp:214-238) ----------------------------------------------------------
+__global__ void __launch_bounds__(kGaThreads) k_ga_eda(const int32_t* __restrict__ elite, int k, uint32_t elite_count,
+                                                       uint32_t bound, uint64_t seed, uint64_t generation,
+                                                       int32_t* __restrict__ out) {
+    __shared__ uint64_t key;
+    const int row = blockIdx.y;
+    if (threadIdx.x == 0) key = stream_key(seed, generation, GAPA_ROLE_SELECT, static_cast<uint64_t>(row));
+    __syncthreads();
+    const uint64_t kk = key;
+    int32_t* dst = out + static_cast<size_t>(row) * k;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+        const uint32_t v = draw_index(kk, static_cast<uint64_t>(j) + 1, bound);
+        dst[j] = v < elite_count ? elite[static_cast<size_t>(v) * k + j] : static_cast<int32_t>(v - elite_count);
+    }
+}
+
+// ---- selection_weights (ga_ops.cpp:54-76) --------------------------------------------------------
+// The reference stable-sorts, then gives every tie span [i, j) the average of the
+// rank weights s-i .. s-j+1.  For element x that is i = #{strictly better},
+// j = #{better or equal}; counting replaces the sort (O(s^2) compares, s <= 16k).
+__device__ __forceinline__ bool better(double a, double b, int minimize) { return minimize ? a < b : a > b; }
+
+__global__ void __launch_bounds__(kGaThreads) k_ga_weights(const double* __restrict__ fitness, int s, int minimize,
+                                                           double* __restrict__ weights, int* status) {
+    __shared__ double tile[kGaThreads];
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const double mine = i < s ? fitness[i] : 0.0;
+    if (i < s && !isfinite(mine)) *status = GAPA_CUDA_E_NAN;
+    int less = 0, leq = 0;
+    for (int t0 = 0; t0 < s; t0 += kGaThreads) {
+        __syncthreads();
+        if (t0 + threadIdx.x < s) tile[threadIdx.x] = fitness[t0 + threadIdx.x];
+        __syncthreads();
+        const int lim = min(kGaThreads, s - t0);
+        for (int t = 0; t < lim; ++t) {
+            const double other = tile[t];
+            const bool b = better(other, mine, minimize);
+            less += b;
+            leq += b || other == mine;
+        }
+    }
+    if (i < s) weights[i] = (static_cast<double>(s - less) + static_cast<double>(s - leq + 1)) / 2.0;
+}
+
+// cumulative sum + weighted_pick (ga_ops.cpp:78-82, :113-126), one block.
+// Weights are half-integers with total <= s(s+1)/2 < 2^53: every partial sum is
+// exact, so the parallel scan equals the reference's sequential running total.
+__global__ void __launch_bounds__(1024) k_ga_pick(const double* __restrict__ weights, int s, uint64_t seed,
+                                                  uint64_t generation, double* __restrict__ cumulative,
+                                                  int32_t* __restrict__ partner) {
+    __shared__ double part[1024];
+    const int tid = threadIdx.x, nt = blockDim.x;
+    const int per = (s + nt - 1) / nt;
+    const int lo = min(tid * per, s), hi = min(lo + per, s);
+    double sum = 0.0;
+    for (int i = lo; i < hi; ++i) sum += weights[i];
+    part[tid] = sum;
+    __syncthreads();
+    for (int off = 1; off < nt; off <<= 1) {
+        const double add = tid >= off ? part[tid - off] : 0.0;
+        __syncthreads();
+        part[tid] += add;
+        __syncthreads();
+    }
+    double run = part[tid] - sum;
+    for (int i = lo; i < hi; ++i) {
+        run += weights[i];
+        cumulative[i] = run;
+    }
+    const double total = part[nt - 1];
+    __syncthreads();
+    for (int i = tid; i < s; i += nt) {
+        const double target = draw_unit(stream_key(seed, generation, GAPA_ROLE_SELECT, static_cast<uint64_t>(i)), 1) * total;
+        int a = 0, b = s;  // std::upper_bound: first index with cumulative > target
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (cumulative[mid] <= target) a = mid + 1; else b = mid;
+        }
+        partner[i] = min(a, s - 1);
+    }
+}
+
+// ---- elitism (ga_ops.cpp:180-212) ---------------------------------------------------------------------
+// Position of stacked row x in the stable best-first order = #{y : better(y, x) or
+// (equal and y < x)}; originals (index < s) therefore precede mutated rows on ties.
+__global__ void __launch_bounds__(kGaThreads) k_ga_elite_rank(const double* __restrict__ fit, const double* __restrict__ fit_m,
+                                                              int s, int minimize, int32_t* __restrict__ src_of_rank,
+                                                              int* status) {
+    __shared__ double tile[kGaThreads];
+    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int total = 2 * s;
+    const double mine = x < total ? (x < s ? fit[x] : fit_m[x - s]) : 0.0;
+    if (x < total && isnan(mine)) *status = GAPA_CUDA_E_NAN;
+    int rank = 0;
+    for (int t0 = 0; t0 < total; t0 += kGaThreads) {
+        __syncthreads();
+        const int y = t0 + threadIdx.x;
+        if (y < total) tile[threadIdx.x] = y < s ? fit[y] : fit_m[y - s];
+        __syncthreads();
+        const int lim = min(kGaThreads, total - t0);
+        for (int t = 0; t < lim; ++t) {
+            const double other = tile[t];
+            rank += better(other, mine, minimize) || (other == mine && t0 + t < x);
+        }
+    }
+    if (x < total && rank < s) src_of_rank[rank] = x;
+}
+
+__global__ void __launch_bounds__(kGaThreads) k_ga_elite_gather(const int32_t* __restrict__ pop,
+                                                                const int32_t* __restrict__ m_pop,
+                                                                const double* __restrict__ fit,
+                                                                const double* __restrict__ fit_m, int s, int k,
+                                                                const int32_t* __restrict__ src_of_rank,
+                                                                int32_t* __restrict__ next, double* __restrict__ next_fit) {
+    const int r = blockIdx.y;
+    const int src = src_of_rank[r];
+    const int32_t* from = src < s ? pop + static_cast<size_t>(src) * k : m_pop + static_cast<size_t>(src - s) * k;
+    int32_t* to = next + static_cast<size_t>(r) * k;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) to[j] = from[j];
+    if (blockIdx.x == 0 && threadIdx.x == 0) next_fit[r] = src < s ? fit[src] : fit_m[src - s];
+}
+
+__global__ void k_rng_draws(uint64_t seed, uint64_t generation, uint64_t role, uint64_t row, int count, uint64_t* out) {
+    const uint64_t key = stream_key(seed, generation, role, row);
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x)
+        out[j] = draw_u64(key, static_cast<uint64_t>(j) + 1);
+}
+
+// ---- launch helpers (no synchronisation; shared with run.cu) ------------------------------------------
+static dim3 row_grid(int cols, int rows) {
+    const int per_block = kGaThreads * 8;  // 8 genes per thread keeps the per-row key setup amortised
+    return dim3(std::max(1, std::min((cols + per_block - 1) / per_block, 65535)), rows);
+}
+
+int launch_init(uint32_t pool_size, int row_first, int row_count, int budget, uint64_t seed, uint64_t generation,
+                int32_t* out, cudaStream_t st) {
+    if (row_count == 0 || budget == 0) return GAPA_CUDA_OK;
+    GAPA_LAUNCH(k_ga_init, row_grid(budget, row_count), kGaThreads, 0, st, pool_size, row_first, budget, seed, generation, out);
+    return GAPA_CUDA_OK;
+}
+int launch_select(const double* fitness, int s, int minimize, uint64_t seed, uint64_t generation, int32_t* partner,
+                  double* weights, double* cumulative, int* status, cudaStream_t st) {
+    GAPA_LAUNCH(k_ga_weights, (s + kGaThreads - 1) / kGaThreads, kGaThreads, 0, st, fitness, s, minimize, weights, status);
+    GAPA_LAUNCH(k_ga_pick, 1, 1024, 0, st, weights, s, seed, generation, cumulative, partner);
+    return GAPA_CUDA_OK;
+}
+int launch_crossover_mutate(const int32_t* pop, const int32_t* partner, int k, int row_first, int row_count, double pc,
+                            double pm, uint32_t pool_size, uint64_t seed, uint64_t generation, int32_t* out,
+                            cudaStream_t st) {
+    if (row_count == 0 || k == 0) return GAPA_CUDA_OK;
+    GAPA_LAUNCH(k_ga_crossover_mutate, row_grid(k, row_count), kGaThreads, 0, st, pop, partner, k, row_first,
+                bernoulli_threshold(pc), bernoulli_threshold(pm), pool_size, seed, generation, out);
+    return GAPA_CUDA_OK;
+}
+int launch_mutate(const int32_t* block, int rows, int k, int row_offset, double pm, uint32_t pool_size, uint64_t seed,
+                  uint64_t generation, int32_t* out, cudaStream_t st) {
+    if (rows == 0 || k == 0) return GAPA_CUDA_OK;
+    GAPA_LAUNCH(k_ga_mutate, row_grid(k, rows), kGaThreads, 0, st, block, k, row_offset, bernoulli_threshold(pm), pool_size,
+                seed, generation, out);
+    return GAPA_CUDA_OK;
+}
+int launch_eda(const int32_t* elite, int s, int k, int elite_count, uint32_t bound, uint64_t seed, uint64_t generation,
+               int32_t* out, cudaStream_t st) {
+    if (s == 0 || k == 0) return GAPA_CUDA_OK;
+    GAPA_LAUNCH(k_ga_eda, row_grid(k, s), kGaThreads, 0, st, elite, k, static_cast<uint32_t>(elite_count), bound, seed,
+                generation, out);
+    return GAPA_CUDA_OK;
+}
+int launch_elitism(const int32_t* pop, const int32_t* m_pop, int s, int k, const double* fit, const double* fit_m,
+                   int minimize, int32_t* next, double* next_fit, int32_t* src_of_rank, int* status, cudaStream_t st) {
+    GAPA_LAUNCH(k_ga_elite_rank, (2 * s + kGaThreads - 1) / kGaThreads, kGaThreads, 0, st, fit, fit_m, s, minimize,
+                src_of_rank, status);
+    GAPA_LAUNCH(k_ga_elite_gather, row_grid(std::max(k, 1), s), kGaThreads, 0, st, pop, m_pop, fit, fit_m, s, k, src_of_rank,
+                next, next_fit);
+    return GAPA_CUDA_OK;
+}
+
+// Scratch for the *_device entry points (per call; these are not the hot loop —
+// gapa_cuda_run keeps its own persistent buffers).
+struct OpScratch {
+    DevBuf a, b, c;
+    int* status = nullptr;
+    int init(cudaStream_t st) {
+        GAPA_TRY(c.ensure(sizeof(int)));
+        status = c.as<int>();
+        GAPA_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), st));
+        return GAPA_CUDA_OK;
+    }
+    int check(cudaStream_t st, const char* what) {
+        int h = 0;
+        GAPA_CUDA_TRY(cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+        GAPA_CUDA_TRY(cudaStreamSynchronize(st));
+        if (h == GAPA_CUDA_E_NAN) return fail(GAPA_CUDA_E_NAN, "%s", what);
+        return GAPA_CUDA_OK;
+    }
+    ~OpScratch() { a.release(); b.release(); c.release(); }
+};
+
+}  // namespace gapa_b200
+
+using namespace gapa_b200;
+
+// ---- host-buffer forms -------------------------------------------------------------------------------
+namespace {
+struct Tmp {
+    std::vector<void*> ptrs;
+    template <typename T>
+    int up(const T* host, size_t count, T** dev) {
+        GAPA_CUDA_TRY(cudaMalloc(reinterpret_cast<void**>(dev), std::max<size_t>(sizeof(T) * count, 16)));
+        ptrs.push_back(*dev);
+        if (host && count) GAPA_CUDA_TRY(cudaMemcpy(*dev, host, sizeof(T) * count, cudaMemcpyHostToDevice));
+        return GAPA_CUDA_OK;
+    }
+    template <typename T>
+    int down(T* host, const T* dev, size_t count) {
+        if (count) GAPA_CUDA_TRY(cudaMemcpy(host, dev, sizeof(T) * count, cudaMemcpyDeviceToHost));
+        return GAPA_CUDA_OK;
+    }
+    ~Tmp() { for (void* p : ptrs) cudaFree(p); }
+};
+}  // namespace
+
+static int check_rates(double pc, double pm) {
+    if (!(pc >= 0.0 && pc <= 1.0)) return fail(GAPA_CUDA_E_INVALID, "pc must be in [0, 1]");
+    if (!(pm >= 0.0 && pm <= 1.0)) return fail(GAPA_CUDA_E_INVALID, "pm must be in [0, 1]");
+    return GAPA_CUDA_OK;
+}
+
+extern "C" {
+
+int gapa_cuda_ga_init_device(int32_t pool_size, int row_first, int row_count, int budget, uint64_t seed,
+                             uint64_t generation, int32_t* out_dev, void* stream) {
+    if (pool_size < 1) return fail(GAPA_CUDA_E_INVALID, "init_population: empty gene pool");
+    if (row_first < 0 || row_count < 0 || budget < 0) return fail(GAPA_CUDA_E_INVALID, "init_population: negative shape");
+    return launch_init(static_cast<uint32_t>(pool_size), row_first, row_count, budget, seed, generation, out_dev,
+                       static_cast<cudaStream_t>(stream));
+}
+
+int gapa_cuda_ga_select_device(const double* fitness_dev, int s, int minimize, uint64_t seed, uint64_t generation,
+                               int32_t* partner_dev, double* weights_dev, void* stream) {
+    if (s < 1) return fail(GAPA_CUDA_E_INVALID, "roulette_select: empty population");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    OpScratch sc;
+    GAPA_TRY(sc.init(st));
+    GAPA_TRY(sc.a.ensure(sizeof(double) * s));
+    GAPA_TRY(sc.b.ensure(sizeof(double) * s));
+    double* w = weights_dev ? weights_dev : sc.a.as<double>();
+    GAPA_TRY(launch_select(fitness_dev, s, minimize, seed, generation, partner_dev, w, sc.b.as<double>(), sc.status, st));
+    return sc.check(st, "roulette_select: non-finite fitness");
+}
+
+int gapa_cuda_ga_crossover_mutate_device(const int32_t* pop_dev, const int32_t* partner_dev, int s, int k, int row_first,
+                                         int row_count, double pc, double pm, int32_t pool_size, uint64_t seed,
+                                         uint64_t generation, int32_t* out_dev, void* stream) {
+    GAPA_TRY(check_rates(pc, pm));
+    if (pool_size < 1) return fail(GAPA_CUDA_E_INVALID, "mutate: empty gene pool");
+    if (row_first < 0 || row_count < 0 || row_first + row_count > s) return fail(GAPA_CUDA_E_INVALID, "crossover: row block outside the population");
+    return launch_crossover_mutate(pop_dev, partner_dev, k, row_first, row_count, pc, pm, static_cast<uint32_t>(pool_size),
+                                   seed, generation, out_dev, static_cast<cudaStream_t>(stream));
+}
+
+int gapa_cuda_ga_mutate_device(const int32_t* block_dev, int rows, int k, int row_offset, double pm, int32_t pool_size,
+                               uint64_t seed, uint64_t generation, int32_t* out_dev, void* stream) {
+    GAPA_TRY(check_rates(0.0, pm));
+    if (pool_size < 1) return fail(GAPA_CUDA_E_INVALID, "mutate: empty gene pool");
+    return launch_mutate(block_dev, rows, k, row_offset, pm, static_cast<uint32_t>(pool_size), seed, generation, out_dev,
+                         static_cast<cudaStream_t>(stream));
+}
+
+int gapa_cuda_ga_eda_device(const int32_t* elite_dev, int s, int k, int elite_count, int32_t pool_size, uint64_t seed,
+                            uint64_t generation, int smoothing, int32_t* out_dev, void* stream) {
+    if (elite_count < 1 || elite_count > s) return fail(GAPA_CUDA_E_INVALID, "eda_sample: invalid elite count");
+    const uint32_t bound = static_cast<uint32_t>(smoothing ? elite_count + pool_size : elite_count);
+    return launch_eda(elite_dev, s, k, elite_count, bound, seed, generation, out_dev, static_cast<cudaStream_t>(stream));
+}
+
+int gapa_cuda_ga_elitism_device(const int32_t* pop_dev, const int32_t* m_pop_dev, int s, int k, const double* fit_dev,
+                                const double* fit_m_dev, int minimize, int32_t* next_dev, double* next_fit_dev,
+                                void* stream) {
+    if (s < 1) return fail(GAPA_CUDA_E_INVALID, "elitism: empty population");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    OpScratch sc;
+    GAPA_TRY(sc.init(st));
+    GAPA_TRY(sc.a.ensure(sizeof(int32_t) * s));
+    GAPA_TRY(launch_elitism(pop_dev, m_pop_dev, s, k, fit_dev, fit_m_dev, minimize, next_dev, next_fit_dev,
+                            sc.a.as<int32_t>(), sc.status, st));
+    return sc.check(st, "elitism: NaN fitness");
+}
+
+
+int gapa_cuda_ga_init(int device, int32_t pool_size, int row_first, int row_count, int budget, uint64_t seed,
+                      uint64_t generation, int32_t* out) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    Tmp t;
+    int32_t* d = nullptr;
+    const size_t cells = static_cast<size_t>(std::max(row_count, 0)) * std::max(budget, 0);
+    GAPA_TRY(t.up<int32_t>(nullptr, cells, &d));
+    GAPA_TRY(gapa_cuda_ga_init_device(pool_size, row_first, row_count, budget, seed, generation, d, nullptr));
+    return t.down(out, d, cells);
+}
+
+int gapa_cuda_ga_selection_weights(int device, const double* fitness, int s, int minimize, double* weights) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    if (s < 1) return GAPA_CUDA_OK;
+    Tmp t;
+    double *f = nullptr, *w = nullptr;
+    int32_t* p = nullptr;
+    GAPA_TRY(t.up(fitness, s, &f));
+    GAPA_TRY(t.up<double>(nullptr, s, &w));
+    GAPA_TRY(t.up<int32_t>(nullptr, s, &p));
+    int rc = gapa_cuda_ga_select_device(f, s, minimize, 0, 0, p, w, nullptr);
+    if (rc == GAPA_CUDA_E_NAN) return fail(GAPA_CUDA_E_NAN, "selection: non-finite fitness");
+    GAPA_TRY(rc);
+    return t.down(weights, w, s);
+}
+
+int gapa_cuda_ga_select(int device, const double* fitness, int s, int minimize, uint64_t seed, uint64_t generation,
+                        int32_t* partner_index) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    Tmp t;
+    double* f = nullptr;
+    int32_t* p = nullptr;
+    GAPA_TRY(t.up(fitness, std::max(s, 0), &f));
+    GAPA_TRY(t.up<int32_t>(nullptr, std::max(s, 0), &p));
+    GAPA_TRY(gapa_cuda_ga_select_device(f, s, minimize, seed, generation, p, nullptr, nullptr));
+    return t.down(partner_index, p, s);
+}
+
+int gapa_cuda_ga_crossover_mutate(int device, const int32_t* pop, const int32_t* partner_index, int s, int k, int row_first,
+                                  int row_count, double pc, double pm, int32_t pool_size, uint64_t seed,
+                                  uint64_t generation, int32_t* out) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    if (s < 0 || k < 0) return fail(GAPA_CUDA_E_INVALID, "crossover: shape mismatch");
+    for (int i = 0; i < s; ++i)
+        if (partner_index[i] < 0 || partner_index[i] >= s) return fail(GAPA_CUDA_E_INVALID, "crossover: partner index out of range");
+    Tmp t;
+    int32_t *dp = nullptr, *di = nullptr, *d_out = nullptr;
+    GAPA_TRY(t.up(pop, static_cast<size_t>(s) * k, &dp));
+    GAPA_TRY(t.up(partner_index, s, &di));
+    GAPA_TRY(t.up<int32_t>(nullptr, static_cast<size_t>(std::max(row_count, 0)) * k, &d_out));
+    GAPA_TRY(gapa_cuda_ga_crossover_mutate_device(dp, di, s, k, row_first, row_count, pc, pm, pool_size, seed, generation, d_out, nullptr));
+    return t.down(out, d_out, static_cast<size_t>(row_count) * k);
+}
+
+int gapa_cuda_ga_mutate(int device, const int32_t* block, int rows, int k, int row_offset, double pm, int32_t pool_size,
+                        uint64_t seed, uint64_t generation, int32_t* out) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    if (rows < 0 || k < 0) return fail(GAPA_CUDA_E_INVALID, "mutate: shape mismatch");
+    Tmp t;
+    int32_t *db = nullptr, *d_out = nullptr;
+    GAPA_TRY(t.up(block, static_cast<size_t>(rows) * k, &db));
+    GAPA_TRY(t.up<int32_t>(nullptr, static_cast<size_t>(rows) * k, &d_out));
+    GAPA_TRY(gapa_cuda_ga_mutate_device(db, rows, k, row_offset, pm, pool_size, seed, generation, d_out, nullptr));
+    return t.down(out, d_out, static_cast<size_t>(rows) * k);
+}
+
+int gapa_cuda_ga_eda(int device, const int32_t* elite, int s, int k, int elite_count, int32_t pool_size, uint64_t seed,
+                     uint64_t generation, int smoothing, int32_t* out) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    if (s < 0 || k < 0) return fail(GAPA_CUDA_E_INVALID, "eda_sample: shape mismatch");
+    Tmp t;
+    int32_t *de = nullptr, *d_out = nullptr;
+    GAPA_TRY(t.up(elite, static_cast<size_t>(s) * k, &de));
+    GAPA_TRY(t.up<int32_t>(nullptr, static_cast<size_t>(s) * k, &d_out));
+    GAPA_TRY(gapa_cuda_ga_eda_device(de, s, k, elite_count, pool_size, seed, generation, smoothing, d_out, nullptr));
+    return t.down(out, d_out, static_cast<size_t>(s) * k);
+}
+
+int gapa_cuda_ga_elitism(int device, const int32_t* pop, const int32_t* m_pop, int s, int k, const double* fit,
+                         const double* fit_m, int minimize, int32_t* next, double* next_fit) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    if (s < 1 || k < 0) return fail(GAPA_CUDA_E_INVALID, "elitism: shape mismatch");
+    Tmp t;
+    int32_t *dp = nullptr, *dm = nullptr, *dn = nullptr;
+    double *df = nullptr, *dfm = nullptr, *dnf = nullptr;
+    const size_t cells = static_cast<size_t>(s) * k;
+    GAPA_TRY(t.up(pop, cells, &dp));
+    GAPA_TRY(t.up(m_pop, cells, &dm));
+    GAPA_TRY(t.up<int32_t>(nullptr, cells, &dn));
+    GAPA_TRY(t.up(fit, s, &df));
+    GAPA_TRY(t.up(fit_m, s, &dfm));
+    GAPA_TRY(t.up<double>(nullptr, s, &dnf));
+    GAPA_TRY(gapa_cuda_ga_elitism_device(dp, dm, s, k, df, dfm, minimize, dn, dnf, nullptr));
+    GAPA_TRY(t.down(next, dn, cells));
+    return t.down(next_fit, dnf, s);
+}
+
+int gapa_cuda_rng_draws(int device, uint64_t seed, uint64_t generation, uint64_t role, uint64_t row, int count,
+                        uint64_t* out) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    if (count <= 0) return GAPA_CUDA_OK;
+    Tmp t;
+    uint64_t* d = nullptr;
+    GAPA_TRY(t.up<uint64_t>(nullptr, count, &d));
+    GAPA_LAUNCH(k_rng_draws, (count + 255) / 256, 256, 0, nullptr, seed, generation, role, row, count, d);
+    return t.down(out, d, count);
+}
+
+}  // extern "C"

@@ -1,0 +1,158 @@
+// Internal declarations shared by the .cu files behind include/gapa_cuda.h.
+// sm_100a only; nothing here is part of the ABI.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <atomic>
+#include <cstdarg>
+#include <cstdio>
+#include <string>
+#include <vector>
+
+#include "gapa_cuda.h"
+
+namespace gapa_b200 {
+
+// ---- error plumbing --------------------------------------------------------------
+int fail(int code, const char* fmt, ...);
+extern std::atomic<uint64_t> g_launches;
+
+#define GAPA_CUDA_TRY(expr)                                                                     \
+    do {                                                                                        \
+        cudaError_t err__ = (expr);                                                             \
+        if (err__ != cudaSuccess)                                                               \
+            return ::gapa_b200::fail(err__ == cudaErrorMemoryAllocation ? GAPA_CUDA_E_NOMEM     \
+                                                                        : GAPA_CUDA_E_CUDA,     \
+                                     "%s failed: %s (%s:%d)", #expr, cudaGetErrorString(err__), \
+                                     __FILE__, __LINE__);                                       \
+    } while (0)
+
+#define GAPA_TRY(expr)               \
+    do {                             \
+        int rc__ = (expr);           \
+        if (rc__ != GAPA_CUDA_OK) return rc__; \
+    } while (0)
+
+// Counts the launch and checks the launch error.
+#define GAPA_LAUNCH(kernel, grid, block, smem, stream, ...)              \
+    do {                                                                 \
+        kernel<<<(grid), (block), (smem), (stream)>>>(__VA_ARGS__);      \
+        ::gapa_b200::g_launches.fetch_add(1, std::memory_order_relaxed); \
+        GAPA_CUDA_TRY(cudaGetLastError());                               \
+    } while (0)
+
+// ---- device buffer that grows, never shrinks ---------------------------------------
+struct DevBuf {
+    void* ptr = nullptr;
+    size_t cap = 0;
+    int ensure(size_t bytes) {
+        if (bytes <= cap) return GAPA_CUDA_OK;
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+        size_t want = bytes + bytes / 8 + 256;
+        GAPA_CUDA_TRY(cudaMalloc(&ptr, want));
+        cap = want;
+        return GAPA_CUDA_OK;
+    }
+    void release() {
+        if (ptr) cudaFree(ptr);
+        ptr = nullptr;
+        cap = 0;
+    }
+    template <typename T>
+    T* as() const { return static_cast<T*>(ptr); }
+};
+
+// ---- RNG twin of include/gapa/rng.hpp ---------------------------------------------
+__host__ __device__ __forceinline__ uint64_t mix64(uint64_t x) {  // rng.hpp:8-13
+    x += 0x9E3779B97F4A7C15ull;
+    x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+    x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+    return x ^ (x >> 31);
+}
+__host__ __device__ __forceinline__ uint64_t stream_key(uint64_t seed, uint64_t generation, uint64_t role,
+                                                        uint64_t row) {  // rng.hpp:59-65
+    uint64_t key = mix64(seed);
+    key = mix64(key ^ generation);
+    key = mix64(key ^ role);
+    return mix64(key ^ row);
+}
+// j-th draw (j >= 1) of the stream: the reference pre-increments its counter (rng.hpp:21),
+// which makes draws random-access in j — one thread per (row, column) needs no state.
+__host__ __device__ __forceinline__ uint64_t draw_u64(uint64_t key, uint64_t j) {
+    return mix64(key + 0x632BE59BD9B4E019ull * j);
+}
+// next_index (rng.hpp:28-31): high 64 bits of u64 x u32
+__device__ __forceinline__ uint32_t draw_index(uint64_t key, uint64_t j, uint32_t bound) {
+    return static_cast<uint32_t>(__umul64hi(draw_u64(key, j), static_cast<uint64_t>(bound)));
+}
+// next_unit (rng.hpp:24): both steps are exact in FP64
+__device__ __forceinline__ double draw_unit(uint64_t key, uint64_t j) {
+    return __ull2double_rn(draw_u64(key, j) >> 11) * 0x1.0p-53;
+}
+// next_bernoulli(p) (rng.hpp:33) is  (u >> 11) * 2^-53 < p.  The left side is an
+// exactly representable multiple of 2^-53, so the test equals the integer test
+// (u >> 11) < ceil(p * 2^53); the threshold is computed once on the host.
+uint64_t bernoulli_threshold(double p);
+__device__ __forceinline__ bool draw_bernoulli(uint64_t key, uint64_t j, uint64_t threshold) {
+    return (draw_u64(key, j) >> 11) < threshold;
+}
+
+// ---- context -------------------------------------------------------------------------
+struct PcScratch;   // pc_kernels.cu
+struct LpaScratch;  // lpa_kernels.cu
+struct CdaScratch;  // cda_kernels.cu
+
+}  // namespace gapa_b200
+
+struct gapa_cuda_ctx {
+    int device = 0;
+    int32_t n = 0;
+    int64_t m = 0;
+    int sm_count = 148;
+    // host copies of the CSR (pool mapping, validation)
+    std::vector<int32_t> h_row_ptr, h_col_idx, h_edge_id;
+    // device CSR, shared by every individual, read-only
+    int32_t* d_row_ptr = nullptr;   // n + 1
+    int32_t* d_col_idx = nullptr;   // 2m, ascending per row
+    int32_t* d_edge_id = nullptr;   // 2m, rank of the undirected edge in (u,v) order
+    int32_t* d_edge_u = nullptr;    // m, endpoints by edge rank
+    int32_t* d_edge_v = nullptr;
+    int32_t* d_by_degree = nullptr; // n, vertices by descending degree (BFS source candidates)
+    // pool
+    int pool_kind = -1;
+    int32_t pool_size = 0;
+    bool pool_identity = true;
+    int32_t* d_pool_map = nullptr;  // gene id -> node id / edge rank when not identity
+    // link-prediction split
+    int32_t T = 0, P = 0;
+    int32_t* d_pairs = nullptr;     // (T + P) x 2, test pairs first
+    // work stream + timing
+    cudaStream_t stream = nullptr;
+    cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
+    float last_eval_ms = 0.f;
+    // staging for the host-buffer entry point
+    gapa_b200::DevBuf genes_stage, out_stage, status_buf;
+    int32_t* h_status = nullptr;    // pinned
+    gapa_b200::PcScratch* pc = nullptr;
+    gapa_b200::LpaScratch* lpa = nullptr;
+    gapa_b200::CdaScratch* cda = nullptr;
+};
+
+namespace gapa_b200 {
+
+// per-task evaluators: genes/out on the device, work enqueued on ctx->stream_for(stream)
+int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, int cols, double* out_dev,
+            cudaStream_t stream);
+int lpa_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, double* out_dev,
+             cudaStream_t stream);
+int cda_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, double* out_dev,
+             cudaStream_t stream);
+void pc_free(gapa_cuda_ctx* ctx);
+void lpa_free(gapa_cuda_ctx* ctx);
+void cda_free(gapa_cuda_ctx* ctx);
+
+}  // namespace gapa_b200

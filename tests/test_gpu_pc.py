@@ -1,0 +1,117 @@
+"""PC / MCN fitness: CUDA path vs the oracle, bit-exact (integers).
+
+Mirrors tests/test_fitness.cpp:132-162 and acceptance.cpp:83-105 of the reference."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _objective(gp, graph, task):
+    pool = gp.build_gene_pool(graph, gp.PoolKind.NodeRemoval)
+    cls = gp.PairwiseConnectivityObjective if task == 0 else gp.SixDstObjective
+    return cls(graph, pool), pool
+
+
+def _random_graph(rng, n, density):
+    iu = np.triu_indices(n, 1)
+    keep = rng.random(len(iu[0])) < density
+    return np.stack([iu[0][keep], iu[1][keep]], axis=1).astype(np.int32)
+
+
+@pytest.mark.parametrize("task", [0, 1])
+def test_config1_known_answers(gp, oracle, cuda_device, task):
+    g = gp.barabasi_albert(1000, 2, 1)
+    obj, pool = _objective(gp, g, task)
+    pop = gp.init_population(pool.size(), 4, 50, 1)
+    got = obj.evaluate_batch(pop)
+    want = [447931, 449826, 450775, 450775] if task == 0 else [947, 949, 950, 950]  # SURVEY §8c KATs
+    assert got.tolist() == want
+    og = oracle.graph_from_edges(g.n, g.edges())
+    assert np.array_equal(got, oracle.eval_batch(og, task, pop))
+
+
+@pytest.mark.parametrize("task", [0, 1])
+def test_random_instances_exact(gp, oracle, cuda_device, task):
+    """50 random ER graphs x several individuals, like test_fitness.cpp:132-152."""
+    rng = np.random.default_rng(7 + task)
+    for trial in range(50):
+        n = int(rng.integers(4, 90))
+        edges = _random_graph(rng, n, float(rng.uniform(0.01, 0.3)))
+        g = gp.Graph(n, edges)
+        obj, pool = _objective(gp, g, task)
+        k = int(rng.integers(0, n + 1))
+        rows = int(rng.integers(1, 70))
+        batch = rng.integers(0, n, size=(rows, k)).astype(np.int32)
+        og = oracle.graph_from_edges(n, edges)
+        assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(og, task, batch)), (trial, n, k, rows)
+
+
+def test_fixed_values(gp, cuda_device):
+    """K5 -> 10, all removed -> 0 (test_fitness.cpp:154-162); MCN of all-removed is 1."""
+    n = 5
+    edges = [(u, v) for u in range(n) for v in range(u + 1, n)]
+    g = gp.Graph(n, edges)
+    pc, _ = _objective(gp, g, 0)
+    mcn, _ = _objective(gp, g, 1)
+    assert pc.evaluate_batch(np.zeros((1, 0), np.int32)).tolist() == [10.0]
+    assert pc.evaluate_one(np.arange(5)) == 0.0
+    assert mcn.evaluate_one(np.arange(5)) == 1.0
+    assert mcn.evaluate_one([]) == 5.0
+    assert pc.evaluate_one([0, 0, 0]) == 6.0  # duplicates are idempotent: K4 left
+    assert pc.evaluate_batch(np.zeros((0, 3), np.int32)).shape == (0,)
+
+
+def test_fragmented_graphs_use_union_find(gp, oracle, cuda_device):
+    """Paths, rings, stars and disjoint cliques leave most vertices outside the BFS giant."""
+    rng = np.random.default_rng(3)
+    n = 3000
+    path = np.stack([np.arange(n - 1), np.arange(1, n)], axis=1)
+    perm = rng.permutation(n)
+    shuffled_path = perm[path]
+    cliques = np.array([(b * 6 + i, b * 6 + j) for b in range(n // 6) for i in range(6) for j in range(i + 1, 6)])
+    star = np.stack([np.zeros(n - 1, int), np.arange(1, n)], axis=1)
+    for edges in (path, shuffled_path, cliques, star):
+        g = gp.Graph(n, edges)
+        og = oracle.graph_from_edges(n, edges)
+        batch = rng.integers(0, n, size=(130, 40)).astype(np.int32)
+        for task in (0, 1):
+            obj, _ = _objective(gp, g, task)
+            assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(og, task, batch))
+
+
+def test_ragged_group_sizes_and_purity(gp, oracle, cuda_device):
+    g = gp.barabasi_albert(2000, 3, 5)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    obj, pool = _objective(gp, g, 0)
+    for rows in (1, 63, 64, 65, 127, 129, 200):
+        batch = gp.init_population(pool.size(), rows, 100, rows)
+        before = batch.copy()
+        got = obj.evaluate_batch(batch)
+        assert np.array_equal(batch, before)  # inputs never mutated (test_fitness.cpp:396-409)
+        assert np.array_equal(got, oracle.eval_batch(og, 0, batch))
+        assert np.array_equal(got, obj.evaluate_batch(batch))  # re-entrant, same answer
+
+
+def test_custom_node_pool_and_errors(gp, oracle, cuda_device):
+    g = gp.barabasi_albert(300, 2, 9)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    sub = np.arange(0, 300, 3, dtype=np.int32)  # pool over every third node
+    pool = gp.GenePool(gp.PoolKind.NodeRemoval, sub)
+    obj = gp.PairwiseConnectivityObjective(g, pool)
+    batch = np.random.default_rng(1).integers(0, len(sub), size=(10, 20)).astype(np.int32)
+    assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(og, 0, sub[batch]))
+    with pytest.raises(gp.capi.GapaCudaError) as e:
+        obj.evaluate_batch(np.full((2, 3), len(sub), np.int32))
+    assert e.value.code == gp.capi.E_RANGE
+    with pytest.raises(gp.capi.GapaCudaError):
+        gp.PairwiseConnectivityObjective(g, gp.build_gene_pool(g, gp.PoolKind.EdgeRemoval))
+
+
+def test_medium_power_law_graph(gp, oracle, cuda_device):
+    """n = 1e5 BA graph, 5 % removal: the bit-sliced giant sweep + leftovers, vs the CSR oracle."""
+    g = gp.barabasi_albert(100_000, 5, 1)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    obj, pool = _objective(gp, g, 0)
+    batch = gp.init_population(pool.size(), 96, 5000, 1)
+    assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(og, 0, batch, threads=8))
