@@ -1,5 +1,422 @@
+// Community-detection attack fitness (GAPA_TASK_CDA): modularity of the greedy
+// detector's partition on the edge-perturbed graph.
+//
+// Reference path per individual (fitness.cpp:35-41): copy the dense adjacency, clear
+// two bits per gene, return -0.5 if no edge is left, else detect_communities
+// (community.cpp:28-91) — repeat { scan ALL adjacent community pairs (a < b) in (a, b)
+// order, gain = e/m - da*db/(2*m*m) in FP64, keep the strictly greatest; merge b into
+// a } — then modularity() (community.cpp:93-117) summed over communities in order of
+// their smallest member.  The rescans make it O(#merges x #pairs) through std::map.
+//
+// Here: one CTA per individual runs the identical merge sequence on CNM-style state:
+//   * per community an unsorted neighbour list (id, edge count, cached gain) in an
+//     L2-resident entry pool, seeded in place from the CSR rows minus removed edges;
+//   * per community a cached best partner among ids greater than its own.  m is
+//     constant during a detection, so only pairs touching the merged community
+//     change gain; every other cached gain is bit-identical to a fresh evaluation;
+//   * each step = block-wide argmax over the cached bests with the reference's
+//     tie-break (greatest gain, then smallest a, then smallest b == first strictly
+//     greater pair in (a, b) scan order), then a cooperative merge: fold list(b) into
+//     list(a) through a position map in shared memory, and one warp per neighbour c
+//     patches list(c) (b -> a, counts, gain) and refreshes c's cached best.
+// Gains use the reference's exact FP64 expression (IEEE division, no FMA: the library
+// is built with -fmad=false); community ids are "smallest member" because b always
+// merges into a < b; Q is accumulated sequentially in ascending community id, which
+// is first-appearance order (community.cpp:17-26).
+#include <algorithm>
+
 #include "internal.cuh"
+
 namespace gapa_b200 {
-int cda_eval(gapa_cuda_ctx*, const int32_t*, int, int, double*, cudaStream_t) { return fail(GAPA_CUDA_E_INVALID, "cda_fitness: kernel not built yet"); }
-void cda_free(gapa_cuda_ctx*) {}
+
+static constexpr int kCdaThreads = 1024;
+static constexpr int kCdaWarps = kCdaThreads / 32;
+
+struct CdaScratch {
+    DevBuf gone, ints, doubles, e_id, e_cnt, e_gain, status;
+    size_t pool_cap = 0;
+    int slots = 0;
+};
+
+struct CdaArgs {
+    const int32_t* row_ptr;
+    const int32_t* col_idx;
+    const int32_t* edge_id;
+    const int32_t* pool_map;
+    int pool_size;
+    int n;
+    int mask_words;
+    long long csr_slots;   // 2m: the first csr_slots pool entries mirror the CSR rows
+    long long pool_cap;    // entries per individual slot
+    unsigned* gone;        // [slots][mask_words]
+    int32_t* ints;         // [slots][6][n]: cdeg, head, len, cap, merged_into, best_id
+    int32_t* pos_global;   // [slots][n] position map when it does not fit in shared memory (may be null)
+    double* best_gain;     // [slots][n]
+    int32_t* e_id;         // [slots][pool_cap]
+    int32_t* e_cnt;
+    double* e_gain;
+    int* status;           // [0] = GAPA_CUDA_E_RANGE, [1] = pool overflow
+};
+
+struct Cand {
+    double gain;
+    int a, b;
+};
+// the reference's scan keeps the first strictly greater gain in (a asc, b asc) order
+__device__ __forceinline__ bool cand_better(const Cand& x, const Cand& y) {
+    if (x.b < 0) return false;
+    if (y.b < 0) return true;
+    if (x.gain != y.gain) return x.gain > y.gain;
+    if (x.a != y.a) return x.a < y.a;
+    return x.b < y.b;
 }
+__device__ __forceinline__ Cand cand_warp_best(Cand c) {
+    for (int off = 16; off; off >>= 1) {
+        Cand o;
+        o.gain = __shfl_xor_sync(0xffffffffu, c.gain, off);
+        o.a = __shfl_xor_sync(0xffffffffu, c.a, off);
+        o.b = __shfl_xor_sync(0xffffffffu, c.b, off);
+        if (cand_better(o, c)) c = o;
+    }
+    return c;
+}
+// community.cpp:63
+__device__ __forceinline__ double merge_gain(int edges, int da, int db, double m, double den) {
+    return static_cast<double>(edges) / m - static_cast<double>(da) * static_cast<double>(db) / den;
+}
+
+extern __shared__ int32_t cda_smem[];
+
+__global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, const int32_t* __restrict__ genes, int rows, int cols,
+                                                        int pos_in_smem, double* __restrict__ out) {
+    __shared__ Cand warp_cand[kCdaWarps];
+    __shared__ Cand chosen;
+    __shared__ long long sh_total;
+    __shared__ long long sh_pool_top;
+    __shared__ int sh_len, sh_pb, sh_new_head, sh_abort, sh_count;
+    __shared__ int sh_scan[kCdaThreads];
+
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int n = A.n;
+    const size_t slot = blockIdx.x;
+    unsigned* gone = A.gone + slot * A.mask_words;
+    int32_t* cdeg = A.ints + slot * 6 * static_cast<size_t>(n);
+    int32_t* head = cdeg + n;
+    int32_t* len = head + n;
+    int32_t* cap = len + n;
+    int32_t* merged_into = cap + n;
+    int32_t* best_id = merged_into + n;
+    double* best_gain = A.best_gain + slot * n;
+    int32_t* e_id = A.e_id + slot * A.pool_cap;
+    int32_t* e_cnt = A.e_cnt + slot * A.pool_cap;
+    double* e_gain = A.e_gain + slot * A.pool_cap;
+    int32_t* pos = pos_in_smem ? cda_smem : A.pos_global + slot * n;
+
+    for (int r = blockIdx.x; r < rows; r += gridDim.x) {
+        // ---- perturbation: edge-removed bitmask (gene_pool.cpp:53-56) -----------------
+        for (int w = tid; w < A.mask_words; w += kCdaThreads) gone[w] = 0u;
+        if (tid == 0) { sh_total = 0; sh_abort = 0; }
+        __syncthreads();
+        const int32_t* g = genes + static_cast<size_t>(r) * cols;
+        for (int j = tid; j < cols; j += kCdaThreads) {
+            const int gene = g[j];
+            if (gene < 0 || gene >= A.pool_size) { A.status[0] = GAPA_CUDA_E_RANGE; sh_abort = 1; continue; }
+            const int e = A.pool_map ? A.pool_map[gene] : gene;
+            atomicOr(&gone[e >> 5], 1u << (e & 31));
+        }
+        __syncthreads();
+        if (sh_abort) { if (tid == 0) out[r] = 0.0; __syncthreads(); continue; }
+
+        // ---- singleton communities: list(u) = surviving CSR row, in place --------------
+        long long my_deg = 0;
+        for (int u = tid; u < n; u += kCdaThreads) {
+            const int off = A.row_ptr[u], end = A.row_ptr[u + 1];
+            int cnt = 0;
+            for (int i = off; i < end; ++i) {
+                const int e = A.edge_id[i];
+                if (!((gone[e >> 5] >> (e & 31)) & 1u)) {
+                    e_id[off + cnt] = A.col_idx[i];
+                    e_cnt[off + cnt] = 1;
+                    ++cnt;
+                }
+            }
+            head[u] = off; len[u] = cnt; cap[u] = end - off; cdeg[u] = cnt; merged_into[u] = -1;
+            pos[u] = -1;
+            my_deg += cnt;
+        }
+        for (int off = 16; off; off >>= 1) my_deg += __shfl_down_sync(0xffffffffu, my_deg, off);
+        if (lane == 0 && my_deg) atomicAdd(reinterpret_cast<unsigned long long*>(&sh_total), static_cast<unsigned long long>(my_deg));
+        __syncthreads();
+        const long long total_degree = sh_total;
+        if (total_degree == 0) {  // fitness.cpp:39
+            if (tid == 0) out[r] = -0.5;
+            __syncthreads();
+            continue;
+        }
+        const double m = static_cast<double>(total_degree) / 2.0;  // community.cpp:36
+        const double den = 2.0 * m * m;
+        if (tid == 0) sh_pool_top = A.csr_slots;
+
+        // initial gains and cached bests
+        for (int u = tid; u < n; u += kCdaThreads) {
+            const int h = head[u], l = len[u], du = cdeg[u];
+            Cand best{0.0, u, -1};
+            for (int i = 0; i < l; ++i) {
+                const int v = e_id[h + i];
+                const double gn = merge_gain(1, du, cdeg[v], m, den);
+                e_gain[h + i] = gn;
+                if (v > u && gn > 0.0) {
+                    const Cand c{gn, u, v};
+                    if (cand_better(c, best)) best = c;
+                }
+            }
+            best_gain[u] = best.gain;
+            best_id[u] = best.b;
+        }
+        __syncthreads();
+
+        // ---- greedy agglomeration (community.cpp:55-87) --------------------------------
+        for (;;) {
+            Cand mine{0.0, -1, -1};
+            for (int c = tid; c < n; c += kCdaThreads) {
+                const int b = best_id[c];
+                if (b >= 0) {
+                    const Cand x{best_gain[c], c, b};
+                    if (cand_better(x, mine)) mine = x;
+                }
+            }
+            mine = cand_warp_best(mine);
+            if (lane == 0) warp_cand[warp] = mine;
+            __syncthreads();
+            if (warp == 0) {
+                Cand x = warp_cand[lane];
+                x = cand_warp_best(x);
+                if (lane == 0) chosen = x;
+            }
+            __syncthreads();
+            const int a = chosen.a, b = chosen.b;
+            if (b < 0) break;
+
+            // make room: list(a) must hold len(a) + len(b) entries
+            const int la = len[a], lb = len[b];
+            int ha = head[a];
+            const int hb = head[b];
+            if (cap[a] < la + lb) {
+                if (tid == 0) {
+                    const long long want = 2ll * (la + lb);
+                    if (sh_pool_top + want > A.pool_cap) { sh_abort = 1; A.status[1] = 1; }
+                    else { sh_new_head = static_cast<int>(sh_pool_top); sh_pool_top += want; }
+                }
+                __syncthreads();
+                if (sh_abort) break;
+                const int nh = sh_new_head;
+                for (int i = tid; i < la; i += kCdaThreads) { e_id[nh + i] = e_id[ha + i]; e_cnt[nh + i] = e_cnt[ha + i]; }
+                __syncthreads();
+                if (tid == 0) { head[a] = nh; cap[a] = 2 * (la + lb); }
+                ha = nh;
+            }
+            // mark positions of list(a)
+            for (int i = tid; i < la; i += kCdaThreads) pos[e_id[ha + i]] = i;
+            if (tid == 0) sh_len = la;
+            __syncthreads();
+            if (tid == 0) sh_pb = pos[b];
+            // fold list(b) into list(a)
+            for (int j = tid; j < lb; j += kCdaThreads) {
+                const int c = e_id[hb + j];
+                if (c == a) continue;
+                const int e = e_cnt[hb + j];
+                const int p = pos[c];
+                if (p >= 0) e_cnt[ha + p] += e;
+                else {
+                    const int q = atomicAdd(&sh_len, 1);
+                    e_id[ha + q] = c;
+                    e_cnt[ha + q] = e;
+                }
+            }
+            __syncthreads();
+            for (int i = tid; i < la; i += kCdaThreads) pos[e_id[ha + i]] = -1;
+            __syncthreads();
+            if (tid == 0) {  // drop the (a, b) entry itself
+                const int last = sh_len - 1, pb = sh_pb;
+                if (pb != last) { e_id[ha + pb] = e_id[ha + last]; e_cnt[ha + pb] = e_cnt[ha + last]; }
+                sh_len = last;
+                len[a] = last;
+                cdeg[a] += cdeg[b];
+                len[b] = 0;
+                merged_into[b] = a;
+                best_id[b] = -1;
+            }
+            __syncthreads();
+            const int la2 = sh_len, da = cdeg[a];
+
+            // one warp per neighbour c of the merged community
+            Cand best_a{0.0, a, -1};
+            for (int i = warp; i < la2; i += kCdaWarps) {
+                const int c = e_id[ha + i], e = e_cnt[ha + i];
+                const double gn = merge_gain(e, da, cdeg[c], m, den);
+                if (c > a && gn > 0.0) {
+                    const Cand x{gn, a, c};
+                    if (cand_better(x, best_a)) best_a = x;
+                }
+                const int hc = head[c];
+                int lc = len[c];
+                int pa = -1, pbb = -1;
+                for (int t = lane; t < lc; t += 32) {
+                    const int id = e_id[hc + t];
+                    if (id == a) pa = t;
+                    if (id == b) pbb = t;
+                }
+                pa = __reduce_max_sync(0xffffffffu, pa);
+                pbb = __reduce_max_sync(0xffffffffu, pbb);
+                if (lane == 0) {
+                    e_gain[ha + i] = gn;
+                    if (pa >= 0) {
+                        if (pbb >= 0) {
+                            const int last = lc - 1;
+                            if (pbb != last) {
+                                e_id[hc + pbb] = e_id[hc + last];
+                                e_cnt[hc + pbb] = e_cnt[hc + last];
+                                e_gain[hc + pbb] = e_gain[hc + last];
+                                if (pa == last) pa = pbb;
+                            }
+                            lc = last;
+                            len[c] = lc;
+                        }
+                        e_cnt[hc + pa] = e;
+                        e_gain[hc + pa] = gn;
+                    } else {
+                        e_id[hc + pbb] = a;
+                        e_cnt[hc + pbb] = e;
+                        e_gain[hc + pbb] = gn;
+                    }
+                }
+                lc = __shfl_sync(0xffffffffu, lc, 0);
+                __syncwarp();
+                Cand best_c{0.0, c, -1};
+                for (int t = lane; t < lc; t += 32) {
+                    const int id = e_id[hc + t];
+                    const double gg = e_gain[hc + t];
+                    if (id > c && gg > 0.0) {
+                        const Cand x{gg, c, id};
+                        if (cand_better(x, best_c)) best_c = x;
+                    }
+                }
+                best_c = cand_warp_best(best_c);
+                if (lane == 0) { best_gain[c] = best_c.gain; best_id[c] = best_c.b; }
+            }
+            if (lane == 0) warp_cand[warp] = best_a;  // identical in every lane of the warp
+            __syncthreads();
+            if (warp == 0) {
+                Cand x = warp_cand[lane];
+                x = cand_warp_best(x);
+                if (lane == 0) { best_gain[a] = x.gain; best_id[a] = x.b; }
+            }
+            __syncthreads();
+        }
+        if (sh_abort) { if (tid == 0) out[r] = 0.0; __syncthreads(); continue; }
+
+        // ---- modularity (community.cpp:93-117) ------------------------------------------
+        // Live communities in ascending id == first-appearance order.  A term that is
+        // exactly zero cannot change the running sum, so only non-zero terms are queued.
+        const double two_m = static_cast<double>(total_degree);
+        const int per = (n + kCdaThreads - 1) / kCdaThreads;
+        const int c_lo = min(tid * per, n), c_hi = min(c_lo + per, n);
+        int queued = 0;
+        for (int c = c_lo; c < c_hi; ++c) {
+            if (merged_into[c] != -1) continue;
+            long long outside = 0;
+            const int h = head[c], l = len[c];
+            for (int i = 0; i < l; ++i) outside += e_cnt[h + i];
+            const double intra = static_cast<double>((cdeg[c] - outside) / 2);
+            const double ee = intra / (two_m / 2.0);
+            const double aa = static_cast<double>(cdeg[c]) / two_m;
+            const double term = ee - aa * aa;
+            best_gain[c] = term;
+            best_id[c] = term != 0.0 ? 1 : 0;
+            queued += term != 0.0;
+        }
+        sh_scan[tid] = queued;
+        __syncthreads();
+        for (int off = 1; off < kCdaThreads; off <<= 1) {
+            const int add = tid >= off ? sh_scan[tid - off] : 0;
+            __syncthreads();
+            sh_scan[tid] += add;
+            __syncthreads();
+        }
+        int write = sh_scan[tid] - queued;
+        for (int c = c_lo; c < c_hi; ++c)
+            if (merged_into[c] == -1 && best_id[c]) head[write++] = c;  // head[] is free now: ordered queue
+        if (tid == kCdaThreads - 1) sh_count = sh_scan[tid];
+        __syncthreads();
+        if (tid == 0) {
+            double q = 0.0;
+            const int count = sh_count;
+            for (int i = 0; i < count; ++i) q += best_gain[head[i]];
+            out[r] = q;
+        }
+        __syncthreads();
+    }
+}
+
+int cda_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, double* out_dev, cudaStream_t stream) {
+    if (!ctx->cda) ctx->cda = new CdaScratch();
+    CdaScratch* s = ctx->cda;
+    const int n = ctx->n;
+    if (n == 0) return fail(GAPA_CUDA_E_INVALID, "cda_fitness: empty graph");
+    const long long csr_slots = 2 * ctx->m;
+    const int mask_words = static_cast<int>((ctx->m + 31) / 32) + 1;
+    const int slots = std::max(1, std::min(rows, ctx->sm_count));
+    const bool pos_in_smem = static_cast<size_t>(n) * sizeof(int32_t) <= 160 * 1024;
+    if (s->pool_cap == 0) s->pool_cap = static_cast<size_t>(csr_slots) * 6 + 4096;
+
+    for (;;) {
+        GAPA_TRY(s->gone.ensure(sizeof(unsigned) * mask_words * static_cast<size_t>(slots)));
+        GAPA_TRY(s->ints.ensure(sizeof(int32_t) * 7 * static_cast<size_t>(n) * slots));
+        GAPA_TRY(s->doubles.ensure(sizeof(double) * static_cast<size_t>(n) * slots));
+        GAPA_TRY(s->e_id.ensure(sizeof(int32_t) * s->pool_cap * slots));
+        GAPA_TRY(s->e_cnt.ensure(sizeof(int32_t) * s->pool_cap * slots));
+        GAPA_TRY(s->e_gain.ensure(sizeof(double) * s->pool_cap * slots));
+        GAPA_TRY(s->status.ensure(2 * sizeof(int)));
+        GAPA_CUDA_TRY(cudaMemsetAsync(s->status.ptr, 0, 2 * sizeof(int), stream));
+
+        CdaArgs A;
+        A.row_ptr = ctx->d_row_ptr;
+        A.col_idx = ctx->d_col_idx;
+        A.edge_id = ctx->d_edge_id;
+        A.pool_map = ctx->pool_identity ? nullptr : ctx->d_pool_map;
+        A.pool_size = ctx->pool_size;
+        A.n = n;
+        A.mask_words = mask_words;
+        A.csr_slots = csr_slots;
+        A.pool_cap = static_cast<long long>(s->pool_cap);
+        A.gone = s->gone.as<unsigned>();
+        A.ints = s->ints.as<int32_t>();
+        A.pos_global = pos_in_smem ? nullptr : s->ints.as<int32_t>() + static_cast<size_t>(6) * n * slots;
+        A.best_gain = s->doubles.as<double>();
+        A.e_id = s->e_id.as<int32_t>();
+        A.e_cnt = s->e_cnt.as<int32_t>();
+        A.e_gain = s->e_gain.as<double>();
+        A.status = s->status.as<int>();
+        const size_t smem = pos_in_smem ? static_cast<size_t>(n) * sizeof(int32_t) : 0;
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_cda, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+        GAPA_LAUNCH(k_cda, slots, kCdaThreads, smem, stream, A, genes_dev, rows, cols, pos_in_smem ? 1 : 0, out_dev);
+        GAPA_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, s->status.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
+        GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
+        if (ctx->h_status[0] == GAPA_CUDA_E_RANGE) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
+        if (ctx->h_status[1]) {  // entry pool exhausted: double it and evaluate the batch again
+            s->pool_cap *= 2;
+            continue;
+        }
+        return GAPA_CUDA_OK;
+    }
+}
+
+void cda_free(gapa_cuda_ctx* ctx) {
+    if (!ctx->cda) return;
+    CdaScratch* s = ctx->cda;
+    for (DevBuf* b : {&s->gone, &s->ints, &s->doubles, &s->e_id, &s->e_cnt, &s->e_gain, &s->status}) b->release();
+    delete s;
+    ctx->cda = nullptr;
+}
+
+}  // namespace gapa_b200

@@ -317,6 +317,8 @@ int gapa_cuda_eval_batch_device(gapa_cuda_ctx* c, int task, const int32_t* genes
     if (rows < 0 || cols < 0) return fail(GAPA_CUDA_E_INVALID, "eval_batch: negative shape");
     if (rows == 0) return GAPA_CUDA_OK;
     if (!out_dev || (cols > 0 && !genes_dev)) return fail(GAPA_CUDA_E_INVALID, "eval_batch: null buffer");
+    std::unique_lock<std::mutex> lock(c->mu, std::defer_lock);
+    if (stream != static_cast<void*>(c->stream)) lock.lock();  // the host-buffer form already holds it
     GAPA_CUDA_TRY(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     GAPA_CUDA_TRY(cudaEventRecord(c->ev_start, s));
@@ -337,6 +339,7 @@ int gapa_cuda_eval_batch(gapa_cuda_ctx* c, int task, const int32_t* genes_host, 
     if (rows < 0 || cols < 0) return fail(GAPA_CUDA_E_INVALID, "eval_batch: negative shape");
     if (rows == 0) return GAPA_CUDA_OK;
     if (!out_host || (cols > 0 && !genes_host)) return fail(GAPA_CUDA_E_INVALID, "eval_batch: null buffer");
+    std::lock_guard<std::mutex> lock(c->mu);
     GAPA_CUDA_TRY(cudaSetDevice(c->device));
     const size_t cells = static_cast<size_t>(rows) * cols;
     GAPA_TRY(c->genes_stage.ensure(sizeof(int32_t) * std::max<size_t>(cells, 1)));

@@ -5,7 +5,10 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <algorithm>
 #include <atomic>
+#include <mutex>
+#include <utility>
 #include <cstdarg>
 #include <cstdio>
 #include <string>
@@ -134,6 +137,9 @@ struct gapa_cuda_ctx {
     cudaStream_t stream = nullptr;
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
     float last_eval_ms = 0.f;
+    // FitnessFunction methods are const and called concurrently from worker threads in the
+    // reference (modes.cpp:85,209); evaluations on one context are serialised here.
+    std::mutex mu;
     // staging for the host-buffer entry point
     gapa_b200::DevBuf genes_stage, out_stage, status_buf;
     int32_t* h_status = nullptr;    // pinned

@@ -1,3 +1,196 @@
+// gapa_cuda_run: the generation loop of modes.cpp:132-178 (identical results to
+// run_serial, modes.cpp:359-418) with the population resident in HBM.
+//
+//   gen 1:      init_population (generation key 0) -> evaluate
+//   every gen:  roulette_select -> crossover -> mutate   (or eda_sample -> mutate)
+//               -> evaluate(M_POP) -> elitism -> best = fit[0], mean = sum(fit)/s
+//
+// Sharding (world > 1) follows the reference's M mode (modes.cpp:190-349) with the
+// roles the SURVEY recommends: every rank holds the whole population and runs the
+// cheap, globally keyed operators redundantly (they are bit-identical on every rank),
+// evaluates only its partition_rows block (modes.cpp:506-516), and one all-gather of
+// fitness doubles per evaluation is the only exchange — genomes never cross NVLink.
+#include <chrono>
+#include <cmath>
+
 #include "internal.cuh"
+
+namespace gapa_b200 {
+int launch_init(uint32_t, int, int, int, uint64_t, uint64_t, int32_t*, cudaStream_t);
+int launch_select(const double*, int, int, uint64_t, uint64_t, int32_t*, double*, double*, int*, cudaStream_t);
+int launch_crossover_mutate(const int32_t*, const int32_t*, int, int, int, double, double, uint32_t, uint64_t, uint64_t,
+                            int32_t*, cudaStream_t);
+int launch_mutate(const int32_t*, int, int, int, double, uint32_t, uint64_t, uint64_t, int32_t*, cudaStream_t);
+int launch_eda(const int32_t*, int, int, int, uint32_t, uint64_t, uint64_t, int32_t*, cudaStream_t);
+int launch_elitism(const int32_t*, const int32_t*, int, int, const double*, const double*, int, int32_t*, double*, int32_t*,
+                   int*, cudaStream_t);
+
+// record_generation (modes.cpp:35-43): best = front, mean = SEQUENTIAL sum / s so that
+// non-integer fitness reproduces std::accumulate bit for bit.
+__global__ void k_ga_stats(const double* __restrict__ fit, int s, double* best, double* mean) {
+    if (blockIdx.x || threadIdx.x) return;
+    double sum = 0.0;
+    for (int i = 0; i < s; ++i) sum += fit[i];
+    *best = fit[0];
+    *mean = sum / static_cast<double>(s);
+}
+
+__global__ void k_check_nan(const double* __restrict__ fit, int s, int* status) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < s && isnan(fit[i])) *status = GAPA_CUDA_E_NAN;
+}
+}  // namespace gapa_b200
+
 using namespace gapa_b200;
-extern "C" int gapa_cuda_run(gapa_cuda_ctx*, const gapa_cuda_run_params*, gapa_cuda_allgather_fn, void*, gapa_cuda_run_result*) { return fail(GAPA_CUDA_E_INVALID, "run: not built yet"); }
+
+namespace {
+struct RunBuffers {
+    DevBuf pop, crossed, mutated, next, partner, fit, fit_m, fit_next, weights, cumulative, src_of_rank, status, hist;
+    ~RunBuffers() {
+        for (DevBuf* b : {&pop, &crossed, &mutated, &next, &partner, &fit, &fit_m, &fit_next, &weights, &cumulative,
+                          &src_of_rank, &status, &hist})
+            b->release();
+    }
+};
+
+int eval_rows(gapa_cuda_ctx* ctx, int task, const int32_t* genes, int rows, int cols, double* out, cudaStream_t st,
+              double* seconds) {
+    if (rows == 0) return GAPA_CUDA_OK;
+    GAPA_CUDA_TRY(cudaEventRecord(ctx->ev_start, st));
+    int rc;
+    if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) rc = pc_eval(ctx, task, genes, rows, cols, out, st);
+    else if (task == GAPA_TASK_CDA) rc = cda_eval(ctx, genes, rows, cols, out, st);
+    else rc = lpa_eval(ctx, genes, rows, cols, out, st);
+    GAPA_TRY(rc);
+    GAPA_CUDA_TRY(cudaEventRecord(ctx->ev_stop, st));
+    GAPA_CUDA_TRY(cudaEventSynchronize(ctx->ev_stop));
+    float ms = 0.f;
+    GAPA_CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_stop));
+    ctx->last_eval_ms = ms;
+    *seconds += ms * 1e-3;
+    return GAPA_CUDA_OK;
+}
+}  // namespace
+
+extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, gapa_cuda_allgather_fn exchange,
+                             void* exchange_user, gapa_cuda_run_result* result) {
+    if (!ctx || !p || !result) return fail(GAPA_CUDA_E_INVALID, "run: null argument");
+    // GAParams::validate (ga_ops.cpp:11-17) + validate_for_run (modes.cpp:26-29)
+    if (p->pop_size < 2) return fail(GAPA_CUDA_E_INVALID, "pop_size must be >= 2");
+    if (p->budget < 1) return fail(GAPA_CUDA_E_INVALID, "budget must be >= 1");
+    if (!(p->pc >= 0.0 && p->pc <= 1.0)) return fail(GAPA_CUDA_E_INVALID, "pc must be in [0, 1]");
+    if (!(p->pm >= 0.0 && p->pm <= 1.0)) return fail(GAPA_CUDA_E_INVALID, "pm must be in [0, 1]");
+    if (p->eda_interval < 0) return fail(GAPA_CUDA_E_INVALID, "eda_interval must be >= 1");
+    if (p->iterations < 1) return fail(GAPA_CUDA_E_INVALID, "iterations must be >= 1");
+    const int world = p->world < 1 ? 1 : p->world, rank = p->world < 1 ? 0 : p->rank;
+    if (rank < 0 || rank >= world) return fail(GAPA_CUDA_E_INVALID, "run: rank outside world");
+    if (world > 1 && !exchange) return fail(GAPA_CUDA_E_INVALID, "run: sharded run needs an exchange hook");
+    if (ctx->pool_size < 1) return fail(GAPA_CUDA_E_INVALID, "init_population: empty gene pool");
+    switch (p->task) {
+        case GAPA_TASK_PC: case GAPA_TASK_MCN:
+            if (ctx->pool_kind != GAPA_POOL_NODE_REMOVAL) return fail(GAPA_CUDA_E_INVALID, "run: incompatible gene pool kind");
+            break;
+        case GAPA_TASK_CDA:
+            if (ctx->pool_kind == GAPA_POOL_NODE_REMOVAL) return fail(GAPA_CUDA_E_INVALID, "run: incompatible gene pool kind");
+            break;
+        case GAPA_TASK_LPA:
+            if (ctx->pool_kind != GAPA_POOL_EDGE_REMOVAL || ctx->T < 1) return fail(GAPA_CUDA_E_INVALID, "run: link-prediction task needs an edge-removal pool and a split");
+            break;
+        default: return fail(GAPA_CUDA_E_INVALID, "unknown fitness task %d", p->task);
+    }
+    GAPA_CUDA_TRY(cudaSetDevice(ctx->device));
+
+    const int s = p->pop_size, k = p->budget, iters = p->iterations, minimize = p->minimize ? 1 : 0;
+    const uint32_t pool = static_cast<uint32_t>(ctx->pool_size);
+    const int block = (s + world - 1) / world;  // partition_rows, modes.cpp:506-516
+    const int lo = std::min(rank * block, s), hi = std::min(lo + block, s);
+    const size_t cells = static_cast<size_t>(s) * k, padded = static_cast<size_t>(block) * world;
+    cudaStream_t st = ctx->stream;
+
+    RunBuffers B;
+    GAPA_TRY(B.pop.ensure(sizeof(int32_t) * cells));
+    GAPA_TRY(B.mutated.ensure(sizeof(int32_t) * cells));
+    GAPA_TRY(B.next.ensure(sizeof(int32_t) * cells));
+    if (p->eda_interval > 0) GAPA_TRY(B.crossed.ensure(sizeof(int32_t) * cells));
+    GAPA_TRY(B.partner.ensure(sizeof(int32_t) * s));
+    GAPA_TRY(B.fit.ensure(sizeof(double) * padded));
+    GAPA_TRY(B.fit_m.ensure(sizeof(double) * padded));
+    GAPA_TRY(B.fit_next.ensure(sizeof(double) * padded));
+    GAPA_TRY(B.weights.ensure(sizeof(double) * s));
+    GAPA_TRY(B.cumulative.ensure(sizeof(double) * s));
+    GAPA_TRY(B.src_of_rank.ensure(sizeof(int32_t) * s));
+    GAPA_TRY(B.status.ensure(sizeof(int)));
+    GAPA_TRY(B.hist.ensure(sizeof(double) * 2 * iters));
+    int32_t* pop = B.pop.as<int32_t>();
+    int32_t* mutated = B.mutated.as<int32_t>();
+    int32_t* next = B.next.as<int32_t>();
+    double* fit = B.fit.as<double>();
+    double* fit_m = B.fit_m.as<double>();
+    double* fit_next = B.fit_next.as<double>();
+    double* hist = B.hist.as<double>();
+    int* status = B.status.as<int>();
+    GAPA_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), st));
+    GAPA_CUDA_TRY(cudaMemsetAsync(fit, 0, sizeof(double) * padded, st));
+    GAPA_CUDA_TRY(cudaMemsetAsync(fit_m, 0, sizeof(double) * padded, st));
+
+    result->fitness_batch_calls = 0;
+    result->eval_seconds = 0.0;
+    auto evaluate = [&](const int32_t* rows_all, double* fit_all) -> int {
+        ++result->fitness_batch_calls;
+        GAPA_TRY(eval_rows(ctx, p->task, rows_all + static_cast<size_t>(lo) * k, hi - lo, k, fit_all + lo, st,
+                           &result->eval_seconds));
+        if (world > 1) {
+            const int rc = exchange(exchange_user, fit_all, s, block, st);
+            if (rc != 0) return fail(GAPA_CUDA_E_CUDA, "run: exchange hook failed with status %d", rc);
+        }
+        return GAPA_CUDA_OK;
+    };
+    auto check_status = [&](const char* what) -> int {
+        int h = 0;
+        GAPA_CUDA_TRY(cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+        GAPA_CUDA_TRY(cudaStreamSynchronize(st));
+        if (h == GAPA_CUDA_E_NAN) return fail(GAPA_CUDA_E_NAN, "%s", what);
+        return GAPA_CUDA_OK;
+    };
+
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int gen = 1; gen <= iters; ++gen) {
+        if (gen == 1) {
+            GAPA_TRY(launch_init(pool, 0, s, k, p->seed, 0, pop, st));
+            GAPA_TRY(evaluate(pop, fit));
+            GAPA_LAUNCH(k_check_nan, (s + 255) / 256, 256, 0, st, fit, s, status);
+            GAPA_TRY(check_status("fitness evaluation failed during initialization"));  // modes.cpp:314-315
+        }
+        const uint64_t g = static_cast<uint64_t>(gen);
+        if (p->eda_interval > 0 && gen % p->eda_interval == 0) {  // modes.cpp:31-33,167-168
+            GAPA_TRY(launch_eda(pop, s, k, s, static_cast<uint32_t>(s) + pool, p->seed, g, B.crossed.as<int32_t>(), st));
+            GAPA_TRY(launch_mutate(B.crossed.as<int32_t>(), s, k, 0, p->pm, pool, p->seed, g, mutated, st));
+        } else {
+            GAPA_TRY(launch_select(fit, s, minimize, p->seed, g, B.partner.as<int32_t>(), B.weights.as<double>(),
+                                   B.cumulative.as<double>(), status, st));
+            GAPA_TRY(launch_crossover_mutate(pop, B.partner.as<int32_t>(), k, 0, s, p->pc, p->pm, pool, p->seed, g, mutated, st));
+        }
+        GAPA_TRY(evaluate(mutated, fit_m));
+        GAPA_TRY(launch_elitism(pop, mutated, s, k, fit, fit_m, minimize, next, fit_next, B.src_of_rank.as<int32_t>(),
+                                status, st));
+        std::swap(pop, next);
+        std::swap(fit, fit_next);
+        GAPA_LAUNCH(k_ga_stats, 1, 1, 0, st, fit, s, hist + (gen - 1), hist + iters + (gen - 1));
+        // NaN / non-finite fitness is an Error in the reference (ga_ops.cpp:56-57, :189-192);
+        // the flag is polled every few generations and at the end to keep the loop asynchronous.
+        if ((gen & 15) == 0 || gen == iters) {
+            int h = 0;
+            GAPA_CUDA_TRY(cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+            GAPA_CUDA_TRY(cudaStreamSynchronize(st));
+            if (h == GAPA_CUDA_E_NAN) return fail(GAPA_CUDA_E_NAN, "elitism: NaN fitness");
+        }
+    }
+    GAPA_CUDA_TRY(cudaStreamSynchronize(st));
+    result->total_wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+
+    if (result->history_best) GAPA_CUDA_TRY(cudaMemcpy(result->history_best, hist, sizeof(double) * iters, cudaMemcpyDeviceToHost));
+    if (result->history_mean) GAPA_CUDA_TRY(cudaMemcpy(result->history_mean, hist + iters, sizeof(double) * iters, cudaMemcpyDeviceToHost));
+    if (result->final_population) GAPA_CUDA_TRY(cudaMemcpy(result->final_population, pop, sizeof(int32_t) * cells, cudaMemcpyDeviceToHost));
+    if (result->final_fitness) GAPA_CUDA_TRY(cudaMemcpy(result->final_fitness, fit, sizeof(double) * s, cudaMemcpyDeviceToHost));
+    return GAPA_CUDA_OK;
+}

@@ -1,0 +1,129 @@
+"""LPA (RA-AUC) and CDA (greedy-detector modularity) fitness: CUDA path vs the oracle.
+
+Bit-exact FP64 is the bar: identical GA trajectories need identical ties.
+Mirrors tests/test_fitness.cpp:279-307 (CDA identities), :336-394 (RA / AUC / LPA)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def _edge_pool(gp, g):
+    return gp.build_gene_pool(g, gp.PoolKind.EdgeRemoval)
+
+
+# ------------------------------------------------------------------------------- LPA
+def test_lpa_known_answers(gp, oracle, cuda_device):
+    g = gp.erdos_renyi(500, 0.03, 1)
+    split = gp.build_lp_split(g, 0.1, 1)
+    pool = _edge_pool(gp, split.train)
+    k = gp.perturbation_budget(split.train, gp.PoolKind.EdgeRemoval, 0.1)
+    assert (g.edge_count(), len(split.test_edges), split.train.edge_count(), k) == (3709, 371, 3338, 334)
+    obj = gp.LinkPredictionAttackObjective(split, pool)
+    pop = gp.init_population(pool.size(), 3, k, 1)
+    got = obj.evaluate_batch(pop)
+    assert got.tolist() == [0.50374525032512119, 0.49914632994529246, 0.51192595229619087]  # SURVEY §8c KATs
+    assert obj.evaluate_one([]) == 0.50795184574363739  # empty perturbation == unattacked, exactly
+    og = oracle.graph_from_edges(g.n, g.edges())
+    os_ = oracle.split_build(og, 0.1, 1)
+    assert np.array_equal(got, oracle.eval_batch(os_, 3, pop))
+
+
+def test_lpa_random_instances_exact(gp, oracle, cuda_device):
+    rng = np.random.default_rng(21)
+    for trial in range(12):
+        n = int(rng.integers(30, 400))
+        g = gp.erdos_renyi(n, float(rng.uniform(0.03, 0.2)), trial + 1)
+        if g.edge_count() < 20:
+            continue
+        frac = float(rng.uniform(0.05, 0.5))
+        split = gp.build_lp_split(g, frac, trial)
+        pool = _edge_pool(gp, split.train)
+        obj = gp.LinkPredictionAttackObjective(split, pool)
+        os_ = oracle.split_build(oracle.graph_from_edges(g.n, g.edges()), frac, trial)
+        rows, k = int(rng.integers(1, 40)), int(rng.integers(0, pool.size() + 1))
+        batch = rng.integers(0, pool.size(), size=(rows, k)).astype(np.int32)
+        assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(os_, 3, batch)), trial
+
+
+def test_lpa_all_removed_is_half(gp, cuda_device):
+    g = gp.barabasi_albert(200, 3, 2)
+    split = gp.build_lp_split(g, 0.2, 3)
+    pool = _edge_pool(gp, split.train)
+    obj = gp.LinkPredictionAttackObjective(split, pool)
+    assert obj.evaluate_one(np.arange(pool.size())) == 0.5  # test_fitness.cpp:378-394
+    with pytest.raises(gp.capi.GapaCudaError):
+        gp.LinkPredictionAttackObjective(split, gp.build_gene_pool(split.train, gp.PoolKind.NodeRemoval))
+    with pytest.raises(gp.capi.GapaCudaError) as e:
+        obj.evaluate_one([pool.size()])
+    assert e.value.code == gp.capi.E_RANGE
+
+
+# ------------------------------------------------------------------------------- CDA
+def test_cda_known_answers(gp, oracle, cuda_device):
+    g = gp.planted_partition(10, 50, 0.2, 0.01, 1)
+    pool = _edge_pool(gp, g)
+    k = gp.perturbation_budget(g, gp.PoolKind.EdgeRemoval, 0.05)
+    assert (g.n, g.edge_count(), k) == (500, 3668, 184)
+    obj = gp.ModularityAttackObjective(g, pool)
+    pop = gp.init_population(pool.size(), 3, k, 1)
+    got = obj.evaluate_batch(pop)
+    assert got.tolist() == [0.52118299521350409, 0.53218590159358303, 0.50903959381049579]  # SURVEY §8c KATs
+    assert obj.evaluate_one([]) == 0.51897794328383418  # empty perturbation == unattacked Q exactly
+    og = oracle.graph_from_edges(g.n, g.edges())
+    assert np.array_equal(got, oracle.eval_batch(og, 2, pop))
+
+
+def test_cda_identities(gp, cuda_device):
+    two_triangles = gp.Graph(6, [(0, 1), (1, 2), (0, 2), (3, 4), (4, 5), (3, 5)])
+    pool = _edge_pool(gp, two_triangles)
+    obj = gp.ModularityAttackObjective(two_triangles, pool)
+    assert obj.evaluate_one([]) == 0.5
+    assert obj.evaluate_one(np.arange(pool.size())) == -0.5  # all edges removed: the floor, exactly
+    assert obj.evaluate_batch(np.zeros((0, 2), np.int32)).shape == (0,)
+    with pytest.raises(gp.capi.GapaCudaError):
+        gp.ModularityAttackObjective(two_triangles, gp.build_gene_pool(two_triangles, gp.PoolKind.NodeRemoval))
+
+
+def test_cda_random_instances_exact(gp, oracle, cuda_device):
+    rng = np.random.default_rng(4)
+    for trial in range(25):
+        n = int(rng.integers(6, 160))
+        kind = trial % 3
+        if kind == 0:
+            g = gp.erdos_renyi(n, float(rng.uniform(0.03, 0.3)), trial + 1)
+        elif kind == 1:
+            g = gp.barabasi_albert(n, int(rng.integers(1, 4)), trial + 1)
+        else:
+            g = gp.planted_partition(int(rng.integers(2, 6)), int(rng.integers(5, 30)), 0.4, 0.03, trial + 1)
+        if g.edge_count() == 0:
+            continue
+        pool = _edge_pool(gp, g)
+        obj = gp.ModularityAttackObjective(g, pool)
+        og = oracle.graph_from_edges(g.n, g.edges())
+        rows, k = int(rng.integers(1, 12)), int(rng.integers(0, pool.size() + 1))
+        batch = rng.integers(0, pool.size(), size=(rows, k)).astype(np.int32)
+        got, want = obj.evaluate_batch(batch), oracle.eval_batch(og, 2, batch)
+        assert np.array_equal(got, want), (trial, np.abs(got - want).max())
+
+
+def test_cda_more_individuals_than_sms(gp, oracle, cuda_device):
+    g = gp.planted_partition(4, 25, 0.3, 0.02, 7)
+    pool = _edge_pool(gp, g)
+    obj = gp.ModularityAttackObjective(g, pool)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    batch = gp.init_population(pool.size(), 400, 12, 3)
+    assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(og, 2, batch, threads=8))
+
+
+def test_cda_config2_sample(gp, oracle, cuda_device):
+    """BASELINE config 2 shape: SBM 10 x 500, 5 % edge deletion (2 individuals vs the oracle)."""
+    g = gp.planted_partition(10, 500, 0.02, 0.0005, 1)
+    assert g.edge_count() == 30321
+    pool = _edge_pool(gp, g)
+    k = gp.perturbation_budget(g, gp.PoolKind.EdgeRemoval, 0.05)
+    obj = gp.ModularityAttackObjective(g, pool)
+    assert obj.evaluate_one([]) == 0.61708453864200974  # BASELINE.md §2, unattacked Q
+    og = oracle.graph_from_edges(g.n, g.edges())
+    batch = gp.init_population(pool.size(), 2, k, 1)
+    assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(og, 2, batch, threads=2))

@@ -1,0 +1,114 @@
+"""Generation loop on the GPU: trajectories identical to the reference given the same seed.
+
+Mirrors test_parallel.cpp:86-116 (history best AND mean, final population) and the
+run-level cases of test_ga_engine.cpp:309-361."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+GOLDEN = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _same(result, want):
+    assert np.array_equal(result.history_best, want["best"])
+    assert np.array_equal(result.history_mean, want["mean"])
+    assert np.array_equal(result.final_population, want["population"])
+    assert np.array_equal(result.final_fitness, want["fitness"])
+
+
+def test_config1_full_run(gp, oracle, cuda_device):
+    """BASELINE config 1: BA(1000, 2), k = 50, pop 100, 100 generations, pc .6 pm .2, seed 1."""
+    g = gp.barabasi_albert(1000, 2, 1)
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    obj = gp.PairwiseConnectivityObjective(g, pool)
+    params = gp.GAParams(pc=0.6, pm=0.2, pop_size=100, budget=50, iterations=100, seed=1)
+    res = gp.run_ga(params, pool, obj)
+    assert res.history_best[0] == 444153.0 and res.best_fitness == 408159.0  # SURVEY §8c golden values
+    assert res.fitness_batch_calls == 101  # iterations + 1 (test_parallel.cpp:147-158)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    _same(res, oracle.run_ga(og, 0, 0.6, 0.2, 100, 50, 100, 1, threads=8))
+    assert np.all(np.diff(res.history_best) <= 0)  # monotone under elitism
+
+
+@pytest.mark.parametrize("task", [0, 1])
+def test_small_runs_match_oracle(gp, oracle, cuda_device, task):
+    for seed, eda in [(3, 0), (4, 3)]:
+        g = gp.erdos_renyi(100, 0.04, 665)
+        pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+        cls = gp.PairwiseConnectivityObjective if task == 0 else gp.SixDstObjective
+        params = gp.GAParams(pc=0.8, pm=0.1, pop_size=30, budget=8, iterations=25, seed=seed, eda_interval=eda or None)
+        res = gp.run_ga(params, pool, cls(g, pool))
+        og = oracle.graph_from_edges(g.n, g.edges())
+        _same(res, oracle.run_ga(og, task, 0.8, 0.1, 30, 8, 25, seed, eda_interval=eda))
+
+
+def test_lpa_and_cda_runs_match_oracle(gp, oracle, cuda_device):
+    g = gp.erdos_renyi(120, 0.08, 2)
+    split = gp.build_lp_split(g, 0.2, 5)
+    pool = gp.build_gene_pool(split.train, gp.PoolKind.EdgeRemoval)
+    params = gp.GAParams(pc=0.7, pm=0.1, pop_size=20, budget=30, iterations=15, seed=9)
+    res = gp.run_ga(params, pool, gp.LinkPredictionAttackObjective(split, pool))
+    os_ = oracle.split_build(oracle.graph_from_edges(g.n, g.edges()), 0.2, 5)
+    _same(res, oracle.run_ga(os_, 3, 0.7, 0.1, 20, 30, 15, 9))
+
+    g = gp.planted_partition(4, 20, 0.3, 0.03, 1)
+    pool = gp.build_gene_pool(g, gp.PoolKind.EdgeRemoval)
+    params = gp.GAParams(pc=0.8, pm=0.1, pop_size=16, budget=10, iterations=12, seed=2)
+    res = gp.run_ga(params, pool, gp.ModularityAttackObjective(g, pool))
+    _same(res, oracle.run_ga(oracle.graph_from_edges(g.n, g.edges()), 2, 0.8, 0.1, 16, 10, 12, 2))
+
+
+def test_sharded_run_equals_single(gp, cuda_device):
+    """world = 2 simulated in one process: each 'rank' evaluates its partition_rows block and the
+    exchange hook fills in the other block from a full single-GPU evaluation."""
+    import ctypes as C
+    g = gp.barabasi_albert(400, 2, 3)
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    obj = gp.PairwiseConnectivityObjective(g, pool)
+    params = gp.GAParams(pc=0.6, pm=0.2, pop_size=25, budget=20, iterations=10, seed=5)
+    single = gp.run_ga(params, pool, obj)
+    lib = gp.capi.load()
+    helper = gp.PairwiseConnectivityObjective(g, pool)
+
+    for rank in (0, 1):
+        lo, hi = gp.partition_rows(25, 2)[rank]
+        state = {"gen": 0}
+
+        # the hook needs each generation's mutated matrix; derive it with the operator API
+        fit = helper.evaluate_batch(gp.init_population(pool.size(), 25, 20, 5))
+        pop = gp.init_population(pool.size(), 25, 20, 5)
+        mutated_by_gen = []
+        for gen in range(1, 11):
+            idx = gp.roulette_pick(fit, gp.Direction.Minimize, 5, gen)
+            mutated = gp.crossover_mutate(pop, idx, 0.6, 0.2, pool.size(), 5, gen)
+            fm = helper.evaluate_batch(mutated)
+            mutated_by_gen.append(mutated)
+            pop, fit = gp.elitism(pop, mutated, fit, fm, gp.Direction.Minimize)
+        assert np.array_equal(pop, single.final_population)  # stepwise operator API == fused run
+
+        def exchange2(user, fit_ptr, s, block, stream, state=state):
+            gp.capi.check(lib.gapa_cuda_stream_sync(0, stream))
+            gen = state["gen"]
+            m = gp.init_population(pool.size(), 25, 20, 5) if gen == 0 else mutated_by_gen[gen - 1]
+            full = np.ascontiguousarray(helper.evaluate_batch(m))
+            gp.capi.check(lib.gapa_cuda_memcpy_h2d(0, fit_ptr, full.ctypes.data_as(C.c_void_p), 8 * s))
+            state["gen"] += 1
+            return 0
+
+        res = gp.run_ga(params, pool, obj, rank=rank, world=2, exchange=exchange2)
+        assert np.array_equal(res.final_population, single.final_population)
+        assert np.array_equal(res.history_mean, single.history_mean)
+
+
+def test_run_rejects_bad_params(gp, cuda_device):
+    g = gp.barabasi_albert(50, 2, 1)
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    obj = gp.PairwiseConnectivityObjective(g, pool)
+    for bad in (dict(pop_size=1), dict(budget=0), dict(iterations=0), dict(pc=1.5), dict(pm=-0.1), dict(eda_interval=0)):
+        kw = dict(pc=0.5, pm=0.1, pop_size=10, budget=3, iterations=2, seed=1)
+        kw.update(bad)
+        with pytest.raises(gp.capi.GapaCudaError):
+            gp.run_ga(gp.GAParams(**kw), pool, obj)
