@@ -1,0 +1,206 @@
+"""Generates tests/golden/*.json from the UNMODIFIED reference (oracle/_ref, compiled from
+/root/reference/proj by oracle/Makefile).  Run in the authoring container only:
+
+    python tests/golden/make_golden.py
+
+The JSON files are committed; nothing in tests/ or bench.py reads /root/reference at run
+time.  Doubles are stored with repr() and round-trip exactly.
+"""
+import hashlib
+import json
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
+from oracle.bindings import (MODE_M, MODE_S, MODE_SERIAL, TASK_CDA, TASK_LPA, TASK_MCN, TASK_PC, Ref)  # noqa: E402
+
+r = Ref()
+
+
+def sha(a) -> str:
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+def dump(name, obj):
+    with open(os.path.join(HERE, name), "w") as f:
+        json.dump(obj, f, indent=None, separators=(",", ":"))
+    print(name, os.path.getsize(os.path.join(HERE, name)), "bytes")
+
+
+def ints(a):
+    return np.asarray(a).astype(np.int64).tolist()
+
+
+def floats(a):
+    return [float(x) for x in np.asarray(a, dtype=np.float64)]
+
+
+# ------------------------------------------------------------------ rng + operators
+rng_cases = []
+for seed, gen, role, row in [(1, 0, 1, 0), (1, 3, 4, 7), (2**63 + 5, 100, 2, 4095), (0, 0, 5, 0), (20240601, 50, 3, 19)]:
+    rng_cases.append({
+        "seed": seed, "generation": gen, "role": role, "row": row,
+        "u64": [int(x) for x in r.stream_u64(seed, gen, role, row, 8)],
+        "unit": floats(r.stream_unit(seed, gen, role, row, 8)),
+        "index_1000": ints(r.stream_index(seed, gen, role, row, 1000, 8)),
+        "index_big": ints(r.stream_index(seed, gen, role, row, 4_000_000_000, 8)),
+    })
+ops = {"mix64": {str(x): r.mix64(x) for x in (0, 1, 2**64 - 1, 0x9E3779B97F4A7C15)}, "streams": rng_cases}
+
+gen = np.random.default_rng(12345)
+ops["init"] = []
+for pool, s, k, seed, g_ in [(1000, 4, 6, 1, 0), (1000, 100, 50, 1, 0), (7, 33, 1, 9, 0), (2_000_000_000, 5, 300, 3, 4)]:
+    m = r.init_population(pool, s, k, seed, g_)
+    ops["init"].append({"pool": pool, "s": s, "k": k, "seed": seed, "generation": g_, "sha": sha(m),
+                        "row0": ints(m[0][:16]), "block_1_3_sha": sha(r.init_population_block(pool, 1, 3, k, seed, g_))})
+
+ops["selection"] = []
+for s, ties, minimize in [(4, True, True), (4, True, False), (100, False, True), (257, True, True), (257, True, False), (1000, False, False)]:
+    f = gen.integers(0, 20, s).astype(float) if ties else gen.random(s)
+    if s == 4:
+        f = np.array([5.0, 3.0, 3.0, 9.0])
+    pop = gen.integers(0, 50, (s, 3)).astype(np.int32)
+    idx, partners = r.roulette_select(pop, f, minimize, 5, s)
+    assert np.array_equal(pop[idx], partners)
+    ops["selection"].append({"fitness": floats(f), "minimize": minimize, "seed": 5, "generation": s,
+                             "weights": floats(r.selection_weights(f, minimize)), "partner_index": ints(idx)})
+
+ops["variation"] = []
+for s, k, pool, pc, pm in [(12, 7, 1000, 0.6, 0.2), (5, 40, 9, 0.0, 1.0), (5, 40, 9, 1.0, 0.0), (30, 11, 2**31 - 1, 0.8, 0.1)]:
+    pop = gen.integers(0, pool, (s, k)).astype(np.int32)
+    f = gen.random(s)
+    idx, partners = r.roulette_select(pop, f, True, 3, 17)
+    crossed = r.crossover(pop, partners, pc, 3, 17)
+    mutated = r.mutate(crossed, pm, pool, 3, 17)
+    assert np.array_equal(mutated[2:5], r.mutate_block(crossed[2:5], 2, pm, pool, 3, 17))
+    ops["variation"].append({"pop": ints(pop), "partner_index": ints(idx), "pool": pool, "pc": pc, "pm": pm, "seed": 3,
+                             "generation": 17, "crossed": ints(crossed), "mutated": ints(mutated)})
+
+ops["elitism"] = []
+for s, k, minimize in [(4, 2, True), (4, 2, False), (37, 3, True), (64, 1, False)]:
+    pop, mp = gen.integers(0, 50, (s, k)).astype(np.int32), gen.integers(0, 50, (s, k)).astype(np.int32)
+    f, fm = gen.integers(0, 6, s).astype(float), gen.integers(0, 6, s).astype(float)
+    nxt, nf = r.elitism(pop, mp, f, fm, minimize)
+    ops["elitism"].append({"pop": ints(pop), "m_pop": ints(mp), "fit": floats(f), "fit_m": floats(fm), "minimize": minimize,
+                           "next": ints(nxt), "next_fit": floats(nf)})
+
+ops["eda"] = []
+for ec, smooth in [(30, True), (5, True), (30, False)]:
+    elite = gen.integers(0, 40, (30, 12)).astype(np.int32)
+    ops["eda"].append({"elite": ints(elite), "elite_count": ec, "pool": 40, "seed": 4, "generation": 6, "smoothing": smooth,
+                       "out": ints(r.eda_sample(elite, ec, 40, 4, 6, smooth))})
+ops["partition_rows"] = [{"s": s, "pn": pn, "blocks": r.partition_rows(s, pn)} for s, pn in [(10, 3), (4096, 8), (7, 8), (100, 1), (5, 2)]]
+dump("ops.json", ops)
+
+# ------------------------------------------------------------------ graphs + fitness
+fit = {"graphs": {}, "pc_mcn": [], "cda": [], "lpa": []}
+for name, g in [("ba_1000_2_1", r.graph_ba(1000, 2, 1)), ("er_500_0.03_1", r.graph_er(500, 0.03, 1)),
+                ("sbm_10_50_0.2_0.01_1", r.graph_sbm(10, 50, 0.2, 0.01, 1)), ("ba_3000_5_7", r.graph_ba(3000, 5, 7)),
+                ("er_100_0.04_665", r.graph_er(100, 0.04, 665)), ("sbm_4_16_0.28_0.02_671", r.graph_sbm(4, 16, 0.28, 0.02, 671))]:
+    e = r.graph_edges(g)
+    fit["graphs"][name] = {"n": r.graph_n(g), "m": r.graph_m(g), "sha": sha(e), "first": ints(e[:6])}
+
+# acceptance #3 style: random graphs x individuals, PC and MCN (exact)
+for trial in range(40):
+    n = int(gen.integers(4, 70))
+    dens = float(gen.uniform(0.02, 0.4))
+    iu = np.triu_indices(n, 1)
+    keep = gen.random(len(iu[0])) < dens
+    edges = np.stack([iu[0][keep], iu[1][keep]], 1).astype(np.int32)
+    g = r.graph_from_edges(n, edges)
+    k = int(gen.integers(0, n + 1))
+    batch = gen.integers(0, n, (3, k)).astype(np.int32)
+    fit["pc_mcn"].append({"n": n, "edges": ints(edges), "genes": ints(batch),
+                          "pc": floats(r.eval_batch(g, TASK_PC, batch)), "mcn": floats(r.eval_batch(g, TASK_MCN, batch))})
+g = r.graph_ba(1000, 2, 1)
+pop = r.init_population(1000, 4, 50, 1)
+fit["config1"] = {"pc": floats(r.eval_batch(g, TASK_PC, pop)), "mcn": floats(r.eval_batch(g, TASK_MCN, pop))}
+g = r.graph_ba(3000, 5, 7)
+pop = r.init_population(3000, 70, 150, 2)
+fit["ba_3000"] = {"pc": floats(r.eval_batch(g, TASK_PC, pop, threads=8)), "mcn": floats(r.eval_batch(g, TASK_MCN, pop[:6], threads=6))}
+
+# CDA: small graphs (edges inline) + the SURVEY KAT instance
+for trial in range(14):
+    kind = trial % 3
+    n = int(gen.integers(6, 60))
+    if kind == 0:
+        g = r.graph_er(n, float(gen.uniform(0.05, 0.35)), 100 + trial)
+    elif kind == 1:
+        g = r.graph_ba(n, int(gen.integers(1, 4)), 100 + trial)
+    else:
+        g = r.graph_sbm(int(gen.integers(2, 5)), int(gen.integers(4, 14)), 0.5, 0.04, 100 + trial)
+    m = r.graph_m(g)
+    if m == 0:
+        continue
+    k = int(gen.integers(0, m + 1))
+    batch = gen.integers(0, m, (3, k)).astype(np.int32)
+    fit["cda"].append({"n": r.graph_n(g), "edges": ints(r.graph_edges(g)), "genes": ints(batch),
+                       "q": floats(r.eval_batch(g, TASK_CDA, batch)), "q0": r.modularity_unattacked(g),
+                       "communities": ints(r.detect_communities(g))})
+g = r.graph_sbm(10, 50, 0.2, 0.01, 1)
+k = r.budget(g, 0, 0.05)
+pop = r.init_population(r.graph_m(g), 3, k, 1)
+fit["cda_kat"] = {"k": k, "q": floats(r.eval_batch(g, TASK_CDA, pop)), "q0": r.modularity_unattacked(g)}
+kar = r.graph_load("/root/reference/proj/data/karate.txt")
+fit["karate"] = {"n": r.graph_n(kar), "edges": ints(r.graph_edges(kar)), "q0": r.modularity_unattacked(kar),
+                 "communities": ints(r.detect_communities(kar))}
+pop = r.init_population(r.graph_m(kar), 5, 8, 11)
+fit["karate"]["genes"] = ints(pop)
+fit["karate"]["q"] = floats(r.eval_batch(kar, TASK_CDA, pop))
+
+# LPA
+for trial, (gname, g) in enumerate([("er", r.graph_er(120, 0.08, 2)), ("ba", r.graph_ba(150, 3, 4)),
+                                    ("sbm", r.graph_sbm(4, 16, 0.28, 0.02, 671))]):
+    frac, sseed = [0.2, 0.1, 0.1][trial], [5, 6, 672][trial]
+    sp = r.split_build(g, frac, sseed)
+    test, probe = r.split_pairs(sp)
+    train = r.split_train(sp)
+    mt = r.graph_m(train)
+    k = r.budget(train, 0, 0.1)
+    batch = r.init_population(mt, 4, k, 3)
+    fit["lpa"].append({"n": r.graph_n(g), "edges": ints(r.graph_edges(g)), "fraction": frac, "split_seed": sseed,
+                       "test": ints(test), "probe": ints(probe), "train_sha": sha(r.graph_edges(train)), "genes": ints(batch),
+                       "auc": floats(r.eval_batch(sp, TASK_LPA, batch)), "auc0": r.auc_unattacked(sp),
+                       "ra_first_test": [r.ra_score(train, int(u), int(v)) for u, v in test[:5]]})
+g = r.graph_er(500, 0.03, 1)
+sp = r.split_build(g, 0.1, 1)
+train = r.split_train(sp)
+k = r.budget(train, 0, 0.1)
+pop = r.init_population(r.graph_m(train), 3, k, 1)
+fit["lpa_kat"] = {"T": len(r.split_pairs(sp)[0]), "train_m": r.graph_m(train), "k": k,
+                  "auc": floats(r.eval_batch(sp, TASK_LPA, pop)), "auc0": r.auc_unattacked(sp)}
+dump("fitness.json", fit)
+
+# ------------------------------------------------------------------ trajectories
+runs = {}
+
+
+def run_case(name, ctx, task, pc, pm, s, k, iters, seed, eda=0, modes=((MODE_S, 1, 1),)):
+    base = r.run_ga(ctx, task, pc, pm, s, k, iters, seed, eda, MODE_SERIAL)
+    for mode, pn, qn in modes:  # every topology reproduces the serial run bit for bit
+        other = r.run_ga(ctx, task, pc, pm, s, k, iters, seed, eda, mode, pn, qn)
+        assert np.array_equal(base["best"], other["best"]) and np.array_equal(base["mean"], other["mean"])
+        assert np.array_equal(base["population"], other["population"])
+    runs[name] = {"task": task, "pc": pc, "pm": pm, "pop_size": s, "budget": k, "iterations": iters, "seed": seed,
+                  "eda_interval": eda, "best": floats(base["best"]), "mean": floats(base["mean"]),
+                  "final_fitness": floats(base["fitness"]), "final_population_sha": sha(base["population"]),
+                  "best_individual": ints(base["population"][0])}
+
+
+run_case("config1_pc_ba1000", r.graph_ba(1000, 2, 1), TASK_PC, 0.6, 0.2, 100, 50, 100, 1, modes=((MODE_S, 1, 1), (MODE_M, 8, 1)))
+run_case("acceptance6_sixdst_er100", r.graph_er(100, 0.04, 665), TASK_MCN, 0.5, 0.3, 20, 10, 50, 20240601, modes=((MODE_S, 1, 1), (MODE_M, 2, 1)))
+run_case("pc_er100_eda3", r.graph_er(100, 0.04, 665), TASK_PC, 0.8, 0.1, 30, 8, 25, 4, eda=3)
+g = r.graph_sbm(4, 16, 0.28, 0.02, 671)
+sp = r.split_build(g, 0.1, 672)
+k = r.budget(r.split_train(sp), 0, 0.1)
+run_case("acceptance10_lpa_sbm64", sp, TASK_LPA, 0.7, 0.1, 50, k, 200, 673)
+runs["acceptance10_lpa_sbm64"]["auc0"] = r.auc_unattacked(sp)
+run_case("cda_sbm80", r.graph_sbm(4, 20, 0.3, 0.03, 1), TASK_CDA, 0.8, 0.1, 16, 10, 12, 2)
+run_case("cda_karate", kar, TASK_CDA, 0.8, 0.1, 20, 4, 30, 7)
+dump("runs.json", runs)
+print("acceptance #6 final MCN", runs["acceptance6_sixdst_er100"]["best"][-1], "(reference test_output.txt:50 says 81)")
+print("acceptance #10 AUC", runs["acceptance10_lpa_sbm64"]["auc0"], "->", runs["acceptance10_lpa_sbm64"]["best"][-1])
+print("config 1 best", runs["config1_pc_ba1000"]["best"][0], "->", runs["config1_pc_ba1000"]["best"][-1])

@@ -1,0 +1,32 @@
+"""CPU: the C oracle against the golden vectors produced by the unmodified reference.
+This is what pins the oracle; it runs everywhere, no reference needed."""
+import pytest
+
+import golden_cases as gc
+
+
+@pytest.fixture(scope="module")
+def impl(oracle):
+    return gc.OracleImpl(oracle)
+
+
+@pytest.mark.parametrize("check", [gc.check_rng_and_init, gc.check_selection, gc.check_variation,
+                                   gc.check_elitism_eda_partition, gc.check_generators, gc.check_pc_mcn, gc.check_cda,
+                                   gc.check_lpa], ids=lambda f: f.__name__)
+def test_oracle_matches_golden(impl, check):
+    check(impl)
+
+
+@pytest.mark.parametrize("name", gc.RUN_NAMES)
+def test_oracle_trajectories_match_golden(impl, name):
+    gc.check_run(impl, name)
+
+
+def test_recorded_reference_values(oracle):
+    """Values the reference's own test run recorded (proj/test_output.txt:50-54)."""
+    runs = gc.load("runs.json")
+    assert runs["acceptance6_sixdst_er100"]["best"][-1] == 81.0                      # criterion 6: final MCN 81
+    assert f'{runs["acceptance10_lpa_sbm64"]["auc0"]:.6f}' == "0.728395"           # criterion 10
+    assert f'{runs["acceptance10_lpa_sbm64"]["best"][-1]:.6f}' == "0.388889"
+    assert f'{gc.load("fitness.json")["karate"]["q0"]:.6f}' == "0.380671"          # criterion 8: unattacked Q
+    assert oracle.mix64(0) == 0xE220A8397B1DCDAF and oracle.mix64(1) == 0x910A2DEC89025CC1

@@ -1,0 +1,122 @@
+"""CPU: the C oracle against the compiled, unmodified reference (oracle/_ref) on wider random
+sweeps than the golden files hold.  Skipped where the reference binary is not available."""
+import numpy as np
+import pytest
+
+from oracle.bindings import MODE_M, MODE_S, TASK_CDA, TASK_LPA, TASK_MCN, TASK_PC
+
+
+def _rand_edges(rng, n, dens):
+    iu = np.triu_indices(n, 1)
+    keep = rng.random(len(iu[0])) < dens
+    return np.stack([iu[0][keep], iu[1][keep]], 1).astype(np.int32)
+
+
+def test_rng_streams(oracle, ref):
+    rng = np.random.default_rng(1)
+    for _ in range(50):
+        seed, gen, row = (int(x) for x in rng.integers(0, 2**62, 3))
+        role = int(rng.integers(1, 6))
+        assert np.array_equal(oracle.stream_u64(seed, gen, role, row, 16), ref.stream_u64(seed, gen, role, row, 16))
+        assert np.array_equal(oracle.stream_unit(seed, gen, role, row, 16), ref.stream_unit(seed, gen, role, row, 16))
+        b = int(rng.integers(1, 2**32 - 1))
+        assert np.array_equal(oracle.stream_index(seed, gen, role, row, b, 16), ref.stream_index(seed, gen, role, row, b, 16))
+
+
+def test_generators_and_pools(oracle, ref):
+    for og, rg in [(oracle.graph_ba(700, 3, 5), ref.graph_ba(700, 3, 5)), (oracle.graph_ba(50, 1, 2), ref.graph_ba(50, 1, 2)),
+                   (oracle.graph_er(300, 0.05, 9), ref.graph_er(300, 0.05, 9)),
+                   (oracle.graph_sbm(5, 40, 0.3, 0.02, 4), ref.graph_sbm(5, 40, 0.3, 0.02, 4))]:
+        assert np.array_equal(og.edges, ref.graph_edges(rg))
+        u, v = ref.pool_genes(rg, 0)  # EdgeRemoval pool order == oracle edge ranks
+        assert np.array_equal(u, og.pool_u) and np.array_equal(v, og.pool_v)
+        for rate in (0.05, 0.1, 1.0, 0.0001):
+            assert oracle.budget(og.m, rate) == ref.budget(rg, 0, rate)
+            assert oracle.budget(og.n, rate) == ref.budget(rg, 2, rate)
+
+
+def test_pc_mcn_500_pairs(oracle, ref):
+    """acceptance.cpp:83-105 — 500 (graph, individual) pairs, exact."""
+    rng = np.random.default_rng(3)
+    for _ in range(100):
+        n = int(rng.integers(4, 80))
+        e = _rand_edges(rng, n, float(rng.uniform(0.01, 0.4)))
+        og, rg = oracle.graph_from_edges(n, e), ref.graph_from_edges(n, e)
+        batch = rng.integers(0, n, (5, int(rng.integers(0, n + 1)))).astype(np.int32)
+        for task in (TASK_PC, TASK_MCN):
+            assert np.array_equal(oracle.eval_batch(og, task, batch), ref.eval_batch(rg, task, batch))
+
+
+def test_cda_random(oracle, ref):
+    rng = np.random.default_rng(4)
+    for trial in range(30):
+        n = int(rng.integers(5, 90))
+        e = _rand_edges(rng, n, float(rng.uniform(0.03, 0.3)))
+        if len(e) == 0:
+            continue
+        og, rg = oracle.graph_from_edges(n, e), ref.graph_from_edges(n, e)
+        assert np.array_equal(oracle.detect_communities(og), ref.detect_communities(rg))
+        batch = rng.integers(0, len(e), (3, int(rng.integers(0, len(e) + 1)))).astype(np.int32)
+        assert np.array_equal(oracle.eval_batch(og, TASK_CDA, batch), ref.eval_batch(rg, TASK_CDA, batch))
+
+
+def test_cda_sbm_1000(oracle, ref):
+    og, rg = oracle.graph_sbm(10, 100, 0.1, 0.005, 1), ref.graph_sbm(10, 100, 0.1, 0.005, 1)
+    k = oracle.budget(og.m, 0.05)
+    pop = oracle.init_population(og.m, 2, k, 1)
+    assert np.array_equal(oracle.eval_batch(og, TASK_CDA, pop), ref.eval_batch(rg, TASK_CDA, pop, threads=2))
+
+
+def test_lpa_random(oracle, ref):
+    rng = np.random.default_rng(5)
+    for trial in range(15):
+        n = int(rng.integers(30, 250))
+        og, rg = oracle.graph_er(n, 0.1, trial), ref.graph_er(n, 0.1, trial)
+        frac = float(rng.uniform(0.05, 0.5))
+        so, sr = oracle.split_build(og, frac, trial + 7), ref.split_build(rg, frac, trial + 7)
+        t, p = ref.split_pairs(sr)
+        assert np.array_equal(so.test, t) and np.array_equal(so.probe, p)
+        assert np.array_equal(so.train.edges, ref.graph_edges(ref.split_train(sr)))
+        batch = rng.integers(0, so.train.m, (4, int(rng.integers(0, so.train.m)))).astype(np.int32)
+        assert np.array_equal(oracle.eval_batch(so, TASK_LPA, batch), ref.eval_batch(sr, TASK_LPA, batch))
+        u, v = (int(x) for x in so.test[0])
+        assert oracle.ra_score(so.train, u, v) == ref.ra_score(ref.split_train(sr), u, v)
+
+
+def test_operators_random(oracle, ref):
+    rng = np.random.default_rng(6)
+    for trial in range(40):
+        s, k, pool = int(rng.integers(2, 120)), int(rng.integers(1, 40)), int(rng.integers(1, 5000))
+        seed, gen = int(rng.integers(0, 2**40)), int(rng.integers(0, 500))
+        pop = rng.integers(0, pool, (s, k)).astype(np.int32)
+        f = rng.integers(0, 8, s).astype(float) if trial % 2 else rng.random(s)
+        minimize = bool(trial % 3)
+        assert np.array_equal(oracle.selection_weights(f, minimize), ref.selection_weights(f, minimize))
+        idx, partners = ref.roulette_select(pop, f, minimize, seed, gen)
+        assert np.array_equal(oracle.roulette_pick(f, minimize, seed, gen), idx)
+        pc, pm = float(rng.random()), float(rng.random())
+        crossed = ref.crossover(pop, partners, pc, seed, gen)
+        assert np.array_equal(oracle.crossover(pop, idx, pc, seed, gen), crossed)
+        assert np.array_equal(oracle.mutate_block(crossed, 0, pm, pool, seed, gen), ref.mutate(crossed, pm, pool, seed, gen))
+        mp = rng.integers(0, pool, (s, k)).astype(np.int32)
+        fm = rng.integers(0, 8, s).astype(float)
+        a, b = oracle.elitism(pop, mp, f, fm, minimize)
+        c, d = ref.elitism(pop, mp, f, fm, minimize)
+        assert np.array_equal(a, c) and np.array_equal(b, d)
+        ec = int(rng.integers(1, s + 1))
+        assert np.array_equal(oracle.eda_sample(pop, ec, pool, seed, gen, trial % 2 == 0),
+                              ref.eda_sample(pop, ec, pool, seed, gen, trial % 2 == 0))
+    with pytest.raises(ValueError):
+        oracle.elitism(pop, mp, [float("nan")] * s, fm, True)
+    with pytest.raises(ValueError):
+        ref.elitism(pop, mp, [float("nan")] * s, fm, True)
+
+
+def test_trajectories_all_modes(oracle, ref):
+    """test_parallel.cpp:86-116: the oracle loop equals the reference in serial, S and M modes."""
+    og, rg = oracle.graph_ba(300, 2, 8), ref.graph_ba(300, 2, 8)
+    want = oracle.run_ga(og, TASK_PC, 0.6, 0.2, 24, 15, 20, 77, eda_interval=4)
+    for mode, pn in [(MODE_S, 1), (MODE_M, 3)]:
+        got = ref.run_ga(rg, TASK_PC, 0.6, 0.2, 24, 15, 20, 77, eda_interval=4, mode=mode, pn=pn)
+        for key in ("best", "mean", "population", "fitness"):
+            assert np.array_equal(want[key], got[key]), (mode, key)
