@@ -1,0 +1,342 @@
+#!/usr/bin/env python
+"""bench.py — the driver's measurement contract for the GAPA hot path on B200.
+
+    python bench.py --gpus N --steps K --warmup W [--impl reference] [--workload c4|c1|...]
+
+A *step* is one generation of the hot path over the whole population:
+select -> crossover+mutate -> batched fitness evaluation of M_POP -> elitism
+(modes.cpp:159-175), population resident in HBM.  `value` = fitness evaluations per second
+of the whole job (all ranks), device-timed with CUDA events on the stream the kernels run
+on, max over ranks.  `e2e` = the same metric through the reference-facing plugin call
+FitnessFunction::evaluate_batch with HOST buffers (pinned H2D of the gene matrix + kernels
++ D2H of the fitness vector inside the timed region).
+
+Default workload = BASELINE.json configs[3] ("C4"): critical-node detection, pairwise-
+connectivity fitness, Barabasi-Albert n = 1,000,000 attach 5 (m = 4,999,985), budget
+k = 50,000, population 4096 — the configuration north_star's roofline target is quoted on
+and the largest that the metric names; it fits one GPU.  With N > 1 the population is
+sharded over ranks (strong scaling: total population fixed) and the only exchange is one
+NCCL all-gather of fitness doubles per generation.
+
+`--impl reference` times the reference's CPU path for the same config on the host cores:
+the unmodified reference (oracle/_ref) where its dense n x n storage can hold the graph
+(n <= 20,000), else the CSR port of the same algorithm (oracle/), on a bounded sample.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+WORKLOADS = {
+    # name: (task, graph kind, graph args, pool kind, rate, pop, pc, pm, description)
+    "c4": dict(task="pc", graph=("ba", 1_000_000, 5, 1), rate=0.05, pop=4096, pc=0.6, pm=0.2,
+               name="C4: CND pairwise-connectivity GA, Barabasi-Albert n=1e6 attach=5 (m=4,999,985), k=50,000, pop 4096"),
+    "c1": dict(task="pc", graph=("ba", 1000, 2, 1), rate=0.05, pop=100, pc=0.6, pm=0.2,
+               name="C1: CND pairwise-connectivity GA, Barabasi-Albert n=1000 attach=2 (m=1997), k=50, pop 100"),
+    "c2": dict(task="cda", graph=("sbm", 10, 500, 0.02, 0.0005, 1), rate=0.05, pop=100, pc=0.8, pm=0.1,
+               name="C2: CDA modularity GA, SBM 10x500 (m=30,321), 5% edge deletion k=1517, pop 100"),
+    "c3": dict(task="lpa", graph=("er", 10_000, 10 / 9999, 1), rate=0.1, pop=50, pc=0.7, pm=0.1,
+               name="C3: LPA RA-AUC GA, Erdos-Renyi n=1e4 <d>=10 (m=50,277), 10% hidden, k=4525, pop 50"),
+    "n1e5": dict(task="pc", graph=("ba", 100_000, 5, 1), rate=0.05, pop=4096, pc=0.6, pm=0.2,
+                 name="C5 point: CND-PC, BA n=1e5 attach=5, k=5000, pop 4096"),
+}
+TASK_ID = {"pc": 0, "mcn": 1, "cda": 2, "lpa": 3}
+
+
+def algorithmic_bytes(task: str, n: int, m: int, k: int, T: int = 0, P: int = 0, dbar: float = 0.0) -> float:
+    """algorithmic bytes per evaluation (int32 indices, FP64 outputs)."""
+    if task in ("pc", "mcn"):
+        return 4 * (n + 1) + 8 * m + 4 * k + 2 * ((n + 7) // 8) + 8 * n + 8
+    if task == "lpa":
+        return 4 * k + 2 * ((m + 7) // 8) + 8 * n + (T + P) * (16 + 2 * 8 * dbar) + 8 * (T + P) + 8
+    return 4 * (n + 1) + 8 * m + 4 * m + 4 * k + 2 * ((m + 7) // 8) + 16 * m + 8 * n + 8  # cda
+
+
+def peaks() -> tuple[float, str]:
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return float(json.load(f)["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons DURING the timed region (B200_PROFILING.md recipe)."""
+
+    def __init__(self, index: int):
+        self.rows, self.proc, self.index = [], None, index
+
+    def start(self):
+        q = ("clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.hw_slowdown,"
+             "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown,"
+             "clocks_event_reasons.sw_power_cap")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", f"--id={self.index}", f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            threading.Thread(target=self._read, daemon=True).start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.rows.append([c.strip() for c in line.split(",")])
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        time.sleep(0.15)
+        self.proc.terminate()
+        sm = [float(r[0]) for r in self.rows if len(r) >= 7 and r[0].replace(".", "").isdigit()]
+        mx = [float(r[1]) for r in self.rows if len(r) >= 7 and r[1].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in self.rows if len(r) >= 7 for i in range(4) if r[3 + i].lower().startswith("active")})
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": reasons, "samples": len(sm)}
+
+
+def host_threads() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except Exception:
+        return os.cpu_count() or 1
+
+
+# --------------------------------------------------------------------------------- CPU arms
+def cpu_reference_throughput(w: dict, target_seconds: float, threads: int) -> dict:
+    """evals/s of the reference CPU path on a bounded sample of workload `w` (the checker is the
+    thing timed here, and only here)."""
+    from oracle.bindings import Oracle, Ref
+    o = Oracle()
+    kind, *args = w["graph"]
+    task = TASK_ID[w["task"]]
+    use_ref = Ref.available() and args[0] * (args[1] if kind == "sbm" else 1) <= 20_000
+    if use_ref:
+        r = Ref()
+        g = getattr(r, "graph_" + kind)(*args)
+        if task == 3:
+            ctx = r.split_build(g, 0.1, 1)
+            basis = r.graph_m(r.split_train(ctx))
+        else:
+            ctx, basis = g, (r.graph_n(g) if task in (0, 1) else r.graph_m(g))
+        impl, label = r, "reference"
+    else:
+        g = getattr(o, "graph_" + kind)(*args)
+        if task == 3:
+            ctx = o.split_build(g, 0.1, 1)
+            basis = ctx.train.m
+        else:
+            ctx, basis = g, (g.n if task in (0, 1) else g.m)
+        impl, label = o, "port"
+    k = o.budget(basis, w["rate"])
+    rows = max(threads, 1)
+    total_rows, total_t = 0, 0.0
+    while True:
+        batch = o.init_population(basis, rows, k, 1)
+        t0 = time.perf_counter()
+        impl.eval_batch(ctx, task, batch, threads=threads)
+        dt = time.perf_counter() - t0
+        total_rows, total_t = rows, dt
+        if dt >= target_seconds / 3 or rows >= w["pop"] * 4:
+            break
+        rows = int(min(w["pop"] * 4, max(rows * 2, rows * (target_seconds / 2) / max(dt, 1e-3))))
+    return {"value": total_rows / total_t, "unit": "evals/s", "cores": threads, "kind": label,
+            "sample": f"{total_rows} individuals of the workload evaluated once on {threads} host threads "
+                      f"({'unmodified reference, dense BitMatrix' if use_ref else 'CSR port of the reference algorithm; the reference itself needs n^2/8 bytes per individual'}) in {total_t:.2f} s"}
+
+
+def run_reference_arm(args, w):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    threads = host_threads()
+    steps = max(args.steps, 1)
+    per_step = min(60.0, 150.0 / (steps + args.warmup))
+    vals = []
+    base = None
+    for i in range(args.warmup + steps):
+        base = cpu_reference_throughput(w, per_step, threads)
+        if i >= args.warmup:
+            vals.append(base["value"])
+    value = float(np.mean(vals))
+    base["value"] = value
+    line = {"impl": "reference", "metric": "fitness_evals_per_sec", "value": value, "unit": "evals/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * w["pop"] / value, "higher_is_better": True,
+            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "config": {"workload": w["name"], "population": w["pop"]},
+            "cpu_baseline": base,
+            "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# --------------------------------------------------------------------------------- GPU arm
+def run_gpu_arm(args, w):
+    import torch
+    import torch.distributed as dist
+    import paper_2412_20980_b200 as gp
+    from paper_2412_20980_b200.driver import CudaOps, Shard, ShardedGa, torch_allgather
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if not torch.cuda.is_available():
+        raise SystemExit("bench.py: no CUDA device — the hot path has no CPU fallback")
+    torch.cuda.set_device(local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+
+    kind, *gargs = w["graph"]
+    graph = {"ba": gp.barabasi_albert, "er": gp.erdos_renyi, "sbm": gp.planted_partition}[kind](*gargs)
+    task = w["task"]
+    T = P = 0
+    if task == "lpa":
+        split = gp.build_lp_split(graph, 0.1, 1)
+        pool = gp.build_gene_pool(split.train, gp.PoolKind.EdgeRemoval)
+        obj = gp.LinkPredictionAttackObjective(split, pool, device=local)
+        base_graph, T, P = split.train, len(split.test_edges), len(split.probe_nonedges)
+    elif task == "cda":
+        pool = gp.build_gene_pool(graph, gp.PoolKind.EdgeRemoval)
+        obj = gp.ModularityAttackObjective(graph, pool, device=local)
+        base_graph = graph
+    else:
+        pool = gp.build_gene_pool(graph, gp.PoolKind.NodeRemoval)
+        obj = (gp.PairwiseConnectivityObjective if task == "pc" else gp.SixDstObjective)(graph, pool, device=local)
+        base_graph = graph
+    n, m = base_graph.node_count(), base_graph.edge_count()
+    k = gp.perturbation_budget(base_graph, pool.kind(), w["rate"])
+    s = args.pop or w["pop"]
+    params = gp.GAParams(pc=w["pc"], pm=w["pm"], pop_size=s, budget=k, iterations=args.warmup + args.steps + 1, seed=1)
+    shard = Shard(rank, world, s)
+    ga = ShardedGa(params, CudaOps(obj, local), shard, torch_allgather())
+    lib = gp.capi.load()
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+            torch.cuda.synchronize()
+
+    ga.initialize()
+    for _ in range(args.warmup):
+        ga.step()
+    barrier()
+    sampler = ClockSampler(local)
+    if rank == 0:
+        sampler.start()
+    launches0 = lib.gapa_cuda_launch_count()
+    eval_ms = []
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    ev0.record()
+    for _ in range(args.steps):
+        ga.step()
+        eval_ms.append(obj.dgraph.last_eval_ms())
+    ev1.record()
+    barrier()
+    step_ms_total = ev0.elapsed_time(ev1)
+    launches = lib.gapa_cuda_launch_count() - launches0
+    clocks = sampler.stop() if rank == 0 else None
+
+    # e2e: the plugin boundary with HOST buffers — evaluate_batch(host genes) -> host fitness,
+    # this rank's block of the current M_POP, pinned memory, copies inside the timed region.
+    lo, hi = shard.rows
+    host_genes = torch.empty((hi - lo, k), dtype=torch.int32, pin_memory=True)
+    host_genes.copy_(ga.mutated[lo:hi])
+    host_out = torch.empty(max(hi - lo, 1), dtype=torch.float64, pin_memory=True)
+    torch.cuda.synchronize()
+
+    def e2e_once():
+        gp.capi.check(lib.gapa_cuda_eval_batch(obj.dgraph.handle, obj.task, host_genes.data_ptr(), hi - lo, k,
+                                               host_out.data_ptr()))
+
+    for _ in range(min(args.warmup, 3)):
+        e2e_once()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_once()
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    assert np.array_equal(host_out[:hi - lo].numpy(), ga.fit_m[lo:hi].cpu().numpy()), "e2e result differs from the device path"
+
+    times = torch.tensor([step_ms_total, e2e_s * 1e3, float(np.mean(eval_ms))], dtype=torch.float64, device="cuda")
+    if world > 1:
+        dist.all_reduce(times, op=dist.ReduceOp.MAX)
+    step_ms_total, e2e_ms_total, eval_ms_mean = (float(x) for x in times.cpu())
+
+    if rank == 0:
+        ms_per_step = step_ms_total / args.steps
+        value = s * args.steps / (step_ms_total * 1e-3)
+        e2e_value = s * args.steps / (e2e_ms_total * 1e-3)
+        dbar = 2.0 * m / max(n, 1)
+        b_eval = algorithmic_bytes(task, n, m, k, T, P, dbar)
+        peak, peak_src = peaks()
+        rows_per_rank = shard.block
+        achieved = b_eval * rows_per_rank / (eval_ms_mean * 1e-3) / 1e9
+        traffic = None
+        try:
+            with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as f:
+                traffic = json.load(f).get(args.workload)
+        except Exception:
+            pass
+        line = {
+            "metric": "fitness_evals_per_sec", "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int64" if task in ("pc", "mcn") else "f64", "data": "synthetic",
+            "config": {"workload": w["name"], "population": s, "budget": k, "n": n, "m": m,
+                       "step": "one generation: select -> crossover+mutate -> evaluate(M_POP) -> elitism, population in HBM",
+                       "parallelism": f"population rows sharded over {world} GPU(s), graph replicated, 1 fitness all-gather/generation",
+                       "l2": "inputs larger than L2 (gene matrix %.0f MB + alive/reached words %.0f MB per step vs 126 MB L2)"
+                             % (4.0 * s * k / 1e6, 16.0 * n * ((rows_per_rank + 63) // 64) / 1e6)},
+            "generations_per_sec": 1e3 / ms_per_step,
+            "fitness_eval_ms_per_step": eval_ms_mean,
+            "fitness_evals_per_sec_kernels_only": rows_per_rank * world / (eval_ms_mean * 1e-3),
+            "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(4 * (hi - lo) * k) * world,
+                    "d2h_bytes_per_step": int(8 * (hi - lo)) * world,
+                    "path": "gapa_cuda_eval_batch(host genes) -> host fitness (FitnessFunction::evaluate_batch boundary)"},
+            "gpu_launches": int(launches),
+            "clocks": clocks,
+            "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
+                         "traffic": traffic, "peak_source": peak_src,
+                         "kernel": "fitness evaluation pipeline (k_pc_sweep dominant)" if task in ("pc", "mcn") else f"{task} fitness pipeline",
+                         "algorithmic_bytes_per_eval": b_eval,
+                         "note": "achieved = SURVEY §8(d) bytes/eval x evals per batch / device time of the whole evaluation "
+                                 "(CUDA events on the launch stream). frac > 1 is possible by construction: 64 individuals share "
+                                 "one pass over the CSR (bit-sliced), while §8(d) charges every individual its own pass."},
+        }
+        if world == 1 and not args.no_cpu_baseline:
+            line["cpu_baseline"] = cpu_reference_throughput(w, 12.0, host_threads())
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
+    ap.add_argument("--pop", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    w = WORKLOADS[args.workload]
+    if args.impl == "reference":
+        run_reference_arm(args, w)
+    else:
+        run_gpu_arm(args, w)
+
+
+if __name__ == "__main__":
+    main()

@@ -132,6 +132,11 @@ int gapa_cuda_ga_elitism_device(const int32_t* pop_dev, const int32_t* m_pop_dev
                                 const double* fit_dev, const double* fit_m_dev, int minimize,
                                 int32_t* next_dev, double* next_fit_dev, void* stream);
 
+/* record_generation (modes.cpp:35-43): best_dev[0] = fit[0], mean_dev[0] = sequential
+ * sum(fit) / s — the reference's std::accumulate order, so non-integer fitness means
+ * are bit-identical. */
+int gapa_cuda_ga_stats_device(const double* fit_dev, int s, double* best_dev, double* mean_dev, void* stream);
+
 /* Host-buffer forms of the same operators (H2D, kernel, D2H, synchronous) — the
  * exact shapes of the reference free functions, used by the host adapters and
  * the parity tests.  `device` selects the GPU. */

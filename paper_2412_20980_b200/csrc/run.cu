@@ -72,6 +72,12 @@ int eval_rows(gapa_cuda_ctx* ctx, int task, const int32_t* genes, int rows, int 
 }
 }  // namespace
 
+extern "C" int gapa_cuda_ga_stats_device(const double* fit_dev, int s, double* best_dev, double* mean_dev, void* stream) {
+    if (s < 1 || !fit_dev || !best_dev || !mean_dev) return fail(GAPA_CUDA_E_INVALID, "stats: bad arguments");
+    GAPA_LAUNCH(k_ga_stats, 1, 1, 0, static_cast<cudaStream_t>(stream), fit_dev, s, best_dev, mean_dev);
+    return GAPA_CUDA_OK;
+}
+
 extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, gapa_cuda_allgather_fn exchange,
                              void* exchange_user, gapa_cuda_run_result* result) {
     if (!ctx || !p || !result) return fail(GAPA_CUDA_E_INVALID, "run: null argument");

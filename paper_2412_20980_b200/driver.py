@@ -1,0 +1,201 @@
+"""Sharded generation loop: one process per GPU, population rows partitioned across ranks.
+
+Shape of the reference's M mode (modes.cpp:190-349) mapped onto GPUs:
+
+  * the graph (CSR), pool and split are replicated on every GPU;
+  * every rank keeps the WHOLE population in its HBM and runs select / crossover+mutate /
+    elitism redundantly — the operators are keyed by (seed, generation, role, global row)
+    (rng.hpp:49-65), so every rank produces bit-identical matrices and genomes never
+    cross NVLink;
+  * rank r evaluates only rows partition_rows(s, world)[r] (modes.cpp:506-516);
+  * ONE all-gather of fitness doubles per evaluation is the only exchange (block padded to
+    ceil(s/world) so counts are equal), issued through torch.distributed (NCCL over
+    NVLink/NVSwitch on GPUs).
+
+`ShardedGa` holds the loop and the sharding arithmetic; the compute is delegated to an
+`ops` object.  The product's ops is `CudaOps` (C ABI, device pointers, torch tensors only as
+device-memory owners).  Tests inject a CPU ops object to exercise the N>1 host logic under
+gloo without a GPU — the product never does.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import capi
+from .api import Direction, FitnessFunction, GAParams, RunResult, partition_rows
+from .capi import GapaCudaError, check
+
+
+@dataclass
+class Shard:
+    rank: int
+    world: int
+    pop_size: int
+
+    @property
+    def block(self) -> int:  # ceil(s / world), modes.cpp:507
+        return (self.pop_size + self.world - 1) // self.world
+
+    @property
+    def rows(self) -> tuple[int, int]:
+        return partition_rows(self.pop_size, self.world)[self.rank]
+
+    @property
+    def padded(self) -> int:
+        return self.block * self.world
+
+
+class CudaOps:
+    """Device ops over torch-owned HBM buffers, on torch's current stream."""
+
+    def __init__(self, fitness: FitnessFunction, device_index: int):
+        import torch
+        self.torch = torch
+        self.lib = capi.load()
+        self.fitness = fitness
+        self.device = torch.device("cuda", device_index)
+        self.pool_size = fitness.pool.size()
+
+    def _stream(self) -> int:
+        return self.torch.cuda.current_stream(self.device).cuda_stream
+
+    def empty_genes(self, rows, cols):
+        return self.torch.empty((rows, max(cols, 0)), dtype=self.torch.int32, device=self.device)
+
+    def zeros_f64(self, count):
+        return self.torch.zeros(count, dtype=self.torch.float64, device=self.device)
+
+    def empty_i32(self, count):
+        return self.torch.empty(count, dtype=self.torch.int32, device=self.device)
+
+    def init(self, out, seed, generation):
+        s, k = out.shape
+        check(self.lib.gapa_cuda_ga_init_device(self.pool_size, 0, s, k, seed, generation, out.data_ptr(), self._stream()))
+
+    def select(self, fit, s, minimize, seed, generation, partner):
+        check(self.lib.gapa_cuda_ga_select_device(fit.data_ptr(), s, minimize, seed, generation, partner.data_ptr(), None,
+                                                  self._stream()))
+
+    def crossover_mutate(self, pop, partner, pc, pm, seed, generation, out):
+        s, k = pop.shape
+        check(self.lib.gapa_cuda_ga_crossover_mutate_device(pop.data_ptr(), partner.data_ptr(), s, k, 0, s, pc, pm,
+                                                            self.pool_size, seed, generation, out.data_ptr(), self._stream()))
+
+    def eda(self, pop, seed, generation, out):
+        s, k = pop.shape
+        check(self.lib.gapa_cuda_ga_eda_device(pop.data_ptr(), s, k, s, self.pool_size, seed, generation, 1, out.data_ptr(),
+                                               self._stream()))
+
+    def mutate(self, block, pm, seed, generation, out):
+        s, k = block.shape
+        check(self.lib.gapa_cuda_ga_mutate_device(block.data_ptr(), s, k, 0, pm, self.pool_size, seed, generation,
+                                                  out.data_ptr(), self._stream()))
+
+    def eval_rows(self, genes, lo, hi, fit_out):
+        """fitness of rows [lo, hi) of `genes` into fit_out[lo:hi]"""
+        if hi <= lo:
+            return
+        k = genes.shape[1]
+        self.fitness.dgraph.eval_batch_device(self.fitness.task, genes.data_ptr() + 4 * lo * k, hi - lo, k,
+                                              fit_out.data_ptr() + 8 * lo, self._stream())
+
+    def elitism(self, pop, mutated, fit, fit_m, minimize, nxt, next_fit):
+        s, k = pop.shape
+        check(self.lib.gapa_cuda_ga_elitism_device(pop.data_ptr(), mutated.data_ptr(), s, k, fit.data_ptr(), fit_m.data_ptr(),
+                                                   minimize, nxt.data_ptr(), next_fit.data_ptr(), self._stream()))
+
+    def stats(self, fit, s, hist, index, iters):
+        check(self.lib.gapa_cuda_ga_stats_device(fit.data_ptr(), s, hist.data_ptr() + 8 * index,
+                                                 hist.data_ptr() + 8 * (iters + index), self._stream()))
+
+    def to_host(self, t):
+        return t.cpu().numpy()
+
+
+def torch_allgather(group=None):
+    """In-place all-gather of the padded fitness vector over torch.distributed."""
+    import torch.distributed as dist
+
+    def gather(fit_padded, shard: Shard):
+        if shard.world == 1:
+            return
+        lo = shard.rank * shard.block
+        dist.all_gather_into_tensor(fit_padded, fit_padded[lo:lo + shard.block], group=group)
+
+    return gather
+
+
+class ShardedGa:
+    def __init__(self, params: GAParams, ops, shard: Shard, gather):
+        params.validate()
+        if params.iterations < 1:
+            raise GapaCudaError(capi.E_INVALID, "iterations must be >= 1")
+        if shard.pop_size != params.pop_size:
+            raise GapaCudaError(capi.E_INVALID, "shard does not match the population size")
+        self.p, self.ops, self.shard, self.gather = params, ops, shard, gather
+        s, k = params.pop_size, params.budget
+        self.minimize = 1 if params.direction == Direction.Minimize else 0
+        self.pop = ops.empty_genes(s, k)
+        self.mutated = ops.empty_genes(s, k)
+        self.next = ops.empty_genes(s, k)
+        self.crossed = ops.empty_genes(s, k) if params.eda_interval else None
+        self.partner = ops.empty_i32(s)
+        self.fit = ops.zeros_f64(shard.padded)
+        self.fit_m = ops.zeros_f64(shard.padded)
+        self.fit_next = ops.zeros_f64(shard.padded)
+        self.hist = ops.zeros_f64(2 * params.iterations)
+        self.generation = 0
+        self.fitness_batch_calls = 0
+
+    def _evaluate(self, genes, fit):
+        lo, hi = self.shard.rows
+        self.fitness_batch_calls += 1
+        self.ops.eval_rows(genes, lo, hi, fit)
+        self.gather(fit, self.shard)
+
+    def initialize(self):
+        """gen 1 prologue: init_population with generation key 0, then evaluate (modes.cpp:162-165)"""
+        self.ops.init(self.pop, self.p.seed, 0)
+        self._evaluate(self.pop, self.fit)
+
+    def step(self):
+        """one generation: select -> crossover -> mutate -> evaluate(M_POP) -> elitism"""
+        p, ops = self.p, self.ops
+        self.generation += 1
+        gen = self.generation
+        s = p.pop_size
+        if p.eda_interval and gen % p.eda_interval == 0:  # modes.cpp:31-33,167-168
+            ops.eda(self.pop, p.seed, gen, self.crossed)
+            ops.mutate(self.crossed, p.pm, p.seed, gen, self.mutated)
+        else:
+            ops.select(self.fit, s, self.minimize, p.seed, gen, self.partner)
+            ops.crossover_mutate(self.pop, self.partner, p.pc, p.pm, p.seed, gen, self.mutated)
+        self._evaluate(self.mutated, self.fit_m)
+        ops.elitism(self.pop, self.mutated, self.fit, self.fit_m, self.minimize, self.next, self.fit_next)
+        self.pop, self.next = self.next, self.pop
+        self.fit, self.fit_next = self.fit_next, self.fit
+        if gen <= p.iterations:
+            ops.stats(self.fit, s, self.hist, gen - 1, p.iterations)
+
+    def run(self) -> RunResult:
+        self.initialize()
+        for _ in range(self.p.iterations):
+            self.step()
+        return self.result()
+
+    def result(self) -> RunResult:
+        s, it = self.p.pop_size, self.p.iterations
+        hist = np.asarray(self.ops.to_host(self.hist))
+        pop = np.asarray(self.ops.to_host(self.pop))
+        fit = np.asarray(self.ops.to_host(self.fit))[:s]
+        return RunResult(pop, fit, pop[0].copy(), float(fit[0]), hist[:it].copy(), hist[it:2 * it].copy(),
+                         self.fitness_batch_calls)
+
+
+def run_ga_sharded(params: GAParams, fitness: FitnessFunction, rank: int = 0, world: int = 1, device_index: int = 0,
+                   group=None) -> RunResult:
+    """GPU front door for the sharded run; with world == 1 it equals api.run_ga."""
+    ops = CudaOps(fitness, device_index)
+    return ShardedGa(params, ops, Shard(rank, world, params.pop_size), torch_allgather(group)).run()
