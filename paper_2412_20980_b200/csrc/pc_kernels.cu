@@ -12,21 +12,30 @@
 //     single pass over the shared CSR serves 64 individuals and every 32-byte
 //     sector fetched for a neighbour word carries 64 individuals of state.
 //     The CSR is never copied; a perturbation is just the alive-word bit.
-//   * phase 1 (k_sweep) closes reachability from one high-degree source per
-//     individual by asynchronous bottom-up sweeps: a vertex ORs its
-//     neighbours' reached words until every individual it is alive in is
-//     covered (early exit after ~2 neighbours on power-law graphs, because
-//     rows are sorted and the oldest / highest-degree neighbours come first).
-//   * phase 2 finishes exactly, whatever phase 1 left: alive-but-unreached
-//     vertices that have an alive neighbour are compacted to (vertex, bits)
-//     entries and resolved by a lock-free union-find over compact slots, with
-//     one virtual "giant" node per individual standing for everything phase 1
-//     reached.  Isolated leftovers are singletons and need no work.
-//   * component sizes: reached count = n - (zero bits of the reached words),
-//     counted per bit position with shared-memory histograms.
+//   * mask build without global atomics: one CTA per individual sets its removed
+//     vertices in a SHARED-MEMORY bitmap (k_pc_bitmask), then a register-level
+//     64x64 bit transpose turns 64 per-individual bitmaps into per-vertex words
+//     (k_pc_transpose).  The bitmap popcount is the number of distinct removed
+//     vertices, so no per-bit counting pass over the words is ever needed.
+//   * phase 1 closes reachability from one high-degree source per individual with
+//     asynchronous bottom-up sweeps: a vertex ORs its neighbours' reached words
+//     until every individual it is alive in is covered.  Rows are ascending, so on
+//     power-law graphs the oldest / highest-degree neighbours come first and the loop
+//     exits after ~2 neighbours — PROVIDED the low-id core is already closed when the
+//     rest is swept.  k_pc_prefix therefore converges a prefix of the vertex order
+//     inside one CTA per group (in-kernel iteration, no host round trip), and the
+//     full sweeps then run over blocks in ascending vertex order with a few groups
+//     interleaved so the in-flight window per group stays small.
+//   * phase 2 finishes exactly, whatever phase 1 left: the last sweep compacts the
+//     alive-but-unreached vertices that have an alive neighbour to (vertex, bits)
+//     entries, resolved by a lock-free union-find over compact slots, with one
+//     virtual "giant" node per individual standing for everything phase 1 reached
+//     (leftovers adjacent to a reached vertex are attached to it, so correctness
+//     never depends on phase 1 having converged).  Isolated leftovers are singletons.
 // Integer arithmetic end to end; PC fits int64 and is exact in the returned
 // double for n <= 9.4e7 (PC < 2^53).
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -35,50 +44,102 @@ namespace gapa_b200 {
 typedef unsigned long long word_t;
 static constexpr int kBits = 64;
 static constexpr int kThreads = 256;
+static constexpr int kMaskThreads = 1024;
+static constexpr int kTransThreads = 128;
+static constexpr int kPrefixThreads = 1024;
 
 struct PcCounters {
     unsigned int n_entries;
     unsigned int n_slots;
     int overflow;
     int range_error;
+    int changed;  // any sweep since the last reset set a new reached bit
 };
 
 struct PcScratch {
-    DevBuf alive, reached, entry_of, zeros, flags, counters;
+    DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters;
     DevBuf left_v, left_g, left_w, left_base, parent, comp_size, pc_extra, mcn_extra;
     size_t cap_entries = 0, cap_slots = 0;
-    int sweeps_last = 0;
+    int prefix = 32768, interleave = 8;
+    bool configured = false;
 };
 
 // ---------------------------------------------------------------------------------
-// mask build
-__global__ void __launch_bounds__(kThreads) k_pc_init(word_t* __restrict__ alive, word_t* __restrict__ reached,
-                                                      int n, int groups, int rows) {
-    const size_t total = static_cast<size_t>(groups) * n;
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int g = static_cast<int>(i / n);
-        const int valid = min(kBits, rows - g * kBits);
-        alive[i] = valid >= kBits ? ~0ull : ((1ull << valid) - 1ull);
-        reached[i] = 0ull;
-    }
-}
+// mask build, step 1: apply_in_place for NodeRemoval (gene_pool.cpp:61-64) into a
+// shared-memory bitmap of one individual (one vertex chunk of it when n is large).
+// Duplicate genes are idempotent.  Bit c of 64-bit word w = vertex 64 w + c removed.
+extern __shared__ __align__(16) unsigned pc_smem_bits[];
 
-// apply_in_place for NodeRemoval (gene_pool.cpp:61-64): clear the individual's bit
-// in the removed vertex's alive word.  Duplicates are idempotent.
-__global__ void __launch_bounds__(kThreads) k_pc_remove(const int32_t* __restrict__ genes, size_t cells, int cols,
-                                                        const int32_t* __restrict__ pool_map, int pool_size, int n,
-                                                        word_t* alive, PcCounters* counters) {
-    for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < cells;
-         i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int row = static_cast<int>(i / cols);
-        const int gene = genes[i];
+__global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(const int32_t* __restrict__ genes, int cols,
+                                                             const int32_t* __restrict__ pool_map, int pool_size, int n,
+                                                             int chunk_bits, int words_per_row, word_t* __restrict__ removed,
+                                                             int* removed_count, PcCounters* counters) {
+    const int row = blockIdx.x;
+    const int v0 = blockIdx.y * chunk_bits;
+    const int v1 = min(n, v0 + chunk_bits);
+    const int words64 = (v1 - v0 + 63) >> 6;
+    for (int w = threadIdx.x; w < 2 * words64; w += kMaskThreads) pc_smem_bits[w] = 0u;
+    __syncthreads();
+    const int32_t* g = genes + static_cast<size_t>(row) * cols;
+    for (int j = threadIdx.x; j < cols; j += kMaskThreads) {
+        const int gene = g[j];
         if (gene < 0 || gene >= pool_size) {
             counters->range_error = 1;
             continue;
         }
         const int node = pool_map ? pool_map[gene] : gene;
-        atomicAnd(&alive[static_cast<size_t>(row >> 6) * n + node], ~(1ull << (row & 63)));
+        if (node >= v0 && node < v1) atomicOr(&pc_smem_bits[(node - v0) >> 5], 1u << ((node - v0) & 31));
+    }
+    __syncthreads();
+    const word_t* bits64 = reinterpret_cast<const word_t*>(pc_smem_bits);
+    word_t* out = removed + static_cast<size_t>(row) * words_per_row + (v0 >> 6);
+    int distinct = 0;
+    for (int w = threadIdx.x; w < words64; w += kMaskThreads) {
+        const word_t x = bits64[w];
+        distinct += __popcll(x);
+        out[w] = x;
+    }
+    for (int off = 16; off; off >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, off);
+    if ((threadIdx.x & 31) == 0 && distinct) atomicAdd(&removed_count[row], distinct);
+}
+
+// mask build, step 2: 64 individuals x 64 vertices bit transpose in registers.
+// a[i] bit c (individual i, vertex c)  ->  a[c] bit i; alive = ~removed.  Rows past
+// the end of the batch read as "everything removed", which zeroes their bits.
+__global__ void __launch_bounds__(kTransThreads) k_pc_transpose(const word_t* __restrict__ removed, int words_per_row,
+                                                                int n, int rows, word_t* __restrict__ alive) {
+    word_t* tile = reinterpret_cast<word_t*>(pc_smem_bits);  // kBits x (kTransThreads + 1) words, padded against bank conflicts
+    const int g = blockIdx.y;
+    const int vb0 = blockIdx.x * kTransThreads;
+    const int vb = vb0 + threadIdx.x;
+    word_t a[kBits];
+    if (vb < words_per_row) {
+#pragma unroll
+        for (int i = 0; i < kBits; ++i) {
+            const int row = g * kBits + i;
+            a[i] = row < rows ? removed[static_cast<size_t>(row) * words_per_row + vb] : ~0ull;
+        }
+        word_t m = 0x00000000FFFFFFFFull;
+#pragma unroll
+        for (int j = 32; j != 0; j >>= 1) {
+#pragma unroll
+            for (int k = 0; k < kBits; k = (k + j + 1) & ~j) {
+                const word_t t = ((a[k] >> j) ^ a[k + j]) & m;
+                a[k] ^= t << j;
+                a[k + j] ^= t;
+            }
+            m ^= m << (j >> 1);
+        }
+#pragma unroll
+        for (int c = 0; c < kBits; ++c) tile[c * (kTransThreads + 1) + threadIdx.x] = ~a[c];
+    }
+    __syncthreads();
+    // coalesced write-out: the block's tile is kTransThreads * 64 consecutive vertices
+    word_t* out = alive + static_cast<size_t>(g) * n;
+    const int v_base = vb0 * kBits;
+    for (int idx = threadIdx.x; idx < kTransThreads * kBits; idx += kTransThreads) {
+        const int v = v_base + idx;
+        if (v < n) out[v] = tile[(idx & 63) * (kTransThreads + 1) + (idx >> 6)];
     }
 }
 
@@ -104,96 +165,133 @@ __global__ void __launch_bounds__(kThreads) k_pc_source(const int32_t* __restric
 }
 
 // ---------------------------------------------------------------------------------
-// phase 1: asynchronous bottom-up reachability sweep, one thread per vertex and
-// group.  Reads of neighbours' words race benignly with writes (words only gain
-// bits; 64-bit stores are single transactions), so a sweep can use bits set
-// earlier in the same sweep and converges in far fewer passes than BFS levels.
+// phase 1.  Reads of neighbours' words race benignly with writes (words only gain
+// bits; 64-bit stores are single transactions), so a sweep can use bits set earlier
+// in the same sweep.  `limit` truncates the scan to neighbours below it (rows are
+// ascending), which is what keeps hub rows short while only a prefix is active.
+__device__ __forceinline__ word_t gather_reached(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                                                 const word_t* reached_g, int v, int limit, word_t todo) {
+    const int beg = row_ptr[v], end = row_ptr[v + 1];
+    word_t got = 0ull;
+    int e = beg;
+    for (; e + 1 < end; e += 2) {  // two neighbours per step: both loads are in flight together
+        const int u0 = col_idx[e], u1 = col_idx[e + 1];
+        if (u1 >= limit) {
+            if (u0 < limit) got |= __ldcg(&reached_g[u0]);
+            return got & todo;
+        }
+        got |= __ldcg(&reached_g[u0]) | __ldcg(&reached_g[u1]);
+        if ((got & todo) == todo) return todo;
+    }
+    if (e < end) {
+        const int u = col_idx[e];
+        if (u < limit) got |= __ldcg(&reached_g[u]);
+    }
+    return got & todo;
+}
+
+// Closes the first `prefix` vertices of every group inside one CTA: iterate ascending
+// passes until nothing changes.  With one CTA the in-flight window is 1024 vertices,
+// so a pass propagates almost like a sequential scan.
+__global__ void __launch_bounds__(kPrefixThreads) k_pc_prefix(const int32_t* __restrict__ row_ptr,
+                                                              const int32_t* __restrict__ col_idx, int n, int prefix,
+                                                              const word_t* __restrict__ alive, word_t* reached) {
+    const size_t base = static_cast<size_t>(blockIdx.x) * n;
+    const word_t* alive_g = alive + base;
+    word_t* reached_g = reached + base;
+    const int stages[2] = {min(prefix, 2 * kPrefixThreads), prefix};
+    for (int s = 0; s < 2; ++s) {
+        const int limit = stages[s];
+        if (s == 1 && limit == stages[0]) break;
+        for (int pass = 0; pass < 24; ++pass) {
+            int any = 0;
+            for (int v = threadIdx.x; v < limit; v += kPrefixThreads) {
+                const word_t mine = reached_g[v];
+                const word_t todo = alive_g[v] & ~mine;
+                if (!todo) continue;
+                const word_t got = gather_reached(row_ptr, col_idx, reached_g, v, limit, todo);
+                if (got) {
+                    reached_g[v] = mine | got;
+                    any = 1;
+                }
+            }
+            if (!__syncthreads_or(any)) break;
+        }
+    }
+}
+
+// Full sweep, one thread per (vertex, group); `interleave` groups share blockIdx.x so
+// that blocks are scheduled in ascending vertex order with a small window per group.
+// FINAL additionally records what is still unreached: per-individual counts and the
+// compacted non-isolated leftovers for phase 2.
+template <bool FINAL>
 __global__ void __launch_bounds__(kThreads) k_pc_sweep(const int32_t* __restrict__ row_ptr,
-                                                       const int32_t* __restrict__ col_idx, int n,
-                                                       const word_t* __restrict__ alive, word_t* reached,
-                                                       const int* __restrict__ changed_in, int* changed_out) {
-    const int g = blockIdx.y;
-    if (changed_in && !changed_in[g]) return;
-    const int v = blockIdx.x * blockDim.x + threadIdx.x;
-    int any = 0;
+                                                       const int32_t* __restrict__ col_idx, int n, int groups,
+                                                       int interleave, const word_t* __restrict__ alive, word_t* reached,
+                                                       int* unreached, int32_t* entry_of, int32_t* left_v, int32_t* left_g,
+                                                       word_t* left_w, int32_t* left_base, int32_t* parent,
+                                                       int32_t* comp_size, unsigned cap_entries, unsigned cap_slots,
+                                                       int slot0, PcCounters* counters) {
+    __shared__ int hist[kBits];
+    const int g = blockIdx.y * interleave + (blockIdx.x % interleave);
+    if (g >= groups) return;
+    const int v = (blockIdx.x / interleave) * kThreads + threadIdx.x;
+    if (FINAL) {
+        if (threadIdx.x < kBits) hist[threadIdx.x] = 0;
+        __syncthreads();
+    }
+    int any = 0, any_left = 0;
     if (v < n) {
         const size_t base = static_cast<size_t>(g) * n;
         const word_t mine = reached[base + v];
         const word_t todo = alive[base + v] & ~mine;
         if (todo) {
-            const int beg = row_ptr[v], end = row_ptr[v + 1];
-            word_t got = 0ull;
-            int e = beg;
-            // two neighbours per step: both loads are in flight together
-            for (; e + 1 < end; e += 2) {
-                const int u0 = col_idx[e], u1 = col_idx[e + 1];
-                const word_t r0 = __ldcg(&reached[base + u0]);
-                const word_t r1 = __ldcg(&reached[base + u1]);
-                got |= r0 | r1;
-                if ((got & todo) == todo) break;
-            }
-            if (e + 1 == end && (got & todo) != todo) got |= __ldcg(&reached[base + col_idx[e]]);
-            got &= todo;
+            const word_t got = gather_reached(row_ptr, col_idx, reached + base, v, n, todo);
             if (got) {
                 reached[base + v] = mine | got;
                 any = 1;
             }
-        }
-    }
-    if (__syncthreads_or(any) && threadIdx.x == 0) changed_out[g] = 1;
-}
-
-// ---------------------------------------------------------------------------------
-// finalize: per bit position count the vertices NOT reached (so reached = n - zeros),
-// and compact the alive, unreached, non-isolated (vertex, bits) leftovers.
-__global__ void __launch_bounds__(kThreads) k_pc_finalize(
-    const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx, int n, int rows,
-    const word_t* __restrict__ alive, const word_t* __restrict__ reached, int* zeros, int32_t* entry_of,
-    int32_t* left_v, int32_t* left_g, word_t* left_w, int32_t* left_base, int32_t* parent, int32_t* comp_size,
-    unsigned cap_entries, unsigned cap_slots, int slot0, PcCounters* counters) {
-    __shared__ int hist[kBits];
-    const int g = blockIdx.y;
-    if (threadIdx.x < kBits) hist[threadIdx.x] = 0;
-    __syncthreads();
-    const size_t base = static_cast<size_t>(g) * n;
-    const int valid = min(kBits, rows - g * kBits);
-    const word_t group_mask = valid >= kBits ? ~0ull : ((1ull << valid) - 1ull);
-    for (int v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
-        const word_t r = reached[base + v];
-        word_t z = ~r & group_mask;
-        while (z) {
-            const int b = __ffsll(static_cast<long long>(z)) - 1;
-            z &= z - 1;
-            atomicAdd(&hist[b], 1);
-        }
-        word_t left = alive[base + v] & ~r;
-        if (left) {
-            // keep only the individuals in which v has an alive neighbour
-            word_t nb = 0ull;
-            for (int e = row_ptr[v]; e < row_ptr[v + 1] && (nb & left) != left; ++e) nb |= alive[base + col_idx[e]];
-            left &= nb;
-        }
-        if (left) {
-            const int cnt = __popcll(left);
-            const unsigned e = atomicAdd(&counters->n_entries, 1u);
-            const unsigned s = atomicAdd(&counters->n_slots, static_cast<unsigned>(cnt));
-            if (e < cap_entries && s + cnt <= cap_slots) {
-                left_v[e] = v;
-                left_g[e] = g;
-                left_w[e] = left;
-                left_base[e] = static_cast<int32_t>(s);
-                entry_of[base + v] = static_cast<int32_t>(e);
-                for (int i = 0; i < cnt; ++i) {
-                    parent[slot0 + s + i] = slot0 + static_cast<int32_t>(s) + i;
-                    comp_size[slot0 + s + i] = 0;
+            if (FINAL) {
+                word_t rest = todo & ~got;
+                if (rest) {
+                    any_left = 1;
+                    word_t z = rest;
+                    while (z) {
+                        const int b = __ffsll(static_cast<long long>(z)) - 1;
+                        z &= z - 1;
+                        atomicAdd(&hist[b], 1);
+                    }
+                    // keep only the individuals in which v has an alive neighbour
+                    word_t nb = 0ull;
+                    for (int e = row_ptr[v]; e < row_ptr[v + 1] && (nb & rest) != rest; ++e) nb |= alive[base + col_idx[e]];
+                    rest &= nb;
                 }
-            } else {
-                counters->overflow = 1;
+                if (rest) {
+                    const int cnt = __popcll(rest);
+                    const unsigned e = atomicAdd(&counters->n_entries, 1u);
+                    const unsigned s = atomicAdd(&counters->n_slots, static_cast<unsigned>(cnt));
+                    if (e < cap_entries && s + cnt <= cap_slots) {
+                        left_v[e] = v;
+                        left_g[e] = g;
+                        left_w[e] = rest;
+                        left_base[e] = static_cast<int32_t>(s);
+                        entry_of[base + v] = static_cast<int32_t>(e);
+                        for (int i = 0; i < cnt; ++i) {
+                            parent[slot0 + s + i] = slot0 + static_cast<int32_t>(s) + i;
+                            comp_size[slot0 + s + i] = 0;
+                        }
+                    } else {
+                        counters->overflow = 1;
+                    }
+                }
             }
         }
     }
-    __syncthreads();
-    if (threadIdx.x < kBits && hist[threadIdx.x]) atomicAdd(&zeros[g * kBits + threadIdx.x], hist[threadIdx.x]);
+    if (__syncthreads_or(any) && threadIdx.x == 0) counters->changed = 1;
+    if (FINAL) {
+        if (__syncthreads_or(any_left) && threadIdx.x < kBits && hist[threadIdx.x])
+            atomicAdd(&unreached[g * kBits + threadIdx.x], hist[threadIdx.x]);
+    }
 }
 
 // ---------------------------------------------------------------------------------
@@ -244,7 +342,7 @@ __global__ void __launch_bounds__(kThreads) k_pc_hook(const int32_t* __restrict_
             const word_t common = w & alive[base + u];
             if (!common) continue;
             const word_t ru = reached[base + u];
-            word_t attach = common & ru;  // non-zero only when phase 1 stopped before converging
+            word_t attach = common & ru;  // v was not reached but its neighbour was: v belongs to the giant
             while (attach) {
                 const int b = __ffsll(static_cast<long long>(attach)) - 1;
                 attach &= attach - 1;
@@ -301,15 +399,17 @@ __global__ void __launch_bounds__(kThreads) k_pc_reduce(const int32_t* __restric
 }
 
 // pairwise_connectivity / largest_component_size (components.cpp:49-62) -> double
-// (fitness.cpp:25,32).  Every vertex outside the giant and outside the union-find
-// components is a singleton: 0 pairs, size 1.
-__global__ void __launch_bounds__(kThreads) k_pc_result(int n, int rows, int task, const int* __restrict__ zeros,
+// (fitness.cpp:25,32).  giant = n - removed - unreached + leftovers attached to it;
+// every vertex outside the giant and outside the union-find components is a
+// singleton: 0 pairs, size 1.
+__global__ void __launch_bounds__(kThreads) k_pc_result(int n, int rows, int task, const int* __restrict__ removed_count,
+                                                        const int* __restrict__ unreached,
                                                         const int32_t* __restrict__ comp_size,
                                                         const unsigned long long* __restrict__ pc_extra,
                                                         const int* __restrict__ mcn_extra, double* out) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
-    const long long giant = static_cast<long long>(n) - zeros[r] + comp_size[r];
+    const long long giant = static_cast<long long>(n) - removed_count[r] - unreached[r] + comp_size[r];
     if (task == GAPA_TASK_PC) {
         const unsigned long long pairs = static_cast<unsigned long long>(giant * (giant - 1) / 2) + pc_extra[r];
         out[r] = static_cast<double>(pairs);
@@ -320,13 +420,14 @@ __global__ void __launch_bounds__(kThreads) k_pc_result(int n, int rows, int tas
     }
 }
 
-__global__ void k_pc_reset(int groups, int32_t* parent, int32_t* comp_size, int* zeros,
-                           unsigned long long* pc_extra, int* mcn_extra, PcCounters* counters, bool keep_range) {
+// reset of everything the final sweep / phase 2 accumulate into
+__global__ void k_pc_reset(int groups, int32_t* parent, int32_t* comp_size, int* unreached,
+                           unsigned long long* pc_extra, int* mcn_extra, PcCounters* counters, int first) {
     const int total = groups * kBits;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         parent[i] = i;
         comp_size[i] = 0;
-        zeros[i] = 0;
+        unreached[i] = 0;
         pc_extra[i] = 0ull;
         mcn_extra[i] = 0;
     }
@@ -334,7 +435,8 @@ __global__ void k_pc_reset(int groups, int32_t* parent, int32_t* comp_size, int*
         counters->n_entries = 0u;
         counters->n_slots = 0u;
         counters->overflow = 0;
-        if (!keep_range) counters->range_error = 0;
+        counters->changed = 0;
+        if (first) counters->range_error = 0;
     }
 }
 
@@ -352,113 +454,136 @@ static int ensure_phase2(PcScratch* s, int groups, size_t entries, size_t slots)
     return GAPA_CUDA_OK;
 }
 
+static int env_int(const char* name, int fallback, int lo, int hi) {
+    const char* raw = std::getenv(name);
+    if (!raw || !*raw) return fallback;
+    const long v = std::strtol(raw, nullptr, 10);
+    return static_cast<int>(std::min<long>(hi, std::max<long>(lo, v)));
+}
+
 int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, int cols, double* out_dev,
             cudaStream_t stream) {
     if (!ctx->pc) ctx->pc = new PcScratch();
     PcScratch* s = ctx->pc;
+    if (!s->configured) {  // tuning knobs (defaults are what bench.py measures)
+        s->prefix = env_int("GAPA_PC_PREFIX", 32768, 0, 1 << 24);
+        s->interleave = env_int("GAPA_PC_INTERLEAVE", 8, 1, 64);
+        // the shared-memory bitmap may use most of the SM (one CTA per individual)
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
+        s->configured = true;
+    }
     const int n = ctx->n;
-    // groups per pass bounded by a scratch budget (alive + reached + entry_of = 20 B per vertex and group)
+    const int sm = ctx->sm_count;
+    const int words_per_row = std::max(1, (n + 63) / 64);
+    const int chunk_bits = std::min(words_per_row * 64, 192 * 1024 * 8);  // <= 192 KB of shared memory
+    const int chunks = (words_per_row * 64 + chunk_bits - 1) / chunk_bits;
+    // groups per pass bounded by a scratch budget: alive + reached + entry_of (20 B) + bitmaps (8 B / 64) per vertex
     const size_t budget = 24ull << 30;
     const int all_groups = (rows + kBits - 1) / kBits;
-    const int max_groups = static_cast<int>(std::max<size_t>(1, budget / (20ull * std::max(n, 1))));
-    const int sm = ctx->sm_count;
+    const int max_groups = static_cast<int>(std::max<size_t>(1, budget / (28ull * std::max(n, 1))));
 
     for (int g0 = 0; g0 < all_groups; g0 += max_groups) {
         const int groups = std::min(max_groups, all_groups - g0);
         const int row0 = g0 * kBits;
         const int crows = std::min(rows - row0, groups * kBits);
         const size_t words = static_cast<size_t>(groups) * std::max(n, 1);
+        GAPA_TRY(s->removed.ensure(sizeof(word_t) * static_cast<size_t>(crows) * words_per_row));
+        GAPA_TRY(s->removed_count.ensure(sizeof(int) * groups * kBits));
         GAPA_TRY(s->alive.ensure(sizeof(word_t) * words));
         GAPA_TRY(s->reached.ensure(sizeof(word_t) * words));
         GAPA_TRY(s->entry_of.ensure(sizeof(int32_t) * words));
-        GAPA_TRY(s->zeros.ensure(sizeof(int) * groups * kBits));
+        GAPA_TRY(s->unreached.ensure(sizeof(int) * groups * kBits));
         GAPA_TRY(s->pc_extra.ensure(sizeof(unsigned long long) * groups * kBits));
         GAPA_TRY(s->mcn_extra.ensure(sizeof(int) * groups * kBits));
-        GAPA_TRY(s->flags.ensure(sizeof(int) * 2 * groups));
         GAPA_TRY(s->counters.ensure(sizeof(PcCounters)));
         if (s->cap_entries == 0 || s->parent.cap < sizeof(int32_t) * (static_cast<size_t>(groups) * kBits + s->cap_slots))
             GAPA_TRY(ensure_phase2(s, groups, std::max<size_t>(s->cap_entries, 1u << 16),
                                    std::max<size_t>(s->cap_slots, 1u << 20)));
         word_t* alive = s->alive.as<word_t>();
         word_t* reached = s->reached.as<word_t>();
-        int* flags = s->flags.as<int>();
         PcCounters* counters = s->counters.as<PcCounters>();
         const int slot0 = groups * kBits;
+        const int reset_grid = std::max(1, (groups * kBits + kThreads - 1) / kThreads);
+        auto reset = [&](int first) -> int {
+            GAPA_LAUNCH(k_pc_reset, reset_grid, kThreads, 0, stream, groups, s->parent.as<int32_t>(),
+                        s->comp_size.as<int32_t>(), s->unreached.as<int>(), s->pc_extra.as<unsigned long long>(),
+                        s->mcn_extra.as<int>(), counters, first);
+            return GAPA_CUDA_OK;
+        };
+        GAPA_TRY(reset(1));
+        GAPA_CUDA_TRY(cudaMemsetAsync(s->removed_count.ptr, 0, sizeof(int) * groups * kBits, stream));
 
-        GAPA_LAUNCH(k_pc_reset, std::max(1, (groups * kBits + kThreads - 1) / kThreads), kThreads, 0, stream, groups,
-                    s->parent.as<int32_t>(), s->comp_size.as<int32_t>(), s->zeros.as<int>(),
-                    s->pc_extra.as<unsigned long long>(), s->mcn_extra.as<int>(), counters, false);
         if (n > 0) {
-            GAPA_LAUNCH(k_pc_init, sm * 8, kThreads, 0, stream, alive, reached, n, groups, crows);
-            const size_t cells = static_cast<size_t>(crows) * cols;
-            if (cells) {
-                const int grid = static_cast<int>(std::min<size_t>((cells + kThreads - 1) / kThreads, static_cast<size_t>(sm) * 32));
-                GAPA_LAUNCH(k_pc_remove, grid, kThreads, 0, stream, genes_dev + static_cast<size_t>(row0) * cols, cells,
-                            cols, ctx->pool_identity ? nullptr : ctx->d_pool_map, ctx->pool_size, n, alive, counters);
-            }
+            // ---- masks ------------------------------------------------------------------
+            GAPA_LAUNCH(k_pc_bitmask, dim3(crows, chunks), kMaskThreads, static_cast<size_t>(chunk_bits) / 8, stream,
+                        genes_dev + static_cast<size_t>(row0) * cols, cols, ctx->pool_identity ? nullptr : ctx->d_pool_map,
+                        ctx->pool_size, n, chunk_bits, words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>(),
+                        counters);
+            GAPA_LAUNCH(k_pc_transpose, dim3((words_per_row + kTransThreads - 1) / kTransThreads, groups), kTransThreads,
+                        sizeof(word_t) * kBits * (kTransThreads + 1), stream, s->removed.as<word_t>(), words_per_row, n, crows, alive);
+            GAPA_CUDA_TRY(cudaMemsetAsync(reached, 0, sizeof(word_t) * words, stream));
             GAPA_LAUNCH(k_pc_source, (crows * 32 + kThreads - 1) / kThreads, kThreads, 0, stream, ctx->d_by_degree, n,
                         crows, alive, reached);
 
-            // phase 1: sweeps in batches; stop as soon as a whole batch-end sweep changed nothing.
-            const dim3 grid((n + kThreads - 1) / kThreads, groups);
-            const int kBatch = 3, kMaxSweeps = 96;
-            int sweep = 0;
-            bool converged = false;
-            while (!converged && sweep < kMaxSweeps) {
-                for (int i = 0; i < kBatch; ++i, ++sweep) {
-                    int* out_flags = flags + (sweep & 1) * groups;
-                    const int* in_flags = sweep == 0 ? nullptr : flags + ((sweep - 1) & 1) * groups;
-                    GAPA_CUDA_TRY(cudaMemsetAsync(out_flags, 0, sizeof(int) * groups, stream));
-                    GAPA_LAUNCH(k_pc_sweep, grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, alive, reached,
-                                in_flags, out_flags);
-                }
-                // any group still changing?  (tiny D2H; the stream is idle-waited once per batch)
-                std::vector<int> h(groups);
-                GAPA_CUDA_TRY(cudaMemcpyAsync(h.data(), flags + ((sweep - 1) & 1) * groups, sizeof(int) * groups,
-                                              cudaMemcpyDeviceToHost, stream));
-                GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
-                converged = std::all_of(h.begin(), h.end(), [](int x) { return x == 0; });
-            }
-            s->sweeps_last = sweep;
-
-            // finalize + phase 2, re-run with larger tables if the leftover lists overflowed
-            for (;;) {
-                const int fgrid = std::max(1, std::min((n + kThreads - 1) / kThreads, sm * 4));
-                GAPA_LAUNCH(k_pc_finalize, dim3(fgrid, groups), kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n,
-                            crows, alive, reached, s->zeros.as<int>(), s->entry_of.as<int32_t>(), s->left_v.as<int32_t>(),
-                            s->left_g.as<int32_t>(), s->left_w.as<word_t>(), s->left_base.as<int32_t>(),
-                            s->parent.as<int32_t>(), s->comp_size.as<int32_t>(), static_cast<unsigned>(s->cap_entries),
-                            static_cast<unsigned>(s->cap_slots), slot0, counters);
-                PcCounters h;
+            // ---- phase 1 ------------------------------------------------------------------
+            const int prefix = std::min(s->prefix, n);
+            if (prefix > 0)
+                GAPA_LAUNCH(k_pc_prefix, groups, kPrefixThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, prefix, alive,
+                            reached);
+            const int il = std::min(s->interleave, groups);
+            const dim3 grid(((n + kThreads - 1) / kThreads) * il, (groups + il - 1) / il);
+            auto sweep = [&](bool final_pass) -> int {
+                if (final_pass)
+                    GAPA_LAUNCH(k_pc_sweep<true>, grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, groups, il,
+                                alive, reached, s->unreached.as<int>(), s->entry_of.as<int32_t>(), s->left_v.as<int32_t>(),
+                                s->left_g.as<int32_t>(), s->left_w.as<word_t>(), s->left_base.as<int32_t>(),
+                                s->parent.as<int32_t>(), s->comp_size.as<int32_t>(), static_cast<unsigned>(s->cap_entries),
+                                static_cast<unsigned>(s->cap_slots), slot0, counters);
+                else
+                    GAPA_LAUNCH(k_pc_sweep<false>, grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, groups, il,
+                                alive, reached, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u, 0u,
+                                slot0, counters);
+                return GAPA_CUDA_OK;
+            };
+            // One ordinary sweep, then the recording sweep.  If a lot is still unreached AND the
+            // sweeps were still making progress, sweep more before handing the rest to phase 2
+            // (which is exact for any leftover, just slower than sweeping when there is much of it).
+            const unsigned many = static_cast<unsigned>(std::max<size_t>(8192, words / 512));
+            PcCounters h{};
+            for (int round = 0;; ++round) {
+                GAPA_TRY(sweep(false));
+                if (round > 0) GAPA_TRY(sweep(false));
+                GAPA_TRY(sweep(true));
                 GAPA_CUDA_TRY(cudaMemcpyAsync(&h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
                 GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
                 if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
-                if (h.overflow) {
-                    GAPA_TRY(ensure_phase2(s, groups, static_cast<size_t>(h.n_entries) + 1024, static_cast<size_t>(h.n_slots) + 1024));
-                    GAPA_LAUNCH(k_pc_reset, std::max(1, (groups * kBits + kThreads - 1) / kThreads), kThreads, 0, stream,
-                                groups, s->parent.as<int32_t>(), s->comp_size.as<int32_t>(), s->zeros.as<int>(),
-                                s->pc_extra.as<unsigned long long>(), s->mcn_extra.as<int>(), counters, true);
-                    continue;
-                }
-                if (h.n_entries) {
-                    const int pgrid = static_cast<int>(std::min<unsigned>((h.n_entries + kThreads - 1) / kThreads, sm * 8));
-                    GAPA_LAUNCH(k_pc_hook, pgrid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, alive, reached,
-                                s->entry_of.as<int32_t>(), s->left_v.as<int32_t>(), s->left_g.as<int32_t>(),
-                                s->left_w.as<word_t>(), s->left_base.as<int32_t>(), s->parent.as<int32_t>(), slot0, counters);
-                    GAPA_LAUNCH(k_pc_count, pgrid, kThreads, 0, stream, s->left_w.as<word_t>(), s->left_base.as<int32_t>(),
-                                s->parent.as<int32_t>(), s->comp_size.as<int32_t>(), slot0, counters);
-                    GAPA_LAUNCH(k_pc_reduce, pgrid, kThreads, 0, stream, s->left_g.as<int32_t>(), s->left_w.as<word_t>(),
-                                s->left_base.as<int32_t>(), s->parent.as<int32_t>(), s->comp_size.as<int32_t>(), slot0,
-                                s->pc_extra.as<unsigned long long>(), s->mcn_extra.as<int>(), counters);
-                }
-                break;
+                const bool retry_bigger = h.overflow != 0;
+                const bool keep_sweeping = h.changed && h.n_entries > many && round < 48;
+                if (!retry_bigger && !keep_sweeping) break;
+                if (retry_bigger)
+                    GAPA_TRY(ensure_phase2(s, groups, std::max<size_t>(s->cap_entries, static_cast<size_t>(h.n_entries) + 1024),
+                                           std::max<size_t>(s->cap_slots, static_cast<size_t>(h.n_slots) + 1024)));
+                GAPA_TRY(reset(0));
+            }
+            // ---- phase 2 ------------------------------------------------------------------
+            if (h.n_entries) {
+                const int pgrid = static_cast<int>(std::min<unsigned>((h.n_entries + kThreads - 1) / kThreads, sm * 8));
+                GAPA_LAUNCH(k_pc_hook, pgrid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, alive, reached,
+                            s->entry_of.as<int32_t>(), s->left_v.as<int32_t>(), s->left_g.as<int32_t>(),
+                            s->left_w.as<word_t>(), s->left_base.as<int32_t>(), s->parent.as<int32_t>(), slot0, counters);
+                GAPA_LAUNCH(k_pc_count, pgrid, kThreads, 0, stream, s->left_w.as<word_t>(), s->left_base.as<int32_t>(),
+                            s->parent.as<int32_t>(), s->comp_size.as<int32_t>(), slot0, counters);
+                GAPA_LAUNCH(k_pc_reduce, pgrid, kThreads, 0, stream, s->left_g.as<int32_t>(), s->left_w.as<word_t>(),
+                            s->left_base.as<int32_t>(), s->parent.as<int32_t>(), s->comp_size.as<int32_t>(), slot0,
+                            s->pc_extra.as<unsigned long long>(), s->mcn_extra.as<int>(), counters);
             }
         } else if (static_cast<size_t>(crows) * cols) {
             return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
         }
-        GAPA_LAUNCH(k_pc_result, (crows + kThreads - 1) / kThreads, kThreads, 0, stream, n, crows, task, s->zeros.as<int>(),
-                    s->comp_size.as<int32_t>(), s->pc_extra.as<unsigned long long>(), s->mcn_extra.as<int>(),
-                    out_dev + row0);
+        GAPA_LAUNCH(k_pc_result, (crows + kThreads - 1) / kThreads, kThreads, 0, stream, n, crows, task,
+                    s->removed_count.as<int>(), s->unreached.as<int>(), s->comp_size.as<int32_t>(),
+                    s->pc_extra.as<unsigned long long>(), s->mcn_extra.as<int>(), out_dev + row0);
     }
     return GAPA_CUDA_OK;
 }
@@ -466,8 +591,9 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
 void pc_free(gapa_cuda_ctx* ctx) {
     if (!ctx->pc) return;
     PcScratch* s = ctx->pc;
-    for (DevBuf* b : {&s->alive, &s->reached, &s->entry_of, &s->zeros, &s->flags, &s->counters, &s->left_v, &s->left_g,
-                      &s->left_w, &s->left_base, &s->parent, &s->comp_size, &s->pc_extra, &s->mcn_extra})
+    for (DevBuf* b : {&s->removed, &s->removed_count, &s->alive, &s->reached, &s->entry_of, &s->unreached, &s->counters,
+                      &s->left_v, &s->left_g, &s->left_w, &s->left_base, &s->parent, &s->comp_size, &s->pc_extra,
+                      &s->mcn_extra})
         b->release();
     delete s;
     ctx->pc = nullptr;
