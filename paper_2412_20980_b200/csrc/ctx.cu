@@ -221,6 +221,8 @@ int gapa_cuda_destroy(gapa_cuda_ctx* c) {
     if (c->ev_start) cudaEventDestroy(c->ev_start);
     if (c->ev_stop) cudaEventDestroy(c->ev_stop);
     if (c->stream) cudaStreamDestroy(c->stream);
+    if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
+    for (cudaEvent_t ev : c->copy_events) cudaEventDestroy(ev);
     delete c;
     return GAPA_CUDA_OK;
 }
@@ -344,9 +346,35 @@ int gapa_cuda_eval_batch(gapa_cuda_ctx* c, int task, const int32_t* genes_host, 
     const size_t cells = static_cast<size_t>(rows) * cols;
     GAPA_TRY(c->genes_stage.ensure(sizeof(int32_t) * std::max<size_t>(cells, 1)));
     GAPA_TRY(c->out_stage.ensure(sizeof(double) * rows));
+    // Row chunks of ~64 MB (whole 64-individual groups): the H2D copy of chunk i+1 runs on the
+    // copy stream while the kernels of chunk i run on the work stream, so a PCIe-bound call
+    // costs max(copy, compute) instead of their sum.
+    const size_t row_bytes = sizeof(int32_t) * static_cast<size_t>(std::max(cols, 1));
+    int chunk_rows = static_cast<int>(std::min<size_t>(rows, std::max<size_t>(64, ((64ull << 20) / row_bytes) & ~size_t{63})));
+    const int chunks = (rows + chunk_rows - 1) / chunk_rows;
+    if (!c->copy_stream) GAPA_CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
+    while (static_cast<int>(c->copy_events.size()) < chunks) {
+        cudaEvent_t ev;
+        GAPA_CUDA_TRY(cudaEventCreateWithFlags(&ev, cudaEventDisableTiming));
+        c->copy_events.push_back(ev);
+    }
+    int32_t* stage = c->genes_stage.as<int32_t>();
     if (cells)
-        GAPA_CUDA_TRY(cudaMemcpyAsync(c->genes_stage.ptr, genes_host, sizeof(int32_t) * cells, cudaMemcpyHostToDevice, c->stream));
-    GAPA_TRY(gapa_cuda_eval_batch_device(c, task, c->genes_stage.as<int32_t>(), rows, cols, c->out_stage.as<double>(), c->stream));
+        for (int i = 0; i < chunks; ++i) {
+            const int r0 = i * chunk_rows, cr = std::min(chunk_rows, rows - r0);
+            GAPA_CUDA_TRY(cudaMemcpyAsync(stage + static_cast<size_t>(r0) * cols, genes_host + static_cast<size_t>(r0) * cols,
+                                          sizeof(int32_t) * static_cast<size_t>(cr) * cols, cudaMemcpyHostToDevice, c->copy_stream));
+            GAPA_CUDA_TRY(cudaEventRecord(c->copy_events[i], c->copy_stream));
+        }
+    float total_ms = 0.f;
+    for (int i = 0; i < chunks; ++i) {
+        const int r0 = i * chunk_rows, cr = std::min(chunk_rows, rows - r0);
+        if (cells) GAPA_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_events[i], 0));
+        GAPA_TRY(gapa_cuda_eval_batch_device(c, task, stage + static_cast<size_t>(r0) * cols, cr, cols,
+                                             c->out_stage.as<double>() + r0, c->stream));
+        total_ms += c->last_eval_ms;
+    }
+    c->last_eval_ms = total_ms;
     GAPA_CUDA_TRY(cudaMemcpyAsync(out_host, c->out_stage.ptr, sizeof(double) * rows, cudaMemcpyDeviceToHost, c->stream));
     GAPA_CUDA_TRY(cudaStreamSynchronize(c->stream));
     return GAPA_CUDA_OK;

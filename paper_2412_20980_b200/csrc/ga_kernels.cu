@@ -92,10 +92,15 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_eda(const int32_t* __restrict
 // j = #{better or equal}; counting replaces the sort (O(s^2) compares, s <= 16k).
 __device__ __forceinline__ bool better(double a, double b, int minimize) { return minimize ? a < b : a > b; }
 
+// kSplit lanes share one element and each scans 1/kSplit of every tile, so s elements
+// give s / 32 blocks instead of s / 256 (s is only a few thousand).
+static constexpr int kSplit = 8;
+static constexpr int kPerBlock = kGaThreads / kSplit;
+
 __global__ void __launch_bounds__(kGaThreads) k_ga_weights(const double* __restrict__ fitness, int s, int minimize,
                                                            double* __restrict__ weights, int* status) {
     __shared__ double tile[kGaThreads];
-    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    const int i = blockIdx.x * kPerBlock + threadIdx.x / kSplit, part = threadIdx.x % kSplit;
     const double mine = i < s ? fitness[i] : 0.0;
     if (i < s && !isfinite(mine)) *status = GAPA_CUDA_E_NAN;
     int less = 0, leq = 0;
@@ -104,14 +109,18 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_weights(const double* __restr
         if (t0 + threadIdx.x < s) tile[threadIdx.x] = fitness[t0 + threadIdx.x];
         __syncthreads();
         const int lim = min(kGaThreads, s - t0);
-        for (int t = 0; t < lim; ++t) {
+        for (int t = part; t < lim; t += kSplit) {
             const double other = tile[t];
             const bool b = better(other, mine, minimize);
             less += b;
             leq += b || other == mine;
         }
     }
-    if (i < s) weights[i] = (static_cast<double>(s - less) + static_cast<double>(s - leq + 1)) / 2.0;
+    for (int off = kSplit / 2; off; off >>= 1) {
+        less += __shfl_down_sync(0xffffffffu, less, off, kSplit);
+        leq += __shfl_down_sync(0xffffffffu, leq, off, kSplit);
+    }
+    if (i < s && part == 0) weights[i] = (static_cast<double>(s - less) + static_cast<double>(s - leq + 1)) / 2.0;
 }
 
 // cumulative sum + weighted_pick (ga_ops.cpp:78-82, :113-126), one block.
@@ -159,7 +168,7 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_elite_rank(const double* __re
                                                               int s, int minimize, int32_t* __restrict__ src_of_rank,
                                                               int* status) {
     __shared__ double tile[kGaThreads];
-    const int x = blockIdx.x * blockDim.x + threadIdx.x;
+    const int x = blockIdx.x * kPerBlock + threadIdx.x / kSplit, part = threadIdx.x % kSplit;
     const int total = 2 * s;
     const double mine = x < total ? (x < s ? fit[x] : fit_m[x - s]) : 0.0;
     if (x < total && isnan(mine)) *status = GAPA_CUDA_E_NAN;
@@ -170,12 +179,13 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_elite_rank(const double* __re
         if (y < total) tile[threadIdx.x] = y < s ? fit[y] : fit_m[y - s];
         __syncthreads();
         const int lim = min(kGaThreads, total - t0);
-        for (int t = 0; t < lim; ++t) {
+        for (int t = part; t < lim; t += kSplit) {
             const double other = tile[t];
             rank += better(other, mine, minimize) || (other == mine && t0 + t < x);
         }
     }
-    if (x < total && rank < s) src_of_rank[rank] = x;
+    for (int off = kSplit / 2; off; off >>= 1) rank += __shfl_down_sync(0xffffffffu, rank, off, kSplit);
+    if (x < total && part == 0 && rank < s) src_of_rank[rank] = x;
 }
 
 __global__ void __launch_bounds__(kGaThreads) k_ga_elite_gather(const int32_t* __restrict__ pop,
@@ -188,7 +198,13 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_elite_gather(const int32_t* _
     const int src = src_of_rank[r];
     const int32_t* from = src < s ? pop + static_cast<size_t>(src) * k : m_pop + static_cast<size_t>(src - s) * k;
     int32_t* to = next + static_cast<size_t>(r) * k;
-    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) to[j] = from[j];
+    if (((reinterpret_cast<uintptr_t>(from) | reinterpret_cast<uintptr_t>(to)) & 15) == 0 && (k & 3) == 0) {
+        const int4* from4 = reinterpret_cast<const int4*>(from);
+        int4* to4 = reinterpret_cast<int4*>(to);
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < (k >> 2); j += gridDim.x * blockDim.x) to4[j] = __ldcs(&from4[j]);
+    } else {
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) to[j] = from[j];
+    }
     if (blockIdx.x == 0 && threadIdx.x == 0) next_fit[r] = src < s ? fit[src] : fit_m[src - s];
 }
 
@@ -212,7 +228,7 @@ int launch_init(uint32_t pool_size, int row_first, int row_count, int budget, ui
 }
 int launch_select(const double* fitness, int s, int minimize, uint64_t seed, uint64_t generation, int32_t* partner,
                   double* weights, double* cumulative, int* status, cudaStream_t st) {
-    GAPA_LAUNCH(k_ga_weights, (s + kGaThreads - 1) / kGaThreads, kGaThreads, 0, st, fitness, s, minimize, weights, status);
+    GAPA_LAUNCH(k_ga_weights, (s + kPerBlock - 1) / kPerBlock, kGaThreads, 0, st, fitness, s, minimize, weights, status);
     GAPA_LAUNCH(k_ga_pick, 1, 1024, 0, st, weights, s, seed, generation, cumulative, partner);
     return GAPA_CUDA_OK;
 }
@@ -240,7 +256,7 @@ int launch_eda(const int32_t* elite, int s, int k, int elite_count, uint32_t bou
 }
 int launch_elitism(const int32_t* pop, const int32_t* m_pop, int s, int k, const double* fit, const double* fit_m,
                    int minimize, int32_t* next, double* next_fit, int32_t* src_of_rank, int* status, cudaStream_t st) {
-    GAPA_LAUNCH(k_ga_elite_rank, (2 * s + kGaThreads - 1) / kGaThreads, kGaThreads, 0, st, fit, fit_m, s, minimize,
+    GAPA_LAUNCH(k_ga_elite_rank, (2 * s + kPerBlock - 1) / kPerBlock, kGaThreads, 0, st, fit, fit_m, s, minimize,
                 src_of_rank, status);
     GAPA_LAUNCH(k_ga_elite_gather, row_grid(std::max(k, 1), s), kGaThreads, 0, st, pop, m_pop, fit, fit_m, s, k, src_of_rank,
                 next, next_fit);

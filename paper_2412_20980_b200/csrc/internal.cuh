@@ -135,6 +135,8 @@ struct gapa_cuda_ctx {
     int32_t* d_pairs = nullptr;     // (T + P) x 2, test pairs first
     // work stream + timing
     cudaStream_t stream = nullptr;
+    cudaStream_t copy_stream = nullptr;          // H2D of the host-buffer entry point, overlapped with compute
+    std::vector<cudaEvent_t> copy_events;
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
     float last_eval_ms = 0.f;
     // FitnessFunction methods are const and called concurrently from worker threads in the

@@ -60,7 +60,7 @@ struct PcScratch {
     DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters;
     DevBuf left_v, left_g, left_w, left_base, parent, comp_size, pc_extra, mcn_extra;
     size_t cap_entries = 0, cap_slots = 0;
-    int prefix = 32768, interleave = 8;
+    int prefix = 32768, interleave = 8, mask_chunks = 1, cached = 1;
     bool configured = false;
 };
 
@@ -74,22 +74,40 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(const int32_t* __re
                                                              const int32_t* __restrict__ pool_map, int pool_size, int n,
                                                              int chunk_bits, int words_per_row, word_t* __restrict__ removed,
                                                              int* removed_count, PcCounters* counters) {
-    const int row = blockIdx.x;
-    const int v0 = blockIdx.y * chunk_bits;
+    const int row = blockIdx.y;  // the chunks of one individual are adjacent blocks: its genes are re-read from L2
+    const int v0 = blockIdx.x * chunk_bits;
     const int v1 = min(n, v0 + chunk_bits);
     const int words64 = (v1 - v0 + 63) >> 6;
     for (int w = threadIdx.x; w < 2 * words64; w += kMaskThreads) pc_smem_bits[w] = 0u;
     __syncthreads();
     const int32_t* g = genes + static_cast<size_t>(row) * cols;
-    for (int j = threadIdx.x; j < cols; j += kMaskThreads) {
-        const int gene = g[j];
+    auto mark = [&](int gene) {
         if (gene < 0 || gene >= pool_size) {
             counters->range_error = 1;
-            continue;
+            return;
         }
         const int node = pool_map ? pool_map[gene] : gene;
         if (node >= v0 && node < v1) atomicOr(&pc_smem_bits[(node - v0) >> 5], 1u << ((node - v0) & 31));
+    };
+    int j0 = 0;
+    if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+        // 16-byte loads, two per thread in flight before the first shared-memory atomic
+        const int4* g4 = reinterpret_cast<const int4*>(g);
+        const int quads = cols >> 2;
+        int q = threadIdx.x;
+        for (; q + kMaskThreads < quads; q += 2 * kMaskThreads) {
+            const int4 a = __ldcs(&g4[q]);
+            const int4 b = __ldcs(&g4[q + kMaskThreads]);
+            mark(a.x); mark(a.y); mark(a.z); mark(a.w);
+            mark(b.x); mark(b.y); mark(b.z); mark(b.w);
+        }
+        if (q < quads) {
+            const int4 a = __ldcs(&g4[q]);
+            mark(a.x); mark(a.y); mark(a.z); mark(a.w);
+        }
+        j0 = quads << 2;
     }
+    for (int j = j0 + threadIdx.x; j < cols; j += kMaskThreads) mark(g[j]);
     __syncthreads();
     const word_t* bits64 = reinterpret_cast<const word_t*>(pc_smem_bits);
     word_t* out = removed + static_cast<size_t>(row) * words_per_row + (v0 >> 6);
@@ -169,6 +187,13 @@ __global__ void __launch_bounds__(kThreads) k_pc_source(const int32_t* __restric
 // bits; 64-bit stores are single transactions), so a sweep can use bits set earlier
 // in the same sweep.  `limit` truncates the scan to neighbours below it (rows are
 // ascending), which is what keeps hub rows short while only a prefix is active.
+// CACHED reads neighbour words through L1: hub words are shared by many threads of an SM and,
+// once the prefix is closed, no longer change; a stale line can only under-report bits, which
+// the next sweep (or phase 2) makes up for.  L1 is invalidated at every kernel boundary.
+template <bool CACHED>
+__device__ __forceinline__ word_t load_word(const word_t* p) { return CACHED ? __ldca(p) : __ldcg(p); }
+
+template <bool CACHED>
 __device__ __forceinline__ word_t gather_reached(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                                                  const word_t* reached_g, int v, int limit, word_t todo) {
     const int beg = row_ptr[v], end = row_ptr[v + 1];
@@ -177,15 +202,15 @@ __device__ __forceinline__ word_t gather_reached(const int32_t* __restrict__ row
     for (; e + 1 < end; e += 2) {  // two neighbours per step: both loads are in flight together
         const int u0 = col_idx[e], u1 = col_idx[e + 1];
         if (u1 >= limit) {
-            if (u0 < limit) got |= __ldcg(&reached_g[u0]);
+            if (u0 < limit) got |= load_word<CACHED>(&reached_g[u0]);
             return got & todo;
         }
-        got |= __ldcg(&reached_g[u0]) | __ldcg(&reached_g[u1]);
+        got |= load_word<CACHED>(&reached_g[u0]) | load_word<CACHED>(&reached_g[u1]);
         if ((got & todo) == todo) return todo;
     }
     if (e < end) {
         const int u = col_idx[e];
-        if (u < limit) got |= __ldcg(&reached_g[u]);
+        if (u < limit) got |= load_word<CACHED>(&reached_g[u]);
     }
     return got & todo;
 }
@@ -209,7 +234,7 @@ __global__ void __launch_bounds__(kPrefixThreads) k_pc_prefix(const int32_t* __r
                 const word_t mine = reached_g[v];
                 const word_t todo = alive_g[v] & ~mine;
                 if (!todo) continue;
-                const word_t got = gather_reached(row_ptr, col_idx, reached_g, v, limit, todo);
+                const word_t got = gather_reached<false>(row_ptr, col_idx, reached_g, v, limit, todo);
                 if (got) {
                     reached_g[v] = mine | got;
                     any = 1;
@@ -224,7 +249,7 @@ __global__ void __launch_bounds__(kPrefixThreads) k_pc_prefix(const int32_t* __r
 // that blocks are scheduled in ascending vertex order with a small window per group.
 // FINAL additionally records what is still unreached: per-individual counts and the
 // compacted non-isolated leftovers for phase 2.
-template <bool FINAL>
+template <bool FINAL, bool CACHED>
 __global__ void __launch_bounds__(kThreads) k_pc_sweep(const int32_t* __restrict__ row_ptr,
                                                        const int32_t* __restrict__ col_idx, int n, int groups,
                                                        int interleave, const word_t* __restrict__ alive, word_t* reached,
@@ -246,7 +271,7 @@ __global__ void __launch_bounds__(kThreads) k_pc_sweep(const int32_t* __restrict
         const word_t mine = reached[base + v];
         const word_t todo = alive[base + v] & ~mine;
         if (todo) {
-            const word_t got = gather_reached(row_ptr, col_idx, reached + base, v, n, todo);
+            const word_t got = gather_reached<CACHED>(row_ptr, col_idx, reached + base, v, n, todo);
             if (got) {
                 reached[base + v] = mine | got;
                 any = 1;
@@ -468,6 +493,8 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
     if (!s->configured) {  // tuning knobs (defaults are what bench.py measures)
         s->prefix = env_int("GAPA_PC_PREFIX", 32768, 0, 1 << 24);
         s->interleave = env_int("GAPA_PC_INTERLEAVE", 8, 1, 64);
+        s->mask_chunks = env_int("GAPA_PC_MASK_CHUNKS", 1, 1, 64);
+        s->cached = env_int("GAPA_PC_L1", 1, 0, 1);
         // the shared-memory bitmap may use most of the SM (one CTA per individual)
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
@@ -476,12 +503,13 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
     const int n = ctx->n;
     const int sm = ctx->sm_count;
     const int words_per_row = std::max(1, (n + 63) / 64);
-    const int chunk_bits = std::min(words_per_row * 64, 192 * 1024 * 8);  // <= 192 KB of shared memory
+    int chunk_bits = std::min(words_per_row * 64, 192 * 1024 * 8);  // <= 192 KB of shared memory
+    if (s->mask_chunks > 1) chunk_bits = std::min(chunk_bits, ((words_per_row + s->mask_chunks - 1) / s->mask_chunks) * 64);
     const int chunks = (words_per_row * 64 + chunk_bits - 1) / chunk_bits;
     // groups per pass bounded by a scratch budget: alive + reached + entry_of (20 B) + bitmaps (8 B / 64) per vertex
     const size_t budget = 24ull << 30;
     const int all_groups = (rows + kBits - 1) / kBits;
-    const int max_groups = static_cast<int>(std::max<size_t>(1, budget / (28ull * std::max(n, 1))));
+    const int max_groups = static_cast<int>(std::min<size_t>(1023, std::max<size_t>(1, budget / (28ull * std::max(n, 1)))));
 
     for (int g0 = 0; g0 < all_groups; g0 += max_groups) {
         const int groups = std::min(max_groups, all_groups - g0);
@@ -516,7 +544,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
 
         if (n > 0) {
             // ---- masks ------------------------------------------------------------------
-            GAPA_LAUNCH(k_pc_bitmask, dim3(crows, chunks), kMaskThreads, static_cast<size_t>(chunk_bits) / 8, stream,
+            GAPA_LAUNCH(k_pc_bitmask, dim3(chunks, crows), kMaskThreads, static_cast<size_t>(chunk_bits) / 8, stream,
                         genes_dev + static_cast<size_t>(row0) * cols, cols, ctx->pool_identity ? nullptr : ctx->d_pool_map,
                         ctx->pool_size, n, chunk_bits, words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>(),
                         counters);
@@ -535,15 +563,19 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
             const dim3 grid(((n + kThreads - 1) / kThreads) * il, (groups + il - 1) / il);
             auto sweep = [&](bool final_pass) -> int {
                 if (final_pass)
-                    GAPA_LAUNCH(k_pc_sweep<true>, grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, groups, il,
+                    GAPA_LAUNCH((k_pc_sweep<true, false>), grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, groups, il,
                                 alive, reached, s->unreached.as<int>(), s->entry_of.as<int32_t>(), s->left_v.as<int32_t>(),
                                 s->left_g.as<int32_t>(), s->left_w.as<word_t>(), s->left_base.as<int32_t>(),
                                 s->parent.as<int32_t>(), s->comp_size.as<int32_t>(), static_cast<unsigned>(s->cap_entries),
                                 static_cast<unsigned>(s->cap_slots), slot0, counters);
+                else if (s->cached)
+                    GAPA_LAUNCH((k_pc_sweep<false, true>), grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, groups,
+                                il, alive, reached, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u,
+                                0u, slot0, counters);
                 else
-                    GAPA_LAUNCH(k_pc_sweep<false>, grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, groups, il,
-                                alive, reached, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u, 0u,
-                                slot0, counters);
+                    GAPA_LAUNCH((k_pc_sweep<false, false>), grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, groups,
+                                il, alive, reached, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u,
+                                0u, slot0, counters);
                 return GAPA_CUDA_OK;
             };
             // One ordinary sweep, then the recording sweep.  If a lot is still unreached AND the

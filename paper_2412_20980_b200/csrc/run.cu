@@ -27,12 +27,50 @@ int launch_elitism(const int32_t*, const int32_t*, int, int, const double*, cons
 
 // record_generation (modes.cpp:35-43): best = front, mean = SEQUENTIAL sum / s so that
 // non-integer fitness reproduces std::accumulate bit for bit.
-__global__ void k_ga_stats(const double* __restrict__ fit, int s, double* best, double* mean) {
-    if (blockIdx.x || threadIdx.x) return;
+__global__ void __launch_bounds__(1024) k_ga_stats(const double* __restrict__ fit, int s, double* best, double* mean) {
+    __shared__ double stage[4096];
+    __shared__ double warp_sum[32];
+    __shared__ int not_exact;
+    const int tid = threadIdx.x;
+    if (tid == 0) not_exact = 0;
+    __syncthreads();
+    // Integer-valued fitness whose running sums stay below 2^53 (PC, MCN) adds exactly in any order.
+    double local = 0.0;
+    const double bound = 9007199254740992.0 / static_cast<double>(s);
+    for (int i = tid; i < s; i += blockDim.x) {
+        const double x = fit[i];
+        if (!(x == floor(x)) || !(fabs(x) < bound)) not_exact = 1;
+        local += x;
+    }
+    __syncthreads();
+    if (!not_exact) {
+        for (int off = 16; off; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
+        if ((tid & 31) == 0) warp_sum[tid >> 5] = local;
+        __syncthreads();
+        if (tid < 32) {
+            double v = tid < (blockDim.x >> 5) ? warp_sum[tid] : 0.0;
+            for (int off = 16; off; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+            if (tid == 0) {
+                *best = fit[0];
+                *mean = v / static_cast<double>(s);
+            }
+        }
+        return;
+    }
+    // general FP64 fitness: the reference's left-to-right std::accumulate, staged through shared memory
     double sum = 0.0;
-    for (int i = 0; i < s; ++i) sum += fit[i];
-    *best = fit[0];
-    *mean = sum / static_cast<double>(s);
+    for (int base = 0; base < s; base += 4096) {
+        const int lim = min(4096, s - base);
+        for (int i = tid; i < lim; i += blockDim.x) stage[i] = fit[base + i];
+        __syncthreads();
+        if (tid == 0)
+            for (int i = 0; i < lim; ++i) sum += stage[i];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        *best = fit[0];
+        *mean = sum / static_cast<double>(s);
+    }
 }
 
 __global__ void k_check_nan(const double* __restrict__ fit, int s, int* status) {
@@ -74,7 +112,7 @@ int eval_rows(gapa_cuda_ctx* ctx, int task, const int32_t* genes, int rows, int 
 
 extern "C" int gapa_cuda_ga_stats_device(const double* fit_dev, int s, double* best_dev, double* mean_dev, void* stream) {
     if (s < 1 || !fit_dev || !best_dev || !mean_dev) return fail(GAPA_CUDA_E_INVALID, "stats: bad arguments");
-    GAPA_LAUNCH(k_ga_stats, 1, 1, 0, static_cast<cudaStream_t>(stream), fit_dev, s, best_dev, mean_dev);
+    GAPA_LAUNCH(k_ga_stats, 1, 1024, 0, static_cast<cudaStream_t>(stream), fit_dev, s, best_dev, mean_dev);
     return GAPA_CUDA_OK;
 }
 
@@ -181,7 +219,7 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
                                 status, st));
         std::swap(pop, next);
         std::swap(fit, fit_next);
-        GAPA_LAUNCH(k_ga_stats, 1, 1, 0, st, fit, s, hist + (gen - 1), hist + iters + (gen - 1));
+        GAPA_LAUNCH(k_ga_stats, 1, 1024, 0, st, fit, s, hist + (gen - 1), hist + iters + (gen - 1));
         // NaN / non-finite fitness is an Error in the reference (ga_ops.cpp:56-57, :189-192);
         // the flag is polled every few generations and at the end to keep the loop asynchronous.
         if ((gen & 15) == 0 || gen == iters) {
