@@ -43,10 +43,12 @@ namespace gapa_b200 {
 
 typedef unsigned long long word_t;
 static constexpr int kBits = 64;
+static constexpr int kPack = 4;  // groups per 32-byte vertex record
 static constexpr int kThreads = 256;
 static constexpr int kMaskThreads = 1024;
 static constexpr int kTransThreads = 128;
 static constexpr int kPrefixThreads = 1024;
+static_assert(kThreads == 4 * 64, "the final sweep's histogram has one counter per thread");
 
 struct PcCounters {
     unsigned int n_entries;
@@ -60,7 +62,7 @@ struct PcScratch {
     DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters;
     DevBuf left_v, left_g, left_w, left_base, parent, comp_size, pc_extra, mcn_extra;
     size_t cap_entries = 0, cap_slots = 0;
-    int prefix = 32768, interleave = 8, mask_chunks = 1, cached = 1;
+    int prefix = 32768, interleave = 8, mask_chunks = 1;
     bool configured = false;
 };
 
@@ -124,6 +126,11 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(const int32_t* __re
 // mask build, step 2: 64 individuals x 64 vertices bit transpose in registers.
 // a[i] bit c (individual i, vertex c)  ->  a[c] bit i; alive = ~removed.  Rows past
 // the end of the batch read as "everything removed", which zeroes their bits.
+//
+// Vertex records: kPack = 4 groups (256 individuals) are stored side by side, one 32-byte
+// record per vertex — word gi of record (sg, v) belongs to group 4 sg + gi.  32 bytes is
+// exactly one memory sector, so the random neighbour read of the sweeps fetches 256
+// individuals of state per sector instead of 64.
 __global__ void __launch_bounds__(kTransThreads) k_pc_transpose(const word_t* __restrict__ removed, int words_per_row,
                                                                 int n, int rows, word_t* __restrict__ alive) {
     word_t* tile = reinterpret_cast<word_t*>(pc_smem_bits);  // kBits x (kTransThreads + 1) words, padded against bank conflicts
@@ -152,13 +159,17 @@ __global__ void __launch_bounds__(kTransThreads) k_pc_transpose(const word_t* __
         for (int c = 0; c < kBits; ++c) tile[c * (kTransThreads + 1) + threadIdx.x] = ~a[c];
     }
     __syncthreads();
-    // coalesced write-out: the block's tile is kTransThreads * 64 consecutive vertices
-    word_t* out = alive + static_cast<size_t>(g) * n;
+    // write-out in vertex order: the block's tile is kTransThreads * 64 consecutive vertices
+    word_t* out = alive + (static_cast<size_t>(g / kPack) * n) * kPack + (g % kPack);
     const int v_base = vb0 * kBits;
     for (int idx = threadIdx.x; idx < kTransThreads * kBits; idx += kTransThreads) {
         const int v = v_base + idx;
-        if (v < n) out[v] = tile[(idx & 63) * (kTransThreads + 1) + (idx >> 6)];
+        if (v < n) out[static_cast<size_t>(v) * kPack] = tile[(idx & 63) * (kTransThreads + 1) + (idx >> 6)];
     }
+}
+
+__device__ __forceinline__ size_t word_index(int g, int n, int v) {
+    return (static_cast<size_t>(g / kPack) * n + v) * kPack + (g % kPack);
 }
 
 // One warp per individual: the first alive vertex in descending-degree order
@@ -169,61 +180,86 @@ __global__ void __launch_bounds__(kThreads) k_pc_source(const int32_t* __restric
     const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
-    const size_t base = static_cast<size_t>(row >> 6) * n;
+    const int g = row >> 6;
     const word_t bit = 1ull << (row & 63);
     for (int i = 0; i < n; i += 32) {
         const int v = i + lane < n ? by_degree[i + lane] : -1;
-        const bool ok = v >= 0 && (alive[base + v] & bit);
+        const bool ok = v >= 0 && (alive[word_index(g, n, v)] & bit);
         const unsigned hit = __ballot_sync(0xffffffffu, ok);
         if (hit) {
-            if (lane == __ffs(hit) - 1) atomicOr(&reached[base + v], bit);
+            if (lane == __ffs(hit) - 1) atomicOr(&reached[word_index(g, n, v)], bit);
             return;
         }
     }
 }
 
 // ---------------------------------------------------------------------------------
-// phase 1.  Reads of neighbours' words race benignly with writes (words only gain
-// bits; 64-bit stores are single transactions), so a sweep can use bits set earlier
-// in the same sweep.  `limit` truncates the scan to neighbours below it (rows are
-// ascending), which is what keeps hub rows short while only a prefix is active.
-// CACHED reads neighbour words through L1: hub words are shared by many threads of an SM and,
-// once the prefix is closed, no longer change; a stale line can only under-report bits, which
-// the next sweep (or phase 2) makes up for.  L1 is invalidated at every kernel boundary.
-template <bool CACHED>
-__device__ __forceinline__ word_t load_word(const word_t* p) { return CACHED ? __ldca(p) : __ldcg(p); }
+// phase 1.  Reads of neighbours' records race benignly with writes (words only gain
+// bits; every 64-bit word is written by single stores), so a sweep can use bits set
+// earlier in the same sweep.  `limit` truncates the scan to neighbours below it (rows
+// are ascending), which is what keeps hub rows short while only a prefix is active.
+struct __align__(32) Rec {
+    word_t w[kPack];
+};
+__device__ __forceinline__ Rec load_rec(const Rec* p) {  // two 16-byte loads of one sector, L2-coherent
+    const ulonglong2 lo = __ldcg(reinterpret_cast<const ulonglong2*>(p));
+    const ulonglong2 hi = __ldcg(reinterpret_cast<const ulonglong2*>(p) + 1);
+    Rec r;
+    r.w[0] = lo.x; r.w[1] = lo.y; r.w[2] = hi.x; r.w[3] = hi.y;
+    return r;
+}
+__device__ __forceinline__ void store_rec(Rec* p, const Rec& r) {
+    reinterpret_cast<ulonglong2*>(p)[0] = make_ulonglong2(r.w[0], r.w[1]);
+    reinterpret_cast<ulonglong2*>(p)[1] = make_ulonglong2(r.w[2], r.w[3]);
+}
+__device__ __forceinline__ bool rec_any(const Rec& r) { return (r.w[0] | r.w[1] | r.w[2] | r.w[3]) != 0ull; }
+__device__ __forceinline__ bool rec_covers(const Rec& got, const Rec& todo) {
+    return ((todo.w[0] & ~got.w[0]) | (todo.w[1] & ~got.w[1]) | (todo.w[2] & ~got.w[2]) | (todo.w[3] & ~got.w[3])) == 0ull;
+}
+__device__ __forceinline__ void rec_or(Rec& a, const Rec& b) {
+#pragma unroll
+    for (int i = 0; i < kPack; ++i) a.w[i] |= b.w[i];
+}
 
-template <bool CACHED>
-__device__ __forceinline__ word_t gather_reached(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
-                                                 const word_t* reached_g, int v, int limit, word_t todo) {
+// OR of the neighbours' reached records until `todo` is covered; returns got & todo.
+__device__ __forceinline__ Rec gather_reached(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                                              const Rec* reached_sg, int v, int limit, const Rec& todo) {
     const int beg = row_ptr[v], end = row_ptr[v + 1];
-    word_t got = 0ull;
+    Rec got{};
     int e = beg;
-    for (; e + 1 < end; e += 2) {  // two neighbours per step: both loads are in flight together
+    for (; e + 1 < end; e += 2) {  // two neighbours per step: both sectors are in flight together
         const int u0 = col_idx[e], u1 = col_idx[e + 1];
         if (u1 >= limit) {
-            if (u0 < limit) got |= load_word<CACHED>(&reached_g[u0]);
-            return got & todo;
+            if (u0 < limit) rec_or(got, load_rec(&reached_sg[u0]));
+            e = end;
+            break;
         }
-        got |= load_word<CACHED>(&reached_g[u0]) | load_word<CACHED>(&reached_g[u1]);
-        if ((got & todo) == todo) return todo;
+        const Rec r0 = load_rec(&reached_sg[u0]), r1 = load_rec(&reached_sg[u1]);
+        rec_or(got, r0);
+        rec_or(got, r1);
+        if (rec_covers(got, todo)) {
+            e = end;
+            break;
+        }
     }
     if (e < end) {
         const int u = col_idx[e];
-        if (u < limit) got |= load_word<CACHED>(&reached_g[u]);
+        if (u < limit) rec_or(got, load_rec(&reached_sg[u]));
     }
-    return got & todo;
+#pragma unroll
+    for (int i = 0; i < kPack; ++i) got.w[i] &= todo.w[i];
+    return got;
 }
 
-// Closes the first `prefix` vertices of every group inside one CTA: iterate ascending
+// Closes the first `prefix` vertices of every super-group inside one CTA: iterate ascending
 // passes until nothing changes.  With one CTA the in-flight window is 1024 vertices,
 // so a pass propagates almost like a sequential scan.
 __global__ void __launch_bounds__(kPrefixThreads) k_pc_prefix(const int32_t* __restrict__ row_ptr,
                                                               const int32_t* __restrict__ col_idx, int n, int prefix,
-                                                              const word_t* __restrict__ alive, word_t* reached) {
+                                                              const Rec* __restrict__ alive, Rec* reached) {
     const size_t base = static_cast<size_t>(blockIdx.x) * n;
-    const word_t* alive_g = alive + base;
-    word_t* reached_g = reached + base;
+    const Rec* alive_sg = alive + base;
+    Rec* reached_sg = reached + base;
     const int stages[2] = {min(prefix, 2 * kPrefixThreads), prefix};
     for (int s = 0; s < 2; ++s) {
         const int limit = stages[s];
@@ -231,12 +267,16 @@ __global__ void __launch_bounds__(kPrefixThreads) k_pc_prefix(const int32_t* __r
         for (int pass = 0; pass < 24; ++pass) {
             int any = 0;
             for (int v = threadIdx.x; v < limit; v += kPrefixThreads) {
-                const word_t mine = reached_g[v];
-                const word_t todo = alive_g[v] & ~mine;
-                if (!todo) continue;
-                const word_t got = gather_reached<false>(row_ptr, col_idx, reached_g, v, limit, todo);
-                if (got) {
-                    reached_g[v] = mine | got;
+                Rec mine = load_rec(&reached_sg[v]);
+                const Rec al = alive_sg[v];
+                Rec todo;
+#pragma unroll
+                for (int i = 0; i < kPack; ++i) todo.w[i] = al.w[i] & ~mine.w[i];
+                if (!rec_any(todo)) continue;
+                const Rec got = gather_reached(row_ptr, col_idx, reached_sg, v, limit, todo);
+                if (rec_any(got)) {
+                    rec_or(mine, got);
+                    store_rec(&reached_sg[v], mine);
                     any = 1;
                 }
             }
@@ -245,68 +285,80 @@ __global__ void __launch_bounds__(kPrefixThreads) k_pc_prefix(const int32_t* __r
     }
 }
 
-// Full sweep, one thread per (vertex, group); `interleave` groups share blockIdx.x so
-// that blocks are scheduled in ascending vertex order with a small window per group.
-// FINAL additionally records what is still unreached: per-individual counts and the
+// Full sweep, one thread per (vertex, super-group); `interleave` super-groups share
+// blockIdx.x so that blocks are scheduled in ascending vertex order with a small window per
+// group.  FINAL additionally records what is still unreached: per-individual counts and the
 // compacted non-isolated leftovers for phase 2.
-template <bool FINAL, bool CACHED>
+template <bool FINAL>
 __global__ void __launch_bounds__(kThreads) k_pc_sweep(const int32_t* __restrict__ row_ptr,
-                                                       const int32_t* __restrict__ col_idx, int n, int groups,
-                                                       int interleave, const word_t* __restrict__ alive, word_t* reached,
+                                                       const int32_t* __restrict__ col_idx, int n, int sgroups,
+                                                       int interleave, const Rec* __restrict__ alive, Rec* reached,
                                                        int* unreached, int32_t* entry_of, int32_t* left_v, int32_t* left_g,
                                                        word_t* left_w, int32_t* left_base, int32_t* parent,
                                                        int32_t* comp_size, unsigned cap_entries, unsigned cap_slots,
                                                        int slot0, PcCounters* counters) {
-    __shared__ int hist[kBits];
-    const int g = blockIdx.y * interleave + (blockIdx.x % interleave);
-    if (g >= groups) return;
+    __shared__ int hist[kPack * kBits];
+    const int sg = blockIdx.y * interleave + (blockIdx.x % interleave);
+    if (sg >= sgroups) return;
     const int v = (blockIdx.x / interleave) * kThreads + threadIdx.x;
     if (FINAL) {
-        if (threadIdx.x < kBits) hist[threadIdx.x] = 0;
+        hist[threadIdx.x] = 0;  // kThreads == kPack * kBits
         __syncthreads();
     }
     int any = 0, any_left = 0;
     if (v < n) {
-        const size_t base = static_cast<size_t>(g) * n;
-        const word_t mine = reached[base + v];
-        const word_t todo = alive[base + v] & ~mine;
-        if (todo) {
-            const word_t got = gather_reached<CACHED>(row_ptr, col_idx, reached + base, v, n, todo);
-            if (got) {
-                reached[base + v] = mine | got;
+        const size_t base = static_cast<size_t>(sg) * n;
+        Rec mine = load_rec(&reached[base + v]);
+        const Rec al = alive[base + v];
+        Rec todo;
+#pragma unroll
+        for (int i = 0; i < kPack; ++i) todo.w[i] = al.w[i] & ~mine.w[i];
+        if (rec_any(todo)) {
+            const Rec got = gather_reached(row_ptr, col_idx, reached + base, v, n, todo);
+            if (rec_any(got)) {
+                rec_or(mine, got);
+                store_rec(&reached[base + v], mine);
                 any = 1;
             }
             if (FINAL) {
-                word_t rest = todo & ~got;
-                if (rest) {
+                Rec rest;
+#pragma unroll
+                for (int i = 0; i < kPack; ++i) rest.w[i] = todo.w[i] & ~got.w[i];
+                if (rec_any(rest)) {
                     any_left = 1;
-                    word_t z = rest;
-                    while (z) {
-                        const int b = __ffsll(static_cast<long long>(z)) - 1;
-                        z &= z - 1;
-                        atomicAdd(&hist[b], 1);
+#pragma unroll
+                    for (int i = 0; i < kPack; ++i) {
+                        word_t z = rest.w[i];
+                        while (z) {
+                            const int b = __ffsll(static_cast<long long>(z)) - 1;
+                            z &= z - 1;
+                            atomicAdd(&hist[i * kBits + b], 1);
+                        }
                     }
                     // keep only the individuals in which v has an alive neighbour
-                    word_t nb = 0ull;
-                    for (int e = row_ptr[v]; e < row_ptr[v + 1] && (nb & rest) != rest; ++e) nb |= alive[base + col_idx[e]];
-                    rest &= nb;
-                }
-                if (rest) {
-                    const int cnt = __popcll(rest);
-                    const unsigned e = atomicAdd(&counters->n_entries, 1u);
-                    const unsigned s = atomicAdd(&counters->n_slots, static_cast<unsigned>(cnt));
-                    if (e < cap_entries && s + cnt <= cap_slots) {
-                        left_v[e] = v;
-                        left_g[e] = g;
-                        left_w[e] = rest;
-                        left_base[e] = static_cast<int32_t>(s);
-                        entry_of[base + v] = static_cast<int32_t>(e);
-                        for (int i = 0; i < cnt; ++i) {
-                            parent[slot0 + s + i] = slot0 + static_cast<int32_t>(s) + i;
-                            comp_size[slot0 + s + i] = 0;
+                    Rec nb{};
+                    for (int e = row_ptr[v]; e < row_ptr[v + 1] && !rec_covers(nb, rest); ++e) rec_or(nb, alive[base + col_idx[e]]);
+#pragma unroll
+                    for (int i = 0; i < kPack; ++i) {
+                        const word_t w = rest.w[i] & nb.w[i];
+                        if (!w) continue;
+                        const int g = sg * kPack + i;
+                        const int cnt = __popcll(w);
+                        const unsigned e = atomicAdd(&counters->n_entries, 1u);
+                        const unsigned s = atomicAdd(&counters->n_slots, static_cast<unsigned>(cnt));
+                        if (e < cap_entries && s + cnt <= cap_slots) {
+                            left_v[e] = v;
+                            left_g[e] = g;
+                            left_w[e] = w;
+                            left_base[e] = static_cast<int32_t>(s);
+                            entry_of[(base + v) * kPack + i] = static_cast<int32_t>(e);
+                            for (int t = 0; t < cnt; ++t) {
+                                parent[slot0 + s + t] = slot0 + static_cast<int32_t>(s) + t;
+                                comp_size[slot0 + s + t] = 0;
+                            }
+                        } else {
+                            counters->overflow = 1;
                         }
-                    } else {
-                        counters->overflow = 1;
                     }
                 }
             }
@@ -314,8 +366,8 @@ __global__ void __launch_bounds__(kThreads) k_pc_sweep(const int32_t* __restrict
     }
     if (__syncthreads_or(any) && threadIdx.x == 0) counters->changed = 1;
     if (FINAL) {
-        if (__syncthreads_or(any_left) && threadIdx.x < kBits && hist[threadIdx.x])
-            atomicAdd(&unreached[g * kBits + threadIdx.x], hist[threadIdx.x]);
+        if (__syncthreads_or(any_left) && hist[threadIdx.x])
+            atomicAdd(&unreached[sg * kPack * kBits + threadIdx.x], hist[threadIdx.x]);
     }
 }
 
@@ -361,12 +413,12 @@ __global__ void __launch_bounds__(kThreads) k_pc_hook(const int32_t* __restrict_
     for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
         const int v = left_v[e], g = left_g[e], base_v = left_base[e];
         const word_t w = left_w[e];
-        const size_t base = static_cast<size_t>(g) * n;
         for (int i = row_ptr[v]; i < row_ptr[v + 1]; ++i) {
             const int u = col_idx[i];
-            const word_t common = w & alive[base + u];
+            const size_t iu = word_index(g, n, u);
+            const word_t common = w & alive[iu];
             if (!common) continue;
-            const word_t ru = reached[base + u];
+            const word_t ru = reached[iu];
             word_t attach = common & ru;  // v was not reached but its neighbour was: v belongs to the giant
             while (attach) {
                 const int b = __ffsll(static_cast<long long>(attach)) - 1;
@@ -375,7 +427,7 @@ __global__ void __launch_bounds__(kThreads) k_pc_hook(const int32_t* __restrict_
             }
             word_t rest = common & ~ru;
             if (rest && u < v) {  // leftover-leftover edges are seen from both ends; take one
-                const int eu = entry_of[base + u];
+                const int eu = entry_of[iu];
                 const word_t wu = left_w[eu];
                 const int base_u = left_base[eu];
                 while (rest) {
@@ -494,7 +546,6 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
         s->prefix = env_int("GAPA_PC_PREFIX", 32768, 0, 1 << 24);
         s->interleave = env_int("GAPA_PC_INTERLEAVE", 8, 1, 64);
         s->mask_chunks = env_int("GAPA_PC_MASK_CHUNKS", 1, 1, 64);
-        s->cached = env_int("GAPA_PC_L1", 1, 0, 1);
         // the shared-memory bitmap may use most of the SM (one CTA per individual)
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
@@ -515,32 +566,34 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
         const int groups = std::min(max_groups, all_groups - g0);
         const int row0 = g0 * kBits;
         const int crows = std::min(rows - row0, groups * kBits);
-        const size_t words = static_cast<size_t>(groups) * std::max(n, 1);
+        const int sgroups = (groups + kPack - 1) / kPack;  // 4 groups share one 32-byte vertex record
+        const int pgroups = sgroups * kPack;
+        const size_t words = static_cast<size_t>(pgroups) * std::max(n, 1);
         GAPA_TRY(s->removed.ensure(sizeof(word_t) * static_cast<size_t>(crows) * words_per_row));
-        GAPA_TRY(s->removed_count.ensure(sizeof(int) * groups * kBits));
+        GAPA_TRY(s->removed_count.ensure(sizeof(int) * pgroups * kBits));
         GAPA_TRY(s->alive.ensure(sizeof(word_t) * words));
         GAPA_TRY(s->reached.ensure(sizeof(word_t) * words));
         GAPA_TRY(s->entry_of.ensure(sizeof(int32_t) * words));
-        GAPA_TRY(s->unreached.ensure(sizeof(int) * groups * kBits));
-        GAPA_TRY(s->pc_extra.ensure(sizeof(unsigned long long) * groups * kBits));
-        GAPA_TRY(s->mcn_extra.ensure(sizeof(int) * groups * kBits));
+        GAPA_TRY(s->unreached.ensure(sizeof(int) * pgroups * kBits));
+        GAPA_TRY(s->pc_extra.ensure(sizeof(unsigned long long) * pgroups * kBits));
+        GAPA_TRY(s->mcn_extra.ensure(sizeof(int) * pgroups * kBits));
         GAPA_TRY(s->counters.ensure(sizeof(PcCounters)));
-        if (s->cap_entries == 0 || s->parent.cap < sizeof(int32_t) * (static_cast<size_t>(groups) * kBits + s->cap_slots))
-            GAPA_TRY(ensure_phase2(s, groups, std::max<size_t>(s->cap_entries, 1u << 16),
+        if (s->cap_entries == 0 || s->parent.cap < sizeof(int32_t) * (static_cast<size_t>(pgroups) * kBits + s->cap_slots))
+            GAPA_TRY(ensure_phase2(s, pgroups, std::max<size_t>(s->cap_entries, 1u << 16),
                                    std::max<size_t>(s->cap_slots, 1u << 20)));
         word_t* alive = s->alive.as<word_t>();
         word_t* reached = s->reached.as<word_t>();
         PcCounters* counters = s->counters.as<PcCounters>();
-        const int slot0 = groups * kBits;
-        const int reset_grid = std::max(1, (groups * kBits + kThreads - 1) / kThreads);
+        const int slot0 = pgroups * kBits;
+        const int reset_grid = std::max(1, (pgroups * kBits + kThreads - 1) / kThreads);
         auto reset = [&](int first) -> int {
-            GAPA_LAUNCH(k_pc_reset, reset_grid, kThreads, 0, stream, groups, s->parent.as<int32_t>(),
+            GAPA_LAUNCH(k_pc_reset, reset_grid, kThreads, 0, stream, pgroups, s->parent.as<int32_t>(),
                         s->comp_size.as<int32_t>(), s->unreached.as<int>(), s->pc_extra.as<unsigned long long>(),
                         s->mcn_extra.as<int>(), counters, first);
             return GAPA_CUDA_OK;
         };
         GAPA_TRY(reset(1));
-        GAPA_CUDA_TRY(cudaMemsetAsync(s->removed_count.ptr, 0, sizeof(int) * groups * kBits, stream));
+        GAPA_CUDA_TRY(cudaMemsetAsync(s->removed_count.ptr, 0, sizeof(int) * pgroups * kBits, stream));
 
         if (n > 0) {
             // ---- masks ------------------------------------------------------------------
@@ -548,34 +601,32 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
                         genes_dev + static_cast<size_t>(row0) * cols, cols, ctx->pool_identity ? nullptr : ctx->d_pool_map,
                         ctx->pool_size, n, chunk_bits, words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>(),
                         counters);
-            GAPA_LAUNCH(k_pc_transpose, dim3((words_per_row + kTransThreads - 1) / kTransThreads, groups), kTransThreads,
+            GAPA_LAUNCH(k_pc_transpose, dim3((words_per_row + kTransThreads - 1) / kTransThreads, pgroups), kTransThreads,
                         sizeof(word_t) * kBits * (kTransThreads + 1), stream, s->removed.as<word_t>(), words_per_row, n, crows, alive);
             GAPA_CUDA_TRY(cudaMemsetAsync(reached, 0, sizeof(word_t) * words, stream));
             GAPA_LAUNCH(k_pc_source, (crows * 32 + kThreads - 1) / kThreads, kThreads, 0, stream, ctx->d_by_degree, n,
                         crows, alive, reached);
 
             // ---- phase 1 ------------------------------------------------------------------
+            const Rec* alive_rec = reinterpret_cast<const Rec*>(alive);
+            Rec* reached_rec = reinterpret_cast<Rec*>(reached);
             const int prefix = std::min(s->prefix, n);
             if (prefix > 0)
-                GAPA_LAUNCH(k_pc_prefix, groups, kPrefixThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, prefix, alive,
-                            reached);
-            const int il = std::min(s->interleave, groups);
-            const dim3 grid(((n + kThreads - 1) / kThreads) * il, (groups + il - 1) / il);
+                GAPA_LAUNCH(k_pc_prefix, sgroups, kPrefixThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, prefix,
+                            alive_rec, reached_rec);
+            const int il = std::min(std::max(1, s->interleave / kPack), sgroups);
+            const dim3 grid(((n + kThreads - 1) / kThreads) * il, (sgroups + il - 1) / il);
             auto sweep = [&](bool final_pass) -> int {
                 if (final_pass)
-                    GAPA_LAUNCH((k_pc_sweep<true, false>), grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, groups, il,
-                                alive, reached, s->unreached.as<int>(), s->entry_of.as<int32_t>(), s->left_v.as<int32_t>(),
-                                s->left_g.as<int32_t>(), s->left_w.as<word_t>(), s->left_base.as<int32_t>(),
-                                s->parent.as<int32_t>(), s->comp_size.as<int32_t>(), static_cast<unsigned>(s->cap_entries),
-                                static_cast<unsigned>(s->cap_slots), slot0, counters);
-                else if (s->cached)
-                    GAPA_LAUNCH((k_pc_sweep<false, true>), grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, groups,
-                                il, alive, reached, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u,
-                                0u, slot0, counters);
+                    GAPA_LAUNCH(k_pc_sweep<true>, grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, sgroups, il,
+                                alive_rec, reached_rec, s->unreached.as<int>(), s->entry_of.as<int32_t>(),
+                                s->left_v.as<int32_t>(), s->left_g.as<int32_t>(), s->left_w.as<word_t>(),
+                                s->left_base.as<int32_t>(), s->parent.as<int32_t>(), s->comp_size.as<int32_t>(),
+                                static_cast<unsigned>(s->cap_entries), static_cast<unsigned>(s->cap_slots), slot0, counters);
                 else
-                    GAPA_LAUNCH((k_pc_sweep<false, false>), grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, groups,
-                                il, alive, reached, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, 0u,
-                                0u, slot0, counters);
+                    GAPA_LAUNCH(k_pc_sweep<false>, grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, sgroups, il,
+                                alive_rec, reached_rec, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
+                                0u, 0u, slot0, counters);
                 return GAPA_CUDA_OK;
             };
             // One ordinary sweep, then the recording sweep.  If a lot is still unreached AND the
@@ -594,7 +645,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
                 const bool keep_sweeping = h.changed && h.n_entries > many && round < 48;
                 if (!retry_bigger && !keep_sweeping) break;
                 if (retry_bigger)
-                    GAPA_TRY(ensure_phase2(s, groups, std::max<size_t>(s->cap_entries, static_cast<size_t>(h.n_entries) + 1024),
+                    GAPA_TRY(ensure_phase2(s, pgroups, std::max<size_t>(s->cap_entries, static_cast<size_t>(h.n_entries) + 1024),
                                            std::max<size_t>(s->cap_slots, static_cast<size_t>(h.n_slots) + 1024)));
                 GAPA_TRY(reset(0));
             }
