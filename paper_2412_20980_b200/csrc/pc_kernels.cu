@@ -37,7 +37,11 @@
 #include <algorithm>
 #include <cstdlib>
 
+#include <cooperative_groups.h>
+
 #include "internal.cuh"
+
+namespace cg = cooperative_groups;
 
 namespace gapa_b200 {
 
@@ -48,6 +52,7 @@ static constexpr int kThreads = 256;
 static constexpr int kMaskThreads = 1024;
 static constexpr int kTransThreads = 128;
 static constexpr int kPrefixThreads = 1024;
+static constexpr int kPrefixCluster = 8;  // CTAs per super-group in the prefix kernel (portable cluster size)
 static_assert(kThreads == 4 * 64, "the final sweep's histogram has one counter per thread");
 
 struct PcCounters {
@@ -59,7 +64,7 @@ struct PcCounters {
 };
 
 struct PcScratch {
-    DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters;
+    DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters, pass_flags, block_done;
     DevBuf left_v, left_g, left_w, left_base, parent, comp_size, pc_extra, mcn_extra;
     size_t cap_entries = 0, cap_slots = 0;
     int prefix = 32768, interleave = 8, mask_chunks = 1;
@@ -127,10 +132,11 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(const int32_t* __re
 // a[i] bit c (individual i, vertex c)  ->  a[c] bit i; alive = ~removed.  Rows past
 // the end of the batch read as "everything removed", which zeroes their bits.
 //
-// Vertex records: kPack = 4 groups (256 individuals) are stored side by side, one 32-byte
-// record per vertex — word gi of record (sg, v) belongs to group 4 sg + gi.  32 bytes is
-// exactly one memory sector, so the random neighbour read of the sweeps fetches 256
-// individuals of state per sector instead of 64.
+// `alive` is only ever read at a thread's own vertex (coalesced), so it stays group-major:
+// alive[g][v].  `reached` is what the sweeps read at RANDOM neighbours, so kPack = 4 groups
+// (256 individuals) are stored side by side, one 32-byte record per vertex — word gi of
+// record (sg, v) belongs to group 4 sg + gi.  32 bytes is exactly one memory sector: a
+// neighbour read fetches 256 individuals of state per sector instead of 64.
 __global__ void __launch_bounds__(kTransThreads) k_pc_transpose(const word_t* __restrict__ removed, int words_per_row,
                                                                 int n, int rows, word_t* __restrict__ alive) {
     word_t* tile = reinterpret_cast<word_t*>(pc_smem_bits);  // kBits x (kTransThreads + 1) words, padded against bank conflicts
@@ -159,12 +165,12 @@ __global__ void __launch_bounds__(kTransThreads) k_pc_transpose(const word_t* __
         for (int c = 0; c < kBits; ++c) tile[c * (kTransThreads + 1) + threadIdx.x] = ~a[c];
     }
     __syncthreads();
-    // write-out in vertex order: the block's tile is kTransThreads * 64 consecutive vertices
-    word_t* out = alive + (static_cast<size_t>(g / kPack) * n) * kPack + (g % kPack);
+    // coalesced write-out: the block's tile is kTransThreads * 64 consecutive vertices
+    word_t* out = alive + static_cast<size_t>(g) * n;
     const int v_base = vb0 * kBits;
     for (int idx = threadIdx.x; idx < kTransThreads * kBits; idx += kTransThreads) {
         const int v = v_base + idx;
-        if (v < n) out[static_cast<size_t>(v) * kPack] = tile[(idx & 63) * (kTransThreads + 1) + (idx >> 6)];
+        if (v < n) out[v] = tile[(idx & 63) * (kTransThreads + 1) + (idx >> 6)];
     }
 }
 
@@ -184,7 +190,7 @@ __global__ void __launch_bounds__(kThreads) k_pc_source(const int32_t* __restric
     const word_t bit = 1ull << (row & 63);
     for (int i = 0; i < n; i += 32) {
         const int v = i + lane < n ? by_degree[i + lane] : -1;
-        const bool ok = v >= 0 && (alive[word_index(g, n, v)] & bit);
+        const bool ok = v >= 0 && (alive[static_cast<size_t>(g) * n + v] & bit);
         const unsigned hit = __ballot_sync(0xffffffffu, ok);
         if (hit) {
             if (lane == __ffs(hit) - 1) atomicOr(&reached[word_index(g, n, v)], bit);
@@ -221,10 +227,24 @@ __device__ __forceinline__ void rec_or(Rec& a, const Rec& b) {
     for (int i = 0; i < kPack; ++i) a.w[i] |= b.w[i];
 }
 
+__device__ __forceinline__ Rec load_alive(const word_t* __restrict__ alive, int sg, int n, int v) {
+    Rec r;
+#pragma unroll
+    for (int i = 0; i < kPack; ++i) r.w[i] = alive[(static_cast<size_t>(sg) * kPack + i) * n + v];
+    return r;
+}
+
 // OR of the neighbours' reached records until `todo` is covered; returns got & todo.
+// `max_pairs` bounds the scan (hub rows are long); a truncated scan reports `truncated`.
 __device__ __forceinline__ Rec gather_reached(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
-                                              const Rec* reached_sg, int v, int limit, const Rec& todo) {
-    const int beg = row_ptr[v], end = row_ptr[v + 1];
+                                              const Rec* reached_sg, int v, int limit, const Rec& todo,
+                                              int max_pairs = 0x3fffffff, bool* truncated = nullptr) {
+    const int beg = row_ptr[v];
+    int end = row_ptr[v + 1];
+    if (end - beg > 2 * max_pairs) {
+        end = beg + 2 * max_pairs;
+        if (truncated) *truncated = true;
+    }
     Rec got{};
     int e = beg;
     for (; e + 1 < end; e += 2) {  // two neighbours per step: both sectors are in flight together
@@ -251,36 +271,50 @@ __device__ __forceinline__ Rec gather_reached(const int32_t* __restrict__ row_pt
     return got;
 }
 
-// Closes the first `prefix` vertices of every super-group inside one CTA: iterate ascending
-// passes until nothing changes.  With one CTA the in-flight window is 1024 vertices,
-// so a pass propagates almost like a sequential scan.
-__global__ void __launch_bounds__(kPrefixThreads) k_pc_prefix(const int32_t* __restrict__ row_ptr,
-                                                              const int32_t* __restrict__ col_idx, int n, int prefix,
-                                                              const Rec* __restrict__ alive, Rec* reached) {
-    const size_t base = static_cast<size_t>(blockIdx.x) * n;
-    const Rec* alive_sg = alive + base;
-    Rec* reached_sg = reached + base;
-    const int stages[2] = {min(prefix, 2 * kPrefixThreads), prefix};
+// Closes the first `prefix` vertices of every super-group inside one thread-block CLUSTER of
+// kPrefixCluster CTAs (8192 threads): iterate ascending passes until nothing changes, with
+// cluster-wide barriers between passes — no host round trip, no cooperative launch.  The
+// in-flight window is the cluster, so a pass propagates almost like a sequential scan.
+__global__ void __cluster_dims__(kPrefixCluster, 1, 1) __launch_bounds__(kPrefixThreads)
+    k_pc_prefix(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx, int n, int prefix,
+                const word_t* __restrict__ alive, Rec* reached, int* pass_flags) {
+    cg::cluster_group cluster = cg::this_cluster();
+    const int sg = blockIdx.x / kPrefixCluster;
+    const int lane_in_cluster = (blockIdx.x % kPrefixCluster) * kPrefixThreads + threadIdx.x;
+    constexpr int kStride = kPrefixCluster * kPrefixThreads;
+    Rec* reached_sg = reached + static_cast<size_t>(sg) * n;
+    int* flags = pass_flags + sg * 64;  // one flag per pass; zeroed by the host
+    const int stages[2] = {min(prefix, kStride / 4), prefix};
+    int pass_id = 0;
     for (int s = 0; s < 2; ++s) {
         const int limit = stages[s];
         if (s == 1 && limit == stages[0]) break;
-        for (int pass = 0; pass < 24; ++pass) {
+        for (int pass = 0; pass < 24; ++pass, ++pass_id) {
             int any = 0;
-            for (int v = threadIdx.x; v < limit; v += kPrefixThreads) {
+            for (int v = lane_in_cluster; v < limit; v += kStride) {
                 Rec mine = load_rec(&reached_sg[v]);
-                const Rec al = alive_sg[v];
+                const Rec al = load_alive(alive, sg, n, v);
                 Rec todo;
 #pragma unroll
                 for (int i = 0; i < kPack; ++i) todo.w[i] = al.w[i] & ~mine.w[i];
                 if (!rec_any(todo)) continue;
-                const Rec got = gather_reached(row_ptr, col_idx, reached_sg, v, limit, todo);
+                // Bounded scan: in the first passes an unreached hub would otherwise walk hundreds of
+                // still-unreached younger neighbours serially.  Exactness does not depend on this
+                // kernel (the sweeps and phase 2 finish), only the speed of what follows does.
+                bool cut = false;
+                const Rec got = gather_reached(row_ptr, col_idx, reached_sg, v, limit, todo, 12 + 4 * pass, &cut);
                 if (rec_any(got)) {
                     rec_or(mine, got);
                     store_rec(&reached_sg[v], mine);
                     any = 1;
+                } else if (cut) {
+                    any = 1;
                 }
             }
-            if (!__syncthreads_or(any)) break;
+            if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(&flags[pass_id], 1);
+            __threadfence();
+            cluster.sync();
+            if (!*reinterpret_cast<volatile int*>(&flags[pass_id])) break;
         }
     }
 }
@@ -292,14 +326,18 @@ __global__ void __launch_bounds__(kPrefixThreads) k_pc_prefix(const int32_t* __r
 template <bool FINAL>
 __global__ void __launch_bounds__(kThreads) k_pc_sweep(const int32_t* __restrict__ row_ptr,
                                                        const int32_t* __restrict__ col_idx, int n, int sgroups,
-                                                       int interleave, const Rec* __restrict__ alive, Rec* reached,
+                                                       int interleave, const word_t* __restrict__ alive, Rec* reached,
                                                        int* unreached, int32_t* entry_of, int32_t* left_v, int32_t* left_g,
                                                        word_t* left_w, int32_t* left_base, int32_t* parent,
                                                        int32_t* comp_size, unsigned cap_entries, unsigned cap_slots,
-                                                       int slot0, PcCounters* counters) {
+                                                       int slot0, PcCounters* counters, unsigned char* block_done) {
     __shared__ int hist[kPack * kBits];
     const int sg = blockIdx.y * interleave + (blockIdx.x % interleave);
     if (sg >= sgroups) return;
+    // block_done[sg][chunk] = every (vertex, individual) of the chunk is reached or removed; set by
+    // the ordinary sweep so that the recording sweep skips those chunks without touching HBM.
+    const size_t done_index = static_cast<size_t>(sg) * (gridDim.x / interleave) + blockIdx.x / interleave;
+    if (FINAL && block_done && block_done[done_index]) return;
     const int v = (blockIdx.x / interleave) * kThreads + threadIdx.x;
     if (FINAL) {
         hist[threadIdx.x] = 0;  // kThreads == kPack * kBits
@@ -309,7 +347,7 @@ __global__ void __launch_bounds__(kThreads) k_pc_sweep(const int32_t* __restrict
     if (v < n) {
         const size_t base = static_cast<size_t>(sg) * n;
         Rec mine = load_rec(&reached[base + v]);
-        const Rec al = alive[base + v];
+        const Rec al = load_alive(alive, sg, n, v);
         Rec todo;
 #pragma unroll
         for (int i = 0; i < kPack; ++i) todo.w[i] = al.w[i] & ~mine.w[i];
@@ -320,10 +358,11 @@ __global__ void __launch_bounds__(kThreads) k_pc_sweep(const int32_t* __restrict
                 store_rec(&reached[base + v], mine);
                 any = 1;
             }
-            if (FINAL) {
-                Rec rest;
+            Rec rest;
 #pragma unroll
-                for (int i = 0; i < kPack; ++i) rest.w[i] = todo.w[i] & ~got.w[i];
+            for (int i = 0; i < kPack; ++i) rest.w[i] = todo.w[i] & ~got.w[i];
+            if (!FINAL) any_left = rec_any(rest);
+            if (FINAL) {
                 if (rec_any(rest)) {
                     any_left = 1;
 #pragma unroll
@@ -337,7 +376,7 @@ __global__ void __launch_bounds__(kThreads) k_pc_sweep(const int32_t* __restrict
                     }
                     // keep only the individuals in which v has an alive neighbour
                     Rec nb{};
-                    for (int e = row_ptr[v]; e < row_ptr[v + 1] && !rec_covers(nb, rest); ++e) rec_or(nb, alive[base + col_idx[e]]);
+                    for (int e = row_ptr[v]; e < row_ptr[v + 1] && !rec_covers(nb, rest); ++e) rec_or(nb, load_alive(alive, sg, n, col_idx[e]));
 #pragma unroll
                     for (int i = 0; i < kPack; ++i) {
                         const word_t w = rest.w[i] & nb.w[i];
@@ -365,9 +404,11 @@ __global__ void __launch_bounds__(kThreads) k_pc_sweep(const int32_t* __restrict
         }
     }
     if (__syncthreads_or(any) && threadIdx.x == 0) counters->changed = 1;
+    const int left = __syncthreads_or(any_left);
     if (FINAL) {
-        if (__syncthreads_or(any_left) && hist[threadIdx.x])
-            atomicAdd(&unreached[sg * kPack * kBits + threadIdx.x], hist[threadIdx.x]);
+        if (left && hist[threadIdx.x]) atomicAdd(&unreached[sg * kPack * kBits + threadIdx.x], hist[threadIdx.x]);
+    } else if (threadIdx.x == 0) {
+        block_done[done_index] = left ? 0 : 1;
     }
 }
 
@@ -416,7 +457,7 @@ __global__ void __launch_bounds__(kThreads) k_pc_hook(const int32_t* __restrict_
         for (int i = row_ptr[v]; i < row_ptr[v + 1]; ++i) {
             const int u = col_idx[i];
             const size_t iu = word_index(g, n, u);
-            const word_t common = w & alive[iu];
+            const word_t common = w & alive[static_cast<size_t>(g) * n + u];
             if (!common) continue;
             const word_t ru = reached[iu];
             word_t attach = common & ru;  // v was not reached but its neighbour was: v belongs to the giant
@@ -608,35 +649,41 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
                         crows, alive, reached);
 
             // ---- phase 1 ------------------------------------------------------------------
-            const Rec* alive_rec = reinterpret_cast<const Rec*>(alive);
+            const word_t* alive_rec = alive;
             Rec* reached_rec = reinterpret_cast<Rec*>(reached);
             const int prefix = std::min(s->prefix, n);
-            if (prefix > 0)
-                GAPA_LAUNCH(k_pc_prefix, sgroups, kPrefixThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, prefix,
-                            alive_rec, reached_rec);
+            if (prefix > 0) {
+                GAPA_TRY(s->pass_flags.ensure(sizeof(int) * 64 * sgroups));
+                GAPA_CUDA_TRY(cudaMemsetAsync(s->pass_flags.ptr, 0, sizeof(int) * 64 * sgroups, stream));
+                GAPA_LAUNCH(k_pc_prefix, sgroups * kPrefixCluster, kPrefixThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n,
+                            prefix, alive_rec, reached_rec, s->pass_flags.as<int>());
+            }
             const int il = std::min(std::max(1, s->interleave / kPack), sgroups);
             const dim3 grid(((n + kThreads - 1) / kThreads) * il, (sgroups + il - 1) / il);
+            GAPA_TRY(s->block_done.ensure(static_cast<size_t>(sgroups) * ((n + kThreads - 1) / kThreads)));
+            unsigned char* block_done = s->block_done.as<unsigned char>();
             auto sweep = [&](bool final_pass) -> int {
                 if (final_pass)
                     GAPA_LAUNCH(k_pc_sweep<true>, grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, sgroups, il,
                                 alive_rec, reached_rec, s->unreached.as<int>(), s->entry_of.as<int32_t>(),
                                 s->left_v.as<int32_t>(), s->left_g.as<int32_t>(), s->left_w.as<word_t>(),
                                 s->left_base.as<int32_t>(), s->parent.as<int32_t>(), s->comp_size.as<int32_t>(),
-                                static_cast<unsigned>(s->cap_entries), static_cast<unsigned>(s->cap_slots), slot0, counters);
+                                static_cast<unsigned>(s->cap_entries), static_cast<unsigned>(s->cap_slots), slot0, counters, block_done);
                 else
                     GAPA_LAUNCH(k_pc_sweep<false>, grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, sgroups, il,
                                 alive_rec, reached_rec, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                0u, 0u, slot0, counters);
+                                0u, 0u, slot0, counters, block_done);
                 return GAPA_CUDA_OK;
             };
-            // One ordinary sweep, then the recording sweep.  If a lot is still unreached AND the
-            // sweeps were still making progress, sweep more before handing the rest to phase 2
-            // (which is exact for any leftover, just slower than sweeping when there is much of it).
+            // With the prefix closed, ONE ordered sweep reaches nearly everything on power-law graphs and
+            // marks the 256-vertex chunks that are complete; the recording sweep then only visits the
+            // few incomplete chunks, and phase 2 (exact for any leftover, attaching to the giant through
+            // reached neighbours) finishes.  If a lot is still unreached AND the sweeps were still
+            // making progress, sweep more before phase 2.
             const unsigned many = static_cast<unsigned>(std::max<size_t>(8192, words / 512));
             PcCounters h{};
             for (int round = 0;; ++round) {
-                GAPA_TRY(sweep(false));
-                if (round > 0) GAPA_TRY(sweep(false));
+                for (int i = 0; i < (round == 0 ? 1 : 2); ++i) GAPA_TRY(sweep(false));
                 GAPA_TRY(sweep(true));
                 GAPA_CUDA_TRY(cudaMemcpyAsync(&h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
                 GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
@@ -674,7 +721,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
 void pc_free(gapa_cuda_ctx* ctx) {
     if (!ctx->pc) return;
     PcScratch* s = ctx->pc;
-    for (DevBuf* b : {&s->removed, &s->removed_count, &s->alive, &s->reached, &s->entry_of, &s->unreached, &s->counters,
+    for (DevBuf* b : {&s->removed, &s->removed_count, &s->alive, &s->reached, &s->entry_of, &s->unreached, &s->counters, &s->pass_flags, &s->block_done,
                       &s->left_v, &s->left_g, &s->left_w, &s->left_base, &s->parent, &s->comp_size, &s->pc_extra,
                       &s->mcn_extra})
         b->release();
