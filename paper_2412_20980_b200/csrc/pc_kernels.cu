@@ -67,7 +67,7 @@ struct PcScratch {
     DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters, pass_flags, block_done;
     DevBuf left_v, left_g, left_w, left_base, parent, comp_size, pc_extra, mcn_extra;
     size_t cap_entries = 0, cap_slots = 0;
-    int prefix = 32768, interleave = 8, mask_chunks = 1;
+    int prefix = 32768, interleave = 8, mask_chunks = 1, small_path = 1;
     bool configured = false;
 };
 
@@ -559,6 +559,78 @@ __global__ void k_pc_reset(int groups, int32_t* parent, int32_t* comp_size, int*
 }
 
 // ---------------------------------------------------------------------------------
+// Small graphs (n <= kSmallMaxN): the bit-sliced pipeline is launch-latency-bound there, so one
+// CTA takes one individual through the whole reference algorithm in SHARED memory — removed
+// bitmap, lock-free union-find over the alive edges (edge list, coalesced), component sizes,
+// sum of s(s-1)/2 and max s — in a single kernel.  Same integers as the big path.
+static constexpr int kSmallMaxN = 16384;
+static constexpr int kSmallThreads = 128;
+
+__global__ void __launch_bounds__(kSmallThreads) k_pc_small(const int32_t* __restrict__ genes, int cols,
+                                                            const int32_t* __restrict__ pool_map, int pool_size, int n, int m,
+                                                            const int32_t* __restrict__ edge_u,
+                                                            const int32_t* __restrict__ edge_v, int task,
+                                                            double* __restrict__ out, PcCounters* counters) {
+    extern __shared__ int32_t small_smem[];
+    __shared__ long long warp_pairs[kSmallThreads / 32];
+    __shared__ int warp_best[kSmallThreads / 32];
+    const int tid = threadIdx.x, row = blockIdx.x;
+    int32_t* parent = small_smem;
+    int32_t* size = parent + n;
+    unsigned* gone = reinterpret_cast<unsigned*>(size + n);
+    const int gone_words = (n + 31) >> 5;
+    for (int w = tid; w < gone_words; w += kSmallThreads) gone[w] = 0u;
+    for (int v = tid; v < n; v += kSmallThreads) {
+        parent[v] = v;
+        size[v] = 0;
+    }
+    __syncthreads();
+    const int32_t* g = genes + static_cast<size_t>(row) * cols;
+    for (int j = tid; j < cols; j += kSmallThreads) {
+        const int gene = g[j];
+        if (gene < 0 || gene >= pool_size) {
+            counters->range_error = 1;
+            continue;
+        }
+        const int node = pool_map ? pool_map[gene] : gene;
+        atomicOr(&gone[node >> 5], 1u << (node & 31));
+    }
+    __syncthreads();
+    for (int e = tid; e < m; e += kSmallThreads) {
+        const int u = edge_u[e], v = edge_v[e];
+        if (((gone[u >> 5] >> (u & 31)) | (gone[v >> 5] >> (v & 31))) & 1u) continue;
+        uf_union(parent, u, v);
+    }
+    __syncthreads();
+    for (int v = tid; v < n; v += kSmallThreads)
+        if (!((gone[v >> 5] >> (v & 31)) & 1u)) atomicAdd(&size[uf_find(parent, v)], 1);
+    __syncthreads();
+    long long pairs = 0;
+    int best = n > 0 ? 1 : 0;  // removed vertices are singletons
+    for (int v = tid; v < n; v += kSmallThreads) {
+        const long long sz = size[v];
+        pairs += sz * (sz - 1) / 2;
+        best = max(best, static_cast<int>(sz));
+    }
+    for (int off = 16; off; off >>= 1) {
+        pairs += __shfl_down_sync(0xffffffffu, pairs, off);
+        best = max(best, __shfl_down_sync(0xffffffffu, best, off));
+    }
+    if ((tid & 31) == 0) {
+        warp_pairs[tid >> 5] = pairs;
+        warp_best[tid >> 5] = best;
+    }
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < kSmallThreads / 32; ++w) {
+            pairs += warp_pairs[w];
+            best = max(best, warp_best[w]);
+        }
+        out[row] = task == GAPA_TASK_PC ? static_cast<double>(pairs) : static_cast<double>(best);
+    }
+}
+
+// ---------------------------------------------------------------------------------
 static int ensure_phase2(PcScratch* s, int groups, size_t entries, size_t slots) {
     const size_t giant = static_cast<size_t>(groups) * kBits;
     GAPA_TRY(s->left_v.ensure(sizeof(int32_t) * entries));
@@ -587,6 +659,8 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
         s->prefix = env_int("GAPA_PC_PREFIX", 32768, 0, 1 << 24);
         s->interleave = env_int("GAPA_PC_INTERLEAVE", 8, 1, 64);
         s->mask_chunks = env_int("GAPA_PC_MASK_CHUNKS", 1, 1, 64);
+        s->small_path = env_int("GAPA_PC_SMALL", 1, 0, 1);  // 0 forces the bit-sliced pipeline on small graphs (tests)
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         // the shared-memory bitmap may use most of the SM (one CTA per individual)
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
@@ -594,6 +668,20 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
     }
     const int n = ctx->n;
     const int sm = ctx->sm_count;
+    if (n > 0 && n <= kSmallMaxN && s->small_path) {
+        const size_t smem = sizeof(int32_t) * (2 * static_cast<size_t>(n) + ((n + 31) >> 5) + 1);
+        GAPA_TRY(s->counters.ensure(sizeof(PcCounters)));
+        PcCounters* counters = s->counters.as<PcCounters>();
+        GAPA_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(PcCounters), stream));
+        GAPA_LAUNCH(k_pc_small, rows, kSmallThreads, smem, stream, genes_dev, cols,
+                    ctx->pool_identity ? nullptr : ctx->d_pool_map, ctx->pool_size, n, static_cast<int>(ctx->m), ctx->d_edge_u,
+                    ctx->d_edge_v, task, out_dev, counters);
+        PcCounters h{};
+        GAPA_CUDA_TRY(cudaMemcpyAsync(&h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
+        GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
+        if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
+        return GAPA_CUDA_OK;
+    }
     const int words_per_row = std::max(1, (n + 63) / 64);
     int chunk_bits = std::min(words_per_row * 64, 192 * 1024 * 8);  // <= 192 KB of shared memory
     if (s->mask_chunks > 1) chunk_bits = std::min(chunk_bits, ((words_per_row + s->mask_chunks - 1) / s->mask_chunks) * 64);

@@ -7,6 +7,14 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
+@pytest.fixture(params=["warp-per-individual", "bit-sliced"], autouse=True)
+def pc_path(request, monkeypatch):
+    """Every case runs through both PC implementations: the shared-memory warp kernel that small
+    graphs take by default, and the bit-sliced pipeline (forced here; the default above n = 16384)."""
+    monkeypatch.setenv("GAPA_PC_SMALL", "1" if request.param == "warp-per-individual" else "0")
+    return request.param
+
+
 def _objective(gp, graph, task):
     pool = gp.build_gene_pool(graph, gp.PoolKind.NodeRemoval)
     cls = gp.PairwiseConnectivityObjective if task == 0 else gp.SixDstObjective
