@@ -313,6 +313,14 @@ def run_gpu_arm(args, w):
                                  "(CUDA events on the launch stream). frac > 1 is possible by construction: 64 individuals share "
                                  "one pass over the CSR (bit-sliced), while §8(d) charges every individual its own pass."},
         }
+        if world == 1:
+            # the same generations through the in-library loop (gapa_cuda_run: no host round trip per
+            # operator) — what a C++ host gets from run_ga_cuda(); reported beside the stepwise driver
+            iters = max(args.steps, 5)
+            loop = gp.run_ga(gp.GAParams(pc=w["pc"], pm=w["pm"], pop_size=s, budget=k, iterations=iters, seed=1), pool, obj)
+            line["library_loop"] = {"generations_per_sec": iters / loop.total_wall_seconds, "iterations": iters,
+                                    "evals_per_sec": s * (iters + 1) / loop.total_wall_seconds,
+                                    "eval_ms_per_generation": 1e3 * loop.eval_seconds / (iters + 1)}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_reference_throughput(w, 12.0, host_threads())
         print(json.dumps(line), flush=True)

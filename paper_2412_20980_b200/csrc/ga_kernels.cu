@@ -7,6 +7,7 @@
 // state, any row partition gives the same result.
 #include <algorithm>
 #include <cmath>
+#include <map>
 
 #include "internal.cuh"
 
@@ -263,26 +264,39 @@ int launch_elitism(const int32_t* pop, const int32_t* m_pop, int s, int k, const
     return GAPA_CUDA_OK;
 }
 
-// Scratch for the *_device entry points (per call; these are not the hot loop —
-// gapa_cuda_run keeps its own persistent buffers).
+// Scratch for the *_device entry points: persistent per (host thread, device, stream), so a
+// generation loop driven from the host pays no cudaMalloc / cudaFree per operator.  Work on one
+// stream is ordered, which makes reuse of the buffers across consecutive calls safe.
 struct OpScratch {
     DevBuf a, b, c;
     int* status = nullptr;
+    int* h_status = nullptr;  // pinned
     int init(cudaStream_t st) {
         GAPA_TRY(c.ensure(sizeof(int)));
         status = c.as<int>();
+        if (!h_status) GAPA_CUDA_TRY(cudaMallocHost(&h_status, sizeof(int)));
         GAPA_CUDA_TRY(cudaMemsetAsync(status, 0, sizeof(int), st));
         return GAPA_CUDA_OK;
     }
     int check(cudaStream_t st, const char* what) {
-        int h = 0;
-        GAPA_CUDA_TRY(cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, st));
+        GAPA_CUDA_TRY(cudaMemcpyAsync(h_status, status, sizeof(int), cudaMemcpyDeviceToHost, st));
         GAPA_CUDA_TRY(cudaStreamSynchronize(st));
-        if (h == GAPA_CUDA_E_NAN) return fail(GAPA_CUDA_E_NAN, "%s", what);
+        if (*h_status == GAPA_CUDA_E_NAN) return fail(GAPA_CUDA_E_NAN, "%s", what);
         return GAPA_CUDA_OK;
     }
-    ~OpScratch() { a.release(); b.release(); c.release(); }
 };
+
+static OpScratch& op_scratch(cudaStream_t st) {
+    struct Key {
+        int device;
+        cudaStream_t stream;
+        bool operator<(const Key& o) const { return device != o.device ? device < o.device : stream < o.stream; }
+    };
+    static thread_local std::map<Key, OpScratch> pool;
+    int device = 0;
+    cudaGetDevice(&device);
+    return pool[Key{device, st}];
+}
 
 }  // namespace gapa_b200
 
@@ -328,7 +342,7 @@ int gapa_cuda_ga_select_device(const double* fitness_dev, int s, int minimize, u
                                int32_t* partner_dev, double* weights_dev, void* stream) {
     if (s < 1) return fail(GAPA_CUDA_E_INVALID, "roulette_select: empty population");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    OpScratch sc;
+    OpScratch& sc = op_scratch(st);
     GAPA_TRY(sc.init(st));
     GAPA_TRY(sc.a.ensure(sizeof(double) * s));
     GAPA_TRY(sc.b.ensure(sizeof(double) * s));
@@ -367,7 +381,7 @@ int gapa_cuda_ga_elitism_device(const int32_t* pop_dev, const int32_t* m_pop_dev
                                 void* stream) {
     if (s < 1) return fail(GAPA_CUDA_E_INVALID, "elitism: empty population");
     cudaStream_t st = static_cast<cudaStream_t>(stream);
-    OpScratch sc;
+    OpScratch& sc = op_scratch(st);
     GAPA_TRY(sc.init(st));
     GAPA_TRY(sc.a.ensure(sizeof(int32_t) * s));
     GAPA_TRY(launch_elitism(pop_dev, m_pop_dev, s, k, fit_dev, fit_m_dev, minimize, next_dev, next_fit_dev,

@@ -153,10 +153,13 @@ struct gapa_cuda_ctx {
 namespace gapa_b200 {
 
 // per-task evaluators: genes/out on the device, work enqueued on ctx->stream_for(stream)
+// `trusted` = the genes were produced by this library's own operators (always inside the pool),
+// so evaluators that need no other host decision skip the range-status readback and stay
+// asynchronous.
 int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, int cols, double* out_dev,
-            cudaStream_t stream);
+            cudaStream_t stream, bool trusted = false);
 int lpa_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, double* out_dev,
-             cudaStream_t stream);
+             cudaStream_t stream, bool trusted = false);
 int cda_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, double* out_dev,
              cudaStream_t stream);
 void pc_free(gapa_cuda_ctx* ctx);

@@ -652,7 +652,7 @@ static int env_int(const char* name, int fallback, int lo, int hi) {
 }
 
 int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, int cols, double* out_dev,
-            cudaStream_t stream) {
+            cudaStream_t stream, bool trusted) {
     if (!ctx->pc) ctx->pc = new PcScratch();
     PcScratch* s = ctx->pc;
     if (!s->configured) {  // tuning knobs (defaults are what bench.py measures)
@@ -676,6 +676,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
         GAPA_LAUNCH(k_pc_small, rows, kSmallThreads, smem, stream, genes_dev, cols,
                     ctx->pool_identity ? nullptr : ctx->d_pool_map, ctx->pool_size, n, static_cast<int>(ctx->m), ctx->d_edge_u,
                     ctx->d_edge_v, task, out_dev, counters);
+        if (trusted) return GAPA_CUDA_OK;
         PcCounters h{};
         GAPA_CUDA_TRY(cudaMemcpyAsync(&h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
         GAPA_CUDA_TRY(cudaStreamSynchronize(stream));

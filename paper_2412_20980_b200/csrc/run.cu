@@ -91,22 +91,40 @@ struct RunBuffers {
     }
 };
 
+// Evaluation of a row block inside the loop.  Timing uses one CUDA-event pair per call, read back
+// only when the run is over, so the loop itself never waits on the device for bookkeeping.
+struct EvalTimer {
+    std::vector<cudaEvent_t> events;
+    ~EvalTimer() { for (cudaEvent_t e : events) cudaEventDestroy(e); }
+    int mark(cudaStream_t st) {
+        cudaEvent_t e;
+        GAPA_CUDA_TRY(cudaEventCreate(&e));
+        events.push_back(e);
+        GAPA_CUDA_TRY(cudaEventRecord(e, st));
+        return GAPA_CUDA_OK;
+    }
+    int total_seconds(double* out) {
+        double ms_total = 0.0;
+        for (size_t i = 0; i + 1 < events.size(); i += 2) {
+            float ms = 0.f;
+            GAPA_CUDA_TRY(cudaEventElapsedTime(&ms, events[i], events[i + 1]));
+            ms_total += ms;
+        }
+        *out = ms_total * 1e-3;
+        return GAPA_CUDA_OK;
+    }
+};
+
 int eval_rows(gapa_cuda_ctx* ctx, int task, const int32_t* genes, int rows, int cols, double* out, cudaStream_t st,
-              double* seconds) {
+              EvalTimer* timer) {
     if (rows == 0) return GAPA_CUDA_OK;
-    GAPA_CUDA_TRY(cudaEventRecord(ctx->ev_start, st));
+    GAPA_TRY(timer->mark(st));
     int rc;
-    if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) rc = pc_eval(ctx, task, genes, rows, cols, out, st);
+    if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) rc = pc_eval(ctx, task, genes, rows, cols, out, st, true);
     else if (task == GAPA_TASK_CDA) rc = cda_eval(ctx, genes, rows, cols, out, st);
-    else rc = lpa_eval(ctx, genes, rows, cols, out, st);
+    else rc = lpa_eval(ctx, genes, rows, cols, out, st, true);
     GAPA_TRY(rc);
-    GAPA_CUDA_TRY(cudaEventRecord(ctx->ev_stop, st));
-    GAPA_CUDA_TRY(cudaEventSynchronize(ctx->ev_stop));
-    float ms = 0.f;
-    GAPA_CUDA_TRY(cudaEventElapsedTime(&ms, ctx->ev_start, ctx->ev_stop));
-    ctx->last_eval_ms = ms;
-    *seconds += ms * 1e-3;
-    return GAPA_CUDA_OK;
+    return timer->mark(st);
 }
 }  // namespace
 
@@ -179,10 +197,10 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
 
     result->fitness_batch_calls = 0;
     result->eval_seconds = 0.0;
+    EvalTimer timer;
     auto evaluate = [&](const int32_t* rows_all, double* fit_all) -> int {
         ++result->fitness_batch_calls;
-        GAPA_TRY(eval_rows(ctx, p->task, rows_all + static_cast<size_t>(lo) * k, hi - lo, k, fit_all + lo, st,
-                           &result->eval_seconds));
+        GAPA_TRY(eval_rows(ctx, p->task, rows_all + static_cast<size_t>(lo) * k, hi - lo, k, fit_all + lo, st, &timer));
         if (world > 1) {
             const int rc = exchange(exchange_user, fit_all, s, block, st);
             if (rc != 0) return fail(GAPA_CUDA_E_CUDA, "run: exchange hook failed with status %d", rc);
@@ -230,6 +248,7 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
         }
     }
     GAPA_CUDA_TRY(cudaStreamSynchronize(st));
+    GAPA_TRY(timer.total_seconds(&result->eval_seconds));
     result->total_wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 
     if (result->history_best) GAPA_CUDA_TRY(cudaMemcpy(result->history_best, hist, sizeof(double) * iters, cudaMemcpyDeviceToHost));
