@@ -31,6 +31,8 @@ namespace gapa_b200 {
 
 static constexpr int kCdaThreads = 1024;
 static constexpr int kCdaWarps = kCdaThreads / 32;
+static constexpr int kCdaShortList = 24;   // neighbour lists up to this length are patched by one thread
+static constexpr int kCdaLongQueue = 1024;  // longer ones are queued for a warp each
 
 struct CdaScratch {
     DevBuf gone, ints, doubles, e_id, e_cnt, e_gain, status;
@@ -95,11 +97,16 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, const int32_t
     __shared__ long long sh_pool_top;
     __shared__ int sh_len, sh_pb, sh_new_head, sh_abort, sh_count;
     __shared__ int sh_scan[kCdaThreads];
+    __shared__ int long_queue[kCdaLongQueue];
+    __shared__ int sh_long;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = A.n;
     const size_t slot = blockIdx.x;
     unsigned* gone = A.gone + slot * A.mask_words;
+    // pos_in_smem: 0 = everything in global scratch, 1 = position map in shared memory,
+    // 2 = position map AND the per-community arrays (degree, list head / length, cached best) in
+    // shared memory — every merge step chases these, so for n up to ~6000 they stay on chip.
     int32_t* cdeg = A.ints + slot * 6 * static_cast<size_t>(n);
     int32_t* head = cdeg + n;
     int32_t* len = head + n;
@@ -107,10 +114,17 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, const int32_t
     int32_t* merged_into = cap + n;
     int32_t* best_id = merged_into + n;
     double* best_gain = A.best_gain + slot * n;
+    if (pos_in_smem == 2) {
+        best_gain = reinterpret_cast<double*>(cda_smem);  // 8-byte aligned at the start of the carve-out
+        cdeg = cda_smem + 2 * static_cast<size_t>(n);
+        head = cdeg + n;
+        len = head + n;
+        best_id = len + n;
+    }
     int32_t* e_id = A.e_id + slot * A.pool_cap;
     int32_t* e_cnt = A.e_cnt + slot * A.pool_cap;
     double* e_gain = A.e_gain + slot * A.pool_cap;
-    int32_t* pos = pos_in_smem ? cda_smem : A.pos_global + slot * n;
+    int32_t* pos = pos_in_smem == 2 ? cda_smem + 6 * static_cast<size_t>(n) : (pos_in_smem ? cda_smem : A.pos_global + slot * n);
 
     for (int r = blockIdx.x; r < rows; r += gridDim.x) {
         // ---- perturbation: edge-removed bitmask (gene_pool.cpp:53-56) -----------------
@@ -249,15 +263,83 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, const int32_t
             __syncthreads();
             const int la2 = sh_len, da = cdeg[a];
 
-            // one warp per neighbour c of the merged community
+            // Patch the mirror entry of every neighbour c of the merged community and refresh c's
+            // cached best.  Short lists (the common case: the merged community is adjacent to many
+            // small ones) take one THREAD each, so ~1000 neighbours are patched concurrently; long
+            // lists are queued and taken by one WARP each.
             Cand best_a{0.0, a, -1};
-            for (int i = warp; i < la2; i += kCdaWarps) {
+            if (tid == 0) sh_long = 0;
+            __syncthreads();
+            for (int i = tid; i < la2; i += kCdaThreads) {
                 const int c = e_id[ha + i], e = e_cnt[ha + i];
                 const double gn = merge_gain(e, da, cdeg[c], m, den);
+                e_gain[ha + i] = gn;
                 if (c > a && gn > 0.0) {
                     const Cand x{gn, a, c};
                     if (cand_better(x, best_a)) best_a = x;
                 }
+                const int hc = head[c];
+                int lc = len[c];
+                if (lc > kCdaShortList) {
+                    const int q = atomicAdd(&sh_long, 1);
+                    if (q < kCdaLongQueue) { long_queue[q] = i; continue; }
+                }
+                int pa = -1, pbb = -1;
+                for (int t0 = 0; t0 < lc; t0 += 8) {  // 8 independent loads in flight per step
+                    int ids[8];
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) ids[u] = t0 + u < lc ? e_id[hc + t0 + u] : -1;
+#pragma unroll
+                    for (int u = 0; u < 8; ++u) {
+                        if (ids[u] == a) pa = t0 + u;
+                        if (ids[u] == b) pbb = t0 + u;
+                    }
+                }
+                if (pa >= 0) {
+                    if (pbb >= 0) {
+                        const int last = lc - 1;
+                        if (pbb != last) {
+                            e_id[hc + pbb] = e_id[hc + last];
+                            e_cnt[hc + pbb] = e_cnt[hc + last];
+                            e_gain[hc + pbb] = e_gain[hc + last];
+                            if (pa == last) pa = pbb;
+                        }
+                        lc = last;
+                        len[c] = lc;
+                    }
+                    e_cnt[hc + pa] = e;
+                    e_gain[hc + pa] = gn;
+                } else {
+                    e_id[hc + pbb] = a;
+                    e_cnt[hc + pbb] = e;
+                    e_gain[hc + pbb] = gn;
+                }
+                Cand best_c{0.0, c, -1};
+                for (int t0 = 0; t0 < lc; t0 += 4) {
+                    int ids[4];
+                    double gs[4];
+#pragma unroll
+                    for (int u = 0; u < 4; ++u) {
+                        const bool in = t0 + u < lc;
+                        ids[u] = in ? e_id[hc + t0 + u] : -1;
+                        gs[u] = in ? e_gain[hc + t0 + u] : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (ids[u] > c && gs[u] > 0.0) {
+                            const Cand x{gs[u], c, ids[u]};
+                            if (cand_better(x, best_c)) best_c = x;
+                        }
+                }
+                best_gain[c] = best_c.gain;
+                best_id[c] = best_c.b;
+            }
+            __syncthreads();
+            const int n_long = min(sh_long, kCdaLongQueue);
+            for (int q = warp; q < n_long; q += kCdaWarps) {
+                const int i = long_queue[q];
+                const int c = e_id[ha + i], e = e_cnt[ha + i];
+                const double gn = e_gain[ha + i];
                 const int hc = head[c];
                 int lc = len[c];
                 int pa = -1, pbb = -1;
@@ -269,7 +351,6 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, const int32_t
                 pa = __reduce_max_sync(0xffffffffu, pa);
                 pbb = __reduce_max_sync(0xffffffffu, pbb);
                 if (lane == 0) {
-                    e_gain[ha + i] = gn;
                     if (pa >= 0) {
                         if (pbb >= 0) {
                             const int last = lc - 1;
@@ -304,7 +385,8 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, const int32_t
                 best_c = cand_warp_best(best_c);
                 if (lane == 0) { best_gain[c] = best_c.gain; best_id[c] = best_c.b; }
             }
-            if (lane == 0) warp_cand[warp] = best_a;  // identical in every lane of the warp
+            best_a = cand_warp_best(best_a);
+            if (lane == 0) warp_cand[warp] = best_a;
             __syncthreads();
             if (warp == 0) {
                 Cand x = warp_cand[lane];
@@ -366,7 +448,7 @@ int cda_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, d
     const long long csr_slots = 2 * ctx->m;
     const int mask_words = static_cast<int>((ctx->m + 31) / 32) + 1;
     const int slots = std::max(1, std::min(rows, ctx->sm_count));
-    const bool pos_in_smem = static_cast<size_t>(n) * sizeof(int32_t) <= 160 * 1024;
+    const int pos_in_smem = static_cast<size_t>(n) * 7 * sizeof(int32_t) <= 200 * 1024 ? 2 : (static_cast<size_t>(n) * sizeof(int32_t) <= 160 * 1024 ? 1 : 0);
     if (s->pool_cap == 0) s->pool_cap = static_cast<size_t>(csr_slots) * 6 + 4096;
 
     for (;;) {
@@ -397,9 +479,9 @@ int cda_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, d
         A.e_cnt = s->e_cnt.as<int32_t>();
         A.e_gain = s->e_gain.as<double>();
         A.status = s->status.as<int>();
-        const size_t smem = pos_in_smem ? static_cast<size_t>(n) * sizeof(int32_t) : 0;
+        const size_t smem = pos_in_smem == 2 ? static_cast<size_t>(n) * 7 * sizeof(int32_t) : (pos_in_smem ? static_cast<size_t>(n) * sizeof(int32_t) : 0);
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_cda, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        GAPA_LAUNCH(k_cda, slots, kCdaThreads, smem, stream, A, genes_dev, rows, cols, pos_in_smem ? 1 : 0, out_dev);
+        GAPA_LAUNCH(k_cda, slots, kCdaThreads, smem, stream, A, genes_dev, rows, cols, pos_in_smem, out_dev);
         GAPA_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, s->status.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
         GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
         if (ctx->h_status[0] == GAPA_CUDA_E_RANGE) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
