@@ -46,8 +46,8 @@ def build(force: bool = False, verbose: bool = False) -> str:
     for src in SOURCES:
         obj = os.path.join(PKG, "build", src.replace(".cu", ".o"))
         objs.append(obj)
-        cmd = [nvcc(), *NVCC_FLAGS, "-I", os.path.join(REPO, "include"), "-I", CSRC, "-c", os.path.join(CSRC, src),
-               "-o", obj]
+        cmd = [nvcc(), *NVCC_FLAGS, *os.environ.get("GAPA_NVCC_EXTRA", "").split(), "-I", os.path.join(REPO, "include"),
+               "-I", CSRC, "-c", os.path.join(CSRC, src), "-o", obj]
         if verbose:
             cmd.insert(1, "-Xptxas=-v")
         procs.append((src, subprocess.Popen(cmd, stdout=subprocess.PIPE, stderr=subprocess.STDOUT, text=True)))

@@ -323,8 +323,11 @@ __global__ void __cluster_dims__(kPrefixCluster, 1, 1) __launch_bounds__(kPrefix
 // blockIdx.x so that blocks are scheduled in ascending vertex order with a small window per
 // group.  FINAL additionally records what is still unreached: per-individual counts and the
 // compacted non-isolated leftovers for phase 2.
+#ifndef GAPA_SWEEP_MIN_BLOCKS
+#define GAPA_SWEEP_MIN_BLOCKS 4
+#endif
 template <bool FINAL>
-__global__ void __launch_bounds__(kThreads) k_pc_sweep(const int32_t* __restrict__ row_ptr,
+__global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep(const int32_t* __restrict__ row_ptr,
                                                        const int32_t* __restrict__ col_idx, int n, int sgroups,
                                                        int interleave, const word_t* __restrict__ alive, Rec* reached,
                                                        int* unreached, int32_t* entry_of, int32_t* left_v, int32_t* left_g,
