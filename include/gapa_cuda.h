@@ -132,6 +132,18 @@ int gapa_cuda_ga_elitism_device(const int32_t* pop_dev, const int32_t* m_pop_dev
                                 const double* fit_dev, const double* fit_m_dev, int minimize,
                                 int32_t* next_dev, double* next_fit_dev, void* stream);
 
+/* elitism for a row-sharded generation (the GPU form of M mode, modes.cpp:190-349): this rank built
+ * only rows [block_lo, block_hi) of M_POP (m_block_dev, block_hi - block_lo rows); surviving mutated
+ * rows of other ranks are recomputed from the replicated parents and the keyed streams instead of
+ * being fetched — crossover+mutate when partner_dev != NULL, eda_sample+mutate (elite = the whole
+ * population, add-one smoothing; modes.cpp:167-168) when it is NULL.  Result == gapa_cuda_ga_elitism_device
+ * on the full M_POP. */
+int gapa_cuda_ga_elitism_sharded_device(const int32_t* pop_dev, const int32_t* m_block_dev, int block_lo, int block_hi,
+                                        const int32_t* partner_dev, int s, int k, const double* fit_dev,
+                                        const double* fit_m_dev, int minimize, double pc, double pm,
+                                        int32_t pool_size, uint64_t seed, uint64_t generation, int32_t* next_dev,
+                                        double* next_fit_dev, void* stream);
+
 /* record_generation (modes.cpp:35-43): best_dev[0] = fit[0], mean_dev[0] = sequential
  * sum(fit) / s — the reference's std::accumulate order, so non-integer fitness means
  * are bit-identical. */

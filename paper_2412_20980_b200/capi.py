@@ -64,6 +64,8 @@ SIGNATURES = {
     "gapa_cuda_ga_eda_device": (C.c_int, [VP, C.c_int, C.c_int, C.c_int, C.c_int32, C.c_uint64, C.c_uint64, C.c_int,
                                           VP, VP]),
     "gapa_cuda_ga_elitism_device": (C.c_int, [VP, VP, C.c_int, C.c_int, VP, VP, C.c_int, VP, VP, VP]),
+    "gapa_cuda_ga_elitism_sharded_device": (C.c_int, [VP, VP, C.c_int, C.c_int, VP, C.c_int, C.c_int, VP, VP, C.c_int,
+                                                      C.c_double, C.c_double, C.c_int32, C.c_uint64, C.c_uint64, VP, VP, VP]),
     "gapa_cuda_ga_stats_device": (C.c_int, [VP, C.c_int, VP, VP, VP]),
     "gapa_cuda_ga_init": (C.c_int, [C.c_int, C.c_int32, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, VP]),
     "gapa_cuda_ga_selection_weights": (C.c_int, [C.c_int, VP, C.c_int, C.c_int, VP]),

@@ -73,14 +73,14 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_mutate(const int32_t* __restr
 
 // ---- eda_sample (ga_ops.cpp:214-238) ----------------------------------------------------------
 __global__ void __launch_bounds__(kGaThreads) k_ga_eda(const int32_t* __restrict__ elite, int k, uint32_t elite_count,
-                                                       uint32_t bound, uint64_t seed, uint64_t generation,
+                                                       uint32_t bound, int row_first, uint64_t seed, uint64_t generation,
                                                        int32_t* __restrict__ out) {
     __shared__ uint64_t key;
-    const int row = blockIdx.y;
+    const int row = row_first + blockIdx.y;  // out holds rows [row_first, row_first + gridDim.y)
     if (threadIdx.x == 0) key = stream_key(seed, generation, GAPA_ROLE_SELECT, static_cast<uint64_t>(row));
     __syncthreads();
     const uint64_t kk = key;
-    int32_t* dst = out + static_cast<size_t>(row) * k;
+    int32_t* dst = out + static_cast<size_t>(blockIdx.y) * k;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
         const uint32_t v = draw_index(kk, static_cast<uint64_t>(j) + 1, bound);
         dst[j] = v < elite_count ? elite[static_cast<size_t>(v) * k + j] : static_cast<int32_t>(v - elite_count);
@@ -248,11 +248,11 @@ int launch_mutate(const int32_t* block, int rows, int k, int row_offset, double 
                 seed, generation, out);
     return GAPA_CUDA_OK;
 }
-int launch_eda(const int32_t* elite, int s, int k, int elite_count, uint32_t bound, uint64_t seed, uint64_t generation,
-               int32_t* out, cudaStream_t st) {
-    if (s == 0 || k == 0) return GAPA_CUDA_OK;
-    GAPA_LAUNCH(k_ga_eda, row_grid(k, s), kGaThreads, 0, st, elite, k, static_cast<uint32_t>(elite_count), bound, seed,
-                generation, out);
+int launch_eda(const int32_t* elite, int row_first, int row_count, int k, int elite_count, uint32_t bound, uint64_t seed,
+               uint64_t generation, int32_t* out, cudaStream_t st) {
+    if (row_count == 0 || k == 0) return GAPA_CUDA_OK;
+    GAPA_LAUNCH(k_ga_eda, row_grid(k, row_count), kGaThreads, 0, st, elite, k, static_cast<uint32_t>(elite_count), bound,
+                row_first, seed, generation, out);
     return GAPA_CUDA_OK;
 }
 int launch_elitism(const int32_t* pop, const int32_t* m_pop, int s, int k, const double* fit, const double* fit_m,
@@ -261,6 +261,71 @@ int launch_elitism(const int32_t* pop, const int32_t* m_pop, int s, int k, const
                 src_of_rank, status);
     GAPA_LAUNCH(k_ga_elite_gather, row_grid(std::max(k, 1), s), kGaThreads, 0, st, pop, m_pop, fit, fit_m, s, k, src_of_rank,
                 next, next_fit);
+    return GAPA_CUDA_OK;
+}
+
+// ---- elitism for a row-sharded generation --------------------------------------------------------------
+// Under sharding every rank keeps the whole population but builds only ITS block of M_POP (the rows
+// it evaluates).  A surviving mutated row that another rank built is not fetched over NVLink: it is
+// RECOMPUTED here from the replicated parent population and the keyed streams — crossover + mutate
+// (or eda_sample + mutate on EDA generations) are pure functions of (pop, partner, seed,
+// generation, global row), so the recomputed row is bit-identical to the one the owner evaluated.
+// Genomes therefore never cross the interconnect; the only exchange stays the fitness all-gather.
+__global__ void __launch_bounds__(kGaThreads) k_ga_elite_gather_sharded(
+    const int32_t* __restrict__ pop, const int32_t* __restrict__ m_block, int block_lo, int block_hi,
+    const int32_t* __restrict__ partner, const double* __restrict__ fit, const double* __restrict__ fit_m, int s, int k,
+    uint64_t pc_thr, uint64_t pm_thr, uint32_t pool_size, uint64_t seed, uint64_t generation,
+    const int32_t* __restrict__ src_of_rank, int32_t* __restrict__ next, double* __restrict__ next_fit) {
+    __shared__ uint64_t keys[4];
+    const int r = blockIdx.y;
+    const int src = src_of_rank[r];
+    int32_t* to = next + static_cast<size_t>(r) * k;
+    if (blockIdx.x == 0 && threadIdx.x == 0) next_fit[r] = src < s ? fit[src] : fit_m[src - s];
+    const int row = src - s;  // row of M_POP when src >= s
+    if (src < s || (row >= block_lo && row < block_hi)) {
+        const int32_t* from = src < s ? pop + static_cast<size_t>(src) * k : m_block + static_cast<size_t>(row - block_lo) * k;
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) to[j] = from[j];
+        return;
+    }
+    // foreign mutated row: rebuild it
+    if (threadIdx.x < 4)
+        keys[threadIdx.x] = stream_key(seed, generation, GAPA_ROLE_SELECT + threadIdx.x, static_cast<uint64_t>(row));
+    __syncthreads();
+    const uint64_t ks = keys[0], kc = keys[1], km = keys[2], ki = keys[3];
+    const int32_t* mine = pop + static_cast<size_t>(row) * k;
+    if (partner) {  // crossover + mutate, ga_ops.cpp:130-178
+        const int32_t* theirs = pop + static_cast<size_t>(partner[row]) * k;
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+            const uint64_t d = static_cast<uint64_t>(j) + 1;
+            int32_t g;
+            if (draw_bernoulli(km, d, pm_thr)) g = static_cast<int32_t>(draw_index(ki, d, pool_size));
+            else g = draw_bernoulli(kc, d, pc_thr) ? theirs[j] : mine[j];
+            to[j] = g;
+        }
+    } else {  // eda_sample(elite = whole population, smoothing) + mutate, modes.cpp:167-168, ga_ops.cpp:214-238
+        const uint32_t elite = static_cast<uint32_t>(s), bound = elite + pool_size;
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+            const uint64_t d = static_cast<uint64_t>(j) + 1;
+            int32_t g;
+            if (draw_bernoulli(km, d, pm_thr)) g = static_cast<int32_t>(draw_index(ki, d, pool_size));
+            else {
+                const uint32_t v = draw_index(ks, d, bound);
+                g = v < elite ? pop[static_cast<size_t>(v) * k + j] : static_cast<int32_t>(v - elite);
+            }
+            to[j] = g;
+        }
+    }
+}
+
+int launch_elitism_sharded(const int32_t* pop, const int32_t* m_block, int block_lo, int block_hi, const int32_t* partner,
+                           int s, int k, const double* fit, const double* fit_m, int minimize, double pc, double pm,
+                           uint32_t pool_size, uint64_t seed, uint64_t generation, int32_t* next, double* next_fit,
+                           int32_t* src_of_rank, int* status, cudaStream_t st) {
+    GAPA_LAUNCH(k_ga_elite_rank, (2 * s + kPerBlock - 1) / kPerBlock, kGaThreads, 0, st, fit, fit_m, s, minimize,
+                src_of_rank, status);
+    GAPA_LAUNCH(k_ga_elite_gather_sharded, row_grid(std::max(k, 1), s), kGaThreads, 0, st, pop, m_block, block_lo, block_hi,
+                partner, fit, fit_m, s, k, bernoulli_threshold(pc), bernoulli_threshold(pm), pool_size, seed, generation,
+                src_of_rank, next, next_fit);
     return GAPA_CUDA_OK;
 }
 
@@ -373,7 +438,7 @@ int gapa_cuda_ga_eda_device(const int32_t* elite_dev, int s, int k, int elite_co
                             uint64_t generation, int smoothing, int32_t* out_dev, void* stream) {
     if (elite_count < 1 || elite_count > s) return fail(GAPA_CUDA_E_INVALID, "eda_sample: invalid elite count");
     const uint32_t bound = static_cast<uint32_t>(smoothing ? elite_count + pool_size : elite_count);
-    return launch_eda(elite_dev, s, k, elite_count, bound, seed, generation, out_dev, static_cast<cudaStream_t>(stream));
+    return launch_eda(elite_dev, 0, s, k, elite_count, bound, seed, generation, out_dev, static_cast<cudaStream_t>(stream));
 }
 
 int gapa_cuda_ga_elitism_device(const int32_t* pop_dev, const int32_t* m_pop_dev, int s, int k, const double* fit_dev,
@@ -389,6 +454,25 @@ int gapa_cuda_ga_elitism_device(const int32_t* pop_dev, const int32_t* m_pop_dev
     return sc.check(st, "elitism: NaN fitness");
 }
 
+
+int gapa_cuda_ga_elitism_sharded_device(const int32_t* pop_dev, const int32_t* m_block_dev, int block_lo, int block_hi,
+                                        const int32_t* partner_dev, int s, int k, const double* fit_dev,
+                                        const double* fit_m_dev, int minimize, double pc, double pm, int32_t pool_size,
+                                        uint64_t seed, uint64_t generation, int32_t* next_dev, double* next_fit_dev,
+                                        void* stream) {
+    if (s < 1) return fail(GAPA_CUDA_E_INVALID, "elitism: empty population");
+    if (block_lo < 0 || block_hi < block_lo || block_hi > s) return fail(GAPA_CUDA_E_INVALID, "elitism: row block outside the population");
+    GAPA_TRY(check_rates(pc, pm));
+    if (pool_size < 1) return fail(GAPA_CUDA_E_INVALID, "mutate: empty gene pool");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    OpScratch& sc = op_scratch(st);
+    GAPA_TRY(sc.init(st));
+    GAPA_TRY(sc.a.ensure(sizeof(int32_t) * s));
+    GAPA_TRY(launch_elitism_sharded(pop_dev, m_block_dev, block_lo, block_hi, partner_dev, s, k, fit_dev, fit_m_dev, minimize,
+                                    pc, pm, static_cast<uint32_t>(pool_size), seed, generation, next_dev, next_fit_dev,
+                                    sc.a.as<int32_t>(), sc.status, st));
+    return sc.check(st, "elitism: NaN fitness");
+}
 
 int gapa_cuda_ga_init(int device, int32_t pool_size, int row_first, int row_count, int budget, uint64_t seed,
                       uint64_t generation, int32_t* out) {

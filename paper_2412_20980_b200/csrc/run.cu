@@ -5,11 +5,13 @@
 //   every gen:  roulette_select -> crossover -> mutate   (or eda_sample -> mutate)
 //               -> evaluate(M_POP) -> elitism -> best = fit[0], mean = sum(fit)/s
 //
-// Sharding (world > 1) follows the reference's M mode (modes.cpp:190-349) with the
-// roles the SURVEY recommends: every rank holds the whole population and runs the
-// cheap, globally keyed operators redundantly (they are bit-identical on every rank),
-// evaluates only its partition_rows block (modes.cpp:506-516), and one all-gather of
-// fitness doubles per evaluation is the only exchange — genomes never cross NVLink.
+// Sharding (world > 1) follows the reference's M mode (modes.cpp:190-349): rank r owns the
+// partition_rows block r (modes.cpp:506-516) — it builds (crossover + mutate, or eda + mutate)
+// and evaluates only those rows of M_POP.  Every rank keeps the whole parent population;
+// selection and the elitism ranking are tiny and run redundantly; one all-gather of fitness
+// doubles per evaluation is the ONLY exchange.  Surviving mutated rows of other ranks are
+// recomputed from the replicated parents and the keyed streams (bit-identical by
+// construction), so genomes never cross NVLink.
 #include <chrono>
 #include <cmath>
 
@@ -21,7 +23,9 @@ int launch_select(const double*, int, int, uint64_t, uint64_t, int32_t*, double*
 int launch_crossover_mutate(const int32_t*, const int32_t*, int, int, int, double, double, uint32_t, uint64_t, uint64_t,
                             int32_t*, cudaStream_t);
 int launch_mutate(const int32_t*, int, int, int, double, uint32_t, uint64_t, uint64_t, int32_t*, cudaStream_t);
-int launch_eda(const int32_t*, int, int, int, uint32_t, uint64_t, uint64_t, int32_t*, cudaStream_t);
+int launch_eda(const int32_t*, int, int, int, int, uint32_t, uint64_t, uint64_t, int32_t*, cudaStream_t);
+int launch_elitism_sharded(const int32_t*, const int32_t*, int, int, const int32_t*, int, int, const double*, const double*, int,
+                           double, double, uint32_t, uint64_t, uint64_t, int32_t*, double*, int32_t*, int*, cudaStream_t);
 int launch_elitism(const int32_t*, const int32_t*, int, int, const double*, const double*, int, int32_t*, double*, int32_t*,
                    int*, cudaStream_t);
 
@@ -224,17 +228,27 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
             GAPA_TRY(check_status("fitness evaluation failed during initialization"));  // modes.cpp:314-315
         }
         const uint64_t g = static_cast<uint64_t>(gen);
-        if (p->eda_interval > 0 && gen % p->eda_interval == 0) {  // modes.cpp:31-33,167-168
-            GAPA_TRY(launch_eda(pop, s, k, s, static_cast<uint32_t>(s) + pool, p->seed, g, B.crossed.as<int32_t>(), st));
-            GAPA_TRY(launch_mutate(B.crossed.as<int32_t>(), s, k, 0, p->pm, pool, p->seed, g, mutated, st));
+        // Variation is built only for the rows this rank evaluates (all rows when world == 1).
+        const bool eda_gen = p->eda_interval > 0 && gen % p->eda_interval == 0;  // modes.cpp:31-33,167-168
+        int32_t* m_block = mutated + static_cast<size_t>(lo) * k;
+        if (eda_gen) {
+            int32_t* c_block = B.crossed.as<int32_t>() + static_cast<size_t>(lo) * k;
+            GAPA_TRY(launch_eda(pop, lo, hi - lo, k, s, static_cast<uint32_t>(s) + pool, p->seed, g, c_block, st));
+            GAPA_TRY(launch_mutate(c_block, hi - lo, k, lo, p->pm, pool, p->seed, g, m_block, st));
         } else {
             GAPA_TRY(launch_select(fit, s, minimize, p->seed, g, B.partner.as<int32_t>(), B.weights.as<double>(),
                                    B.cumulative.as<double>(), status, st));
-            GAPA_TRY(launch_crossover_mutate(pop, B.partner.as<int32_t>(), k, 0, s, p->pc, p->pm, pool, p->seed, g, mutated, st));
+            GAPA_TRY(launch_crossover_mutate(pop, B.partner.as<int32_t>(), k, lo, hi - lo, p->pc, p->pm, pool, p->seed, g,
+                                             m_block, st));
         }
         GAPA_TRY(evaluate(mutated, fit_m));
-        GAPA_TRY(launch_elitism(pop, mutated, s, k, fit, fit_m, minimize, next, fit_next, B.src_of_rank.as<int32_t>(),
-                                status, st));
+        if (world == 1)
+            GAPA_TRY(launch_elitism(pop, mutated, s, k, fit, fit_m, minimize, next, fit_next, B.src_of_rank.as<int32_t>(),
+                                    status, st));
+        else  // surviving rows built by other ranks are recomputed, never fetched
+            GAPA_TRY(launch_elitism_sharded(pop, m_block, lo, hi, eda_gen ? nullptr : B.partner.as<int32_t>(), s, k, fit, fit_m,
+                                            minimize, p->pc, p->pm, pool, p->seed, g, next, fit_next,
+                                            B.src_of_rank.as<int32_t>(), status, st));
         std::swap(pop, next);
         std::swap(fit, fit_next);
         GAPA_LAUNCH(k_ga_stats, 1, 1024, 0, st, fit, s, hist + (gen - 1), hist + iters + (gen - 1));

@@ -3,11 +3,14 @@
 Shape of the reference's M mode (modes.cpp:190-349) mapped onto GPUs:
 
   * the graph (CSR), pool and split are replicated on every GPU;
-  * every rank keeps the WHOLE population in its HBM and runs select / crossover+mutate /
-    elitism redundantly — the operators are keyed by (seed, generation, role, global row)
-    (rng.hpp:49-65), so every rank produces bit-identical matrices and genomes never
-    cross NVLink;
-  * rank r evaluates only rows partition_rows(s, world)[r] (modes.cpp:506-516);
+  * every rank keeps the WHOLE parent population in its HBM; selection and the elitism ranking
+    are tiny and run redundantly — the operators are keyed by (seed, generation, role, global
+    row) (rng.hpp:49-65), so every rank produces bit-identical results;
+  * rank r owns rows partition_rows(s, world)[r] (modes.cpp:506-516): it builds (crossover +
+    mutate, or eda_sample + mutate) and evaluates only those rows of M_POP;
+  * surviving mutated rows of OTHER ranks are recomputed inside the elitism gather from the
+    replicated parents and the keyed streams instead of being fetched, so genomes never cross
+    NVLink;
   * ONE all-gather of fitness doubles per evaluation is the only exchange (block padded to
     ceil(s/world) so counts are equal), issued through torch.distributed (NCCL over
     NVLink/NVSwitch on GPUs).
@@ -78,20 +81,21 @@ class CudaOps:
         check(self.lib.gapa_cuda_ga_select_device(fit.data_ptr(), s, minimize, seed, generation, partner.data_ptr(), None,
                                                   self._stream()))
 
-    def crossover_mutate(self, pop, partner, pc, pm, seed, generation, out):
+    def crossover_mutate(self, pop, partner, pc, pm, seed, generation, lo, hi, out):
+        """rows [lo, hi) of M_POP into out[lo:hi] (out is the full-size matrix)"""
         s, k = pop.shape
-        check(self.lib.gapa_cuda_ga_crossover_mutate_device(pop.data_ptr(), partner.data_ptr(), s, k, 0, s, pc, pm,
-                                                            self.pool_size, seed, generation, out.data_ptr(), self._stream()))
+        check(self.lib.gapa_cuda_ga_crossover_mutate_device(pop.data_ptr(), partner.data_ptr(), s, k, lo, hi - lo, pc, pm,
+                                                            self.pool_size, seed, generation, out.data_ptr() + 4 * lo * k,
+                                                            self._stream()))
 
-    def eda(self, pop, seed, generation, out):
+    def eda_mutate(self, pop, pm, seed, generation, lo, hi, scratch, out):
+        """eda_sample (elite = whole population, smoothing) then mutate; rows [lo, hi) into out[lo:hi].
+        eda_sample is evaluated for all rows (it is cheap) so the entry point keeps the reference's shape."""
         s, k = pop.shape
-        check(self.lib.gapa_cuda_ga_eda_device(pop.data_ptr(), s, k, s, self.pool_size, seed, generation, 1, out.data_ptr(),
-                                               self._stream()))
-
-    def mutate(self, block, pm, seed, generation, out):
-        s, k = block.shape
-        check(self.lib.gapa_cuda_ga_mutate_device(block.data_ptr(), s, k, 0, pm, self.pool_size, seed, generation,
-                                                  out.data_ptr(), self._stream()))
+        check(self.lib.gapa_cuda_ga_eda_device(pop.data_ptr(), s, k, s, self.pool_size, seed, generation, 1,
+                                               scratch.data_ptr(), self._stream()))
+        check(self.lib.gapa_cuda_ga_mutate_device(scratch.data_ptr() + 4 * lo * k, hi - lo, k, lo, pm, self.pool_size, seed,
+                                                  generation, out.data_ptr() + 4 * lo * k, self._stream()))
 
     def eval_rows(self, genes, lo, hi, fit_out):
         """fitness of rows [lo, hi) of `genes` into fit_out[lo:hi]"""
@@ -101,10 +105,18 @@ class CudaOps:
         self.fitness.dgraph.eval_batch_device(self.fitness.task, genes.data_ptr() + 4 * lo * k, hi - lo, k,
                                               fit_out.data_ptr() + 8 * lo, self._stream())
 
-    def elitism(self, pop, mutated, fit, fit_m, minimize, nxt, next_fit):
+    def elitism(self, pop, mutated, lo, hi, partner, fit, fit_m, minimize, pc, pm, seed, generation, nxt, next_fit):
+        """`mutated` holds valid rows only in [lo, hi); partner is None on EDA generations"""
         s, k = pop.shape
-        check(self.lib.gapa_cuda_ga_elitism_device(pop.data_ptr(), mutated.data_ptr(), s, k, fit.data_ptr(), fit_m.data_ptr(),
-                                                   minimize, nxt.data_ptr(), next_fit.data_ptr(), self._stream()))
+        if lo == 0 and hi == s:
+            check(self.lib.gapa_cuda_ga_elitism_device(pop.data_ptr(), mutated.data_ptr(), s, k, fit.data_ptr(),
+                                                       fit_m.data_ptr(), minimize, nxt.data_ptr(), next_fit.data_ptr(),
+                                                       self._stream()))
+        else:
+            check(self.lib.gapa_cuda_ga_elitism_sharded_device(
+                pop.data_ptr(), mutated.data_ptr() + 4 * lo * k, lo, hi, partner.data_ptr() if partner is not None else None,
+                s, k, fit.data_ptr(), fit_m.data_ptr(), minimize, pc, pm, self.pool_size, seed, generation, nxt.data_ptr(),
+                next_fit.data_ptr(), self._stream()))
 
     def stats(self, fit, s, hist, index, iters):
         check(self.lib.gapa_cuda_ga_stats_device(fit.data_ptr(), s, hist.data_ptr() + 8 * index,
@@ -166,14 +178,16 @@ class ShardedGa:
         self.generation += 1
         gen = self.generation
         s = p.pop_size
-        if p.eda_interval and gen % p.eda_interval == 0:  # modes.cpp:31-33,167-168
-            ops.eda(self.pop, p.seed, gen, self.crossed)
-            ops.mutate(self.crossed, p.pm, p.seed, gen, self.mutated)
+        lo, hi = self.shard.rows
+        eda_gen = bool(p.eda_interval and gen % p.eda_interval == 0)  # modes.cpp:31-33,167-168
+        if eda_gen:
+            ops.eda_mutate(self.pop, p.pm, p.seed, gen, lo, hi, self.crossed, self.mutated)
         else:
             ops.select(self.fit, s, self.minimize, p.seed, gen, self.partner)
-            ops.crossover_mutate(self.pop, self.partner, p.pc, p.pm, p.seed, gen, self.mutated)
+            ops.crossover_mutate(self.pop, self.partner, p.pc, p.pm, p.seed, gen, lo, hi, self.mutated)
         self._evaluate(self.mutated, self.fit_m)
-        ops.elitism(self.pop, self.mutated, self.fit, self.fit_m, self.minimize, self.next, self.fit_next)
+        ops.elitism(self.pop, self.mutated, lo, hi, None if eda_gen else self.partner, self.fit, self.fit_m, self.minimize,
+                    p.pc, p.pm, p.seed, gen, self.next, self.fit_next)
         self.pop, self.next = self.next, self.pop
         self.fit, self.fit_next = self.fit_next, self.fit
         if gen <= p.iterations:

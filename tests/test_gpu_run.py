@@ -61,14 +61,15 @@ def test_lpa_and_cda_runs_match_oracle(gp, oracle, cuda_device):
     _same(res, oracle.run_ga(oracle.graph_from_edges(g.n, g.edges()), 2, 0.8, 0.1, 16, 10, 12, 2))
 
 
-def test_sharded_run_equals_single(gp, cuda_device):
+@pytest.mark.parametrize("eda", [0, 4])
+def test_sharded_run_equals_single(gp, cuda_device, eda):
     """world = 2 simulated in one process: each 'rank' evaluates its partition_rows block and the
     exchange hook fills in the other block from a full single-GPU evaluation."""
     import ctypes as C
     g = gp.barabasi_albert(400, 2, 3)
     pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
     obj = gp.PairwiseConnectivityObjective(g, pool)
-    params = gp.GAParams(pc=0.6, pm=0.2, pop_size=25, budget=20, iterations=10, seed=5)
+    params = gp.GAParams(pc=0.6, pm=0.2, pop_size=25, budget=20, iterations=10, seed=5, eda_interval=eda or None)
     single = gp.run_ga(params, pool, obj)
     lib = gp.capi.load()
     helper = gp.PairwiseConnectivityObjective(g, pool)
@@ -82,8 +83,11 @@ def test_sharded_run_equals_single(gp, cuda_device):
         pop = gp.init_population(pool.size(), 25, 20, 5)
         mutated_by_gen = []
         for gen in range(1, 11):
-            idx = gp.roulette_pick(fit, gp.Direction.Minimize, 5, gen)
-            mutated = gp.crossover_mutate(pop, idx, 0.6, 0.2, pool.size(), 5, gen)
+            if eda and gen % eda == 0:
+                mutated = gp.mutate(gp.eda_sample(pop, 25, pool.size(), 5, gen), 0.2, pool.size(), 5, gen)
+            else:
+                idx = gp.roulette_pick(fit, gp.Direction.Minimize, 5, gen)
+                mutated = gp.crossover_mutate(pop, idx, 0.6, 0.2, pool.size(), 5, gen)
             fm = helper.evaluate_batch(mutated)
             mutated_by_gen.append(mutated)
             pop, fit = gp.elitism(pop, mutated, fit, fm, gp.Direction.Minimize)
@@ -112,3 +116,46 @@ def test_run_rejects_bad_params(gp, cuda_device):
         kw.update(bad)
         with pytest.raises(gp.capi.GapaCudaError):
             gp.run_ga(gp.GAParams(**kw), pool, obj)
+
+
+@pytest.mark.parametrize("eda", [0, 3])
+def test_sharded_driver_recomputes_foreign_rows(gp, oracle, cuda_device, eda):
+    """driver.ShardedGa with the CUDA ops as rank 0 and as rank 1 of a 2-rank run, one process: the
+    fake all-gather fills the other rank's fitness block by building that block with the operator
+    API and evaluating it.  Each rank builds only its own rows of M_POP, so the final population is
+    only right if the elitism gather recomputes surviving foreign rows exactly."""
+    import torch
+    from paper_2412_20980_b200.driver import CudaOps, Shard, ShardedGa
+
+    g = gp.barabasi_albert(500, 2, 4)
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    obj = gp.PairwiseConnectivityObjective(g, pool)
+    helper = gp.PairwiseConnectivityObjective(g, pool)
+    s, k, iters = 37, 15, 9
+    params = gp.GAParams(pc=0.6, pm=0.2, pop_size=s, budget=k, iterations=iters, seed=11, eda_interval=eda or None)
+    want = oracle.run_ga(oracle.graph_from_edges(g.n, g.edges()), 0, 0.6, 0.2, s, k, iters, 11, eda_interval=eda)
+    for rank in (0, 1):
+        shard = Shard(rank, 2, s)
+        other_lo, other_hi = gp.partition_rows(s, 2)[1 - rank]
+        box = {}
+
+        def gather(fit, shard_, box=box, other_lo=other_lo, other_hi=other_hi):
+            ga = box["ga"]
+            pop = ga.pop.cpu().numpy()
+            gen = ga.generation
+            if gen == 0:
+                rows = pop[other_lo:other_hi]
+            elif eda and gen % eda == 0:
+                rows = gp.mutate_block(gp.eda_sample(pop, s, pool.size(), 11, gen)[other_lo:other_hi], other_lo, 0.2,
+                                       pool.size(), 11, gen)
+            else:
+                rows = gp.crossover_mutate(pop, ga.partner.cpu().numpy(), 0.6, 0.2, pool.size(), 11, gen, other_lo,
+                                           other_hi - other_lo)
+            fit[other_lo:other_hi] = torch.from_numpy(helper.evaluate_batch(rows)).to(fit.device)
+
+        ga = ShardedGa(params, CudaOps(obj, 0), shard, gather)
+        box["ga"] = ga
+        res = ga.run()
+        assert np.array_equal(res.final_population, want["population"]), rank
+        assert np.array_equal(res.history_best, want["best"]) and np.array_equal(res.history_mean, want["mean"])
+        assert np.array_equal(res.final_fitness, want["fitness"])

@@ -33,16 +33,23 @@ class OracleOps:
     def init(self, out, seed, gen): out.copy_(torch.from_numpy(self.o.init_population(self.pool_size, out.shape[0], out.shape[1], seed, gen)))
     def select(self, fit, s, minimize, seed, gen, partner):
         partner.copy_(torch.from_numpy(self.o.roulette_pick(fit[:s].numpy(), bool(minimize), seed, gen)))
-    def crossover_mutate(self, pop, partner, pc, pm, seed, gen, out):
-        c = self.o.crossover(pop.numpy(), partner.numpy(), pc, seed, gen)
-        out.copy_(torch.from_numpy(self.o.mutate_block(c, 0, pm, self.pool_size, seed, gen)))
-    def eda(self, pop, seed, gen, out): out.copy_(torch.from_numpy(self.o.eda_sample(pop.numpy(), pop.shape[0], self.pool_size, seed, gen, True)))
-    def mutate(self, block, pm, seed, gen, out): out.copy_(torch.from_numpy(self.o.mutate_block(block.numpy(), 0, pm, self.pool_size, seed, gen)))
+    def _variation(self, pop, partner, pc, pm, seed, gen):
+        c = (self.o.crossover(pop.numpy(), partner.numpy(), pc, seed, gen) if partner is not None
+             else self.o.eda_sample(pop.numpy(), pop.shape[0], self.pool_size, seed, gen, True))
+        return self.o.mutate_block(c, 0, pm, self.pool_size, seed, gen)
+    def crossover_mutate(self, pop, partner, pc, pm, seed, gen, lo, hi, out):
+        out.fill_(-7)  # rows outside [lo, hi) are NOT built on this rank
+        out[lo:hi] = torch.from_numpy(self._variation(pop, partner, pc, pm, seed, gen)[lo:hi])
+    def eda_mutate(self, pop, pm, seed, gen, lo, hi, scratch, out):
+        out.fill_(-7)
+        out[lo:hi] = torch.from_numpy(self._variation(pop, None, 0.0, pm, seed, gen)[lo:hi])
     def eval_rows(self, genes, lo, hi, fit_out):
         if hi > lo: fit_out[lo:hi] = torch.from_numpy(self.o.eval_batch(self.ctx, self.task, genes[lo:hi].numpy()))
-    def elitism(self, pop, mut, fit, fit_m, minimize, nxt, next_fit):
+    def elitism(self, pop, mut, lo, hi, partner, fit, fit_m, minimize, pc, pm, seed, gen, nxt, next_fit):
         s = pop.shape[0]
-        a, b = self.o.elitism(pop.numpy(), mut.numpy(), fit[:s].numpy(), fit_m[:s].numpy(), bool(minimize))
+        full = self._variation(pop, partner, pc, pm, seed, gen)  # foreign rows are recomputed, not fetched
+        assert np.array_equal(full[lo:hi], mut[lo:hi].numpy())
+        a, b = self.o.elitism(pop.numpy(), full, fit[:s].numpy(), fit_m[:s].numpy(), bool(minimize))
         nxt.copy_(torch.from_numpy(a)); next_fit[:s] = torch.from_numpy(b)
     def stats(self, fit, s, hist, index, iters):
         total = 0.0
