@@ -53,6 +53,58 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_crossover_mutate(
     }
 }
 
+// Four genes per thread (16-byte loads / stores), all draws of a gene share the product C * j,
+// the golden-ratio add of mix64 is folded into the row keys, and the 53-bit Bernoulli test
+// (u >> 11) < T is done as u < (T << 11).  Every gene evaluates all three draws: inside a warp
+// both sides of the mutate / crossover branch are taken anyway, and straight-line code keeps
+// twelve independent hash chains in flight.  Results are identical to the scalar kernel.
+__device__ __forceinline__ uint64_t mix64_tail(uint64_t y) {  // mix64(x) with y = x + 0x9E3779B97F4A7C15
+    y = (y ^ (y >> 30)) * 0xBF58476D1CE4E5B9ull;
+    y = (y ^ (y >> 27)) * 0x94D049BB133111EBull;
+    return y ^ (y >> 31);
+}
+struct BernoulliLimit {  // (u >> 11) < threshold  <=>  always || u < limit
+    uint64_t limit;
+    bool always;
+};
+static BernoulliLimit bernoulli_limit(double p) {
+    const uint64_t t = bernoulli_threshold(p);
+    return {t >= (1ull << 53) ? ~0ull : t << 11, t >= (1ull << 53)};
+}
+
+__global__ void __launch_bounds__(kGaThreads) k_ga_crossover_mutate4(
+    const int32_t* __restrict__ pop, const int32_t* __restrict__ partner, int k, int row_first, uint64_t pc_limit,
+    bool pc_always, uint64_t pm_limit, bool pm_always, uint32_t pool_size, uint64_t seed, uint64_t generation,
+    int32_t* __restrict__ out) {
+    __shared__ uint64_t keys[3];
+    const int row = row_first + blockIdx.y;
+    if (threadIdx.x < 3)
+        keys[threadIdx.x] = stream_key(seed, generation, GAPA_ROLE_CROSSOVER_MASK + threadIdx.x, static_cast<uint64_t>(row)) +
+                            0x9E3779B97F4A7C15ull;
+    __syncthreads();
+    const uint64_t kc = keys[0], km = keys[1], ki = keys[2];
+    const int4* mine = reinterpret_cast<const int4*>(pop + static_cast<size_t>(row) * k);
+    const int4* theirs = reinterpret_cast<const int4*>(pop + static_cast<size_t>(partner[row]) * k);
+    int4* dst = reinterpret_cast<int4*>(out + static_cast<size_t>(blockIdx.y) * k);
+    const int quads = k >> 2;
+    for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < quads; q += gridDim.x * blockDim.x) {
+        const int4 a = mine[q], b = theirs[q];
+        const int av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+        int r[4];
+        uint64_t prod = 0x632BE59BD9B4E019ull * (static_cast<uint64_t>(q) * 4 + 1);  // C * j, j = column + 1
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+            const uint64_t um = mix64_tail(km + prod), ux = mix64_tail(kc + prod), ui = mix64_tail(ki + prod);
+            const bool flip = pm_always || um < pm_limit;
+            const bool take = pc_always || ux < pc_limit;
+            const int fresh = static_cast<int>(__umul64hi(ui, static_cast<uint64_t>(pool_size)));
+            r[t] = flip ? fresh : (take ? bv[t] : av[t]);
+            prod += 0x632BE59BD9B4E019ull;
+        }
+        dst[q] = make_int4(r[0], r[1], r[2], r[3]);
+    }
+}
+
 // ---- mutate_block alone (ga_ops.cpp:164-178) ------------------------------------------------
 __global__ void __launch_bounds__(kGaThreads) k_ga_mutate(const int32_t* __restrict__ block, int k, int row_offset,
                                                           uint64_t pm_thr, uint32_t pool_size, uint64_t seed,
@@ -237,6 +289,12 @@ int launch_crossover_mutate(const int32_t* pop, const int32_t* partner, int k, i
                             double pm, uint32_t pool_size, uint64_t seed, uint64_t generation, int32_t* out,
                             cudaStream_t st) {
     if (row_count == 0 || k == 0) return GAPA_CUDA_OK;
+    if ((k & 3) == 0 && ((reinterpret_cast<uintptr_t>(pop) | reinterpret_cast<uintptr_t>(out)) & 15) == 0) {
+        const BernoulliLimit c = bernoulli_limit(pc), m = bernoulli_limit(pm);
+        GAPA_LAUNCH(k_ga_crossover_mutate4, row_grid(k / 4, row_count), kGaThreads, 0, st, pop, partner, k, row_first, c.limit,
+                    c.always, m.limit, m.always, pool_size, seed, generation, out);
+        return GAPA_CUDA_OK;
+    }
     GAPA_LAUNCH(k_ga_crossover_mutate, row_grid(k, row_count), kGaThreads, 0, st, pop, partner, k, row_first,
                 bernoulli_threshold(pc), bernoulli_threshold(pm), pool_size, seed, generation, out);
     return GAPA_CUDA_OK;
