@@ -267,6 +267,8 @@ int gapa_cuda_pool_set(gapa_cuda_ctx* c, int kind, int32_t n_genes, const int32_
     c->pool_kind = kind;
     c->pool_size = n_genes;
     c->pool_identity = identity;
+    c->h_pool_map = identity ? std::vector<int32_t>() : map;
+    ++c->pool_version;
     return GAPA_CUDA_OK;
 }
 

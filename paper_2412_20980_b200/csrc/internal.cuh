@@ -130,6 +130,8 @@ struct gapa_cuda_ctx {
     int32_t pool_size = 0;
     bool pool_identity = true;
     int32_t* d_pool_map = nullptr;  // gene id -> node id / edge rank when not identity
+    std::vector<int32_t> h_pool_map;  // host copy of the same map (empty when identity)
+    unsigned long long pool_version = 0;  // bumped by gapa_cuda_pool_set
     // link-prediction split
     int32_t T = 0, P = 0;
     int32_t* d_pairs = nullptr;     // (T + P) x 2, test pairs first

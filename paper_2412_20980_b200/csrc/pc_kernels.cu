@@ -67,7 +67,12 @@ struct PcScratch {
     DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters, pass_flags, block_done;
     DevBuf left_v, left_g, left_w, left_base, parent, comp_size, pc_extra, mcn_extra;
     size_t cap_entries = 0, cap_slots = 0;
-    int prefix = 32768, interleave = 8, mask_chunks = 1, small_path = 1;
+    int prefix = 32768, interleave = 8, mask_chunks = 1, small_path = 1, relabel = -1;
+    // hub-first internal vertex order for the bit-sliced path (see ensure_order)
+    DevBuf ord_row_ptr, ord_col_idx, ord_gene_map;
+    bool ord_ready = false, ord_relabeled = false;
+    unsigned long long ord_pool_version = ~0ull;
+    std::vector<int32_t> perm;  // original vertex -> internal vertex when relabelled
     bool configured = false;
 };
 
@@ -189,7 +194,7 @@ __global__ void __launch_bounds__(kThreads) k_pc_source(const int32_t* __restric
     const int g = row >> 6;
     const word_t bit = 1ull << (row & 63);
     for (int i = 0; i < n; i += 32) {
-        const int v = i + lane < n ? by_degree[i + lane] : -1;
+        const int v = i + lane < n ? (by_degree ? by_degree[i + lane] : i + lane) : -1;
         const bool ok = v >= 0 && (alive[static_cast<size_t>(g) * n + v] & bit);
         const unsigned hit = __ballot_sync(0xffffffffu, ok);
         if (hit) {
@@ -654,6 +659,60 @@ static int env_int(const char* name, int fallback, int lo, int hi) {
     return static_cast<int>(std::min<long>(hi, std::max<long>(lo, v)));
 }
 
+// The sweeps assume that LOW vertex ids are the well-connected core: rows are scanned in ascending
+// id, the prefix kernel closes ids [0, prefix), and blocks run in ascending id.  Generators that grow
+// a graph (Barabasi-Albert) number vertices that way already.  For any other numbering the bit-sliced
+// path works on an internal relabelling by descending degree — component sizes do not depend on
+// vertex names — built once per (graph, pool) on the host: a permuted CSR with ascending rows and a
+// gene -> internal vertex map.  Natural order is kept when its first n/32 ids already hold at least
+// 70 % of the edge endpoints that the n/32 highest-degree vertices hold.
+static int ensure_order(gapa_cuda_ctx* ctx, PcScratch* s) {
+    if (s->ord_ready && s->ord_pool_version == ctx->pool_version) return GAPA_CUDA_OK;
+    const int n = ctx->n;
+    const std::vector<int32_t>& rp = ctx->h_row_ptr;
+    const std::vector<int32_t>& ci = ctx->h_col_idx;
+    if (!s->ord_ready) {
+        std::vector<int32_t> order(n);
+        for (int v = 0; v < n; ++v) order[v] = v;
+        std::stable_sort(order.begin(), order.end(), [&](int32_t a, int32_t b) { return rp[a + 1] - rp[a] > rp[b + 1] - rp[b]; });
+        const int head = std::max(1, n / 32);
+        long long mass_natural = 0, mass_degree = 0;
+        for (int i = 0; i < head; ++i) {
+            mass_natural += rp[i + 1] - rp[i];
+            mass_degree += rp[order[i] + 1] - rp[order[i]];
+        }
+        s->ord_relabeled = s->relabel == 1 || (s->relabel != 0 && mass_natural * 10 < mass_degree * 7);
+        s->perm.clear();
+        if (s->ord_relabeled) {
+            s->perm.resize(n);
+            for (int i = 0; i < n; ++i) s->perm[order[i]] = i;
+            std::vector<int32_t> row_ptr(static_cast<size_t>(n) + 1, 0), col_idx(ci.size());
+            for (int i = 0; i < n; ++i) row_ptr[i + 1] = row_ptr[i] + (rp[order[i] + 1] - rp[order[i]]);
+            for (int i = 0; i < n; ++i) {
+                const int old = order[i];
+                int32_t* dst = col_idx.data() + row_ptr[i];
+                for (int e = rp[old]; e < rp[old + 1]; ++e) *dst++ = s->perm[ci[e]];
+                std::sort(col_idx.data() + row_ptr[i], dst);
+            }
+            GAPA_TRY(s->ord_row_ptr.ensure(sizeof(int32_t) * row_ptr.size()));
+            GAPA_TRY(s->ord_col_idx.ensure(sizeof(int32_t) * std::max<size_t>(col_idx.size(), 1)));
+            GAPA_CUDA_TRY(cudaMemcpy(s->ord_row_ptr.ptr, row_ptr.data(), sizeof(int32_t) * row_ptr.size(), cudaMemcpyHostToDevice));
+            if (!col_idx.empty())
+                GAPA_CUDA_TRY(cudaMemcpy(s->ord_col_idx.ptr, col_idx.data(), sizeof(int32_t) * col_idx.size(), cudaMemcpyHostToDevice));
+        }
+        s->ord_ready = true;
+    }
+    if (s->ord_relabeled) {  // gene -> internal vertex
+        std::vector<int32_t> map(static_cast<size_t>(std::max(ctx->pool_size, 1)));
+        for (int gidx = 0; gidx < ctx->pool_size; ++gidx)
+            map[gidx] = s->perm[ctx->pool_identity ? gidx : ctx->h_pool_map[gidx]];
+        GAPA_TRY(s->ord_gene_map.ensure(sizeof(int32_t) * map.size()));
+        GAPA_CUDA_TRY(cudaMemcpy(s->ord_gene_map.ptr, map.data(), sizeof(int32_t) * map.size(), cudaMemcpyHostToDevice));
+    }
+    s->ord_pool_version = ctx->pool_version;
+    return GAPA_CUDA_OK;
+}
+
 int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, int cols, double* out_dev,
             cudaStream_t stream, bool trusted) {
     if (!ctx->pc) ctx->pc = new PcScratch();
@@ -662,6 +721,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
         s->prefix = env_int("GAPA_PC_PREFIX", 32768, 0, 1 << 24);
         s->interleave = env_int("GAPA_PC_INTERLEAVE", 8, 1, 64);
         s->mask_chunks = env_int("GAPA_PC_MASK_CHUNKS", 1, 1, 64);
+        s->relabel = env_int("GAPA_PC_RELABEL", -1, -1, 1);  // -1 automatic, 0 never, 1 always (tests)
         s->small_path = env_int("GAPA_PC_SMALL", 1, 0, 1);  // 0 forces the bit-sliced pipeline on small graphs (tests)
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         // the shared-memory bitmap may use most of the SM (one CTA per individual)
@@ -686,6 +746,11 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
         if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
         return GAPA_CUDA_OK;
     }
+    GAPA_TRY(ensure_order(ctx, s));
+    const int32_t* g_row_ptr = s->ord_relabeled ? s->ord_row_ptr.as<int32_t>() : ctx->d_row_ptr;
+    const int32_t* g_col_idx = s->ord_relabeled ? s->ord_col_idx.as<int32_t>() : ctx->d_col_idx;
+    const int32_t* g_gene_map = s->ord_relabeled ? s->ord_gene_map.as<int32_t>() : (ctx->pool_identity ? nullptr : ctx->d_pool_map);
+    const int32_t* g_by_degree = s->ord_relabeled ? nullptr : ctx->d_by_degree;
     const int words_per_row = std::max(1, (n + 63) / 64);
     int chunk_bits = std::min(words_per_row * 64, 192 * 1024 * 8);  // <= 192 KB of shared memory
     if (s->mask_chunks > 1) chunk_bits = std::min(chunk_bits, ((words_per_row + s->mask_chunks - 1) / s->mask_chunks) * 64);
@@ -731,13 +796,13 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
         if (n > 0) {
             // ---- masks ------------------------------------------------------------------
             GAPA_LAUNCH(k_pc_bitmask, dim3(chunks, crows), kMaskThreads, static_cast<size_t>(chunk_bits) / 8, stream,
-                        genes_dev + static_cast<size_t>(row0) * cols, cols, ctx->pool_identity ? nullptr : ctx->d_pool_map,
+                        genes_dev + static_cast<size_t>(row0) * cols, cols, g_gene_map,
                         ctx->pool_size, n, chunk_bits, words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>(),
                         counters);
             GAPA_LAUNCH(k_pc_transpose, dim3((words_per_row + kTransThreads - 1) / kTransThreads, pgroups), kTransThreads,
                         sizeof(word_t) * kBits * (kTransThreads + 1), stream, s->removed.as<word_t>(), words_per_row, n, crows, alive);
             GAPA_CUDA_TRY(cudaMemsetAsync(reached, 0, sizeof(word_t) * words, stream));
-            GAPA_LAUNCH(k_pc_source, (crows * 32 + kThreads - 1) / kThreads, kThreads, 0, stream, ctx->d_by_degree, n,
+            GAPA_LAUNCH(k_pc_source, (crows * 32 + kThreads - 1) / kThreads, kThreads, 0, stream, g_by_degree, n,
                         crows, alive, reached);
 
             // ---- phase 1 ------------------------------------------------------------------
@@ -747,7 +812,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
             if (prefix > 0) {
                 GAPA_TRY(s->pass_flags.ensure(sizeof(int) * 64 * sgroups));
                 GAPA_CUDA_TRY(cudaMemsetAsync(s->pass_flags.ptr, 0, sizeof(int) * 64 * sgroups, stream));
-                GAPA_LAUNCH(k_pc_prefix, sgroups * kPrefixCluster, kPrefixThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n,
+                GAPA_LAUNCH(k_pc_prefix, sgroups * kPrefixCluster, kPrefixThreads, 0, stream, g_row_ptr, g_col_idx, n,
                             prefix, alive_rec, reached_rec, s->pass_flags.as<int>());
             }
             const int il = std::min(std::max(1, s->interleave / kPack), sgroups);
@@ -756,13 +821,13 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
             unsigned char* block_done = s->block_done.as<unsigned char>();
             auto sweep = [&](bool final_pass) -> int {
                 if (final_pass)
-                    GAPA_LAUNCH(k_pc_sweep<true>, grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, sgroups, il,
+                    GAPA_LAUNCH(k_pc_sweep<true>, grid, kThreads, 0, stream, g_row_ptr, g_col_idx, n, sgroups, il,
                                 alive_rec, reached_rec, s->unreached.as<int>(), s->entry_of.as<int32_t>(),
                                 s->left_v.as<int32_t>(), s->left_g.as<int32_t>(), s->left_w.as<word_t>(),
                                 s->left_base.as<int32_t>(), s->parent.as<int32_t>(), s->comp_size.as<int32_t>(),
                                 static_cast<unsigned>(s->cap_entries), static_cast<unsigned>(s->cap_slots), slot0, counters, block_done);
                 else
-                    GAPA_LAUNCH(k_pc_sweep<false>, grid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, sgroups, il,
+                    GAPA_LAUNCH(k_pc_sweep<false>, grid, kThreads, 0, stream, g_row_ptr, g_col_idx, n, sgroups, il,
                                 alive_rec, reached_rec, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
                                 0u, 0u, slot0, counters, block_done);
                 return GAPA_CUDA_OK;
@@ -791,7 +856,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
             // ---- phase 2 ------------------------------------------------------------------
             if (h.n_entries) {
                 const int pgrid = static_cast<int>(std::min<unsigned>((h.n_entries + kThreads - 1) / kThreads, sm * 8));
-                GAPA_LAUNCH(k_pc_hook, pgrid, kThreads, 0, stream, ctx->d_row_ptr, ctx->d_col_idx, n, alive, reached,
+                GAPA_LAUNCH(k_pc_hook, pgrid, kThreads, 0, stream, g_row_ptr, g_col_idx, n, alive, reached,
                             s->entry_of.as<int32_t>(), s->left_v.as<int32_t>(), s->left_g.as<int32_t>(),
                             s->left_w.as<word_t>(), s->left_base.as<int32_t>(), s->parent.as<int32_t>(), slot0, counters);
                 GAPA_LAUNCH(k_pc_count, pgrid, kThreads, 0, stream, s->left_w.as<word_t>(), s->left_base.as<int32_t>(),

@@ -123,3 +123,25 @@ def test_medium_power_law_graph(gp, oracle, cuda_device):
     obj, pool = _objective(gp, g, 0)
     batch = gp.init_population(pool.size(), 96, 5000, 1)
     assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(og, 0, batch, threads=8))
+
+
+def test_shuffled_labels_use_the_hub_first_internal_order(gp, oracle, cuda_device, pc_path, monkeypatch):
+    """A power-law graph whose labels carry no structure: the bit-sliced path relabels by degree
+    internally (automatic here; forced on and off as well) and must return the same integers."""
+    rng = np.random.default_rng(12)
+    base = gp.barabasi_albert(20_000, 3, 2)
+    perm = rng.permutation(base.n).astype(np.int32)
+    edges = perm[base.edges()]
+    g = gp.Graph(base.n, edges)
+    og = oracle.graph_from_edges(g.n, edges)
+    batch = rng.integers(0, g.n, size=(70, 900)).astype(np.int32)
+    want_pc, want_mcn = oracle.eval_batch(og, 0, batch, threads=8), oracle.eval_batch(og, 1, batch, threads=8)
+    sub = np.sort(rng.choice(g.n, 5000, replace=False)).astype(np.int32)  # custom pool composed with the relabelling
+    for relabel in ("-1", "1", "0"):
+        monkeypatch.setenv("GAPA_PC_RELABEL", relabel)
+        pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+        assert np.array_equal(gp.PairwiseConnectivityObjective(g, pool).evaluate_batch(batch), want_pc)
+        assert np.array_equal(gp.SixDstObjective(g, pool).evaluate_batch(batch), want_mcn)
+        obj = gp.PairwiseConnectivityObjective(g, gp.GenePool(gp.PoolKind.NodeRemoval, sub))
+        genes = rng.integers(0, len(sub), size=(9, 300)).astype(np.int32)
+        assert np.array_equal(obj.evaluate_batch(genes), oracle.eval_batch(og, 0, sub[genes]))
