@@ -1,0 +1,105 @@
+"""Edge cases the reference tests or implies: empty perturbations and batches, tiny and edgeless
+graphs, budgets larger than the pool, custom (re-ordered) edge pools, CSR construction, argument
+errors.  All through the C ABI, against the oracle."""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def test_tiny_and_edgeless_graphs(gp, oracle, cuda_device):
+    for n, edges in [(1, []), (2, []), (2, [(0, 1)]), (3, [(0, 2)]), (65, [(i, i + 1) for i in range(64)])]:
+        g = gp.Graph(n, np.array(edges, dtype=np.int32).reshape(-1, 2))
+        og = oracle.graph_from_edges(n, edges)
+        pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+        batch = np.array([[0] * 3, [n - 1] * 3, [0, n - 1, n // 2]], dtype=np.int32)
+        for task, cls in ((0, gp.PairwiseConnectivityObjective), (1, gp.SixDstObjective)):
+            obj = cls(g, pool)
+            assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(og, task, batch))
+            assert obj.evaluate_batch(np.zeros((2, 0), np.int32)).tolist() == oracle.eval_batch(og, task, np.zeros((2, 0), np.int32)).tolist()
+
+
+def test_budget_larger_than_pool_and_heavy_duplicates(gp, oracle, cuda_device):
+    g = gp.barabasi_albert(40, 2, 3)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    rng = np.random.default_rng(0)
+    batch = rng.integers(0, g.n, size=(5, 400)).astype(np.int32)  # k = 10 n: almost everything removed, many duplicates
+    assert np.array_equal(gp.PairwiseConnectivityObjective(g, gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)).evaluate_batch(batch),
+                          oracle.eval_batch(og, 0, batch))
+    pool = gp.build_gene_pool(g, gp.PoolKind.EdgeRemoval)
+    ebatch = rng.integers(0, pool.size(), size=(5, 5 * pool.size())).astype(np.int32)
+    got = gp.ModularityAttackObjective(g, pool).evaluate_batch(ebatch)
+    assert np.array_equal(got, oracle.eval_batch(og, 2, ebatch))
+
+
+def test_custom_edge_pool_order(gp, oracle, cuda_device):
+    """A GenePool whose gene ids are NOT the (u,v)-sorted ranks: the C ABI maps (u, v) to CSR edge ranks."""
+    g = gp.planted_partition(3, 20, 0.3, 0.05, 5)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    base = gp.build_gene_pool(g, gp.PoolKind.EdgeRemoval)
+    rng = np.random.default_rng(3)
+    order = rng.permutation(base.size())[: base.size() // 2]  # a shuffled half of the edges
+    flip = rng.random(len(order)) < 0.5                         # endpoints given in either order
+    u = np.where(flip, base.v[order], base.u[order]).astype(np.int32)
+    v = np.where(flip, base.u[order], base.v[order]).astype(np.int32)
+    pool = gp.GenePool(gp.PoolKind.EdgeRemoval, u, v)
+    genes = rng.integers(0, pool.size(), size=(6, 25)).astype(np.int32)
+    want = oracle.eval_batch(og, 2, order[genes].astype(np.int32))
+    assert np.array_equal(gp.ModularityAttackObjective(g, pool).evaluate_batch(genes), want)
+    with pytest.raises(gp.capi.GapaCudaError):
+        gp.ModularityAttackObjective(g, gp.GenePool(gp.PoolKind.EdgeRemoval, [0], [0]))  # not an edge
+
+
+def test_csr_constructor_and_argument_errors(gp, oracle, cuda_device):
+    lib = gp.capi.load()
+    og = oracle.graph_ba(200, 2, 1)
+    h = C.c_void_p()
+    rp, ci = np.ascontiguousarray(og.row_ptr), np.ascontiguousarray(og.col_idx)
+    gp.capi.check(lib.gapa_cuda_graph_create_csr(og.n, og.m, rp.ctypes.data, ci.ctypes.data, 0, C.byref(h)))
+    genes = oracle.init_population(og.n, 70, 10, 2)
+    out = np.zeros(70)
+    gp.capi.check(lib.gapa_cuda_eval_batch(h, 0, genes.ctypes.data, 70, 10, out.ctypes.data))
+    assert np.array_equal(out, oracle.eval_batch(og, 0, genes))
+    n_, m_, dev = C.c_int32(), C.c_int64(), C.c_int()
+    gp.capi.check(lib.gapa_cuda_graph_info(h, C.byref(n_), C.byref(m_), C.byref(dev)))
+    assert (n_.value, m_.value, dev.value) == (og.n, og.m, 0)
+    assert lib.gapa_cuda_eval_batch(h, 2, genes.ctypes.data, 70, 10, out.ctypes.data) == gp.capi.E_INVALID  # CDA on a node pool
+    assert lib.gapa_cuda_eval_batch(h, 9, genes.ctypes.data, 70, 10, out.ctypes.data) == gp.capi.E_INVALID
+    assert lib.gapa_cuda_eval_batch(h, 0, genes.ctypes.data, -1, 10, out.ctypes.data) == gp.capi.E_INVALID
+    assert b"unknown" in lib.gapa_cuda_last_error() or b"negative" in lib.gapa_cuda_last_error()
+    lib.gapa_cuda_destroy(h)
+    bad = ci.copy()
+    bad[0], bad[1] = bad[1], bad[0]  # row 0 no longer ascending
+    assert lib.gapa_cuda_graph_create_csr(og.n, og.m, rp.ctypes.data, bad.ctypes.data, 0, C.byref(h)) == gp.capi.E_INVALID
+    for edges in ([(0, 0)], [(0, 1), (1, 0)], [(0, 7)]):  # self-loop, duplicate, out of range (graph.cpp:26-31)
+        e = np.array(edges, dtype=np.int32)
+        assert lib.gapa_cuda_graph_create(5, len(e), e.ctypes.data, 0, C.byref(h)) == gp.capi.E_INVALID
+    assert lib.gapa_cuda_graph_create(5, 0, None, 99, C.byref(h)) == gp.capi.E_INVALID  # no such device
+
+
+def test_lpa_edge_cases(gp, oracle, cuda_device):
+    g = gp.barabasi_albert(60, 2, 8)
+    split = gp.build_lp_split(g, 0.5, 2)  # largest allowed test fraction
+    os_ = oracle.split_build(oracle.graph_from_edges(g.n, g.edges()), 0.5, 2)
+    pool = gp.build_gene_pool(split.train, gp.PoolKind.EdgeRemoval)
+    obj = gp.LinkPredictionAttackObjective(split, pool)
+    rng = np.random.default_rng(4)
+    for k in (0, 1, pool.size(), 3 * pool.size()):
+        batch = rng.integers(0, pool.size(), size=(3, k)).astype(np.int32)
+        assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(os_, 3, batch)), k
+
+
+def test_two_contexts_and_repeated_calls(gp, oracle, cuda_device):
+    """Two objectives on different graphs, interleaved calls, growing and shrinking batches."""
+    ga, gb = gp.barabasi_albert(3000, 3, 1), gp.erdos_renyi(400, 0.02, 2)
+    oa, ob = oracle.graph_from_edges(ga.n, ga.edges()), oracle.graph_from_edges(gb.n, gb.edges())
+    a = gp.PairwiseConnectivityObjective(ga, gp.build_gene_pool(ga, gp.PoolKind.NodeRemoval))
+    b = gp.SixDstObjective(gb, gp.build_gene_pool(gb, gp.PoolKind.NodeRemoval))
+    rng = np.random.default_rng(6)
+    for rows in (3, 300, 1, 129, 64):
+        xa = rng.integers(0, ga.n, size=(rows, 50)).astype(np.int32)
+        xb = rng.integers(0, gb.n, size=(rows, 20)).astype(np.int32)
+        assert np.array_equal(a.evaluate_batch(xa), oracle.eval_batch(oa, 0, xa))
+        assert np.array_equal(b.evaluate_batch(xb), oracle.eval_batch(ob, 1, xb))
