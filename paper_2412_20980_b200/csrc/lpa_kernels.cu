@@ -14,6 +14,7 @@
 // All partial sums of the reference's `wins` are multiples of 0.5 below 2^53, hence
 // exact, so (2*wins)/2.0 / (T*P) is the same double.
 #include <algorithm>
+#include <cstdlib>
 
 #include "internal.cuh"
 
@@ -147,7 +148,9 @@ int lpa_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, d
     const int n = ctx->n, T = ctx->T, P = ctx->P, n_pairs = T + P;
     const int mask_words = static_cast<int>((ctx->m + 31) / 32) + 1;
     const size_t per_row = sizeof(unsigned) * mask_words + sizeof(int32_t) * n + sizeof(double) * n_pairs;
-    const int chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(rows, (8ull << 30) / per_row)));
+    size_t budget = 8ull << 30;  // scratch per pass; GAPA_SCRATCH_MB overrides (tests force several passes)
+    if (const char* raw = std::getenv("GAPA_SCRATCH_MB")) budget = static_cast<size_t>(std::max(1L, std::strtol(raw, nullptr, 10))) << 20;
+    const int chunk = static_cast<int>(std::max<size_t>(1, std::min<size_t>(rows, budget / per_row)));
     GAPA_TRY(s->gone.ensure(sizeof(unsigned) * mask_words * static_cast<size_t>(chunk)));
     GAPA_TRY(s->deg.ensure(sizeof(int32_t) * std::max(n, 1) * static_cast<size_t>(chunk)));
     GAPA_TRY(s->scores.ensure(sizeof(double) * n_pairs * static_cast<size_t>(chunk)));

@@ -756,7 +756,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
     if (s->mask_chunks > 1) chunk_bits = std::min(chunk_bits, ((words_per_row + s->mask_chunks - 1) / s->mask_chunks) * 64);
     const int chunks = (words_per_row * 64 + chunk_bits - 1) / chunk_bits;
     // groups per pass bounded by a scratch budget: alive + reached + entry_of (20 B) + bitmaps (8 B / 64) per vertex
-    const size_t budget = 24ull << 30;
+    const size_t budget = static_cast<size_t>(env_int("GAPA_SCRATCH_MB", 24 * 1024, 1, 1 << 20)) << 20;  // scratch per pass
     const int all_groups = (rows + kBits - 1) / kBits;
     const int max_groups = static_cast<int>(std::min<size_t>(1023, std::max<size_t>(1, budget / (28ull * std::max(n, 1)))));
 

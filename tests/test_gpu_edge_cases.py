@@ -103,3 +103,23 @@ def test_two_contexts_and_repeated_calls(gp, oracle, cuda_device):
         xb = rng.integers(0, gb.n, size=(rows, 20)).astype(np.int32)
         assert np.array_equal(a.evaluate_batch(xa), oracle.eval_batch(oa, 0, xa))
         assert np.array_equal(b.evaluate_batch(xb), oracle.eval_batch(ob, 1, xb))
+
+
+def test_batches_larger_than_the_scratch_budget(gp, oracle, cuda_device, monkeypatch):
+    """GAPA_SCRATCH_MB = 1 forces the PC pipeline and the LPA kernels to process a batch in several
+    passes (the path a 16k-individual batch on a 1M-node graph takes with the real budget)."""
+    monkeypatch.setenv("GAPA_SCRATCH_MB", "1")
+    monkeypatch.setenv("GAPA_PC_SMALL", "0")
+    g = gp.barabasi_albert(4000, 3, 2)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    batch = gp.init_population(pool.size(), 333, 200, 5)  # 6 groups; 1 MB holds ~9 vertex-group slices
+    for task, cls in ((0, gp.PairwiseConnectivityObjective), (1, gp.SixDstObjective)):
+        assert np.array_equal(cls(g, pool).evaluate_batch(batch), oracle.eval_batch(og, task, batch, threads=8))
+    g = gp.erdos_renyi(3000, 0.004, 3)
+    split = gp.build_lp_split(g, 0.1, 1)
+    epool = gp.build_gene_pool(split.train, gp.PoolKind.EdgeRemoval)
+    os_ = oracle.split_build(oracle.graph_from_edges(g.n, g.edges()), 0.1, 1)
+    ebatch = gp.init_population(epool.size(), 90, 500, 6)
+    assert np.array_equal(gp.LinkPredictionAttackObjective(split, epool).evaluate_batch(ebatch),
+                          oracle.eval_batch(os_, 3, ebatch, threads=8))
