@@ -251,7 +251,7 @@ def run_gpu_arm(args, w):
     # this rank's block of the current M_POP, pinned memory, copies inside the timed region.
     lo, hi = shard.rows
     host_genes = torch.empty((hi - lo, k), dtype=torch.int32, pin_memory=True)
-    host_genes.copy_(ga.mutated[lo:hi])
+    host_genes.copy_(ga.population()[lo:hi])  # this rank's block of the current parents; their fitness is ga.fit
     host_out = torch.empty(max(hi - lo, 1), dtype=torch.float64, pin_memory=True)
     torch.cuda.synchronize()
 
@@ -267,7 +267,7 @@ def run_gpu_arm(args, w):
         e2e_once()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    assert np.array_equal(host_out[:hi - lo].numpy(), ga.fit_m[lo:hi].cpu().numpy()), "e2e result differs from the device path"
+    assert np.array_equal(host_out[:hi - lo].numpy(), ga.fit[lo:hi].cpu().numpy()), "e2e result differs from the device path"
 
     times = torch.tensor([step_ms_total, e2e_s * 1e3, float(np.mean(eval_ms))], dtype=torch.float64, device="cuda")
     if world > 1:

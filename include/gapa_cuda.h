@@ -144,6 +144,35 @@ int gapa_cuda_ga_elitism_sharded_device(const int32_t* pop_dev, const int32_t* m
                                         int32_t pool_size, uint64_t seed, uint64_t generation, int32_t* next_dev,
                                         double* next_fit_dev, void* stream);
 
+/* ---- slot-pool population store (the loop's zero-copy form of POP / M_POP, modes.cpp:159-175) ----
+ * pool_dev holds 2s rows of k genes; parent_dev[r] / child_dev[r] name the slot of parent row r (best
+ * first) and of child row r.  Variation writes children into their slots, evaluators read rows
+ * through a slot table, elitism permutes the tables — no genome is copied.  partner_dev == NULL
+ * selects the EDA form (eda_sample over all parents with smoothing, then mutate). */
+int gapa_cuda_ga_slots_identity_device(int s, int32_t* parent_dev, int32_t* child_dev, void* stream);
+/* children of rows [row_first, row_first + row_count): crossover (ga_ops.cpp:130-144) + mutate_block
+ * (:164-178), or eda_sample (:214-238) + mutate_block */
+int gapa_cuda_ga_slots_variation_device(int32_t* pool_dev, const int32_t* parent_dev, const int32_t* child_dev,
+                                        const int32_t* partner_dev, int s, int k, int row_first, int row_count,
+                                        double pc, double pm, int32_t pool_size, uint64_t seed, uint64_t generation,
+                                        void* stream);
+/* elitism (ga_ops.cpp:180-212) as a permutation: next_parent = slots of the s best of the 2s stacked
+ * rows (stable, originals first on ties), next_child = the s freed slots, next_fit = their fitness.
+ * Children of rows outside [block_lo, block_hi) that survive are rebuilt in their slots from the
+ * parents and the keyed streams (row sharding: they were built on another rank). */
+int gapa_cuda_ga_slots_elitism_device(int32_t* pool_dev, const int32_t* parent_dev, const int32_t* child_dev,
+                                      const int32_t* partner_dev, int s, int k, int block_lo, int block_hi,
+                                      const double* fit_dev, const double* fit_m_dev, int minimize, double pc,
+                                      double pm, int32_t pool_size, uint64_t seed, uint64_t generation,
+                                      int32_t* next_parent_dev, int32_t* next_child_dev, double* next_fit_dev,
+                                      void* stream);
+/* dense row-major matrix of the rows table_dev names (PopulationMatrix, population.hpp:12-40) */
+int gapa_cuda_ga_slots_gather_device(const int32_t* pool_dev, const int32_t* table_dev, int rows, int k,
+                                     int32_t* out_dev, void* stream);
+/* evaluate_batch over rows addressed through a slot table: row i = pool_dev + slot_dev[i] * cols */
+int gapa_cuda_eval_rows_device(gapa_cuda_ctx* ctx, int task, const int32_t* pool_dev, const int32_t* slot_dev,
+                               int rows, int cols, double* out_dev, void* stream);
+
 /* record_generation (modes.cpp:35-43): best_dev[0] = fit[0], mean_dev[0] = sequential
  * sum(fit) / s — the reference's std::accumulate order, so non-integer fitness means
  * are bit-identical. */

@@ -89,7 +89,7 @@ __device__ __forceinline__ double merge_gain(int edges, int da, int db, double m
 
 extern __shared__ int32_t cda_smem[];
 
-__global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, const int32_t* __restrict__ genes, int rows, int cols,
+__global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows genes, int rows,
                                                         int pos_in_smem, double* __restrict__ out) {
     __shared__ Cand warp_cand[kCdaWarps];
     __shared__ Cand chosen;
@@ -131,7 +131,8 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, const int32_t
         for (int w = tid; w < A.mask_words; w += kCdaThreads) gone[w] = 0u;
         if (tid == 0) { sh_total = 0; sh_abort = 0; }
         __syncthreads();
-        const int32_t* g = genes + static_cast<size_t>(r) * cols;
+        const int cols = genes.cols;
+        const int32_t* g = genes.row(r);
         for (int j = tid; j < cols; j += kCdaThreads) {
             const int gene = g[j];
             if (gene < 0 || gene >= A.pool_size) { A.status[0] = GAPA_CUDA_E_RANGE; sh_abort = 1; continue; }
@@ -440,7 +441,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, const int32_t
     }
 }
 
-int cda_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, double* out_dev, cudaStream_t stream) {
+int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream) {
     if (!ctx->cda) ctx->cda = new CdaScratch();
     CdaScratch* s = ctx->cda;
     const int n = ctx->n;
@@ -481,7 +482,7 @@ int cda_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, d
         A.status = s->status.as<int>();
         const size_t smem = pos_in_smem == 2 ? static_cast<size_t>(n) * 7 * sizeof(int32_t) : (pos_in_smem ? static_cast<size_t>(n) * sizeof(int32_t) : 0);
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_cda, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        GAPA_LAUNCH(k_cda, slots, kCdaThreads, smem, stream, A, genes_dev, rows, cols, pos_in_smem, out_dev);
+        GAPA_LAUNCH(k_cda, slots, kCdaThreads, smem, stream, A, genes, rows, pos_in_smem, out_dev);
         GAPA_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, s->status.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
         GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
         if (ctx->h_status[0] == GAPA_CUDA_E_RANGE) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");

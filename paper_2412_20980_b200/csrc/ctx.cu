@@ -314,6 +314,23 @@ static int check_task(const gapa_cuda_ctx* c, int task) {
     return fail(GAPA_CUDA_E_INVALID, "unknown fitness task %d", task);
 }
 
+static int eval_rows_locked(gapa_cuda_ctx* c, int task, const GeneRows& genes, int rows, double* out_dev, void* stream) {
+    std::unique_lock<std::mutex> lock(c->mu, std::defer_lock);
+    if (stream != static_cast<void*>(c->stream)) lock.lock();  // the host-buffer form already holds it
+    GAPA_CUDA_TRY(cudaSetDevice(c->device));
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    GAPA_CUDA_TRY(cudaEventRecord(c->ev_start, s));
+    int rc;
+    if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) rc = pc_eval(c, task, genes, rows, out_dev, s);
+    else if (task == GAPA_TASK_CDA) rc = cda_eval(c, genes, rows, out_dev, s);
+    else rc = lpa_eval(c, genes, rows, out_dev, s);
+    if (rc != GAPA_CUDA_OK) return rc;
+    GAPA_CUDA_TRY(cudaEventRecord(c->ev_stop, s));
+    GAPA_CUDA_TRY(cudaEventSynchronize(c->ev_stop));
+    GAPA_CUDA_TRY(cudaEventElapsedTime(&c->last_eval_ms, c->ev_start, c->ev_stop));
+    return GAPA_CUDA_OK;
+}
+
 int gapa_cuda_eval_batch_device(gapa_cuda_ctx* c, int task, const int32_t* genes_dev, int rows, int cols,
                                 double* out_dev, void* stream) {
     if (!c) return fail(GAPA_CUDA_E_INVALID, "eval_batch: null context");
@@ -321,20 +338,17 @@ int gapa_cuda_eval_batch_device(gapa_cuda_ctx* c, int task, const int32_t* genes
     if (rows < 0 || cols < 0) return fail(GAPA_CUDA_E_INVALID, "eval_batch: negative shape");
     if (rows == 0) return GAPA_CUDA_OK;
     if (!out_dev || (cols > 0 && !genes_dev)) return fail(GAPA_CUDA_E_INVALID, "eval_batch: null buffer");
-    std::unique_lock<std::mutex> lock(c->mu, std::defer_lock);
-    if (stream != static_cast<void*>(c->stream)) lock.lock();  // the host-buffer form already holds it
-    GAPA_CUDA_TRY(cudaSetDevice(c->device));
-    cudaStream_t s = static_cast<cudaStream_t>(stream);
-    GAPA_CUDA_TRY(cudaEventRecord(c->ev_start, s));
-    int rc;
-    if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) rc = pc_eval(c, task, genes_dev, rows, cols, out_dev, s);
-    else if (task == GAPA_TASK_CDA) rc = cda_eval(c, genes_dev, rows, cols, out_dev, s);
-    else rc = lpa_eval(c, genes_dev, rows, cols, out_dev, s);
-    if (rc != GAPA_CUDA_OK) return rc;
-    GAPA_CUDA_TRY(cudaEventRecord(c->ev_stop, s));
-    GAPA_CUDA_TRY(cudaEventSynchronize(c->ev_stop));
-    GAPA_CUDA_TRY(cudaEventElapsedTime(&c->last_eval_ms, c->ev_start, c->ev_stop));
-    return GAPA_CUDA_OK;
+    return eval_rows_locked(c, task, GeneRows{genes_dev, nullptr, cols}, rows, out_dev, stream);
+}
+
+int gapa_cuda_eval_rows_device(gapa_cuda_ctx* c, int task, const int32_t* pool_dev, const int32_t* slot_dev, int rows,
+                               int cols, double* out_dev, void* stream) {
+    if (!c) return fail(GAPA_CUDA_E_INVALID, "eval_rows: null context");
+    GAPA_TRY(check_task(c, task));
+    if (rows < 0 || cols < 0) return fail(GAPA_CUDA_E_INVALID, "eval_rows: negative shape");
+    if (rows == 0) return GAPA_CUDA_OK;
+    if (!out_dev || !slot_dev || (cols > 0 && !pool_dev)) return fail(GAPA_CUDA_E_INVALID, "eval_rows: null buffer");
+    return eval_rows_locked(c, task, GeneRows{pool_dev, slot_dev, cols}, rows, out_dev, stream);
 }
 
 int gapa_cuda_eval_batch(gapa_cuda_ctx* c, int task, const int32_t* genes_host, int rows, int cols, double* out_host) {

@@ -445,6 +445,11 @@ struct Tmp {
 };
 }  // namespace
 
+namespace gapa_b200 {
+int launch_slots_elitism(int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int, int, const double*, const double*,
+                         int, double, double, uint32_t, uint64_t, uint64_t, int32_t*, int32_t*, double*, int32_t*, int*, cudaStream_t);
+}
+
 static int check_rates(double pc, double pm) {
     if (!(pc >= 0.0 && pc <= 1.0)) return fail(GAPA_CUDA_E_INVALID, "pc must be in [0, 1]");
     if (!(pm >= 0.0 && pm <= 1.0)) return fail(GAPA_CUDA_E_INVALID, "pm must be in [0, 1]");
@@ -529,6 +534,25 @@ int gapa_cuda_ga_elitism_sharded_device(const int32_t* pop_dev, const int32_t* m
     GAPA_TRY(launch_elitism_sharded(pop_dev, m_block_dev, block_lo, block_hi, partner_dev, s, k, fit_dev, fit_m_dev, minimize,
                                     pc, pm, static_cast<uint32_t>(pool_size), seed, generation, next_dev, next_fit_dev,
                                     sc.a.as<int32_t>(), sc.status, st));
+    return sc.check(st, "elitism: NaN fitness");
+}
+
+int gapa_cuda_ga_slots_elitism_device(int32_t* pool_dev, const int32_t* parent_dev, const int32_t* child_dev,
+                                      const int32_t* partner_dev, int s, int k, int block_lo, int block_hi,
+                                      const double* fit_dev, const double* fit_m_dev, int minimize, double pc, double pm,
+                                      int32_t pool_size, uint64_t seed, uint64_t generation, int32_t* next_parent_dev,
+                                      int32_t* next_child_dev, double* next_fit_dev, void* stream) {
+    if (s < 1) return fail(GAPA_CUDA_E_INVALID, "elitism: empty population");
+    if (block_lo < 0 || block_hi < block_lo || block_hi > s) return fail(GAPA_CUDA_E_INVALID, "elitism: row block outside the population");
+    GAPA_TRY(check_rates(pc, pm));
+    if (pool_size < 1) return fail(GAPA_CUDA_E_INVALID, "mutate: empty gene pool");
+    cudaStream_t st = static_cast<cudaStream_t>(stream);
+    OpScratch& sc = op_scratch(st);
+    GAPA_TRY(sc.init(st));
+    GAPA_TRY(sc.a.ensure(sizeof(int32_t) * 2 * s));
+    GAPA_TRY(launch_slots_elitism(pool_dev, parent_dev, child_dev, partner_dev, s, k, block_lo, block_hi, fit_dev, fit_m_dev,
+                                  minimize, pc, pm, static_cast<uint32_t>(pool_size), seed, generation, next_parent_dev,
+                                  next_child_dev, next_fit_dev, sc.a.as<int32_t>(), sc.status, st));
     return sc.check(st, "elitism: NaN fitness");
 }
 

@@ -104,6 +104,22 @@ __device__ __forceinline__ bool draw_bernoulli(uint64_t key, uint64_t j, uint64_
     return (draw_u64(key, j) >> 11) < threshold;
 }
 
+// ---- gene matrix view -----------------------------------------------------------------
+// Row r of a batch lives at base + slot[r] * cols (slot == nullptr: the dense row-major matrix of
+// population.hpp:12-40).  The in-library generation loop keeps parents and children in one pool of
+// 2s row slots and hands evaluators a slot table, so elitism never copies a genome.
+struct GeneRows {
+    const int32_t* base;
+    const int32_t* slot;
+    int cols;
+    __host__ __device__ const int32_t* row(int r) const {
+        return base + static_cast<size_t>(slot ? slot[r] : r) * cols;
+    }
+    GeneRows from(int r0) const {  // the same batch starting at row r0
+        return slot ? GeneRows{base, slot + r0, cols} : GeneRows{base + static_cast<size_t>(r0) * cols, nullptr, cols};
+    }
+};
+
 // ---- context -------------------------------------------------------------------------
 struct PcScratch;   // pc_kernels.cu
 struct LpaScratch;  // lpa_kernels.cu
@@ -158,12 +174,10 @@ namespace gapa_b200 {
 // `trusted` = the genes were produced by this library's own operators (always inside the pool),
 // so evaluators that need no other host decision skip the range-status readback and stay
 // asynchronous.
-int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, int cols, double* out_dev,
-            cudaStream_t stream, bool trusted = false);
-int lpa_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, double* out_dev,
-             cudaStream_t stream, bool trusted = false);
-int cda_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, double* out_dev,
-             cudaStream_t stream);
+int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_dev, cudaStream_t stream,
+            bool trusted = false);
+int lpa_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream, bool trusted = false);
+int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream);
 void pc_free(gapa_cuda_ctx* ctx);
 void lpa_free(gapa_cuda_ctx* ctx);
 void cda_free(gapa_cuda_ctx* ctx);

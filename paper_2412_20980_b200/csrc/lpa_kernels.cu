@@ -37,15 +37,15 @@ __global__ void __launch_bounds__(kLpaThreads) k_lpa_init(const int32_t* __restr
 }
 
 // apply_in_place for EdgeRemoval (gene_pool.cpp:53-56); duplicates idempotent.
-__global__ void __launch_bounds__(kLpaThreads) k_lpa_remove(const int32_t* __restrict__ genes, size_t cells, int cols,
+__global__ void __launch_bounds__(kLpaThreads) k_lpa_remove(GeneRows genes, size_t cells,
                                                             const int32_t* __restrict__ pool_map, int pool_size,
                                                             const int32_t* __restrict__ edge_u,
                                                             const int32_t* __restrict__ edge_v, int n, int mask_words,
                                                             unsigned* gone, int32_t* deg, int* status) {
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < cells;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
-        const int r = static_cast<int>(i / cols);
-        const int gene = genes[i];
+        const int r = static_cast<int>(i / genes.cols);
+        const int gene = genes.row(r)[i - static_cast<size_t>(r) * genes.cols];
         if (gene < 0 || gene >= pool_size) {
             *status = GAPA_CUDA_E_RANGE;
             continue;
@@ -141,8 +141,8 @@ __global__ void k_lpa_final(const unsigned long long* __restrict__ twice, int ro
     out[r] = wins / (static_cast<double>(T) * static_cast<double>(P));  // link_prediction.cpp:96
 }
 
-int lpa_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, double* out_dev, cudaStream_t stream,
-             bool trusted) {
+int lpa_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream, bool trusted) {
+    const int cols = genes.cols;
     if (!ctx->lpa) ctx->lpa = new LpaScratch();
     LpaScratch* s = ctx->lpa;
     const int n = ctx->n, T = ctx->T, P = ctx->P, n_pairs = T + P;
@@ -167,7 +167,7 @@ int lpa_eval(gapa_cuda_ctx* ctx, const int32_t* genes_dev, int rows, int cols, d
         const size_t cells = static_cast<size_t>(cr) * cols;
         if (cells) {
             const int grid = static_cast<int>(std::min<size_t>((cells + kLpaThreads - 1) / kLpaThreads, static_cast<size_t>(sm) * 32));
-            GAPA_LAUNCH(k_lpa_remove, grid, kLpaThreads, 0, stream, genes_dev + static_cast<size_t>(r0) * cols, cells, cols,
+            GAPA_LAUNCH(k_lpa_remove, grid, kLpaThreads, 0, stream, genes.from(r0), cells,
                         ctx->pool_identity ? nullptr : ctx->d_pool_map, ctx->pool_size, ctx->d_edge_u, ctx->d_edge_v, n,
                         mask_words, s->gone.as<unsigned>(), s->deg.as<int32_t>(), status);
         }

@@ -82,7 +82,7 @@ struct PcScratch {
 // Duplicate genes are idempotent.  Bit c of 64-bit word w = vertex 64 w + c removed.
 extern __shared__ __align__(16) unsigned pc_smem_bits[];
 
-__global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(const int32_t* __restrict__ genes, int cols,
+__global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(GeneRows genes,
                                                              const int32_t* __restrict__ pool_map, int pool_size, int n,
                                                              int chunk_bits, int words_per_row, word_t* __restrict__ removed,
                                                              int* removed_count, PcCounters* counters) {
@@ -92,7 +92,8 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(const int32_t* __re
     const int words64 = (v1 - v0 + 63) >> 6;
     for (int w = threadIdx.x; w < 2 * words64; w += kMaskThreads) pc_smem_bits[w] = 0u;
     __syncthreads();
-    const int32_t* g = genes + static_cast<size_t>(row) * cols;
+    const int cols = genes.cols;
+    const int32_t* g = genes.row(row);
     auto mark = [&](int gene) {
         if (gene < 0 || gene >= pool_size) {
             counters->range_error = 1;
@@ -574,7 +575,7 @@ __global__ void k_pc_reset(int groups, int32_t* parent, int32_t* comp_size, int*
 static constexpr int kSmallMaxN = 16384;
 static constexpr int kSmallThreads = 128;
 
-__global__ void __launch_bounds__(kSmallThreads) k_pc_small(const int32_t* __restrict__ genes, int cols,
+__global__ void __launch_bounds__(kSmallThreads) k_pc_small(GeneRows genes,
                                                             const int32_t* __restrict__ pool_map, int pool_size, int n, int m,
                                                             const int32_t* __restrict__ edge_u,
                                                             const int32_t* __restrict__ edge_v, int task,
@@ -593,7 +594,8 @@ __global__ void __launch_bounds__(kSmallThreads) k_pc_small(const int32_t* __res
         size[v] = 0;
     }
     __syncthreads();
-    const int32_t* g = genes + static_cast<size_t>(row) * cols;
+    const int cols = genes.cols;
+    const int32_t* g = genes.row(row);
     for (int j = tid; j < cols; j += kSmallThreads) {
         const int gene = g[j];
         if (gene < 0 || gene >= pool_size) {
@@ -713,8 +715,8 @@ static int ensure_order(gapa_cuda_ctx* ctx, PcScratch* s) {
     return GAPA_CUDA_OK;
 }
 
-int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, int cols, double* out_dev,
-            cudaStream_t stream, bool trusted) {
+int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_dev, cudaStream_t stream, bool trusted) {
+    const int cols = genes.cols;
     if (!ctx->pc) ctx->pc = new PcScratch();
     PcScratch* s = ctx->pc;
     if (!s->configured) {  // tuning knobs (defaults are what bench.py measures)
@@ -736,7 +738,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
         GAPA_TRY(s->counters.ensure(sizeof(PcCounters)));
         PcCounters* counters = s->counters.as<PcCounters>();
         GAPA_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(PcCounters), stream));
-        GAPA_LAUNCH(k_pc_small, rows, kSmallThreads, smem, stream, genes_dev, cols,
+        GAPA_LAUNCH(k_pc_small, rows, kSmallThreads, smem, stream, genes,
                     ctx->pool_identity ? nullptr : ctx->d_pool_map, ctx->pool_size, n, static_cast<int>(ctx->m), ctx->d_edge_u,
                     ctx->d_edge_v, task, out_dev, counters);
         if (trusted) return GAPA_CUDA_OK;
@@ -796,7 +798,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, in
         if (n > 0) {
             // ---- masks ------------------------------------------------------------------
             GAPA_LAUNCH(k_pc_bitmask, dim3(chunks, crows), kMaskThreads, static_cast<size_t>(chunk_bits) / 8, stream,
-                        genes_dev + static_cast<size_t>(row0) * cols, cols, g_gene_map,
+                        genes.from(row0), g_gene_map,
                         ctx->pool_size, n, chunk_bits, words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>(),
                         counters);
             GAPA_LAUNCH(k_pc_transpose, dim3((words_per_row + kTransThreads - 1) / kTransThreads, pgroups), kTransThreads,

@@ -24,6 +24,12 @@ int launch_crossover_mutate(const int32_t*, const int32_t*, int, int, int, doubl
                             int32_t*, cudaStream_t);
 int launch_mutate(const int32_t*, int, int, int, double, uint32_t, uint64_t, uint64_t, int32_t*, cudaStream_t);
 int launch_eda(const int32_t*, int, int, int, int, uint32_t, uint64_t, uint64_t, int32_t*, cudaStream_t);
+int launch_slots_identity(int, int32_t*, int32_t*, cudaStream_t);
+int launch_slots_variation(int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int, int, double, double, uint32_t,
+                           uint64_t, uint64_t, cudaStream_t);
+int launch_slots_elitism(int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int, int, const double*, const double*,
+                         int, double, double, uint32_t, uint64_t, uint64_t, int32_t*, int32_t*, double*, int32_t*, int*, cudaStream_t);
+int launch_slots_gather(const int32_t*, const int32_t*, int, int, int32_t*, cudaStream_t);
 int launch_elitism_sharded(const int32_t*, const int32_t*, int, int, const int32_t*, int, int, const double*, const double*, int,
                            double, double, uint32_t, uint64_t, uint64_t, int32_t*, double*, int32_t*, int*, cudaStream_t);
 int launch_elitism(const int32_t*, const int32_t*, int, int, const double*, const double*, int, int32_t*, double*, int32_t*,
@@ -119,14 +125,13 @@ struct EvalTimer {
     }
 };
 
-int eval_rows(gapa_cuda_ctx* ctx, int task, const int32_t* genes, int rows, int cols, double* out, cudaStream_t st,
-              EvalTimer* timer) {
+int eval_rows(gapa_cuda_ctx* ctx, int task, const GeneRows& view, int rows, double* out, cudaStream_t st, EvalTimer* timer) {
     if (rows == 0) return GAPA_CUDA_OK;
     GAPA_TRY(timer->mark(st));
     int rc;
-    if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) rc = pc_eval(ctx, task, genes, rows, cols, out, st, true);
-    else if (task == GAPA_TASK_CDA) rc = cda_eval(ctx, genes, rows, cols, out, st);
-    else rc = lpa_eval(ctx, genes, rows, cols, out, st, true);
+    if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) rc = pc_eval(ctx, task, view, rows, out, st, true);
+    else if (task == GAPA_TASK_CDA) rc = cda_eval(ctx, view, rows, out, st);
+    else rc = lpa_eval(ctx, view, rows, out, st, true);
     GAPA_TRY(rc);
     return timer->mark(st);
 }
@@ -173,23 +178,24 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
     const size_t cells = static_cast<size_t>(s) * k, padded = static_cast<size_t>(block) * world;
     cudaStream_t st = ctx->stream;
 
+    // Population store: one pool of 2s row slots + parent / child slot tables (slot_kernels.cu).
     RunBuffers B;
-    GAPA_TRY(B.pop.ensure(sizeof(int32_t) * cells));
-    GAPA_TRY(B.mutated.ensure(sizeof(int32_t) * cells));
-    GAPA_TRY(B.next.ensure(sizeof(int32_t) * cells));
-    if (p->eda_interval > 0) GAPA_TRY(B.crossed.ensure(sizeof(int32_t) * cells));
+    GAPA_TRY(B.pop.ensure(sizeof(int32_t) * 2 * cells));
+    GAPA_TRY(B.next.ensure(sizeof(int32_t) * 4 * s));  // parent, child, next parent, next child tables
     GAPA_TRY(B.partner.ensure(sizeof(int32_t) * s));
     GAPA_TRY(B.fit.ensure(sizeof(double) * padded));
     GAPA_TRY(B.fit_m.ensure(sizeof(double) * padded));
     GAPA_TRY(B.fit_next.ensure(sizeof(double) * padded));
     GAPA_TRY(B.weights.ensure(sizeof(double) * s));
     GAPA_TRY(B.cumulative.ensure(sizeof(double) * s));
-    GAPA_TRY(B.src_of_rank.ensure(sizeof(int32_t) * s));
+    GAPA_TRY(B.src_of_rank.ensure(sizeof(int32_t) * 2 * s));
     GAPA_TRY(B.status.ensure(sizeof(int)));
     GAPA_TRY(B.hist.ensure(sizeof(double) * 2 * iters));
-    int32_t* pop = B.pop.as<int32_t>();
-    int32_t* mutated = B.mutated.as<int32_t>();
-    int32_t* next = B.next.as<int32_t>();
+    int32_t* pool_rows = B.pop.as<int32_t>();
+    int32_t* parent = B.next.as<int32_t>();
+    int32_t* child = parent + s;
+    int32_t* next_parent = child + s;
+    int32_t* next_child = next_parent + s;
     double* fit = B.fit.as<double>();
     double* fit_m = B.fit_m.as<double>();
     double* fit_next = B.fit_next.as<double>();
@@ -202,9 +208,9 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
     result->fitness_batch_calls = 0;
     result->eval_seconds = 0.0;
     EvalTimer timer;
-    auto evaluate = [&](const int32_t* rows_all, double* fit_all) -> int {
+    auto evaluate = [&](const int32_t* table, double* fit_all) -> int {  // rows [lo, hi) named by `table`
         ++result->fitness_batch_calls;
-        GAPA_TRY(eval_rows(ctx, p->task, rows_all + static_cast<size_t>(lo) * k, hi - lo, k, fit_all + lo, st, &timer));
+        GAPA_TRY(eval_rows(ctx, p->task, GeneRows{pool_rows, table + lo, k}, hi - lo, fit_all + lo, st, &timer));
         if (world > 1) {
             const int rc = exchange(exchange_user, fit_all, s, block, st);
             if (rc != 0) return fail(GAPA_CUDA_E_CUDA, "run: exchange hook failed with status %d", rc);
@@ -222,34 +228,26 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
     const auto t0 = std::chrono::steady_clock::now();
     for (int gen = 1; gen <= iters; ++gen) {
         if (gen == 1) {
-            GAPA_TRY(launch_init(pool, 0, s, k, p->seed, 0, pop, st));
-            GAPA_TRY(evaluate(pop, fit));
+            GAPA_TRY(launch_slots_identity(s, parent, child, st));
+            GAPA_TRY(launch_init(pool, 0, s, k, p->seed, 0, pool_rows, st));  // parents occupy slots 0..s-1
+            GAPA_TRY(evaluate(parent, fit));
             GAPA_LAUNCH(k_check_nan, (s + 255) / 256, 256, 0, st, fit, s, status);
             GAPA_TRY(check_status("fitness evaluation failed during initialization"));  // modes.cpp:314-315
         }
         const uint64_t g = static_cast<uint64_t>(gen);
-        // Variation is built only for the rows this rank evaluates (all rows when world == 1).
+        // Children are built only for the rows this rank evaluates (all rows when world == 1).
         const bool eda_gen = p->eda_interval > 0 && gen % p->eda_interval == 0;  // modes.cpp:31-33,167-168
-        int32_t* m_block = mutated + static_cast<size_t>(lo) * k;
-        if (eda_gen) {
-            int32_t* c_block = B.crossed.as<int32_t>() + static_cast<size_t>(lo) * k;
-            GAPA_TRY(launch_eda(pop, lo, hi - lo, k, s, static_cast<uint32_t>(s) + pool, p->seed, g, c_block, st));
-            GAPA_TRY(launch_mutate(c_block, hi - lo, k, lo, p->pm, pool, p->seed, g, m_block, st));
-        } else {
+        const int32_t* partner = eda_gen ? nullptr : B.partner.as<int32_t>();
+        if (!eda_gen)
             GAPA_TRY(launch_select(fit, s, minimize, p->seed, g, B.partner.as<int32_t>(), B.weights.as<double>(),
                                    B.cumulative.as<double>(), status, st));
-            GAPA_TRY(launch_crossover_mutate(pop, B.partner.as<int32_t>(), k, lo, hi - lo, p->pc, p->pm, pool, p->seed, g,
-                                             m_block, st));
-        }
-        GAPA_TRY(evaluate(mutated, fit_m));
-        if (world == 1)
-            GAPA_TRY(launch_elitism(pop, mutated, s, k, fit, fit_m, minimize, next, fit_next, B.src_of_rank.as<int32_t>(),
-                                    status, st));
-        else  // surviving rows built by other ranks are recomputed, never fetched
-            GAPA_TRY(launch_elitism_sharded(pop, m_block, lo, hi, eda_gen ? nullptr : B.partner.as<int32_t>(), s, k, fit, fit_m,
-                                            minimize, p->pc, p->pm, pool, p->seed, g, next, fit_next,
-                                            B.src_of_rank.as<int32_t>(), status, st));
-        std::swap(pop, next);
+        GAPA_TRY(launch_slots_variation(pool_rows, parent, child, partner, s, k, lo, hi - lo, p->pc, p->pm, pool, p->seed, g, st));
+        GAPA_TRY(evaluate(child, fit_m));
+        // elitism permutes the slot tables; survivors built by other ranks are rebuilt in place
+        GAPA_TRY(launch_slots_elitism(pool_rows, parent, child, partner, s, k, lo, hi, fit, fit_m, minimize, p->pc, p->pm, pool,
+                                      p->seed, g, next_parent, next_child, fit_next, B.src_of_rank.as<int32_t>(), status, st));
+        std::swap(parent, next_parent);
+        std::swap(child, next_child);
         std::swap(fit, fit_next);
         GAPA_LAUNCH(k_ga_stats, 1, 1024, 0, st, fit, s, hist + (gen - 1), hist + iters + (gen - 1));
         // NaN / non-finite fitness is an Error in the reference (ga_ops.cpp:56-57, :189-192);
@@ -267,7 +265,15 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
 
     if (result->history_best) GAPA_CUDA_TRY(cudaMemcpy(result->history_best, hist, sizeof(double) * iters, cudaMemcpyDeviceToHost));
     if (result->history_mean) GAPA_CUDA_TRY(cudaMemcpy(result->history_mean, hist + iters, sizeof(double) * iters, cudaMemcpyDeviceToHost));
-    if (result->final_population) GAPA_CUDA_TRY(cudaMemcpy(result->final_population, pop, sizeof(int32_t) * cells, cudaMemcpyDeviceToHost));
+    if (result->final_population) {  // RunResult::final_population: the parents in best-first order
+        DevBuf dense;
+        GAPA_TRY(dense.ensure(sizeof(int32_t) * std::max<size_t>(cells, 1)));
+        int rc = launch_slots_gather(pool_rows, parent, s, k, dense.as<int32_t>(), st);
+        if (rc == GAPA_CUDA_OK && cudaMemcpyAsync(result->final_population, dense.ptr, sizeof(int32_t) * cells, cudaMemcpyDeviceToHost, st) != cudaSuccess) rc = GAPA_CUDA_E_CUDA;
+        if (rc == GAPA_CUDA_OK && cudaStreamSynchronize(st) != cudaSuccess) rc = GAPA_CUDA_E_CUDA;
+        dense.release();
+        if (rc != GAPA_CUDA_OK) return fail(rc, "run: could not materialise the final population");
+    }
     if (result->final_fitness) GAPA_CUDA_TRY(cudaMemcpy(result->final_fitness, fit, sizeof(double) * s, cudaMemcpyDeviceToHost));
     return GAPA_CUDA_OK;
 }

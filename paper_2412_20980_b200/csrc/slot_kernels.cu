@@ -1,0 +1,248 @@
+// The population store of the generation loop: ONE pool of 2s row slots in HBM plus two index
+// tables — parent[r] = slot of parent row r (best first), child[r] = slot of child row r (the s
+// slots that are free this generation).  Variation writes children straight into their slots and
+// the evaluators read them through the table (GeneRows), so elitism (ga_ops.cpp:180-212) is a
+// permutation of indices: no genome is ever copied, whatever survives stays where it was built.
+//
+// Under row sharding (modes.cpp:190-349 on GPUs) a rank builds only the children of its own row
+// block; a surviving child that another rank built is recomputed into its slot from the replicated
+// parents and the keyed streams (k_ga_slots_rebuild) — never fetched over the interconnect.
+//
+// Every gene equals the reference's: parents/children are the matrices POP / M_POP of
+// modes.cpp:159-175 seen through the tables (gapa_cuda_ga_slots_gather materialises them).
+#include <algorithm>
+
+#include "internal.cuh"
+
+namespace gapa_b200 {
+
+static constexpr int kSlotThreads = 256;
+static constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+static constexpr uint64_t kCounterStep = 0x632BE59BD9B4E019ull;  // rng.hpp:21
+
+__device__ __forceinline__ uint64_t hash_tail(uint64_t y) {  // mix64(x) with y = x + kGolden (rng.hpp:8-13)
+    y = (y ^ (y >> 30)) * 0xBF58476D1CE4E5B9ull;
+    y = (y ^ (y >> 27)) * 0x94D049BB133111EBull;
+    return y ^ (y >> 31);
+}
+
+struct VariationParams {
+    uint64_t pc_limit, pm_limit;  // next_bernoulli(p) == always || u < limit  (u >> 11 < ceil(p 2^53))
+    bool pc_always, pm_always;
+    uint32_t pool_size;  // gene pool
+    uint32_t s;          // population size (elite count of eda_sample, modes.cpp:168)
+    uint64_t seed, generation;
+};
+
+// One child gene.  partner_row < 0 selects the EDA form: eda_sample over the whole parent
+// population with add-one smoothing (ga_ops.cpp:214-238), then mutate; otherwise crossover
+// (ga_ops.cpp:130-144) then mutate (:164-178).  `prod` = kCounterStep * (column + 1); the keys
+// already include kGolden.
+__device__ __forceinline__ int32_t child_gene(const VariationParams& P, const int32_t* __restrict__ pool,
+                                              const int32_t* __restrict__ parent, int k, int col, int mine, int theirs,
+                                              bool eda, uint64_t ks, uint64_t kc, uint64_t km, uint64_t ki, uint64_t prod) {
+    const uint64_t um = hash_tail(km + prod);
+    if (P.pm_always || um < P.pm_limit) return static_cast<int32_t>(__umul64hi(hash_tail(ki + prod), static_cast<uint64_t>(P.pool_size)));
+    if (eda) {
+        const uint32_t v = static_cast<uint32_t>(__umul64hi(hash_tail(ks + prod), static_cast<uint64_t>(P.s + P.pool_size)));
+        return v < P.s ? pool[static_cast<size_t>(parent[v]) * k + col] : static_cast<int32_t>(v - P.s);
+    }
+    const uint64_t ux = hash_tail(kc + prod);
+    return (P.pc_always || ux < P.pc_limit) ? theirs : mine;
+}
+
+// Builds child row `row` into its slot.  Shared by the variation kernel (own rows) and the rebuild
+// kernel (foreign survivors).
+__device__ __forceinline__ void build_child_row(const VariationParams& P, int32_t* __restrict__ pool,
+                                                const int32_t* __restrict__ parent, const int32_t* __restrict__ child,
+                                                const int32_t* __restrict__ partner, int k, int row, uint64_t* keys) {
+    if (threadIdx.x < 4)
+        keys[threadIdx.x] = stream_key(P.seed, P.generation, GAPA_ROLE_SELECT + threadIdx.x, static_cast<uint64_t>(row)) + kGolden;
+    __syncthreads();
+    const uint64_t ks = keys[0], kc = keys[1], km = keys[2], ki = keys[3];
+    const bool eda = partner == nullptr;
+    const int32_t* mine = pool + static_cast<size_t>(parent[row]) * k;
+    const int32_t* theirs = eda ? mine : pool + static_cast<size_t>(parent[partner[row]]) * k;
+    int32_t* dst = pool + static_cast<size_t>(child[row]) * k;
+    if ((k & 3) == 0) {  // slots are 16-byte aligned when k is a multiple of 4
+        const int4* mine4 = reinterpret_cast<const int4*>(mine);
+        const int4* theirs4 = reinterpret_cast<const int4*>(theirs);
+        int4* dst4 = reinterpret_cast<int4*>(dst);
+        for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < (k >> 2); q += gridDim.x * blockDim.x) {
+            const int4 a = mine4[q];
+            const int4 b = eda ? a : theirs4[q];
+            const int av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+            int r[4];
+            uint64_t prod = kCounterStep * (static_cast<uint64_t>(q) * 4 + 1);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                r[t] = child_gene(P, pool, parent, k, 4 * q + t, av[t], bv[t], eda, ks, kc, km, ki, prod);
+                prod += kCounterStep;
+            }
+            dst4[q] = make_int4(r[0], r[1], r[2], r[3]);
+        }
+    } else {
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x)
+            dst[j] = child_gene(P, pool, parent, k, j, mine[j], theirs[j], eda, ks, kc, km, ki,
+                                kCounterStep * (static_cast<uint64_t>(j) + 1));
+    }
+}
+
+// children of rows [row_first, row_first + gridDim.y)
+__global__ void __launch_bounds__(kSlotThreads) k_ga_slots_variation(VariationParams P, int32_t* __restrict__ pool,
+                                                                     const int32_t* __restrict__ parent,
+                                                                     const int32_t* __restrict__ child,
+                                                                     const int32_t* __restrict__ partner, int k, int row_first) {
+    __shared__ uint64_t keys[4];
+    build_child_row(P, pool, parent, child, partner, k, row_first + blockIdx.y, keys);
+}
+
+// Stable best-first position of every stacked row (parents 0..s-1, children s..2s-1):
+// order[rank] = stacked index; originals precede children on ties (ga_ops.cpp:194-201).
+static constexpr int kSplit = 8;
+__global__ void __launch_bounds__(kSlotThreads) k_ga_slots_rank(const double* __restrict__ fit, const double* __restrict__ fit_m,
+                                                                int s, int minimize, int32_t* __restrict__ order, int* status) {
+    __shared__ double tile[kSlotThreads];
+    const int x = blockIdx.x * (kSlotThreads / kSplit) + threadIdx.x / kSplit, part = threadIdx.x % kSplit;
+    const int total = 2 * s;
+    const double mine = x < total ? (x < s ? fit[x] : fit_m[x - s]) : 0.0;
+    if (x < total && isnan(mine)) *status = GAPA_CUDA_E_NAN;
+    int rank = 0;
+    for (int t0 = 0; t0 < total; t0 += kSlotThreads) {
+        __syncthreads();
+        const int y = t0 + threadIdx.x;
+        if (y < total) tile[threadIdx.x] = y < s ? fit[y] : fit_m[y - s];
+        __syncthreads();
+        const int lim = min(kSlotThreads, total - t0);
+        for (int t = part; t < lim; t += kSplit) {
+            const double other = tile[t];
+            const bool before = minimize ? other < mine : other > mine;
+            rank += before || (other == mine && t0 + t < x);
+        }
+    }
+    for (int off = kSplit / 2; off; off >>= 1) rank += __shfl_down_sync(0xffffffffu, rank, off, kSplit);
+    if (x < total && part == 0) order[rank] = x;
+}
+
+// Survivors that this rank did not build (children of rows outside [block_lo, block_hi)).
+__global__ void __launch_bounds__(kSlotThreads) k_ga_slots_rebuild(VariationParams P, int32_t* __restrict__ pool,
+                                                                   const int32_t* __restrict__ parent,
+                                                                   const int32_t* __restrict__ child,
+                                                                   const int32_t* __restrict__ partner, int k, int s,
+                                                                   const int32_t* __restrict__ order, int block_lo, int block_hi) {
+    __shared__ uint64_t keys[4];
+    const int x = order[blockIdx.y];  // blockIdx.y = rank < s: a survivor
+    const int row = x - s;
+    if (x < s || (row >= block_lo && row < block_hi)) return;
+    build_child_row(P, pool, parent, child, partner, k, row, keys);
+}
+
+// next parent table = slots of the s best, next child table = slots of the s others (now free)
+__global__ void __launch_bounds__(kSlotThreads) k_ga_slots_commit(const int32_t* __restrict__ parent, const int32_t* __restrict__ child,
+                                                                  const double* __restrict__ fit, const double* __restrict__ fit_m, int s,
+                                                                  const int32_t* __restrict__ order, int32_t* __restrict__ next_parent,
+                                                                  int32_t* __restrict__ next_child, double* __restrict__ next_fit) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= s) return;
+    const int keep = order[r], drop = order[s + r];
+    next_parent[r] = keep < s ? parent[keep] : child[keep - s];
+    next_fit[r] = keep < s ? fit[keep] : fit_m[keep - s];
+    next_child[r] = drop < s ? parent[drop] : child[drop - s];
+}
+
+__global__ void __launch_bounds__(kSlotThreads) k_ga_slots_identity(int s, int32_t* parent, int32_t* child) {
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r < s) {
+        parent[r] = r;
+        child[r] = s + r;
+    }
+}
+
+// dense row-major copy of the rows a table names (population.hpp:12-40)
+__global__ void __launch_bounds__(kSlotThreads) k_ga_slots_gather(const int32_t* __restrict__ pool, const int32_t* __restrict__ table,
+                                                                  int k, int32_t* __restrict__ out) {
+    const int32_t* from = pool + static_cast<size_t>(table[blockIdx.y]) * k;
+    int32_t* to = out + static_cast<size_t>(blockIdx.y) * k;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) to[j] = from[j];
+}
+
+static dim3 slot_grid(int cols, int rows) {
+    const int per_block = kSlotThreads * 8;
+    return dim3(std::max(1, std::min((cols + per_block - 1) / per_block, 65535)), rows);
+}
+
+static VariationParams make_params(double pc, double pm, uint32_t pool_size, int s, uint64_t seed, uint64_t generation) {
+    const uint64_t tc = bernoulli_threshold(pc), tm = bernoulli_threshold(pm);
+    VariationParams P;
+    P.pc_always = tc >= (1ull << 53);
+    P.pm_always = tm >= (1ull << 53);
+    P.pc_limit = P.pc_always ? ~0ull : tc << 11;
+    P.pm_limit = P.pm_always ? ~0ull : tm << 11;
+    P.pool_size = pool_size;
+    P.s = static_cast<uint32_t>(s);
+    P.seed = seed;
+    P.generation = generation;
+    return P;
+}
+
+// ---- launchers shared with run.cu (no synchronisation) ---------------------------------------------------
+int launch_slots_identity(int s, int32_t* parent, int32_t* child, cudaStream_t st) {
+    GAPA_LAUNCH(k_ga_slots_identity, (s + kSlotThreads - 1) / kSlotThreads, kSlotThreads, 0, st, s, parent, child);
+    return GAPA_CUDA_OK;
+}
+int launch_slots_variation(int32_t* pool, const int32_t* parent, const int32_t* child, const int32_t* partner, int s, int k,
+                           int row_first, int row_count, double pc, double pm, uint32_t pool_size, uint64_t seed,
+                           uint64_t generation, cudaStream_t st) {
+    if (row_count == 0 || k == 0) return GAPA_CUDA_OK;
+    GAPA_LAUNCH(k_ga_slots_variation, slot_grid((k & 3) ? k : k / 4, row_count), kSlotThreads, 0, st,
+                make_params(pc, pm, pool_size, s, seed, generation), pool, parent, child, partner, k, row_first);
+    return GAPA_CUDA_OK;
+}
+int launch_slots_elitism(int32_t* pool, const int32_t* parent, const int32_t* child, const int32_t* partner, int s, int k,
+                         int block_lo, int block_hi, const double* fit, const double* fit_m, int minimize, double pc, double pm,
+                         uint32_t pool_size, uint64_t seed, uint64_t generation, int32_t* next_parent, int32_t* next_child,
+                         double* next_fit, int32_t* order, int* status, cudaStream_t st) {
+    constexpr int per_block = kSlotThreads / kSplit;
+    GAPA_LAUNCH(k_ga_slots_rank, (2 * s + per_block - 1) / per_block, kSlotThreads, 0, st, fit, fit_m, s, minimize, order, status);
+    if ((block_lo > 0 || block_hi < s) && k > 0)
+        GAPA_LAUNCH(k_ga_slots_rebuild, slot_grid((k & 3) ? k : k / 4, s), kSlotThreads, 0, st,
+                    make_params(pc, pm, pool_size, s, seed, generation), pool, parent, child, partner, k, s, order, block_lo, block_hi);
+    GAPA_LAUNCH(k_ga_slots_commit, (s + kSlotThreads - 1) / kSlotThreads, kSlotThreads, 0, st, parent, child, fit, fit_m, s, order,
+                next_parent, next_child, next_fit);
+    return GAPA_CUDA_OK;
+}
+int launch_slots_gather(const int32_t* pool, const int32_t* table, int rows, int k, int32_t* out, cudaStream_t st) {
+    if (rows == 0 || k == 0) return GAPA_CUDA_OK;
+    GAPA_LAUNCH(k_ga_slots_gather, slot_grid(k, rows), kSlotThreads, 0, st, pool, table, k, out);
+    return GAPA_CUDA_OK;
+}
+
+}  // namespace gapa_b200
+
+using namespace gapa_b200;
+
+extern "C" {
+
+int gapa_cuda_ga_slots_identity_device(int s, int32_t* parent_dev, int32_t* child_dev, void* stream) {
+    if (s < 1 || !parent_dev || !child_dev) return fail(GAPA_CUDA_E_INVALID, "slots: bad arguments");
+    return launch_slots_identity(s, parent_dev, child_dev, static_cast<cudaStream_t>(stream));
+}
+
+int gapa_cuda_ga_slots_variation_device(int32_t* pool_dev, const int32_t* parent_dev, const int32_t* child_dev,
+                                        const int32_t* partner_dev, int s, int k, int row_first, int row_count, double pc,
+                                        double pm, int32_t pool_size, uint64_t seed, uint64_t generation, void* stream) {
+    if (!(pc >= 0.0 && pc <= 1.0)) return fail(GAPA_CUDA_E_INVALID, "pc must be in [0, 1]");
+    if (!(pm >= 0.0 && pm <= 1.0)) return fail(GAPA_CUDA_E_INVALID, "pm must be in [0, 1]");
+    if (pool_size < 1) return fail(GAPA_CUDA_E_INVALID, "mutate: empty gene pool");
+    if (row_first < 0 || row_count < 0 || row_first + row_count > s) return fail(GAPA_CUDA_E_INVALID, "variation: row block outside the population");
+    return launch_slots_variation(pool_dev, parent_dev, child_dev, partner_dev, s, k, row_first, row_count, pc, pm,
+                                  static_cast<uint32_t>(pool_size), seed, generation, static_cast<cudaStream_t>(stream));
+}
+
+int gapa_cuda_ga_slots_gather_device(const int32_t* pool_dev, const int32_t* table_dev, int rows, int k, int32_t* out_dev,
+                                     void* stream) {
+    if (rows < 0 || k < 0) return fail(GAPA_CUDA_E_INVALID, "gather: negative shape");
+    return launch_slots_gather(pool_dev, table_dev, rows, k, out_dev, static_cast<cudaStream_t>(stream));
+}
+
+}  // extern "C"

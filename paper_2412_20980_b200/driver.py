@@ -3,8 +3,9 @@
 Shape of the reference's M mode (modes.cpp:190-349) mapped onto GPUs:
 
   * the graph (CSR), pool and split are replicated on every GPU;
-  * every rank keeps the WHOLE parent population in its HBM; selection and the elitism ranking
-    are tiny and run redundantly — the operators are keyed by (seed, generation, role, global
+  * every rank keeps the WHOLE parent population in its HBM, in a pool of 2s row slots behind
+    parent / child index tables (elitism permutes indices, genomes are never copied); selection and
+    the elitism ranking are tiny and run redundantly — the operators are keyed by (seed, generation, role, global
     row) (rng.hpp:49-65), so every rank produces bit-identical results;
   * rank r owns rows partition_rows(s, world)[r] (modes.cpp:506-516): it builds (crossover +
     mutate, or eda_sample + mutate) and evaluates only those rows of M_POP;
@@ -51,7 +52,11 @@ class Shard:
 
 
 class CudaOps:
-    """Device ops over torch-owned HBM buffers, on torch's current stream."""
+    """Device ops over torch-owned HBM buffers, on torch's current stream.
+
+    The population store is the slot pool of csrc/slot_kernels.cu: `pool` holds 2s rows, `parent` /
+    `child` are the slot tables; variation writes children into their slots, evaluation reads rows
+    through a table, elitism permutes the tables (no genome is copied)."""
 
     def __init__(self, fitness: FitnessFunction, device_index: int):
         import torch
@@ -73,54 +78,50 @@ class CudaOps:
     def empty_i32(self, count):
         return self.torch.empty(count, dtype=self.torch.int32, device=self.device)
 
-    def init(self, out, seed, generation):
-        s, k = out.shape
-        check(self.lib.gapa_cuda_ga_init_device(self.pool_size, 0, s, k, seed, generation, out.data_ptr(), self._stream()))
+    def init(self, pool, parent, child, s, seed, generation):
+        """parents into slots 0..s-1, tables to the identity (init_population, ga_ops.cpp:31-34)"""
+        k = pool.shape[1]
+        check(self.lib.gapa_cuda_ga_slots_identity_device(s, parent.data_ptr(), child.data_ptr(), self._stream()))
+        check(self.lib.gapa_cuda_ga_init_device(self.pool_size, 0, s, k, seed, generation, pool.data_ptr(), self._stream()))
 
     def select(self, fit, s, minimize, seed, generation, partner):
         check(self.lib.gapa_cuda_ga_select_device(fit.data_ptr(), s, minimize, seed, generation, partner.data_ptr(), None,
                                                   self._stream()))
 
-    def crossover_mutate(self, pop, partner, pc, pm, seed, generation, lo, hi, out):
-        """rows [lo, hi) of M_POP into out[lo:hi] (out is the full-size matrix)"""
-        s, k = pop.shape
-        check(self.lib.gapa_cuda_ga_crossover_mutate_device(pop.data_ptr(), partner.data_ptr(), s, k, lo, hi - lo, pc, pm,
-                                                            self.pool_size, seed, generation, out.data_ptr() + 4 * lo * k,
-                                                            self._stream()))
+    def variation(self, pool, parent, child, partner, s, pc, pm, seed, generation, lo, hi):
+        """children of rows [lo, hi) into their slots; partner None = EDA generation"""
+        check(self.lib.gapa_cuda_ga_slots_variation_device(
+            pool.data_ptr(), parent.data_ptr(), child.data_ptr(), partner.data_ptr() if partner is not None else None, s,
+            pool.shape[1], lo, hi - lo, pc, pm, self.pool_size, seed, generation, self._stream()))
 
-    def eda_mutate(self, pop, pm, seed, generation, lo, hi, scratch, out):
-        """eda_sample (elite = whole population, smoothing) then mutate; rows [lo, hi) into out[lo:hi].
-        eda_sample is evaluated for all rows (it is cheap) so the entry point keeps the reference's shape."""
-        s, k = pop.shape
-        check(self.lib.gapa_cuda_ga_eda_device(pop.data_ptr(), s, k, s, self.pool_size, seed, generation, 1,
-                                               scratch.data_ptr(), self._stream()))
-        check(self.lib.gapa_cuda_ga_mutate_device(scratch.data_ptr() + 4 * lo * k, hi - lo, k, lo, pm, self.pool_size, seed,
-                                                  generation, out.data_ptr() + 4 * lo * k, self._stream()))
-
-    def eval_rows(self, genes, lo, hi, fit_out):
-        """fitness of rows [lo, hi) of `genes` into fit_out[lo:hi]"""
+    def eval_rows(self, pool, table, lo, hi, fit_out):
+        """fitness of the rows table[lo:hi] names into fit_out[lo:hi]"""
         if hi <= lo:
             return
-        k = genes.shape[1]
-        self.fitness.dgraph.eval_batch_device(self.fitness.task, genes.data_ptr() + 4 * lo * k, hi - lo, k,
-                                              fit_out.data_ptr() + 8 * lo, self._stream())
+        check(self.lib.gapa_cuda_eval_rows_device(self.fitness.dgraph.handle, self.fitness.task, pool.data_ptr(),
+                                                  table.data_ptr() + 4 * lo, hi - lo, pool.shape[1],
+                                                  fit_out.data_ptr() + 8 * lo, self._stream()))
 
-    def elitism(self, pop, mutated, lo, hi, partner, fit, fit_m, minimize, pc, pm, seed, generation, nxt, next_fit):
-        """`mutated` holds valid rows only in [lo, hi); partner is None on EDA generations"""
-        s, k = pop.shape
-        if lo == 0 and hi == s:
-            check(self.lib.gapa_cuda_ga_elitism_device(pop.data_ptr(), mutated.data_ptr(), s, k, fit.data_ptr(),
-                                                       fit_m.data_ptr(), minimize, nxt.data_ptr(), next_fit.data_ptr(),
-                                                       self._stream()))
-        else:
-            check(self.lib.gapa_cuda_ga_elitism_sharded_device(
-                pop.data_ptr(), mutated.data_ptr() + 4 * lo * k, lo, hi, partner.data_ptr() if partner is not None else None,
-                s, k, fit.data_ptr(), fit_m.data_ptr(), minimize, pc, pm, self.pool_size, seed, generation, nxt.data_ptr(),
-                next_fit.data_ptr(), self._stream()))
+    def elitism(self, pool, parent, child, partner, s, lo, hi, fit, fit_m, minimize, pc, pm, seed, generation, next_parent,
+                next_child, next_fit):
+        check(self.lib.gapa_cuda_ga_slots_elitism_device(
+            pool.data_ptr(), parent.data_ptr(), child.data_ptr(), partner.data_ptr() if partner is not None else None, s,
+            pool.shape[1], lo, hi, fit.data_ptr(), fit_m.data_ptr(), minimize, pc, pm, self.pool_size, seed, generation,
+            next_parent.data_ptr(), next_child.data_ptr(), next_fit.data_ptr(), self._stream()))
+
+    def gather(self, pool, table, rows):
+        """dense [rows, k] matrix of the rows the table names"""
+        out = self.empty_genes(rows, pool.shape[1])
+        check(self.lib.gapa_cuda_ga_slots_gather_device(pool.data_ptr(), table.data_ptr(), rows, pool.shape[1], out.data_ptr(),
+                                                        self._stream()))
+        return out
 
     def stats(self, fit, s, hist, index, iters):
         check(self.lib.gapa_cuda_ga_stats_device(fit.data_ptr(), s, hist.data_ptr() + 8 * index,
                                                  hist.data_ptr() + 8 * (iters + index), self._stream()))
+
+    def last_eval_ms(self) -> float:
+        return self.fitness.dgraph.last_eval_ms()
 
     def to_host(self, t):
         return t.cpu().numpy()
@@ -149,10 +150,9 @@ class ShardedGa:
         self.p, self.ops, self.shard, self.gather = params, ops, shard, gather
         s, k = params.pop_size, params.budget
         self.minimize = 1 if params.direction == Direction.Minimize else 0
-        self.pop = ops.empty_genes(s, k)
-        self.mutated = ops.empty_genes(s, k)
-        self.next = ops.empty_genes(s, k)
-        self.crossed = ops.empty_genes(s, k) if params.eda_interval else None
+        self.pool = ops.empty_genes(2 * s, k)          # 2s row slots: s parents + s children
+        self.parent, self.child = ops.empty_i32(s), ops.empty_i32(s)
+        self.next_parent, self.next_child = ops.empty_i32(s), ops.empty_i32(s)
         self.partner = ops.empty_i32(s)
         self.fit = ops.zeros_f64(shard.padded)
         self.fit_m = ops.zeros_f64(shard.padded)
@@ -161,16 +161,16 @@ class ShardedGa:
         self.generation = 0
         self.fitness_batch_calls = 0
 
-    def _evaluate(self, genes, fit):
+    def _evaluate(self, table, fit):
         lo, hi = self.shard.rows
         self.fitness_batch_calls += 1
-        self.ops.eval_rows(genes, lo, hi, fit)
+        self.ops.eval_rows(self.pool, table, lo, hi, fit)
         self.gather(fit, self.shard)
 
     def initialize(self):
         """gen 1 prologue: init_population with generation key 0, then evaluate (modes.cpp:162-165)"""
-        self.ops.init(self.pop, self.p.seed, 0)
-        self._evaluate(self.pop, self.fit)
+        self.ops.init(self.pool, self.parent, self.child, self.p.pop_size, self.p.seed, 0)
+        self._evaluate(self.parent, self.fit)
 
     def step(self):
         """one generation: select -> crossover -> mutate -> evaluate(M_POP) -> elitism"""
@@ -180,18 +180,22 @@ class ShardedGa:
         s = p.pop_size
         lo, hi = self.shard.rows
         eda_gen = bool(p.eda_interval and gen % p.eda_interval == 0)  # modes.cpp:31-33,167-168
-        if eda_gen:
-            ops.eda_mutate(self.pop, p.pm, p.seed, gen, lo, hi, self.crossed, self.mutated)
-        else:
+        partner = None if eda_gen else self.partner
+        if not eda_gen:
             ops.select(self.fit, s, self.minimize, p.seed, gen, self.partner)
-            ops.crossover_mutate(self.pop, self.partner, p.pc, p.pm, p.seed, gen, lo, hi, self.mutated)
-        self._evaluate(self.mutated, self.fit_m)
-        ops.elitism(self.pop, self.mutated, lo, hi, None if eda_gen else self.partner, self.fit, self.fit_m, self.minimize,
-                    p.pc, p.pm, p.seed, gen, self.next, self.fit_next)
-        self.pop, self.next = self.next, self.pop
+        ops.variation(self.pool, self.parent, self.child, partner, s, p.pc, p.pm, p.seed, gen, lo, hi)
+        self._evaluate(self.child, self.fit_m)
+        ops.elitism(self.pool, self.parent, self.child, partner, s, lo, hi, self.fit, self.fit_m, self.minimize, p.pc, p.pm,
+                    p.seed, gen, self.next_parent, self.next_child, self.fit_next)
+        self.parent, self.next_parent = self.next_parent, self.parent
+        self.child, self.next_child = self.next_child, self.child
         self.fit, self.fit_next = self.fit_next, self.fit
         if gen <= p.iterations:
             ops.stats(self.fit, s, self.hist, gen - 1, p.iterations)
+
+    def population(self):
+        """the parents as a dense best-first matrix (PopulationMatrix)"""
+        return self.ops.gather(self.pool, self.parent, self.p.pop_size)
 
     def run(self) -> RunResult:
         self.initialize()
@@ -202,7 +206,7 @@ class ShardedGa:
     def result(self) -> RunResult:
         s, it = self.p.pop_size, self.p.iterations
         hist = np.asarray(self.ops.to_host(self.hist))
-        pop = np.asarray(self.ops.to_host(self.pop))
+        pop = np.asarray(self.ops.to_host(self.population()))
         fit = np.asarray(self.ops.to_host(self.fit))[:s]
         return RunResult(pop, fit, pop[0].copy(), float(fit[0]), hist[:it].copy(), hist[it:2 * it].copy(),
                          self.fitness_batch_calls)

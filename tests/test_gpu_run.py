@@ -141,7 +141,7 @@ def test_sharded_driver_recomputes_foreign_rows(gp, oracle, cuda_device, eda):
 
         def gather(fit, shard_, box=box, other_lo=other_lo, other_hi=other_hi):
             ga = box["ga"]
-            pop = ga.pop.cpu().numpy()
+            pop = ga.population().cpu().numpy()
             gen = ga.generation
             if gen == 0:
                 rows = pop[other_lo:other_hi]

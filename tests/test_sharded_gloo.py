@@ -24,33 +24,38 @@ from paper_2412_20980_b200.api import GAParams
 from paper_2412_20980_b200.driver import ShardedGa, Shard, torch_allgather
 
 class OracleOps:
-    """test stand-in for CudaOps: same interface, numpy/oracle arithmetic on CPU tensors"""
+    """test stand-in for CudaOps: same slot-pool interface, numpy/oracle arithmetic on CPU tensors"""
     def __init__(self, o, ctx, task, pool_size):
         self.o, self.ctx, self.task, self.pool_size = o, ctx, task, pool_size
-    def empty_genes(self, r, c): return torch.zeros((r, c), dtype=torch.int32)
+    def empty_genes(self, r, c): return torch.full((r, c), -7, dtype=torch.int32)
     def zeros_f64(self, n): return torch.zeros(n, dtype=torch.float64)
     def empty_i32(self, n): return torch.zeros(n, dtype=torch.int32)
-    def init(self, out, seed, gen): out.copy_(torch.from_numpy(self.o.init_population(self.pool_size, out.shape[0], out.shape[1], seed, gen)))
+    def init(self, pool, parent, child, s, seed, gen):
+        parent.copy_(torch.arange(s, dtype=torch.int32)); child.copy_(torch.arange(s, 2 * s, dtype=torch.int32))
+        pool[:s] = torch.from_numpy(self.o.init_population(self.pool_size, s, pool.shape[1], seed, gen))
     def select(self, fit, s, minimize, seed, gen, partner):
         partner.copy_(torch.from_numpy(self.o.roulette_pick(fit[:s].numpy(), bool(minimize), seed, gen)))
-    def _variation(self, pop, partner, pc, pm, seed, gen):
-        c = (self.o.crossover(pop.numpy(), partner.numpy(), pc, seed, gen) if partner is not None
-             else self.o.eda_sample(pop.numpy(), pop.shape[0], self.pool_size, seed, gen, True))
+    def _children(self, pool, parent, partner, pc, pm, seed, gen):
+        pop = pool[parent.long()].numpy()
+        c = (self.o.crossover(pop, partner.numpy(), pc, seed, gen) if partner is not None
+             else self.o.eda_sample(pop, pop.shape[0], self.pool_size, seed, gen, True))
         return self.o.mutate_block(c, 0, pm, self.pool_size, seed, gen)
-    def crossover_mutate(self, pop, partner, pc, pm, seed, gen, lo, hi, out):
-        out.fill_(-7)  # rows outside [lo, hi) are NOT built on this rank
-        out[lo:hi] = torch.from_numpy(self._variation(pop, partner, pc, pm, seed, gen)[lo:hi])
-    def eda_mutate(self, pop, pm, seed, gen, lo, hi, scratch, out):
-        out.fill_(-7)
-        out[lo:hi] = torch.from_numpy(self._variation(pop, None, 0.0, pm, seed, gen)[lo:hi])
-    def eval_rows(self, genes, lo, hi, fit_out):
-        if hi > lo: fit_out[lo:hi] = torch.from_numpy(self.o.eval_batch(self.ctx, self.task, genes[lo:hi].numpy()))
-    def elitism(self, pop, mut, lo, hi, partner, fit, fit_m, minimize, pc, pm, seed, gen, nxt, next_fit):
-        s = pop.shape[0]
-        full = self._variation(pop, partner, pc, pm, seed, gen)  # foreign rows are recomputed, not fetched
-        assert np.array_equal(full[lo:hi], mut[lo:hi].numpy())
-        a, b = self.o.elitism(pop.numpy(), full, fit[:s].numpy(), fit_m[:s].numpy(), bool(minimize))
-        nxt.copy_(torch.from_numpy(a)); next_fit[:s] = torch.from_numpy(b)
+    def variation(self, pool, parent, child, partner, s, pc, pm, seed, gen, lo, hi):
+        rows = self._children(pool, parent, partner, pc, pm, seed, gen)
+        pool[child[lo:hi].long()] = torch.from_numpy(rows[lo:hi])  # only this rank's block is built
+    def eval_rows(self, pool, table, lo, hi, fit_out):
+        if hi > lo: fit_out[lo:hi] = torch.from_numpy(self.o.eval_batch(self.ctx, self.task, pool[table[lo:hi].long()].numpy()))
+    def elitism(self, pool, parent, child, partner, s, lo, hi, fit, fit_m, minimize, pc, pm, seed, gen, next_parent, next_child, next_fit):
+        f = np.concatenate([fit[:s].numpy(), fit_m[:s].numpy()])
+        order = np.argsort(f if minimize else -f, kind="stable")
+        slots = torch.cat([parent, child])
+        full = self._children(pool, parent, partner, pc, pm, seed, gen)
+        assert np.array_equal(full[lo:hi], pool[child[lo:hi].long()].numpy())
+        for x in order[:s]:                      # foreign survivors are rebuilt, not fetched
+            if x >= s and not (lo <= x - s < hi): pool[int(child[x - s])] = torch.from_numpy(full[x - s])
+        next_parent.copy_(slots[order[:s]]); next_child.copy_(slots[order[s:]])
+        next_fit[:s] = torch.from_numpy(f[order[:s]])
+    def gather(self, pool, table, rows): return pool[table[:rows].long()].clone()
     def stats(self, fit, s, hist, index, iters):
         total = 0.0
         for x in fit[:s].tolist(): total += x
