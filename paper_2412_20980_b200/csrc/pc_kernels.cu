@@ -61,6 +61,7 @@ struct PcCounters {
     int overflow;
     int range_error;
     int changed;  // any sweep since the last reset set a new reached bit
+    unsigned int n_incomplete;  // 256-vertex chunks the recording sweep still has to visit
 };
 
 struct PcScratch {
@@ -332,22 +333,37 @@ __global__ void __cluster_dims__(kPrefixCluster, 1, 1) __launch_bounds__(kPrefix
 #ifndef GAPA_SWEEP_MIN_BLOCKS
 #define GAPA_SWEEP_MIN_BLOCKS 4
 #endif
+struct SweepArgs {
+    const int32_t* row_ptr;
+    const int32_t* col_idx;
+    int n, sgroups, interleave;
+    const word_t* alive;
+    Rec* reached;
+    int* unreached;
+    int32_t *entry_of, *left_v, *left_g;
+    word_t* left_w;
+    int32_t *left_base, *parent, *comp_size;
+    unsigned cap_entries, cap_slots;
+    int slot0;
+    PcCounters* counters;
+    int2* incomplete;  // (super-group, chunk) list written by the ordinary sweep, read by the recording one
+    int record;        // ordinary sweep: append incomplete chunks to the list
+};
+
 template <bool FINAL>
-__global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep(const int32_t* __restrict__ row_ptr,
-                                                       const int32_t* __restrict__ col_idx, int n, int sgroups,
-                                                       int interleave, const word_t* __restrict__ alive, Rec* reached,
-                                                       int* unreached, int32_t* entry_of, int32_t* left_v, int32_t* left_g,
-                                                       word_t* left_w, int32_t* left_base, int32_t* parent,
-                                                       int32_t* comp_size, unsigned cap_entries, unsigned cap_slots,
-                                                       int slot0, PcCounters* counters, unsigned char* block_done) {
-    __shared__ int hist[kPack * kBits];
-    const int sg = blockIdx.y * interleave + (blockIdx.x % interleave);
-    if (sg >= sgroups) return;
-    // block_done[sg][chunk] = every (vertex, individual) of the chunk is reached or removed; set by
-    // the ordinary sweep so that the recording sweep skips those chunks without touching HBM.
-    const size_t done_index = static_cast<size_t>(sg) * (gridDim.x / interleave) + blockIdx.x / interleave;
-    if (FINAL && block_done && block_done[done_index]) return;
-    const int v = (blockIdx.x / interleave) * kThreads + threadIdx.x;
+__device__ __forceinline__ void sweep_chunk(const SweepArgs& A, int sg, int chunk, int* hist) {
+    const int32_t* __restrict__ row_ptr = A.row_ptr;
+    const int32_t* __restrict__ col_idx = A.col_idx;
+    const word_t* __restrict__ alive = A.alive;
+    Rec* reached = A.reached;
+    PcCounters* counters = A.counters;
+    const int n = A.n, slot0 = A.slot0;
+    const unsigned cap_entries = A.cap_entries, cap_slots = A.cap_slots;
+    int* unreached = A.unreached;
+    int32_t *entry_of = A.entry_of, *left_v = A.left_v, *left_g = A.left_g, *left_base = A.left_base, *parent = A.parent,
+            *comp_size = A.comp_size;
+    word_t* left_w = A.left_w;
+    const int v = chunk * kThreads + threadIdx.x;
     if (FINAL) {
         hist[threadIdx.x] = 0;  // kThreads == kPack * kBits
         __syncthreads();
@@ -416,8 +432,26 @@ __global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep(co
     const int left = __syncthreads_or(any_left);
     if (FINAL) {
         if (left && hist[threadIdx.x]) atomicAdd(&unreached[sg * kPack * kBits + threadIdx.x], hist[threadIdx.x]);
-    } else if (threadIdx.x == 0) {
-        block_done[done_index] = left ? 0 : 1;
+    } else if (left && A.record && threadIdx.x == 0) {
+        A.incomplete[atomicAdd(&counters->n_incomplete, 1u)] = make_int2(sg, chunk);
+    }
+}
+
+// ordinary sweep: blocks in ascending vertex order, `interleave` super-groups share blockIdx.x
+__global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep(SweepArgs A) {
+    const int sg = blockIdx.y * A.interleave + (blockIdx.x % A.interleave);
+    if (sg >= A.sgroups) return;
+    sweep_chunk<false>(A, sg, blockIdx.x / A.interleave, nullptr);
+}
+
+// recording sweep: a persistent grid walks the list of incomplete chunks
+__global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_record(SweepArgs A) {
+    __shared__ int hist[kPack * kBits];
+    const unsigned total = A.counters->n_incomplete;
+    for (unsigned i = blockIdx.x; i < total; i += gridDim.x) {
+        const int2 item = A.incomplete[i];
+        __syncthreads();  // hist of the previous chunk has been flushed
+        sweep_chunk<true>(A, item.x, item.y, hist);
     }
 }
 
@@ -563,6 +597,7 @@ __global__ void k_pc_reset(int groups, int32_t* parent, int32_t* comp_size, int*
         counters->n_slots = 0u;
         counters->overflow = 0;
         counters->changed = 0;
+        counters->n_incomplete = 0u;
         if (first) counters->range_error = 0;
     }
 }
@@ -819,19 +854,22 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             }
             const int il = std::min(std::max(1, s->interleave / kPack), sgroups);
             const dim3 grid(((n + kThreads - 1) / kThreads) * il, (sgroups + il - 1) / il);
-            GAPA_TRY(s->block_done.ensure(static_cast<size_t>(sgroups) * ((n + kThreads - 1) / kThreads)));
-            unsigned char* block_done = s->block_done.as<unsigned char>();
-            auto sweep = [&](bool final_pass) -> int {
-                if (final_pass)
-                    GAPA_LAUNCH(k_pc_sweep<true>, grid, kThreads, 0, stream, g_row_ptr, g_col_idx, n, sgroups, il,
-                                alive_rec, reached_rec, s->unreached.as<int>(), s->entry_of.as<int32_t>(),
-                                s->left_v.as<int32_t>(), s->left_g.as<int32_t>(), s->left_w.as<word_t>(),
-                                s->left_base.as<int32_t>(), s->parent.as<int32_t>(), s->comp_size.as<int32_t>(),
-                                static_cast<unsigned>(s->cap_entries), static_cast<unsigned>(s->cap_slots), slot0, counters, block_done);
-                else
-                    GAPA_LAUNCH(k_pc_sweep<false>, grid, kThreads, 0, stream, g_row_ptr, g_col_idx, n, sgroups, il,
-                                alive_rec, reached_rec, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr, nullptr,
-                                0u, 0u, slot0, counters, block_done);
+            GAPA_TRY(s->block_done.ensure(sizeof(int2) * static_cast<size_t>(sgroups) * ((n + kThreads - 1) / kThreads)));
+            SweepArgs A;
+            A.row_ptr = g_row_ptr; A.col_idx = g_col_idx; A.n = n; A.sgroups = sgroups; A.interleave = il;
+            A.alive = alive_rec; A.reached = reached_rec; A.unreached = s->unreached.as<int>();
+            A.entry_of = s->entry_of.as<int32_t>(); A.left_v = s->left_v.as<int32_t>(); A.left_g = s->left_g.as<int32_t>();
+            A.left_w = s->left_w.as<word_t>(); A.left_base = s->left_base.as<int32_t>(); A.parent = s->parent.as<int32_t>();
+            A.comp_size = s->comp_size.as<int32_t>(); A.slot0 = slot0; A.counters = counters;
+            A.incomplete = s->block_done.as<int2>(); A.record = 0;
+            auto sweep = [&](bool final_pass, bool record) -> int {
+                A.cap_entries = static_cast<unsigned>(s->cap_entries);  // may have grown after an overflow retry
+                A.cap_slots = static_cast<unsigned>(s->cap_slots);
+                A.left_v = s->left_v.as<int32_t>(); A.left_g = s->left_g.as<int32_t>(); A.left_w = s->left_w.as<word_t>();
+                A.left_base = s->left_base.as<int32_t>(); A.parent = s->parent.as<int32_t>(); A.comp_size = s->comp_size.as<int32_t>();
+                A.record = record ? 1 : 0;
+                if (final_pass) GAPA_LAUNCH(k_pc_record, sm * 4, kThreads, 0, stream, A);
+                else GAPA_LAUNCH(k_pc_sweep, grid, kThreads, 0, stream, A);
                 return GAPA_CUDA_OK;
             };
             // With the prefix closed, ONE ordered sweep reaches nearly everything on power-law graphs and
@@ -842,8 +880,9 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             const unsigned many = static_cast<unsigned>(std::max<size_t>(8192, words / 512));
             PcCounters h{};
             for (int round = 0;; ++round) {
-                for (int i = 0; i < (round == 0 ? 1 : 2); ++i) GAPA_TRY(sweep(false));
-                GAPA_TRY(sweep(true));
+                const int ordinary = round == 0 ? 1 : 2;
+                for (int i = 0; i < ordinary; ++i) GAPA_TRY(sweep(false, i + 1 == ordinary));
+                GAPA_TRY(sweep(true, false));
                 GAPA_CUDA_TRY(cudaMemcpyAsync(&h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
                 GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
                 if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
