@@ -156,6 +156,14 @@ int gapa_cuda_ga_slots_variation_device(int32_t* pool_dev, const int32_t* parent
                                         const int32_t* partner_dev, int s, int k, int row_first, int row_count,
                                         double pc, double pm, int32_t pool_size, uint64_t seed, uint64_t generation,
                                         void* stream);
+/* variation + evaluation of the same row block in one call: builds the children of rows
+ * [row_first, row_first + row_count) into their slots and writes their fitness to
+ * fit_block_dev[0 .. row_count).  For the PC / MCN tasks the child genes go to HBM and into the
+ * shared-memory removal bitmap in one fused kernel (the row is never read back). */
+int gapa_cuda_ga_slots_variation_eval_device(gapa_cuda_ctx* ctx, int task, int32_t* pool_dev, const int32_t* parent_dev,
+                                             const int32_t* child_dev, const int32_t* partner_dev, int s, int k,
+                                             int row_first, int row_count, double pc, double pm, uint64_t seed,
+                                             uint64_t generation, double* fit_block_dev, void* stream);
 /* elitism (ga_ops.cpp:180-212) as a permutation: next_parent = slots of the s best of the 2s stacked
  * rows (stable, originals first on ties), next_child = the s freed slots, next_fit = their fitness.
  * Children of rows outside [block_lo, block_hi) that survive are rebuilt in their slots from the

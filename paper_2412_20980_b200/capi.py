@@ -69,6 +69,8 @@ SIGNATURES = {
     "gapa_cuda_ga_slots_identity_device": (C.c_int, [C.c_int, VP, VP, VP]),
     "gapa_cuda_ga_slots_variation_device": (C.c_int, [VP, VP, VP, VP, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                                       C.c_double, C.c_int32, C.c_uint64, C.c_uint64, VP]),
+    "gapa_cuda_ga_slots_variation_eval_device": (C.c_int, [VP, C.c_int, VP, VP, VP, VP, C.c_int, C.c_int, C.c_int, C.c_int,
+                                                           C.c_double, C.c_double, C.c_uint64, C.c_uint64, VP, VP]),
     "gapa_cuda_ga_slots_elitism_device": (C.c_int, [VP, VP, VP, VP, C.c_int, C.c_int, C.c_int, C.c_int, VP, VP, C.c_int,
                                                     C.c_double, C.c_double, C.c_int32, C.c_uint64, C.c_uint64, VP, VP, VP, VP]),
     "gapa_cuda_ga_slots_gather_device": (C.c_int, [VP, VP, C.c_int, C.c_int, VP, VP]),

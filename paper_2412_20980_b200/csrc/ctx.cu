@@ -10,6 +10,7 @@
 #include <numeric>
 
 #include "internal.cuh"
+#include "variation.cuh"
 
 namespace gapa_b200 {
 
@@ -314,16 +315,20 @@ static int check_task(const gapa_cuda_ctx* c, int task) {
     return fail(GAPA_CUDA_E_INVALID, "unknown fitness task %d", task);
 }
 
-static int eval_rows_locked(gapa_cuda_ctx* c, int task, const GeneRows& genes, int rows, double* out_dev, void* stream) {
+static int eval_rows_locked(gapa_cuda_ctx* c, int task, const GeneRows& genes, int rows, double* out_dev, void* stream,
+                            const VariationSpec* vary = nullptr) {
     std::unique_lock<std::mutex> lock(c->mu, std::defer_lock);
     if (stream != static_cast<void*>(c->stream)) lock.lock();  // the host-buffer form already holds it
     GAPA_CUDA_TRY(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     GAPA_CUDA_TRY(cudaEventRecord(c->ev_start, s));
     int rc;
-    if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) rc = pc_eval(c, task, genes, rows, out_dev, s);
-    else if (task == GAPA_TASK_CDA) rc = cda_eval(c, genes, rows, out_dev, s);
-    else rc = lpa_eval(c, genes, rows, out_dev, s);
+    if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) {
+        rc = pc_eval(c, task, genes, rows, out_dev, s, vary != nullptr, vary);  // builds the children itself
+    } else {
+        if (vary) GAPA_TRY(launch_variation_spec(*vary, genes.cols, rows, s));
+        rc = task == GAPA_TASK_CDA ? cda_eval(c, genes, rows, out_dev, s) : lpa_eval(c, genes, rows, out_dev, s, vary != nullptr);
+    }
     if (rc != GAPA_CUDA_OK) return rc;
     GAPA_CUDA_TRY(cudaEventRecord(c->ev_stop, s));
     GAPA_CUDA_TRY(cudaEventSynchronize(c->ev_stop));
@@ -349,6 +354,28 @@ int gapa_cuda_eval_rows_device(gapa_cuda_ctx* c, int task, const int32_t* pool_d
     if (rows == 0) return GAPA_CUDA_OK;
     if (!out_dev || !slot_dev || (cols > 0 && !pool_dev)) return fail(GAPA_CUDA_E_INVALID, "eval_rows: null buffer");
     return eval_rows_locked(c, task, GeneRows{pool_dev, slot_dev, cols}, rows, out_dev, stream);
+}
+
+int gapa_cuda_ga_slots_variation_eval_device(gapa_cuda_ctx* c, int task, int32_t* pool_dev, const int32_t* parent_dev,
+                                             const int32_t* child_dev, const int32_t* partner_dev, int s, int k, int row_first,
+                                             int row_count, double pc, double pm, uint64_t seed, uint64_t generation,
+                                             double* fit_block_dev, void* stream) {
+    if (!c) return fail(GAPA_CUDA_E_INVALID, "variation_eval: null context");
+    GAPA_TRY(check_task(c, task));
+    if (!(pc >= 0.0 && pc <= 1.0)) return fail(GAPA_CUDA_E_INVALID, "pc must be in [0, 1]");
+    if (!(pm >= 0.0 && pm <= 1.0)) return fail(GAPA_CUDA_E_INVALID, "pm must be in [0, 1]");
+    if (s < 1 || k < 0 || row_first < 0 || row_count < 0 || row_first + row_count > s)
+        return fail(GAPA_CUDA_E_INVALID, "variation_eval: row block outside the population");
+    if (row_count == 0) return GAPA_CUDA_OK;
+    if (!pool_dev || !parent_dev || !child_dev || !fit_block_dev) return fail(GAPA_CUDA_E_INVALID, "variation_eval: null buffer");
+    VariationSpec spec;
+    spec.P = make_variation_params(pc, pm, static_cast<uint32_t>(c->pool_size), s, seed, generation);
+    spec.pool = pool_dev;
+    spec.parent = parent_dev;
+    spec.child = child_dev;
+    spec.partner = partner_dev;
+    spec.row_first = row_first;
+    return eval_rows_locked(c, task, GeneRows{pool_dev, child_dev + row_first, k}, row_count, fit_block_dev, stream, &spec);
 }
 
 int gapa_cuda_eval_batch(gapa_cuda_ctx* c, int task, const int32_t* genes_host, int rows, int cols, double* out_host) {

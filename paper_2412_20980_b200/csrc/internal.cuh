@@ -174,8 +174,12 @@ namespace gapa_b200 {
 // `trusted` = the genes were produced by this library's own operators (always inside the pool),
 // so evaluators that need no other host decision skip the range-status readback and stay
 // asynchronous.
+// `vary` (optional): the rows are children that do not exist yet — the evaluator builds them into
+// their slots first (fused with the mask build where the kernel structure allows it).
+struct VariationSpec;
 int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_dev, cudaStream_t stream,
-            bool trusted = false);
+            bool trusted = false, const VariationSpec* vary = nullptr);
+int launch_variation_spec(const VariationSpec& spec, int k, int rows, cudaStream_t stream);  // slot_kernels.cu
 int lpa_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream, bool trusted = false);
 int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream);
 void pc_free(gapa_cuda_ctx* ctx);

@@ -40,6 +40,7 @@
 #include <cooperative_groups.h>
 
 #include "internal.cuh"
+#include "variation.cuh"
 
 namespace cg = cooperative_groups;
 
@@ -133,6 +134,70 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(GeneRows genes,
     }
     for (int off = 16; off; off >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, off);
     if ((threadIdx.x & 31) == 0 && distinct) atomicAdd(&removed_count[row], distinct);
+}
+
+// Fused variation + mask build for the generation loop: the CTA BUILDS child row
+// `V.row_first + blockIdx.x` (crossover + mutate, or eda + mutate — variation.cuh), stores each gene
+// to the child's slot and sets it in the shared-memory bitmap in the same pass.  The hash arithmetic
+// of the variation (integer pipes) and the shared-memory atomics of the mask build (LSU) overlap
+// inside one kernel, and the 4 k bytes of the child row are never read back from HBM.
+__global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask_vary(VariationSpec V, int k, const int32_t* __restrict__ gene_map,
+                                                                  int n, int words_per_row, word_t* __restrict__ removed,
+                                                                  int* removed_count) {
+    __shared__ uint64_t keys[4];
+    const int local = blockIdx.x, row = V.row_first + local;
+    const int words64 = (n + 63) >> 6;
+    for (int w = threadIdx.x; w < 2 * words64; w += kMaskThreads) pc_smem_bits[w] = 0u;
+    if (threadIdx.x < 4)
+        keys[threadIdx.x] = stream_key(V.P.seed, V.P.generation, GAPA_ROLE_SELECT + threadIdx.x, static_cast<uint64_t>(row)) + kGolden;
+    __syncthreads();
+    const uint64_t ks = keys[0], kc = keys[1], km = keys[2], ki = keys[3];
+    const bool eda = V.partner == nullptr;
+    const int32_t* mine = V.pool + static_cast<size_t>(V.parent[row]) * k;
+    const int32_t* theirs = eda ? mine : V.pool + static_cast<size_t>(V.parent[V.partner[row]]) * k;
+    int32_t* dst = V.pool + static_cast<size_t>(V.child[row]) * k;
+    auto mark = [&](int gene) {
+        const int node = gene_map ? gene_map[gene] : gene;
+        atomicOr(&pc_smem_bits[node >> 5], 1u << (node & 31));
+    };
+    if ((k & 3) == 0) {
+        const int4* mine4 = reinterpret_cast<const int4*>(mine);
+        const int4* theirs4 = reinterpret_cast<const int4*>(theirs);
+        int4* dst4 = reinterpret_cast<int4*>(dst);
+        for (int q = threadIdx.x; q < (k >> 2); q += kMaskThreads) {
+            const int4 a = mine4[q];
+            const int4 b = eda ? a : theirs4[q];
+            const int av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+            int r[4];
+            uint64_t prod = kCounterStep * (static_cast<uint64_t>(q) * 4 + 1);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) {
+                r[t] = child_gene(V.P, V.pool, V.parent, k, 4 * q + t, av[t], bv[t], eda, ks, kc, km, ki, prod);
+                prod += kCounterStep;
+            }
+            dst4[q] = make_int4(r[0], r[1], r[2], r[3]);
+#pragma unroll
+            for (int t = 0; t < 4; ++t) mark(r[t]);
+        }
+    } else {
+        for (int j = threadIdx.x; j < k; j += kMaskThreads) {
+            const int gsel = child_gene(V.P, V.pool, V.parent, k, j, mine[j], theirs[j], eda, ks, kc, km, ki,
+                                        kCounterStep * (static_cast<uint64_t>(j) + 1));
+            dst[j] = gsel;
+            mark(gsel);
+        }
+    }
+    __syncthreads();
+    const word_t* bits64 = reinterpret_cast<const word_t*>(pc_smem_bits);
+    word_t* out = removed + static_cast<size_t>(local) * words_per_row;
+    int distinct = 0;
+    for (int w = threadIdx.x; w < words64; w += kMaskThreads) {
+        const word_t x = bits64[w];
+        distinct += __popcll(x);
+        out[w] = x;
+    }
+    for (int off = 16; off; off >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, off);
+    if ((threadIdx.x & 31) == 0 && distinct) atomicAdd(&removed_count[local], distinct);
 }
 
 // mask build, step 2: 64 individuals x 64 vertices bit transpose in registers.
@@ -750,7 +815,8 @@ static int ensure_order(gapa_cuda_ctx* ctx, PcScratch* s) {
     return GAPA_CUDA_OK;
 }
 
-int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_dev, cudaStream_t stream, bool trusted) {
+int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_dev, cudaStream_t stream, bool trusted,
+            const VariationSpec* vary) {
     const int cols = genes.cols;
     if (!ctx->pc) ctx->pc = new PcScratch();
     PcScratch* s = ctx->pc;
@@ -763,12 +829,14 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         // the shared-memory bitmap may use most of the SM (one CTA per individual)
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
         s->configured = true;
     }
     const int n = ctx->n;
     const int sm = ctx->sm_count;
     if (n > 0 && n <= kSmallMaxN && s->small_path) {
+        if (vary) GAPA_TRY(launch_variation_spec(*vary, cols, rows, stream));
         const size_t smem = sizeof(int32_t) * (2 * static_cast<size_t>(n) + ((n + 31) >> 5) + 1);
         GAPA_TRY(s->counters.ensure(sizeof(PcCounters)));
         PcCounters* counters = s->counters.as<PcCounters>();
@@ -832,10 +900,22 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
 
         if (n > 0) {
             // ---- masks ------------------------------------------------------------------
+            if (vary && chunks == 1 && cols > 0) {
+                VariationSpec pass = *vary;
+                pass.row_first += row0;
+                GAPA_LAUNCH(k_pc_bitmask_vary, crows, kMaskThreads, static_cast<size_t>(chunk_bits) / 8, stream, pass, cols, g_gene_map,
+                            n, words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>());
+            } else {
+                if (vary) {
+                    VariationSpec pass = *vary;
+                    pass.row_first += row0;
+                    GAPA_TRY(launch_variation_spec(pass, cols, crows, stream));
+                }
             GAPA_LAUNCH(k_pc_bitmask, dim3(chunks, crows), kMaskThreads, static_cast<size_t>(chunk_bits) / 8, stream,
                         genes.from(row0), g_gene_map,
                         ctx->pool_size, n, chunk_bits, words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>(),
                         counters);
+            }
             GAPA_LAUNCH(k_pc_transpose, dim3((words_per_row + kTransThreads - 1) / kTransThreads, pgroups), kTransThreads,
                         sizeof(word_t) * kBits * (kTransThreads + 1), stream, s->removed.as<word_t>(), words_per_row, n, crows, alive);
             GAPA_CUDA_TRY(cudaMemsetAsync(reached, 0, sizeof(word_t) * words, stream));

@@ -16,6 +16,7 @@
 #include <cmath>
 
 #include "internal.cuh"
+#include "variation.cuh"
 
 namespace gapa_b200 {
 int launch_init(uint32_t, int, int, int, uint64_t, uint64_t, int32_t*, cudaStream_t);
@@ -125,13 +126,17 @@ struct EvalTimer {
     }
 };
 
-int eval_rows(gapa_cuda_ctx* ctx, int task, const GeneRows& view, int rows, double* out, cudaStream_t st, EvalTimer* timer) {
+int eval_rows(gapa_cuda_ctx* ctx, int task, const GeneRows& view, int rows, double* out, cudaStream_t st, EvalTimer* timer,
+              const VariationSpec* vary = nullptr) {
     if (rows == 0) return GAPA_CUDA_OK;
     GAPA_TRY(timer->mark(st));
     int rc;
-    if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) rc = pc_eval(ctx, task, view, rows, out, st, true);
-    else if (task == GAPA_TASK_CDA) rc = cda_eval(ctx, view, rows, out, st);
-    else rc = lpa_eval(ctx, view, rows, out, st, true);
+    if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) {
+        rc = pc_eval(ctx, task, view, rows, out, st, true, vary);  // builds the children itself (fused with the mask build)
+    } else {
+        if (vary) GAPA_TRY(launch_variation_spec(*vary, view.cols, rows, st));
+        rc = task == GAPA_TASK_CDA ? cda_eval(ctx, view, rows, out, st) : lpa_eval(ctx, view, rows, out, st, true);
+    }
     GAPA_TRY(rc);
     return timer->mark(st);
 }
@@ -208,9 +213,9 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
     result->fitness_batch_calls = 0;
     result->eval_seconds = 0.0;
     EvalTimer timer;
-    auto evaluate = [&](const int32_t* table, double* fit_all) -> int {  // rows [lo, hi) named by `table`
+    auto evaluate = [&](const int32_t* table, double* fit_all, const VariationSpec* vary = nullptr) -> int {  // rows [lo, hi) named by `table`
         ++result->fitness_batch_calls;
-        GAPA_TRY(eval_rows(ctx, p->task, GeneRows{pool_rows, table + lo, k}, hi - lo, fit_all + lo, st, &timer));
+        GAPA_TRY(eval_rows(ctx, p->task, GeneRows{pool_rows, table + lo, k}, hi - lo, fit_all + lo, st, &timer, vary));
         if (world > 1) {
             const int rc = exchange(exchange_user, fit_all, s, block, st);
             if (rc != 0) return fail(GAPA_CUDA_E_CUDA, "run: exchange hook failed with status %d", rc);
@@ -241,8 +246,14 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
         if (!eda_gen)
             GAPA_TRY(launch_select(fit, s, minimize, p->seed, g, B.partner.as<int32_t>(), B.weights.as<double>(),
                                    B.cumulative.as<double>(), status, st));
-        GAPA_TRY(launch_slots_variation(pool_rows, parent, child, partner, s, k, lo, hi - lo, p->pc, p->pm, pool, p->seed, g, st));
-        GAPA_TRY(evaluate(child, fit_m));
+        VariationSpec vary;  // the evaluation builds the children of rows [lo, hi) into their slots first
+        vary.P = make_variation_params(p->pc, p->pm, pool, s, p->seed, g);
+        vary.pool = pool_rows;
+        vary.parent = parent;
+        vary.child = child;
+        vary.partner = partner;
+        vary.row_first = lo;
+        GAPA_TRY(evaluate(child, fit_m, &vary));
         // elitism permutes the slot tables; survivors built by other ranks are rebuilt in place
         GAPA_TRY(launch_slots_elitism(pool_rows, parent, child, partner, s, k, lo, hi, fit, fit_m, minimize, p->pc, p->pm, pool,
                                       p->seed, g, next_parent, next_child, fit_next, B.src_of_rank.as<int32_t>(), status, st));

@@ -13,44 +13,11 @@
 #include <algorithm>
 
 #include "internal.cuh"
+#include "variation.cuh"
 
 namespace gapa_b200 {
 
 static constexpr int kSlotThreads = 256;
-static constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
-static constexpr uint64_t kCounterStep = 0x632BE59BD9B4E019ull;  // rng.hpp:21
-
-__device__ __forceinline__ uint64_t hash_tail(uint64_t y) {  // mix64(x) with y = x + kGolden (rng.hpp:8-13)
-    y = (y ^ (y >> 30)) * 0xBF58476D1CE4E5B9ull;
-    y = (y ^ (y >> 27)) * 0x94D049BB133111EBull;
-    return y ^ (y >> 31);
-}
-
-struct VariationParams {
-    uint64_t pc_limit, pm_limit;  // next_bernoulli(p) == always || u < limit  (u >> 11 < ceil(p 2^53))
-    bool pc_always, pm_always;
-    uint32_t pool_size;  // gene pool
-    uint32_t s;          // population size (elite count of eda_sample, modes.cpp:168)
-    uint64_t seed, generation;
-};
-
-// One child gene.  partner_row < 0 selects the EDA form: eda_sample over the whole parent
-// population with add-one smoothing (ga_ops.cpp:214-238), then mutate; otherwise crossover
-// (ga_ops.cpp:130-144) then mutate (:164-178).  `prod` = kCounterStep * (column + 1); the keys
-// already include kGolden.
-__device__ __forceinline__ int32_t child_gene(const VariationParams& P, const int32_t* __restrict__ pool,
-                                              const int32_t* __restrict__ parent, int k, int col, int mine, int theirs,
-                                              bool eda, uint64_t ks, uint64_t kc, uint64_t km, uint64_t ki, uint64_t prod) {
-    const uint64_t um = hash_tail(km + prod);
-    if (P.pm_always || um < P.pm_limit) return static_cast<int32_t>(__umul64hi(hash_tail(ki + prod), static_cast<uint64_t>(P.pool_size)));
-    if (eda) {
-        const uint32_t v = static_cast<uint32_t>(__umul64hi(hash_tail(ks + prod), static_cast<uint64_t>(P.s + P.pool_size)));
-        return v < P.s ? pool[static_cast<size_t>(parent[v]) * k + col] : static_cast<int32_t>(v - P.s);
-    }
-    const uint64_t ux = hash_tail(kc + prod);
-    return (P.pc_always || ux < P.pc_limit) ? theirs : mine;
-}
-
 // Builds child row `row` into its slot.  Shared by the variation kernel (own rows) and the rebuild
 // kernel (foreign survivors).
 __device__ __forceinline__ void build_child_row(const VariationParams& P, int32_t* __restrict__ pool,
@@ -171,20 +138,6 @@ static dim3 slot_grid(int cols, int rows) {
     return dim3(std::max(1, std::min((cols + per_block - 1) / per_block, 65535)), rows);
 }
 
-static VariationParams make_params(double pc, double pm, uint32_t pool_size, int s, uint64_t seed, uint64_t generation) {
-    const uint64_t tc = bernoulli_threshold(pc), tm = bernoulli_threshold(pm);
-    VariationParams P;
-    P.pc_always = tc >= (1ull << 53);
-    P.pm_always = tm >= (1ull << 53);
-    P.pc_limit = P.pc_always ? ~0ull : tc << 11;
-    P.pm_limit = P.pm_always ? ~0ull : tm << 11;
-    P.pool_size = pool_size;
-    P.s = static_cast<uint32_t>(s);
-    P.seed = seed;
-    P.generation = generation;
-    return P;
-}
-
 // ---- launchers shared with run.cu (no synchronisation) ---------------------------------------------------
 int launch_slots_identity(int s, int32_t* parent, int32_t* child, cudaStream_t st) {
     GAPA_LAUNCH(k_ga_slots_identity, (s + kSlotThreads - 1) / kSlotThreads, kSlotThreads, 0, st, s, parent, child);
@@ -195,7 +148,13 @@ int launch_slots_variation(int32_t* pool, const int32_t* parent, const int32_t* 
                            uint64_t generation, cudaStream_t st) {
     if (row_count == 0 || k == 0) return GAPA_CUDA_OK;
     GAPA_LAUNCH(k_ga_slots_variation, slot_grid((k & 3) ? k : k / 4, row_count), kSlotThreads, 0, st,
-                make_params(pc, pm, pool_size, s, seed, generation), pool, parent, child, partner, k, row_first);
+                make_variation_params(pc, pm, pool_size, s, seed, generation), pool, parent, child, partner, k, row_first);
+    return GAPA_CUDA_OK;
+}
+int launch_variation_spec(const VariationSpec& spec, int k, int rows, cudaStream_t st) {
+    if (rows == 0 || k == 0) return GAPA_CUDA_OK;
+    GAPA_LAUNCH(k_ga_slots_variation, slot_grid((k & 3) ? k : k / 4, rows), kSlotThreads, 0, st, spec.P, spec.pool, spec.parent,
+                spec.child, spec.partner, k, spec.row_first);
     return GAPA_CUDA_OK;
 }
 int launch_slots_elitism(int32_t* pool, const int32_t* parent, const int32_t* child, const int32_t* partner, int s, int k,
@@ -206,7 +165,7 @@ int launch_slots_elitism(int32_t* pool, const int32_t* parent, const int32_t* ch
     GAPA_LAUNCH(k_ga_slots_rank, (2 * s + per_block - 1) / per_block, kSlotThreads, 0, st, fit, fit_m, s, minimize, order, status);
     if ((block_lo > 0 || block_hi < s) && k > 0)
         GAPA_LAUNCH(k_ga_slots_rebuild, slot_grid((k & 3) ? k : k / 4, s), kSlotThreads, 0, st,
-                    make_params(pc, pm, pool_size, s, seed, generation), pool, parent, child, partner, k, s, order, block_lo, block_hi);
+                    make_variation_params(pc, pm, pool_size, s, seed, generation), pool, parent, child, partner, k, s, order, block_lo, block_hi);
     GAPA_LAUNCH(k_ga_slots_commit, (s + kSlotThreads - 1) / kSlotThreads, kSlotThreads, 0, st, parent, child, fit, fit_m, s, order,
                 next_parent, next_child, next_fit);
     return GAPA_CUDA_OK;

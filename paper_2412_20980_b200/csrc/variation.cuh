@@ -1,0 +1,71 @@
+// Child-gene arithmetic shared by the slot-pool variation kernels (slot_kernels.cu) and the fused
+// variation + mask-build kernel of the PC fitness (pc_kernels.cu).  Bit-exact twins of
+// ga_ops.cpp:130-178 and :214-238 on the keyed streams of rng.hpp.
+#pragma once
+
+#include "internal.cuh"
+
+namespace gapa_b200 {
+
+static constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
+static constexpr uint64_t kCounterStep = 0x632BE59BD9B4E019ull;  // rng.hpp:21
+
+__device__ __forceinline__ uint64_t hash_tail(uint64_t y) {  // mix64(x) with y = x + kGolden (rng.hpp:8-13)
+    y = (y ^ (y >> 30)) * 0xBF58476D1CE4E5B9ull;
+    y = (y ^ (y >> 27)) * 0x94D049BB133111EBull;
+    return y ^ (y >> 31);
+}
+
+struct VariationParams {
+    uint64_t pc_limit, pm_limit;  // next_bernoulli(p) == always || u < limit  (u >> 11 < ceil(p 2^53))
+    bool pc_always, pm_always;
+    uint32_t pool_size;  // gene pool
+    uint32_t s;          // population size (elite count of eda_sample, modes.cpp:168)
+    uint64_t seed, generation;
+};
+
+// One child gene.  partner_row < 0 selects the EDA form: eda_sample over the whole parent
+// population with add-one smoothing (ga_ops.cpp:214-238), then mutate; otherwise crossover
+// (ga_ops.cpp:130-144) then mutate (:164-178).  `prod` = kCounterStep * (column + 1); the keys
+// already include kGolden.
+__device__ __forceinline__ int32_t child_gene(const VariationParams& P, const int32_t* __restrict__ pool,
+                                              const int32_t* __restrict__ parent, int k, int col, int mine, int theirs,
+                                              bool eda, uint64_t ks, uint64_t kc, uint64_t km, uint64_t ki, uint64_t prod) {
+    const uint64_t um = hash_tail(km + prod);
+    if (P.pm_always || um < P.pm_limit) return static_cast<int32_t>(__umul64hi(hash_tail(ki + prod), static_cast<uint64_t>(P.pool_size)));
+    if (eda) {
+        const uint32_t v = static_cast<uint32_t>(__umul64hi(hash_tail(ks + prod), static_cast<uint64_t>(P.s + P.pool_size)));
+        return v < P.s ? pool[static_cast<size_t>(parent[v]) * k + col] : static_cast<int32_t>(v - P.s);
+    }
+    const uint64_t ux = hash_tail(kc + prod);
+    return (P.pc_always || ux < P.pc_limit) ? theirs : mine;
+}
+
+
+inline VariationParams make_variation_params(double pc, double pm, uint32_t pool_size, int s, uint64_t seed, uint64_t generation) {
+    const uint64_t tc = bernoulli_threshold(pc), tm = bernoulli_threshold(pm);
+    VariationParams P;
+    P.pc_always = tc >= (1ull << 53);
+    P.pm_always = tm >= (1ull << 53);
+    P.pc_limit = P.pc_always ? ~0ull : tc << 11;
+    P.pm_limit = P.pm_always ? ~0ull : tm << 11;
+    P.pool_size = pool_size;
+    P.s = static_cast<uint32_t>(s);
+    P.seed = seed;
+    P.generation = generation;
+    return P;
+}
+
+// What the evaluators need to BUILD the children they evaluate (row r of the batch = child of
+// global row row_first + r): the fused PC path writes each child gene to its slot and into the
+// shared-memory bitmap in the same pass.
+struct VariationSpec {
+    VariationParams P;
+    int32_t* pool;           // 2s x k row slots
+    const int32_t* parent;   // slot tables
+    const int32_t* child;
+    const int32_t* partner;  // nullptr = EDA generation
+    int row_first;
+};
+
+}  // namespace gapa_b200

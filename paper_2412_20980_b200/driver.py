@@ -94,6 +94,15 @@ class CudaOps:
             pool.data_ptr(), parent.data_ptr(), child.data_ptr(), partner.data_ptr() if partner is not None else None, s,
             pool.shape[1], lo, hi - lo, pc, pm, self.pool_size, seed, generation, self._stream()))
 
+    def variation_eval(self, pool, parent, child, partner, s, pc, pm, seed, generation, lo, hi, fit_out):
+        """children of rows [lo, hi) built into their slots AND evaluated into fit_out[lo:hi] in one call"""
+        if hi <= lo:
+            return
+        check(self.lib.gapa_cuda_ga_slots_variation_eval_device(
+            self.fitness.dgraph.handle, self.fitness.task, pool.data_ptr(), parent.data_ptr(), child.data_ptr(),
+            partner.data_ptr() if partner is not None else None, s, pool.shape[1], lo, hi - lo, pc, pm, seed, generation,
+            fit_out.data_ptr() + 8 * lo, self._stream()))
+
     def eval_rows(self, pool, table, lo, hi, fit_out):
         """fitness of the rows table[lo:hi] names into fit_out[lo:hi]"""
         if hi <= lo:
@@ -183,8 +192,9 @@ class ShardedGa:
         partner = None if eda_gen else self.partner
         if not eda_gen:
             ops.select(self.fit, s, self.minimize, p.seed, gen, self.partner)
-        ops.variation(self.pool, self.parent, self.child, partner, s, p.pc, p.pm, p.seed, gen, lo, hi)
-        self._evaluate(self.child, self.fit_m)
+        self.fitness_batch_calls += 1
+        ops.variation_eval(self.pool, self.parent, self.child, partner, s, p.pc, p.pm, p.seed, gen, lo, hi, self.fit_m)
+        self.gather(self.fit_m, self.shard)
         ops.elitism(self.pool, self.parent, self.child, partner, s, lo, hi, self.fit, self.fit_m, self.minimize, p.pc, p.pm,
                     p.seed, gen, self.next_parent, self.next_child, self.fit_next)
         self.parent, self.next_parent = self.next_parent, self.parent

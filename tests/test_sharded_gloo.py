@@ -43,6 +43,9 @@ class OracleOps:
     def variation(self, pool, parent, child, partner, s, pc, pm, seed, gen, lo, hi):
         rows = self._children(pool, parent, partner, pc, pm, seed, gen)
         pool[child[lo:hi].long()] = torch.from_numpy(rows[lo:hi])  # only this rank's block is built
+    def variation_eval(self, pool, parent, child, partner, s, pc, pm, seed, gen, lo, hi, fit_out):
+        self.variation(pool, parent, child, partner, s, pc, pm, seed, gen, lo, hi)
+        self.eval_rows(pool, child, lo, hi, fit_out)
     def eval_rows(self, pool, table, lo, hi, fit_out):
         if hi > lo: fit_out[lo:hi] = torch.from_numpy(self.o.eval_batch(self.ctx, self.task, pool[table[lo:hi].long()].numpy()))
     def elitism(self, pool, parent, child, partner, s, lo, hi, fit, fit_m, minimize, pc, pm, seed, gen, next_parent, next_child, next_fit):
