@@ -22,6 +22,7 @@ REF_SO = os.path.join(HERE, "_ref", "libgapa_ref.so")
 REFERENCE_SRC = "/root/reference/proj"
 
 TASK_PC, TASK_MCN, TASK_CDA, TASK_LPA = 0, 1, 2, 3
+TASK_SIXDST, TASK_CDA_ADD = 4, 5  # sixdst_fitness(SixDegrees); cda_fitness over the EdgeAddition pool
 ROLE_INIT, ROLE_SELECT, ROLE_CROSSOVER_MASK, ROLE_MUTATION_MASK, ROLE_MUTATION_INDEX = 1, 2, 3, 4, 5
 MODE_SERIAL, MODE_S, MODE_SM, MODE_M, MODE_MNM = 0, 1, 2, 3, 4
 
@@ -57,7 +58,8 @@ class OrcGraphStruct(C.Structure):
     _fields_ = [("n", C.c_int32), ("m", C.c_int64), ("edge_uv", C.POINTER(C.c_int32)),
                 ("row_ptr", C.POINTER(C.c_int32)), ("col_idx", C.POINTER(C.c_int32)),
                 ("edge_id", C.POINTER(C.c_int32)), ("pool_u", C.POINTER(C.c_int32)),
-                ("pool_v", C.POINTER(C.c_int32))]
+                ("pool_v", C.POINTER(C.c_int32)), ("add_size", C.c_int64), ("add_u", C.POINTER(C.c_int32)),
+                ("add_v", C.POINTER(C.c_int32))]
 
 
 class OrcSplitStruct(C.Structure):
@@ -130,6 +132,8 @@ class Oracle:
         lib.orc_graph_sbm.restype = G
         lib.orc_graph_sbm.argtypes = [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64]
         lib.orc_graph_free.argtypes = [G]
+        lib.orc_graph_build_addition_pool.restype = C.c_int64
+        lib.orc_graph_build_addition_pool.argtypes = [G]
         lib.orc_budget.restype = C.c_int32
         lib.orc_budget.argtypes = [C.c_int64, C.c_double]
         lib.orc_split_build.restype = S
@@ -187,6 +191,16 @@ class Oracle:
 
     def budget(self, basis, rate):
         return int(self.lib.orc_budget(basis, rate))
+
+    def addition_pool(self, g: OracleGraph):
+        """EdgeAddition pool (gene_pool.cpp:81-87) of g as (u[], v[]); cached on the graph,
+        and what TASK_CDA_ADD evaluates against."""
+        size = int(self.lib.orc_graph_build_addition_pool(g._ptr))
+        if size < 0:
+            raise ValueError("gene pool: graph is complete, no edges can be added")
+        s = g._ptr.contents
+        return (np.ctypeslib.as_array(s.add_u, shape=(size,)).copy(),
+                np.ctypeslib.as_array(s.add_v, shape=(size,)).copy())
 
     def split_build(self, g: OracleGraph, fraction, seed):
         return OracleSplit(self.lib, self.lib.orc_split_build(g._ptr, fraction, seed))

@@ -63,7 +63,7 @@ static void ivec_push(ivec* a, int32_t x) {
 void orc_graph_free(orc_graph* g) {
     if (!g) return;
     free(g->edge_uv); free(g->row_ptr); free(g->col_idx); free(g->edge_id);
-    free(g->pool_u); free(g->pool_v); free(g);
+    free(g->pool_u); free(g->pool_v); free(g->add_u); free(g->add_v); free(g);
 }
 
 static int cmp_i32(const void* a, const void* b) {
@@ -310,6 +310,52 @@ int orc_pc_batch(const orc_graph* g, int task, const int32_t* genes, int rows, i
     return rc;
 }
 
+/* fitness.cpp:18-26 with ClosurePolicy::SixDegrees.  accessibility.cpp:20-37
+ * squares A + I at most three times: after j squarings entry (u, v) is set iff
+ * dist(u, v) <= 2^j, so the closure row of u is the ball of radius 8 around u
+ * (u itself included through the diagonal; a removed node keeps only its
+ * diagonal bit).  Restated as one depth-limited BFS per source on the CSR. */
+int orc_sixdst_batch(const orc_graph* g, const int32_t* genes, int rows, int cols, double* out) {
+    const int32_t n = g->n;
+    uint8_t* removed = (uint8_t*)malloc((size_t)n + 1);
+    int32_t* mark = (int32_t*)malloc(sizeof(int32_t) * ((size_t)n + 1));
+    int32_t* queue = (int32_t*)malloc(sizeof(int32_t) * ((size_t)n + 1));
+    int rc = 0;
+    for (int r = 0; r < rows && !rc; ++r) {
+        memset(removed, 0, (size_t)n + 1);
+        for (int j = 0; j < cols; ++j) {
+            const int32_t x = genes[(size_t)r * cols + j];
+            if (x < 0 || x >= n) { rc = 1; break; }
+            removed[x] = 1;
+        }
+        if (rc) break;
+        for (int32_t u = 0; u < n; ++u) mark[u] = -1;
+        int32_t best = 0;
+        for (int32_t src = 0; src < n; ++src) {
+            int32_t size = 1;
+            if (!removed[src]) {
+                int32_t head = 0, tail = 0;
+                queue[tail++] = src; mark[src] = src;
+                for (int depth = 0; depth < 8 && head < tail; ++depth) {
+                    const int32_t level_end = tail;
+                    for (; head < level_end; ++head) {
+                        const int32_t u = queue[head];
+                        for (int32_t i = g->row_ptr[u]; i < g->row_ptr[u + 1]; ++i) {
+                            const int32_t v = g->col_idx[i];
+                            if (mark[v] != src && !removed[v]) { mark[v] = src; queue[tail++] = v; }
+                        }
+                    }
+                }
+                size = tail;
+            }
+            if (size > best) best = size;
+        }
+        out[r] = (double)best;
+    }
+    free(removed); free(mark); free(queue);
+    return rc;
+}
+
 /* ===================================================================== CDA */
 
 typedef struct { int32_t id; int64_t cnt; } nb_t;
@@ -460,6 +506,62 @@ int orc_cda_batch(const orc_graph* g, const int32_t* genes, int rows, int cols, 
     return rc;
 }
 
+/* gene_pool.cpp:81-87: every pair u < v that is not an edge, lexicographic. */
+int64_t orc_graph_build_addition_pool(orc_graph* g) {
+    if (g->add_u) return g->add_size;
+    const int64_t n = g->n, size = n * (n - 1) / 2 - g->m;
+    if (size <= 0 || size > 0x7fffffffll) return -1;
+    g->add_u = (int32_t*)malloc(sizeof(int32_t) * (size_t)size);
+    g->add_v = (int32_t*)malloc(sizeof(int32_t) * (size_t)size);
+    int64_t next = 0;
+    for (int32_t u = 0; u < g->n; ++u) {
+        int32_t i = g->row_ptr[u];
+        const int32_t ie = g->row_ptr[u + 1];
+        while (i < ie && g->col_idx[i] <= u) ++i;
+        for (int32_t v = u + 1; v < g->n; ++v) {
+            if (i < ie && g->col_idx[i] == v) { ++i; continue; }
+            g->add_u[next] = u; g->add_v[next] = v; ++next;
+        }
+    }
+    g->add_size = next;
+    return next;
+}
+
+/* fitness.cpp:35-41 with an EdgeAddition pool: apply_in_place sets both bits of
+ * every gene's pair (gene_pool.cpp:57-60; duplicates idempotent), then the same
+ * detector and modularity run on the enlarged graph. */
+int orc_cda_add_batch(const orc_graph* g, const int32_t* genes, int rows, int cols, double* out) {
+    if (!g->add_u) return 2;
+    int32_t* uv = (int32_t*)malloc(sizeof(int32_t) * 2 * (size_t)(g->m + cols + 1));
+    uint8_t* seen = (uint8_t*)calloc((size_t)g->add_size + 1, 1);
+    int32_t* owner = (int32_t*)malloc(sizeof(int32_t) * ((size_t)g->n + 1));
+    int rc = 0;
+    for (int r = 0; r < rows && !rc; ++r) {
+        memcpy(uv, g->edge_uv, sizeof(int32_t) * 2 * (size_t)g->m);
+        int64_t m2 = g->m;
+        for (int j = 0; j < cols; ++j) {
+            const int32_t e = genes[(size_t)r * cols + j];
+            if (e < 0 || e >= g->add_size) { rc = 1; break; }
+            if (seen[e]) continue;
+            seen[e] = 1;
+            uv[2 * m2] = g->add_u[e]; uv[2 * m2 + 1] = g->add_v[e]; ++m2;
+        }
+        for (int j = 0; j < cols; ++j) {
+            const int32_t e = genes[(size_t)r * cols + j];
+            if (e >= 0 && e < g->add_size) seen[e] = 0;
+        }
+        if (rc) break;
+        if (m2 == 0) { out[r] = -0.5; continue; }
+        orc_graph* p = orc_graph_create(g->n, m2, uv);
+        if (!p) { rc = 2; break; }
+        detect_on(p, NULL, owner);
+        out[r] = modularity_on(p, NULL, owner);
+        orc_graph_free(p);
+    }
+    free(uv); free(seen); free(owner);
+    return rc;
+}
+
 /* ===================================================================== LPA */
 
 /* link_prediction.cpp:55-69 on the CSR minus `gone` edges; deg[] are the
@@ -554,6 +656,8 @@ static int eval_block(const void* ctx, int task, const int32_t* genes, int rows,
         case ORC_TASK_MCN: return orc_pc_batch((const orc_graph*)ctx, task, genes, rows, cols, out);
         case ORC_TASK_CDA: return orc_cda_batch((const orc_graph*)ctx, genes, rows, cols, out);
         case ORC_TASK_LPA: return orc_lpa_batch((const orc_split*)ctx, genes, rows, cols, out);
+        case ORC_TASK_SIXDST: return orc_sixdst_batch((const orc_graph*)ctx, genes, rows, cols, out);
+        case ORC_TASK_CDA_ADD: return orc_cda_add_batch((const orc_graph*)ctx, genes, rows, cols, out);
     }
     return 2;
 }
@@ -718,8 +822,10 @@ int orc_eda_sample(const int32_t* elite, int s, int k, int elite_count, int pool
 static int pool_size_of(const void* ctx, int task) {
     switch (task) {
         case ORC_TASK_PC:
-        case ORC_TASK_MCN: return ((const orc_graph*)ctx)->n;
+        case ORC_TASK_MCN:
+        case ORC_TASK_SIXDST: return ((const orc_graph*)ctx)->n;
         case ORC_TASK_CDA: return (int)((const orc_graph*)ctx)->m;
+        case ORC_TASK_CDA_ADD: return (int)((const orc_graph*)ctx)->add_size;
         case ORC_TASK_LPA: return (int)((const orc_split*)ctx)->train->m;
     }
     return 0;

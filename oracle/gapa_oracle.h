@@ -33,7 +33,9 @@ uint32_t orc_draw_index(uint64_t key, uint64_t j, uint32_t bound);
 enum { ORC_ROLE_INIT = 1, ORC_ROLE_SELECT = 2, ORC_ROLE_CROSSOVER_MASK = 3,
        ORC_ROLE_MUTATION_MASK = 4, ORC_ROLE_MUTATION_INDEX = 5 };
 
-enum { ORC_TASK_PC = 0, ORC_TASK_MCN = 1, ORC_TASK_CDA = 2, ORC_TASK_LPA = 3 };
+enum { ORC_TASK_PC = 0, ORC_TASK_MCN = 1, ORC_TASK_CDA = 2, ORC_TASK_LPA = 3,
+       ORC_TASK_SIXDST = 4,   /* sixdst_fitness(ClosurePolicy::SixDegrees), fitness.cpp:18-26      */
+       ORC_TASK_CDA_ADD = 5   /* cda_fitness over the EdgeAddition pool, gene_pool.cpp:57-60,81-87 */ };
 
 /* ---- graph: canonical edge list (insertion order) + sorted CSR ----------- */
 typedef struct orc_graph {
@@ -46,6 +48,11 @@ typedef struct orc_graph {
                           = EdgeRemoval gene id (gene_pool.cpp:73-79)          */
     int32_t* pool_u;   /* m, endpoints of gene id e                            */
     int32_t* pool_v;
+    /* EdgeAddition pool (gene_pool.cpp:81-87): every non-edge (u < v) in
+     * lexicographic order; built on demand by orc_graph_build_addition_pool */
+    int64_t add_size;
+    int32_t* add_u;
+    int32_t* add_v;
 } orc_graph;
 
 orc_graph* orc_graph_create(int32_t n, int64_t m, const int32_t* uv); /* NULL on bad input */
@@ -73,6 +80,14 @@ void orc_split_free(orc_split* s);
  * out-of-range gene. */
 int orc_pc_batch(const orc_graph* g, int task, const int32_t* genes, int rows, int cols, double* out);
 int orc_cda_batch(const orc_graph* g, const int32_t* genes, int rows, int cols, double* out);
+/* ClosurePolicy::SixDegrees (accessibility.cpp:20-37): (A+I) squared at most 3 times covers
+ * exactly the paths of length <= 8, so row u of the closure is the radius-8 ball of u in the
+ * perturbed graph; fitness = the largest ball (fitness.cpp:23-25). */
+int orc_sixdst_batch(const orc_graph* g, const int32_t* genes, int rows, int cols, double* out);
+/* EdgeAddition: returns the pool size, or -1 if the graph is complete / the pool
+ * does not fit int32 (gene_pool.cpp:81-87). */
+int64_t orc_graph_build_addition_pool(orc_graph* g);
+int orc_cda_add_batch(const orc_graph* g, const int32_t* genes, int rows, int cols, double* out);
 int orc_lpa_batch(const orc_split* s, const int32_t* genes, int rows, int cols, double* out);
 /* task dispatch + contiguous row blocks (modes.cpp:506-516) over pthreads */
 int orc_eval_batch(const void* g_or_split, int task, const int32_t* genes, int rows, int cols,

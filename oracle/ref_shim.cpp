@@ -66,7 +66,7 @@ int guarded(Fn&& fn) {
     }
 }
 
-enum Task { kTaskPc = 0, kTaskMcn = 1, kTaskCda = 2, kTaskLpa = 3 };
+enum Task { kTaskPc = 0, kTaskMcn = 1, kTaskCda = 2, kTaskLpa = 3, kTaskSixDegrees = 4, kTaskCdaAdd = 5 };
 
 }  // namespace
 
@@ -183,6 +183,33 @@ void ref_split_pairs(void* s, std::int32_t* test_uv, std::int32_t* probe_uv) {
 void* ref_split_train(void* s) { return new RefGraph{static_cast<RefSplit*>(s)->split.train}; }
 
 // ---- fitness.hpp ---------------------------------------------------------------
+// The reference's own pool builder + objective for a task code:
+// 0 pc_fitness, 1 sixdst_fitness(Exact), 2 cda_fitness over the EdgeRemoval pool,
+// 3 lpa_fitness (handle is a split; pool over split.train), 4 sixdst_fitness(SixDegrees),
+// 5 cda_fitness over the EdgeAddition pool.
+static void make_objective(void* g_or_split, int task, std::unique_ptr<GenePool>& pool,
+                           std::unique_ptr<FitnessFunction>& fn) {
+    if (task == kTaskLpa) {
+        auto* s = static_cast<RefSplit*>(g_or_split);
+        pool = std::make_unique<GenePool>(build_gene_pool(s->split.train, PoolKind::EdgeRemoval));
+        fn = std::make_unique<LinkPredictionAttackObjective>(s->split, *pool);
+        return;
+    }
+    auto* g = static_cast<RefGraph*>(g_or_split);
+    if (task == kTaskCda || task == kTaskCdaAdd) {
+        pool = std::make_unique<GenePool>(
+            build_gene_pool(g->graph, task == kTaskCda ? PoolKind::EdgeRemoval : PoolKind::EdgeAddition));
+        fn = std::make_unique<ModularityAttackObjective>(g->graph.adjacency(), *pool);
+        return;
+    }
+    pool = std::make_unique<GenePool>(build_gene_pool(g->graph, PoolKind::NodeRemoval));
+    if (task == kTaskPc)
+        fn = std::make_unique<PairwiseConnectivityObjective>(g->graph.adjacency(), *pool);
+    else
+        fn = std::make_unique<SixDstObjective>(g->graph.adjacency(), *pool,
+                                               task == kTaskSixDegrees ? ClosurePolicy::SixDegrees : ClosurePolicy::Exact);
+}
+
 // task 0: pc_fitness, 1: sixdst_fitness(Exact), 2: cda_fitness (edge-removal
 // pool), 3: lpa_fitness (g_or_split is a split handle, pool over split.train).
 // `threads` > 1 splits the rows over std::threads the way
@@ -193,23 +220,7 @@ int ref_eval_batch(void* g_or_split, int task, const std::int32_t* genes, int ro
         const PopulationMatrix batch = to_matrix(genes, rows, cols);
         std::unique_ptr<GenePool> pool;
         std::unique_ptr<FitnessFunction> fn;
-        if (task == kTaskLpa) {
-            auto* s = static_cast<RefSplit*>(g_or_split);
-            pool = std::make_unique<GenePool>(build_gene_pool(s->split.train, PoolKind::EdgeRemoval));
-            fn = std::make_unique<LinkPredictionAttackObjective>(s->split, *pool);
-        } else {
-            auto* g = static_cast<RefGraph*>(g_or_split);
-            if (task == kTaskCda) {
-                pool = std::make_unique<GenePool>(build_gene_pool(g->graph, PoolKind::EdgeRemoval));
-                fn = std::make_unique<ModularityAttackObjective>(g->graph.adjacency(), *pool);
-            } else {
-                pool = std::make_unique<GenePool>(build_gene_pool(g->graph, PoolKind::NodeRemoval));
-                if (task == kTaskPc)
-                    fn = std::make_unique<PairwiseConnectivityObjective>(g->graph.adjacency(), *pool);
-                else
-                    fn = std::make_unique<SixDstObjective>(g->graph.adjacency(), *pool);
-            }
-        }
+        make_objective(g_or_split, task, pool, fn);
         if (threads <= 1) {
             const FitnessVector fv = fn->evaluate_batch(batch);
             std::copy(fv.begin(), fv.end(), out);
@@ -359,23 +370,7 @@ int ref_run_ga(void* g_or_split, int task, double pc, double pm, int pop_size, i
     return guarded([&] {
         std::unique_ptr<GenePool> pool;
         std::unique_ptr<FitnessFunction> fn;
-        if (task == kTaskLpa) {
-            auto* s = static_cast<RefSplit*>(g_or_split);
-            pool = std::make_unique<GenePool>(build_gene_pool(s->split.train, PoolKind::EdgeRemoval));
-            fn = std::make_unique<LinkPredictionAttackObjective>(s->split, *pool);
-        } else {
-            auto* g = static_cast<RefGraph*>(g_or_split);
-            if (task == kTaskCda) {
-                pool = std::make_unique<GenePool>(build_gene_pool(g->graph, PoolKind::EdgeRemoval));
-                fn = std::make_unique<ModularityAttackObjective>(g->graph.adjacency(), *pool);
-            } else {
-                pool = std::make_unique<GenePool>(build_gene_pool(g->graph, PoolKind::NodeRemoval));
-                if (task == kTaskPc)
-                    fn = std::make_unique<PairwiseConnectivityObjective>(g->graph.adjacency(), *pool);
-                else
-                    fn = std::make_unique<SixDstObjective>(g->graph.adjacency(), *pool);
-            }
-        }
+        make_objective(g_or_split, task, pool, fn);
         GAParams params;
         params.pc = pc;
         params.pm = pm;

@@ -3,7 +3,7 @@ sweeps than the golden files hold.  Skipped where the reference binary is not av
 import numpy as np
 import pytest
 
-from oracle.bindings import MODE_M, MODE_S, TASK_CDA, TASK_LPA, TASK_MCN, TASK_PC
+from oracle.bindings import MODE_M, MODE_S, TASK_CDA, TASK_CDA_ADD, TASK_LPA, TASK_MCN, TASK_PC, TASK_SIXDST
 
 
 def _rand_edges(rng, n, dens):
@@ -120,3 +120,49 @@ def test_trajectories_all_modes(oracle, ref):
         got = ref.run_ga(rg, TASK_PC, 0.6, 0.2, 24, 15, 20, 77, eda_interval=4, mode=mode, pn=pn)
         for key in ("best", "mean", "population", "fitness"):
             assert np.array_equal(want[key], got[key]), (mode, key)
+
+
+def test_sixdegrees_closure(oracle, ref):
+    """sixdst_fitness(SixDegrees) (fitness.cpp:18-26, accessibility.cpp:20-37): radius-8 balls.
+    Sparse graphs and paths so that the diameter exceeds 8 and the truncation matters
+    (test_fitness.cpp:94-103 uses a 12-node path)."""
+    rng = np.random.default_rng(11)
+    truncated = 0
+    for trial in range(60):
+        n = int(rng.integers(4, 120))
+        if trial % 3 == 0:  # a path plus a few chords
+            e = np.stack([np.arange(n - 1), np.arange(1, n)], 1).astype(np.int32)
+        else:
+            e = _rand_edges(rng, n, float(rng.uniform(0.5, 2.5)) / n)
+        og, rg = oracle.graph_from_edges(n, e), ref.graph_from_edges(n, e)
+        batch = rng.integers(0, n, (4, int(rng.integers(0, max(1, n // 6) + 1)))).astype(np.int32)
+        six = oracle.eval_batch(og, TASK_SIXDST, batch)
+        assert np.array_equal(six, ref.eval_batch(rg, TASK_SIXDST, batch))
+        exact = oracle.eval_batch(og, TASK_MCN, batch)
+        assert np.all(six <= exact)
+        truncated += int(np.any(six < exact))
+    assert truncated > 10  # the sweep really exercises the radius-8 cut
+
+
+def test_edge_addition_pool_and_cda(oracle, ref):
+    """EdgeAddition pools (gene_pool.cpp:57-60, :81-87) under cda_fitness."""
+    rng = np.random.default_rng(12)
+    for trial in range(25):
+        n = int(rng.integers(5, 70))
+        e = _rand_edges(rng, n, float(rng.uniform(0.0, 0.3)) if trial else 0.0)  # trial 0: edgeless graph
+        og, rg = oracle.graph_from_edges(n, e), ref.graph_from_edges(n, e)
+        u, v = oracle.addition_pool(og)
+        ru, rv = ref.pool_genes(rg, 1)
+        assert np.array_equal(u, ru) and np.array_equal(v, rv)
+        assert len(u) == n * (n - 1) // 2 - len(e)
+        cols = int(rng.integers(0, 40))
+        batch = rng.integers(0, len(u), (3, cols)).astype(np.int32)
+        if cols > 2:
+            batch[0, 1] = batch[0, 0]  # duplicate gene: idempotent
+        assert np.array_equal(oracle.eval_batch(og, TASK_CDA_ADD, batch), ref.eval_batch(rg, TASK_CDA_ADD, batch))
+    og, rg = oracle.graph_sbm(4, 30, 0.3, 0.02, 2), ref.graph_sbm(4, 30, 0.3, 0.02, 2)
+    oracle.addition_pool(og)
+    a = oracle.run_ga(og, TASK_CDA_ADD, 0.8, 0.1, 8, 12, 4, 3)
+    b = ref.run_ga(rg, TASK_CDA_ADD, 0.8, 0.1, 8, 12, 4, 3)
+    assert np.array_equal(a["best"], b["best"]) and np.array_equal(a["mean"], b["mean"])
+    assert np.array_equal(a["population"], b["population"])
