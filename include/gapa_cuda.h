@@ -47,7 +47,9 @@ enum {
     GAPA_TASK_PC = 0,  /* pairwise connectivity, pc_fitness        (fitness.cpp:28-33)  */
     GAPA_TASK_MCN = 1, /* largest component, sixdst_fitness(Exact) (fitness.cpp:18-26)  */
     GAPA_TASK_CDA = 2, /* modularity of the greedy detector        (fitness.cpp:35-41)  */
-    GAPA_TASK_LPA = 3  /* AUC of the RA predictor                  (fitness.cpp:43-48)  */
+    GAPA_TASK_LPA = 3, /* AUC of the RA predictor                  (fitness.cpp:43-48)  */
+    GAPA_TASK_SIXDST = 4 /* sixdst_fitness(ClosurePolicy::SixDegrees): largest radius-8 ball
+                            (fitness.cpp:18-26 over accessibility.cpp:20-37, <= 3 squarings)   */
 };
 
 /* PoolKind, gene_pool.hpp:14 (same order) */
@@ -80,7 +82,11 @@ int gapa_cuda_graph_info(const gapa_cuda_ctx* ctx, int32_t* n, int64_t* m, int* 
  * (u == NULL means the identity pool of build_gene_pool, gene_pool.cpp:89-92),
  * v ignored.  kind EDGE_REMOVAL: (u[i], v[i]) must be edges of the graph
  * (u == NULL means build_gene_pool's (u,v)-sorted order, gene_pool.cpp:73-79).
- * EDGE_ADDITION is not on this path yet and returns GAPA_CUDA_E_INVALID. */
+ * kind EDGE_ADDITION (cda task only, fitness.cpp:54-57): (u[i], v[i]) is the pair gene i
+ * adds (gene_pool.cpp:57-60); u == NULL means every non-edge a < b in lexicographic
+ * order (gene_pool.cpp:81-87; fails on a complete graph like :86).  A pair that is
+ * already an edge is accepted and is a no-op, as in the reference.  Repeated elements
+ * are rejected for every kind (gene_pool.cpp:36-41). */
 int gapa_cuda_pool_set(gapa_cuda_ctx* ctx, int kind, int32_t n_genes, const int32_t* u, const int32_t* v);
 int gapa_cuda_pool_info(const gapa_cuda_ctx* ctx, int* kind, int32_t* n_genes);
 
@@ -252,6 +258,9 @@ int gapa_host_planted_partition(int32_t blocks, int32_t block_size, double p_in,
 /* train_uv[(m-T) x 2], test_uv[T x 2], probe_uv[T x 2]; null outputs = query T */
 int gapa_host_lp_split(int32_t n, int64_t m, const int32_t* edges, double fraction, uint64_t seed,
                        int32_t* train_uv, int32_t* test_uv, int32_t* probe_uv, int32_t* test_count);
+/* EdgeAddition pool of build_gene_pool (gene_pool.cpp:81-87): every non-edge a < b in
+ * lexicographic order; uv == NULL queries *count.  Fails on a complete graph (:86). */
+int gapa_host_nonedges(int32_t n, int64_t m, const int32_t* edges, int32_t* uv, int64_t capacity, int64_t* count);
 /* perturbation_budget (gene_pool.cpp:98-102): k = max(1, ceil(rate * basis)) */
 int gapa_host_budget(int64_t basis, double rate, int32_t* k);
 

@@ -92,6 +92,26 @@ int main() {
             compare_modes("CDA sbm80 + EDA", p, pool, cpu, gpu);
             expect(same_outputs(run_mode_s(p, pool, cpu), gapa_b200::run_ga_cuda(p, gpu)), "CDA run_ga_cuda with EDA");
         }
+        {  // truncated closure (ClosurePolicy::SixDegrees) on a tree, where radius 8 matters
+            const Graph g = barabasi_albert(300, 1, 668);
+            const GenePool pool = build_gene_pool(g, PoolKind::NodeRemoval);
+            GAParams p;
+            p.pc = 0.5; p.pm = 0.3; p.pop_size = 24; p.iterations = 20; p.seed = 670;
+            p.budget = perturbation_budget(g, PoolKind::NodeRemoval, 0.1);
+            const SixDstObjective cpu(g.adjacency(), pool, ClosurePolicy::SixDegrees);
+            const gapa_b200::CudaSixDstObjective gpu(g, pool, ClosurePolicy::SixDegrees);
+            compare_modes("SixDST SixDegrees ba300", p, pool, cpu, gpu);
+        }
+        {  // acceptance criterion 8 instance (acceptance.cpp:207-246), EdgeAddition pool, shortened
+            const Graph g = planted_partition(4, 9, 0.5, 0.05, 3);
+            const GenePool pool = build_gene_pool(g, PoolKind::EdgeAddition);
+            GAParams p;
+            p.pc = 0.8; p.pm = 0.1; p.pop_size = 30; p.iterations = 20; p.seed = 667;
+            p.budget = perturbation_budget(g, PoolKind::EdgeAddition, 0.1);
+            const ModularityAttackObjective cpu(g.adjacency(), pool);
+            const gapa_b200::CudaModularityAttackObjective gpu(g, pool);
+            compare_modes("CDA EdgeAddition sbm36", p, pool, cpu, gpu);
+        }
         {  // operator free functions in the reference's shapes
             const RngPolicy rng(9);
             const PopulationMatrix pop = init_population(500, 40, 17, rng);

@@ -18,12 +18,17 @@ import numpy as np
 from . import capi
 from .capi import GapaCudaError, check
 
-TASK_PC, TASK_MCN, TASK_CDA, TASK_LPA = 0, 1, 2, 3
+TASK_PC, TASK_MCN, TASK_CDA, TASK_LPA, TASK_SIXDST = 0, 1, 2, 3, 4
 
 
 class Direction(enum.Enum):  # population.hpp:9
     Maximize = 0
     Minimize = 1
+
+
+class ClosurePolicy(enum.Enum):  # accessibility.hpp:14
+    Exact = 0
+    SixDegrees = 1
 
 
 class PoolKind(enum.IntEnum):  # gene_pool.hpp:14
@@ -107,11 +112,15 @@ def planted_partition(blocks: int, block_size: int, p_in: float, p_out: float, s
 class GenePool:
     """gene_pool.hpp:32-52.  `u`, `v` hold the element of every gene id (v = -1 for nodes)."""
 
-    def __init__(self, kind: PoolKind, u, v=None, graph: Graph | None = None):
+    def __init__(self, kind: PoolKind, u, v=None, graph: Graph | None = None, canonical: bool = False):
         self._kind = PoolKind(kind)
         self.u = _i32(u, 1)
         self.v = np.full_like(self.u, -1) if v is None else _i32(v, 1)
         self.graph = graph
+        self.canonical = canonical  # exactly build_gene_pool(graph, kind): the device side rebuilds it itself
+
+    def gene(self, gene_id: int) -> tuple[int, int]:
+        return int(self.u[gene_id]), int(self.v[gene_id])
 
     def kind(self) -> PoolKind:
         return self._kind
@@ -129,7 +138,13 @@ def build_gene_pool(g: Graph, kind: PoolKind) -> GenePool:  # gene_pool.cpp:69-9
     if kind == PoolKind.EdgeRemoval:
         e = g.sorted_edges()
         return GenePool(kind, e[:, 0], e[:, 1], graph=g)
-    raise GapaCudaError(capi.E_INVALID, "edge-addition pools are not on the CUDA path yet")
+    e = np.ascontiguousarray(g.edges())
+    count = C.c_int64(0)
+    lib = capi.load()
+    check(lib.gapa_host_nonedges(g.n, len(e), _ptr(e) if len(e) else None, None, 0, C.byref(count)))
+    uv = np.zeros((count.value, 2), dtype=np.int32)
+    check(lib.gapa_host_nonedges(g.n, len(e), _ptr(e) if len(e) else None, _ptr(uv), count.value, C.byref(count)))
+    return GenePool(kind, uv[:, 0], uv[:, 1], graph=g, canonical=True)
 
 
 def perturbation_budget(g: Graph, kind: PoolKind, rate: float) -> int:  # gene_pool.cpp:98-102
@@ -175,7 +190,9 @@ class DeviceGraph:
         self.n, self.m = g.n, g.edge_count()
 
     def set_pool(self, pool: GenePool) -> None:
-        if pool.kind() == PoolKind.NodeRemoval:
+        if pool.canonical and pool.kind() == PoolKind.EdgeAddition:  # 12.5 M pairs at n = 5000: built on the C side
+            check(self.lib.gapa_cuda_pool_set(self.handle, int(pool.kind()), pool.size(), None, None))
+        elif pool.kind() == PoolKind.NodeRemoval:
             check(self.lib.gapa_cuda_pool_set(self.handle, int(pool.kind()), pool.size(), _ptr(pool.u), None))
         else:
             check(self.lib.gapa_cuda_pool_set(self.handle, int(pool.kind()), pool.size(), _ptr(pool.u), _ptr(pool.v)))
@@ -245,12 +262,16 @@ class PairwiseConnectivityObjective(FitnessFunction):  # fitness.hpp:68-77
         self.dgraph.set_pool(pool)
 
 
-class SixDstObjective(FitnessFunction):  # fitness.hpp:56-66, ClosurePolicy::Exact only
+class SixDstObjective(FitnessFunction):  # fitness.hpp:56-66
+    """Exact closure = largest component (the PC kernels); SixDegrees = largest radius-8 ball
+    (accessibility.hpp:12-14, the truncated multi-source BFS kernel)."""
     task = TASK_MCN
 
-    def __init__(self, graph: Graph, pool: GenePool, device: int = 0):
+    def __init__(self, graph: Graph, pool: GenePool, device: int = 0, policy: ClosurePolicy = ClosurePolicy.Exact):
         _require_kind(pool, PoolKind.NodeRemoval, "SixDstObjective")
         super().__init__(DeviceGraph(graph, device), pool)
+        self.policy = ClosurePolicy(policy)
+        self.task = TASK_MCN if self.policy == ClosurePolicy.Exact else TASK_SIXDST
         self.dgraph.set_pool(pool)
 
 
@@ -279,9 +300,10 @@ def pc_fitness(graph: Graph, batch, pool: GenePool, device: int = 0) -> np.ndarr
     return PairwiseConnectivityObjective(graph, pool, device).evaluate_batch(batch)
 
 
-def sixdst_fitness(graph: Graph, batch, pool: GenePool, device: int = 0) -> np.ndarray:  # fitness.hpp:33-34
+def sixdst_fitness(graph: Graph, batch, pool: GenePool, policy: ClosurePolicy = ClosurePolicy.Exact,
+                   device: int = 0) -> np.ndarray:  # fitness.hpp:33-36
     _require_kind(pool, PoolKind.NodeRemoval, "sixdst_fitness")
-    return SixDstObjective(graph, pool, device).evaluate_batch(batch)
+    return SixDstObjective(graph, pool, device, policy).evaluate_batch(batch)
 
 
 def cda_fitness(graph: Graph, batch, pool: GenePool, device: int = 0) -> np.ndarray:  # fitness.hpp:44-45

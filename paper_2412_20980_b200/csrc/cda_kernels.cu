@@ -10,7 +10,10 @@
 //
 // Here: one CTA per individual runs the identical merge sequence on CNM-style state:
 //   * per community an unsorted neighbour list (id, edge count, cached gain) in an
-//     L2-resident entry pool, seeded in place from the CSR rows minus removed edges;
+//     L2-resident entry pool, seeded in place from the CSR rows minus removed edges
+//     (EdgeRemoval pools), or from the CSR rows plus the distinct added pairs
+//     (EdgeAddition pools, gene_pool.cpp:57-60) — lists are unsorted, so an added edge
+//     is just one more entry at each end;
 //   * per community a cached best partner among ids greater than its own.  m is
 //     constant during a detection, so only pairs touching the merged community
 //     change gain; every other cached gain is bit-identical to a fresh evaluation;
@@ -45,6 +48,8 @@ struct CdaArgs {
     const int32_t* col_idx;
     const int32_t* edge_id;
     const int32_t* pool_map;
+    const int32_t* add_u;  // EdgeAddition pool: gene -> endpoints (-1 = pair already an edge); null for EdgeRemoval
+    const int32_t* add_v;
     int pool_size;
     int n;
     int mask_words;
@@ -127,8 +132,13 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
     int32_t* pos = pos_in_smem == 2 ? cda_smem + 6 * static_cast<size_t>(n) : (pos_in_smem ? cda_smem : A.pos_global + slot * n);
 
     for (int r = blockIdx.x; r < rows; r += gridDim.x) {
-        // ---- perturbation: edge-removed bitmask (gene_pool.cpp:53-56) -----------------
+        // ---- perturbation (gene_pool.cpp:53-60) ----------------------------------------
+        // EdgeRemoval: bit per edge rank.  EdgeAddition: bit per pool gene, so that a repeated gene
+        // adds its pair once; merged_into[] doubles as the per-vertex count of added edges.
+        const bool adding = A.add_u != nullptr;
         for (int w = tid; w < A.mask_words; w += kCdaThreads) gone[w] = 0u;
+        if (adding)
+            for (int u = tid; u < n; u += kCdaThreads) merged_into[u] = 0;
         if (tid == 0) { sh_total = 0; sh_abort = 0; }
         __syncthreads();
         const int cols = genes.cols;
@@ -136,28 +146,81 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         for (int j = tid; j < cols; j += kCdaThreads) {
             const int gene = g[j];
             if (gene < 0 || gene >= A.pool_size) { A.status[0] = GAPA_CUDA_E_RANGE; sh_abort = 1; continue; }
-            const int e = A.pool_map ? A.pool_map[gene] : gene;
-            atomicOr(&gone[e >> 5], 1u << (e & 31));
+            if (adding) {
+                const int a = A.add_u[gene];
+                if (a < 0) continue;
+                const unsigned bit = 1u << (gene & 31);
+                if (!(atomicOr(&gone[gene >> 5], bit) & bit)) {
+                    atomicAdd(&merged_into[a], 1);
+                    atomicAdd(&merged_into[A.add_v[gene]], 1);
+                }
+            } else {
+                const int e = A.pool_map ? A.pool_map[gene] : gene;
+                atomicOr(&gone[e >> 5], 1u << (e & 31));
+            }
         }
         __syncthreads();
         if (sh_abort) { if (tid == 0) out[r] = 0.0; __syncthreads(); continue; }
 
-        // ---- singleton communities: list(u) = surviving CSR row, in place --------------
+        // ---- singleton communities: list(u) = perturbed adjacency row ------------------
         long long my_deg = 0;
-        for (int u = tid; u < n; u += kCdaThreads) {
-            const int off = A.row_ptr[u], end = A.row_ptr[u + 1];
-            int cnt = 0;
-            for (int i = off; i < end; ++i) {
-                const int e = A.edge_id[i];
-                if (!((gone[e >> 5] >> (e & 31)) & 1u)) {
-                    e_id[off + cnt] = A.col_idx[i];
-                    e_cnt[off + cnt] = 1;
-                    ++cnt;
+        if (!adding) {  // surviving CSR row, in place
+            for (int u = tid; u < n; u += kCdaThreads) {
+                const int off = A.row_ptr[u], end = A.row_ptr[u + 1];
+                int cnt = 0;
+                for (int i = off; i < end; ++i) {
+                    const int e = A.edge_id[i];
+                    if (!((gone[e >> 5] >> (e & 31)) & 1u)) {
+                        e_id[off + cnt] = A.col_idx[i];
+                        e_cnt[off + cnt] = 1;
+                        ++cnt;
+                    }
+                }
+                head[u] = off; len[u] = cnt; cap[u] = end - off; cdeg[u] = cnt; merged_into[u] = -1;
+                pos[u] = -1;
+                my_deg += cnt;
+            }
+        } else {  // CSR row followed by room for the added pairs: heads by a block-wide prefix sum
+            const int per = (n + kCdaThreads - 1) / kCdaThreads;
+            const int u_lo = min(tid * per, n), u_hi = min(u_lo + per, n);
+            int want = 0;
+            for (int u = u_lo; u < u_hi; ++u) want += A.row_ptr[u + 1] - A.row_ptr[u] + merged_into[u];
+            sh_scan[tid] = want;
+            __syncthreads();
+            for (int off = 1; off < kCdaThreads; off <<= 1) {
+                const int add = tid >= off ? sh_scan[tid - off] : 0;
+                __syncthreads();
+                sh_scan[tid] += add;
+                __syncthreads();
+            }
+            int at = sh_scan[tid] - want;
+            for (int u = u_lo; u < u_hi; ++u) {
+                const int off = A.row_ptr[u], deg = A.row_ptr[u + 1] - off, full = deg + merged_into[u];
+                for (int i = 0; i < deg; ++i) {
+                    e_id[at + i] = A.col_idx[off + i];
+                    e_cnt[at + i] = 1;
+                }
+                head[u] = at; len[u] = deg; cap[u] = full; cdeg[u] = full; merged_into[u] = -1;
+                pos[u] = -1;
+                at += full;
+            }
+            my_deg = want;
+            __syncthreads();
+            for (int j = tid; j < cols; j += kCdaThreads) {  // the thread that clears a gene's bit appends its pair
+                const int gene = g[j];
+                const int a = A.add_u[gene];
+                if (a < 0) continue;
+                const unsigned bit = 1u << (gene & 31);
+                if (atomicAnd(&gone[gene >> 5], ~bit) & bit) {
+                    const int b = A.add_v[gene];
+                    const int qa = head[a] + atomicAdd(&len[a], 1);
+                    e_id[qa] = b;
+                    e_cnt[qa] = 1;
+                    const int qb = head[b] + atomicAdd(&len[b], 1);
+                    e_id[qb] = a;
+                    e_cnt[qb] = 1;
                 }
             }
-            head[u] = off; len[u] = cnt; cap[u] = end - off; cdeg[u] = cnt; merged_into[u] = -1;
-            pos[u] = -1;
-            my_deg += cnt;
         }
         for (int off = 16; off; off >>= 1) my_deg += __shfl_down_sync(0xffffffffu, my_deg, off);
         if (lane == 0 && my_deg) atomicAdd(reinterpret_cast<unsigned long long*>(&sh_total), static_cast<unsigned long long>(my_deg));
@@ -170,7 +233,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         }
         const double m = static_cast<double>(total_degree) / 2.0;  // community.cpp:36
         const double den = 2.0 * m * m;
-        if (tid == 0) sh_pool_top = A.csr_slots;
+        if (tid == 0) sh_pool_top = adding ? total_degree : A.csr_slots;
 
         // initial gains and cached bests
         for (int u = tid; u < n; u += kCdaThreads) {
@@ -447,10 +510,11 @@ int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
     const int n = ctx->n;
     if (n == 0) return fail(GAPA_CUDA_E_INVALID, "cda_fitness: empty graph");
     const long long csr_slots = 2 * ctx->m;
-    const int mask_words = static_cast<int>((ctx->m + 31) / 32) + 1;
+    const bool adding = ctx->pool_kind == GAPA_POOL_EDGE_ADDITION;
+    const int mask_words = static_cast<int>(((adding ? static_cast<int64_t>(ctx->pool_size) : ctx->m) + 31) / 32) + 1;
     const int slots = std::max(1, std::min(rows, ctx->sm_count));
     const int pos_in_smem = static_cast<size_t>(n) * 7 * sizeof(int32_t) <= 200 * 1024 ? 2 : (static_cast<size_t>(n) * sizeof(int32_t) <= 160 * 1024 ? 1 : 0);
-    if (s->pool_cap == 0) s->pool_cap = static_cast<size_t>(csr_slots) * 6 + 4096;
+    s->pool_cap = std::max(s->pool_cap, static_cast<size_t>(csr_slots + (adding ? 2ll * genes.cols : 0)) * 6 + 4096);
 
     for (;;) {
         GAPA_TRY(s->gone.ensure(sizeof(unsigned) * mask_words * static_cast<size_t>(slots)));
@@ -467,6 +531,8 @@ int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
         A.col_idx = ctx->d_col_idx;
         A.edge_id = ctx->d_edge_id;
         A.pool_map = ctx->pool_identity ? nullptr : ctx->d_pool_map;
+        A.add_u = adding ? ctx->d_add_u : nullptr;
+        A.add_v = adding ? ctx->d_add_v : nullptr;
         A.pool_size = ctx->pool_size;
         A.n = n;
         A.mask_words = mask_words;

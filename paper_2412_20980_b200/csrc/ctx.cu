@@ -212,8 +212,9 @@ int gapa_cuda_destroy(gapa_cuda_ctx* c) {
     pc_free(c);
     lpa_free(c);
     cda_free(c);
+    sixdst_free(c);
     for (int32_t* p : {c->d_row_ptr, c->d_col_idx, c->d_edge_id, c->d_edge_u, c->d_edge_v, c->d_by_degree,
-                       c->d_pool_map, c->d_pairs})
+                       c->d_pool_map, c->d_pairs, c->d_add_u, c->d_add_v})
         if (p) cudaFree(p);
     c->genes_stage.release();
     c->out_stage.release();
@@ -236,13 +237,65 @@ int gapa_cuda_graph_info(const gapa_cuda_ctx* c, int32_t* n, int64_t* m, int* de
     return GAPA_CUDA_OK;
 }
 
+// EdgeAddition pools: with u == NULL every non-edge (a < b) in lexicographic order
+// (build_gene_pool, gene_pool.cpp:81-87); otherwise the caller's pairs.
+static int pool_set_addition(gapa_cuda_ctx* c, int32_t n_genes, const int32_t* u, const int32_t* v) {
+    std::vector<int32_t> au, av;
+    if (!u) {
+        const int64_t n = c->n, size = n * (n - 1) / 2 - c->m;
+        if (size <= 0) return fail(GAPA_CUDA_E_INVALID, "gene pool: graph is complete, no edges can be added");
+        if (size > 0x7fffffffll) return fail(GAPA_CUDA_E_INVALID, "gene pool: %lld non-edges do not fit int32 gene ids", static_cast<long long>(size));
+        au.reserve(static_cast<size_t>(size));
+        av.reserve(static_cast<size_t>(size));
+        for (int32_t a = 0; a < c->n; ++a) {
+            int32_t i = c->h_row_ptr[a];
+            const int32_t ie = c->h_row_ptr[a + 1];
+            while (i < ie && c->h_col_idx[i] <= a) ++i;
+            for (int32_t b = a + 1; b < c->n; ++b) {
+                if (i < ie && c->h_col_idx[i] == b) { ++i; continue; }
+                au.push_back(a);
+                av.push_back(b);
+            }
+        }
+    } else {
+        if (!v) return fail(GAPA_CUDA_E_INVALID, "pool_set: edge pool needs both endpoint arrays");
+        if (n_genes < 0) return fail(GAPA_CUDA_E_INVALID, "pool_set: negative size");
+        au.resize(static_cast<size_t>(n_genes));
+        av.resize(static_cast<size_t>(n_genes));
+        std::vector<uint64_t> keys(static_cast<size_t>(n_genes));
+        for (int32_t i = 0; i < n_genes; ++i) {
+            int32_t a = u[i], b = v[i];
+            if (a < 0 || b < 0 || a >= c->n || b >= c->n || a == b)
+                return fail(GAPA_CUDA_E_INVALID, "pool_set: (%d, %d) is not a valid node pair", a, b);
+            if (a > b) std::swap(a, b);
+            keys[i] = (static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(b);
+            const bool present = edge_rank(c, a, b) >= 0;  // adjacency.set on a set bit: no-op
+            au[i] = present ? -1 : a;
+            av[i] = present ? -1 : b;
+        }
+        std::sort(keys.begin(), keys.end());
+        if (std::adjacent_find(keys.begin(), keys.end()) != keys.end())
+            return fail(GAPA_CUDA_E_INVALID, "gene pool: duplicate element");  // gene_pool.cpp:40
+    }
+    GAPA_CUDA_TRY(cudaSetDevice(c->device));
+    for (int32_t** p : {&c->d_pool_map, &c->d_add_u, &c->d_add_v})
+        if (*p) { cudaFree(*p); *p = nullptr; }
+    GAPA_TRY(upload_i32(au, &c->d_add_u));
+    GAPA_TRY(upload_i32(av, &c->d_add_v));
+    c->pool_kind = GAPA_POOL_EDGE_ADDITION;
+    c->pool_size = static_cast<int32_t>(au.size());
+    c->pool_identity = true;
+    c->h_pool_map.clear();
+    ++c->pool_version;
+    return GAPA_CUDA_OK;
+}
+
 int gapa_cuda_pool_set(gapa_cuda_ctx* c, int kind, int32_t n_genes, const int32_t* u, const int32_t* v) {
     if (!c) return fail(GAPA_CUDA_E_INVALID, "pool_set: null context");
-    if (kind == GAPA_POOL_EDGE_ADDITION)
-        return fail(GAPA_CUDA_E_INVALID, "pool_set: edge-addition pools are not on the CUDA path yet");
-    if (kind != GAPA_POOL_NODE_REMOVAL && kind != GAPA_POOL_EDGE_REMOVAL)
+    if (kind != GAPA_POOL_NODE_REMOVAL && kind != GAPA_POOL_EDGE_REMOVAL && kind != GAPA_POOL_EDGE_ADDITION)
         return fail(GAPA_CUDA_E_INVALID, "pool_set: unknown pool kind %d", kind);
     if (c->n == 0) return fail(GAPA_CUDA_E_INVALID, "gene pool: graph is empty");  // gene_pool.cpp:70
+    if (kind == GAPA_POOL_EDGE_ADDITION) return pool_set_addition(c, n_genes, u, v);
     const int32_t full = kind == GAPA_POOL_NODE_REMOVAL ? c->n : static_cast<int32_t>(c->m);
     if (!u) n_genes = full;
     if (n_genes < 0) return fail(GAPA_CUDA_E_INVALID, "pool_set: negative size");
@@ -262,8 +315,15 @@ int gapa_cuda_pool_set(gapa_cuda_ctx* c, int kind, int32_t n_genes, const int32_
         map[i] = target;
         identity &= (target == i);
     }
+    if (!identity) {  // GenePool's constructor rejects repeated elements (gene_pool.cpp:36-41)
+        std::vector<int32_t> sorted(map);
+        std::sort(sorted.begin(), sorted.end());
+        if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+            return fail(GAPA_CUDA_E_INVALID, "gene pool: duplicate element");
+    }
     GAPA_CUDA_TRY(cudaSetDevice(c->device));
-    if (c->d_pool_map) { cudaFree(c->d_pool_map); c->d_pool_map = nullptr; }
+    for (int32_t** p : {&c->d_pool_map, &c->d_add_u, &c->d_add_v})
+        if (*p) { cudaFree(*p); *p = nullptr; }
     if (!identity) GAPA_TRY(upload_i32(map, &c->d_pool_map));
     c->pool_kind = kind;
     c->pool_size = n_genes;
@@ -301,6 +361,7 @@ static int check_task(const gapa_cuda_ctx* c, int task) {
     switch (task) {
         case GAPA_TASK_PC:
         case GAPA_TASK_MCN:
+        case GAPA_TASK_SIXDST:
             if (c->pool_kind != GAPA_POOL_NODE_REMOVAL)
                 return fail(GAPA_CUDA_E_INVALID, "%s: incompatible gene pool kind", task == GAPA_TASK_PC ? "pc_fitness" : "sixdst_fitness");
             return GAPA_CUDA_OK;
@@ -327,7 +388,9 @@ static int eval_rows_locked(gapa_cuda_ctx* c, int task, const GeneRows& genes, i
         rc = pc_eval(c, task, genes, rows, out_dev, s, vary != nullptr, vary);  // builds the children itself
     } else {
         if (vary) GAPA_TRY(launch_variation_spec(*vary, genes.cols, rows, s));
-        rc = task == GAPA_TASK_CDA ? cda_eval(c, genes, rows, out_dev, s) : lpa_eval(c, genes, rows, out_dev, s, vary != nullptr);
+        rc = task == GAPA_TASK_CDA      ? cda_eval(c, genes, rows, out_dev, s)
+             : task == GAPA_TASK_SIXDST ? sixdst_eval(c, genes, rows, out_dev, s, vary != nullptr)
+                                        : lpa_eval(c, genes, rows, out_dev, s, vary != nullptr);
     }
     if (rc != GAPA_CUDA_OK) return rc;
     GAPA_CUDA_TRY(cudaEventRecord(c->ev_stop, s));

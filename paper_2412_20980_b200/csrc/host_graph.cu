@@ -153,4 +153,41 @@ int gapa_host_budget(int64_t basis, double rate, int32_t* k) {
     return GAPA_CUDA_OK;
 }
 
+// EdgeAddition pool of build_gene_pool (gene_pool.cpp:81-87): every pair a < b that is not
+// an edge, in lexicographic order.  `edges` are m (u, v) pairs in either orientation.
+int gapa_host_nonedges(int32_t n, int64_t m, const int32_t* edges, int32_t* uv, int64_t capacity, int64_t* count) {
+    if (n < 1 || m < 0 || (m > 0 && !edges)) return fail(GAPA_CUDA_E_INVALID, "gene pool: graph is empty");
+    std::vector<std::vector<int32_t>> above(static_cast<size_t>(n));
+    for (int64_t e = 0; e < m; ++e) {
+        int32_t a = edges[2 * e], b = edges[2 * e + 1];
+        if (a < 0 || b < 0 || a >= n || b >= n || a == b) return fail(GAPA_CUDA_E_INVALID, "gene pool: invalid edge (%d, %d)", a, b);
+        if (a > b) std::swap(a, b);
+        above[a].push_back(b);
+    }
+    int64_t present = 0;
+    for (auto& row : above) {
+        std::sort(row.begin(), row.end());
+        row.erase(std::unique(row.begin(), row.end()), row.end());
+        present += static_cast<int64_t>(row.size());
+    }
+    const int64_t size = static_cast<int64_t>(n) * (n - 1) / 2 - present;
+    if (size <= 0) return fail(GAPA_CUDA_E_INVALID, "gene pool: graph is complete, no edges can be added");
+    if (count) *count = size;
+    if (!uv) return GAPA_CUDA_OK;  // size query
+    if (capacity < size) return fail(GAPA_CUDA_E_INVALID, "gene pool: pair buffer too small (%lld < %lld)",
+                                     static_cast<long long>(capacity), static_cast<long long>(size));
+    int64_t at = 0;
+    for (int32_t a = 0; a < n; ++a) {
+        size_t i = 0;
+        const std::vector<int32_t>& row = above[a];
+        for (int32_t b = a + 1; b < n; ++b) {
+            if (i < row.size() && row[i] == b) { ++i; continue; }
+            uv[2 * at] = a;
+            uv[2 * at + 1] = b;
+            ++at;
+        }
+    }
+    return GAPA_CUDA_OK;
+}
+
 }  // extern "C"

@@ -124,6 +124,7 @@ struct GeneRows {
 struct PcScratch;   // pc_kernels.cu
 struct LpaScratch;  // lpa_kernels.cu
 struct CdaScratch;  // cda_kernels.cu
+struct SixScratch;  // sixdst_kernels.cu
 
 }  // namespace gapa_b200
 
@@ -148,6 +149,10 @@ struct gapa_cuda_ctx {
     int32_t* d_pool_map = nullptr;  // gene id -> node id / edge rank when not identity
     std::vector<int32_t> h_pool_map;  // host copy of the same map (empty when identity)
     unsigned long long pool_version = 0;  // bumped by gapa_cuda_pool_set
+    // EdgeAddition pool (gene_pool.cpp:57-60, :81-87): gene id -> endpoints of the pair it adds;
+    // (-1, -1) when the pair is already an edge of the graph (setting a set bit is a no-op)
+    int32_t* d_add_u = nullptr;
+    int32_t* d_add_v = nullptr;
     // link-prediction split
     int32_t T = 0, P = 0;
     int32_t* d_pairs = nullptr;     // (T + P) x 2, test pairs first
@@ -166,6 +171,7 @@ struct gapa_cuda_ctx {
     gapa_b200::PcScratch* pc = nullptr;
     gapa_b200::LpaScratch* lpa = nullptr;
     gapa_b200::CdaScratch* cda = nullptr;
+    gapa_b200::SixScratch* six = nullptr;
 };
 
 namespace gapa_b200 {
@@ -182,7 +188,9 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
 int launch_variation_spec(const VariationSpec& spec, int k, int rows, cudaStream_t stream);  // slot_kernels.cu
 int lpa_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream, bool trusted = false);
 int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream);
+int sixdst_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream, bool trusted = false);
 void pc_free(gapa_cuda_ctx* ctx);
+void sixdst_free(gapa_cuda_ctx* ctx);
 void lpa_free(gapa_cuda_ctx* ctx);
 void cda_free(gapa_cuda_ctx* ctx);
 

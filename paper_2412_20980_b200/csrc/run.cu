@@ -135,7 +135,9 @@ int eval_rows(gapa_cuda_ctx* ctx, int task, const GeneRows& view, int rows, doub
         rc = pc_eval(ctx, task, view, rows, out, st, true, vary);  // builds the children itself (fused with the mask build)
     } else {
         if (vary) GAPA_TRY(launch_variation_spec(*vary, view.cols, rows, st));
-        rc = task == GAPA_TASK_CDA ? cda_eval(ctx, view, rows, out, st) : lpa_eval(ctx, view, rows, out, st, true);
+        rc = task == GAPA_TASK_CDA      ? cda_eval(ctx, view, rows, out, st)
+             : task == GAPA_TASK_SIXDST ? sixdst_eval(ctx, view, rows, out, st, true)
+                                        : lpa_eval(ctx, view, rows, out, st, true);
     }
     GAPA_TRY(rc);
     return timer->mark(st);
@@ -163,7 +165,7 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
     if (world > 1 && !exchange) return fail(GAPA_CUDA_E_INVALID, "run: sharded run needs an exchange hook");
     if (ctx->pool_size < 1) return fail(GAPA_CUDA_E_INVALID, "init_population: empty gene pool");
     switch (p->task) {
-        case GAPA_TASK_PC: case GAPA_TASK_MCN:
+        case GAPA_TASK_PC: case GAPA_TASK_MCN: case GAPA_TASK_SIXDST:
             if (ctx->pool_kind != GAPA_POOL_NODE_REMOVAL) return fail(GAPA_CUDA_E_INVALID, "run: incompatible gene pool kind");
             break;
         case GAPA_TASK_CDA:

@@ -66,6 +66,7 @@ private:
 };
 
 enum class PoolKind { EdgeRemoval, EdgeAddition, NodeRemoval };  // gene_pool.hpp:14
+enum class ClosurePolicy { Exact, SixDegrees };                   // accessibility.hpp:14
 struct GeneElement {                                              // gene_pool.hpp:21-25
     int u = -1, v = -1;
     bool is_node() const { return v < 0; }
@@ -91,8 +92,16 @@ inline GenePool build_gene_pool(const Graph& g, PoolKind kind) {  // gene_pool.c
         auto sorted = g.edges();
         std::sort(sorted.begin(), sorted.end());
         for (auto [u, v] : sorted) genes.push_back({u, v});
-    } else {
-        throw Error("gene pool: edge-addition pools are not on the CUDA path");
+    } else {  // every non-edge u < v, lexicographic (gene_pool.cpp:81-87)
+        auto sorted = g.edges();
+        std::sort(sorted.begin(), sorted.end());
+        std::size_t next = 0;
+        for (int u = 0; u < g.node_count(); ++u)
+            for (int v = u + 1; v < g.node_count(); ++v) {
+                if (next < sorted.size() && sorted[next] == std::pair(u, v)) { ++next; continue; }
+                genes.push_back({u, v});
+            }
+        if (genes.empty()) throw Error("gene pool: graph is complete, no edges can be added");
     }
     return GenePool(kind, std::move(genes));
 }

@@ -17,6 +17,7 @@
 #pragma once
 
 #ifdef GAPA_B200_USE_REFERENCE_HEADERS
+#include "gapa/accessibility.hpp"
 #include "gapa/error.hpp"
 #include "gapa/fitness.hpp"
 #include "gapa/ga_ops.hpp"
@@ -182,10 +183,15 @@ public:
     CudaPairwiseConnectivityObjective(const gapa::Graph& g, const gapa::GenePool& pool, int device = 0)
         : CudaObjective((require_kind(pool, gapa::PoolKind::NodeRemoval, "PairwiseConnectivityObjective"), GAPA_TASK_PC), g, pool, device) {}
 };
-class CudaSixDstObjective : public CudaObjective {  // fitness.hpp:56-66, ClosurePolicy::Exact
+// fitness.hpp:56-66.  Exact closure = largest component (the PC kernels); SixDegrees = largest
+// radius-8 ball (accessibility.hpp:12-14), the truncated multi-source BFS kernel.
+class CudaSixDstObjective : public CudaObjective {
 public:
-    CudaSixDstObjective(const gapa::Graph& g, const gapa::GenePool& pool, int device = 0)
-        : CudaObjective((require_kind(pool, gapa::PoolKind::NodeRemoval, "SixDstObjective"), GAPA_TASK_MCN), g, pool, device) {}
+    CudaSixDstObjective(const gapa::Graph& g, const gapa::GenePool& pool,
+                        gapa::ClosurePolicy policy = gapa::ClosurePolicy::Exact, int device = 0)
+        : CudaObjective((require_kind(pool, gapa::PoolKind::NodeRemoval, "SixDstObjective"),
+                         policy == gapa::ClosurePolicy::Exact ? GAPA_TASK_MCN : GAPA_TASK_SIXDST),
+                        g, pool, device) {}
 };
 class CudaModularityAttackObjective : public CudaObjective {  // fitness.hpp:79-88
 public:

@@ -50,6 +50,26 @@ int main() {
             try { gb::CudaPairwiseConnectivityObjective bad(g, build_gene_pool(g, PoolKind::EdgeRemoval)); } catch (const Error&) { threw = true; }
             CHECK(threw);  // pool-kind enforcement
         }
+        {  // truncated closure on P40 (test_fitness.cpp:94-103): radius-8 balls, not the whole path
+            std::vector<std::pair<int, int>> e;
+            for (int u = 0; u + 1 < 40; ++u) e.emplace_back(u, u + 1);
+            const Graph g(40, e);
+            const GenePool pool = build_gene_pool(g, PoolKind::NodeRemoval);
+            const gb::CudaSixDstObjective six(g, pool, ClosurePolicy::SixDegrees);
+            const gb::CudaSixDstObjective exact(g, pool);
+            CHECK(six.evaluate_one({}) == 17.0);
+            CHECK(exact.evaluate_one({}) == 40.0);
+            CHECK(six.evaluate_one(std::vector<std::int32_t>{8, 25}) == 16.0);
+        }
+        {  // EdgeAddition pool (gene_pool.cpp:81-87): two triangles, adding the three cross pairs of node 0
+            const Graph g(6, {{0, 1}, {1, 2}, {0, 2}, {3, 4}, {4, 5}, {3, 5}});
+            const GenePool pool = build_gene_pool(g, PoolKind::EdgeAddition);
+            CHECK(pool.size() == 9 && pool.gene(0).u == 0 && pool.gene(0).v == 3 && pool.gene(8).u == 2 && pool.gene(8).v == 5);
+            const gb::CudaModularityAttackObjective cda(g, pool);
+            CHECK(cda.evaluate_one({}) == 0.5);
+            CHECK(cda.evaluate_one(std::vector<std::int32_t>{0, 0}) == cda.evaluate_one(std::vector<std::int32_t>{0}));
+            CHECK(cda.evaluate_one(std::vector<std::int32_t>{0}) < 0.5);
+        }
         {  // CDA identities: empty perturbation == unattacked Q, all edges removed == -0.5
             const Graph g(6, {{0, 1}, {1, 2}, {0, 2}, {3, 4}, {4, 5}, {3, 5}});
             const GenePool pool = build_gene_pool(g, PoolKind::EdgeRemoval);

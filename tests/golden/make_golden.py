@@ -15,7 +15,8 @@ import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, os.path.dirname(os.path.dirname(HERE)))
-from oracle.bindings import (MODE_M, MODE_S, MODE_SERIAL, TASK_CDA, TASK_LPA, TASK_MCN, TASK_PC, Ref)  # noqa: E402
+from oracle.bindings import (MODE_M, MODE_S, MODE_SERIAL, TASK_CDA, TASK_CDA_ADD, TASK_LPA, TASK_MCN, TASK_PC, TASK_SIXDST,
+                             Ref)  # noqa: E402
 
 r = Ref()
 
@@ -204,3 +205,58 @@ dump("runs.json", runs)
 print("acceptance #6 final MCN", runs["acceptance6_sixdst_er100"]["best"][-1], "(reference test_output.txt:50 says 81)")
 print("acceptance #10 AUC", runs["acceptance10_lpa_sbm64"]["auc0"], "->", runs["acceptance10_lpa_sbm64"]["best"][-1])
 print("config 1 best", runs["config1_pc_ba1000"]["best"][0], "->", runs["config1_pc_ba1000"]["best"][-1])
+
+
+# ------------------------------------------------------------------ truncated closure, edge addition
+# (own generator so that the files above stay byte-identical when this section grows)
+gen2 = np.random.default_rng(777)
+wide = {"sixdst": [], "cda_add": []}
+path40 = np.stack([np.arange(39), np.arange(1, 40)], 1).astype(np.int32)  # test_fitness.cpp:94-103
+for trial in range(16):
+    if trial == 0:
+        n, edges = 40, path40
+    else:
+        n = int(gen2.integers(10, 150))
+        iu = np.triu_indices(n, 1)
+        keep = gen2.random(len(iu[0])) < float(gen2.uniform(0.6, 2.2)) / n
+        edges = np.stack([iu[0][keep], iu[1][keep]], 1).astype(np.int32)
+        if trial % 4 == 1:  # a long path through everything plus the random chords: large diameter
+            chain = np.stack([np.arange(n - 1), np.arange(1, n)], 1).astype(np.int32)
+            edges = np.unique(np.concatenate([edges, chain]), axis=0)
+    g = r.graph_from_edges(n, edges)
+    k = 0 if trial == 0 else int(gen2.integers(0, n // 5 + 1))
+    batch = gen2.integers(0, n, (3, k)).astype(np.int32)
+    wide["sixdst"].append({"n": n, "edges": ints(edges), "genes": ints(batch),
+                           "six": floats(r.eval_batch(g, TASK_SIXDST, batch)), "mcn": floats(r.eval_batch(g, TASK_MCN, batch))})
+g = r.graph_ba(1000, 2, 1)
+pop = r.init_population(1000, 4, 50, 1)
+wide["sixdst_config1"] = floats(r.eval_batch(g, TASK_SIXDST, pop))
+
+for trial in range(12):
+    n = int(gen2.integers(5, 60))
+    iu = np.triu_indices(n, 1)
+    keep = gen2.random(len(iu[0])) < (0.0 if trial == 0 else float(gen2.uniform(0.03, 0.3)))
+    edges = np.stack([iu[0][keep], iu[1][keep]], 1).astype(np.int32)
+    g = r.graph_from_edges(n, edges)
+    pu, pv = r.pool_genes(g, 1)
+    k = int(gen2.integers(0, 30))
+    batch = gen2.integers(0, len(pu), (3, k)).astype(np.int32)
+    if k > 2:
+        batch[1, 2] = batch[1, 0]
+    wide["cda_add"].append({"n": n, "edges": ints(edges), "pool_size": len(pu), "pool_sha": sha(np.stack([pu, pv], 1)),
+                            "genes": ints(batch), "q": floats(r.eval_batch(g, TASK_CDA_ADD, batch))})
+pu, pv = r.pool_genes(kar, 1)
+pop = r.init_population(len(pu), 5, 8, 11)
+wide["karate_add"] = {"pool_size": len(pu), "pool_first": ints(np.stack([pu, pv], 1)[:6]), "genes": ints(pop),
+                      "q": floats(r.eval_batch(kar, TASK_CDA_ADD, pop))}
+dump("widen.json", wide)
+
+runs = {}
+# acceptance #8 (acceptance.cpp:207-246): karate, QAttack defaults over the EdgeAddition pool, 300 iterations
+run_case("acceptance8_cda_add_karate", kar, TASK_CDA_ADD, 0.8, 0.1, 100, r.budget(kar, 1, 0.1), 300, 667)
+runs["acceptance8_cda_add_karate"]["q0"] = r.modularity_unattacked(kar)
+run_case("sixdegrees_ba300", r.graph_ba(300, 1, 668), TASK_SIXDST, 0.5, 0.3, 24, r.budget(r.graph_ba(300, 1, 668), 2, 0.1), 30, 670,
+         modes=((MODE_S, 1, 1), (MODE_M, 3, 1)))
+dump("runs_widen.json", runs)
+print("acceptance #8 Q", runs["acceptance8_cda_add_karate"]["q0"], "->", runs["acceptance8_cda_add_karate"]["best"][-1],
+      "(reference test_output.txt:52 says 0.380671 -> 0.26156 @300)")

@@ -12,6 +12,7 @@ import numpy as np
 
 GOLDEN = os.path.join(os.path.dirname(os.path.abspath(__file__)), "golden")
 TASK_PC, TASK_MCN, TASK_CDA, TASK_LPA = 0, 1, 2, 3
+TASK_SIXDST, TASK_CDA_ADD = 4, 5  # sixdst_fitness(SixDegrees); cda_fitness over the EdgeAddition pool
 
 
 def load(name):
@@ -52,8 +53,14 @@ class OracleImpl:
     def split(self, g, frac, seed):
         s = self.o.split_build(g, frac, seed)
         return s, s.test, s.probe, s.train.edges
-    def eval(self, ctx, task, genes): return self.o.eval_batch(ctx, task, genes)
+    def addition_pool(self, g): return np.stack(self.o.addition_pool(g), 1)
+    def eval(self, ctx, task, genes):
+        if task == TASK_CDA_ADD:
+            self.o.addition_pool(ctx)
+        return self.o.eval_batch(ctx, task, genes)
     def run(self, ctx, task, c):
+        if task == TASK_CDA_ADD:
+            self.o.addition_pool(ctx)
         r = self.o.run_ga(ctx, task, c["pc"], c["pm"], c["pop_size"], c["budget"], c["iterations"], c["seed"],
                           eda_interval=c["eda_interval"], threads=8)
         return r["best"], r["mean"], r["population"], r["fitness"]
@@ -89,8 +96,15 @@ class CudaImpl:
             return gp.LinkPredictionAttackObjective(ctx, gp.build_gene_pool(ctx.train, gp.PoolKind.EdgeRemoval))
         if task == TASK_CDA:
             return gp.ModularityAttackObjective(ctx, gp.build_gene_pool(ctx, gp.PoolKind.EdgeRemoval))
+        if task == TASK_CDA_ADD:
+            return gp.ModularityAttackObjective(ctx, gp.build_gene_pool(ctx, gp.PoolKind.EdgeAddition))
+        if task == TASK_SIXDST:
+            return gp.SixDstObjective(ctx, gp.build_gene_pool(ctx, gp.PoolKind.NodeRemoval), policy=gp.ClosurePolicy.SixDegrees)
         cls = gp.PairwiseConnectivityObjective if task == TASK_PC else gp.SixDstObjective
         return cls(ctx, gp.build_gene_pool(ctx, gp.PoolKind.NodeRemoval))
+    def addition_pool(self, g):
+        p = self.gp.build_gene_pool(g, self.gp.PoolKind.EdgeAddition)
+        return np.stack([p.u, p.v], 1)
     def eval(self, ctx, task, genes): return self.objective(ctx, task).evaluate_batch(genes)
     def run(self, ctx, task, c):
         obj = self.objective(ctx, task)
@@ -196,6 +210,37 @@ def check_lpa(impl):
     assert impl.eval(split, TASK_LPA, impl.init_population(k["train_m"], 3, k["k"], 1)).tolist() == k["auc"]
 
 
+def check_sixdegrees(impl):
+    """sixdst_fitness(SixDegrees): largest radius-8 ball (fitness.cpp:18-26, accessibility.cpp:20-37)."""
+    g = load("widen.json")
+    for c in g["sixdst"]:
+        ctx = impl.graph(c["n"], i32(c["edges"], 2))
+        genes = i32(c["genes"]).reshape(3, -1)
+        assert impl.eval(ctx, TASK_SIXDST, genes).tolist() == c["six"]
+        assert impl.eval(ctx, TASK_MCN, genes).tolist() == c["mcn"]
+    assert g["sixdst"][0]["six"] == [17.0] * 3 and g["sixdst"][0]["mcn"] == [40.0] * 3  # P40: 8 each side + self
+    ctx = impl.graph_named("ba", 1000, 2, 1)
+    assert impl.eval(ctx, TASK_SIXDST, impl.init_population(1000, 4, 50, 1)).tolist() == g["sixdst_config1"]
+
+
+def check_cda_add(impl):
+    """cda_fitness over EdgeAddition pools (gene_pool.cpp:57-60, :81-87)."""
+    g = load("widen.json")
+    for c in g["cda_add"]:
+        ctx = impl.graph(c["n"], i32(c["edges"], 2))
+        pool = impl.addition_pool(ctx)
+        assert len(pool) == c["pool_size"] and sha(np.asarray(pool, dtype=np.int32)) == c["pool_sha"]
+        genes = i32(c["genes"]).reshape(3, -1)
+        assert impl.eval(ctx, TASK_CDA_ADD, genes).tolist() == c["q"]
+    k = load("fitness.json")["karate"]
+    ctx = impl.graph(k["n"], i32(k["edges"], 2))
+    ka = g["karate_add"]
+    pool = impl.addition_pool(ctx)
+    assert len(pool) == ka["pool_size"] and np.asarray(pool)[:6].tolist() == ka["pool_first"]
+    assert impl.eval(ctx, TASK_CDA_ADD, i32(ka["genes"])).tolist() == ka["q"]
+    assert impl.eval(ctx, TASK_CDA_ADD, np.zeros((1, 0), np.int32)).tolist() == [k["q0"]]
+
+
 def _run_ctx(impl, name):
     if name == "config1_pc_ba1000":
         return impl.graph_named("ba", 1000, 2, 1)
@@ -205,14 +250,16 @@ def _run_ctx(impl, name):
         return impl.split(impl.graph_named("sbm", 4, 16, 0.28, 0.02, 671), 0.1, 672)[0]
     if name == "cda_sbm80":
         return impl.graph_named("sbm", 4, 20, 0.3, 0.03, 1)
-    if name == "cda_karate":
+    if name == "sixdegrees_ba300":
+        return impl.graph_named("ba", 300, 1, 668)
+    if name in ("cda_karate", "acceptance8_cda_add_karate"):
         k = load("fitness.json")["karate"]
         return impl.graph(k["n"], i32(k["edges"], 2))
     raise KeyError(name)
 
 
 def check_run(impl, name):
-    c = load("runs.json")[name]
+    c = load("runs_widen.json" if name in WIDE_RUN_NAMES else "runs.json")[name]
     best, mean, pop, fit = impl.run(_run_ctx(impl, name), c["task"], c)
     assert np.asarray(best).tolist() == c["best"]
     assert np.asarray(mean).tolist() == c["mean"]          # sequential-sum mean, bit for bit
@@ -221,5 +268,6 @@ def check_run(impl, name):
     assert np.asarray(pop)[0].tolist() == c["best_individual"]
 
 
+WIDE_RUN_NAMES = ["acceptance8_cda_add_karate", "sixdegrees_ba300"]
 RUN_NAMES = ["config1_pc_ba1000", "acceptance6_sixdst_er100", "pc_er100_eda3", "acceptance10_lpa_sbm64", "cda_sbm80",
-             "cda_karate"]
+             "cda_karate"] + WIDE_RUN_NAMES

@@ -13,7 +13,7 @@ def impl(gp, cuda_device):
 
 @pytest.mark.parametrize("check", [gc.check_rng_and_init, gc.check_selection, gc.check_variation,
                                    gc.check_elitism_eda_partition, gc.check_generators, gc.check_pc_mcn, gc.check_cda,
-                                   gc.check_lpa], ids=lambda f: f.__name__)
+                                   gc.check_lpa, gc.check_sixdegrees, gc.check_cda_add], ids=lambda f: f.__name__)
 def test_cuda_matches_golden(impl, check):
     check(impl)
 

@@ -12,7 +12,7 @@ def impl(oracle):
 
 @pytest.mark.parametrize("check", [gc.check_rng_and_init, gc.check_selection, gc.check_variation,
                                    gc.check_elitism_eda_partition, gc.check_generators, gc.check_pc_mcn, gc.check_cda,
-                                   gc.check_lpa], ids=lambda f: f.__name__)
+                                   gc.check_lpa, gc.check_sixdegrees, gc.check_cda_add], ids=lambda f: f.__name__)
 def test_oracle_matches_golden(impl, check):
     check(impl)
 
@@ -29,4 +29,5 @@ def test_recorded_reference_values(oracle):
     assert f'{runs["acceptance10_lpa_sbm64"]["auc0"]:.6f}' == "0.728395"           # criterion 10
     assert f'{runs["acceptance10_lpa_sbm64"]["best"][-1]:.6f}' == "0.388889"
     assert f'{gc.load("fitness.json")["karate"]["q0"]:.6f}' == "0.380671"          # criterion 8: unattacked Q
+    assert f'{gc.load("runs_widen.json")["acceptance8_cda_add_karate"]["best"][-1]:.5f}' == "0.26156"  # attacked Q @300
     assert oracle.mix64(0) == 0xE220A8397B1DCDAF and oracle.mix64(1) == 0x910A2DEC89025CC1
