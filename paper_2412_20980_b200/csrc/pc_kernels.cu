@@ -164,9 +164,18 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask_vary(VariationSpec 
         const int4* mine4 = reinterpret_cast<const int4*>(mine);
         const int4* theirs4 = reinterpret_cast<const int4*>(theirs);
         int4* dst4 = reinterpret_cast<int4*>(dst);
-        for (int q = threadIdx.x; q < (k >> 2); q += kMaskThreads) {
-            const int4 a = mine4[q];
-            const int4 b = eda ? a : theirs4[q];
+        const int quads = k >> 2;
+        int4 a_next = make_int4(0, 0, 0, 0), b_next = a_next;
+        if (threadIdx.x < quads) {
+            a_next = __ldcs(&mine4[threadIdx.x]);
+            b_next = eda ? a_next : __ldcs(&theirs4[threadIdx.x]);
+        }
+        for (int q = threadIdx.x; q < quads; q += kMaskThreads) {
+            const int4 a = a_next, b = b_next;
+            if (q + kMaskThreads < quads) {  // next quad's parents are in flight while this one is hashed
+                a_next = __ldcs(&mine4[q + kMaskThreads]);
+                b_next = eda ? a_next : __ldcs(&theirs4[q + kMaskThreads]);
+            }
             const int av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
             int r[4];
             uint64_t prod = kCounterStep * (static_cast<uint64_t>(q) * 4 + 1);

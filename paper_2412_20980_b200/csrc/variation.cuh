@@ -31,14 +31,18 @@ struct VariationParams {
 __device__ __forceinline__ int32_t child_gene(const VariationParams& P, const int32_t* __restrict__ pool,
                                               const int32_t* __restrict__ parent, int k, int col, int mine, int theirs,
                                               bool eda, uint64_t ks, uint64_t kc, uint64_t km, uint64_t ki, uint64_t prod) {
+    // Exactly TWO hashes per gene and no divergent branch: the mutation-mask draw decides WHICH second
+    // stream is read at this column (MutationIndex for a flipped gene, else CrossoverMask / Select) —
+    // a flipped gene never needs its crossover draw (mutate overwrites it, ga_ops.cpp:171-174), and the
+    // streams are counter-based, so the unread draw is simply never computed.
     const uint64_t um = hash_tail(km + prod);
-    if (P.pm_always || um < P.pm_limit) return static_cast<int32_t>(__umul64hi(hash_tail(ki + prod), static_cast<uint64_t>(P.pool_size)));
-    if (eda) {
-        const uint32_t v = static_cast<uint32_t>(__umul64hi(hash_tail(ks + prod), static_cast<uint64_t>(P.s + P.pool_size)));
-        return v < P.s ? pool[static_cast<size_t>(parent[v]) * k + col] : static_cast<int32_t>(v - P.s);
-    }
-    const uint64_t ux = hash_tail(kc + prod);
-    return (P.pc_always || ux < P.pc_limit) ? theirs : mine;
+    const bool flip = P.pm_always || um < P.pm_limit;
+    const uint64_t u2 = hash_tail((flip ? ki : (eda ? ks : kc)) + prod);
+    const uint32_t bound = flip ? P.pool_size : P.s + P.pool_size;  // next_index bound (rng.hpp:28-31)
+    const uint32_t idx = static_cast<uint32_t>(__umul64hi(u2, static_cast<uint64_t>(bound)));
+    if (flip) return static_cast<int32_t>(idx);
+    if (eda) return idx < P.s ? pool[static_cast<size_t>(parent[idx]) * k + col] : static_cast<int32_t>(idx - P.s);
+    return (P.pc_always || u2 < P.pc_limit) ? theirs : mine;
 }
 
 
