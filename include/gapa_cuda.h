@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define GAPA_CUDA_ABI_VERSION 1
+#define GAPA_CUDA_ABI_VERSION 2
 
 enum {
     GAPA_CUDA_OK = 0,
@@ -242,6 +242,18 @@ typedef struct gapa_cuda_run_result {
     uint64_t fitness_batch_calls;
     double total_wall_seconds; /* generation loop only */
     double eval_seconds;       /* device time inside fitness kernels (CUDA events)        */
+    /* GenerationStats timing columns (modes.hpp:63-71), each [iterations] or NULL.  Device time
+     * between CUDA events recorded on the run's stream and read back after the loop, so asking for
+     * them adds no synchronisation.  wall = one generation (generation 1 includes init + the first
+     * evaluation, modes.cpp:139-156); exchange = time inside the exchange hook (the fitness
+     * all-gather; 0 on one GPU); lifecycle = 0 (no worker threads are spawned or joined);
+     * compute = wall - exchange - lifecycle (record_generation, modes.cpp:38-40);
+     * messages = exchanges issued in that generation. */
+    double* gen_wall_seconds;
+    double* gen_compute_seconds;
+    double* gen_exchange_seconds;
+    double* gen_lifecycle_seconds;
+    uint64_t* gen_messages;
 } gapa_cuda_run_result;
 
 int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* params, gapa_cuda_allgather_fn exchange,

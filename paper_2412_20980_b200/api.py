@@ -449,6 +449,17 @@ def partition_rows(pop_size: int, pn: int) -> list[tuple[int, int]]:  # modes.cp
 
 # ---------------------------------------------------------------------------- run
 @dataclass
+class GenerationStats:  # modes.hpp:63-71
+    best: float = 0.0
+    mean: float = 0.0
+    wall_seconds: float = 0.0
+    compute_seconds: float = 0.0
+    exchange_seconds: float = 0.0
+    lifecycle_seconds: float = 0.0
+    messages: int = 0
+
+
+@dataclass
 class RunResult:  # modes.hpp:73-82
     final_population: np.ndarray
     final_fitness: np.ndarray
@@ -459,7 +470,18 @@ class RunResult:  # modes.hpp:73-82
     fitness_batch_calls: int = 0
     total_wall_seconds: float = 0.0
     eval_seconds: float = 0.0
+    history: list = field(default_factory=list)  # one GenerationStats per generation
     extra: dict = field(default_factory=dict)
+
+
+def overhead_report(result: RunResult) -> str:
+    """modes.cpp:518-530: aligned per-generation table of {wall, compute, exchange, lifecycle, messages},
+    byte-compatible with the reference's format."""
+    lines = ["gen  wall_s      compute_s   exchange_s  lifecycle_s messages\n"]
+    for g, h in enumerate(result.history):
+        lines.append("%-4d %-11.6f %-11.6f %-11.6f %-11.6f %d\n" % (g + 1, h.wall_seconds, h.compute_seconds,
+                                                                  h.exchange_seconds, h.lifecycle_seconds, h.messages))
+    return "".join(lines)
 
 
 def run_ga(params: GAParams, pool: GenePool, fitness: FitnessFunction, rank: int = 0, world: int = 1,
@@ -474,9 +496,16 @@ def run_ga(params: GAParams, pool: GenePool, fitness: FitnessFunction, rank: int
     fp, ff = np.zeros((s, k), dtype=np.int32), np.zeros(s)
     p = capi.RunParams(params.pc, params.pm, s, k, it, _minimize(params.direction), params.eda_interval or 0,
                        fitness.task, params.seed, rank, world)
+    wall, comp, exch, life = (np.zeros(it) for _ in range(4))
+    msgs = np.zeros(it, dtype=np.uint64)
     r = capi.RunResult(hb.ctypes.data_as(capi.c_f64p), hm.ctypes.data_as(capi.c_f64p),
-                       fp.ctypes.data_as(capi.c_i32p), ff.ctypes.data_as(capi.c_f64p), 0, 0.0, 0.0)
+                       fp.ctypes.data_as(capi.c_i32p), ff.ctypes.data_as(capi.c_f64p), 0, 0.0, 0.0,
+                       wall.ctypes.data_as(capi.c_f64p), comp.ctypes.data_as(capi.c_f64p),
+                       exch.ctypes.data_as(capi.c_f64p), life.ctypes.data_as(capi.c_f64p),
+                       msgs.ctypes.data_as(C.POINTER(C.c_uint64)))
     cb = capi.ALLGATHER_FN(exchange) if exchange is not None else C.cast(None, capi.ALLGATHER_FN)
     check(lib.gapa_cuda_run(fitness.dgraph.handle, C.byref(p), cb, None, C.byref(r)))
+    history = [GenerationStats(float(hb[i]), float(hm[i]), float(wall[i]), float(comp[i]), float(exch[i]), float(life[i]),
+                               int(msgs[i])) for i in range(it)]
     return RunResult(fp, ff, fp[0].copy(), float(ff[0]), hb, hm, int(r.fitness_batch_calls),
-                     float(r.total_wall_seconds), float(r.eval_seconds))
+                     float(r.total_wall_seconds), float(r.eval_seconds), history)

@@ -36,7 +36,8 @@ class RunParams(C.Structure):
 class RunResult(C.Structure):
     _fields_ = [("history_best", c_f64p), ("history_mean", c_f64p), ("final_population", c_i32p),
                 ("final_fitness", c_f64p), ("fitness_batch_calls", C.c_uint64), ("total_wall_seconds", C.c_double),
-                ("eval_seconds", C.c_double)]
+                ("eval_seconds", C.c_double), ("gen_wall_seconds", c_f64p), ("gen_compute_seconds", c_f64p),
+                ("gen_exchange_seconds", c_f64p), ("gen_lifecycle_seconds", c_f64p), ("gen_messages", C.POINTER(C.c_uint64))]
 
 
 ALLGATHER_FN = C.CFUNCTYPE(C.c_int, VP, VP, C.c_int, C.c_int, VP)

@@ -215,12 +215,22 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
     result->fitness_batch_calls = 0;
     result->eval_seconds = 0.0;
     EvalTimer timer;
+    // GenerationStats timing (modes.hpp:63-71): generation boundaries and the exchange hook are
+    // bracketed by events on the run's stream; everything is read back after the loop.
+    const bool want_stats = result->gen_wall_seconds || result->gen_compute_seconds || result->gen_exchange_seconds ||
+                            result->gen_lifecycle_seconds || result->gen_messages;
+    EvalTimer gen_marks, exchange_marks;
+    std::vector<int> exchanges_in_gen(static_cast<size_t>(iters), 0);
+    int current_gen = 1;
     auto evaluate = [&](const int32_t* table, double* fit_all, const VariationSpec* vary = nullptr) -> int {  // rows [lo, hi) named by `table`
         ++result->fitness_batch_calls;
         GAPA_TRY(eval_rows(ctx, p->task, GeneRows{pool_rows, table + lo, k}, hi - lo, fit_all + lo, st, &timer, vary));
         if (world > 1) {
+            if (want_stats) GAPA_TRY(exchange_marks.mark(st));
             const int rc = exchange(exchange_user, fit_all, s, block, st);
             if (rc != 0) return fail(GAPA_CUDA_E_CUDA, "run: exchange hook failed with status %d", rc);
+            if (want_stats) GAPA_TRY(exchange_marks.mark(st));
+            ++exchanges_in_gen[current_gen - 1];
         }
         return GAPA_CUDA_OK;
     };
@@ -234,6 +244,8 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
 
     const auto t0 = std::chrono::steady_clock::now();
     for (int gen = 1; gen <= iters; ++gen) {
+        current_gen = gen;
+        if (want_stats) GAPA_TRY(gen_marks.mark(st));
         if (gen == 1) {
             GAPA_TRY(launch_slots_identity(s, parent, child, st));
             GAPA_TRY(launch_init(pool, 0, s, k, p->seed, 0, pool_rows, st));  // parents occupy slots 0..s-1
@@ -272,8 +284,28 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
             if (h == GAPA_CUDA_E_NAN) return fail(GAPA_CUDA_E_NAN, "elitism: NaN fitness");
         }
     }
+    if (want_stats) GAPA_TRY(gen_marks.mark(st));
     GAPA_CUDA_TRY(cudaStreamSynchronize(st));
     GAPA_TRY(timer.total_seconds(&result->eval_seconds));
+    if (want_stats) {
+        size_t next_exchange = 0;
+        for (int gi = 0; gi < iters; ++gi) {
+            float wall_ms = 0.f;
+            GAPA_CUDA_TRY(cudaEventElapsedTime(&wall_ms, gen_marks.events[gi], gen_marks.events[gi + 1]));
+            double exchange_s = 0.0;
+            for (int e = 0; e < exchanges_in_gen[gi]; ++e, next_exchange += 2) {
+                float ms = 0.f;
+                GAPA_CUDA_TRY(cudaEventElapsedTime(&ms, exchange_marks.events[next_exchange], exchange_marks.events[next_exchange + 1]));
+                exchange_s += ms * 1e-3;
+            }
+            const double wall_s = wall_ms * 1e-3;
+            if (result->gen_wall_seconds) result->gen_wall_seconds[gi] = wall_s;
+            if (result->gen_exchange_seconds) result->gen_exchange_seconds[gi] = exchange_s;
+            if (result->gen_lifecycle_seconds) result->gen_lifecycle_seconds[gi] = 0.0;
+            if (result->gen_compute_seconds) result->gen_compute_seconds[gi] = std::max(0.0, wall_s - exchange_s);  // modes.cpp:38-40
+            if (result->gen_messages) result->gen_messages[gi] = static_cast<uint64_t>(exchanges_in_gen[gi]);
+        }
+    }
     result->total_wall_seconds = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
 
     if (result->history_best) GAPA_CUDA_TRY(cudaMemcpy(result->history_best, hist, sizeof(double) * iters, cudaMemcpyDeviceToHost));

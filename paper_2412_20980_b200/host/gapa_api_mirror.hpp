@@ -132,8 +132,10 @@ struct GAParams {  // ga_ops.hpp:12-23
     std::uint64_t seed = 1;
 };
 
-struct GenerationStats {  // modes.hpp:63-71 (the two value columns)
+struct GenerationStats {  // modes.hpp:63-71
     double best = 0.0, mean = 0.0;
+    double wall_seconds = 0.0, compute_seconds = 0.0, exchange_seconds = 0.0, lifecycle_seconds = 0.0;
+    std::uint64_t messages = 0;
 };
 struct RunResult {  // modes.hpp:73-82
     PopulationMatrix final_population;

@@ -306,7 +306,8 @@ inline gapa::RunResult run_ga_cuda(const gapa::GAParams& params, const CudaObjec
     p.rank = 0;
     p.world = 1;
     const int s = std::max(params.pop_size, 0), k = std::max(params.budget, 0), it = std::max(params.iterations, 0);
-    std::vector<double> best(it), mean(it);
+    std::vector<double> best(it), mean(it), wall(it), compute(it), exch(it), life(it);
+    std::vector<std::uint64_t> messages(it);
     gapa::RunResult out;
     out.final_population = gapa::PopulationMatrix(s, k);
     out.final_fitness.assign(s, 0.0);
@@ -315,6 +316,11 @@ inline gapa::RunResult run_ga_cuda(const gapa::GAParams& params, const CudaObjec
     r.history_mean = mean.data();
     r.final_population = out.final_population.data.data();
     r.final_fitness = out.final_fitness.data();
+    r.gen_wall_seconds = wall.data();  // GenerationStats timing columns: device time between CUDA events
+    r.gen_compute_seconds = compute.data();
+    r.gen_exchange_seconds = exch.data();
+    r.gen_lifecycle_seconds = life.data();
+    r.gen_messages = messages.data();
     const auto& lib = CudaLib::get();
     const int status = lib.gapa_cuda_run(objective.problem().handle(), &p, nullptr, nullptr, &r);
     if (status == GAPA_CUDA_E_INVALID) throw gapa::ConfigError(lib.gapa_cuda_last_error());
@@ -323,6 +329,11 @@ inline gapa::RunResult run_ga_cuda(const gapa::GAParams& params, const CudaObjec
     for (int i = 0; i < it; ++i) {
         out.history[i].best = best[i];
         out.history[i].mean = mean[i];
+        out.history[i].wall_seconds = wall[i];
+        out.history[i].compute_seconds = compute[i];
+        out.history[i].exchange_seconds = exch[i];
+        out.history[i].lifecycle_seconds = life[i];
+        out.history[i].messages = messages[i];
     }
     out.best_individual.assign(out.final_population.row(0).begin(), out.final_population.row(0).end());
     out.best_fitness = out.final_fitness.front();

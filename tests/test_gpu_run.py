@@ -105,6 +105,10 @@ def test_sharded_run_equals_single(gp, cuda_device, eda):
         res = gp.run_ga(params, pool, obj, rank=rank, world=2, exchange=exchange2)
         assert np.array_equal(res.final_population, single.final_population)
         assert np.array_equal(res.history_mean, single.history_mean)
+        # GenerationStats columns (modes.hpp:63-71): generation 1 exchanges twice (init + M_POP), the rest once
+        assert [h.messages for h in res.history] == [2] + [1] * 9
+        assert all(h.exchange_seconds > 0 and h.lifecycle_seconds == 0 for h in res.history)
+        assert all(abs(h.compute_seconds + h.exchange_seconds - h.wall_seconds) < 1e-9 for h in res.history)
 
 
 def test_run_rejects_bad_params(gp, cuda_device):
@@ -159,3 +163,23 @@ def test_sharded_driver_recomputes_foreign_rows(gp, oracle, cuda_device, eda):
         assert np.array_equal(res.final_population, want["population"]), rank
         assert np.array_equal(res.history_best, want["best"]) and np.array_equal(res.history_mean, want["mean"])
         assert np.array_equal(res.final_fitness, want["fitness"])
+
+
+def test_generation_stats_and_overhead_report(gp, cuda_device):
+    """GenerationStats / overhead_report (modes.hpp:63-99, modes.cpp:518-530) on one GPU: the three time
+    columns sum to wall, nothing is exchanged, and the table has the reference's layout."""
+    g = gp.barabasi_albert(3000, 3, 2)
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    obj = gp.PairwiseConnectivityObjective(g, pool)
+    res = gp.run_ga(gp.GAParams(pc=0.6, pm=0.2, pop_size=64, budget=150, iterations=6, seed=3), pool, obj)
+    assert len(res.history) == 6
+    assert [h.best for h in res.history] == res.history_best.tolist()
+    assert [h.mean for h in res.history] == res.history_mean.tolist()
+    assert all(h.wall_seconds > 0 and h.messages == 0 and h.exchange_seconds == 0 for h in res.history)
+    assert all(h.compute_seconds == h.wall_seconds for h in res.history)
+    assert sum(h.wall_seconds for h in res.history) <= res.total_wall_seconds * 1.05 + 1e-3
+    assert res.eval_seconds <= sum(h.wall_seconds for h in res.history) * 1.001 + 1e-6
+    lines = gp.overhead_report(res).splitlines()
+    assert lines[0] == "gen  wall_s      compute_s   exchange_s  lifecycle_s messages"
+    assert len(lines) == 7 and lines[1].startswith("1    0.") and lines[1].endswith(" 0") and lines[6].startswith("6    ")
+    assert [len(x) for x in lines[1].split(" ") if x][1:5] == [8, 8, 8, 8]
