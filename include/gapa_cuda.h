@@ -282,6 +282,17 @@ int gapa_cuda_free(int device, void* dev);
 int gapa_cuda_memcpy_h2d(int device, void* dst_dev, const void* src_host, uint64_t bytes);
 int gapa_cuda_memcpy_d2h(int device, void* dst_host, const void* src_dev, uint64_t bytes);
 int gapa_cuda_stream_sync(int device, void* stream);
+/* ---- reporting outputs for ONE individual (the experiment driver's metric columns, bench.cpp:268-311) ----
+ * gapa_cuda_detect_communities: CommunityPartition of detect_communities (community.cpp:28-91) on the
+ * graph perturbed by `genes` (EdgeRemoval or EdgeAddition pool), normalised by first appearance
+ * (community.cpp:17-26), into assignment[n]; *q (optional) = the cda fitness of the same individual.
+ * gapa_cuda_lpa_scores: ra_scores (link_prediction.cpp:71-77) of the T test and P probe pairs on the
+ * perturbed train graph — the inputs of lp_auc_precision's precision half (:98-117); *auc optional. */
+int gapa_cuda_detect_communities(gapa_cuda_ctx* ctx, const int32_t* genes_host, int cols, int32_t* assignment_host,
+                                 double* q_host);
+int gapa_cuda_lpa_scores(gapa_cuda_ctx* ctx, const int32_t* genes_host, int cols, double* test_scores_host,
+                         double* probe_scores_host, double* auc_host);
+
 /* launch counter: kernels launched by this library since load (bench.py's gpu_launches) */
 uint64_t gapa_cuda_launch_count(void);
 /* timing of the last eval on a context: device milliseconds between CUDA events

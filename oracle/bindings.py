@@ -368,6 +368,14 @@ class Ref:
         lib.ref_eda_sample.argtypes = [_i32p, C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, C.c_int,
                                        _i32p]
         lib.ref_partition_rows.argtypes = [C.c_int, C.c_int, _i32p]
+        lib.ref_nmi.restype = C.c_double
+        lib.ref_nmi.argtypes = [_i32p, _i32p, C.c_int]
+        lib.ref_detect_perturbed.argtypes = [V, C.c_int, _i32p, C.c_int, _i32p]
+        lib.ref_lp_metrics.argtypes = [V, _i32p, C.c_int, _f64p, _f64p]
+        self.have_bench = bool(lib.ref_have_bench())
+        if self.have_bench:
+            lib.ref_run_experiment.argtypes = [C.c_char_p, C.c_char_p, C.POINTER(C.c_int), C.c_int, C.c_char_p, C.c_int]
+            lib.ref_csv_without_wall_time.argtypes = [C.c_char_p, C.c_char_p, C.c_int]
         lib.ref_run_ga.argtypes = [V, C.c_int, C.c_double, C.c_double, C.c_int, C.c_int, C.c_int, C.c_int,
                                    C.c_uint64, C.c_int, C.c_int, C.c_int, _f64p, _f64p, _i32p, _f64p,
                                    C.POINTER(C.c_double)]
@@ -553,3 +561,40 @@ class Ref:
                                hb, hm, fp.reshape(-1), ff, C.byref(wall)):
             raise ValueError(self._err())
         return {"best": hb, "mean": hm, "population": fp, "fitness": ff, "wall_seconds": wall.value}
+
+    # -- reporting metrics + experiment driver
+    def nmi(self, a, b):
+        a, b = np.ascontiguousarray(a, dtype=np.int32), np.ascontiguousarray(b, dtype=np.int32)
+        return float(self.lib.ref_nmi(a, b, len(a)))
+
+    def detect_perturbed(self, g, kind, genes):
+        genes = np.ascontiguousarray(genes, dtype=np.int32).reshape(-1)
+        out = np.zeros(max(self.graph_n(g), 1), dtype=np.int32)
+        if self.lib.ref_detect_perturbed(g._ptr, kind, genes if genes.size else np.zeros(1, np.int32), genes.size, out):
+            raise ValueError(self._err())
+        return out[:self.graph_n(g)]
+
+    def lp_metrics(self, split, genes):
+        """(auc, precision, scores[T + P]) of evaluate_ra_predictor on the perturbed train graph."""
+        genes = np.ascontiguousarray(genes, dtype=np.int32).reshape(-1)
+        t, p = self.lib.ref_split_test_count(split._ptr), self.lib.ref_split_probe_count(split._ptr)
+        out, scores = np.zeros(2), np.zeros(max(t + p, 1))
+        if self.lib.ref_lp_metrics(split._ptr, genes if genes.size else np.zeros(1, np.int32), genes.size, out, scores):
+            raise ValueError(self._err())
+        return float(out[0]), float(out[1]), scores[:t + p]
+
+    def run_experiment(self, config_json: str, axis: str = "", values=()):
+        """bench::run_experiment (or bench::sweep when `axis` is given) -> CSV text."""
+        if not self.have_bench:
+            raise RuntimeError("reference library was built without bench.cpp")
+        buf = C.create_string_buffer(1 << 20)
+        vals = (C.c_int * max(len(values), 1))(*values)
+        if self.lib.ref_run_experiment(config_json.encode(), axis.encode(), vals, len(values), buf, len(buf)):
+            raise ValueError(self._err())
+        return buf.value.decode()
+
+    def csv_without_wall_time(self, text: str):
+        buf = C.create_string_buffer(len(text) + 16)
+        if self.lib.ref_csv_without_wall_time(text.encode(), buf, len(buf)):
+            raise ValueError(self._err())
+        return buf.value.decode()

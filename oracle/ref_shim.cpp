@@ -24,6 +24,9 @@
 #include "gapa/community.hpp"
 #include "gapa/error.hpp"
 #include "gapa/fitness.hpp"
+#ifdef REF_HAVE_BENCH
+#include "gapa/bench.hpp"
+#endif
 #include "gapa/ga_ops.hpp"
 #include "gapa/gene_pool.hpp"
 #include "gapa/generators.hpp"
@@ -394,5 +397,67 @@ int ref_run_ga(void* g_or_split, int task, double pc, double pm, int pop_size, i
         if (wall_seconds) *wall_seconds = r.total_wall_seconds;
     });
 }
+
+// ---- reporting metrics and the experiment driver ----------------------
+double ref_nmi(const std::int32_t* a, const std::int32_t* b, int n) {
+    double v = 0.0;
+    guarded([&] {
+        v = nmi(CommunityPartition{std::vector<int>(a, a + n)}, CommunityPartition{std::vector<int>(b, b + n)});
+    });
+    return v;
+}
+// detect_communities on the perturbed graph; kind 0 EdgeRemoval / 1 EdgeAddition pool of build_gene_pool
+int ref_detect_perturbed(void* g, int kind, const std::int32_t* genes, int cols, std::int32_t* assignment) {
+    return guarded([&] {
+        const Graph& graph = static_cast<RefGraph*>(g)->graph;
+        const GenePool pool = build_gene_pool(graph, static_cast<PoolKind>(kind));
+        const BitMatrix attacked = apply_perturbation(graph.adjacency(), pool, std::span<const std::int32_t>(genes, cols));
+        const CommunityPartition p = detect_communities(attacked);
+        std::copy(p.assignment.begin(), p.assignment.end(), assignment);
+    });
+}
+// evaluate_ra_predictor on the perturbed train graph: out = {auc, precision}; scores = T test then P probe
+int ref_lp_metrics(void* s, const std::int32_t* genes, int cols, double* out, double* scores) {
+    return guarded([&] {
+        auto* sp = static_cast<RefSplit*>(s);
+        const GenePool pool = build_gene_pool(sp->split.train, PoolKind::EdgeRemoval);
+        const BitMatrix attacked = apply_perturbation(sp->split.train.adjacency(), pool, std::span<const std::int32_t>(genes, cols));
+        const LpMetrics m = evaluate_ra_predictor(sp->split, attacked);
+        out[0] = m.auc;
+        out[1] = m.precision;
+        if (scores) {
+            const auto t = ra_scores(attacked, sp->split.test_edges), p = ra_scores(attacked, sp->split.probe_nonedges);
+            std::copy(t.begin(), t.end(), scores);
+            std::copy(p.begin(), p.end(), scores + t.size());
+        }
+    });
+}
+#ifdef REF_HAVE_BENCH
+// bench::run_experiment / sweep on a JSON config (bench.cpp:142-366); CSV text into `csv` (NUL-terminated).
+// axis: "" = run_experiment, "pop_size" / "pn" = sweep over `values`.
+int ref_run_experiment(const char* config_json, const char* axis, const int* values, int n_values, char* csv, int capacity) {
+    return guarded([&] {
+        const bench::ExperimentConfig cfg = bench::parse_config(config_json);
+        const std::string ax = axis ? axis : "";
+        const auto rows = ax.empty() ? bench::run_experiment(cfg)
+                                     : bench::sweep(cfg, bench::axis_from_string(ax), std::vector<int>(values, values + n_values));
+        const std::string text = bench::report(rows, bench::ReportFormat::Csv);
+        if (static_cast<int>(text.size()) + 1 > capacity) throw Error("ref_run_experiment: csv buffer too small");
+        std::copy(text.begin(), text.end(), csv);
+        csv[text.size()] = 0;
+    });
+}
+int ref_csv_without_wall_time(const char* csv_in, char* out, int capacity) {
+    return guarded([&] {
+        const std::string text = bench::csv_without_wall_time(csv_in);
+        if (static_cast<int>(text.size()) + 1 > capacity) throw Error("ref_csv_without_wall_time: buffer too small");
+        std::copy(text.begin(), text.end(), out);
+        out[text.size()] = 0;
+    });
+}
+int ref_have_bench() { return 1; }
+#else
+int ref_have_bench() { return 0; }
+#endif
 
 }  // extern "C"

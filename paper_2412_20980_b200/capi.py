@@ -95,6 +95,8 @@ SIGNATURES = {
                                               C.POINTER(C.c_int64)]),
     "gapa_host_lp_split": (C.c_int, [C.c_int32, C.c_int64, VP, C.c_double, C.c_uint64, VP, VP, VP,
                                      C.POINTER(C.c_int32)]),
+    "gapa_cuda_detect_communities": (C.c_int, [VP, VP, C.c_int, VP, C.POINTER(C.c_double)]),
+    "gapa_cuda_lpa_scores": (C.c_int, [VP, VP, C.c_int, VP, VP, C.POINTER(C.c_double)]),
     "gapa_host_budget": (C.c_int, [C.c_int64, C.c_double, C.POINTER(C.c_int32)]),
     "gapa_host_nonedges": (C.c_int, [C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]),
     "gapa_cuda_malloc": (C.c_int, [C.c_int, C.c_uint64, C.POINTER(VP)]),

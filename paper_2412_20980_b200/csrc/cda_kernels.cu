@@ -95,7 +95,8 @@ __device__ __forceinline__ double merge_gain(int edges, int da, int db, double m
 extern __shared__ int32_t cda_smem[];
 
 __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows genes, int rows,
-                                                        int pos_in_smem, double* __restrict__ out) {
+                                                        int pos_in_smem, double* __restrict__ out,
+                                                        int32_t* __restrict__ owner_out) {
     __shared__ Cand warp_cand[kCdaWarps];
     __shared__ Cand chosen;
     __shared__ long long sh_total;
@@ -461,6 +462,16 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         }
         if (sh_abort) { if (tid == 0) out[r] = 0.0; __syncthreads(); continue; }
 
+        // detect_communities' partition (community.cpp:28-91) for the reporting path: the owner of
+        // u is the root of its merge chain == the smallest member of its community.
+        if (owner_out) {
+            for (int u = tid; u < n; u += kCdaThreads) {
+                int root = u;
+                while (merged_into[root] != -1) root = merged_into[root];
+                owner_out[static_cast<size_t>(r) * n + u] = root;
+            }
+        }
+
         // ---- modularity (community.cpp:93-117) ------------------------------------------
         // Live communities in ascending id == first-appearance order.  A term that is
         // exactly zero cannot change the running sum, so only non-zero terms are queued.
@@ -504,7 +515,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
     }
 }
 
-int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream) {
+int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream, int32_t* owner_out_dev) {
     if (!ctx->cda) ctx->cda = new CdaScratch();
     CdaScratch* s = ctx->cda;
     const int n = ctx->n;
@@ -548,7 +559,7 @@ int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
         A.status = s->status.as<int>();
         const size_t smem = pos_in_smem == 2 ? static_cast<size_t>(n) * 7 * sizeof(int32_t) : (pos_in_smem ? static_cast<size_t>(n) * sizeof(int32_t) : 0);
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_cda, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        GAPA_LAUNCH(k_cda, slots, kCdaThreads, smem, stream, A, genes, rows, pos_in_smem, out_dev);
+        GAPA_LAUNCH(k_cda, slots, kCdaThreads, smem, stream, A, genes, rows, pos_in_smem, out_dev, owner_out_dev);
         GAPA_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, s->status.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
         GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
         if (ctx->h_status[0] == GAPA_CUDA_E_RANGE) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");

@@ -486,6 +486,61 @@ int gapa_cuda_eval_batch(gapa_cuda_ctx* c, int task, const int32_t* genes_host, 
     return GAPA_CUDA_OK;
 }
 
+// ---- reporting outputs of one individual (bench.cpp:268-311) -----------------------------------------
+// The partition detect_communities returns on the perturbed graph, normalised by first appearance
+// (community.cpp:17-26), for the NMI columns; and the RA scores behind the AUC, for the precision column.
+int gapa_cuda_detect_communities(gapa_cuda_ctx* c, const int32_t* genes_host, int cols, int32_t* assignment_host, double* q_host) {
+    if (!c) return fail(GAPA_CUDA_E_INVALID, "detect_communities: null context");
+    GAPA_TRY(check_task(c, GAPA_TASK_CDA));
+    if (cols < 0 || !assignment_host || (cols > 0 && !genes_host)) return fail(GAPA_CUDA_E_INVALID, "detect_communities: bad arguments");
+    std::lock_guard<std::mutex> lock(c->mu);
+    GAPA_CUDA_TRY(cudaSetDevice(c->device));
+    const int n = c->n;
+    GAPA_TRY(c->genes_stage.ensure(sizeof(int32_t) * std::max(cols, 1)));
+    GAPA_TRY(c->out_stage.ensure(sizeof(double) + sizeof(int32_t) * static_cast<size_t>(n)));
+    if (cols) GAPA_CUDA_TRY(cudaMemcpyAsync(c->genes_stage.ptr, genes_host, sizeof(int32_t) * cols, cudaMemcpyHostToDevice, c->stream));
+    double* q_dev = c->out_stage.as<double>();
+    int32_t* owner_dev = reinterpret_cast<int32_t*>(q_dev + 1);
+    // an edgeless perturbed graph never reaches the detector's merge loop: everyone stays a singleton
+    std::vector<int32_t> owner(static_cast<size_t>(n));
+    std::iota(owner.begin(), owner.end(), 0);
+    GAPA_CUDA_TRY(cudaMemcpyAsync(owner_dev, owner.data(), sizeof(int32_t) * n, cudaMemcpyHostToDevice, c->stream));
+    GAPA_TRY(cda_eval(c, GeneRows{c->genes_stage.as<int32_t>(), nullptr, cols}, 1, q_dev, c->stream, owner_dev));
+    double q = 0.0;
+    GAPA_CUDA_TRY(cudaMemcpyAsync(owner.data(), owner_dev, sizeof(int32_t) * n, cudaMemcpyDeviceToHost, c->stream));
+    GAPA_CUDA_TRY(cudaMemcpyAsync(&q, q_dev, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    GAPA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    // owners are smallest members, so ascending owner == first appearance (community.cpp:17-26)
+    std::vector<int32_t> label(static_cast<size_t>(n), -1);
+    int32_t next = 0;
+    for (int u = 0; u < n; ++u) {
+        if (label[owner[u]] < 0) label[owner[u]] = next++;
+        assignment_host[u] = label[owner[u]];
+    }
+    if (q_host) *q_host = q;
+    return GAPA_CUDA_OK;
+}
+
+int gapa_cuda_lpa_scores(gapa_cuda_ctx* c, const int32_t* genes_host, int cols, double* test_scores_host,
+                         double* probe_scores_host, double* auc_host) {
+    if (!c) return fail(GAPA_CUDA_E_INVALID, "lpa_scores: null context");
+    GAPA_TRY(check_task(c, GAPA_TASK_LPA));
+    if (cols < 0 || (cols > 0 && !genes_host)) return fail(GAPA_CUDA_E_INVALID, "lpa_scores: bad arguments");
+    std::lock_guard<std::mutex> lock(c->mu);
+    GAPA_CUDA_TRY(cudaSetDevice(c->device));
+    GAPA_TRY(c->genes_stage.ensure(sizeof(int32_t) * std::max(cols, 1)));
+    GAPA_TRY(c->out_stage.ensure(sizeof(double)));
+    if (cols) GAPA_CUDA_TRY(cudaMemcpyAsync(c->genes_stage.ptr, genes_host, sizeof(int32_t) * cols, cudaMemcpyHostToDevice, c->stream));
+    GAPA_TRY(lpa_eval(c, GeneRows{c->genes_stage.as<int32_t>(), nullptr, cols}, 1, c->out_stage.as<double>(), c->stream));
+    const double* scores = lpa_last_scores(c);
+    if (test_scores_host) GAPA_CUDA_TRY(cudaMemcpyAsync(test_scores_host, scores, sizeof(double) * c->T, cudaMemcpyDeviceToHost, c->stream));
+    if (probe_scores_host && c->P > 0)
+        GAPA_CUDA_TRY(cudaMemcpyAsync(probe_scores_host, scores + c->T, sizeof(double) * c->P, cudaMemcpyDeviceToHost, c->stream));
+    if (auc_host) GAPA_CUDA_TRY(cudaMemcpyAsync(auc_host, c->out_stage.ptr, sizeof(double), cudaMemcpyDeviceToHost, c->stream));
+    GAPA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    return GAPA_CUDA_OK;
+}
+
 int gapa_cuda_last_eval_ms(const gapa_cuda_ctx* c, float* ms) {
     if (!c || !ms) return fail(GAPA_CUDA_E_INVALID, "last_eval_ms: null argument");
     *ms = c->last_eval_ms;

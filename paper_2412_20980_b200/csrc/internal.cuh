@@ -187,7 +187,9 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             bool trusted = false, const VariationSpec* vary = nullptr);
 int launch_variation_spec(const VariationSpec& spec, int k, int rows, cudaStream_t stream);  // slot_kernels.cu
 int lpa_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream, bool trusted = false);
-int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream);
+int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream,
+             int32_t* owner_out_dev = nullptr);  // optional [rows x n]: smallest member of each vertex's community
+const double* lpa_last_scores(const gapa_cuda_ctx* ctx);  // scores of the last evaluated chunk: per row T test then P probe
 int sixdst_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cudaStream_t stream, bool trusted = false);
 void pc_free(gapa_cuda_ctx* ctx);
 void sixdst_free(gapa_cuda_ctx* ctx);

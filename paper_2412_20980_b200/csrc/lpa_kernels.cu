@@ -186,6 +186,8 @@ int lpa_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
     return GAPA_CUDA_OK;
 }
 
+const double* lpa_last_scores(const gapa_cuda_ctx* ctx) { return ctx->lpa ? ctx->lpa->scores.as<double>() : nullptr; }
+
 void lpa_free(gapa_cuda_ctx* ctx) {
     if (!ctx->lpa) return;
     for (DevBuf* b : {&ctx->lpa->gone, &ctx->lpa->deg, &ctx->lpa->scores, &ctx->lpa->twice, &ctx->lpa->status}) b->release();

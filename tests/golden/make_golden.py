@@ -260,3 +260,90 @@ run_case("sixdegrees_ba300", r.graph_ba(300, 1, 668), TASK_SIXDST, 0.5, 0.3, 24,
 dump("runs_widen.json", runs)
 print("acceptance #8 Q", runs["acceptance8_cda_add_karate"]["q0"], "->", runs["acceptance8_cda_add_karate"]["best"][-1],
       "(reference test_output.txt:52 says 0.380671 -> 0.26156 @300)")
+
+
+# ------------------------------------------------------------------ loaders, reporting metrics, experiment CSV
+# Datasets are written here (committed under tests/golden/datasets/) and read back by the reference's own
+# load_edge_list_file / run_experiment, so the golden CSV rows and the files always belong together.
+DS = os.path.join(HERE, "datasets")
+os.makedirs(DS, exist_ok=True)
+gen3 = np.random.default_rng(4242)
+
+
+def write_edge_list(name, n, edges, label=lambda i: str(i), noise=False):
+    lines = ["# synthetic dataset for tests/golden/experiments.json (tests/golden/make_golden.py)", ""]
+    order = gen3.permutation(len(edges))
+    for idx, e in enumerate(order):
+        u, v = (int(x) for x in edges[e])
+        if gen3.random() < 0.5:
+            u, v = v, u
+        lines.append(f"{label(u)}\t{label(v)}" if idx % 3 else f"  {label(u)} {label(v)}  ")
+        if noise and idx == 5:
+            lines += ["% comment in the other style", f"{label(u)} {label(u)}", f"{label(v)} {label(u)}", "   "]
+    with open(os.path.join(DS, name), "w") as f:
+        f.write("\n".join(lines) + "\n")
+
+
+kar_edges = np.asarray(fit["karate"]["edges"], dtype=np.int32)
+write_edge_list("karate.txt", 34, kar_edges, label=lambda i: str(i + 1))
+sbm_g = r.graph_sbm(4, 15, 0.35, 0.03, 9)
+sbm_edges = r.graph_edges(sbm_g)
+write_edge_list("sbm60.txt", 60, sbm_edges, label=lambda i: f"n{i:02d}", noise=True)
+with open(os.path.join(DS, "sbm60_truth.txt"), "w") as f:
+    f.write("# label community\n" + "".join(f"n{i:02d} block{i // 15}\n" for i in gen3.permutation(60)))
+tree_edges = r.graph_edges(r.graph_ba(120, 1, 31))
+write_edge_list("tree120.txt", 120, tree_edges)
+er_edges = r.graph_edges(r.graph_er(90, 0.09, 17))
+write_edge_list("er90.txt", 90, er_edges, label=lambda i: f"v{i}")
+
+rel = lambda name: "tests/golden/datasets/" + name  # configs use repo-relative paths: run from the repo root
+os.chdir(os.path.dirname(os.path.dirname(HERE)))
+experiments = []
+for cfg, axis, values in [
+    ({"algorithm": "qattack", "dataset": rel("karate.txt"), "iterations": 40, "pop_size": 20, "seed": 667, "repetitions": 2}, "", ()),
+    ({"algorithm": "cda-eda", "dataset": rel("karate.txt"), "iterations": 12, "pop_size": 16, "seed": 5, "eda_interval": 3}, "", ()),
+    ({"task": "cda-modularity", "pool": "edge-removal", "dataset": rel("sbm60.txt"), "ground_truth": rel("sbm60_truth.txt"),
+      "pc": 0.8, "pm": 0.1, "iterations": 10, "pop_size": 12, "seed": 3, "perturbation_rate": 0.15}, "", ()),
+    ({"algorithm": "cutoff-pc", "dataset": rel("tree120.txt"), "iterations": 30, "pop_size": 16, "seed": 11, "mode": "m", "pn": 2}, "", ()),
+    ({"algorithm": "sixdst", "dataset": rel("tree120.txt"), "iterations": 25, "pop_size": 14, "seed": 12, "fast_closure": True,
+      "perturbation_rate": 0.05}, "", ()),
+    ({"algorithm": "sixdst", "dataset": rel("er90.txt"), "iterations": 20, "pop_size": 10, "seed": 13}, "", ()),
+    ({"algorithm": "lpa-ga", "dataset": rel("sbm60.txt"), "iterations": 20, "pop_size": 12, "seed": 21, "repetitions": 2,
+      "test_fraction": 0.2}, "", ()),
+    ({"algorithm": "lpa-eda", "dataset": rel("er90.txt"), "iterations": 8, "pop_size": 10, "seed": 22}, "", ()),
+    ({"task": "cnd-pc", "dataset": rel("er90.txt"), "pc": 0.6, "pm": 0.2, "iterations": 10, "seed": 30}, "pop_size", (8, 12)),
+]:
+    csv = r.run_experiment(json.dumps(cfg), axis, list(values))
+    experiments.append({"config": cfg, "axis": axis, "values": list(values), "csv": csv,
+                        "csv_without_wall_time": r.csv_without_wall_time(csv)})
+    print(csv.splitlines()[1][:150])
+
+metrics = {"nmi": [], "lp": [], "detect": []}
+for trial in range(12):
+    n = int(gen3.integers(1, 60))
+    a, b = gen3.integers(0, int(gen3.integers(1, 8)), n), gen3.integers(0, int(gen3.integers(1, 8)), n)
+    if trial == 0:
+        b = a.copy()
+    if trial == 1:
+        a, b = np.zeros(n, int), np.zeros(n, int)
+    metrics["nmi"].append({"a": ints(a), "b": ints(b), "nmi": r.nmi(a, b)})
+for kind, g, edges in [(0, sbm_g, sbm_edges), (1, sbm_g, sbm_edges), (1, kar, kar_edges)]:
+    psize = len(r.pool_genes(g, kind)[0])
+    for k in (0, 7, 25):
+        genes = gen3.integers(0, psize, k).astype(np.int32)
+        metrics["detect"].append({"n": r.graph_n(g), "edges": ints(edges), "kind": kind, "genes": ints(genes),
+                                  "assignment": ints(r.detect_perturbed(g, kind, genes))})
+for gname, g, frac, sseed in [("sbm", sbm_g, 0.2, 21), ("er", r.graph_er(90, 0.09, 17), 0.1, 22)]:
+    sp = r.split_build(g, frac, sseed)
+    mt = r.graph_m(r.split_train(sp))
+    for k in (0, 9):
+        genes = gen3.integers(0, mt, k).astype(np.int32)
+        auc, prec, scores = r.lp_metrics(sp, genes)
+        metrics["lp"].append({"n": r.graph_n(g), "edges": ints(r.graph_edges(g)), "fraction": frac, "split_seed": sseed,
+                              "genes": ints(genes), "auc": auc, "precision": prec, "scores": floats(scores)})
+datasets = {}
+for name in ("karate.txt", "sbm60.txt", "tree120.txt", "er90.txt"):
+    g = r.graph_load(rel(name))
+    e = r.graph_edges(g)
+    datasets[name] = {"n": r.graph_n(g), "m": r.graph_m(g), "sha": sha(e), "first": ints(e[:5])}
+dump("experiments.json", {"experiments": experiments, "metrics": metrics, "datasets": datasets})
