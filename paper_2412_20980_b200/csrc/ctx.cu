@@ -112,7 +112,11 @@ static int finish_create(gapa_cuda_ctx* c, int device, gapa_cuda_ctx** out) {
         GAPA_TRY(upload_i32(eu, &c->d_edge_u));
         GAPA_TRY(upload_i32(ev, &c->d_edge_v));
         GAPA_TRY(upload_i32(by_degree, &c->d_by_degree));
-        GAPA_CUDA_TRY(cudaStreamCreateWithFlags(&c->stream, cudaStreamNonBlocking));
+        {  // the work stream outranks the evaluators' side streams (background clears, pc_kernels.cu)
+            int least = 0, greatest = 0;
+            GAPA_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            GAPA_CUDA_TRY(cudaStreamCreateWithPriority(&c->stream, cudaStreamNonBlocking, greatest));
+        }
         GAPA_CUDA_TRY(cudaEventCreate(&c->ev_start));
         GAPA_CUDA_TRY(cudaEventCreate(&c->ev_stop));
         GAPA_CUDA_TRY(cudaMallocHost(&c->h_status, 64 * sizeof(int32_t)));

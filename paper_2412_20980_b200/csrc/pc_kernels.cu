@@ -76,6 +76,10 @@ struct PcScratch {
     unsigned long long ord_pool_version = ~0ull;
     std::vector<int32_t> perm;  // original vertex -> internal vertex when relabelled
     bool configured = false;
+    // side stream that clears the `reached` records while the mask build runs (the two do not touch the same memory)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_pass_begin = nullptr, ev_cleared = nullptr;
+    int overlap_clear = 1;
 };
 
 // ---------------------------------------------------------------------------------
@@ -840,6 +844,14 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
+        s->overlap_clear = env_int("GAPA_PC_OVERLAP_CLEAR", 1, 0, 1);
+        {  // lowest priority: the clear yields to every kernel of the work stream
+            int least = 0, greatest = 0;
+            GAPA_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+            GAPA_CUDA_TRY(cudaStreamCreateWithPriority(&s->aux, cudaStreamNonBlocking, least));
+        }
+        GAPA_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_pass_begin, cudaEventDisableTiming));
+        GAPA_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_cleared, cudaEventDisableTiming));
         s->configured = true;
     }
     const int n = ctx->n;
@@ -908,6 +920,10 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         GAPA_CUDA_TRY(cudaMemsetAsync(s->removed_count.ptr, 0, sizeof(int) * pgroups * kBits, stream));
 
         if (n > 0) {
+            // The 0.5 GB clear of the `reached` records depends on nothing this pass computes, only on the
+            // previous user of the buffer being done: it runs on a side stream underneath the mask build,
+            // which is bound by integer issue, not by HBM.
+            if (s->overlap_clear) GAPA_CUDA_TRY(cudaEventRecord(s->ev_pass_begin, stream));
             // ---- masks ------------------------------------------------------------------
             if (vary && chunks == 1 && cols > 0) {
                 VariationSpec pass = *vary;
@@ -925,9 +941,15 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
                         ctx->pool_size, n, chunk_bits, words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>(),
                         counters);
             }
+            if (s->overlap_clear) {  // issued AFTER the mask kernel so that its CTAs only fill what that kernel leaves free
+                GAPA_CUDA_TRY(cudaStreamWaitEvent(s->aux, s->ev_pass_begin, 0));
+                GAPA_CUDA_TRY(cudaMemsetAsync(reached, 0, sizeof(word_t) * words, s->aux));
+                GAPA_CUDA_TRY(cudaEventRecord(s->ev_cleared, s->aux));
+            }
             GAPA_LAUNCH(k_pc_transpose, dim3((words_per_row + kTransThreads - 1) / kTransThreads, pgroups), kTransThreads,
                         sizeof(word_t) * kBits * (kTransThreads + 1), stream, s->removed.as<word_t>(), words_per_row, n, crows, alive);
-            GAPA_CUDA_TRY(cudaMemsetAsync(reached, 0, sizeof(word_t) * words, stream));
+            if (s->overlap_clear) GAPA_CUDA_TRY(cudaStreamWaitEvent(stream, s->ev_cleared, 0));
+            else GAPA_CUDA_TRY(cudaMemsetAsync(reached, 0, sizeof(word_t) * words, stream));
             GAPA_LAUNCH(k_pc_source, (crows * 32 + kThreads - 1) / kThreads, kThreads, 0, stream, g_by_degree, n,
                         crows, alive, reached);
 
@@ -1012,6 +1034,9 @@ void pc_free(gapa_cuda_ctx* ctx) {
                       &s->left_v, &s->left_g, &s->left_w, &s->left_base, &s->parent, &s->comp_size, &s->pc_extra,
                       &s->mcn_extra})
         b->release();
+    if (s->aux) cudaStreamDestroy(s->aux);
+    if (s->ev_pass_begin) cudaEventDestroy(s->ev_pass_begin);
+    if (s->ev_cleared) cudaEventDestroy(s->ev_cleared);
     delete s;
     ctx->pc = nullptr;
 }
