@@ -34,7 +34,9 @@ namespace gapa_b200 {
 
 static constexpr int kCdaThreads = 1024;
 static constexpr int kCdaWarps = kCdaThreads / 32;
-static constexpr int kCdaShortList = 24;   // neighbour lists up to this length are patched by one thread
+static constexpr int kCdaGroup = 8;        // lanes that patch one neighbour's list together
+static constexpr int kCdaShortList = 64;   // neighbour lists up to this length are patched by one lane group ...
+static constexpr int kCdaThreadList = 24;  // ... or by one thread when the merged community has many neighbours
 static constexpr int kCdaLongQueue = 1024;  // longer ones are queued for a warp each
 
 struct CdaScratch {
@@ -329,75 +331,156 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             const int la2 = sh_len, da = cdeg[a];
 
             // Patch the mirror entry of every neighbour c of the merged community and refresh c's
-            // cached best.  Short lists (the common case: the merged community is adjacent to many
-            // small ones) take one THREAD each, so ~1000 neighbours are patched concurrently; long
-            // lists are queued and taken by one WARP each.
+            // cached best.  This is the critical path of a merge step (everything else waits at the next
+            // barrier), so a neighbour's list is scanned by a GROUP of kCdaGroup lanes — 128 neighbours at a
+            // time, each list read in one or two round trips to L2 instead of one per 8 entries; lists
+            // longer than kCdaShortList are queued and taken by one WARP each.
             Cand best_a{0.0, a, -1};
             if (tid == 0) sh_long = 0;
             __syncthreads();
-            for (int i = tid; i < la2; i += kCdaThreads) {
-                const int c = e_id[ha + i], e = e_cnt[ha + i];
-                const double gn = merge_gain(e, da, cdeg[c], m, den);
-                e_gain[ha + i] = gn;
-                if (c > a && gn > 0.0) {
-                    const Cand x{gn, a, c};
-                    if (cand_better(x, best_a)) best_a = x;
-                }
-                const int hc = head[c];
-                int lc = len[c];
-                if (lc > kCdaShortList) {
-                    const int q = atomicAdd(&sh_long, 1);
-                    if (q < kCdaLongQueue) { long_queue[q] = i; continue; }
-                }
-                int pa = -1, pbb = -1;
-                for (int t0 = 0; t0 < lc; t0 += 8) {  // 8 independent loads in flight per step
-                    int ids[8];
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) ids[u] = t0 + u < lc ? e_id[hc + t0 + u] : -1;
-#pragma unroll
-                    for (int u = 0; u < 8; ++u) {
-                        if (ids[u] == a) pa = t0 + u;
-                        if (ids[u] == b) pbb = t0 + u;
-                    }
-                }
-                if (pa >= 0) {
-                    if (pbb >= 0) {
-                        const int last = lc - 1;
-                        if (pbb != last) {
-                            e_id[hc + pbb] = e_id[hc + last];
-                            e_cnt[hc + pbb] = e_cnt[hc + last];
-                            e_gain[hc + pbb] = e_gain[hc + last];
-                            if (pa == last) pa = pbb;
+            if (la2 <= kCdaThreads / kCdaGroup) {  // few neighbours: latency matters, spread each list over a lane group
+                const int gl = lane % kCdaGroup;
+                const unsigned gmask = ((1u << kCdaGroup) - 1u) << (lane - gl);
+                for (int i0 = 0; i0 < la2; i0 += kCdaThreads / kCdaGroup) {
+                    const int i = i0 + tid / kCdaGroup;
+                    if (i >= la2) continue;  // uniform within a group
+                    const int c = e_id[ha + i], e = e_cnt[ha + i];
+                    const double gn = merge_gain(e, da, cdeg[c], m, den);
+                    const int hc = head[c];
+                    int lc = len[c];
+                    int queued = 0;
+                    if (gl == 0) {
+                        e_gain[ha + i] = gn;
+                        if (c > a && gn > 0.0) {
+                            const Cand x{gn, a, c};
+                            if (cand_better(x, best_a)) best_a = x;
                         }
-                        lc = last;
-                        len[c] = lc;
+                        if (lc > kCdaShortList) {
+                            const int q = atomicAdd(&sh_long, 1);
+                            if (q < kCdaLongQueue) { long_queue[q] = i; queued = 1; }
+                        }
                     }
-                    e_cnt[hc + pa] = e;
-                    e_gain[hc + pa] = gn;
-                } else {
-                    e_id[hc + pbb] = a;
-                    e_cnt[hc + pbb] = e;
-                    e_gain[hc + pbb] = gn;
-                }
-                Cand best_c{0.0, c, -1};
-                for (int t0 = 0; t0 < lc; t0 += 4) {
-                    int ids[4];
-                    double gs[4];
-#pragma unroll
-                    for (int u = 0; u < 4; ++u) {
-                        const bool in = t0 + u < lc;
-                        ids[u] = in ? e_id[hc + t0 + u] : -1;
-                        gs[u] = in ? e_gain[hc + t0 + u] : 0.0;
+                    if (__shfl_sync(gmask, queued, lane - gl)) continue;
+                    int pa = -1, pbb = -1;
+                    for (int t = gl; t < lc; t += kCdaGroup) {
+                        const int id = e_id[hc + t];
+                        if (id == a) pa = t;
+                        if (id == b) pbb = t;
                     }
-#pragma unroll
-                    for (int u = 0; u < 4; ++u)
-                        if (ids[u] > c && gs[u] > 0.0) {
-                            const Cand x{gs[u], c, ids[u]};
+    #pragma unroll
+                    for (int off = kCdaGroup / 2; off; off >>= 1) {
+                        pa = max(pa, __shfl_xor_sync(gmask, pa, off));
+                        pbb = max(pbb, __shfl_xor_sync(gmask, pbb, off));
+                    }
+                    if (gl == 0) {
+                        if (pa >= 0) {
+                            if (pbb >= 0) {
+                                const int last = lc - 1;
+                                if (pbb != last) {
+                                    e_id[hc + pbb] = e_id[hc + last];
+                                    e_cnt[hc + pbb] = e_cnt[hc + last];
+                                    e_gain[hc + pbb] = e_gain[hc + last];
+                                    if (pa == last) pa = pbb;
+                                }
+                                len[c] = last;
+                            }
+                            e_cnt[hc + pa] = e;
+                            e_gain[hc + pa] = gn;
+                        } else {
+                            e_id[hc + pbb] = a;
+                            e_cnt[hc + pbb] = e;
+                            e_gain[hc + pbb] = gn;
+                        }
+                    }
+                    if (pa >= 0 && pbb >= 0) --lc;  // the same on every lane of the group
+                    __syncwarp(gmask);               // the leader's patch is visible to the group
+                    Cand best_c{0.0, c, -1};
+                    for (int t = gl; t < lc; t += kCdaGroup) {
+                        const int id = e_id[hc + t];
+                        const double gg = e_gain[hc + t];
+                        if (id > c && gg > 0.0) {
+                            const Cand x{gg, c, id};
                             if (cand_better(x, best_c)) best_c = x;
                         }
+                    }
+    #pragma unroll
+                    for (int off = kCdaGroup / 2; off; off >>= 1) {
+                        Cand o;
+                        o.gain = __shfl_xor_sync(gmask, best_c.gain, off);
+                        o.a = c;
+                        o.b = __shfl_xor_sync(gmask, best_c.b, off);
+                        if (cand_better(o, best_c)) best_c = o;
+                    }
+                    if (gl == 0) {
+                        best_gain[c] = best_c.gain;
+                        best_id[c] = best_c.b;
+                    }
                 }
-                best_gain[c] = best_c.gain;
-                best_id[c] = best_c.b;
+            } else {  // many neighbours: throughput matters, one thread per neighbour
+                for (int i = tid; i < la2; i += kCdaThreads) {
+                    const int c = e_id[ha + i], e = e_cnt[ha + i];
+                    const double gn = merge_gain(e, da, cdeg[c], m, den);
+                    e_gain[ha + i] = gn;
+                    if (c > a && gn > 0.0) {
+                        const Cand x{gn, a, c};
+                        if (cand_better(x, best_a)) best_a = x;
+                    }
+                    const int hc = head[c];
+                    int lc = len[c];
+                    if (lc > kCdaThreadList) {
+                        const int q = atomicAdd(&sh_long, 1);
+                        if (q < kCdaLongQueue) { long_queue[q] = i; continue; }
+                    }
+                    int pa = -1, pbb = -1;
+                    for (int t0 = 0; t0 < lc; t0 += 8) {  // 8 independent loads in flight per step
+                        int ids[8];
+    #pragma unroll
+                        for (int u = 0; u < 8; ++u) ids[u] = t0 + u < lc ? e_id[hc + t0 + u] : -1;
+    #pragma unroll
+                        for (int u = 0; u < 8; ++u) {
+                            if (ids[u] == a) pa = t0 + u;
+                            if (ids[u] == b) pbb = t0 + u;
+                        }
+                    }
+                    if (pa >= 0) {
+                        if (pbb >= 0) {
+                            const int last = lc - 1;
+                            if (pbb != last) {
+                                e_id[hc + pbb] = e_id[hc + last];
+                                e_cnt[hc + pbb] = e_cnt[hc + last];
+                                e_gain[hc + pbb] = e_gain[hc + last];
+                                if (pa == last) pa = pbb;
+                            }
+                            lc = last;
+                            len[c] = lc;
+                        }
+                        e_cnt[hc + pa] = e;
+                        e_gain[hc + pa] = gn;
+                    } else {
+                        e_id[hc + pbb] = a;
+                        e_cnt[hc + pbb] = e;
+                        e_gain[hc + pbb] = gn;
+                    }
+                    Cand best_c{0.0, c, -1};
+                    for (int t0 = 0; t0 < lc; t0 += 4) {
+                        int ids[4];
+                        double gs[4];
+    #pragma unroll
+                        for (int u = 0; u < 4; ++u) {
+                            const bool in = t0 + u < lc;
+                            ids[u] = in ? e_id[hc + t0 + u] : -1;
+                            gs[u] = in ? e_gain[hc + t0 + u] : 0.0;
+                        }
+    #pragma unroll
+                        for (int u = 0; u < 4; ++u)
+                            if (ids[u] > c && gs[u] > 0.0) {
+                                const Cand x{gs[u], c, ids[u]};
+                                if (cand_better(x, best_c)) best_c = x;
+                            }
+                    }
+                    best_gain[c] = best_c.gain;
+                    best_id[c] = best_c.b;
+                }
             }
             __syncthreads();
             const int n_long = min(sh_long, kCdaLongQueue);
