@@ -72,6 +72,7 @@ struct PcScratch {
     int prefix = 32768, interleave = 8, mask_chunks = 1, small_path = 1, relabel = -1;
     // hub-first internal vertex order for the bit-sliced path (see ensure_order)
     DevBuf ord_row_ptr, ord_col_idx, ord_gene_map;
+    DevBuf nbr4;  // int4 per vertex: the first four entries of its (ascending) row, -1 padded — see gather_first4
     bool ord_ready = false, ord_relabeled = false;
     unsigned long long ord_pool_version = ~0ull;
     std::vector<int32_t> perm;  // original vertex -> internal vertex when relabelled
@@ -292,16 +293,16 @@ __global__ void __launch_bounds__(kThreads) k_pc_source(const int32_t* __restric
 struct __align__(32) Rec {
     word_t w[kPack];
 };
-__device__ __forceinline__ Rec load_rec(const Rec* p) {  // two 16-byte loads of one sector, L2-coherent
-    const ulonglong2 lo = __ldcg(reinterpret_cast<const ulonglong2*>(p));
-    const ulonglong2 hi = __ldcg(reinterpret_cast<const ulonglong2*>(p) + 1);
+// One 256-bit access per record (LDG.E.256 / STG.E.256, new on sm_100): a warp gathering 32 random records
+// sends 32 requests to the crossbar instead of 64 — the L1 -> XBAR request path was the busiest unit of the
+// sweep (65 %) with two 16-byte loads per sector.  L2-coherent (other blocks set bits concurrently).
+__device__ __forceinline__ Rec load_rec(const Rec* p) {
     Rec r;
-    r.w[0] = lo.x; r.w[1] = lo.y; r.w[2] = hi.x; r.w[3] = hi.y;
+    asm volatile("ld.global.cg.v4.u64 {%0,%1,%2,%3}, [%4];" : "=l"(r.w[0]), "=l"(r.w[1]), "=l"(r.w[2]), "=l"(r.w[3]) : "l"(p) : "memory");
     return r;
 }
 __device__ __forceinline__ void store_rec(Rec* p, const Rec& r) {
-    reinterpret_cast<ulonglong2*>(p)[0] = make_ulonglong2(r.w[0], r.w[1]);
-    reinterpret_cast<ulonglong2*>(p)[1] = make_ulonglong2(r.w[2], r.w[3]);
+    asm volatile("st.global.v4.u64 [%0], {%1,%2,%3,%4};" ::"l"(p), "l"(r.w[0]), "l"(r.w[1]), "l"(r.w[2]), "l"(r.w[3]) : "memory");
 }
 __device__ __forceinline__ bool rec_any(const Rec& r) { return (r.w[0] | r.w[1] | r.w[2] | r.w[3]) != 0ull; }
 __device__ __forceinline__ bool rec_covers(const Rec& got, const Rec& todo) {
@@ -350,6 +351,55 @@ __device__ __forceinline__ Rec gather_reached(const int32_t* __restrict__ row_pt
     if (e < end) {
         const int u = col_idx[e];
         if (u < limit) rec_or(got, load_rec(&reached_sg[u]));
+    }
+#pragma unroll
+    for (int i = 0; i < kPack; ++i) got.w[i] &= todo.w[i];
+    return got;
+}
+
+// The sweeps' gather with the index chain taken off the critical path.  `first` holds the first four
+// neighbours of v (one coalesced 16-byte load issued together with v's own records), so the common
+// case — covered by the two or four oldest neighbours — is  {own records, first} -> {neighbour
+// records}: two dependent memory latencies instead of row_ptr -> col_idx -> records -> col_idx -> ...
+// Only vertices that need more than four neighbours touch row_ptr / col_idx at all.
+__device__ __forceinline__ Rec gather_first4(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
+                                             const Rec* reached_sg, int v, const int4 first, const Rec& todo) {
+    Rec got{};
+    bool done = false;
+    if (first.x >= 0) {
+        const Rec r0 = load_rec(&reached_sg[first.x]);
+        if (first.y >= 0) {
+            const Rec r1 = load_rec(&reached_sg[first.y]);
+            rec_or(got, r1);
+        }
+        rec_or(got, r0);
+        done = rec_covers(got, todo) || first.z < 0;
+        if (!done) {
+            const Rec r2 = load_rec(&reached_sg[first.z]);
+            if (first.w >= 0) {
+                const Rec r3 = load_rec(&reached_sg[first.w]);
+                rec_or(got, r3);
+            }
+            rec_or(got, r2);
+            done = rec_covers(got, todo) || first.w < 0;
+        }
+    } else {
+        done = true;  // isolated vertex
+    }
+    if (!done) {
+        const int end = row_ptr[v + 1];
+        int e = row_ptr[v] + 4;
+        for (; e + 1 < end; e += 2) {
+            const int u0 = col_idx[e], u1 = col_idx[e + 1];
+            const Rec r0 = load_rec(&reached_sg[u0]), r1 = load_rec(&reached_sg[u1]);
+            rec_or(got, r0);
+            rec_or(got, r1);
+            if (rec_covers(got, todo)) {
+                e = end;
+                break;
+            }
+        }
+        if (e < end) rec_or(got, load_rec(&reached_sg[col_idx[e]]));
     }
 #pragma unroll
     for (int i = 0; i < kPack; ++i) got.w[i] &= todo.w[i];
@@ -414,6 +464,7 @@ __global__ void __cluster_dims__(kPrefixCluster, 1, 1) __launch_bounds__(kPrefix
 struct SweepArgs {
     const int32_t* row_ptr;
     const int32_t* col_idx;
+    const int4* nbr4;
     int n, sgroups, interleave;
     const word_t* alive;
     Rec* reached;
@@ -449,13 +500,14 @@ __device__ __forceinline__ void sweep_chunk(const SweepArgs& A, int sg, int chun
     int any = 0, any_left = 0;
     if (v < n) {
         const size_t base = static_cast<size_t>(sg) * n;
+        const int4 first = __ldg(&A.nbr4[v]);  // in flight together with v's own records
         Rec mine = load_rec(&reached[base + v]);
         const Rec al = load_alive(alive, sg, n, v);
         Rec todo;
 #pragma unroll
         for (int i = 0; i < kPack; ++i) todo.w[i] = al.w[i] & ~mine.w[i];
         if (rec_any(todo)) {
-            const Rec got = gather_reached(row_ptr, col_idx, reached + base, v, n, todo);
+            const Rec got = gather_first4(row_ptr, col_idx, reached + base, v, first, todo);
             if (rec_any(got)) {
                 rec_or(mine, got);
                 store_rec(&reached[base + v], mine);
@@ -815,6 +867,24 @@ static int ensure_order(gapa_cuda_ctx* ctx, PcScratch* s) {
             if (!col_idx.empty())
                 GAPA_CUDA_TRY(cudaMemcpy(s->ord_col_idx.ptr, col_idx.data(), sizeof(int32_t) * col_idx.size(), cudaMemcpyHostToDevice));
         }
+        {  // first four neighbours of every vertex in the order the sweeps use
+            const std::vector<int32_t>* use_rp = &rp;
+            const std::vector<int32_t>* use_ci = &ci;
+            std::vector<int32_t> drp, dci;
+            if (s->ord_relabeled) {
+                drp.resize(static_cast<size_t>(n) + 1);
+                dci.resize(ci.size());
+                GAPA_CUDA_TRY(cudaMemcpy(drp.data(), s->ord_row_ptr.ptr, sizeof(int32_t) * drp.size(), cudaMemcpyDeviceToHost));
+                if (!dci.empty()) GAPA_CUDA_TRY(cudaMemcpy(dci.data(), s->ord_col_idx.ptr, sizeof(int32_t) * dci.size(), cudaMemcpyDeviceToHost));
+                use_rp = &drp;
+                use_ci = &dci;
+            }
+            std::vector<int32_t> first(static_cast<size_t>(4) * std::max(n, 1), -1);
+            for (int v = 0; v < n; ++v)
+                for (int t = 0; t < 4 && (*use_rp)[v] + t < (*use_rp)[v + 1]; ++t) first[4 * static_cast<size_t>(v) + t] = (*use_ci)[(*use_rp)[v] + t];
+            GAPA_TRY(s->nbr4.ensure(sizeof(int32_t) * first.size()));
+            GAPA_CUDA_TRY(cudaMemcpy(s->nbr4.ptr, first.data(), sizeof(int32_t) * first.size(), cudaMemcpyHostToDevice));
+        }
         s->ord_ready = true;
     }
     if (s->ord_relabeled) {  // gene -> internal vertex
@@ -967,7 +1037,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             const dim3 grid(((n + kThreads - 1) / kThreads) * il, (sgroups + il - 1) / il);
             GAPA_TRY(s->block_done.ensure(sizeof(int2) * static_cast<size_t>(sgroups) * ((n + kThreads - 1) / kThreads)));
             SweepArgs A;
-            A.row_ptr = g_row_ptr; A.col_idx = g_col_idx; A.n = n; A.sgroups = sgroups; A.interleave = il;
+            A.row_ptr = g_row_ptr; A.col_idx = g_col_idx; A.nbr4 = s->nbr4.as<int4>(); A.n = n; A.sgroups = sgroups; A.interleave = il;
             A.alive = alive_rec; A.reached = reached_rec; A.unreached = s->unreached.as<int>();
             A.entry_of = s->entry_of.as<int32_t>(); A.left_v = s->left_v.as<int32_t>(); A.left_g = s->left_g.as<int32_t>();
             A.left_w = s->left_w.as<word_t>(); A.left_base = s->left_base.as<int32_t>(); A.parent = s->parent.as<int32_t>();
@@ -1030,7 +1100,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
 void pc_free(gapa_cuda_ctx* ctx) {
     if (!ctx->pc) return;
     PcScratch* s = ctx->pc;
-    for (DevBuf* b : {&s->removed, &s->removed_count, &s->alive, &s->reached, &s->entry_of, &s->unreached, &s->counters, &s->pass_flags, &s->block_done,
+    for (DevBuf* b : {&s->nbr4, &s->removed, &s->removed_count, &s->alive, &s->reached, &s->entry_of, &s->unreached, &s->counters, &s->pass_flags, &s->block_done,
                       &s->left_v, &s->left_g, &s->left_w, &s->left_base, &s->parent, &s->comp_size, &s->pc_extra,
                       &s->mcn_extra})
         b->release();
