@@ -89,6 +89,13 @@ struct PcScratch {
 // Duplicate genes are idempotent.  Bit c of 64-bit word w = vertex 64 w + c removed.
 extern __shared__ __align__(16) unsigned pc_smem_bits[];
 
+// eight consecutive int32 with one 256-bit streaming load (sm_100: LDG.E.EF.256); p must be 32-byte aligned
+__device__ __forceinline__ void load8_stream(const int32_t* p, int (&v)[8]) {
+    asm volatile("ld.global.cs.v8.s32 {%0,%1,%2,%3,%4,%5,%6,%7}, [%8];"
+                 : "=r"(v[0]), "=r"(v[1]), "=r"(v[2]), "=r"(v[3]), "=r"(v[4]), "=r"(v[5]), "=r"(v[6]), "=r"(v[7])
+                 : "l"(p));
+}
+
 __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(GeneRows genes,
                                                              const int32_t* __restrict__ pool_map, int pool_size, int n,
                                                              int chunk_bits, int words_per_row, word_t* __restrict__ removed,
@@ -110,7 +117,28 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(GeneRows genes,
         if (node >= v0 && node < v1) atomicOr(&pc_smem_bits[(node - v0) >> 5], 1u << ((node - v0) & 31));
     };
     int j0 = 0;
-    if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
+    if ((reinterpret_cast<uintptr_t>(g) & 31) == 0) {
+        // 32-byte streaming loads (LDG.E.256), two per thread — 64 KB per SM — in flight before the first
+        // shared-memory atomic: with one CTA per SM the kernel lives on bytes in flight per thread
+        const int octs = cols >> 3;
+        int o = threadIdx.x;
+        for (; o + kMaskThreads < octs; o += 2 * kMaskThreads) {
+            int a[8], b[8];
+            load8_stream(g + 8 * static_cast<size_t>(o), a);
+            load8_stream(g + 8 * static_cast<size_t>(o + kMaskThreads), b);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) mark(a[t]);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) mark(b[t]);
+        }
+        if (o < octs) {
+            int a[8];
+            load8_stream(g + 8 * static_cast<size_t>(o), a);
+#pragma unroll
+            for (int t = 0; t < 8; ++t) mark(a[t]);
+        }
+        j0 = octs << 3;
+    } else if ((reinterpret_cast<uintptr_t>(g) & 15) == 0) {
         // 16-byte loads, two per thread in flight before the first shared-memory atomic
         const int4* g4 = reinterpret_cast<const int4*>(g);
         const int quads = cols >> 2;
