@@ -24,6 +24,7 @@ static constexpr int kLpaThreads = 256;
 
 struct LpaScratch {
     DevBuf gone, deg, scores, twice, status;
+    int sorted_auc = -1;  // GAPA_LPA_SORTED_AUC=0 forces the T x P grid kernel (tests run both)
 };
 
 __global__ void __launch_bounds__(kLpaThreads) k_lpa_init(const int32_t* __restrict__ row_ptr, int n, int rows,
@@ -134,6 +135,68 @@ __global__ void __launch_bounds__(kLpaThreads) k_lpa_auc(const double* __restric
     if (threadIdx.x == 0 && block_sum) atomicAdd(&twice[r], block_sum);
 }
 
+// The same 2 * wins without the T x P grid: one CTA per individual sorts the P probe scores in shared
+// memory (bitonic network on order-preserving 64-bit integer keys) and every test score finds, by two
+// binary searches, how many probe scores are below it and how many equal it:
+//     2 * wins = sum over t of  2 * #(p < t) + #(p == t)
+// — O((T + P) log P) integer compares instead of T * P FP64 compares (25 M per individual at C3).
+// Same integers, so the AUC is the same double.
+static constexpr int kLpaSortThreads = 1024;
+extern __shared__ unsigned long long lpa_keys[];
+
+__device__ __forceinline__ unsigned long long score_key(double x) {
+    if (x == 0.0) x = 0.0;  // -0.0 == +0.0 must compare equal as keys too
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    return (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // total order of finite doubles
+}
+
+__global__ void __launch_bounds__(kLpaSortThreads) k_lpa_auc_sorted(const double* __restrict__ scores, int T, int P, int P2,
+                                                                    unsigned long long* twice) {
+    __shared__ unsigned long long warp_sum[kLpaSortThreads / 32];
+    const int r = blockIdx.x, tid = threadIdx.x;
+    const double* row = scores + static_cast<size_t>(r) * (T + P);
+    for (int i = tid; i < P2; i += kLpaSortThreads) lpa_keys[i] = i < P ? score_key(row[T + i]) : ~0ull;  // pads sort to the end
+    __syncthreads();
+    for (int k = 2; k <= P2; k <<= 1)
+        for (int j = k >> 1; j > 0; j >>= 1) {
+            for (int i = tid; i < P2; i += kLpaSortThreads) {
+                const int partner = i ^ j;
+                if (partner > i) {
+                    const unsigned long long a = lpa_keys[i], b = lpa_keys[partner];
+                    if ((a > b) == ((i & k) == 0)) {
+                        lpa_keys[i] = b;
+                        lpa_keys[partner] = a;
+                    }
+                }
+            }
+            __syncthreads();
+        }
+    unsigned long long acc = 0ull;
+    for (int t = tid; t < T; t += kLpaSortThreads) {
+        const unsigned long long key = score_key(row[t]);
+        int lo = 0, hi = P;  // first index with keys[idx] >= key
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (lpa_keys[mid] < key) lo = mid + 1; else hi = mid;
+        }
+        const int below = lo;
+        hi = P;  // first index with keys[idx] > key
+        while (lo < hi) {
+            const int mid = (lo + hi) >> 1;
+            if (lpa_keys[mid] <= key) lo = mid + 1; else hi = mid;
+        }
+        acc += 2ull * static_cast<unsigned long long>(below) + static_cast<unsigned long long>(lo - below);
+    }
+    for (int off = 16; off; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
+    if ((tid & 31) == 0) warp_sum[tid >> 5] = acc;
+    __syncthreads();
+    if (tid == 0) {
+        unsigned long long total = 0ull;
+        for (int w = 0; w < kLpaSortThreads / 32; ++w) total += warp_sum[w];
+        twice[r] = total;
+    }
+}
+
 __global__ void k_lpa_final(const unsigned long long* __restrict__ twice, int rows, int T, int P, double* out) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
@@ -145,6 +208,11 @@ int lpa_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
     const int cols = genes.cols;
     if (!ctx->lpa) ctx->lpa = new LpaScratch();
     LpaScratch* s = ctx->lpa;
+    if (s->sorted_auc < 0) {
+        const char* raw = std::getenv("GAPA_LPA_SORTED_AUC");
+        s->sorted_auc = (raw && *raw == '0') ? 0 : 1;
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_lpa_auc_sorted, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+    }
     const int n = ctx->n, T = ctx->T, P = ctx->P, n_pairs = T + P;
     const int mask_words = static_cast<int>((ctx->m + 31) / 32) + 1;
     const size_t per_row = sizeof(unsigned) * mask_words + sizeof(int32_t) * n + sizeof(double) * n_pairs;
@@ -174,7 +242,12 @@ int lpa_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
         GAPA_LAUNCH(k_lpa_scores, dim3((n_pairs + kLpaThreads - 1) / kLpaThreads, cr), kLpaThreads, 0, stream, ctx->d_row_ptr,
                     ctx->d_col_idx, ctx->d_edge_id, ctx->d_pairs, n_pairs, n, mask_words, s->gone.as<unsigned>(),
                     s->deg.as<int32_t>(), s->scores.as<double>());
-        if (P > 0)
+        int P2 = 2;
+        while (P2 < P) P2 <<= 1;
+        if (P > 0 && s->sorted_auc && sizeof(unsigned long long) * static_cast<size_t>(P2) <= 200 * 1024) {
+            GAPA_LAUNCH(k_lpa_auc_sorted, cr, kLpaSortThreads, sizeof(unsigned long long) * P2, stream, s->scores.as<double>(), T, P, P2,
+                        s->twice.as<unsigned long long>());
+        } else if (P > 0)  // probe set too large for shared memory: the exact T x P grid
             GAPA_LAUNCH(k_lpa_auc, dim3((T + kLpaThreads - 1) / kLpaThreads, cr), kLpaThreads, 0, stream,
                         s->scores.as<double>(), T, P, s->twice.as<unsigned long long>());
         GAPA_LAUNCH(k_lpa_final, (cr + 255) / 256, 256, 0, stream, s->twice.as<unsigned long long>(), cr, T, P, out_dev + r0);

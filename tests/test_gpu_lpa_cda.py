@@ -127,3 +127,32 @@ def test_cda_config2_sample(gp, oracle, cuda_device):
     og = oracle.graph_from_edges(g.n, g.edges())
     batch = gp.init_population(pool.size(), 2, k, 1)
     assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(og, 2, batch, threads=2))
+
+
+@pytest.mark.parametrize("sorted_auc", ["1", "0"])
+def test_lpa_auc_paths_agree_with_the_oracle(gp, oracle, cuda_device, monkeypatch, sorted_auc):
+    """The AUC's 2*wins comes from a shared-memory sort + binary searches, or (probe set too large, or
+    GAPA_LPA_SORTED_AUC=0) from the T x P grid; both must give the oracle's double.  Sparse graphs make most
+    RA scores exactly 0 — the tie term carries the result."""
+    monkeypatch.setenv("GAPA_LPA_SORTED_AUC", sorted_auc)
+    rng = np.random.default_rng(77)
+    for n, p, frac in ((600, 0.004, 0.3), (3000, 0.004, 0.1), (90, 0.3, 0.5)):
+        g = gp.erdos_renyi(n, p, 5)
+        split = gp.build_lp_split(g, frac, 9)
+        pool = _edge_pool(gp, split.train)
+        obj = gp.LinkPredictionAttackObjective(split, pool)
+        os_ = oracle.split_build(oracle.graph_from_edges(g.n, g.edges()), frac, 9)
+        batch = rng.integers(0, pool.size(), size=(7, pool.size() // 5)).astype(np.int32)
+        assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(os_, 3, batch)), (n, sorted_auc)
+        assert obj.evaluate_one([]) == oracle.eval_batch(os_, 3, np.zeros((1, 0), np.int32))[0]
+
+
+def test_lpa_probe_set_beyond_shared_memory_uses_the_grid(gp, oracle, cuda_device):
+    g = gp.erdos_renyi(4000, 0.02, 3)  # m ~ 160 k, T = P ~ 64 k > 25,600 keys of shared memory
+    split = gp.build_lp_split(g, 0.4, 4)
+    assert len(split.probe_nonedges) > 25600
+    pool = _edge_pool(gp, split.train)
+    obj = gp.LinkPredictionAttackObjective(split, pool)
+    os_ = oracle.split_build(oracle.graph_from_edges(g.n, g.edges()), 0.4, 4)
+    batch = gp.init_population(pool.size(), 2, 2000, 8)
+    assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(os_, 3, batch, threads=2))
