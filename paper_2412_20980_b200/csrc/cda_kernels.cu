@@ -34,9 +34,18 @@ namespace gapa_b200 {
 
 static constexpr int kCdaThreads = 1024;
 static constexpr int kCdaWarps = kCdaThreads / 32;
-static constexpr int kCdaGroup = 8;        // lanes that patch one neighbour's list together
-static constexpr int kCdaShortList = 64;   // neighbour lists up to this length are patched by one lane group ...
-static constexpr int kCdaThreadList = 24;  // ... or by one thread when the merged community has many neighbours
+#ifndef GAPA_CDA_GROUP
+#define GAPA_CDA_GROUP 8
+#endif
+#ifndef GAPA_CDA_SHORT
+#define GAPA_CDA_SHORT 64
+#endif
+#ifndef GAPA_CDA_THREADLIST
+#define GAPA_CDA_THREADLIST 24
+#endif
+static constexpr int kCdaGroup = GAPA_CDA_GROUP;        // lanes that patch one neighbour's list together
+static constexpr int kCdaShortList = GAPA_CDA_SHORT;   // neighbour lists up to this length are patched by one lane group ...
+static constexpr int kCdaThreadList = GAPA_CDA_THREADLIST;  // ... or by one thread when the merged community has many neighbours
 static constexpr int kCdaLongQueue = 1024;  // longer ones are queued for a warp each
 
 struct CdaScratch {
@@ -94,7 +103,46 @@ __device__ __forceinline__ double merge_gain(int edges, int da, int db, double m
     return static_cast<double>(edges) / m - static_cast<double>(da) * static_cast<double>(db) / den;
 }
 
+// Cached best of a neighbour c of the merged community a when c's best partner was neither a nor b: every
+// other entry of list(c) keeps its gain (deg(c), deg(d) and e(c, d) are untouched by the merge), the entry of
+// b is gone and was not the best, so only the patched (c, a) entry can displace the cached best — O(1), no
+// second scan of the list.  Same result as a fresh scan: the order of candidates is total.
+__device__ __forceinline__ void refresh_best_unchanged(double* best_gain, int32_t* best_id, int c, int old_best, int a, double gn) {
+    if (a > c && gn > 0.0) {
+        const Cand cur{old_best >= 0 ? best_gain[c] : 0.0, c, old_best};
+        const Cand x{gn, c, a};
+        if (cand_better(x, cur)) {
+            best_gain[c] = gn;
+            best_id[c] = a;
+        }
+    }
+}
+
 extern __shared__ int32_t cda_smem[];
+
+// Optional phase timers of the merge loop (build with GAPA_NVCC_EXTRA=-DGAPA_CDA_PROFILE; tools/probe_cda.py
+// prints them): clock64 deltas of thread 0 of CTA 0 between the barriers that end each phase.
+#ifdef GAPA_CDA_PROFILE
+__device__ unsigned long long g_cda_phase[8];
+#define CDA_TICK(k)                                                      \
+    do {                                                                 \
+        if (tid == 0 && blockIdx.x == 0) {                               \
+            const long long now__ = clock64();                           \
+            g_cda_phase[k] += static_cast<unsigned long long>(now__ - t_phase); \
+            t_phase = now__;                                             \
+        }                                                                \
+    } while (0)
+extern "C" int gapa_cuda_cda_phase_cycles(unsigned long long* out8, int reset) {
+    if (cudaMemcpyFromSymbol(out8, g_cda_phase, sizeof(unsigned long long) * 8) != cudaSuccess) return 4;
+    if (reset) {
+        unsigned long long zero[8] = {0};
+        if (cudaMemcpyToSymbol(g_cda_phase, zero, sizeof(zero)) != cudaSuccess) return 4;
+    }
+    return 0;
+}
+#else
+#define CDA_TICK(k) do { } while (0)
+#endif
 
 __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows genes, int rows,
                                                         int pos_in_smem, double* __restrict__ out,
@@ -257,6 +305,9 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         __syncthreads();
 
         // ---- greedy agglomeration (community.cpp:55-87) --------------------------------
+#ifdef GAPA_CDA_PROFILE
+        long long t_phase = clock64();
+#endif
         for (;;) {
             Cand mine{0.0, -1, -1};
             for (int c = tid; c < n; c += kCdaThreads) {
@@ -277,6 +328,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             __syncthreads();
             const int a = chosen.a, b = chosen.b;
             if (b < 0) break;
+            CDA_TICK(0);  // argmax
 
             // make room: list(a) must hold len(a) + len(b) entries
             const int la = len[a], lb = len[b];
@@ -300,6 +352,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             for (int i = tid; i < la; i += kCdaThreads) pos[e_id[ha + i]] = i;
             if (tid == 0) sh_len = la;
             __syncthreads();
+            CDA_TICK(1);  // room + mark positions
             if (tid == 0) sh_pb = pos[b];
             // fold list(b) into list(a)
             for (int j = tid; j < lb; j += kCdaThreads) {
@@ -315,8 +368,10 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                 }
             }
             __syncthreads();
+            CDA_TICK(2);  // fold
             for (int i = tid; i < la; i += kCdaThreads) pos[e_id[ha + i]] = -1;
             __syncthreads();
+            CDA_TICK(3);  // clear positions
             if (tid == 0) {  // drop the (a, b) entry itself
                 const int last = sh_len - 1, pb = sh_pb;
                 if (pb != last) { e_id[ha + pb] = e_id[ha + last]; e_cnt[ha + pb] = e_cnt[ha + last]; }
@@ -338,6 +393,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             Cand best_a{0.0, a, -1};
             if (tid == 0) sh_long = 0;
             __syncthreads();
+            CDA_TICK(4);  // drop
             if (la2 <= kCdaThreads / kCdaGroup) {  // few neighbours: latency matters, spread each list over a lane group
                 const int gl = lane % kCdaGroup;
                 const unsigned gmask = ((1u << kCdaGroup) - 1u) << (lane - gl);
@@ -393,6 +449,11 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                         }
                     }
                     if (pa >= 0 && pbb >= 0) --lc;  // the same on every lane of the group
+                    const int old_best = best_id[c];
+                    if (old_best != a && old_best != b) {  // see refresh_best_unchanged
+                        if (gl == 0) refresh_best_unchanged(best_gain, best_id, c, old_best, a, gn);
+                        continue;
+                    }
                     __syncwarp(gmask);               // the leader's patch is visible to the group
                     Cand best_c{0.0, c, -1};
                     for (int t = gl; t < lc; t += kCdaGroup) {
@@ -461,6 +522,11 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                         e_cnt[hc + pbb] = e;
                         e_gain[hc + pbb] = gn;
                     }
+                    const int old_best = best_id[c];
+                    if (old_best != a && old_best != b) {
+                        refresh_best_unchanged(best_gain, best_id, c, old_best, a, gn);
+                        continue;
+                    }
                     Cand best_c{0.0, c, -1};
                     for (int t0 = 0; t0 < lc; t0 += 4) {
                         int ids[4];
@@ -483,6 +549,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                 }
             }
             __syncthreads();
+            CDA_TICK(5);  // patch (short lists)
             const int n_long = min(sh_long, kCdaLongQueue);
             for (int q = warp; q < n_long; q += kCdaWarps) {
                 const int i = long_queue[q];
@@ -520,6 +587,11 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                     }
                 }
                 lc = __shfl_sync(0xffffffffu, lc, 0);
+                const int old_best = best_id[c];
+                if (old_best != a && old_best != b) {
+                    if (lane == 0) refresh_best_unchanged(best_gain, best_id, c, old_best, a, gn);
+                    continue;
+                }
                 __syncwarp();
                 Cand best_c{0.0, c, -1};
                 for (int t = lane; t < lc; t += 32) {
@@ -536,12 +608,14 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             best_a = cand_warp_best(best_a);
             if (lane == 0) warp_cand[warp] = best_a;
             __syncthreads();
+            CDA_TICK(6);  // patch (long lists)
             if (warp == 0) {
                 Cand x = warp_cand[lane];
                 x = cand_warp_best(x);
                 if (lane == 0) { best_gain[a] = x.gain; best_id[a] = x.b; }
             }
             __syncthreads();
+            CDA_TICK(7);  // best of the merged community
         }
         if (sh_abort) { if (tid == 0) out[r] = 0.0; __syncthreads(); continue; }
 

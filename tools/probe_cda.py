@@ -14,3 +14,18 @@ pop = gp.init_population(pool.size(), rows, k, 1)
 for it in range(3):
     t0 = time.time(); f = obj.evaluate_batch(pop); dt = time.time() - t0
     print(f"n={g.n} m={g.edge_count()} k={k} rows={rows}: wall {dt*1e3:.1f} ms device {obj.dgraph.last_eval_ms():.1f} ms  Q[0]={f[0]:.6f}", flush=True)
+
+import ctypes as C
+lib = gp.capi.load()
+if hasattr(lib, "gapa_cuda_cda_phase_cycles") or True:
+    try:
+        fn = lib.gapa_cuda_cda_phase_cycles
+        buf = (C.c_ulonglong * 8)()
+        fn(buf, 1)
+        obj.evaluate_batch(pop[:1])
+        fn(buf, 0)
+        names = ["argmax", "room+mark", "fold", "clear", "drop", "patch short", "patch long", "best(a)"]
+        tot = sum(buf)
+        print("phase cycles of one individual (CTA 0):", {n: f"{100 * v / tot:.1f}%" for n, v in zip(names, buf)}, f"total {tot / 1.965e6:.1f} ms")
+    except AttributeError:
+        pass
