@@ -336,7 +336,7 @@ def run_gpu_arm(args, w):
         if world == 1:
             # the same generations through the in-library loop (gapa_cuda_run: no host round trip per
             # operator) — what a C++ host gets from run_ga_cuda(); reported beside the stepwise driver
-            iters = max(args.steps, 5)
+            iters = max(args.steps, 5) if ms_per_step > 1.0 else 200  # short generations: amortise init + the final read-back
             loop = gp.run_ga(gp.GAParams(pc=w["pc"], pm=w["pm"], pop_size=s, budget=k, iterations=iters, seed=1), pool, obj)
             line["library_loop"] = {"generations_per_sec": iters / loop.total_wall_seconds, "iterations": iters,
                                     "evals_per_sec": s * (iters + 1) / loop.total_wall_seconds,

@@ -214,6 +214,54 @@ __global__ void __launch_bounds__(1024) k_ga_pick(const double* __restrict__ wei
     }
 }
 
+// selection_weights + cumulative sum + weighted_pick in ONE block for s <= 1024: small populations are
+// launch-latency-bound (C1: seven launches of 3-5 us per generation), so the loop fuses what it can.
+__global__ void __launch_bounds__(1024) k_ga_select_small(const double* __restrict__ fitness, int s, int minimize, uint64_t seed,
+                                                          uint64_t generation, double* __restrict__ weights,
+                                                          double* __restrict__ cumulative, int32_t* __restrict__ partner,
+                                                          int* status) {
+    __shared__ double f[1024];
+    __shared__ double part[1024];
+    const int tid = threadIdx.x;
+    const double mine = tid < s ? fitness[tid] : 0.0;
+    if (tid < s) {
+        f[tid] = mine;
+        if (!isfinite(mine)) *status = GAPA_CUDA_E_NAN;
+    }
+    __syncthreads();
+    double w = 0.0;
+    if (tid < s) {
+        int less = 0, leq = 0;
+        for (int t = 0; t < s; ++t) {
+            const double other = f[t];
+            const bool b = better(other, mine, minimize);
+            less += b;
+            leq += b || other == mine;
+        }
+        w = (static_cast<double>(s - less) + static_cast<double>(s - leq + 1)) / 2.0;
+        weights[tid] = w;
+    }
+    part[tid] = w;
+    __syncthreads();
+    for (int off = 1; off < 1024; off <<= 1) {  // half-integers below 2^53: exact in any order
+        const double add = tid >= off ? part[tid - off] : 0.0;
+        __syncthreads();
+        part[tid] += add;
+        __syncthreads();
+    }
+    if (tid < s) cumulative[tid] = part[tid];
+    const double total = part[s - 1];
+    if (tid < s) {
+        const double target = draw_unit(stream_key(seed, generation, GAPA_ROLE_SELECT, static_cast<uint64_t>(tid)), 1) * total;
+        int a = 0, b = s;  // std::upper_bound: first index with cumulative > target
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (part[mid] <= target) a = mid + 1; else b = mid;
+        }
+        partner[tid] = min(a, s - 1);
+    }
+}
+
 // ---- elitism (ga_ops.cpp:180-212) ---------------------------------------------------------------------
 // Position of stacked row x in the stable best-first order = #{y : better(y, x) or
 // (equal and y < x)}; originals (index < s) therefore precede mutated rows on ties.
@@ -281,6 +329,10 @@ int launch_init(uint32_t pool_size, int row_first, int row_count, int budget, ui
 }
 int launch_select(const double* fitness, int s, int minimize, uint64_t seed, uint64_t generation, int32_t* partner,
                   double* weights, double* cumulative, int* status, cudaStream_t st) {
+    if (s <= 1024) {
+        GAPA_LAUNCH(k_ga_select_small, 1, 1024, 0, st, fitness, s, minimize, seed, generation, weights, cumulative, partner, status);
+        return GAPA_CUDA_OK;
+    }
     GAPA_LAUNCH(k_ga_weights, (s + kPerBlock - 1) / kPerBlock, kGaThreads, 0, st, fitness, s, minimize, weights, status);
     GAPA_LAUNCH(k_ga_pick, 1, 1024, 0, st, weights, s, seed, generation, cumulative, partner);
     return GAPA_CUDA_OK;

@@ -772,8 +772,10 @@ __global__ void __launch_bounds__(kSmallThreads) k_pc_small(GeneRows genes,
                                                             const int32_t* __restrict__ pool_map, int pool_size, int n, int m,
                                                             const int32_t* __restrict__ edge_u,
                                                             const int32_t* __restrict__ edge_v, int task,
-                                                            double* __restrict__ out, PcCounters* counters) {
+                                                            double* __restrict__ out, PcCounters* counters, VariationSpec V,
+                                                            int have_vary) {
     extern __shared__ int32_t small_smem[];
+    __shared__ uint64_t vary_keys[4];
     __shared__ long long warp_pairs[kSmallThreads / 32];
     __shared__ int warp_best[kSmallThreads / 32];
     const int tid = threadIdx.x, row = blockIdx.x;
@@ -788,15 +790,36 @@ __global__ void __launch_bounds__(kSmallThreads) k_pc_small(GeneRows genes,
     }
     __syncthreads();
     const int cols = genes.cols;
-    const int32_t* g = genes.row(row);
-    for (int j = tid; j < cols; j += kSmallThreads) {
-        const int gene = g[j];
-        if (gene < 0 || gene >= pool_size) {
-            counters->range_error = 1;
-            continue;
+    if (have_vary) {
+        // generation loop: this CTA BUILDS child row V.row_first + row (variation.cuh) into its slot and marks
+        // its genes in the same pass — one launch less per generation where launches are what a generation costs
+        const int vrow = V.row_first + row;
+        if (tid < 4)
+            vary_keys[tid] = stream_key(V.P.seed, V.P.generation, GAPA_ROLE_SELECT + tid, static_cast<uint64_t>(vrow)) + kGolden;
+        __syncthreads();
+        const uint64_t ks = vary_keys[0], kc = vary_keys[1], km = vary_keys[2], ki = vary_keys[3];
+        const bool eda = V.partner == nullptr;
+        const int32_t* mine = V.pool + static_cast<size_t>(V.parent[vrow]) * cols;
+        const int32_t* theirs = eda ? mine : V.pool + static_cast<size_t>(V.parent[V.partner[vrow]]) * cols;
+        int32_t* dst = V.pool + static_cast<size_t>(V.child[vrow]) * cols;
+        for (int j = tid; j < cols; j += kSmallThreads) {
+            const int gene = child_gene(V.P, V.pool, V.parent, cols, j, mine[j], theirs[j], eda, ks, kc, km, ki,
+                                        kCounterStep * (static_cast<uint64_t>(j) + 1));
+            dst[j] = gene;
+            const int node = pool_map ? pool_map[gene] : gene;
+            atomicOr(&gone[node >> 5], 1u << (node & 31));
         }
-        const int node = pool_map ? pool_map[gene] : gene;
-        atomicOr(&gone[node >> 5], 1u << (node & 31));
+    } else {
+        const int32_t* g = genes.row(row);
+        for (int j = tid; j < cols; j += kSmallThreads) {
+            const int gene = g[j];
+            if (gene < 0 || gene >= pool_size) {
+                counters->range_error = 1;
+                continue;
+            }
+            const int node = pool_map ? pool_map[gene] : gene;
+            atomicOr(&gone[node >> 5], 1u << (node & 31));
+        }
     }
     __syncthreads();
     for (int e = tid; e < m; e += kSmallThreads) {
@@ -955,14 +978,15 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
     const int n = ctx->n;
     const int sm = ctx->sm_count;
     if (n > 0 && n <= kSmallMaxN && s->small_path) {
-        if (vary) GAPA_TRY(launch_variation_spec(*vary, cols, rows, stream));
         const size_t smem = sizeof(int32_t) * (2 * static_cast<size_t>(n) + ((n + 31) >> 5) + 1);
         GAPA_TRY(s->counters.ensure(sizeof(PcCounters)));
         PcCounters* counters = s->counters.as<PcCounters>();
-        GAPA_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(PcCounters), stream));
+        if (!trusted) GAPA_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(PcCounters), stream));  // trusted genes cannot be out of range
+        const bool fuse = vary && cols > 0;
+        if (vary && !fuse) GAPA_TRY(launch_variation_spec(*vary, cols, rows, stream));
         GAPA_LAUNCH(k_pc_small, rows, kSmallThreads, smem, stream, genes,
                     ctx->pool_identity ? nullptr : ctx->d_pool_map, ctx->pool_size, n, static_cast<int>(ctx->m), ctx->d_edge_u,
-                    ctx->d_edge_v, task, out_dev, counters);
+                    ctx->d_edge_v, task, out_dev, counters, fuse ? *vary : VariationSpec{}, fuse ? 1 : 0);
         if (trusted) return GAPA_CUDA_OK;
         PcCounters h{};
         GAPA_CUDA_TRY(cudaMemcpyAsync(&h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));

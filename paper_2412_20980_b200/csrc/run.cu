@@ -31,6 +31,8 @@ int launch_slots_variation(int32_t*, const int32_t*, const int32_t*, const int32
 int launch_slots_elitism(int32_t*, const int32_t*, const int32_t*, const int32_t*, int, int, int, int, const double*, const double*,
                          int, double, double, uint32_t, uint64_t, uint64_t, int32_t*, int32_t*, double*, int32_t*, int*, cudaStream_t);
 int launch_slots_gather(const int32_t*, const int32_t*, int, int, int32_t*, cudaStream_t);
+int launch_slots_elitism_small(const int32_t*, const int32_t*, int, const double*, const double*, int, int32_t*, int32_t*, double*,
+                               int32_t*, int*, double*, double*, cudaStream_t);
 int launch_elitism_sharded(const int32_t*, const int32_t*, int, int, const int32_t*, int, int, const double*, const double*, int,
                            double, double, uint32_t, uint64_t, uint64_t, int32_t*, double*, int32_t*, int*, cudaStream_t);
 int launch_elitism(const int32_t*, const int32_t*, int, int, const double*, const double*, int, int32_t*, double*, int32_t*,
@@ -269,12 +271,17 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
         vary.row_first = lo;
         GAPA_TRY(evaluate(child, fit_m, &vary));
         // elitism permutes the slot tables; survivors built by other ranks are rebuilt in place
-        GAPA_TRY(launch_slots_elitism(pool_rows, parent, child, partner, s, k, lo, hi, fit, fit_m, minimize, p->pc, p->pm, pool,
-                                      p->seed, g, next_parent, next_child, fit_next, B.src_of_rank.as<int32_t>(), status, st));
+        const bool small = world == 1 && 2 * s <= 1024;  // launch-latency-bound: elitism and the generation's statistics in one launch
+        if (small)
+            GAPA_TRY(launch_slots_elitism_small(parent, child, s, fit, fit_m, minimize, next_parent, next_child, fit_next,
+                                                B.src_of_rank.as<int32_t>(), status, hist + (gen - 1), hist + iters + (gen - 1), st));
+        else
+            GAPA_TRY(launch_slots_elitism(pool_rows, parent, child, partner, s, k, lo, hi, fit, fit_m, minimize, p->pc, p->pm, pool,
+                                          p->seed, g, next_parent, next_child, fit_next, B.src_of_rank.as<int32_t>(), status, st));
         std::swap(parent, next_parent);
         std::swap(child, next_child);
         std::swap(fit, fit_next);
-        GAPA_LAUNCH(k_ga_stats, 1, 1024, 0, st, fit, s, hist + (gen - 1), hist + iters + (gen - 1));
+        if (!small) GAPA_LAUNCH(k_ga_stats, 1, 1024, 0, st, fit, s, hist + (gen - 1), hist + iters + (gen - 1));
         // NaN / non-finite fitness is an Error in the reference (ga_ops.cpp:56-57, :189-192);
         // the flag is polled every few generations and at the end to keep the loop asynchronous.
         if ((gen & 15) == 0 || gen == iters) {

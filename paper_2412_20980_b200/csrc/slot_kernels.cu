@@ -117,6 +117,70 @@ __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_commit(const int32_t*
     next_child[r] = drop < s ? parent[drop] : child[drop - s];
 }
 
+// rank + commit + record_generation (modes.cpp:35-43) in ONE block for 2s <= 1024 (small populations are
+// launch-latency-bound): next tables, next fitness, history best = front, history mean = the reference's
+// left-to-right sum / s (added in parallel only when every value is an integer small enough to add exactly).
+__global__ void __launch_bounds__(1024) k_ga_slots_elitism_small(const int32_t* __restrict__ parent, const int32_t* __restrict__ child,
+                                                                 const double* __restrict__ fit, const double* __restrict__ fit_m,
+                                                                 int s, int minimize, int32_t* __restrict__ order,
+                                                                 int32_t* __restrict__ next_parent, int32_t* __restrict__ next_child,
+                                                                 double* __restrict__ next_fit, int* status, double* hist_best,
+                                                                 double* hist_mean) {
+    __shared__ double f[1024];
+    __shared__ double kept[512];
+    __shared__ int ord[1024];
+    __shared__ double warp_sum[32];
+    __shared__ int not_exact;
+    const int tid = threadIdx.x, total = 2 * s;
+    const double mine = tid < total ? (tid < s ? fit[tid] : fit_m[tid - s]) : 0.0;
+    if (tid < total) {
+        f[tid] = mine;
+        if (isnan(mine)) *status = GAPA_CUDA_E_NAN;
+    }
+    if (tid == 0) not_exact = 0;
+    __syncthreads();
+    if (tid < total) {
+        int rank = 0;
+        for (int t = 0; t < total; ++t) {
+            const double other = f[t];
+            const bool before = minimize ? other < mine : other > mine;
+            rank += before || (other == mine && t < tid);
+        }
+        ord[rank] = tid;
+        order[rank] = tid;
+    }
+    __syncthreads();
+    double x = 0.0;
+    if (tid < s) {
+        const int keep = ord[tid], drop = ord[s + tid];
+        x = f[keep];
+        next_parent[tid] = keep < s ? parent[keep] : child[keep - s];
+        next_fit[tid] = x;
+        kept[tid] = x;
+        next_child[tid] = drop < s ? parent[drop] : child[drop - s];
+        if (!(x == floor(x)) || !(fabs(x) < 9007199254740992.0 / static_cast<double>(s))) not_exact = 1;
+    }
+    __syncthreads();
+    if (!not_exact) {
+        for (int off = 16; off; off >>= 1) x += __shfl_down_sync(0xffffffffu, x, off);
+        if ((tid & 31) == 0) warp_sum[tid >> 5] = x;
+        __syncthreads();
+        if (tid < 32) {
+            double v = warp_sum[tid];
+            for (int off = 16; off; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+            if (tid == 0) {
+                *hist_best = kept[0];
+                *hist_mean = v / static_cast<double>(s);
+            }
+        }
+    } else if (tid == 0) {
+        double sum = 0.0;
+        for (int i = 0; i < s; ++i) sum += kept[i];
+        *hist_best = kept[0];
+        *hist_mean = sum / static_cast<double>(s);
+    }
+}
+
 __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_identity(int s, int32_t* parent, int32_t* child) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r < s) {
@@ -168,6 +232,14 @@ int launch_slots_elitism(int32_t* pool, const int32_t* parent, const int32_t* ch
                     make_variation_params(pc, pm, pool_size, s, seed, generation), pool, parent, child, partner, k, s, order, block_lo, block_hi);
     GAPA_LAUNCH(k_ga_slots_commit, (s + kSlotThreads - 1) / kSlotThreads, kSlotThreads, 0, st, parent, child, fit, fit_m, s, order,
                 next_parent, next_child, next_fit);
+    return GAPA_CUDA_OK;
+}
+// elitism + GenerationStats::best / mean in one launch; only for an unsharded run with 2s <= 1024
+int launch_slots_elitism_small(const int32_t* parent, const int32_t* child, int s, const double* fit, const double* fit_m, int minimize,
+                               int32_t* next_parent, int32_t* next_child, double* next_fit, int32_t* order, int* status,
+                               double* hist_best, double* hist_mean, cudaStream_t st) {
+    GAPA_LAUNCH(k_ga_slots_elitism_small, 1, 1024, 0, st, parent, child, fit, fit_m, s, minimize, order, next_parent, next_child,
+                next_fit, status, hist_best, hist_mean);
     return GAPA_CUDA_OK;
 }
 int launch_slots_gather(const int32_t* pool, const int32_t* table, int rows, int k, int32_t* out, cudaStream_t st) {
