@@ -428,6 +428,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                         pa = max(pa, __shfl_xor_sync(gmask, pa, off));
                         pbb = max(pbb, __shfl_xor_sync(gmask, pbb, off));
                     }
+                    __syncwarp(gmask);  // every lane has read len[c] and its entries before the leader rewrites them
                     if (gl == 0) {
                         if (pa >= 0) {
                             if (pbb >= 0) {
@@ -449,7 +450,8 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                         }
                     }
                     if (pa >= 0 && pbb >= 0) --lc;  // the same on every lane of the group
-                    const int old_best = best_id[c];
+                    // the leader alone reads the cached best (it is also the one that rewrites it) and tells the group
+                    const int old_best = __shfl_sync(gmask, gl == 0 ? best_id[c] : 0, lane - gl);
                     if (old_best != a && old_best != b) {  // see refresh_best_unchanged
                         if (gl == 0) refresh_best_unchanged(best_gain, best_id, c, old_best, a, gn);
                         continue;
@@ -565,6 +567,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                 }
                 pa = __reduce_max_sync(0xffffffffu, pa);
                 pbb = __reduce_max_sync(0xffffffffu, pbb);
+                __syncwarp();  // every lane has read len[c] and its entries before lane 0 rewrites them
                 if (lane == 0) {
                     if (pa >= 0) {
                         if (pbb >= 0) {
@@ -587,7 +590,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                     }
                 }
                 lc = __shfl_sync(0xffffffffu, lc, 0);
-                const int old_best = best_id[c];
+                const int old_best = __shfl_sync(0xffffffffu, lane == 0 ? best_id[c] : 0, 0);
                 if (old_best != a && old_best != b) {
                     if (lane == 0) refresh_best_unchanged(best_gain, best_id, c, old_best, a, gn);
                     continue;
