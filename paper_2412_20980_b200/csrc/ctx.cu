@@ -381,7 +381,7 @@ static int check_task(const gapa_cuda_ctx* c, int task) {
 }
 
 static int eval_rows_locked(gapa_cuda_ctx* c, int task, const GeneRows& genes, int rows, double* out_dev, void* stream,
-                            const VariationSpec* vary = nullptr) {
+                            const VariationSpec* vary = nullptr, bool defer_timing = false) {
     std::unique_lock<std::mutex> lock(c->mu, std::defer_lock);
     if (stream != static_cast<void*>(c->stream)) lock.lock();  // the host-buffer form already holds it
     GAPA_CUDA_TRY(cudaSetDevice(c->device));
@@ -398,6 +398,7 @@ static int eval_rows_locked(gapa_cuda_ctx* c, int task, const GeneRows& genes, i
     }
     if (rc != GAPA_CUDA_OK) return rc;
     GAPA_CUDA_TRY(cudaEventRecord(c->ev_stop, s));
+    if (defer_timing) return GAPA_CUDA_OK;  // the caller synchronises the stream once and reads the events then
     GAPA_CUDA_TRY(cudaEventSynchronize(c->ev_stop));
     GAPA_CUDA_TRY(cudaEventElapsedTime(&c->last_eval_ms, c->ev_start, c->ev_stop));
     return GAPA_CUDA_OK;
@@ -477,16 +478,18 @@ int gapa_cuda_eval_batch(gapa_cuda_ctx* c, int task, const int32_t* genes_host, 
             GAPA_CUDA_TRY(cudaEventRecord(c->copy_events[i], c->copy_stream));
         }
     float total_ms = 0.f;
+    const bool single = chunks == 1;  // small batches: one host synchronisation for kernels + read-back
     for (int i = 0; i < chunks; ++i) {
         const int r0 = i * chunk_rows, cr = std::min(chunk_rows, rows - r0);
         if (cells) GAPA_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_events[i], 0));
-        GAPA_TRY(gapa_cuda_eval_batch_device(c, task, stage + static_cast<size_t>(r0) * cols, cr, cols,
-                                             c->out_stage.as<double>() + r0, c->stream));
+        GAPA_TRY(eval_rows_locked(c, task, GeneRows{stage + static_cast<size_t>(r0) * cols, nullptr, cols}, cr,
+                                  c->out_stage.as<double>() + r0, c->stream, nullptr, single));
         total_ms += c->last_eval_ms;
     }
-    c->last_eval_ms = total_ms;
     GAPA_CUDA_TRY(cudaMemcpyAsync(out_host, c->out_stage.ptr, sizeof(double) * rows, cudaMemcpyDeviceToHost, c->stream));
     GAPA_CUDA_TRY(cudaStreamSynchronize(c->stream));
+    if (single) GAPA_CUDA_TRY(cudaEventElapsedTime(&total_ms, c->ev_start, c->ev_stop));
+    c->last_eval_ms = total_ms;
     return GAPA_CUDA_OK;
 }
 
