@@ -101,8 +101,9 @@ int gapa_cuda_lp_split_set(gapa_cuda_ctx* ctx, int32_t T, const int32_t* test_uv
  * Host form: H2D of genes + kernels + D2H of out, synchronous. */
 int gapa_cuda_eval_batch(gapa_cuda_ctx* ctx, int task, const int32_t* genes_host, int rows, int cols,
                          double* out_host);
-/* Device form: genes and out live in HBM; synchronises `stream` before returning
- * only as far as needed to report status (gene range / NaN). */
+/* Device form: genes and out live in HBM.  Returns when the evaluation has finished on
+ * `stream` (status is final: gene range, CUDA errors; gapa_cuda_last_eval_ms is valid).
+ * Inside gapa_cuda_run the same evaluators run without this wait. */
 int gapa_cuda_eval_batch_device(gapa_cuda_ctx* ctx, int task, const int32_t* genes_dev, int rows, int cols,
                                 double* out_dev, void* stream);
 
