@@ -14,19 +14,25 @@
 //     (EdgeRemoval pools), or from the CSR rows plus the distinct added pairs
 //     (EdgeAddition pools, gene_pool.cpp:57-60) — lists are unsorted, so an added edge
 //     is just one more entry at each end;
-//   * per community a cached best partner among ids greater than its own.  m is
-//     constant during a detection, so only pairs touching the merged community
-//     change gain; every other cached gain is bit-identical to a fresh evaluation;
+//   * per community a cached best partner among ids greater than its own.  Gains are never stored per
+//     entry: gain(c, d) = e(c,d)/m - deg(c) deg(d)/(2 m^2) is evaluated from the entry's count and the two
+//     degrees when a best is (re)computed.  m is constant during a detection, so a merge of b into a only
+//     changes the gains of pairs that touch a — and for a neighbour c of a that is not a neighbour of b
+//     that pair only gets WORSE (deg(a) grew), which matters only if a was c's cached best;
 //   * each step = block-wide argmax over the cached bests with the reference's
 //     tie-break (greatest gain, then smallest a, then smallest b == first strictly
 //     greater pair in (a, b) scan order), then a cooperative merge: fold list(b) into
-//     list(a) through a position map in shared memory, and one warp per neighbour c
-//     patches list(c) (b -> a, counts, gain) and refreshes c's cached best.
+//     list(a) through a position map in shared memory; one pass over the new list(a) finds a's new best
+//     and queues the few communities whose own list needs work — the neighbours of b (mirror entry
+//     b -> a, counts) and the neighbours of a whose cached best was a — each taken by a group of lanes.
+//     A merged community typically has hundreds of neighbours, b a dozen: the lists of the others are
+//     not touched at all.
 // Gains use the reference's exact FP64 expression (IEEE division, no FMA: the library
 // is built with -fmad=false); community ids are "smallest member" because b always
 // merges into a < b; Q is accumulated sequentially in ascending community id, which
 // is first-appearance order (community.cpp:17-26).
 #include <algorithm>
+#include <type_traits>
 
 #include "internal.cuh"
 
@@ -40,16 +46,14 @@ static constexpr int kCdaWarps = kCdaThreads / 32;
 #ifndef GAPA_CDA_SHORT
 #define GAPA_CDA_SHORT 64
 #endif
-#ifndef GAPA_CDA_THREADLIST
-#define GAPA_CDA_THREADLIST 24
-#endif
 static constexpr int kCdaGroup = GAPA_CDA_GROUP;        // lanes that patch one neighbour's list together
-static constexpr int kCdaShortList = GAPA_CDA_SHORT;   // neighbour lists up to this length are patched by one lane group ...
-static constexpr int kCdaThreadList = GAPA_CDA_THREADLIST;  // ... or by one thread when the merged community has many neighbours
+static constexpr int kCdaShortList = GAPA_CDA_SHORT;   // lists up to this length are worked on by one lane group, longer ones by a warp
 static constexpr int kCdaLongQueue = 1024;  // longer ones are queued for a warp each
+static constexpr int kCdaWorkQueue = 2048;  // communities whose own list needs work in one merge step
+static constexpr int kNbFlag = 1 << 30;     // position-map bit: the community is a neighbour of the merged-away b
 
 struct CdaScratch {
-    DevBuf gone, ints, doubles, e_id, e_cnt, e_gain, status;
+    DevBuf gone, ints, doubles, e_id, e_cnt, status;
     size_t pool_cap = 0;
     int slots = 0;
 };
@@ -72,7 +76,6 @@ struct CdaArgs {
     double* best_gain;     // [slots][n]
     int32_t* e_id;         // [slots][pool_cap]
     int32_t* e_cnt;
-    double* e_gain;
     int* status;           // [0] = GAPA_CUDA_E_RANGE, [1] = pool overflow
 };
 
@@ -154,7 +157,8 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
     __shared__ int sh_len, sh_pb, sh_new_head, sh_abort, sh_count;
     __shared__ int sh_scan[kCdaThreads];
     __shared__ int long_queue[kCdaLongQueue];
-    __shared__ int sh_long;
+    __shared__ int work_queue[kCdaWorkQueue];
+    __shared__ int sh_long, sh_work;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int n = A.n;
@@ -179,7 +183,6 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
     }
     int32_t* e_id = A.e_id + slot * A.pool_cap;
     int32_t* e_cnt = A.e_cnt + slot * A.pool_cap;
-    double* e_gain = A.e_gain + slot * A.pool_cap;
     int32_t* pos = pos_in_smem == 2 ? cda_smem + 6 * static_cast<size_t>(n) : (pos_in_smem ? cda_smem : A.pos_global + slot * n);
 
     for (int r = blockIdx.x; r < rows; r += gridDim.x) {
@@ -286,15 +289,15 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         const double den = 2.0 * m * m;
         if (tid == 0) sh_pool_top = adding ? total_degree : A.csr_slots;
 
-        // initial gains and cached bests
+        // initial cached bests
         for (int u = tid; u < n; u += kCdaThreads) {
             const int h = head[u], l = len[u], du = cdeg[u];
             Cand best{0.0, u, -1};
             for (int i = 0; i < l; ++i) {
                 const int v = e_id[h + i];
+                if (v <= u) continue;
                 const double gn = merge_gain(1, du, cdeg[v], m, den);
-                e_gain[h + i] = gn;
-                if (v > u && gn > 0.0) {
+                if (gn > 0.0) {
                     const Cand c{gn, u, v};
                     if (cand_better(c, best)) best = c;
                 }
@@ -303,6 +306,79 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             best_id[u] = best.b;
         }
         __syncthreads();
+
+        // List work for one neighbour c of the merged community a, by a group of W lanes (W = 1: one thread):
+        // if c was a neighbour of b, its mirror entry b becomes / is folded into its entry a (count `e`);
+        // then c's cached best — O(1) unless its best partner was a or b, else a fresh scan of list(c).
+        auto list_work = [&](auto width, int c, int e, bool is_nb, int a, int b, int da, int gl, unsigned gmask) {
+            constexpr int W = decltype(width)::value;
+            const int hc = head[c];
+            int lc = len[c];
+            const int leader = lane - gl;
+            const double gn = merge_gain(e, da, cdeg[c], m, den);
+            if (is_nb) {
+                int pa = -1, pbb = -1;
+                for (int t = gl; t < lc; t += W) {
+                    const int id = e_id[hc + t];
+                    if (id == a) pa = t;
+                    if (id == b) pbb = t;
+                }
+#pragma unroll
+                for (int off = W / 2; off; off >>= 1) {
+                    pa = max(pa, __shfl_xor_sync(gmask, pa, off));
+                    pbb = max(pbb, __shfl_xor_sync(gmask, pbb, off));
+                }
+                __syncwarp(gmask);  // every lane has read len[c] and its entries before the leader rewrites them
+                if (gl == 0) {
+                    if (pa >= 0) {
+                        if (pbb >= 0) {
+                            const int last = lc - 1;
+                            if (pbb != last) {
+                                e_id[hc + pbb] = e_id[hc + last];
+                                e_cnt[hc + pbb] = e_cnt[hc + last];
+                                if (pa == last) pa = pbb;
+                            }
+                            len[c] = last;
+                        }
+                        e_cnt[hc + pa] = e;
+                    } else {
+                        e_id[hc + pbb] = a;
+                        e_cnt[hc + pbb] = e;
+                    }
+                }
+                if (pa >= 0 && pbb >= 0) --lc;  // the same on every lane of the group
+            }
+            // the leader alone reads the cached best (it is also the one that rewrites it) and tells the group
+            const int old_best = __shfl_sync(gmask, gl == 0 ? best_id[c] : 0, leader);
+            if (old_best != a && old_best != b) {
+                if (gl == 0) refresh_best_unchanged(best_gain, best_id, c, old_best, a, gn);
+                return;
+            }
+            __syncwarp(gmask);  // the leader's patch is visible to the group
+            const int dc = cdeg[c];
+            Cand best_c{0.0, c, -1};
+            for (int t = gl; t < lc; t += W) {
+                const int id = e_id[hc + t];
+                if (id <= c) continue;
+                const double gg = merge_gain(e_cnt[hc + t], dc, cdeg[id], m, den);
+                if (gg > 0.0) {
+                    const Cand x{gg, c, id};
+                    if (cand_better(x, best_c)) best_c = x;
+                }
+            }
+#pragma unroll
+            for (int off = W / 2; off; off >>= 1) {
+                Cand o;
+                o.gain = __shfl_xor_sync(gmask, best_c.gain, off);
+                o.a = c;
+                o.b = __shfl_xor_sync(gmask, best_c.b, off);
+                if (cand_better(o, best_c)) best_c = o;
+            }
+            if (gl == 0) {
+                best_gain[c] = best_c.gain;
+                best_id[c] = best_c.b;
+            }
+        };
 
         // ---- greedy agglomeration (community.cpp:55-87) --------------------------------
 #ifdef GAPA_CDA_PROFILE
@@ -348,277 +424,112 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                 if (tid == 0) { head[a] = nh; cap[a] = 2 * (la + lb); }
                 ha = nh;
             }
-            // mark positions of list(a)
+            // positions of list(a) in the map
             for (int i = tid; i < la; i += kCdaThreads) pos[e_id[ha + i]] = i;
             if (tid == 0) sh_len = la;
             __syncthreads();
             CDA_TICK(1);  // room + mark positions
             if (tid == 0) sh_pb = pos[b];
-            // fold list(b) into list(a)
+            // fold list(b) into list(a); every neighbour of b ends up in the map, flagged
             for (int j = tid; j < lb; j += kCdaThreads) {
                 const int c = e_id[hb + j];
                 if (c == a) continue;
                 const int e = e_cnt[hb + j];
                 const int p = pos[c];
-                if (p >= 0) e_cnt[ha + p] += e;
-                else {
+                if (p >= 0) {
+                    e_cnt[ha + p] += e;
+                    pos[c] = p | kNbFlag;
+                } else {
                     const int q = atomicAdd(&sh_len, 1);
                     e_id[ha + q] = c;
                     e_cnt[ha + q] = e;
+                    pos[c] = q | kNbFlag;
                 }
             }
             __syncthreads();
             CDA_TICK(2);  // fold
-            for (int i = tid; i < la; i += kCdaThreads) pos[e_id[ha + i]] = -1;
-            __syncthreads();
-            CDA_TICK(3);  // clear positions
             if (tid == 0) {  // drop the (a, b) entry itself
                 const int last = sh_len - 1, pb = sh_pb;
-                if (pb != last) { e_id[ha + pb] = e_id[ha + last]; e_cnt[ha + pb] = e_cnt[ha + last]; }
+                if (pb != last) {
+                    const int moved = e_id[ha + last];
+                    e_id[ha + pb] = moved;
+                    e_cnt[ha + pb] = e_cnt[ha + last];
+                    pos[moved] = pb | (pos[moved] & kNbFlag);
+                }
+                pos[b] = -1;
                 sh_len = last;
                 len[a] = last;
                 cdeg[a] += cdeg[b];
                 len[b] = 0;
                 merged_into[b] = a;
                 best_id[b] = -1;
+                sh_work = 0;
+                sh_long = 0;
             }
             __syncthreads();
+            CDA_TICK(3);  // drop
             const int la2 = sh_len, da = cdeg[a];
 
-            // Patch the mirror entry of every neighbour c of the merged community and refresh c's
-            // cached best.  This is the critical path of a merge step (everything else waits at the next
-            // barrier), so a neighbour's list is scanned by a GROUP of kCdaGroup lanes — 128 neighbours at a
-            // time, each list read in one or two round trips to L2 instead of one per 8 entries; lists
-            // longer than kCdaShortList are queued and taken by one WARP each.
+            // One pass over the new list(a): a's own best (every gain of a changed), and the queue of communities
+            // whose list needs work — the neighbours of b, and neighbours whose cached best was a (their pair with
+            // a only got worse).  A full queue makes the finder do the work itself.
             Cand best_a{0.0, a, -1};
-            if (tid == 0) sh_long = 0;
-            __syncthreads();
-            CDA_TICK(4);  // drop
-            if (la2 <= kCdaThreads / kCdaGroup) {  // few neighbours: latency matters, spread each list over a lane group
-                const int gl = lane % kCdaGroup;
-                const unsigned gmask = ((1u << kCdaGroup) - 1u) << (lane - gl);
-                for (int i0 = 0; i0 < la2; i0 += kCdaThreads / kCdaGroup) {
-                    const int i = i0 + tid / kCdaGroup;
-                    if (i >= la2) continue;  // uniform within a group
-                    const int c = e_id[ha + i], e = e_cnt[ha + i];
+            for (int i = tid; i < la2; i += kCdaThreads) {
+                const int c = e_id[ha + i], e = e_cnt[ha + i];
+                if (c > a) {
                     const double gn = merge_gain(e, da, cdeg[c], m, den);
-                    const int hc = head[c];
-                    int lc = len[c];
-                    int queued = 0;
-                    if (gl == 0) {
-                        e_gain[ha + i] = gn;
-                        if (c > a && gn > 0.0) {
-                            const Cand x{gn, a, c};
-                            if (cand_better(x, best_a)) best_a = x;
-                        }
-                        if (lc > kCdaShortList) {
-                            const int q = atomicAdd(&sh_long, 1);
-                            if (q < kCdaLongQueue) { long_queue[q] = i; queued = 1; }
-                        }
-                    }
-                    if (__shfl_sync(gmask, queued, lane - gl)) continue;
-                    int pa = -1, pbb = -1;
-                    for (int t = gl; t < lc; t += kCdaGroup) {
-                        const int id = e_id[hc + t];
-                        if (id == a) pa = t;
-                        if (id == b) pbb = t;
-                    }
-    #pragma unroll
-                    for (int off = kCdaGroup / 2; off; off >>= 1) {
-                        pa = max(pa, __shfl_xor_sync(gmask, pa, off));
-                        pbb = max(pbb, __shfl_xor_sync(gmask, pbb, off));
-                    }
-                    __syncwarp(gmask);  // every lane has read len[c] and its entries before the leader rewrites them
-                    if (gl == 0) {
-                        if (pa >= 0) {
-                            if (pbb >= 0) {
-                                const int last = lc - 1;
-                                if (pbb != last) {
-                                    e_id[hc + pbb] = e_id[hc + last];
-                                    e_cnt[hc + pbb] = e_cnt[hc + last];
-                                    e_gain[hc + pbb] = e_gain[hc + last];
-                                    if (pa == last) pa = pbb;
-                                }
-                                len[c] = last;
-                            }
-                            e_cnt[hc + pa] = e;
-                            e_gain[hc + pa] = gn;
-                        } else {
-                            e_id[hc + pbb] = a;
-                            e_cnt[hc + pbb] = e;
-                            e_gain[hc + pbb] = gn;
-                        }
-                    }
-                    if (pa >= 0 && pbb >= 0) --lc;  // the same on every lane of the group
-                    // the leader alone reads the cached best (it is also the one that rewrites it) and tells the group
-                    const int old_best = __shfl_sync(gmask, gl == 0 ? best_id[c] : 0, lane - gl);
-                    if (old_best != a && old_best != b) {  // see refresh_best_unchanged
-                        if (gl == 0) refresh_best_unchanged(best_gain, best_id, c, old_best, a, gn);
-                        continue;
-                    }
-                    __syncwarp(gmask);               // the leader's patch is visible to the group
-                    Cand best_c{0.0, c, -1};
-                    for (int t = gl; t < lc; t += kCdaGroup) {
-                        const int id = e_id[hc + t];
-                        const double gg = e_gain[hc + t];
-                        if (id > c && gg > 0.0) {
-                            const Cand x{gg, c, id};
-                            if (cand_better(x, best_c)) best_c = x;
-                        }
-                    }
-    #pragma unroll
-                    for (int off = kCdaGroup / 2; off; off >>= 1) {
-                        Cand o;
-                        o.gain = __shfl_xor_sync(gmask, best_c.gain, off);
-                        o.a = c;
-                        o.b = __shfl_xor_sync(gmask, best_c.b, off);
-                        if (cand_better(o, best_c)) best_c = o;
-                    }
-                    if (gl == 0) {
-                        best_gain[c] = best_c.gain;
-                        best_id[c] = best_c.b;
-                    }
-                }
-            } else {  // many neighbours: throughput matters, one thread per neighbour
-                for (int i = tid; i < la2; i += kCdaThreads) {
-                    const int c = e_id[ha + i], e = e_cnt[ha + i];
-                    const double gn = merge_gain(e, da, cdeg[c], m, den);
-                    e_gain[ha + i] = gn;
-                    if (c > a && gn > 0.0) {
+                    if (gn > 0.0) {
                         const Cand x{gn, a, c};
                         if (cand_better(x, best_a)) best_a = x;
                     }
-                    const int hc = head[c];
-                    int lc = len[c];
-                    if (lc > kCdaThreadList) {
-                        const int q = atomicAdd(&sh_long, 1);
-                        if (q < kCdaLongQueue) { long_queue[q] = i; continue; }
-                    }
-                    int pa = -1, pbb = -1;
-                    for (int t0 = 0; t0 < lc; t0 += 8) {  // 8 independent loads in flight per step
-                        int ids[8];
-    #pragma unroll
-                        for (int u = 0; u < 8; ++u) ids[u] = t0 + u < lc ? e_id[hc + t0 + u] : -1;
-    #pragma unroll
-                        for (int u = 0; u < 8; ++u) {
-                            if (ids[u] == a) pa = t0 + u;
-                            if (ids[u] == b) pbb = t0 + u;
-                        }
-                    }
-                    if (pa >= 0) {
-                        if (pbb >= 0) {
-                            const int last = lc - 1;
-                            if (pbb != last) {
-                                e_id[hc + pbb] = e_id[hc + last];
-                                e_cnt[hc + pbb] = e_cnt[hc + last];
-                                e_gain[hc + pbb] = e_gain[hc + last];
-                                if (pa == last) pa = pbb;
-                            }
-                            lc = last;
-                            len[c] = lc;
-                        }
-                        e_cnt[hc + pa] = e;
-                        e_gain[hc + pa] = gn;
-                    } else {
-                        e_id[hc + pbb] = a;
-                        e_cnt[hc + pbb] = e;
-                        e_gain[hc + pbb] = gn;
-                    }
-                    const int old_best = best_id[c];
-                    if (old_best != a && old_best != b) {
-                        refresh_best_unchanged(best_gain, best_id, c, old_best, a, gn);
-                        continue;
-                    }
-                    Cand best_c{0.0, c, -1};
-                    for (int t0 = 0; t0 < lc; t0 += 4) {
-                        int ids[4];
-                        double gs[4];
-    #pragma unroll
-                        for (int u = 0; u < 4; ++u) {
-                            const bool in = t0 + u < lc;
-                            ids[u] = in ? e_id[hc + t0 + u] : -1;
-                            gs[u] = in ? e_gain[hc + t0 + u] : 0.0;
-                        }
-    #pragma unroll
-                        for (int u = 0; u < 4; ++u)
-                            if (ids[u] > c && gs[u] > 0.0) {
-                                const Cand x{gs[u], c, ids[u]};
-                                if (cand_better(x, best_c)) best_c = x;
-                            }
-                    }
-                    best_gain[c] = best_c.gain;
-                    best_id[c] = best_c.b;
+                }
+                const bool is_nb = (pos[c] & kNbFlag) != 0;
+                if (is_nb || (c < a && best_id[c] == a)) {
+                    const int q = atomicAdd(&sh_work, 1);
+                    if (q < kCdaWorkQueue) work_queue[q] = i;
+                    else list_work(std::integral_constant<int, 1>{}, c, e, is_nb, a, b, da, 0, 1u << lane);
                 }
             }
             __syncthreads();
-            CDA_TICK(5);  // patch (short lists)
+            CDA_TICK(4);  // scan of list(a)
+            const int n_work = min(sh_work, kCdaWorkQueue);
+            {
+                const int gl = lane % kCdaGroup;
+                const unsigned gmask = ((1u << kCdaGroup) - 1u) << (lane - gl);
+                for (int w0 = 0; w0 < n_work; w0 += kCdaThreads / kCdaGroup) {
+                    const int w = w0 + tid / kCdaGroup;
+                    if (w >= n_work) continue;  // uniform within a group
+                    const int i = work_queue[w];
+                    const int c = e_id[ha + i];
+                    int queued = 0;
+                    if (gl == 0 && len[c] > kCdaShortList) {
+                        const int q = atomicAdd(&sh_long, 1);
+                        if (q < kCdaLongQueue) { long_queue[q] = i; queued = 1; }
+                    }
+                    if (__shfl_sync(gmask, queued, lane - gl)) continue;
+                    list_work(std::integral_constant<int, kCdaGroup>{}, c, e_cnt[ha + i], (pos[c] & kNbFlag) != 0, a, b, da, gl, gmask);
+                }
+            }
+            __syncthreads();
+            CDA_TICK(5);  // list work (short lists)
             const int n_long = min(sh_long, kCdaLongQueue);
             for (int q = warp; q < n_long; q += kCdaWarps) {
                 const int i = long_queue[q];
-                const int c = e_id[ha + i], e = e_cnt[ha + i];
-                const double gn = e_gain[ha + i];
-                const int hc = head[c];
-                int lc = len[c];
-                int pa = -1, pbb = -1;
-                for (int t = lane; t < lc; t += 32) {
-                    const int id = e_id[hc + t];
-                    if (id == a) pa = t;
-                    if (id == b) pbb = t;
-                }
-                pa = __reduce_max_sync(0xffffffffu, pa);
-                pbb = __reduce_max_sync(0xffffffffu, pbb);
-                __syncwarp();  // every lane has read len[c] and its entries before lane 0 rewrites them
-                if (lane == 0) {
-                    if (pa >= 0) {
-                        if (pbb >= 0) {
-                            const int last = lc - 1;
-                            if (pbb != last) {
-                                e_id[hc + pbb] = e_id[hc + last];
-                                e_cnt[hc + pbb] = e_cnt[hc + last];
-                                e_gain[hc + pbb] = e_gain[hc + last];
-                                if (pa == last) pa = pbb;
-                            }
-                            lc = last;
-                            len[c] = lc;
-                        }
-                        e_cnt[hc + pa] = e;
-                        e_gain[hc + pa] = gn;
-                    } else {
-                        e_id[hc + pbb] = a;
-                        e_cnt[hc + pbb] = e;
-                        e_gain[hc + pbb] = gn;
-                    }
-                }
-                lc = __shfl_sync(0xffffffffu, lc, 0);
-                const int old_best = __shfl_sync(0xffffffffu, lane == 0 ? best_id[c] : 0, 0);
-                if (old_best != a && old_best != b) {
-                    if (lane == 0) refresh_best_unchanged(best_gain, best_id, c, old_best, a, gn);
-                    continue;
-                }
-                __syncwarp();
-                Cand best_c{0.0, c, -1};
-                for (int t = lane; t < lc; t += 32) {
-                    const int id = e_id[hc + t];
-                    const double gg = e_gain[hc + t];
-                    if (id > c && gg > 0.0) {
-                        const Cand x{gg, c, id};
-                        if (cand_better(x, best_c)) best_c = x;
-                    }
-                }
-                best_c = cand_warp_best(best_c);
-                if (lane == 0) { best_gain[c] = best_c.gain; best_id[c] = best_c.b; }
+                const int c = e_id[ha + i];
+                list_work(std::integral_constant<int, 32>{}, c, e_cnt[ha + i], (pos[c] & kNbFlag) != 0, a, b, da, lane, 0xffffffffu);
             }
             best_a = cand_warp_best(best_a);
             if (lane == 0) warp_cand[warp] = best_a;
             __syncthreads();
-            CDA_TICK(6);  // patch (long lists)
+            CDA_TICK(6);  // list work (long lists)
             if (warp == 0) {
                 Cand x = warp_cand[lane];
                 x = cand_warp_best(x);
                 if (lane == 0) { best_gain[a] = x.gain; best_id[a] = x.b; }
             }
+            for (int i = tid; i < la2; i += kCdaThreads) pos[e_id[ha + i]] = -1;  // the map is empty again
             __syncthreads();
-            CDA_TICK(7);  // best of the merged community
+            CDA_TICK(7);  // best of the merged community + map reset
         }
         if (sh_abort) { if (tid == 0) out[r] = 0.0; __syncthreads(); continue; }
 
@@ -693,7 +604,6 @@ int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
         GAPA_TRY(s->doubles.ensure(sizeof(double) * static_cast<size_t>(n) * slots));
         GAPA_TRY(s->e_id.ensure(sizeof(int32_t) * s->pool_cap * slots));
         GAPA_TRY(s->e_cnt.ensure(sizeof(int32_t) * s->pool_cap * slots));
-        GAPA_TRY(s->e_gain.ensure(sizeof(double) * s->pool_cap * slots));
         GAPA_TRY(s->status.ensure(2 * sizeof(int)));
         GAPA_CUDA_TRY(cudaMemsetAsync(s->status.ptr, 0, 2 * sizeof(int), stream));
 
@@ -715,7 +625,6 @@ int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
         A.best_gain = s->doubles.as<double>();
         A.e_id = s->e_id.as<int32_t>();
         A.e_cnt = s->e_cnt.as<int32_t>();
-        A.e_gain = s->e_gain.as<double>();
         A.status = s->status.as<int>();
         const size_t smem = pos_in_smem == 2 ? static_cast<size_t>(n) * 7 * sizeof(int32_t) : (pos_in_smem ? static_cast<size_t>(n) * sizeof(int32_t) : 0);
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_cda, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
@@ -734,7 +643,7 @@ int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
 void cda_free(gapa_cuda_ctx* ctx) {
     if (!ctx->cda) return;
     CdaScratch* s = ctx->cda;
-    for (DevBuf* b : {&s->gone, &s->ints, &s->doubles, &s->e_id, &s->e_cnt, &s->e_gain, &s->status}) b->release();
+    for (DevBuf* b : {&s->gone, &s->ints, &s->doubles, &s->e_id, &s->e_cnt, &s->status}) b->release();
     delete s;
     ctx->cda = nullptr;
 }

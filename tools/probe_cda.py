@@ -24,7 +24,7 @@ if hasattr(lib, "gapa_cuda_cda_phase_cycles") or True:
         fn(buf, 1)
         obj.evaluate_batch(pop[:1])
         fn(buf, 0)
-        names = ["argmax", "room+mark", "fold", "clear", "drop", "patch short", "patch long", "best(a)"]
+        names = ["argmax", "room+mark", "fold", "drop", "scan list(a)", "list work (short)", "list work (long)", "best(a)+map reset"]
         tot = sum(buf)
         print("phase cycles of one individual (CTA 0):", {n: f"{100 * v / tot:.1f}%" for n, v in zip(names, buf)}, f"total {tot / 1.965e6:.1f} ms")
     except AttributeError:
