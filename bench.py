@@ -49,6 +49,8 @@ WORKLOADS = {
                name="C3: LPA RA-AUC GA, Erdos-Renyi n=1e4 <d>=10 (m=50,277), 10% hidden, k=4525, pop 50"),
     "n1e5": dict(task="pc", graph=("ba", 100_000, 5, 1), rate=0.05, pop=4096, pc=0.6, pm=0.2,
                  name="C5 point: CND-PC, BA n=1e5 attach=5, k=5000, pop 4096"),
+    "n1e4": dict(task="pc", graph=("ba", 10_000, 5, 1), rate=0.05, pop=4096, pc=0.6, pm=0.2,
+                 name="C5 point: CND-PC, BA n=1e4 attach=5, k=500, pop 4096"),
 }
 TASK_ID = {"pc": 0, "mcn": 1, "cda": 2, "lpa": 3}
 

@@ -959,7 +959,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         s->interleave = env_int("GAPA_PC_INTERLEAVE", 8, 1, 64);
         s->mask_chunks = env_int("GAPA_PC_MASK_CHUNKS", 1, 1, 64);
         s->relabel = env_int("GAPA_PC_RELABEL", -1, -1, 1);  // -1 automatic, 0 never, 1 always (tests)
-        s->small_path = env_int("GAPA_PC_SMALL", 1, 0, 1);  // 0 forces the bit-sliced pipeline on small graphs (tests)
+        s->small_path = env_int("GAPA_PC_SMALL", 1, 0, 2);  // 0: never, 1: where it pays, 2: wherever it fits (tests)
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         // the shared-memory bitmap may use most of the SM (one CTA per individual)
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -977,7 +977,12 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
     }
     const int n = ctx->n;
     const int sm = ctx->sm_count;
-    if (n > 0 && n <= kSmallMaxN && s->small_path) {
+    // Measured crossover (tools/ab_small.sh): the per-individual kernel wins only where the bit-sliced pipeline
+    // is at its launch-latency floor (~0.08 ms): n = 1e3 0.04 vs 0.08 ms at any population; n = 3e3 equal up
+    // to 1024 individuals; n = 1e4 0.2-2.6 ms vs 0.1-0.17 ms.  GAPA_PC_SMALL=2 forces it wherever it fits (tests).
+    const bool small_fits = n > 0 && n <= kSmallMaxN;
+    const bool small_pays = n <= 2048 || (n <= 4096 && rows <= 1024);
+    if (small_fits && (s->small_path == 2 || (s->small_path == 1 && small_pays))) {
         const size_t smem = sizeof(int32_t) * (2 * static_cast<size_t>(n) + ((n + 31) >> 5) + 1);
         GAPA_TRY(s->counters.ensure(sizeof(PcCounters)));
         PcCounters* counters = s->counters.as<PcCounters>();

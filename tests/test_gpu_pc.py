@@ -11,7 +11,7 @@ pytestmark = pytest.mark.gpu
 def pc_path(request, monkeypatch):
     """Every case runs through both PC implementations: the shared-memory warp kernel that small
     graphs take by default, and the bit-sliced pipeline (forced here; the default above n = 16384)."""
-    monkeypatch.setenv("GAPA_PC_SMALL", "1" if request.param == "warp-per-individual" else "0")
+    monkeypatch.setenv("GAPA_PC_SMALL", "2" if request.param == "warp-per-individual" else "0")
     return request.param
 
 
