@@ -152,21 +152,21 @@ static constexpr int kPerBlock = kGaThreads / kSplit;
 
 __global__ void __launch_bounds__(kGaThreads) k_ga_weights(const double* __restrict__ fitness, int s, int minimize,
                                                            double* __restrict__ weights, int* status) {
-    __shared__ double tile[kGaThreads];
+    __shared__ unsigned long long tile[kGaThreads];
     const int i = blockIdx.x * kPerBlock + threadIdx.x / kSplit, part = threadIdx.x % kSplit;
-    const double mine = i < s ? fitness[i] : 0.0;
-    if (i < s && !isfinite(mine)) *status = GAPA_CUDA_E_NAN;
+    const double mine_f = i < s ? fitness[i] : 0.0;
+    if (i < s && !isfinite(mine_f)) *status = GAPA_CUDA_E_NAN;
+    const unsigned long long mine = order_key(mine_f, minimize);
     int less = 0, leq = 0;
     for (int t0 = 0; t0 < s; t0 += kGaThreads) {
         __syncthreads();
-        if (t0 + threadIdx.x < s) tile[threadIdx.x] = fitness[t0 + threadIdx.x];
+        if (t0 + threadIdx.x < s) tile[threadIdx.x] = order_key(fitness[t0 + threadIdx.x], minimize);
         __syncthreads();
         const int lim = min(kGaThreads, s - t0);
         for (int t = part; t < lim; t += kSplit) {
-            const double other = tile[t];
-            const bool b = better(other, mine, minimize);
-            less += b;
-            leq += b || other == mine;
+            const unsigned long long other = tile[t];
+            less += other < mine;
+            leq += other <= mine;
         }
     }
     for (int off = kSplit / 2; off; off >>= 1) {
@@ -268,21 +268,22 @@ __global__ void __launch_bounds__(1024) k_ga_select_small(const double* __restri
 __global__ void __launch_bounds__(kGaThreads) k_ga_elite_rank(const double* __restrict__ fit, const double* __restrict__ fit_m,
                                                               int s, int minimize, int32_t* __restrict__ src_of_rank,
                                                               int* status) {
-    __shared__ double tile[kGaThreads];
+    __shared__ unsigned long long tile[kGaThreads];
     const int x = blockIdx.x * kPerBlock + threadIdx.x / kSplit, part = threadIdx.x % kSplit;
     const int total = 2 * s;
-    const double mine = x < total ? (x < s ? fit[x] : fit_m[x - s]) : 0.0;
-    if (x < total && isnan(mine)) *status = GAPA_CUDA_E_NAN;
+    const double mine_f = x < total ? (x < s ? fit[x] : fit_m[x - s]) : 0.0;
+    if (x < total && isnan(mine_f)) *status = GAPA_CUDA_E_NAN;
+    const unsigned long long mine = order_key(mine_f, minimize);
     int rank = 0;
     for (int t0 = 0; t0 < total; t0 += kGaThreads) {
         __syncthreads();
         const int y = t0 + threadIdx.x;
-        if (y < total) tile[threadIdx.x] = y < s ? fit[y] : fit_m[y - s];
+        if (y < total) tile[threadIdx.x] = order_key(y < s ? fit[y] : fit_m[y - s], minimize);
         __syncthreads();
         const int lim = min(kGaThreads, total - t0);
         for (int t = part; t < lim; t += kSplit) {
-            const double other = tile[t];
-            rank += better(other, mine, minimize) || (other == mine && t0 + t < x);
+            const unsigned long long other = tile[t];
+            rank += (other < mine) | ((other == mine) & (t0 + t < x));
         }
     }
     for (int off = kSplit / 2; off; off >>= 1) rank += __shfl_down_sync(0xffffffffu, rank, off, kSplit);

@@ -104,6 +104,17 @@ __device__ __forceinline__ bool draw_bernoulli(uint64_t key, uint64_t j, uint64_
     return (draw_u64(key, j) >> 11) < threshold;
 }
 
+// Order-preserving 64-bit key of a fitness value: key(x) < key(y)  <=>  x is BETTER than y (direction folded
+// in), key(x) == key(y) <=> x == y (-0.0 and +0.0 share a key).  The O(s^2) counting kernels of selection and
+// elitism compare these integers instead of doubles (two integer instructions per compare instead of FP64
+// set-predicates and a direction select).  NaN is reported separately and never ranked.
+__device__ __forceinline__ unsigned long long order_key(double x, int minimize) {
+    if (x == 0.0) x = 0.0;
+    const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+    const unsigned long long k = (b >> 63) ? ~b : (b | 0x8000000000000000ull);  // ascending with x
+    return minimize ? k : ~k;
+}
+
 // ---- gene matrix view -----------------------------------------------------------------
 // Row r of a batch lives at base + slot[r] * cols (slot == nullptr: the dense row-major matrix of
 // population.hpp:12-40).  The in-library generation loop keeps parents and children in one pool of

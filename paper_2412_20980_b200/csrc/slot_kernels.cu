@@ -69,22 +69,22 @@ __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_variation(VariationPa
 static constexpr int kSplit = 8;
 __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_rank(const double* __restrict__ fit, const double* __restrict__ fit_m,
                                                                 int s, int minimize, int32_t* __restrict__ order, int* status) {
-    __shared__ double tile[kSlotThreads];
+    __shared__ unsigned long long tile[kSlotThreads];
     const int x = blockIdx.x * (kSlotThreads / kSplit) + threadIdx.x / kSplit, part = threadIdx.x % kSplit;
     const int total = 2 * s;
-    const double mine = x < total ? (x < s ? fit[x] : fit_m[x - s]) : 0.0;
-    if (x < total && isnan(mine)) *status = GAPA_CUDA_E_NAN;
+    const double mine_f = x < total ? (x < s ? fit[x] : fit_m[x - s]) : 0.0;
+    if (x < total && isnan(mine_f)) *status = GAPA_CUDA_E_NAN;
+    const unsigned long long mine = order_key(mine_f, minimize);  // integer compares (internal.cuh)
     int rank = 0;
     for (int t0 = 0; t0 < total; t0 += kSlotThreads) {
         __syncthreads();
         const int y = t0 + threadIdx.x;
-        if (y < total) tile[threadIdx.x] = y < s ? fit[y] : fit_m[y - s];
+        if (y < total) tile[threadIdx.x] = order_key(y < s ? fit[y] : fit_m[y - s], minimize);
         __syncthreads();
         const int lim = min(kSlotThreads, total - t0);
         for (int t = part; t < lim; t += kSplit) {
-            const double other = tile[t];
-            const bool before = minimize ? other < mine : other > mine;
-            rank += before || (other == mine && t0 + t < x);
+            const unsigned long long other = tile[t];
+            rank += (other < mine) | ((other == mine) & (t0 + t < x));
         }
     }
     for (int off = kSplit / 2; off; off >>= 1) rank += __shfl_down_sync(0xffffffffu, rank, off, kSplit);
