@@ -69,7 +69,7 @@ struct PcScratch {
     DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters, pass_flags, block_done;
     DevBuf left_v, left_g, left_w, left_base, parent, comp_size, pc_extra, mcn_extra;
     size_t cap_entries = 0, cap_slots = 0;
-    int prefix = 32768, interleave = 8, mask_chunks = 1, small_path = 1, relabel = -1;
+    int prefix = 32768, interleave = 8, mask_chunks = 1, small_path = 1, relabel = -1, prefix_first4 = 1;
     // hub-first internal vertex order for the bit-sliced path (see ensure_order)
     DevBuf ord_row_ptr, ord_col_idx, ord_gene_map;
     DevBuf nbr4;  // int4 per vertex: the first four entries of its (ascending) row, -1 padded — see gather_first4
@@ -439,8 +439,8 @@ __device__ __forceinline__ Rec gather_first4(const int32_t* __restrict__ row_ptr
 // cluster-wide barriers between passes — no host round trip, no cooperative launch.  The
 // in-flight window is the cluster, so a pass propagates almost like a sequential scan.
 __global__ void __cluster_dims__(kPrefixCluster, 1, 1) __launch_bounds__(kPrefixThreads)
-    k_pc_prefix(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx, int n, int prefix,
-                const word_t* __restrict__ alive, Rec* reached, int* pass_flags) {
+    k_pc_prefix(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx, const int4* __restrict__ nbr4,
+                int first4_only, int n, int prefix, const word_t* __restrict__ alive, Rec* reached, int* pass_flags) {
     cg::cluster_group cluster = cg::this_cluster();
     const int sg = blockIdx.x / kPrefixCluster;
     const int lane_in_cluster = (blockIdx.x % kPrefixCluster) * kPrefixThreads + threadIdx.x;
@@ -465,7 +465,21 @@ __global__ void __cluster_dims__(kPrefixCluster, 1, 1) __launch_bounds__(kPrefix
                 // still-unreached younger neighbours serially.  Exactness does not depend on this
                 // kernel (the sweeps and phase 2 finish), only the speed of what follows does.
                 bool cut = false;
-                const Rec got = gather_reached(row_ptr, col_idx, reached_sg, v, limit, todo, 12 + 4 * pass, &cut);
+                Rec got{};
+                if (first4_only) {
+                    // the four lowest neighbours only: in a hub-first order these are the vertex's links towards
+                    // the core, which is where reachability arrives from; whatever this misses (a vertex reached
+                    // only through younger neighbours) is left to the full sweeps and phase 2
+                    const int4 f = __ldg(&nbr4[v]);
+                    const int u[4] = {f.x, f.y, f.z, f.w};
+#pragma unroll
+                    for (int t = 0; t < 4; ++t)
+                        if (u[t] >= 0 && u[t] < limit) rec_or(got, load_rec(&reached_sg[u[t]]));
+#pragma unroll
+                    for (int i = 0; i < kPack; ++i) got.w[i] &= todo.w[i];
+                } else {
+                    got = gather_reached(row_ptr, col_idx, reached_sg, v, limit, todo, 12 + 4 * pass, &cut);
+                }
                 if (rec_any(got)) {
                     rec_or(mine, got);
                     store_rec(&reached_sg[v], mine);
@@ -966,6 +980,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
         s->overlap_clear = env_int("GAPA_PC_OVERLAP_CLEAR", 1, 0, 1);
+        s->prefix_first4 = env_int("GAPA_PC_PREFIX_FIRST4", 1, 0, 1);  // 0: scan whole (bounded) rows in the prefix closure
         {  // lowest priority: the clear yields to every kernel of the work stream
             int least = 0, greatest = 0;
             GAPA_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
@@ -1087,8 +1102,8 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             if (prefix > 0) {
                 GAPA_TRY(s->pass_flags.ensure(sizeof(int) * 64 * sgroups));
                 GAPA_CUDA_TRY(cudaMemsetAsync(s->pass_flags.ptr, 0, sizeof(int) * 64 * sgroups, stream));
-                GAPA_LAUNCH(k_pc_prefix, sgroups * kPrefixCluster, kPrefixThreads, 0, stream, g_row_ptr, g_col_idx, n,
-                            prefix, alive_rec, reached_rec, s->pass_flags.as<int>());
+                GAPA_LAUNCH(k_pc_prefix, sgroups * kPrefixCluster, kPrefixThreads, 0, stream, g_row_ptr, g_col_idx,
+                            s->nbr4.as<int4>(), s->prefix_first4, n, prefix, alive_rec, reached_rec, s->pass_flags.as<int>());
             }
             const int il = std::min(std::max(1, s->interleave / kPack), sgroups);
             const dim3 grid(((n + kThreads - 1) / kThreads) * il, (sgroups + il - 1) / il);
