@@ -63,6 +63,7 @@ struct PcCounters {
     int range_error;
     int changed;  // any sweep since the last reset set a new reached bit
     unsigned int n_incomplete;  // 256-vertex chunks the recording sweep still has to visit
+    int deferred;  // the recording sweep declined to run: too much is still unreached and the sweeps still progress
 };
 
 struct PcScratch {
@@ -519,6 +520,7 @@ struct SweepArgs {
     PcCounters* counters;
     int2* incomplete;  // (super-group, chunk) list written by the ordinary sweep, read by the recording one
     int record;        // ordinary sweep: append incomplete chunks to the list
+    unsigned defer_above;  // recording sweep: with more incomplete chunks than this (and progress) sweep again instead
 };
 
 template <bool FINAL>
@@ -620,6 +622,13 @@ __global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep(Sw
 __global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_record(SweepArgs A) {
     __shared__ int hist[kPack * kBits];
     const unsigned total = A.counters->n_incomplete;
+    // Recording is for the last few percent: per leftover vertex it costs a shared-memory atomic per unreached
+    // individual plus compaction.  On graphs without a hub core one sweep leaves most of the graph unreached
+    // (24 ms of recording at n = 1e6, Erdos-Renyi) — more sweeps first, as long as they still make progress.
+    if (total > A.defer_above && A.counters->changed) {
+        if (blockIdx.x == 0 && threadIdx.x == 0) A.counters->deferred = 1;
+        return;
+    }
     for (unsigned i = blockIdx.x; i < total; i += gridDim.x) {
         const int2 item = A.incomplete[i];
         __syncthreads();  // hist of the previous chunk has been flushed
@@ -770,6 +779,7 @@ __global__ void k_pc_reset(int groups, int32_t* parent, int32_t* comp_size, int*
         counters->overflow = 0;
         counters->changed = 0;
         counters->n_incomplete = 0u;
+        counters->deferred = 0;
         if (first) counters->range_error = 0;
     }
 }
@@ -1115,6 +1125,8 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             A.left_w = s->left_w.as<word_t>(); A.left_base = s->left_base.as<int32_t>(); A.parent = s->parent.as<int32_t>();
             A.comp_size = s->comp_size.as<int32_t>(); A.slot0 = slot0; A.counters = counters;
             A.incomplete = s->block_done.as<int2>(); A.record = 0;
+            const unsigned all_chunks = static_cast<unsigned>(sgroups) * static_cast<unsigned>((n + kThreads - 1) / kThreads);
+            A.defer_above = all_chunks / 8;
             auto sweep = [&](bool final_pass, bool record) -> int {
                 A.cap_entries = static_cast<unsigned>(s->cap_entries);  // may have grown after an overflow retry
                 A.cap_slots = static_cast<unsigned>(s->cap_slots);
@@ -1135,12 +1147,13 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             for (int round = 0;; ++round) {
                 const int ordinary = round == 0 ? 1 : 2;
                 for (int i = 0; i < ordinary; ++i) GAPA_TRY(sweep(false, i + 1 == ordinary));
+                if (round >= 47) A.defer_above = ~0u;  // bounded: the last round records whatever is left
                 GAPA_TRY(sweep(true, false));
                 GAPA_CUDA_TRY(cudaMemcpyAsync(&h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
                 GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
                 if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
                 const bool retry_bigger = h.overflow != 0;
-                const bool keep_sweeping = h.changed && h.n_entries > many && round < 48;
+                const bool keep_sweeping = h.deferred || (h.changed && h.n_entries > many && round < 48);
                 if (!retry_bigger && !keep_sweeping) break;
                 if (retry_bigger)
                     GAPA_TRY(ensure_phase2(s, pgroups, std::max<size_t>(s->cap_entries, static_cast<size_t>(h.n_entries) + 1024),

@@ -145,3 +145,21 @@ def test_shuffled_labels_use_the_hub_first_internal_order(gp, oracle, cuda_devic
         obj = gp.PairwiseConnectivityObjective(g, gp.GenePool(gp.PoolKind.NodeRemoval, sub))
         genes = rng.integers(0, len(sub), size=(9, 300)).astype(np.int32)
         assert np.array_equal(obj.evaluate_batch(genes), oracle.eval_batch(og, 0, sub[genes]))
+
+
+def test_sparse_random_graphs_without_a_hub_core(gp, oracle, cuda_device, monkeypatch):
+    """Erdos-Renyi graphs near the percolation threshold: one sweep leaves most of the graph unreached, the
+    recording sweep defers itself and more sweep rounds run before phase 2 — same integers as the oracle."""
+    monkeypatch.setenv("GAPA_PC_SMALL", "0")
+    rng = np.random.default_rng(5)
+    for n, deg, rows in ((40_000, 3.0, 70), (25_000, 1.6, 130), (60_000, 4.5, 64)):
+        e = rng.integers(0, n, (int(n * deg / 2), 2)).astype(np.int32)
+        e = e[e[:, 0] != e[:, 1]]
+        e.sort(axis=1)
+        e = np.unique(e, axis=0)
+        g = gp.Graph(n, e)
+        og = oracle.graph_from_edges(n, e)
+        pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+        batch = gp.init_population(pool.size(), rows, n // 20, 3)
+        for task, cls in ((0, gp.PairwiseConnectivityObjective), (1, gp.SixDstObjective)):
+            assert np.array_equal(cls(g, pool).evaluate_batch(batch), oracle.eval_batch(og, task, batch, threads=8)), (n, task)
