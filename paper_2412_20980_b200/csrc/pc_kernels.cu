@@ -70,7 +70,7 @@ struct PcScratch {
     DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters, pass_flags, block_done;
     DevBuf left_v, left_g, left_w, left_base, parent, comp_size, pc_extra, mcn_extra;
     size_t cap_entries = 0, cap_slots = 0;
-    int prefix = 32768, interleave = 8, mask_chunks = 1, small_path = 1, relabel = -1, prefix_first4 = 1;
+    int prefix = 32768, interleave = 8, mask_chunks = 1, small_path = 1, relabel = -1, prefix_first4 = 1, trace = 0;
     // hub-first internal vertex order for the bit-sliced path (see ensure_order)
     DevBuf ord_row_ptr, ord_col_idx, ord_gene_map;
     DevBuf nbr4;  // int4 per vertex: the first four entries of its (ascending) row, -1 padded — see gather_first4
@@ -521,6 +521,7 @@ struct SweepArgs {
     int2* incomplete;  // (super-group, chunk) list written by the ordinary sweep, read by the recording one
     int record;        // ordinary sweep: append incomplete chunks to the list
     unsigned defer_above;  // recording sweep: with more incomplete chunks than this (and progress) sweep again instead
+    int descending;        // ordinary sweep: blocks walk the vertex chunks from the highest id down
 };
 
 template <bool FINAL>
@@ -615,7 +616,51 @@ __device__ __forceinline__ void sweep_chunk(const SweepArgs& A, int sg, int chun
 __global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep(SweepArgs A) {
     const int sg = blockIdx.y * A.interleave + (blockIdx.x % A.interleave);
     if (sg >= A.sgroups) return;
-    sweep_chunk<false>(A, sg, blockIdx.x / A.interleave, nullptr);
+    const int chunk = blockIdx.x / A.interleave;
+    sweep_chunk<false>(A, sg, A.descending ? (A.n + kThreads - 1) / kThreads - 1 - chunk : chunk, nullptr);
+}
+
+// Sweep of the EXTRA rounds (one ordered sweep was not enough: no hub core, or a large diameter).  Inside a
+// block all 256 vertices are processed at the same time, so along a path of consecutive ids reachability
+// advances one hop per sweep; here a block repeats its chunk until nothing in it changes (the threads keep
+// their records in registers and only re-gather what is still missing), which lets a chain of any length
+// inside a chunk close in one launch.  Rings and grids: 48 rounds -> a few.
+__global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep_local(SweepArgs A) {
+    const int sg = blockIdx.y * A.interleave + (blockIdx.x % A.interleave);
+    if (sg >= A.sgroups) return;
+    const int slot = blockIdx.x / A.interleave;
+    const int chunk = A.descending ? (A.n + kThreads - 1) / kThreads - 1 - slot : slot;
+    const int v = chunk * kThreads + threadIdx.x;
+    const bool valid = v < A.n;
+    const size_t base = static_cast<size_t>(sg) * A.n;
+    int4 first = make_int4(-1, -1, -1, -1);
+    Rec mine{}, todo{};
+    if (valid) {
+        first = __ldg(&A.nbr4[v]);
+        mine = load_rec(&A.reached[base + v]);
+        const Rec al = load_alive(A.alive, sg, A.n, v);
+#pragma unroll
+        for (int i = 0; i < kPack; ++i) todo.w[i] = al.w[i] & ~mine.w[i];
+    }
+    int any = 0;
+    for (int it = 0; it < 64; ++it) {
+        int gained = 0;
+        if (valid && rec_any(todo)) {
+            const Rec got = gather_first4(A.row_ptr, A.col_idx, A.reached + base, v, first, todo);
+            if (rec_any(got)) {
+                rec_or(mine, got);
+                store_rec(&A.reached[base + v], mine);
+#pragma unroll
+                for (int i = 0; i < kPack; ++i) todo.w[i] &= ~got.w[i];
+                gained = 1;
+                any = 1;
+            }
+        }
+        if (!__syncthreads_or(gained)) break;
+    }
+    if (__syncthreads_or(any) && threadIdx.x == 0) A.counters->changed = 1;
+    const int left = __syncthreads_or(valid && rec_any(todo));
+    if (left && A.record && threadIdx.x == 0) A.incomplete[atomicAdd(&A.counters->n_incomplete, 1u)] = make_int2(sg, chunk);
 }
 
 // recording sweep: a persistent grid walks the list of incomplete chunks
@@ -990,6 +1035,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
         s->overlap_clear = env_int("GAPA_PC_OVERLAP_CLEAR", 1, 0, 1);
+        s->trace = env_int("GAPA_PC_TRACE", 0, 0, 1);  // one stderr line per sweep round
         s->prefix_first4 = env_int("GAPA_PC_PREFIX_FIRST4", 1, 0, 1);  // 0: scan whole (bounded) rows in the prefix closure
         {  // lowest priority: the clear yields to every kernel of the work stream
             int least = 0, greatest = 0;
@@ -1124,16 +1170,18 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             A.entry_of = s->entry_of.as<int32_t>(); A.left_v = s->left_v.as<int32_t>(); A.left_g = s->left_g.as<int32_t>();
             A.left_w = s->left_w.as<word_t>(); A.left_base = s->left_base.as<int32_t>(); A.parent = s->parent.as<int32_t>();
             A.comp_size = s->comp_size.as<int32_t>(); A.slot0 = slot0; A.counters = counters;
-            A.incomplete = s->block_done.as<int2>(); A.record = 0;
+            A.incomplete = s->block_done.as<int2>(); A.record = 0; A.descending = 0;
             const unsigned all_chunks = static_cast<unsigned>(sgroups) * static_cast<unsigned>((n + kThreads - 1) / kThreads);
             A.defer_above = all_chunks / 8;
-            auto sweep = [&](bool final_pass, bool record) -> int {
+            auto sweep = [&](bool final_pass, bool record, bool descending = false, bool local = false) -> int {
+                A.descending = descending ? 1 : 0;
                 A.cap_entries = static_cast<unsigned>(s->cap_entries);  // may have grown after an overflow retry
                 A.cap_slots = static_cast<unsigned>(s->cap_slots);
                 A.left_v = s->left_v.as<int32_t>(); A.left_g = s->left_g.as<int32_t>(); A.left_w = s->left_w.as<word_t>();
                 A.left_base = s->left_base.as<int32_t>(); A.parent = s->parent.as<int32_t>(); A.comp_size = s->comp_size.as<int32_t>();
                 A.record = record ? 1 : 0;
                 if (final_pass) GAPA_LAUNCH(k_pc_record, sm * 4, kThreads, 0, stream, A);
+                else if (local) GAPA_LAUNCH(k_pc_sweep_local, grid, kThreads, 0, stream, A);
                 else GAPA_LAUNCH(k_pc_sweep, grid, kThreads, 0, stream, A);
                 return GAPA_CUDA_OK;
             };
@@ -1145,13 +1193,21 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             const unsigned many = static_cast<unsigned>(std::max<size_t>(8192, words / 512));
             PcCounters h{};
             for (int round = 0;; ++round) {
+                // extra rounds: one sweep in DESCENDING block order, then an ascending one; from the fifth round on
+                // (random graphs converge before that; what is left has a large diameter) each block iterates its
+                // chunk to a local fixpoint (k_pc_sweep_local).  Across blocks reachability runs any distance along
+                // ids in the direction the blocks are scheduled but only one hop against it: high-diameter graphs
+                // (rings, grids) need both directions to converge in a few rounds.
                 const int ordinary = round == 0 ? 1 : 2;
-                for (int i = 0; i < ordinary; ++i) GAPA_TRY(sweep(false, i + 1 == ordinary));
+                for (int i = 0; i < ordinary; ++i) GAPA_TRY(sweep(false, i + 1 == ordinary, ordinary == 2 && i == 0, round >= 4));
                 if (round >= 47) A.defer_above = ~0u;  // bounded: the last round records whatever is left
                 GAPA_TRY(sweep(true, false));
                 GAPA_CUDA_TRY(cudaMemcpyAsync(&h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
                 GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
                 if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
+                if (s->trace)
+                    std::fprintf(stderr, "pc_eval round %d: entries %u slots %u overflow %d changed %d incomplete %u deferred %d (cap %zu / %zu)\n",
+                                 round, h.n_entries, h.n_slots, h.overflow, h.changed, h.n_incomplete, h.deferred, s->cap_entries, s->cap_slots);
                 const bool retry_bigger = h.overflow != 0;
                 const bool keep_sweeping = h.deferred || (h.changed && h.n_entries > many && round < 48);
                 if (!retry_bigger && !keep_sweeping) break;

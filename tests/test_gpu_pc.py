@@ -163,3 +163,22 @@ def test_sparse_random_graphs_without_a_hub_core(gp, oracle, cuda_device, monkey
         batch = gp.init_population(pool.size(), rows, n // 20, 3)
         for task, cls in ((0, gp.PairwiseConnectivityObjective), (1, gp.SixDstObjective)):
             assert np.array_equal(cls(g, pool).evaluate_batch(batch), oracle.eval_batch(og, task, batch, threads=8)), (n, task)
+
+
+def test_high_diameter_graphs(gp, oracle, cuda_device, monkeypatch):
+    """Rings and grids: reachability needs many sweep rounds (descending + ascending, blocks iterating their chunk
+    to a local fixpoint) and a large phase 2 — there is no giant component after 5 % removals on a ring."""
+    monkeypatch.setenv("GAPA_PC_SMALL", "0")
+    n = 30_000
+    ring = np.stack([np.arange(n), (np.arange(n) + 1) % n], 1).astype(np.int32)
+    side = 140
+    idx = np.arange(side * side).reshape(side, side)
+    grid = np.concatenate([np.stack([idx[:, :-1].ravel(), idx[:, 1:].ravel()], 1),
+                           np.stack([idx[:-1].ravel(), idx[1:].ravel()], 1)]).astype(np.int32)
+    for name, nn, e, k in (("ring", n, ring, n // 20), ("ring, nothing removed", n, ring, 0), ("grid", side * side, grid, side * side // 10)):
+        g = gp.Graph(nn, e)
+        og = oracle.graph_from_edges(nn, e)
+        pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+        batch = gp.init_population(pool.size(), 70, k, 4) if k else np.zeros((3, 0), np.int32)
+        for task, cls in ((0, gp.PairwiseConnectivityObjective), (1, gp.SixDstObjective)):
+            assert np.array_equal(cls(g, pool).evaluate_batch(batch), oracle.eval_batch(og, task, batch, threads=8)), (name, task)
