@@ -153,9 +153,24 @@ __device__ __forceinline__ unsigned long long score_key(double x) {
 __global__ void __launch_bounds__(kLpaSortThreads) k_lpa_auc_sorted(const double* __restrict__ scores, int T, int P, int P2,
                                                                     unsigned long long* twice) {
     __shared__ unsigned long long warp_sum[kLpaSortThreads / 32];
+    __shared__ int n_nonzero;
     const int r = blockIdx.x, tid = threadIdx.x;
     const double* row = scores + static_cast<size_t>(r) * (T + P);
-    for (int i = tid; i < P2; i += kLpaSortThreads) lpa_keys[i] = i < P ? score_key(row[T + i]) : ~0ull;  // pads sort to the end
+    // In a sparse graph most pairs have no common neighbour: their score is exactly 0.  Only the non-zero probe
+    // scores are compacted and sorted; the zeros are a count.  (A pair score is a sum of positive terms: never < 0.)
+    if (tid == 0) n_nonzero = 0;
+    __syncthreads();
+    for (int i = tid; i < P; i += kLpaSortThreads) {
+        const double x = row[T + i];
+        if (x != 0.0) lpa_keys[atomicAdd(&n_nonzero, 1)] = score_key(x);
+    }
+    __syncthreads();
+    const int nz = n_nonzero, zeros = P - nz;
+    const unsigned long long zero_key = score_key(0.0);
+    P = nz;
+    P2 = 2;
+    while (P2 < P) P2 <<= 1;
+    for (int i = P + tid; i < P2; i += kLpaSortThreads) lpa_keys[i] = ~0ull;  // pads sort to the end
     __syncthreads();
     for (int k = 2; k <= P2; k <<= 1)
         for (int j = k >> 1; j > 0; j >>= 1) {
@@ -179,13 +194,16 @@ __global__ void __launch_bounds__(kLpaSortThreads) k_lpa_auc_sorted(const double
             const int mid = (lo + hi) >> 1;
             if (lpa_keys[mid] < key) lo = mid + 1; else hi = mid;
         }
-        const int below = lo;
+        int below = lo;
         hi = P;  // first index with keys[idx] > key
         while (lo < hi) {
             const int mid = (lo + hi) >> 1;
             if (lpa_keys[mid] <= key) lo = mid + 1; else hi = mid;
         }
-        acc += 2ull * static_cast<unsigned long long>(below) + static_cast<unsigned long long>(lo - below);
+        int equal = lo - below;
+        if (key > zero_key) below += zeros;        // every zero probe score is below a positive test score
+        else if (key == zero_key) equal += zeros;  // ... and ties with a zero one
+        acc += 2ull * static_cast<unsigned long long>(below) + static_cast<unsigned long long>(equal);
     }
     for (int off = 16; off; off >>= 1) acc += __shfl_down_sync(0xffffffffu, acc, off);
     if ((tid & 31) == 0) warp_sum[tid >> 5] = acc;
