@@ -151,7 +151,8 @@ __device__ __forceinline__ unsigned long long score_key(double x) {
 }
 
 __global__ void __launch_bounds__(kLpaSortThreads) k_lpa_auc_sorted(const double* __restrict__ scores, int T, int P, int P2,
-                                                                    unsigned long long* twice) {
+                                                                    double* __restrict__ out) {
+    const int all_probes = P;
     __shared__ unsigned long long warp_sum[kLpaSortThreads / 32];
     __shared__ int n_nonzero;
     const int r = blockIdx.x, tid = threadIdx.x;
@@ -211,7 +212,8 @@ __global__ void __launch_bounds__(kLpaSortThreads) k_lpa_auc_sorted(const double
     if (tid == 0) {
         unsigned long long total = 0ull;
         for (int w = 0; w < kLpaSortThreads / 32; ++w) total += warp_sum[w];
-        twice[r] = total;
+        const double wins = static_cast<double>(total) / 2.0;
+        out[r] = wins / (static_cast<double>(T) * static_cast<double>(all_probes));  // link_prediction.cpp:96
     }
 }
 
@@ -248,7 +250,6 @@ int lpa_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
     for (int r0 = 0; r0 < rows; r0 += chunk) {
         const int cr = std::min(chunk, rows - r0);
         GAPA_CUDA_TRY(cudaMemsetAsync(s->gone.ptr, 0, sizeof(unsigned) * mask_words * static_cast<size_t>(cr), stream));
-        GAPA_CUDA_TRY(cudaMemsetAsync(s->twice.ptr, 0, sizeof(unsigned long long) * cr, stream));
         if (n > 0) GAPA_LAUNCH(k_lpa_init, sm * 8, kLpaThreads, 0, stream, ctx->d_row_ptr, n, cr, s->deg.as<int32_t>());
         const size_t cells = static_cast<size_t>(cr) * cols;
         if (cells) {
@@ -264,8 +265,11 @@ int lpa_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
         while (P2 < P) P2 <<= 1;
         if (P > 0 && s->sorted_auc && sizeof(unsigned long long) * static_cast<size_t>(P2) <= 200 * 1024) {
             GAPA_LAUNCH(k_lpa_auc_sorted, cr, kLpaSortThreads, sizeof(unsigned long long) * P2, stream, s->scores.as<double>(), T, P, P2,
-                        s->twice.as<unsigned long long>());
-        } else if (P > 0)  // probe set too large for shared memory: the exact T x P grid
+                        out_dev + r0);  // writes the AUC itself
+            continue;
+        }
+        GAPA_CUDA_TRY(cudaMemsetAsync(s->twice.ptr, 0, sizeof(unsigned long long) * cr, stream));
+        if (P > 0)  // probe set too large for shared memory: the exact T x P grid
             GAPA_LAUNCH(k_lpa_auc, dim3((T + kLpaThreads - 1) / kLpaThreads, cr), kLpaThreads, 0, stream,
                         s->scores.as<double>(), T, P, s->twice.as<unsigned long long>());
         GAPA_LAUNCH(k_lpa_final, (cr + 255) / 256, 256, 0, stream, s->twice.as<unsigned long long>(), cr, T, P, out_dev + r0);
