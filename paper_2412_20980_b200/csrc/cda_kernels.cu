@@ -32,6 +32,7 @@
 // merges into a < b; Q is accumulated sequentially in ascending community id, which
 // is first-appearance order (community.cpp:17-26).
 #include <algorithm>
+#include <cstdlib>
 #include <type_traits>
 
 #include "internal.cuh"
@@ -56,6 +57,7 @@ struct CdaScratch {
     DevBuf gone, ints, doubles, e_id, e_cnt, status;
     size_t pool_cap = 0;
     int slots = 0;
+    int hier_argmax = 1;  // GAPA_CDA_HIER=0: flat scan of the cached bests (tests run both)
 };
 
 struct CdaArgs {
@@ -110,13 +112,15 @@ __device__ __forceinline__ double merge_gain(int edges, int da, int db, double m
 // other entry of list(c) keeps its gain (deg(c), deg(d) and e(c, d) are untouched by the merge), the entry of
 // b is gone and was not the best, so only the patched (c, a) entry can displace the cached best — O(1), no
 // second scan of the list.  Same result as a fresh scan: the order of candidates is total.
-__device__ __forceinline__ void refresh_best_unchanged(double* best_gain, int32_t* best_id, int c, int old_best, int a, double gn) {
+__device__ __forceinline__ void refresh_best_unchanged(double* best_gain, int32_t* best_id, int32_t* dirty, int c, int old_best, int a,
+                                                       double gn) {
     if (a > c && gn > 0.0) {
         const Cand cur{old_best >= 0 ? best_gain[c] : 0.0, c, old_best};
         const Cand x{gn, c, a};
         if (cand_better(x, cur)) {
             best_gain[c] = gn;
             best_id[c] = a;
+            if (dirty) dirty[c >> 5] = 1;
         }
     }
 }
@@ -149,7 +153,7 @@ extern "C" int gapa_cuda_cda_phase_cycles(unsigned long long* out8, int reset) {
 
 __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows genes, int rows,
                                                         int pos_in_smem, double* __restrict__ out,
-                                                        int32_t* __restrict__ owner_out) {
+                                                        int32_t* __restrict__ owner_out, int hier_off) {
     __shared__ Cand warp_cand[kCdaWarps];
     __shared__ Cand chosen;
     __shared__ long long sh_total;
@@ -183,6 +187,15 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
     }
     int32_t* e_id = A.e_id + slot * A.pool_cap;
     int32_t* e_cnt = A.e_cnt + slot * A.pool_cap;
+    // Two-level argmax over the cached bests: communities in groups of 32, one cached maximum per group,
+    // recomputed only for the groups whose members changed their cached best in the last merge step (a, b
+    // and the ~20 communities that got list work) — instead of all 1024 threads scanning all n every step.
+    const bool hier = hier_off >= 0;
+    const int n_groups = (n + 31) >> 5;
+    double* gmax_gain = reinterpret_cast<double*>(reinterpret_cast<unsigned char*>(cda_smem) + (hier ? hier_off : 0));
+    int32_t* gmax_a = reinterpret_cast<int32_t*>(gmax_gain + n_groups);
+    int32_t* gmax_b = gmax_a + n_groups;
+    int32_t* dirty = gmax_b + n_groups;
     int32_t* pos = pos_in_smem == 2 ? cda_smem + 6 * static_cast<size_t>(n) : (pos_in_smem ? cda_smem : A.pos_global + slot * n);
 
     for (int r = blockIdx.x; r < rows; r += gridDim.x) {
@@ -289,6 +302,8 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         const double den = 2.0 * m * m;
         if (tid == 0) sh_pool_top = adding ? total_degree : A.csr_slots;
 
+        if (hier)
+            for (int g2 = tid; g2 < n_groups; g2 += kCdaThreads) dirty[g2] = 1;
         // initial cached bests
         for (int u = tid; u < n; u += kCdaThreads) {
             const int h = head[u], l = len[u], du = cdeg[u];
@@ -351,7 +366,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             // the leader alone reads the cached best (it is also the one that rewrites it) and tells the group
             const int old_best = __shfl_sync(gmask, gl == 0 ? best_id[c] : 0, leader);
             if (old_best != a && old_best != b) {
-                if (gl == 0) refresh_best_unchanged(best_gain, best_id, c, old_best, a, gn);
+                if (gl == 0) refresh_best_unchanged(best_gain, best_id, hier ? dirty : nullptr, c, old_best, a, gn);
                 return;
             }
             __syncwarp(gmask);  // the leader's patch is visible to the group
@@ -377,6 +392,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             if (gl == 0) {
                 best_gain[c] = best_c.gain;
                 best_id[c] = best_c.b;
+                if (hier) dirty[c >> 5] = 1;
             }
         };
 
@@ -385,23 +401,48 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         long long t_phase = clock64();
 #endif
         for (;;) {
-            Cand mine{0.0, -1, -1};
-            for (int c = tid; c < n; c += kCdaThreads) {
-                const int b = best_id[c];
-                if (b >= 0) {
-                    const Cand x{best_gain[c], c, b};
-                    if (cand_better(x, mine)) mine = x;
+            if (hier) {
+                for (int g2 = warp; g2 < n_groups; g2 += kCdaWarps) {
+                    if (!dirty[g2]) continue;  // uniform within the warp
+                    const int c = g2 * 32 + lane;
+                    Cand x{0.0, c, -1};
+                    if (c < n) {
+                        const int bb = best_id[c];
+                        if (bb >= 0) { x.gain = best_gain[c]; x.b = bb; }
+                    }
+                    x = cand_warp_best(x);
+                    if (lane == 0) { gmax_gain[g2] = x.gain; gmax_a[g2] = x.a; gmax_b[g2] = x.b; dirty[g2] = 0; }
                 }
+                __syncthreads();
+                if (warp == 0) {
+                    Cand x{0.0, -1, -1};
+                    for (int g2 = lane; g2 < n_groups; g2 += 32) {
+                        const Cand y{gmax_gain[g2], gmax_a[g2], gmax_b[g2]};
+                        if (cand_better(y, x)) x = y;
+                    }
+                    x = cand_warp_best(x);
+                    if (lane == 0) chosen = x;
+                }
+                __syncthreads();
+            } else {
+                Cand mine{0.0, -1, -1};
+                for (int c = tid; c < n; c += kCdaThreads) {
+                    const int b = best_id[c];
+                    if (b >= 0) {
+                        const Cand x{best_gain[c], c, b};
+                        if (cand_better(x, mine)) mine = x;
+                    }
+                }
+                mine = cand_warp_best(mine);
+                if (lane == 0) warp_cand[warp] = mine;
+                __syncthreads();
+                if (warp == 0) {
+                    Cand x = warp_cand[lane];
+                    x = cand_warp_best(x);
+                    if (lane == 0) chosen = x;
+                }
+                __syncthreads();
             }
-            mine = cand_warp_best(mine);
-            if (lane == 0) warp_cand[warp] = mine;
-            __syncthreads();
-            if (warp == 0) {
-                Cand x = warp_cand[lane];
-                x = cand_warp_best(x);
-                if (lane == 0) chosen = x;
-            }
-            __syncthreads();
             const int a = chosen.a, b = chosen.b;
             if (b < 0) break;
             CDA_TICK(0);  // argmax
@@ -463,6 +504,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                 len[b] = 0;
                 merged_into[b] = a;
                 best_id[b] = -1;
+                if (hier) dirty[b >> 5] = 1;
                 sh_work = 0;
                 sh_long = 0;
             }
@@ -525,7 +567,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             if (warp == 0) {
                 Cand x = warp_cand[lane];
                 x = cand_warp_best(x);
-                if (lane == 0) { best_gain[a] = x.gain; best_id[a] = x.b; }
+                if (lane == 0) { best_gain[a] = x.gain; best_id[a] = x.b; if (hier) dirty[a >> 5] = 1; }
             }
             for (int i = tid; i < la2; i += kCdaThreads) pos[e_id[ha + i]] = -1;  // the map is empty again
             __syncthreads();
@@ -591,6 +633,7 @@ int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
     CdaScratch* s = ctx->cda;
     const int n = ctx->n;
     if (n == 0) return fail(GAPA_CUDA_E_INVALID, "cda_fitness: empty graph");
+    if (const char* raw = std::getenv("GAPA_CDA_HIER")) s->hier_argmax = *raw != '0';
     const long long csr_slots = 2 * ctx->m;
     const bool adding = ctx->pool_kind == GAPA_POOL_EDGE_ADDITION;
     const int mask_words = static_cast<int>(((adding ? static_cast<int64_t>(ctx->pool_size) : ctx->m) + 31) / 32) + 1;
@@ -626,9 +669,15 @@ int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
         A.e_id = s->e_id.as<int32_t>();
         A.e_cnt = s->e_cnt.as<int32_t>();
         A.status = s->status.as<int>();
-        const size_t smem = pos_in_smem == 2 ? static_cast<size_t>(n) * 7 * sizeof(int32_t) : (pos_in_smem ? static_cast<size_t>(n) * sizeof(int32_t) : 0);
+        const size_t base_smem = pos_in_smem == 2 ? static_cast<size_t>(n) * 7 * sizeof(int32_t) : (pos_in_smem ? static_cast<size_t>(n) * sizeof(int32_t) : 0);
+        const size_t n_groups = (static_cast<size_t>(n) + 31) / 32;
+        const size_t hier_at = (base_smem + 7) & ~size_t{7};
+        const size_t hier_bytes = n_groups * (sizeof(double) + 3 * sizeof(int32_t));
+        const bool hier = s->hier_argmax && hier_at + hier_bytes <= 209 * 1024;  // 227 KB minus the kernel's static shared memory
+        const size_t smem = hier ? hier_at + hier_bytes : base_smem;
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_cda, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        GAPA_LAUNCH(k_cda, slots, kCdaThreads, smem, stream, A, genes, rows, pos_in_smem, out_dev, owner_out_dev);
+        GAPA_LAUNCH(k_cda, slots, kCdaThreads, smem, stream, A, genes, rows, pos_in_smem, out_dev, owner_out_dev,
+                    hier ? static_cast<int>(hier_at) : -1);
         GAPA_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, s->status.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
         GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
         if (ctx->h_status[0] == GAPA_CUDA_E_RANGE) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");

@@ -85,7 +85,9 @@ def test_cda_identities(gp, cuda_device):
         gp.ModularityAttackObjective(two_triangles, gp.build_gene_pool(two_triangles, gp.PoolKind.NodeRemoval))
 
 
-def test_cda_random_instances_exact(gp, oracle, cuda_device):
+@pytest.mark.parametrize("argmax", ["two-level", "flat"])
+def test_cda_random_instances_exact(gp, oracle, cuda_device, monkeypatch, argmax):
+    monkeypatch.setenv("GAPA_CDA_HIER", "1" if argmax == "two-level" else "0")  # both forms of the cached-best argmax
     rng = np.random.default_rng(4)
     for trial in range(25):
         n = int(rng.integers(6, 160))
