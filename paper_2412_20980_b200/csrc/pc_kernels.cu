@@ -64,6 +64,7 @@ struct PcCounters {
     int changed;  // any sweep since the last reset set a new reached bit
     unsigned int n_incomplete;  // 256-vertex chunks the recording sweep still has to visit
     int deferred;  // the recording sweep declined to run: too much is still unreached and the sweeps still progress
+    unsigned int n_left;  // (vertex, super-group) pairs with unreached individuals after the last ordinary sweep
 };
 
 struct PcScratch {
@@ -520,7 +521,7 @@ struct SweepArgs {
     PcCounters* counters;
     int2* incomplete;  // (super-group, chunk) list written by the ordinary sweep, read by the recording one
     int record;        // ordinary sweep: append incomplete chunks to the list
-    unsigned defer_above;  // recording sweep: with more incomplete chunks than this (and progress) sweep again instead
+    unsigned defer_above;  // recording sweep: with more (vertex, super-group) pairs left than this (and progress) sweep again instead
     int descending;        // ordinary sweep: blocks walk the vertex chunks from the highest id down
 };
 
@@ -604,11 +605,12 @@ __device__ __forceinline__ void sweep_chunk(const SweepArgs& A, int sg, int chun
         }
     }
     if (__syncthreads_or(any) && threadIdx.x == 0) counters->changed = 1;
-    const int left = __syncthreads_or(any_left);
+    const int left = __syncthreads_count(any_left);
     if (FINAL) {
         if (left && hist[threadIdx.x]) atomicAdd(&unreached[sg * kPack * kBits + threadIdx.x], hist[threadIdx.x]);
     } else if (left && A.record && threadIdx.x == 0) {
         A.incomplete[atomicAdd(&counters->n_incomplete, 1u)] = make_int2(sg, chunk);
+        atomicAdd(&counters->n_left, static_cast<unsigned>(left));
     }
 }
 
@@ -659,8 +661,11 @@ __global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep_lo
         if (!__syncthreads_or(gained)) break;
     }
     if (__syncthreads_or(any) && threadIdx.x == 0) A.counters->changed = 1;
-    const int left = __syncthreads_or(valid && rec_any(todo));
-    if (left && A.record && threadIdx.x == 0) A.incomplete[atomicAdd(&A.counters->n_incomplete, 1u)] = make_int2(sg, chunk);
+    const int left = __syncthreads_count(valid && rec_any(todo));
+    if (left && A.record && threadIdx.x == 0) {
+        A.incomplete[atomicAdd(&A.counters->n_incomplete, 1u)] = make_int2(sg, chunk);
+        atomicAdd(&A.counters->n_left, static_cast<unsigned>(left));
+    }
 }
 
 // recording sweep: a persistent grid walks the list of incomplete chunks
@@ -670,7 +675,7 @@ __global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_record(S
     // Recording is for the last few percent: per leftover vertex it costs a shared-memory atomic per unreached
     // individual plus compaction.  On graphs without a hub core one sweep leaves most of the graph unreached
     // (24 ms of recording at n = 1e6, Erdos-Renyi) — more sweeps first, as long as they still make progress.
-    if (total > A.defer_above && A.counters->changed) {
+    if (A.counters->n_left > A.defer_above && A.counters->changed) {
         if (blockIdx.x == 0 && threadIdx.x == 0) A.counters->deferred = 1;
         return;
     }
@@ -825,6 +830,7 @@ __global__ void k_pc_reset(int groups, int32_t* parent, int32_t* comp_size, int*
         counters->changed = 0;
         counters->n_incomplete = 0u;
         counters->deferred = 0;
+        counters->n_left = 0u;
         if (first) counters->range_error = 0;
     }
 }
@@ -1171,8 +1177,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             A.left_w = s->left_w.as<word_t>(); A.left_base = s->left_base.as<int32_t>(); A.parent = s->parent.as<int32_t>();
             A.comp_size = s->comp_size.as<int32_t>(); A.slot0 = slot0; A.counters = counters;
             A.incomplete = s->block_done.as<int2>(); A.record = 0; A.descending = 0;
-            const unsigned all_chunks = static_cast<unsigned>(sgroups) * static_cast<unsigned>((n + kThreads - 1) / kThreads);
-            A.defer_above = all_chunks / 8;
+            A.defer_above = static_cast<unsigned>(std::min<size_t>(0xfffffffeu, static_cast<size_t>(sgroups) * n / 16));  // 6 % of the pairs
             auto sweep = [&](bool final_pass, bool record, bool descending = false, bool local = false) -> int {
                 A.descending = descending ? 1 : 0;
                 A.cap_entries = static_cast<unsigned>(s->cap_entries);  // may have grown after an overflow retry
