@@ -841,8 +841,10 @@ __global__ void k_pc_reset(int groups, int32_t* parent, int32_t* comp_size, int*
 // bitmap, lock-free union-find over the alive edges (edge list, coalesced), component sizes,
 // sum of s(s-1)/2 and max s — in a single kernel.  Same integers as the big path.
 static constexpr int kSmallMaxN = 16384;
-static constexpr int kSmallThreads = 128;
+static constexpr int kSmallThreadsFew = 512;   // CTA size when the batch has fewer rows than the GPU has room for (latency per row)
+static constexpr int kSmallThreadsMany = 128;  // ... and when rows outnumber the SMs several times (throughput)
 
+template <int kSmallThreads>
 __global__ void __launch_bounds__(kSmallThreads) k_pc_small(GeneRows genes,
                                                             const int32_t* __restrict__ pool_map, int pool_size, int n, int m,
                                                             const int32_t* __restrict__ edge_u,
@@ -1035,7 +1037,8 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         s->mask_chunks = env_int("GAPA_PC_MASK_CHUNKS", 1, 1, 64);
         s->relabel = env_int("GAPA_PC_RELABEL", -1, -1, 1);  // -1 automatic, 0 never, 1 always (tests)
         s->small_path = env_int("GAPA_PC_SMALL", 1, 0, 2);  // 0: never, 1: where it pays, 2: wherever it fits (tests)
-        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small<kSmallThreadsFew>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small<kSmallThreadsMany>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         // the shared-memory bitmap may use most of the SM (one CTA per individual)
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1066,9 +1069,14 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         if (!trusted) GAPA_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(PcCounters), stream));  // trusted genes cannot be out of range
         const bool fuse = vary && cols > 0;
         if (vary && !fuse) GAPA_TRY(launch_variation_spec(*vary, cols, rows, stream));
-        GAPA_LAUNCH(k_pc_small, rows, kSmallThreads, smem, stream, genes,
-                    ctx->pool_identity ? nullptr : ctx->d_pool_map, ctx->pool_size, n, static_cast<int>(ctx->m), ctx->d_edge_u,
-                    ctx->d_edge_v, task, out_dev, counters, fuse ? *vary : VariationSpec{}, fuse ? 1 : 0);
+        if (rows <= 2 * sm)  // 100 rows at n = 1000: 0.03 ms with 512 threads per row, 0.05 ms with 128 (tools/ab_build.sh)
+            GAPA_LAUNCH(k_pc_small<kSmallThreadsFew>, rows, kSmallThreadsFew, smem, stream, genes,
+                        ctx->pool_identity ? nullptr : ctx->d_pool_map, ctx->pool_size, n, static_cast<int>(ctx->m), ctx->d_edge_u,
+                        ctx->d_edge_v, task, out_dev, counters, fuse ? *vary : VariationSpec{}, fuse ? 1 : 0);
+        else
+            GAPA_LAUNCH(k_pc_small<kSmallThreadsMany>, rows, kSmallThreadsMany, smem, stream, genes,
+                        ctx->pool_identity ? nullptr : ctx->d_pool_map, ctx->pool_size, n, static_cast<int>(ctx->m), ctx->d_edge_u,
+                        ctx->d_edge_v, task, out_dev, counters, fuse ? *vary : VariationSpec{}, fuse ? 1 : 0);
         if (trusted) return GAPA_CUDA_OK;
         PcCounters h{};
         GAPA_CUDA_TRY(cudaMemcpyAsync(&h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
