@@ -71,7 +71,7 @@ struct PcScratch {
     DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters, pass_flags, block_done;
     DevBuf left_v, left_g, left_w, left_base, parent, comp_size, pc_extra, mcn_extra;
     size_t cap_entries = 0, cap_slots = 0;
-    int prefix = 32768, interleave = 8, mask_chunks = 1, small_path = 1, relabel = -1, prefix_first4 = 1, trace = 0;
+    int prefix = 32768, interleave = 8, mask_chunks = 1, small_path = 1, relabel = -1, prefix_first4 = 1, trace = 0, prefix_cluster = 0;
     // hub-first internal vertex order for the bit-sliced path (see ensure_order)
     DevBuf ord_row_ptr, ord_col_idx, ord_gene_map;
     DevBuf nbr4;  // int4 per vertex: the first four entries of its (ascending) row, -1 padded — see gather_first4
@@ -440,16 +440,19 @@ __device__ __forceinline__ Rec gather_first4(const int32_t* __restrict__ row_ptr
 // kPrefixCluster CTAs (8192 threads): iterate ascending passes until nothing changes, with
 // cluster-wide barriers between passes — no host round trip, no cooperative launch.  The
 // in-flight window is the cluster, so a pass propagates almost like a sequential scan.
-__global__ void __cluster_dims__(kPrefixCluster, 1, 1) __launch_bounds__(kPrefixThreads)
+__global__ void __launch_bounds__(kPrefixThreads)
     k_pc_prefix(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx, const int4* __restrict__ nbr4,
                 int first4_only, int n, int prefix, const word_t* __restrict__ alive, Rec* reached, int* pass_flags) {
     cg::cluster_group cluster = cg::this_cluster();
-    const int sg = blockIdx.x / kPrefixCluster;
-    const int lane_in_cluster = (blockIdx.x % kPrefixCluster) * kPrefixThreads + threadIdx.x;
-    constexpr int kStride = kPrefixCluster * kPrefixThreads;
+    // the cluster size is a launch attribute: kPrefixCluster CTAs while every super-group's cluster is
+    // resident at once, fewer when there are more super-groups than that (waves of idle-heavy clusters cost more)
+    const int csize = static_cast<int>(cluster.num_blocks());
+    const int sg = blockIdx.x / csize;
+    const int lane_in_cluster = static_cast<int>(cluster.block_rank()) * kPrefixThreads + threadIdx.x;
+    const int kStride = csize * kPrefixThreads;
     Rec* reached_sg = reached + static_cast<size_t>(sg) * n;
     int* flags = pass_flags + sg * 64;  // one flag per pass; zeroed by the host
-    const int stages[2] = {min(prefix, kStride / 4), prefix};
+    const int stages[2] = {min(prefix, kPrefixCluster * kPrefixThreads / 4), prefix};
     int pass_id = 0;
     for (int s = 0; s < 2; ++s) {
         const int limit = stages[s];
@@ -1033,6 +1036,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
     PcScratch* s = ctx->pc;
     if (!s->configured) {  // tuning knobs (defaults are what bench.py measures)
         s->prefix = env_int("GAPA_PC_PREFIX", 32768, 0, 1 << 24);
+        s->prefix_cluster = env_int("GAPA_PC_PREFIX_CLUSTER", 0, 0, 8);  // 0 = choose by the number of super-groups
         s->interleave = env_int("GAPA_PC_INTERLEAVE", 8, 1, 64);
         s->mask_chunks = env_int("GAPA_PC_MASK_CHUNKS", 1, 1, 64);
         s->relabel = env_int("GAPA_PC_RELABEL", -1, -1, 1);  // -1 automatic, 0 never, 1 always (tests)
@@ -1172,8 +1176,22 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             if (prefix > 0) {
                 GAPA_TRY(s->pass_flags.ensure(sizeof(int) * 64 * sgroups));
                 GAPA_CUDA_TRY(cudaMemsetAsync(s->pass_flags.ptr, 0, sizeof(int) * 64 * sgroups, stream));
-                GAPA_LAUNCH(k_pc_prefix, sgroups * kPrefixCluster, kPrefixThreads, 0, stream, g_row_ptr, g_col_idx,
-                            s->nbr4.as<int4>(), s->prefix_first4, n, prefix, alive_rec, reached_rec, s->pass_flags.as<int>());
+                // measured on B200 (tools/ab_prefix.sh): 8 CTAs per super-group up to 8 groups, 4 at 16-32, 2 at 64;
+                // beyond that every cluster must be resident at once (one CTA of this kernel per SM)
+                int csize = sgroups <= 8 ? kPrefixCluster : 4;
+                while (csize > 1 && sgroups * csize > sm) csize >>= 1;
+                if (s->prefix_cluster > 0) csize = s->prefix_cluster;
+                cudaLaunchConfig_t cfg{};
+                cfg.gridDim = dim3(sgroups * csize);
+                cfg.blockDim = dim3(kPrefixThreads);
+                cfg.stream = stream;
+                cudaLaunchAttribute attr{};
+                attr.id = cudaLaunchAttributeClusterDimension;
+                attr.val.clusterDim.x = csize; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
+                cfg.attrs = &attr; cfg.numAttrs = 1;
+                GAPA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pc_prefix, g_row_ptr, g_col_idx, static_cast<const int4*>(s->nbr4.as<int4>()),
+                                                 s->prefix_first4, n, prefix, alive_rec, reached_rec, s->pass_flags.as<int>()));
+                g_launches.fetch_add(1, std::memory_order_relaxed);
             }
             const int il = std::min(std::max(1, s->interleave / kPack), sgroups);
             const dim3 grid(((n + kThreads - 1) / kThreads) * il, (sgroups + il - 1) / il);

@@ -76,15 +76,24 @@ __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_rank(const double* __
     if (x < total && isnan(mine_f)) *status = GAPA_CUDA_E_NAN;
     const unsigned long long mine = order_key(mine_f, minimize);  // integer compares (internal.cuh)
     int rank = 0;
+    const int own_t0 = blockIdx.x * (kSlotThreads / kSplit) / kSlotThreads * kSlotThreads;
     for (int t0 = 0; t0 < total; t0 += kSlotThreads) {
         __syncthreads();
         const int y = t0 + threadIdx.x;
         if (y < total) tile[threadIdx.x] = order_key(y < s ? fit[y] : fit_m[y - s], minimize);
         __syncthreads();
         const int lim = min(kSlotThreads, total - t0);
-        for (int t = part; t < lim; t += kSplit) {
-            const unsigned long long other = tile[t];
-            rank += (other < mine) | ((other == mine) & (t0 + t < x));
+        // a block's rows all lie in one tile: tiles before it hold only lower indices (ties count),
+        // tiles after it only higher ones (ties do not); one 64-bit compare per pair in both cases
+        if (t0 + kSlotThreads <= own_t0) {
+            for (int t = part; t < lim; t += kSplit) rank += tile[t] <= mine;
+        } else if (t0 > own_t0) {
+            for (int t = part; t < lim; t += kSplit) rank += tile[t] < mine;
+        } else {
+            for (int t = part; t < lim; t += kSplit) {
+                const unsigned long long other = tile[t];
+                rank += (other < mine) | ((other == mine) & (t0 + t < x));
+            }
         }
     }
     for (int off = kSplit / 2; off; off >>= 1) rank += __shfl_down_sync(0xffffffffu, rank, off, kSplit);

@@ -45,6 +45,18 @@ def test_small_runs_match_oracle(gp, oracle, cuda_device, task):
         _same(res, oracle.run_ga(og, task, 0.8, 0.1, 30, 8, 25, seed, eda_interval=eda))
 
 
+def test_large_population_run_matches_oracle(gp, oracle, cuda_device):
+    """Large ragged population sizes (multi-block ranking, weight and pick kernels),
+    ragged, on a small graph so that fitness ties are everywhere (stable tie-breaks matter)."""
+    g = gp.erdos_renyi(80, 0.05, 7)
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    for s, eda in [(4100, 0), (9001, 2)]:
+        params = gp.GAParams(pc=0.7, pm=0.15, pop_size=s, budget=6, iterations=4, seed=21, eda_interval=eda or None)
+        res = gp.run_ga(params, pool, gp.PairwiseConnectivityObjective(g, pool))
+        _same(res, oracle.run_ga(og, 0, 0.7, 0.15, s, 6, 4, 21, eda_interval=eda, threads=8))
+
+
 def test_lpa_and_cda_runs_match_oracle(gp, oracle, cuda_device):
     g = gp.erdos_renyi(120, 0.08, 2)
     split = gp.build_lp_split(g, 0.2, 5)
