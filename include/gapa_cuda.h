@@ -249,7 +249,9 @@ typedef struct gapa_cuda_run_result {
      * evaluation, modes.cpp:139-156); exchange = time inside the exchange hook (the fitness
      * all-gather; 0 on one GPU); lifecycle = 0 (no worker threads are spawned or joined);
      * compute = wall - exchange - lifecycle (record_generation, modes.cpp:38-40);
-     * messages = exchanges issued in that generation. */
+     * messages = exchanges issued in that generation.  On one GPU with pop_size <= 512 the events are SAMPLED
+     * (generation 1, 2, then every eighth): generations between two marks report their mean wall time and
+     * eval_seconds is scaled from the timed evaluations, because an event costs about as much as a kernel there. */
     double* gen_wall_seconds;
     double* gen_compute_seconds;
     double* gen_exchange_seconds;

@@ -32,7 +32,7 @@ int launch_slots_elitism(int32_t*, const int32_t*, const int32_t*, const int32_t
                          int, double, double, uint32_t, uint64_t, uint64_t, int32_t*, int32_t*, double*, int32_t*, int*, cudaStream_t);
 int launch_slots_gather(const int32_t*, const int32_t*, int, int, int32_t*, cudaStream_t);
 int launch_slots_elitism_small(const int32_t*, const int32_t*, int, const double*, const double*, int, int32_t*, int32_t*, double*,
-                               int32_t*, int*, double*, double*, cudaStream_t);
+                               int32_t*, int*, double*, double*, int, uint64_t, uint64_t, int32_t*, double*, double*, cudaStream_t);
 int launch_elitism_sharded(const int32_t*, const int32_t*, int, int, const int32_t*, int, int, const double*, const double*, int,
                            double, double, uint32_t, uint64_t, uint64_t, int32_t*, double*, int32_t*, int*, cudaStream_t);
 int launch_elitism(const int32_t*, const int32_t*, int, int, const double*, const double*, int, int32_t*, double*, int32_t*,
@@ -106,6 +106,7 @@ struct RunBuffers {
 
 // Evaluation of a row block inside the loop.  Timing uses one CUDA-event pair per call, read back
 // only when the run is over, so the loop itself never waits on the device for bookkeeping.
+static constexpr int kTimingStride = 8;
 struct EvalTimer {
     std::vector<cudaEvent_t> events;
     ~EvalTimer() { for (cudaEvent_t e : events) cudaEventDestroy(e); }
@@ -131,7 +132,7 @@ struct EvalTimer {
 int eval_rows(gapa_cuda_ctx* ctx, int task, const GeneRows& view, int rows, double* out, cudaStream_t st, EvalTimer* timer,
               const VariationSpec* vary = nullptr) {
     if (rows == 0) return GAPA_CUDA_OK;
-    GAPA_TRY(timer->mark(st));
+    if (timer) GAPA_TRY(timer->mark(st));
     int rc;
     if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) {
         rc = pc_eval(ctx, task, view, rows, out, st, true, vary);  // builds the children itself (fused with the mask build)
@@ -142,7 +143,7 @@ int eval_rows(gapa_cuda_ctx* ctx, int task, const GeneRows& view, int rows, doub
                                         : lpa_eval(ctx, view, rows, out, st, true);
     }
     GAPA_TRY(rc);
-    return timer->mark(st);
+    return timer ? timer->mark(st) : GAPA_CUDA_OK;
 }
 }  // namespace
 
@@ -224,9 +225,26 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
     EvalTimer gen_marks, exchange_marks;
     std::vector<int> exchanges_in_gen(static_cast<size_t>(iters), 0);
     int current_gen = 1;
+    // A timing event between two kernels costs ~5 us of device time.  A small population's generation is two launches
+    // of 10-15 us, so there the marks are SAMPLED from generation 2 on: every kTimingStride-th generation is bracketed (its
+    // evaluation and its boundary); eval_seconds is scaled by calls / timed calls and a block of generations shares its
+    // mean wall time.
+    const bool small = world == 1 && 2 * s <= 1024;
+    const int stride = small ? kTimingStride : 1;
+    // generation 1 (initialisation, two evaluations, one-off set-up inside them) is always timed exactly
+    auto sampled_gen = [&](int gen) { return gen <= 2 || (gen - 2) % stride == 0; };
+    EvalTimer first_timer;
+    uint64_t later_calls = 0, later_timed_calls = 0;
+    std::vector<int> marked_gens;  // generations (1-based) whose start carries a mark
     auto evaluate = [&](const int32_t* table, double* fit_all, const VariationSpec* vary = nullptr) -> int {  // rows [lo, hi) named by `table`
         ++result->fitness_batch_calls;
-        GAPA_TRY(eval_rows(ctx, p->task, GeneRows{pool_rows, table + lo, k}, hi - lo, fit_all + lo, st, &timer, vary));
+        const bool timed = sampled_gen(current_gen);
+        if (current_gen > 1) {
+            ++later_calls;
+            later_timed_calls += timed;
+        }
+        GAPA_TRY(eval_rows(ctx, p->task, GeneRows{pool_rows, table + lo, k}, hi - lo, fit_all + lo, st,
+                           current_gen == 1 ? &first_timer : timed ? &timer : nullptr, vary));
         if (world > 1) {
             if (want_stats) GAPA_TRY(exchange_marks.mark(st));
             const int rc = exchange(exchange_user, fit_all, s, block, st);
@@ -247,7 +265,10 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
     const auto t0 = std::chrono::steady_clock::now();
     for (int gen = 1; gen <= iters; ++gen) {
         current_gen = gen;
-        if (want_stats) GAPA_TRY(gen_marks.mark(st));
+        if (want_stats && sampled_gen(gen)) {
+            GAPA_TRY(gen_marks.mark(st));
+            marked_gens.push_back(gen);
+        }
         if (gen == 1) {
             GAPA_TRY(launch_slots_identity(s, parent, child, st));
             GAPA_TRY(launch_init(pool, 0, s, k, p->seed, 0, pool_rows, st));  // parents occupy slots 0..s-1
@@ -259,7 +280,7 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
         // Children are built only for the rows this rank evaluates (all rows when world == 1).
         const bool eda_gen = p->eda_interval > 0 && gen % p->eda_interval == 0;  // modes.cpp:31-33,167-168
         const int32_t* partner = eda_gen ? nullptr : B.partner.as<int32_t>();
-        if (!eda_gen)
+        if (!eda_gen && !(small && gen > 1))  // small populations: selected by the previous generation's elitism launch
             GAPA_TRY(launch_select(fit, s, minimize, p->seed, g, B.partner.as<int32_t>(), B.weights.as<double>(),
                                    B.cumulative.as<double>(), status, st));
         VariationSpec vary;  // the evaluation builds the children of rows [lo, hi) into their slots first
@@ -271,10 +292,13 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
         vary.row_first = lo;
         GAPA_TRY(evaluate(child, fit_m, &vary));
         // elitism permutes the slot tables; survivors built by other ranks are rebuilt in place
-        const bool small = world == 1 && 2 * s <= 1024;  // launch-latency-bound: elitism and the generation's statistics in one launch
+        // small populations: elitism, the generation's statistics AND the next generation's selection in one launch
+        const bool select_next = gen < iters && !(p->eda_interval > 0 && (gen + 1) % p->eda_interval == 0);
         if (small)
             GAPA_TRY(launch_slots_elitism_small(parent, child, s, fit, fit_m, minimize, next_parent, next_child, fit_next,
-                                                B.src_of_rank.as<int32_t>(), status, hist + (gen - 1), hist + iters + (gen - 1), st));
+                                                B.src_of_rank.as<int32_t>(), status, hist + (gen - 1), hist + iters + (gen - 1),
+                                                select_next ? 1 : 0, p->seed, g + 1, B.partner.as<int32_t>(), B.weights.as<double>(),
+                                                B.cumulative.as<double>(), st));
         else
             GAPA_TRY(launch_slots_elitism(pool_rows, parent, child, partner, s, k, lo, hi, fit, fit_m, minimize, p->pc, p->pm, pool,
                                           p->seed, g, next_parent, next_child, fit_next, B.src_of_rank.as<int32_t>(), status, st));
@@ -293,12 +317,23 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
     }
     if (want_stats) GAPA_TRY(gen_marks.mark(st));
     GAPA_CUDA_TRY(cudaStreamSynchronize(st));
+    double first_seconds = 0.0;
+    GAPA_TRY(first_timer.total_seconds(&first_seconds));
     GAPA_TRY(timer.total_seconds(&result->eval_seconds));
+    if (later_timed_calls) result->eval_seconds *= static_cast<double>(later_calls) / static_cast<double>(later_timed_calls);
+    result->eval_seconds += first_seconds;
     if (want_stats) {
+        marked_gens.push_back(iters + 1);
+        std::vector<float> wall_of_gen(static_cast<size_t>(iters), 0.f);
+        for (size_t b = 0; b + 1 < marked_gens.size(); ++b) {  // a block of generations between two marks shares its mean
+            float ms = 0.f;
+            GAPA_CUDA_TRY(cudaEventElapsedTime(&ms, gen_marks.events[b], gen_marks.events[b + 1]));
+            const int g0 = marked_gens[b], g1 = marked_gens[b + 1];
+            for (int gi = g0; gi < g1; ++gi) wall_of_gen[static_cast<size_t>(gi - 1)] = ms / static_cast<float>(g1 - g0);
+        }
         size_t next_exchange = 0;
         for (int gi = 0; gi < iters; ++gi) {
-            float wall_ms = 0.f;
-            GAPA_CUDA_TRY(cudaEventElapsedTime(&wall_ms, gen_marks.events[gi], gen_marks.events[gi + 1]));
+            const float wall_ms = wall_of_gen[static_cast<size_t>(gi)];
             double exchange_s = 0.0;
             for (int e = 0; e < exchanges_in_gen[gi]; ++e, next_exchange += 2) {
                 float ms = 0.f;

@@ -134,8 +134,11 @@ __global__ void __launch_bounds__(1024) k_ga_slots_elitism_small(const int32_t* 
                                                                  int s, int minimize, int32_t* __restrict__ order,
                                                                  int32_t* __restrict__ next_parent, int32_t* __restrict__ next_child,
                                                                  double* __restrict__ next_fit, int* status, double* hist_best,
-                                                                 double* hist_mean) {
+                                                                 double* hist_mean, int select_next, uint64_t seed,
+                                                                 uint64_t next_generation, int32_t* __restrict__ partner,
+                                                                 double* __restrict__ weights, double* __restrict__ cumulative) {
     __shared__ double f[1024];
+    __shared__ double cum[512];
     __shared__ double kept[512];
     __shared__ int ord[1024];
     __shared__ double warp_sum[32];
@@ -187,6 +190,64 @@ __global__ void __launch_bounds__(1024) k_ga_slots_elitism_small(const int32_t* 
         for (int i = 0; i < s; ++i) sum += kept[i];
         *hist_best = kept[0];
         *hist_mean = sum / static_cast<double>(s);
+    }
+    if (!select_next) return;
+    // roulette_select of the NEXT generation (ga_ops.cpp:54-82, :105-128) on the parents just committed, saving that
+    // generation's selection launch.  `kept` is sorted best-first, so the rows strictly better than mine are a prefix
+    // and my ties a contiguous run: two binary searches give the counts selection_weights needs.
+    __syncthreads();
+    double w = 0.0;
+    if (tid < s) {
+        const double mine_next = kept[tid];
+        if (!isfinite(mine_next)) *status = GAPA_CUDA_E_NAN;
+        int a = 0, b = tid;  // first row not strictly better than mine
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            const double other = kept[mid];
+            if (minimize ? other < mine_next : other > mine_next) a = mid + 1; else b = mid;
+        }
+        const int less = a;
+        a = tid + 1, b = s;  // first row strictly worse than mine
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            const double other = kept[mid];
+            if (minimize ? mine_next < other : mine_next > other) b = mid; else a = mid + 1;
+        }
+        const int leq = a;
+        w = (static_cast<double>(s - less) + static_cast<double>(s - leq + 1)) / 2.0;
+        weights[tid] = w;
+    }
+    const int lane = tid & 31, wid = tid >> 5;
+    double v = w;  // inclusive scan; half-integers below 2^53 add exactly in any order
+    for (int off = 1; off < 32; off <<= 1) {
+        const double t = __shfl_up_sync(0xffffffffu, v, off);
+        if (lane >= off) v += t;
+    }
+    if (lane == 31) warp_sum[wid] = v;
+    __syncthreads();
+    if (wid == 0) {
+        double t = warp_sum[lane];
+        for (int off = 1; off < 32; off <<= 1) {
+            const double u = __shfl_up_sync(0xffffffffu, t, off);
+            if (lane >= off) t += u;
+        }
+        warp_sum[lane] = t;
+    }
+    __syncthreads();
+    if (wid > 0) v += warp_sum[wid - 1];
+    if (tid < s) {
+        cum[tid] = v;
+        cumulative[tid] = v;
+    }
+    __syncthreads();
+    if (tid < s) {
+        const double target = draw_unit(stream_key(seed, next_generation, GAPA_ROLE_SELECT, static_cast<uint64_t>(tid)), 1) * cum[s - 1];
+        int a = 0, b = s;  // std::upper_bound: first index with cumulative > target
+        while (a < b) {
+            const int mid = (a + b) >> 1;
+            if (cum[mid] <= target) a = mid + 1; else b = mid;
+        }
+        partner[tid] = min(a, s - 1);
     }
 }
 
@@ -246,9 +307,10 @@ int launch_slots_elitism(int32_t* pool, const int32_t* parent, const int32_t* ch
 // elitism + GenerationStats::best / mean in one launch; only for an unsharded run with 2s <= 1024
 int launch_slots_elitism_small(const int32_t* parent, const int32_t* child, int s, const double* fit, const double* fit_m, int minimize,
                                int32_t* next_parent, int32_t* next_child, double* next_fit, int32_t* order, int* status,
-                               double* hist_best, double* hist_mean, cudaStream_t st) {
+                               double* hist_best, double* hist_mean, int select_next, uint64_t seed, uint64_t next_generation,
+                               int32_t* partner, double* weights, double* cumulative, cudaStream_t st) {
     GAPA_LAUNCH(k_ga_slots_elitism_small, 1, 1024, 0, st, parent, child, fit, fit_m, s, minimize, order, next_parent, next_child,
-                next_fit, status, hist_best, hist_mean);
+                next_fit, status, hist_best, hist_mean, select_next, seed, next_generation, partner, weights, cumulative);
     return GAPA_CUDA_OK;
 }
 int launch_slots_gather(const int32_t* pool, const int32_t* table, int rows, int k, int32_t* out, cudaStream_t st) {
