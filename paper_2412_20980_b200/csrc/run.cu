@@ -107,6 +107,7 @@ struct RunBuffers {
 // Evaluation of a row block inside the loop.  Timing uses one CUDA-event pair per call, read back
 // only when the run is over, so the loop itself never waits on the device for bookkeeping.
 static constexpr int kTimingStride = 8;
+static constexpr float kSampleBelowMs = 0.5f;  // evaluations shorter than this get sampled timing marks
 struct EvalTimer {
     std::vector<cudaEvent_t> events;
     ~EvalTimer() { for (cudaEvent_t e : events) cudaEventDestroy(e); }
@@ -228,11 +229,13 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
     // A timing event between two kernels costs ~5 us of device time.  A small population's generation is two launches
     // of 10-15 us, so there the marks are SAMPLED from generation 2 on: every kTimingStride-th generation is bracketed (its
     // evaluation and its boundary); eval_seconds is scaled by calls / timed calls and a block of generations shares its
-    // mean wall time.
+    // mean wall time.  Larger populations start exact and switch to sampling at the first status poll (generation 16)
+    // if an evaluation takes less than kSampleBelowMs.
     const bool small = world == 1 && 2 * s <= 1024;
-    const int stride = small ? kTimingStride : 1;
+    int stride = small ? kTimingStride : 1;  // larger populations switch at the first status poll if their evaluations are short
+    int exact_until = 2;
     // generation 1 (initialisation, two evaluations, one-off set-up inside them) is always timed exactly
-    auto sampled_gen = [&](int gen) { return gen <= 2 || (gen - 2) % stride == 0; };
+    auto sampled_gen = [&](int gen) { return gen <= exact_until || (gen - 2) % stride == 0; };
     EvalTimer first_timer;
     uint64_t later_calls = 0, later_timed_calls = 0;
     std::vector<int> marked_gens;  // generations (1-based) whose start carries a mark
@@ -313,6 +316,14 @@ extern "C" int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* p, 
             GAPA_CUDA_TRY(cudaMemcpyAsync(&h, status, sizeof(int), cudaMemcpyDeviceToHost, st));
             GAPA_CUDA_TRY(cudaStreamSynchronize(st));
             if (h == GAPA_CUDA_E_NAN) return fail(GAPA_CUDA_E_NAN, "elitism: NaN fitness");
+            if (stride == 1 && world == 1 && timer.events.size() >= 2) {  // the stream is idle: the last evaluation's time is known
+                float ms = 0.f;
+                GAPA_CUDA_TRY(cudaEventElapsedTime(&ms, timer.events[timer.events.size() - 2], timer.events.back()));
+                if (ms < kSampleBelowMs) {
+                    stride = kTimingStride;
+                    exact_until = gen + 1;  // the next generation carries a mark, so the exact block ends there
+                }
+            }
         }
     }
     if (want_stats) GAPA_TRY(gen_marks.mark(st));

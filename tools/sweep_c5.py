@@ -15,13 +15,17 @@ for wl, n in (("n1e4", "1e4"), ("n1e5", "1e5"), ("c4", "1e6")):
             rows.append((n, pop, None, out.stderr[-300:]))
             continue
         rows.append((n, pop, d, ""))
-print("| n | population | step (ms) | generations/s | evals/s (loop) | evals/s (evaluation alone) | e2e evals/s (host buffers) | CPU evals/s (threads) |")
-print("|---|---|---|---|---|---|---|---|")
+print("`step` = one generation driven through the stepwise operator C-ABI (`bench.py`'s `value`, one host synchronisation per generation);"
+      " `library loop` = the same generations inside `gapa_cuda_run` (no per-generation host work).\n")
+print("| n | population | step (ms) | generations/s | evals/s (loop) | library loop generations/s | evals/s (evaluation alone) | e2e evals/s (host buffers) | CPU evals/s (threads) |")
+print("|---|---|---|---|---|---|---|---|---|")
 for n, pop, d, err in rows:
     if d is None:
-        print(f"| {n} | {pop} | failed: {err!r} | | | | | |")
+        print(f"| {n} | {pop} | failed: {err!r} | | | | | | |")
         continue
     cpu = d.get("cpu_baseline")
+    lib = d.get("library_loop")
     print(f"| {n} | {pop} | {d['ms_per_step']:.3f} | {d['generations_per_sec']:.0f} | {d['value']:.3g} | "
+          + (f"{lib['generations_per_sec']:.0f}" if lib else "") + " | "
           f"{d['fitness_evals_per_sec_kernels_only']:.3g} | {d['e2e']['value']:.3g} | "
           + (f"{cpu['value']:.3g} ({cpu['cores']}, {cpu['kind']})" if cpu else "") + " |")
