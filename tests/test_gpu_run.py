@@ -195,3 +195,23 @@ def test_generation_stats_and_overhead_report(gp, cuda_device):
     assert lines[0] == "gen  wall_s      compute_s   exchange_s  lifecycle_s messages"
     assert len(lines) == 7 and lines[1].startswith("1    0.") and lines[1].endswith(" 0") and lines[6].startswith("6    ")
     assert [len(x) for x in lines[1].split(" ") if x][1:5] == [8, 8, 8, 8]
+
+
+def test_sampled_timing_marks_keep_results_and_columns(gp, oracle, cuda_device):
+    """Timing marks are sampled for short generations (run.cu): from generation 2 for populations up to 512, from the
+    first status poll (generation 16) for larger ones.  Sampling must not touch the trajectory, every generation must
+    still report a positive wall time, and the columns must stay consistent with the totals."""
+    g = gp.erdos_renyi(120, 0.04, 9)
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    for s, iters in [(40, 37), (600, 37)]:
+        params = gp.GAParams(pc=0.7, pm=0.1, pop_size=s, budget=7, iterations=iters, seed=4)
+        res = gp.run_ga(params, pool, gp.PairwiseConnectivityObjective(g, pool))
+        _same(res, oracle.run_ga(og, 0, 0.7, 0.1, s, 7, iters, 4, threads=8))
+        walls = [h.wall_seconds for h in res.history]
+        assert len(walls) == iters and all(w > 0 for w in walls)
+        assert all(h.compute_seconds == h.wall_seconds and h.messages == 0 for h in res.history)
+        assert sum(walls) <= res.total_wall_seconds * 1.05 + 1e-3
+        assert 0 < res.eval_seconds <= sum(walls) * 1.001 + 1e-6
+        assert len(set(walls[20:28])) <= 2  # generations between two marks share their mean
+        assert res.fitness_batch_calls == iters + 1
