@@ -123,3 +123,29 @@ def test_batches_larger_than_the_scratch_budget(gp, oracle, cuda_device, monkeyp
     ebatch = gp.init_population(epool.size(), 90, 500, 6)
     assert np.array_equal(gp.LinkPredictionAttackObjective(split, epool).evaluate_batch(ebatch),
                           oracle.eval_batch(os_, 3, ebatch, threads=8))
+
+
+def test_concurrent_callers_share_one_objective(gp, oracle, cuda_device):
+    """fitness.hpp:17-27 objectives are called from many host threads at once (modes.cpp:85, :209): the CUDA
+    objective serialises them internally; every caller must get the fitness of ITS batch."""
+    import threading
+    g = gp.barabasi_albert(3000, 3, 4)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    objs = [gp.PairwiseConnectivityObjective(g, pool), gp.SixDstObjective(g, pool)]
+    batches = [gp.init_population(pool.size(), 40 + 7 * t, 100, 20 + t) for t in range(6)]
+    got = [[None] * len(batches) for _ in objs]
+
+    def worker(t):
+        for _ in range(3):
+            for o, obj in enumerate(objs):
+                got[o][t] = obj.evaluate_batch(batches[t])
+
+    threads = [threading.Thread(target=worker, args=(t,)) for t in range(len(batches))]
+    for th in threads:
+        th.start()
+    for th in threads:
+        th.join()
+    for t, b in enumerate(batches):
+        assert np.array_equal(got[0][t], oracle.eval_batch(og, 0, b))
+        assert np.array_equal(got[1][t], oracle.eval_batch(og, 1, b))

@@ -10,7 +10,7 @@ pytestmark = pytest.mark.gpu
 @pytest.fixture(params=["warp-per-individual", "bit-sliced"], autouse=True)
 def pc_path(request, monkeypatch):
     """Every case runs through both PC implementations: the shared-memory warp kernel that small
-    graphs take by default, and the bit-sliced pipeline (forced here; the default above n = 16384)."""
+    graphs take by default, and the bit-sliced pipeline (forced here; the default above n = 2048-4096, see pc_kernels.cu small_pays)."""
     monkeypatch.setenv("GAPA_PC_SMALL", "2" if request.param == "warp-per-individual" else "0")
     return request.param
 
