@@ -158,6 +158,29 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_weights(const double* __restr
     if (i < s && !isfinite(mine_f)) *status = GAPA_CUDA_E_NAN;
     const unsigned long long mine = order_key(mine_f, minimize);
     int less = 0, leq = 0;
+    // After an elitism step the population is sorted best-first: the rows better than mine are a prefix and my ties
+    // a contiguous run, so two binary searches replace the s compares (every block checks the order itself: s compares
+    // against its own 32 * s).
+    int in_order = 1;
+    for (int t = threadIdx.x; t + 1 < s; t += kGaThreads) in_order &= order_key(fitness[t], minimize) <= order_key(fitness[t + 1], minimize);
+    if (__syncthreads_and(in_order)) {
+        if (i < s && part == 0) {
+            int a = 0, b = i;  // first row not better than mine
+            while (a < b) {
+                const int mid = (a + b) >> 1;
+                if (order_key(fitness[mid], minimize) < mine) a = mid + 1; else b = mid;
+            }
+            less = a;
+            a = i + 1, b = s;  // first row worse than mine
+            while (a < b) {
+                const int mid = (a + b) >> 1;
+                if (order_key(fitness[mid], minimize) <= mine) a = mid + 1; else b = mid;
+            }
+            leq = a;
+            weights[i] = (static_cast<double>(s - less) + static_cast<double>(s - leq + 1)) / 2.0;
+        }
+        return;
+    }
     for (int t0 = 0; t0 < s; t0 += kGaThreads) {
         __syncthreads();
         if (t0 + threadIdx.x < s) tile[threadIdx.x] = order_key(fitness[t0 + threadIdx.x], minimize);

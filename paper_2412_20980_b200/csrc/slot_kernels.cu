@@ -76,6 +76,43 @@ __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_rank(const double* __
     if (x < total && isnan(mine_f)) *status = GAPA_CUDA_E_NAN;
     const unsigned long long mine = order_key(mine_f, minimize);  // integer compares (internal.cuh)
     int rank = 0;
+    // From the second generation on the parents ARE sorted best-first (they are the previous elitism's output).  Every
+    // block checks that while it is cheap (s compares against its own 32 * 2s); if so a parent's position among the
+    // parents is its index, a child's is one binary search, and only the children have to be counted: half the compares.
+    int in_order = 1;
+    for (int t = threadIdx.x; t + 1 < s; t += kSlotThreads) in_order &= order_key(fit[t], minimize) <= order_key(fit[t + 1], minimize);
+    if (__syncthreads_and(in_order)) {
+        const int j = x - s;  // own index among the children (negative for a parent)
+        if (x >= s && x < total) {  // parents that precede this child: ties included (originals first)
+            int a = 0, b = s;
+            while (a < b) {
+                const int mid = (a + b) >> 1;
+                if (order_key(fit[mid], minimize) <= mine) a = mid + 1; else b = mid;
+            }
+            rank = part == 0 ? a : 0;
+        } else {
+            rank = part == 0 ? x : 0;
+        }
+        for (int c0 = 0; c0 < s; c0 += kSlotThreads) {
+            __syncthreads();
+            if (c0 + threadIdx.x < s) tile[threadIdx.x] = order_key(fit_m[c0 + threadIdx.x], minimize);
+            __syncthreads();
+            const int lim = min(kSlotThreads, s - c0);
+            if (j < 0 || c0 > j) {  // a parent precedes every tied child; children after mine do not count on ties
+                for (int t = part; t < lim; t += kSplit) rank += tile[t] < mine;
+            } else if (c0 + kSlotThreads <= j) {
+                for (int t = part; t < lim; t += kSplit) rank += tile[t] <= mine;
+            } else {
+                for (int t = part; t < lim; t += kSplit) {
+                    const unsigned long long other = tile[t];
+                    rank += (other < mine) | ((other == mine) & (c0 + t < j));
+                }
+            }
+        }
+        for (int off = kSplit / 2; off; off >>= 1) rank += __shfl_down_sync(0xffffffffu, rank, off, kSplit);
+        if (x < total && part == 0) order[rank] = x;
+        return;
+    }
     const int own_t0 = blockIdx.x * (kSlotThreads / kSplit) / kSlotThreads * kSlotThreads;
     for (int t0 = 0; t0 < total; t0 += kSlotThreads) {
         __syncthreads();
