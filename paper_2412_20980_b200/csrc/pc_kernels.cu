@@ -98,7 +98,8 @@ __device__ __forceinline__ void load8_stream(const int32_t* p, int (&v)[8]) {
                  : "l"(p));
 }
 
-__global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(GeneRows genes,
+template <int nt>  // threads per CTA: 128..kMaskThreads, chosen by the launch from the genes per individual (mask_threads)
+__global__ void __launch_bounds__(nt) k_pc_bitmask(GeneRows genes,
                                                              const int32_t* __restrict__ pool_map, int pool_size, int n,
                                                              int chunk_bits, int words_per_row, word_t* __restrict__ removed,
                                                              int* removed_count, PcCounters* counters) {
@@ -106,7 +107,7 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(GeneRows genes,
     const int v0 = blockIdx.x * chunk_bits;
     const int v1 = min(n, v0 + chunk_bits);
     const int words64 = (v1 - v0 + 63) >> 6;
-    for (int w = threadIdx.x; w < 2 * words64; w += kMaskThreads) pc_smem_bits[w] = 0u;
+    for (int w = threadIdx.x; w < 2 * words64; w += nt) pc_smem_bits[w] = 0u;
     __syncthreads();
     const int cols = genes.cols;
     const int32_t* g = genes.row(row);
@@ -124,10 +125,10 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(GeneRows genes,
         // shared-memory atomic: with one CTA per SM the kernel lives on bytes in flight per thread
         const int octs = cols >> 3;
         int o = threadIdx.x;
-        for (; o + kMaskThreads < octs; o += 2 * kMaskThreads) {
+        for (; o + nt < octs; o += 2 * nt) {
             int a[8], b[8];
             load8_stream(g + 8 * static_cast<size_t>(o), a);
-            load8_stream(g + 8 * static_cast<size_t>(o + kMaskThreads), b);
+            load8_stream(g + 8 * static_cast<size_t>(o + nt), b);
 #pragma unroll
             for (int t = 0; t < 8; ++t) mark(a[t]);
 #pragma unroll
@@ -145,9 +146,9 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(GeneRows genes,
         const int4* g4 = reinterpret_cast<const int4*>(g);
         const int quads = cols >> 2;
         int q = threadIdx.x;
-        for (; q + kMaskThreads < quads; q += 2 * kMaskThreads) {
+        for (; q + nt < quads; q += 2 * nt) {
             const int4 a = __ldcs(&g4[q]);
-            const int4 b = __ldcs(&g4[q + kMaskThreads]);
+            const int4 b = __ldcs(&g4[q + nt]);
             mark(a.x); mark(a.y); mark(a.z); mark(a.w);
             mark(b.x); mark(b.y); mark(b.z); mark(b.w);
         }
@@ -157,12 +158,12 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(GeneRows genes,
         }
         j0 = quads << 2;
     }
-    for (int j = j0 + threadIdx.x; j < cols; j += kMaskThreads) mark(g[j]);
+    for (int j = j0 + threadIdx.x; j < cols; j += nt) mark(g[j]);
     __syncthreads();
     const word_t* bits64 = reinterpret_cast<const word_t*>(pc_smem_bits);
     word_t* out = removed + static_cast<size_t>(row) * words_per_row + (v0 >> 6);
     int distinct = 0;
-    for (int w = threadIdx.x; w < words64; w += kMaskThreads) {
+    for (int w = threadIdx.x; w < words64; w += nt) {
         const word_t x = bits64[w];
         distinct += __popcll(x);
         out[w] = x;
@@ -176,13 +177,14 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask(GeneRows genes,
 // to the child's slot and sets it in the shared-memory bitmap in the same pass.  The hash arithmetic
 // of the variation (integer pipes) and the shared-memory atomics of the mask build (LSU) overlap
 // inside one kernel, and the 4 k bytes of the child row are never read back from HBM.
-__global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask_vary(VariationSpec V, int k, const int32_t* __restrict__ gene_map,
+template <int nt>
+__global__ void __launch_bounds__(nt) k_pc_bitmask_vary(VariationSpec V, int k, const int32_t* __restrict__ gene_map,
                                                                   int n, int words_per_row, word_t* __restrict__ removed,
                                                                   int* removed_count) {
     __shared__ uint64_t keys[4];
     const int local = blockIdx.x, row = V.row_first + local;
     const int words64 = (n + 63) >> 6;
-    for (int w = threadIdx.x; w < 2 * words64; w += kMaskThreads) pc_smem_bits[w] = 0u;
+    for (int w = threadIdx.x; w < 2 * words64; w += nt) pc_smem_bits[w] = 0u;
     if (threadIdx.x < 4)
         keys[threadIdx.x] = stream_key(V.P.seed, V.P.generation, GAPA_ROLE_SELECT + threadIdx.x, static_cast<uint64_t>(row)) + kGolden;
     __syncthreads();
@@ -205,11 +207,11 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask_vary(VariationSpec 
             a_next = __ldcs(&mine4[threadIdx.x]);
             b_next = eda ? a_next : __ldcs(&theirs4[threadIdx.x]);
         }
-        for (int q = threadIdx.x; q < quads; q += kMaskThreads) {
+        for (int q = threadIdx.x; q < quads; q += nt) {
             const int4 a = a_next, b = b_next;
-            if (q + kMaskThreads < quads) {  // next quad's parents are in flight while this one is hashed
-                a_next = __ldcs(&mine4[q + kMaskThreads]);
-                b_next = eda ? a_next : __ldcs(&theirs4[q + kMaskThreads]);
+            if (q + nt < quads) {  // next quad's parents are in flight while this one is hashed
+                a_next = __ldcs(&mine4[q + nt]);
+                b_next = eda ? a_next : __ldcs(&theirs4[q + nt]);
             }
             const int av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
             int r[4];
@@ -224,7 +226,7 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask_vary(VariationSpec 
             for (int t = 0; t < 4; ++t) mark(r[t]);
         }
     } else {
-        for (int j = threadIdx.x; j < k; j += kMaskThreads) {
+        for (int j = threadIdx.x; j < k; j += nt) {
             const int gsel = child_gene(V.P, V.pool, V.parent, k, j, mine[j], theirs[j], eda, ks, kc, km, ki,
                                         kCounterStep * (static_cast<uint64_t>(j) + 1));
             dst[j] = gsel;
@@ -235,7 +237,7 @@ __global__ void __launch_bounds__(kMaskThreads) k_pc_bitmask_vary(VariationSpec 
     const word_t* bits64 = reinterpret_cast<const word_t*>(pc_smem_bits);
     word_t* out = removed + static_cast<size_t>(local) * words_per_row;
     int distinct = 0;
-    for (int w = threadIdx.x; w < words64; w += kMaskThreads) {
+    for (int w = threadIdx.x; w < words64; w += nt) {
         const word_t x = bits64[w];
         distinct += __popcll(x);
         out[w] = x;
@@ -1044,8 +1046,14 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small<kSmallThreadsFew>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small<kSmallThreadsMany>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         // the shared-memory bitmap may use most of the SM (one CTA per individual)
-        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
         s->overlap_clear = env_int("GAPA_PC_OVERLAP_CLEAR", 1, 0, 1);
         s->trace = env_int("GAPA_PC_TRACE", 0, 0, 1);  // one stderr line per sweep round
@@ -1141,21 +1149,36 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             // which is bound by integer issue, not by HBM.
             if (s->overlap_clear) GAPA_CUDA_TRY(cudaEventRecord(s->ev_pass_begin, stream));
             // ---- masks ------------------------------------------------------------------
+            // one CTA per individual: as many threads as it has 16-byte gene quads (or bitmap words) to work on, so that
+            // small budgets do not occupy an SM with idle warps (k = 500: 128 threads, 16 CTAs per SM instead of 2)
+            int mask_threads = 128;
+            while (mask_threads < kMaskThreads && mask_threads < std::max(cols / 4, chunk_bits / 128)) mask_threads <<= 1;
             if (vary && chunks == 1 && cols > 0) {
                 VariationSpec pass = *vary;
                 pass.row_first += row0;
-                GAPA_LAUNCH(k_pc_bitmask_vary, crows, kMaskThreads, static_cast<size_t>(chunk_bits) / 8, stream, pass, cols, g_gene_map,
-                            n, words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>());
+#define GAPA_MASK_VARY(NT)                                                                                                  \
+    GAPA_LAUNCH(k_pc_bitmask_vary<NT>, crows, NT, static_cast<size_t>(chunk_bits) / 8, stream, pass, cols, g_gene_map, n, \
+                words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>())
+                if (mask_threads == 128) GAPA_MASK_VARY(128);
+                else if (mask_threads == 256) GAPA_MASK_VARY(256);
+                else if (mask_threads == 512) GAPA_MASK_VARY(512);
+                else GAPA_MASK_VARY(1024);
+#undef GAPA_MASK_VARY
             } else {
                 if (vary) {
                     VariationSpec pass = *vary;
                     pass.row_first += row0;
                     GAPA_TRY(launch_variation_spec(pass, cols, crows, stream));
                 }
-            GAPA_LAUNCH(k_pc_bitmask, dim3(chunks, crows), kMaskThreads, static_cast<size_t>(chunk_bits) / 8, stream,
-                        genes.from(row0), g_gene_map,
-                        ctx->pool_size, n, chunk_bits, words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>(),
-                        counters);
+#define GAPA_MASK(NT)                                                                                                       \
+    GAPA_LAUNCH(k_pc_bitmask<NT>, dim3(chunks, crows), NT, static_cast<size_t>(chunk_bits) / 8, stream, genes.from(row0),  \
+                g_gene_map, ctx->pool_size, n, chunk_bits, words_per_row, s->removed.as<word_t>(),                         \
+                s->removed_count.as<int>(), counters)
+                if (mask_threads == 128) GAPA_MASK(128);
+                else if (mask_threads == 256) GAPA_MASK(256);
+                else if (mask_threads == 512) GAPA_MASK(512);
+                else GAPA_MASK(1024);
+#undef GAPA_MASK
             }
             if (s->overlap_clear) {  // issued AFTER the mask kernel so that its CTAs only fill what that kernel leaves free
                 GAPA_CUDA_TRY(cudaStreamWaitEvent(s->aux, s->ev_pass_begin, 0));
