@@ -1048,11 +1048,19 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         // the shared-memory bitmap may use most of the SM (one CTA per individual)
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<640>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<768>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<896>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<640>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<768>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<896>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
         s->overlap_clear = env_int("GAPA_PC_OVERLAP_CLEAR", 1, 0, 1);
@@ -1151,18 +1159,39 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             // ---- masks ------------------------------------------------------------------
             // one CTA per individual: as many threads as it has 16-byte gene quads (or bitmap words) to work on, so that
             // small budgets do not occupy an SM with idle warps (k = 500: 128 threads, 16 CTAs per SM instead of 2)
-            int mask_threads = 128;
-            while (mask_threads < kMaskThreads && mask_threads < std::max(cols / 4, chunk_bits / 128)) mask_threads <<= 1;
-            if (vary && chunks == 1 && cols > 0) {
+            // (k = 5000: 640 threads make two full passes over the 1250 quads where 1024 would idle 40 % of their slots)
+            auto mask_cta = [&](int work) {  // the CTA size whose passes over `work` items waste the fewest thread slots
+                int best = 128;
+                long best_cost = -1;
+                for (int nt = 128; nt <= kMaskThreads; nt += 128) {
+                    const long cost = static_cast<long>((work + nt - 1) / nt) * nt;
+                    if (best_cost < 0 || cost <= best_cost) best = nt, best_cost = cost;
+                }
+                return best;
+            };
+            const bool fused_mask = vary && chunks == 1 && cols > 0;
+            // fused kernel: one 16-byte quad per thread and pass; plain kernel: two 32-byte loads per thread and pass
+            // (with a bitmap that leaves room for only a few CTAs per SM the kernels live on the bytes each CTA keeps in
+            // flight and keep the full 1024 threads: C4 measured 1.93 ms with 1024 against 1.95 ms with 896)
+            const int mask_threads = chunk_bits / 8 > 32 * 1024
+                                         ? kMaskThreads
+                                         : mask_cta(std::max({fused_mask ? cols / 4 : cols / 16, chunk_bits / 512, 1}));
+            if (fused_mask) {
                 VariationSpec pass = *vary;
                 pass.row_first += row0;
 #define GAPA_MASK_VARY(NT)                                                                                                  \
     GAPA_LAUNCH(k_pc_bitmask_vary<NT>, crows, NT, static_cast<size_t>(chunk_bits) / 8, stream, pass, cols, g_gene_map, n, \
                 words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>())
-                if (mask_threads == 128) GAPA_MASK_VARY(128);
-                else if (mask_threads == 256) GAPA_MASK_VARY(256);
-                else if (mask_threads == 512) GAPA_MASK_VARY(512);
-                else GAPA_MASK_VARY(1024);
+                switch (mask_threads) {
+                    case 128: GAPA_MASK_VARY(128); break;
+                    case 256: GAPA_MASK_VARY(256); break;
+                    case 384: GAPA_MASK_VARY(384); break;
+                    case 512: GAPA_MASK_VARY(512); break;
+                    case 640: GAPA_MASK_VARY(640); break;
+                    case 768: GAPA_MASK_VARY(768); break;
+                    case 896: GAPA_MASK_VARY(896); break;
+                    default: GAPA_MASK_VARY(1024); break;
+                }
 #undef GAPA_MASK_VARY
             } else {
                 if (vary) {
@@ -1174,10 +1203,16 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
     GAPA_LAUNCH(k_pc_bitmask<NT>, dim3(chunks, crows), NT, static_cast<size_t>(chunk_bits) / 8, stream, genes.from(row0),  \
                 g_gene_map, ctx->pool_size, n, chunk_bits, words_per_row, s->removed.as<word_t>(),                         \
                 s->removed_count.as<int>(), counters)
-                if (mask_threads == 128) GAPA_MASK(128);
-                else if (mask_threads == 256) GAPA_MASK(256);
-                else if (mask_threads == 512) GAPA_MASK(512);
-                else GAPA_MASK(1024);
+                switch (mask_threads) {
+                    case 128: GAPA_MASK(128); break;
+                    case 256: GAPA_MASK(256); break;
+                    case 384: GAPA_MASK(384); break;
+                    case 512: GAPA_MASK(512); break;
+                    case 640: GAPA_MASK(640); break;
+                    case 768: GAPA_MASK(768); break;
+                    case 896: GAPA_MASK(896); break;
+                    default: GAPA_MASK(1024); break;
+                }
 #undef GAPA_MASK
             }
             if (s->overlap_clear) {  // issued AFTER the mask kernel so that its CTAs only fill what that kernel leaves free
