@@ -202,36 +202,53 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_weights(const double* __restr
 // cumulative sum + weighted_pick (ga_ops.cpp:78-82, :113-126), one block.
 // Weights are half-integers with total <= s(s+1)/2 < 2^53: every partial sum is
 // exact, so the parallel scan equals the reference's sequential running total.
+static constexpr int kPickSmemRows = 24576;  // 192 KB of running totals
 __global__ void __launch_bounds__(1024) k_ga_pick(const double* __restrict__ weights, int s, uint64_t seed,
                                                   uint64_t generation, double* __restrict__ cumulative,
-                                                  int32_t* __restrict__ partner) {
-    __shared__ double part[1024];
-    const int tid = threadIdx.x, nt = blockDim.x;
-    const int per = (s + nt - 1) / nt;
-    const int lo = min(tid * per, s), hi = min(lo + per, s);
-    double sum = 0.0;
-    for (int i = lo; i < hi; ++i) sum += weights[i];
-    part[tid] = sum;
+                                                  int32_t* __restrict__ partner, int in_smem) {
+    // The running totals live in shared memory when they fit (s <= kPickSmemRows): the s binary searches below are
+    // chains of ~log2 s dependent reads, 30 ns each from shared memory against 300+ ns from L2.
+    extern __shared__ double pick_cum[];
+    __shared__ double warp_total[32];
+    __shared__ double carry_s;
+    const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
+    if (tid == 0) carry_s = 0.0;
     __syncthreads();
-    for (int off = 1; off < nt; off <<= 1) {
-        const double add = tid >= off ? part[tid - off] : 0.0;
+    for (int t0 = 0; t0 < s; t0 += 1024) {  // tile-wise inclusive scan: warp shuffles, warp totals, running carry
+        const int i = t0 + tid;
+        double v = i < s ? weights[i] : 0.0;
+        for (int off = 1; off < 32; off <<= 1) {
+            const double t = __shfl_up_sync(0xffffffffu, v, off);
+            if (lane >= off) v += t;
+        }
+        if (lane == 31) warp_total[wid] = v;
         __syncthreads();
-        part[tid] += add;
+        if (wid == 0) {
+            double t = warp_total[lane];
+            for (int off = 1; off < 32; off <<= 1) {
+                const double u = __shfl_up_sync(0xffffffffu, t, off);
+                if (lane >= off) t += u;
+            }
+            warp_total[lane] = t;
+        }
         __syncthreads();
+        v += carry_s + (wid > 0 ? warp_total[wid - 1] : 0.0);
+        if (i < s) {
+            cumulative[i] = v;
+            if (in_smem) pick_cum[i] = v;
+        }
+        __syncthreads();
+        if (tid == 1023) carry_s = v;
     }
-    double run = part[tid] - sum;
-    for (int i = lo; i < hi; ++i) {
-        run += weights[i];
-        cumulative[i] = run;
-    }
-    const double total = part[nt - 1];
     __syncthreads();
-    for (int i = tid; i < s; i += nt) {
+    const double total = carry_s;
+    const double* cum = in_smem ? pick_cum : cumulative;
+    for (int i = tid; i < s; i += 1024) {
         const double target = draw_unit(stream_key(seed, generation, GAPA_ROLE_SELECT, static_cast<uint64_t>(i)), 1) * total;
         int a = 0, b = s;  // std::upper_bound: first index with cumulative > target
         while (a < b) {
             const int mid = (a + b) >> 1;
-            if (cumulative[mid] <= target) a = mid + 1; else b = mid;
+            if (cum[mid] <= target) a = mid + 1; else b = mid;
         }
         partner[i] = min(a, s - 1);
     }
@@ -358,7 +375,11 @@ int launch_select(const double* fitness, int s, int minimize, uint64_t seed, uin
         return GAPA_CUDA_OK;
     }
     GAPA_LAUNCH(k_ga_weights, (s + kPerBlock - 1) / kPerBlock, kGaThreads, 0, st, fitness, s, minimize, weights, status);
-    GAPA_LAUNCH(k_ga_pick, 1, 1024, 0, st, weights, s, seed, generation, cumulative, partner);
+    const int in_smem = s <= kPickSmemRows ? 1 : 0;
+    const size_t pick_smem = in_smem ? sizeof(double) * static_cast<size_t>(s) : 0;
+    if (pick_smem > 48 * 1024)  // per device and cheap: set whenever the launch needs it
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_ga_pick, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(double) * kPickSmemRows));
+    GAPA_LAUNCH(k_ga_pick, 1, 1024, pick_smem, st, weights, s, seed, generation, cumulative, partner, in_smem);
     return GAPA_CUDA_OK;
 }
 int launch_crossover_mutate(const int32_t* pop, const int32_t* partner, int k, int row_first, int row_count, double pc,
