@@ -68,7 +68,7 @@ struct PcCounters {
 };
 
 struct PcScratch {
-    DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters, pass_flags, block_done;
+    DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters, block_done;
     DevBuf left_v, left_g, left_w, left_base, parent, comp_size, pc_extra, mcn_extra;
     size_t cap_entries = 0, cap_slots = 0;
     int prefix = 32768, interleave = 8, mask_chunks = 1, small_path = 1, relabel = -1, prefix_first4 = 1, trace = 0, prefix_cluster = 0;
@@ -444,7 +444,7 @@ __device__ __forceinline__ Rec gather_first4(const int32_t* __restrict__ row_ptr
 // in-flight window is the cluster, so a pass propagates almost like a sequential scan.
 __global__ void __launch_bounds__(kPrefixThreads)
     k_pc_prefix(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx, const int4* __restrict__ nbr4,
-                int first4_only, int n, int prefix, const word_t* __restrict__ alive, Rec* reached, int* pass_flags) {
+                int first4_only, int n, int prefix, const word_t* __restrict__ alive, Rec* reached) {
     cg::cluster_group cluster = cg::this_cluster();
     // the cluster size is a launch attribute: kPrefixCluster CTAs while every super-group's cluster is
     // resident at once, fewer when there are more super-groups than that (waves of idle-heavy clusters cost more)
@@ -453,7 +453,11 @@ __global__ void __launch_bounds__(kPrefixThreads)
     const int lane_in_cluster = static_cast<int>(cluster.block_rank()) * kPrefixThreads + threadIdx.x;
     const int kStride = csize * kPrefixThreads;
     Rec* reached_sg = reached + static_cast<size_t>(sg) * n;
-    int* flags = pass_flags + sg * 64;  // one flag per pass; zeroed by the host
+    // "did anything change in this pass" is exchanged through DISTRIBUTED SHARED MEMORY: every CTA stores its flag into
+    // slot [pass parity][own rank] of every CTA of the cluster, the cluster barrier publishes the stores, and each CTA
+    // reads its own copy — no global atomic, fence and L2 read on the critical path of a pass (3 of its ~5 us).
+    __shared__ int pass_any[2][kPrefixCluster];
+    const int my_rank = static_cast<int>(cluster.block_rank());
     const int stages[2] = {min(prefix, kPrefixCluster * kPrefixThreads / 4), prefix};
     int pass_id = 0;
     for (int s = 0; s < 2; ++s) {
@@ -495,10 +499,13 @@ __global__ void __launch_bounds__(kPrefixThreads)
                     any = 1;
                 }
             }
-            if (__syncthreads_or(any) && threadIdx.x == 0) atomicOr(&flags[pass_id], 1);
-            __threadfence();
-            cluster.sync();
-            if (!*reinterpret_cast<volatile int*>(&flags[pass_id])) break;
+            const int any_cta = __syncthreads_or(any);
+            int* slots = pass_any[pass_id & 1];
+            if (threadIdx.x < csize) *cluster.map_shared_rank(&slots[my_rank], threadIdx.x) = any_cta;
+            cluster.sync();  // release / acquire at cluster scope: the record stores of this pass and the flags
+            int any_cluster = 0;
+            for (int r = 0; r < csize; ++r) any_cluster |= slots[r];
+            if (!any_cluster) break;
         }
     }
 }
@@ -1232,8 +1239,6 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
             Rec* reached_rec = reinterpret_cast<Rec*>(reached);
             const int prefix = std::min(s->prefix, n);
             if (prefix > 0) {
-                GAPA_TRY(s->pass_flags.ensure(sizeof(int) * 64 * sgroups));
-                GAPA_CUDA_TRY(cudaMemsetAsync(s->pass_flags.ptr, 0, sizeof(int) * 64 * sgroups, stream));
                 // measured on B200 (tools/ab_prefix.sh): 8 CTAs per super-group up to 8 groups, 4 at 16-32, 2 at 64;
                 // beyond that every cluster must be resident at once (one CTA of this kernel per SM)
                 int csize = sgroups <= 8 ? kPrefixCluster : 4;
@@ -1248,7 +1253,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
                 attr.val.clusterDim.x = csize; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
                 cfg.attrs = &attr; cfg.numAttrs = 1;
                 GAPA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pc_prefix, g_row_ptr, g_col_idx, static_cast<const int4*>(s->nbr4.as<int4>()),
-                                                 s->prefix_first4, n, prefix, alive_rec, reached_rec, s->pass_flags.as<int>()));
+                                                 s->prefix_first4, n, prefix, alive_rec, reached_rec));
                 g_launches.fetch_add(1, std::memory_order_relaxed);
             }
             const int il = std::min(std::max(1, s->interleave / kPack), sgroups);
@@ -1330,7 +1335,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
 void pc_free(gapa_cuda_ctx* ctx) {
     if (!ctx->pc) return;
     PcScratch* s = ctx->pc;
-    for (DevBuf* b : {&s->nbr4, &s->removed, &s->removed_count, &s->alive, &s->reached, &s->entry_of, &s->unreached, &s->counters, &s->pass_flags, &s->block_done,
+    for (DevBuf* b : {&s->nbr4, &s->removed, &s->removed_count, &s->alive, &s->reached, &s->entry_of, &s->unreached, &s->counters, &s->block_done,
                       &s->left_v, &s->left_g, &s->left_w, &s->left_base, &s->parent, &s->comp_size, &s->pc_extra,
                       &s->mcn_extra})
         b->release();
