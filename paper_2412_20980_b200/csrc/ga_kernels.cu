@@ -234,7 +234,7 @@ __global__ void __launch_bounds__(1024) k_ga_pick(const double* __restrict__ wei
         __syncthreads();
         v += carry_s + (wid > 0 ? warp_total[wid - 1] : 0.0);
         if (i < s) {
-            cumulative[i] = v;
+            if (blockIdx.x == 0 || !in_smem) cumulative[i] = v;  // every block scans (cheap); one publishes the totals
             if (in_smem) pick_cum[i] = v;
         }
         __syncthreads();
@@ -243,7 +243,9 @@ __global__ void __launch_bounds__(1024) k_ga_pick(const double* __restrict__ wei
     __syncthreads();
     const double total = carry_s;
     const double* cum = in_smem ? pick_cum : cumulative;
-    for (int i = tid; i < s; i += 1024) {
+    // the picks are chains of dependent instructions (four mix64 for the stream key, log2 s search steps): with the
+    // totals in shared memory every block redoes the scan and then picks for its own 1024 rows, one row per thread
+    for (int i = blockIdx.x * 1024 + tid; i < s; i += gridDim.x * 1024) {
         const double target = draw_unit(stream_key(seed, generation, GAPA_ROLE_SELECT, static_cast<uint64_t>(i)), 1) * total;
         int a = 0, b = s;  // std::upper_bound: first index with cumulative > target
         while (a < b) {
@@ -379,7 +381,7 @@ int launch_select(const double* fitness, int s, int minimize, uint64_t seed, uin
     const size_t pick_smem = in_smem ? sizeof(double) * static_cast<size_t>(s) : 0;
     if (pick_smem > 48 * 1024)  // per device and cheap: set whenever the launch needs it
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_ga_pick, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(double) * kPickSmemRows));
-    GAPA_LAUNCH(k_ga_pick, 1, 1024, pick_smem, st, weights, s, seed, generation, cumulative, partner, in_smem);
+    GAPA_LAUNCH(k_ga_pick, in_smem ? (s + 1023) / 1024 : 1, 1024, pick_smem, st, weights, s, seed, generation, cumulative, partner, in_smem);
     return GAPA_CUDA_OK;
 }
 int launch_crossover_mutate(const int32_t* pop, const int32_t* partner, int k, int row_first, int row_count, double pc,
