@@ -71,7 +71,7 @@ struct PcScratch {
     DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters, block_done;
     DevBuf left_v, left_g, left_w, left_base, parent, comp_size, pc_extra, mcn_extra;
     size_t cap_entries = 0, cap_slots = 0;
-    int prefix = 32768, interleave = 8, mask_chunks = 1, small_path = 1, relabel = -1, prefix_first4 = 1, trace = 0, prefix_cluster = 0;
+    int prefix = 32768, interleave = 16, mask_chunks = 1, small_path = 1, relabel = -1, prefix_first4 = 1, trace = 0, prefix_cluster = 0;
     // hub-first internal vertex order for the bit-sliced path (see ensure_order)
     DevBuf ord_row_ptr, ord_col_idx, ord_gene_map;
     DevBuf nbr4;  // int4 per vertex: the first four entries of its (ascending) row, -1 padded — see gather_first4
@@ -1046,7 +1046,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
     if (!s->configured) {  // tuning knobs (defaults are what bench.py measures)
         s->prefix = env_int("GAPA_PC_PREFIX", 32768, 0, 1 << 24);
         s->prefix_cluster = env_int("GAPA_PC_PREFIX_CLUSTER", 0, 0, 8);  // 0 = choose by the number of super-groups
-        s->interleave = env_int("GAPA_PC_INTERLEAVE", 8, 1, 64);
+        s->interleave = env_int("GAPA_PC_INTERLEAVE", 16, 1, 64);  // measured: tools/ab_prefix_len.sh
         s->mask_chunks = env_int("GAPA_PC_MASK_CHUNKS", 1, 1, 64);
         s->relabel = env_int("GAPA_PC_RELABEL", -1, -1, 1);  // -1 automatic, 0 never, 1 always (tests)
         s->small_path = env_int("GAPA_PC_SMALL", 1, 0, 2);  // 0: never, 1: where it pays, 2: wherever it fits (tests)
