@@ -174,9 +174,29 @@ def cpu_reference_throughput(w: dict, target_seconds: float, threads: int) -> di
         if dt >= target_seconds / 3 or rows >= cap_rows:
             break
         rows = int(min(cap_rows, max(rows * 2, rows * (target_seconds / 2) / max(dt, 1e-3))))
-    return {"value": total_rows / total_t, "unit": "evals/s", "cores": threads, "kind": label,
+    return {"value": total_rows / total_t, "unit": "evals/s", "cores": threads, "kind": label, "rows": total_rows, "seconds": total_t,
             "sample": f"{total_rows} individuals of the workload evaluated once on {threads} host threads "
                       f"({'unmodified reference, dense BitMatrix' if use_ref else 'CSR port of the reference algorithm; the reference itself needs n^2/8 bytes per individual'}) in {total_t:.2f} s"}
+
+
+def workload_shape(w: dict) -> dict:
+    """n, m, k of a workload without touching a GPU (host generators of the product library: problem setup, CPU)."""
+    import paper_2412_20980_b200 as gp
+    kind, *gargs = w["graph"]
+    graph = {"ba": gp.barabasi_albert, "er": gp.erdos_renyi, "sbm": gp.planted_partition}[kind](*gargs)
+    if w["task"] == "lpa":
+        graph = gp.build_lp_split(graph, 0.1, 1).train
+    kindp = gp.PoolKind.NodeRemoval if w["task"] in ("pc", "mcn") else gp.PoolKind.EdgeRemoval
+    return {"n": graph.node_count(), "m": graph.edge_count(), "budget": gp.perturbation_budget(graph, kindp, w["rate"])}
+
+
+def config_of(w: dict, s: int, k: int, n: int, m: int, world: int, rows_per_rank: int) -> dict:
+    """the `config` object — identical keys and values in both arms"""
+    return {"workload": w["name"], "population": s, "budget": k, "n": n, "m": m,
+            "step": "one generation: select -> crossover+mutate -> evaluate(M_POP) -> elitism, population in HBM",
+            "parallelism": f"population rows sharded over {world} GPU(s), graph replicated, 1 fitness all-gather/generation",
+            "l2": "inputs larger than L2 (gene matrix %.0f MB + alive/reached words %.0f MB per step vs 126 MB L2)"
+                  % (4.0 * s * k / 1e6, 16.0 * n * ((rows_per_rank + 63) // 64) / 1e6)}
 
 
 def run_reference_arm(args, w):
@@ -186,18 +206,27 @@ def run_reference_arm(args, w):
     threads = host_threads()
     steps = max(args.steps, 1)
     per_step = min(60.0, 150.0 / (steps + args.warmup))
-    vals = []
+    vals, secs, rows = [], [], []
     base = None
     for i in range(args.warmup + steps):
         base = cpu_reference_throughput(w, per_step, threads)
         if i >= args.warmup:
             vals.append(base["value"])
-    value = float(np.mean(vals))
+            secs.append(base["seconds"])
+            rows.append(base["rows"])
+    value = float(np.sum(rows) / np.sum(secs))
     base["value"] = value
+    s = args.pop or w["pop"]
+    world = max(args.gpus, 1)
+    shape = workload_shape(w)
+    # A step of this arm is a BOUNDED SAMPLE of the workload's step (rows_per_step individuals of the population,
+    # evaluated once on the host cores): ms_per_step is the measured time of that sample, not of a whole generation.
     line = {"impl": "reference", "metric": "fitness_evals_per_sec", "value": value, "unit": "evals/s", "n_gpus": args.gpus,
-            "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * w["pop"] / value, "higher_is_better": True,
-            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-            "config": {"workload": w["name"], "population": w["pop"]},
+            "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(secs)), "rows_per_step": int(np.mean(rows)),
+            "step_is_sample": True, "ms_per_full_step_extrapolated": 1e3 * s / value,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "dtype": "int64" if w["task"] in ("pc", "mcn") else "f64", "data": "synthetic",
+            "config": config_of(w, s, shape["budget"], shape["n"], shape["m"], world, (s + world - 1) // world),
             "cpu_baseline": base,
             "e2e": {"value": value, "unit": "evals/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -215,9 +244,15 @@ def run_gpu_arm(args, w):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if not torch.cuda.is_available():
         raise SystemExit("bench.py: no CUDA device — the hot path has no CPU fallback")
+    if world != max(args.gpus, 1):
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
+    if torch.cuda.device_count() < world:
+        raise SystemExit(f"bench.py: --gpus {world} but only {torch.cuda.device_count()} CUDA device(s) are visible")
     torch.cuda.set_device(local)
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if rank == 0:
+            print(f"[bench] NCCL communicator: nranks={dist.get_world_size()} backend={dist.get_backend()}", file=sys.stderr, flush=True)
 
     kind, *gargs = w["graph"]
     graph = {"ba": gp.barabasi_albert, "er": gp.erdos_renyi, "sbm": gp.planted_partition}[kind](*gargs)
@@ -303,6 +338,26 @@ def run_gpu_arm(args, w):
     e2e_s = time.perf_counter() - t0
     assert np.array_equal(host_out[:hi - lo].numpy(), ga.fit[lo:hi].cpu().numpy()), "e2e result differs from the device path"
 
+    # N > 1: the sharded run must BE the 1-GPU run (test_parallel.cpp:86-104): rank 0 repeats the same generations
+    # unsharded with the same seed and compares history and final population bit for bit.
+    verify = None
+    if world > 1:
+        mine = ga.result()
+        if rank == 0:
+            solo = ShardedGa(params, CudaOps(obj, local), Shard(0, 1, s), torch_allgather())
+            solo.initialize()
+            for _ in range(ga.generation):
+                solo.step()
+            ref = solo.result()
+            g = ga.generation
+            verify = {"generations": g,
+                      "history_best_equal": bool(np.array_equal(mine.history_best[:g], ref.history_best[:g])),
+                      "history_mean_equal": bool(np.array_equal(mine.history_mean[:g], ref.history_mean[:g])),
+                      "final_population_equal": bool(np.array_equal(mine.final_population, ref.final_population)),
+                      "final_fitness_equal": bool(np.array_equal(mine.final_fitness, ref.final_fitness))}
+            del solo
+        barrier()
+
     times = torch.tensor([step_ms_total, e2e_s * 1e3, float(np.mean(pure_ms)), float(np.mean(eval_ms))], dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
@@ -316,37 +371,37 @@ def run_gpu_arm(args, w):
         b_eval = algorithmic_bytes(task, n, m, k, T, P, dbar)
         peak, peak_src = peaks()
         rows_per_rank = shard.block
-        achieved = b_eval * rows_per_rank / (eval_ms_mean * 1e-3) / 1e9
-        traffic = None
+        survey = b_eval * rows_per_rank / (eval_ms_mean * 1e-3) / 1e9
+        traffic = traffic_src = None
         try:
             with open(os.path.join(ROOT, "profiles", "dram_traffic.json")) as f:
-                traffic = json.load(f).get(args.workload)
+                entry = json.load(f).get(args.workload if not args.pop else f"{args.workload}@{args.pop}")
+            if isinstance(entry, dict):
+                traffic, traffic_src = entry.get("bytes"), entry.get("source")
+            elif entry:
+                traffic = entry
         except Exception:
             pass
-        actual = None
-        if traffic:
-            # ncu-measured DRAM bytes of one full-population evaluation, scaled to this rank's rows
-            actual = traffic * (rows_per_rank / s) / (eval_ms_mean * 1e-3) / 1e9
-        batched = None
         if task in ("pc", "mcn"):
-            # what the bit-sliced algorithm itself has to move for this rank's batch: the CSR once per super-group of
-            # 256 individuals (one pass serves all of them), and per individual its genome, its removal bitmap
-            # (written, then read by the transpose) and its share of the alive / reached words (written + read)
+            # What the bit-sliced algorithm has to move for this rank's batch: the CSR once per super-group
+            # of 256 individuals (one pass serves all of them), and per individual its genome (4k), its removal bitmap
+            # (written, read by the transpose: 2 n/8), its alive bits (written + read: 2 n/8) and its reached bits
+            # (cleared, read, written: 3 n/8).
             sg = (rows_per_rank + 255) // 256
-            b_batched = sg * (4 * (n + 1) + 8 * m) + rows_per_rank * (4 * k + 2 * ((n + 7) // 8) + 4 * (n / 8.0))
-            batched = {"bytes": b_batched, "achieved": b_batched / (eval_ms_mean * 1e-3) / 1e9,
-                       "frac": b_batched / (eval_ms_mean * 1e-3) / 1e9 / peak,
-                       "note": "algorithmic bytes of the BATCHED algorithm (CSR read once per 256 individuals): the figure to "
-                               "hold against the HBM peak; `frac` above uses SURVEY 8(d)'s per-individual bytes"}
+            b_algo = sg * (4 * (n + 1) + 8 * m) + rows_per_rank * (4 * k + 7 * (n / 8.0))
+            algo_note = ("batched algorithm: CSR once per 256 individuals + per individual 4k genome + 7 n/8 bitmap / alive / reached "
+                         "bytes (the clear of the reached records included)")
+        else:
+            b_algo = b_eval * rows_per_rank
+            algo_note = "SURVEY 8(d) bytes per evaluation x evaluations per launch sequence (working set is L2-resident: no roofline claim)"
+        achieved = b_algo / (eval_ms_mean * 1e-3) / 1e9
+        # ncu-measured DRAM bytes of one full-population evaluation (tools/ncu_traffic.py), scaled to this rank's rows
+        actual = traffic * (rows_per_rank / s) / (eval_ms_mean * 1e-3) / 1e9 if traffic else None
         line = {
             "metric": "fitness_evals_per_sec", "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
             "vs_baseline": None, "dtype": "int64" if task in ("pc", "mcn") else "f64", "data": "synthetic",
-            "config": {"workload": w["name"], "population": s, "budget": k, "n": n, "m": m,
-                       "step": "one generation: select -> crossover+mutate -> evaluate(M_POP) -> elitism, population in HBM",
-                       "parallelism": f"population rows sharded over {world} GPU(s), graph replicated, 1 fitness all-gather/generation",
-                       "l2": "inputs larger than L2 (gene matrix %.0f MB + alive/reached words %.0f MB per step vs 126 MB L2)"
-                             % (4.0 * s * k / 1e6, 16.0 * n * ((rows_per_rank + 63) // 64) / 1e6)},
+            "config": config_of(w, s, k, n, m, world, rows_per_rank),
             "generations_per_sec": 1e3 / ms_per_step,
             "fitness_eval_ms_per_step": eval_ms_mean,
             "variation_plus_eval_ms_per_step": fused_ms_mean,
@@ -356,18 +411,22 @@ def run_gpu_arm(args, w):
                     "path": "gapa_cuda_eval_batch(host genes) -> host fitness (FitnessFunction::evaluate_batch boundary)"},
             "gpu_launches": int(launches),
             "clocks": clocks,
+            "comm": {"backend": "nccl" if world > 1 else None, "nranks": world},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
-                         "traffic": traffic, "peak_source": peak_src,
+                         "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                          "kernel": "fitness evaluation pipeline (k_pc_sweep dominant)" if task in ("pc", "mcn") else f"{task} fitness pipeline",
-                         "algorithmic_bytes_per_eval": b_eval,
+                         "algorithmic_bytes_per_launch": b_algo, "algorithmic_bytes_model": algo_note,
                          "actual_dram_gbs": actual, "actual_dram_frac": (actual / peak) if actual else None,
-                         "batched": batched,
-                         "note": "achieved = SURVEY §8(d) bytes/eval x evals per batch / device time of the whole evaluation "
-                                 "(CUDA events on the launch stream). frac > 1 by construction: 256 individuals share one pass "
-                                 "over the CSR (bit-sliced records), while §8(d) charges every individual its own pass. "
-                                 "traffic = ncu dram bytes of one evaluation of the full population (profiles/dram_traffic.json); "
-                                 "actual_dram_* = that traffic / the same device time, i.e. the real HBM utilisation."},
+                         "vs_survey_model": {"bytes_per_eval": b_eval, "achieved": survey, "frac": survey / peak,
+                                             "note": "SURVEY 8(d) charges every individual a private pass over the CSR; the bit-sliced "
+                                                     "kernels share one pass among 256 individuals, so this ratio exceeds 1 and is NOT "
+                                                     "a fraction of the HBM peak"},
+                         "note": "achieved = algorithmic bytes of the launch sequence / device time of the whole evaluation (CUDA events "
+                                 "on the launch stream); traffic = ncu dram__bytes_read+write of the same launch sequence "
+                                 "(profiles/dram_traffic.json, produced by tools/ncu_traffic.py); actual_dram_* = traffic / the same time"},
         }
+        if verify is not None:
+            line["verify"] = verify
         if world == 1:
             # the same generations through the in-library loop (gapa_cuda_run: no host round trip per
             # operator) — what a C++ host gets from run_ga_cuda(); reported beside the stepwise driver
@@ -397,8 +456,20 @@ def main():
     w = WORKLOADS[args.workload]
     if args.impl == "reference":
         run_reference_arm(args, w)
-    else:
-        run_gpu_arm(args, w)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        # `python bench.py --gpus N` on its own: re-launch under torch.distributed.run, one rank per GPU
+        import socket
+        with socket.socket() as sock:
+            sock.bind(("127.0.0.1", 0))
+            port = sock.getsockname()[1]
+        env = dict(os.environ)
+        env.setdefault("NCCL_DEBUG", "INFO")  # the communicator's "nranks N" line goes to stderr
+        env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+        cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+               "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+        raise SystemExit(subprocess.call(cmd, env=env))
+    run_gpu_arm(args, w)
 
 
 if __name__ == "__main__":

@@ -65,13 +65,38 @@ struct PcCounters {
     unsigned int n_incomplete;  // 256-vertex chunks the recording sweep still has to visit
     int deferred;  // the recording sweep declined to run: too much is still unreached and the sweeps still progress
     unsigned int n_left;  // (vertex, super-group) pairs with unreached individuals after the last ordinary sweep
+    int phase2_skipped;   // k_pc_final: more leftover entries than its single CTA takes on (host copy only)
 };
 
-struct PcScratch {
+// Scratch of ONE lane in flight (a lane = a contiguous block of whole 64-individual groups that goes through the
+// pipeline together).  Lanes that run on the same stream reuse the set, so its buffers stay L2-warm.
+struct PcSet {
     DevBuf removed, removed_count, alive, reached, entry_of, unreached, counters, block_done;
     DevBuf left_v, left_g, left_w, left_base, parent, comp_size, pc_extra, mcn_extra;
     size_t cap_entries = 0, cap_slots = 0;
+    cudaStream_t stream = nullptr;  // the lane stream (multi-lane evaluations); single-lane ones run on the caller's
+    // side stream that clears the `reached` records while the mask build runs (the two do not touch the same memory)
+    cudaStream_t aux = nullptr;
+    cudaEvent_t ev_pass_begin = nullptr, ev_cleared = nullptr, ev_done = nullptr;
+    // the accumulators (giant slots, unreached / removed counts, extras, counters) are as a reset leaves them: the last
+    // lane on this set ended in k_pc_final, which cleans up after itself
+    int clean_slots = 0;  // how many accumulator slots (individuals) are in that state
+};
+
+static constexpr int kMaxLanes = 64;
+static constexpr unsigned kFusedPhase2Entries = 4096;  // leftover entries k_pc_final's single CTA resolves itself  // lanes per wave (pinned counter slots)
+
+struct PcScratch {
+    std::vector<PcSet*> sets;
+    PcCounters* h_counters = nullptr;  // pinned, kMaxLanes slots: each lane's counters after its last kernel
+    cudaEvent_t ev_fork = nullptr;
     int prefix = 32768, interleave = 16, mask_chunks = 1, small_path = 1, relabel = -1, prefix_first4 = 1, trace = 0, prefix_cluster = 0;
+    int lane_rows = 4096, lane_streams = 2;
+    // Rounds of sweeps the speculative (host-free) schedule enqueues; learned from the evaluations that needed the
+    // host-driven loop.  0 = this graph needs more rounds than it pays to enqueue blindly: always host-driven.
+    int spec_rounds = 1;
+    bool phase2_big = false;  // the speculative schedule uses the three full-grid phase-2 kernels (learned: k_pc_final declined once)
+    size_t fold_clear_bytes = 16u << 20;  // reached records up to this size are cleared by the transpose kernel
     // hub-first internal vertex order for the bit-sliced path (see ensure_order)
     DevBuf ord_row_ptr, ord_col_idx, ord_gene_map;
     DevBuf nbr4;  // int4 per vertex: the first four entries of its (ascending) row, -1 padded — see gather_first4
@@ -79,9 +104,6 @@ struct PcScratch {
     unsigned long long ord_pool_version = ~0ull;
     std::vector<int32_t> perm;  // original vertex -> internal vertex when relabelled
     bool configured = false;
-    // side stream that clears the `reached` records while the mask build runs (the two do not touch the same memory)
-    cudaStream_t aux = nullptr;
-    cudaEvent_t ev_pass_begin = nullptr, ev_cleared = nullptr;
     int overlap_clear = 1;
 };
 
@@ -256,7 +278,8 @@ __global__ void __launch_bounds__(nt) k_pc_bitmask_vary(VariationSpec V, int k, 
 // record (sg, v) belongs to group 4 sg + gi.  32 bytes is exactly one memory sector: a
 // neighbour read fetches 256 individuals of state per sector instead of 64.
 __global__ void __launch_bounds__(kTransThreads) k_pc_transpose(const word_t* __restrict__ removed, int words_per_row,
-                                                                int n, int rows, word_t* __restrict__ alive) {
+                                                                int n, int rows, word_t* __restrict__ alive,
+                                                                word_t* __restrict__ clear_reached) {
     word_t* tile = reinterpret_cast<word_t*>(pc_smem_bits);  // kBits x (kTransThreads + 1) words, padded against bank conflicts
     const int g = blockIdx.y;
     const int vb0 = blockIdx.x * kTransThreads;
@@ -288,7 +311,11 @@ __global__ void __launch_bounds__(kTransThreads) k_pc_transpose(const word_t* __
     const int v_base = vb0 * kBits;
     for (int idx = threadIdx.x; idx < kTransThreads * kBits; idx += kTransThreads) {
         const int v = v_base + idx;
-        if (v < n) out[v] = tile[(idx & 63) * (kTransThreads + 1) + (idx >> 6)];
+        if (v < n) {
+            out[v] = tile[(idx & 63) * (kTransThreads + 1) + (idx >> 6)];
+            // small batches: this group's word of the vertex's reached record is cleared here instead of by a launch of its own
+            if (clear_reached) clear_reached[(static_cast<size_t>(g / kPack) * n + v) * kPack + (g % kPack)] = 0ull;
+        }
     }
 }
 
@@ -444,7 +471,8 @@ __device__ __forceinline__ Rec gather_first4(const int32_t* __restrict__ row_ptr
 // in-flight window is the cluster, so a pass propagates almost like a sequential scan.
 __global__ void __launch_bounds__(kPrefixThreads)
     k_pc_prefix(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx, const int4* __restrict__ nbr4,
-                int first4_only, int n, int prefix, const word_t* __restrict__ alive, Rec* reached) {
+                int first4_only, int n, int prefix, const word_t* __restrict__ alive, Rec* reached, int pick_sources,
+                const int32_t* __restrict__ by_degree, int rows) {
     cg::cluster_group cluster = cg::this_cluster();
     // the cluster size is a launch attribute: kPrefixCluster CTAs while every super-group's cluster is
     // resident at once, fewer when there are more super-groups than that (waves of idle-heavy clusters cost more)
@@ -453,6 +481,27 @@ __global__ void __launch_bounds__(kPrefixThreads)
     const int lane_in_cluster = static_cast<int>(cluster.block_rank()) * kPrefixThreads + threadIdx.x;
     const int kStride = csize * kPrefixThreads;
     Rec* reached_sg = reached + static_cast<size_t>(sg) * n;
+    if (pick_sources) {
+        // k_pc_source folded in (one launch less): a warp per individual of this super-group marks the first alive
+        // vertex in descending-degree order; the cluster barrier publishes the marks before the first pass
+        const int warps = kStride >> 5, lane = threadIdx.x & 31;
+        for (int r = lane_in_cluster >> 5; r < kPack * kBits; r += warps) {
+            const int row = sg * kPack * kBits + r;
+            if (row >= rows) break;
+            const int g = row >> 6;
+            const word_t bit = 1ull << (row & 63);
+            for (int i = 0; i < n; i += 32) {
+                const int v = i + lane < n ? (by_degree ? by_degree[i + lane] : i + lane) : -1;
+                const bool ok = v >= 0 && (alive[static_cast<size_t>(g) * n + v] & bit);
+                const unsigned hit = __ballot_sync(0xffffffffu, ok);
+                if (hit) {
+                    if (lane == __ffs(hit) - 1) atomicOr(&reinterpret_cast<word_t*>(reached)[word_index(g, n, v)], bit);
+                    break;
+                }
+            }
+        }
+        cluster.sync();
+    }
     // "did anything change in this pass" is exchanged through DISTRIBUTED SHARED MEMORY: every CTA stores its flag into
     // slot [pass parity][own rank] of every CTA of the cluster, the cluster barrier publishes the stores, and each CTA
     // reads its own copy — no global atomic, fence and L2 read on the critical path of a pass (3 of its ~5 us).
@@ -463,7 +512,7 @@ __global__ void __launch_bounds__(kPrefixThreads)
     for (int s = 0; s < 2; ++s) {
         const int limit = stages[s];
         if (s == 1 && limit == stages[0]) break;
-        for (int pass = 0; pass < 24; ++pass, ++pass_id) {
+        for (int pass = 0; pass < 24; ++pass) {
             int any = 0;
             for (int v = lane_in_cluster; v < limit; v += kStride) {
                 Rec mine = load_rec(&reached_sg[v]);
@@ -505,6 +554,9 @@ __global__ void __launch_bounds__(kPrefixThreads)
             cluster.sync();  // release / acquire at cluster scope: the record stores of this pass and the flags
             int any_cluster = 0;
             for (int r = 0; r < csize; ++r) any_cluster |= slots[r];
+            // the parity advances on EVERY pass, the last one of a stage included: the next pass (of either stage) must not
+            // write the slots that slower threads of other CTAs may still be reading
+            ++pass_id;
             if (!any_cluster) break;
         }
     }
@@ -726,86 +778,164 @@ __device__ __forceinline__ int slot_of(int slot0, int base, word_t w, int b) {
     return slot0 + base + __popcll(w & ((1ull << b) - 1ull));
 }
 
-__global__ void __launch_bounds__(kThreads) k_pc_hook(const int32_t* __restrict__ row_ptr,
-                                                      const int32_t* __restrict__ col_idx, int n,
-                                                      const word_t* __restrict__ alive,
-                                                      const word_t* __restrict__ reached,
-                                                      const int32_t* __restrict__ entry_of,
-                                                      const int32_t* __restrict__ left_v,
-                                                      const int32_t* __restrict__ left_g,
-                                                      const word_t* __restrict__ left_w,
-                                                      const int32_t* __restrict__ left_base, int32_t* parent,
-                                                      int slot0, const PcCounters* counters) {
-    const unsigned total = counters->n_entries;
-    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-        const int v = left_v[e], g = left_g[e], base_v = left_base[e];
-        const word_t w = left_w[e];
-        for (int i = row_ptr[v]; i < row_ptr[v + 1]; ++i) {
-            const int u = col_idx[i];
+// The speculative schedule launches phase 2 before the host has looked at the counters: it stands down when the
+// recording sweep overflowed its buffers, declined to run, or asks for more sweeps (the host then redoes the lane with
+// the host-driven loop).  The host-driven loop passes many = ~0u: it only launches phase 2 once those are settled.
+__device__ __forceinline__ bool pc_stand_down(const PcCounters* c, unsigned many) {
+    return c->overflow || c->deferred || (c->changed && c->n_entries > many);
+}
+
+struct Phase2Args {
+    const int32_t* row_ptr;
+    const int32_t* col_idx;
+    int n;
+    const word_t* alive;
+    const word_t* reached;
+    const int32_t* entry_of;
+    const int32_t* left_v;
+    const int32_t* left_g;
+    const word_t* left_w;
+    const int32_t* left_base;
+    int32_t* parent;
+    int32_t* comp_size;
+    int slot0;
+    unsigned long long* pc_extra;
+    int* mcn_extra;
+    const PcCounters* counters;
+};
+
+// entries first, first + stride, ... < total
+__device__ __forceinline__ void pc_hook_body(const Phase2Args& P, unsigned first, unsigned stride, unsigned total) {
+    const int n = P.n, slot0 = P.slot0;
+    for (unsigned e = first; e < total; e += stride) {
+        const int v = P.left_v[e], g = P.left_g[e], base_v = P.left_base[e];
+        const word_t w = P.left_w[e];
+        for (int i = P.row_ptr[v]; i < P.row_ptr[v + 1]; ++i) {
+            const int u = P.col_idx[i];
             const size_t iu = word_index(g, n, u);
-            const word_t common = w & alive[static_cast<size_t>(g) * n + u];
+            const word_t common = w & P.alive[static_cast<size_t>(g) * n + u];
             if (!common) continue;
-            const word_t ru = reached[iu];
+            const word_t ru = P.reached[iu];
             word_t attach = common & ru;  // v was not reached but its neighbour was: v belongs to the giant
             while (attach) {
                 const int b = __ffsll(static_cast<long long>(attach)) - 1;
                 attach &= attach - 1;
-                uf_union(parent, slot_of(slot0, base_v, w, b), g * kBits + b);
+                uf_union(P.parent, slot_of(slot0, base_v, w, b), g * kBits + b);
             }
             word_t rest = common & ~ru;
             if (rest && u < v) {  // leftover-leftover edges are seen from both ends; take one
-                const int eu = entry_of[iu];
-                const word_t wu = left_w[eu];
-                const int base_u = left_base[eu];
+                const int eu = P.entry_of[iu];
+                const word_t wu = P.left_w[eu];
+                const int base_u = P.left_base[eu];
                 while (rest) {
                     const int b = __ffsll(static_cast<long long>(rest)) - 1;
                     rest &= rest - 1;
-                    uf_union(parent, slot_of(slot0, base_v, w, b), slot_of(slot0, base_u, wu, b));
+                    uf_union(P.parent, slot_of(slot0, base_v, w, b), slot_of(slot0, base_u, wu, b));
                 }
             }
         }
     }
 }
-
-__global__ void __launch_bounds__(kThreads) k_pc_count(const word_t* __restrict__ left_w,
-                                                       const int32_t* __restrict__ left_base, int32_t* parent,
-                                                       int32_t* comp_size, int slot0, const PcCounters* counters) {
-    const unsigned total = counters->n_entries;
-    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-        const int cnt = __popcll(left_w[e]);
-        for (int i = 0; i < cnt; ++i) atomicAdd(&comp_size[uf_find(parent, slot0 + left_base[e] + i)], 1);
+__device__ __forceinline__ void pc_count_body(const Phase2Args& P, unsigned first, unsigned stride, unsigned total) {
+    for (unsigned e = first; e < total; e += stride) {
+        const int cnt = __popcll(P.left_w[e]);
+        for (int i = 0; i < cnt; ++i) atomicAdd(&P.comp_size[uf_find(P.parent, P.slot0 + P.left_base[e] + i)], 1);
     }
 }
-
-__global__ void __launch_bounds__(kThreads) k_pc_reduce(const int32_t* __restrict__ left_g,
-                                                        const word_t* __restrict__ left_w,
-                                                        const int32_t* __restrict__ left_base,
-                                                        const int32_t* __restrict__ parent,
-                                                        const int32_t* __restrict__ comp_size, int slot0,
-                                                        unsigned long long* pc_extra, int* mcn_extra,
-                                                        const PcCounters* counters) {
-    const unsigned total = counters->n_entries;
-    for (unsigned e = blockIdx.x * blockDim.x + threadIdx.x; e < total; e += gridDim.x * blockDim.x) {
-        word_t w = left_w[e];
-        const int g = left_g[e];
-        int slot = slot0 + left_base[e];
+__device__ __forceinline__ void pc_reduce_body(const Phase2Args& P, unsigned first, unsigned stride, unsigned total) {
+    for (unsigned e = first; e < total; e += stride) {
+        word_t w = P.left_w[e];
+        const int g = P.left_g[e];
+        int slot = P.slot0 + P.left_base[e];
         while (w) {
             const int b = __ffsll(static_cast<long long>(w)) - 1;
             w &= w - 1;
-            if (parent[slot] == slot) {  // a root that is not a giant node
-                const unsigned long long s = static_cast<unsigned long long>(comp_size[slot]);
-                atomicAdd(&pc_extra[g * kBits + b], s * (s - 1ull) / 2ull);
-                atomicMax(&mcn_extra[g * kBits + b], static_cast<int>(s));
+            if (P.parent[slot] == slot) {  // a root that is not a giant node
+                const unsigned long long s = static_cast<unsigned long long>(P.comp_size[slot]);
+                atomicAdd(&P.pc_extra[g * kBits + b], s * (s - 1ull) / 2ull);
+                atomicMax(&P.mcn_extra[g * kBits + b], static_cast<int>(s));
             }
             ++slot;
         }
     }
 }
 
+__global__ void __launch_bounds__(kThreads) k_pc_hook(Phase2Args P, unsigned many) {
+    if (pc_stand_down(P.counters, many)) return;
+    pc_hook_body(P, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, P.counters->n_entries);
+}
+__global__ void __launch_bounds__(kThreads) k_pc_count(Phase2Args P, unsigned many) {
+    if (pc_stand_down(P.counters, many)) return;
+    pc_count_body(P, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, P.counters->n_entries);
+}
+__global__ void __launch_bounds__(kThreads) k_pc_reduce(Phase2Args P, unsigned many) {
+    if (pc_stand_down(P.counters, many)) return;
+    pc_reduce_body(P, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, P.counters->n_entries);
+}
+
 // pairwise_connectivity / largest_component_size (components.cpp:49-62) -> double
 // (fitness.cpp:25,32).  giant = n - removed - unreached + leftovers attached to it;
 // every vertex outside the giant and outside the union-find components is a
 // singleton: 0 pairs, size 1.
+__device__ __forceinline__ double pc_result_of(int n, int task, int removed, int unreached, int attached, unsigned long long pc_extra,
+                                               int mcn_extra) {
+    const long long giant = static_cast<long long>(n) - removed - unreached + attached;
+    if (task == GAPA_TASK_PC) return static_cast<double>(static_cast<unsigned long long>(giant * (giant - 1) / 2) + pc_extra);
+    long long best = giant > mcn_extra ? giant : mcn_extra;
+    if (n > 0 && best < 1) best = 1;
+    return static_cast<double>(best);
+}
+
+// Last kernel of a speculatively scheduled lane, ONE CTA: phase 2 when the recording sweep left at most `fused_limit`
+// entries (the benchmark graphs leave none: three launches saved), the result of every row, the lane's counters into
+// pinned host memory (no copy operation), and the reset of everything the next lane on this scratch set accumulates
+// into (no reset launch, no memset).  do_phase2 == 0: the three full-grid kernels have already run.
+static constexpr int kFinalThreads = 1024;
+__global__ void __launch_bounds__(kFinalThreads) k_pc_final(Phase2Args P, unsigned many, unsigned fused_limit, int do_phase2, int rows,
+                                                            int task, int* removed_count, int* unreached, double* out,
+                                                            PcCounters* counters, PcCounters* host_out, int reset_slots) {
+    __shared__ PcCounters c;
+    __shared__ int skipped;
+    const unsigned tid = threadIdx.x;
+    if (tid == 0) {
+        c = *counters;
+        skipped = 0;
+    }
+    __syncthreads();
+    if (!pc_stand_down(&c, many)) {
+        if (do_phase2 && c.n_entries) {
+            if (c.n_entries <= fused_limit) {
+                pc_hook_body(P, tid, kFinalThreads, c.n_entries);
+                __syncthreads();
+                pc_count_body(P, tid, kFinalThreads, c.n_entries);
+                __syncthreads();
+                pc_reduce_body(P, tid, kFinalThreads, c.n_entries);
+            } else if (tid == 0) {
+                skipped = 1;
+            }
+        }
+        __syncthreads();
+        if (!skipped)
+            for (int r = tid; r < rows; r += kFinalThreads)
+                out[r] = pc_result_of(P.n, task, removed_count[r], unreached[r], P.comp_size[r], P.pc_extra[r], P.mcn_extra[r]);
+    }
+    __syncthreads();
+    if (tid == 0) {
+        c.phase2_skipped = skipped;
+        *host_out = c;
+        PcCounters zero{};
+        *counters = zero;
+    }
+    for (int i = tid; i < reset_slots; i += kFinalThreads) {
+        P.parent[i] = i;
+        P.comp_size[i] = 0;
+        unreached[i] = 0;
+        P.pc_extra[i] = 0ull;
+        P.mcn_extra[i] = 0;
+        removed_count[i] = 0;
+    }
+}
+
 __global__ void __launch_bounds__(kThreads) k_pc_result(int n, int rows, int task, const int* __restrict__ removed_count,
                                                         const int* __restrict__ unreached,
                                                         const int32_t* __restrict__ comp_size,
@@ -813,15 +943,7 @@ __global__ void __launch_bounds__(kThreads) k_pc_result(int n, int rows, int tas
                                                         const int* __restrict__ mcn_extra, double* out) {
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
-    const long long giant = static_cast<long long>(n) - removed_count[r] - unreached[r] + comp_size[r];
-    if (task == GAPA_TASK_PC) {
-        const unsigned long long pairs = static_cast<unsigned long long>(giant * (giant - 1) / 2) + pc_extra[r];
-        out[r] = static_cast<double>(pairs);
-    } else {
-        long long best = giant > mcn_extra[r] ? giant : mcn_extra[r];
-        if (n > 0 && best < 1) best = 1;
-        out[r] = static_cast<double>(best);
-    }
+    out[r] = pc_result_of(n, task, removed_count[r], unreached[r], comp_size[r], pc_extra[r], mcn_extra[r]);
 }
 
 // reset of everything the final sweep / phase 2 accumulate into
@@ -946,7 +1068,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_pc_small(GeneRows genes,
 }
 
 // ---------------------------------------------------------------------------------
-static int ensure_phase2(PcScratch* s, int groups, size_t entries, size_t slots) {
+static int ensure_phase2(PcSet* s, int groups, size_t entries, size_t slots) {
     const size_t giant = static_cast<size_t>(groups) * kBits;
     GAPA_TRY(s->left_v.ensure(sizeof(int32_t) * entries));
     GAPA_TRY(s->left_g.ensure(sizeof(int32_t) * entries));
@@ -1038,6 +1160,301 @@ static int ensure_order(gapa_cuda_ctx* ctx, PcScratch* s) {
     return GAPA_CUDA_OK;
 }
 
+// clear of the reached records (a kernel rather than cudaMemsetAsync so that profilers list it with its DRAM bytes)
+__global__ void __launch_bounds__(kThreads) k_pc_clear(Rec* __restrict__ recs, size_t count) {
+    const Rec zero{};
+    for (size_t i = static_cast<size_t>(blockIdx.x) * kThreads + threadIdx.x; i < count; i += static_cast<size_t>(gridDim.x) * kThreads)
+        store_rec(&recs[i], zero);
+}
+
+// ---------------------------------------------------------------------------------
+// One lane = `crows` individuals (whole 64-individual groups) taken through the whole pipeline on `stream` with the
+// scratch of `set`.  Two schedules:
+//   * speculative (spec_rounds >= 1): everything — masks, prefix closure, `spec_rounds` rounds of sweeps, the recording
+//     sweep, phase 2 and the result — is enqueued without the host ever looking at the device; the lane's counters
+//     land in pinned memory after the last kernel and the caller checks them once, when the whole evaluation has been
+//     enqueued.  Phase 2 stands down on the device when the recording sweep overflowed / declined / wants more sweeps
+//     (pc_stand_down), and the caller then redoes the lane host-driven.  No host round trip sits inside an evaluation,
+//     so lanes on different streams overlap freely (the integer-bound mask build of one lane under the HBM-bound
+//     sweeps of another).
+//   * host-driven (spec_rounds == 0): sweep rounds until the counters say phase 2 can finish (graphs without a hub
+//     core, high-diameter graphs, buffer growth after an overflow).  *rounds_used reports what it took.
+struct PcLaneJob {
+    int task;
+    GeneRows genes;          // the whole batch
+    int row0, crows;         // this lane's rows
+    double* out_dev;         // the whole batch
+    bool trusted;
+    const VariationSpec* vary;
+};
+
+static int pc_set_create(PcSet** out) {
+    PcSet* set = new PcSet();
+    *out = set;
+    // lowest priority for the clear: it yields to every kernel of the work streams
+    int least = 0, greatest = 0;
+    GAPA_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    GAPA_CUDA_TRY(cudaStreamCreateWithPriority(&set->aux, cudaStreamNonBlocking, least));
+    GAPA_CUDA_TRY(cudaStreamCreateWithFlags(&set->stream, cudaStreamNonBlocking));
+    GAPA_CUDA_TRY(cudaEventCreateWithFlags(&set->ev_pass_begin, cudaEventDisableTiming));
+    GAPA_CUDA_TRY(cudaEventCreateWithFlags(&set->ev_cleared, cudaEventDisableTiming));
+    GAPA_CUDA_TRY(cudaEventCreateWithFlags(&set->ev_done, cudaEventDisableTiming));
+    return GAPA_CUDA_OK;
+}
+
+static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLaneJob& job, cudaStream_t stream, int spec_rounds,
+                       PcCounters* h_out, int* rounds_used) {
+    const int n = ctx->n, sm = ctx->sm_count, cols = job.genes.cols;
+    const int row0 = job.row0, crows = job.crows;
+    const int32_t* g_row_ptr = s->ord_relabeled ? s->ord_row_ptr.as<int32_t>() : ctx->d_row_ptr;
+    const int32_t* g_col_idx = s->ord_relabeled ? s->ord_col_idx.as<int32_t>() : ctx->d_col_idx;
+    const int32_t* g_gene_map = s->ord_relabeled ? s->ord_gene_map.as<int32_t>() : (ctx->pool_identity ? nullptr : ctx->d_pool_map);
+    const int32_t* g_by_degree = s->ord_relabeled ? nullptr : ctx->d_by_degree;
+    const int words_per_row = std::max(1, (n + 63) / 64);
+    int chunk_bits = std::min(words_per_row * 64, 192 * 1024 * 8);  // <= 192 KB of shared memory
+    if (s->mask_chunks > 1) chunk_bits = std::min(chunk_bits, ((words_per_row + s->mask_chunks - 1) / s->mask_chunks) * 64);
+    const int chunks = (words_per_row * 64 + chunk_bits - 1) / chunk_bits;
+    const int groups = (crows + kBits - 1) / kBits;
+    const int sgroups = (groups + kPack - 1) / kPack;  // 4 groups share one 32-byte vertex record
+    const int pgroups = sgroups * kPack;
+    const size_t words = static_cast<size_t>(pgroups) * std::max(n, 1);
+    auto accumulators = [&]() {  // a buffer that had to grow comes back uninitialised
+        return reinterpret_cast<uintptr_t>(set->removed_count.ptr) ^ reinterpret_cast<uintptr_t>(set->unreached.ptr) * 3 ^
+               reinterpret_cast<uintptr_t>(set->pc_extra.ptr) * 5 ^ reinterpret_cast<uintptr_t>(set->mcn_extra.ptr) * 7 ^
+               reinterpret_cast<uintptr_t>(set->counters.ptr) * 11 ^ reinterpret_cast<uintptr_t>(set->parent.ptr) * 13 ^
+               reinterpret_cast<uintptr_t>(set->comp_size.ptr) * 17;
+    };
+    const uintptr_t accumulators_before = accumulators();
+    GAPA_TRY(set->removed.ensure(sizeof(word_t) * static_cast<size_t>(crows) * words_per_row));
+    GAPA_TRY(set->removed_count.ensure(sizeof(int) * pgroups * kBits));
+    GAPA_TRY(set->alive.ensure(sizeof(word_t) * words));
+    GAPA_TRY(set->reached.ensure(sizeof(word_t) * words));
+    GAPA_TRY(set->entry_of.ensure(sizeof(int32_t) * words));
+    GAPA_TRY(set->unreached.ensure(sizeof(int) * pgroups * kBits));
+    GAPA_TRY(set->pc_extra.ensure(sizeof(unsigned long long) * pgroups * kBits));
+    GAPA_TRY(set->mcn_extra.ensure(sizeof(int) * pgroups * kBits));
+    GAPA_TRY(set->counters.ensure(sizeof(PcCounters)));
+    if (set->cap_entries == 0 || set->parent.cap < sizeof(int32_t) * (static_cast<size_t>(pgroups) * kBits + set->cap_slots))
+        GAPA_TRY(ensure_phase2(set, pgroups, std::max<size_t>(set->cap_entries, 1u << 16), std::max<size_t>(set->cap_slots, 1u << 20)));
+    word_t* alive = set->alive.as<word_t>();
+    word_t* reached = set->reached.as<word_t>();
+    PcCounters* counters = set->counters.as<PcCounters>();
+    const int slot0 = pgroups * kBits;
+    const int reset_grid = std::max(1, (pgroups * kBits + kThreads - 1) / kThreads);
+    auto reset = [&](int first) -> int {
+        GAPA_LAUNCH(k_pc_reset, reset_grid, kThreads, 0, stream, pgroups, set->parent.as<int32_t>(), set->comp_size.as<int32_t>(),
+                    set->unreached.as<int>(), set->pc_extra.as<unsigned long long>(), set->mcn_extra.as<int>(), counters, first);
+        return GAPA_CUDA_OK;
+    };
+    const bool speculative = spec_rounds >= 1 && n > 0;
+    if (accumulators() != accumulators_before) set->clean_slots = 0;
+    if (!(speculative && set->clean_slots >= pgroups * kBits)) {
+        GAPA_TRY(reset(1));
+        GAPA_CUDA_TRY(cudaMemsetAsync(set->removed_count.ptr, 0, sizeof(int) * pgroups * kBits, stream));
+    }
+    set->clean_slots = 0;
+    if (rounds_used) *rounds_used = 0;
+
+    if (n > 0) {
+        // The clear of the `reached` records depends on nothing this lane computes, only on the previous user of the
+        // buffer being done: it runs on a side stream underneath the mask build, which is bound by integer issue.
+        if (s->overlap_clear && sizeof(word_t) * words > s->fold_clear_bytes) GAPA_CUDA_TRY(cudaEventRecord(set->ev_pass_begin, stream));
+        const int clear_grid = static_cast<int>(std::max<size_t>(1, std::min<size_t>(static_cast<size_t>(sm) * 8, (words / kPack + kThreads - 1) / kThreads)));
+        // ---- masks ------------------------------------------------------------------
+        // one CTA per individual: as many threads as it has 16-byte gene quads (or bitmap words) to work on, so that
+        // small budgets do not occupy an SM with idle warps (k = 500: 128 threads, 16 CTAs per SM instead of 2)
+        // (k = 5000: 640 threads make two full passes over the 1250 quads where 1024 would idle 40 % of their slots)
+        auto mask_cta = [&](int work) {  // the CTA size whose passes over `work` items waste the fewest thread slots
+            int best = 128;
+            long best_cost = -1;
+            for (int nt = 128; nt <= kMaskThreads; nt += 128) {
+                const long cost = static_cast<long>((work + nt - 1) / nt) * nt;
+                if (best_cost < 0 || cost <= best_cost) best = nt, best_cost = cost;
+            }
+            return best;
+        };
+        const bool fused_mask = job.vary && chunks == 1 && cols > 0;
+        // fused kernel: one 16-byte quad per thread and pass; plain kernel: two 32-byte loads per thread and pass
+        // (with a bitmap that leaves room for only a few CTAs per SM the kernels live on the bytes each CTA keeps in
+        // flight and keep the full 1024 threads: C4 measured 1.93 ms with 1024 against 1.95 ms with 896)
+        const int mask_threads = chunk_bits / 8 > 32 * 1024
+                                     ? kMaskThreads
+                                     : mask_cta(std::max({fused_mask ? cols / 4 : cols / 16, chunk_bits / 512, 1}));
+        if (fused_mask) {
+            VariationSpec pass = *job.vary;
+            pass.row_first += row0;
+#define GAPA_MASK_VARY(NT)                                                                                                  \
+    GAPA_LAUNCH(k_pc_bitmask_vary<NT>, crows, NT, static_cast<size_t>(chunk_bits) / 8, stream, pass, cols, g_gene_map, n, \
+                words_per_row, set->removed.as<word_t>(), set->removed_count.as<int>())
+            switch (mask_threads) {
+                case 128: GAPA_MASK_VARY(128); break;
+                case 256: GAPA_MASK_VARY(256); break;
+                case 384: GAPA_MASK_VARY(384); break;
+                case 512: GAPA_MASK_VARY(512); break;
+                case 640: GAPA_MASK_VARY(640); break;
+                case 768: GAPA_MASK_VARY(768); break;
+                case 896: GAPA_MASK_VARY(896); break;
+                default: GAPA_MASK_VARY(1024); break;
+            }
+#undef GAPA_MASK_VARY
+        } else {
+            if (job.vary) {
+                VariationSpec pass = *job.vary;
+                pass.row_first += row0;
+                GAPA_TRY(launch_variation_spec(pass, cols, crows, stream));
+            }
+#define GAPA_MASK(NT)                                                                                                          \
+    GAPA_LAUNCH(k_pc_bitmask<NT>, dim3(chunks, crows), NT, static_cast<size_t>(chunk_bits) / 8, stream, job.genes.from(row0), \
+                g_gene_map, ctx->pool_size, n, chunk_bits, words_per_row, set->removed.as<word_t>(),                          \
+                set->removed_count.as<int>(), counters)
+            switch (mask_threads) {
+                case 128: GAPA_MASK(128); break;
+                case 256: GAPA_MASK(256); break;
+                case 384: GAPA_MASK(384); break;
+                case 512: GAPA_MASK(512); break;
+                case 640: GAPA_MASK(640); break;
+                case 768: GAPA_MASK(768); break;
+                case 896: GAPA_MASK(896); break;
+                default: GAPA_MASK(1024); break;
+            }
+#undef GAPA_MASK
+        }
+        // small batches are bound by launches: the transpose kernel clears the records and the prefix kernel picks the sources
+        const bool fold_clear = sizeof(word_t) * words <= s->fold_clear_bytes;
+        const int prefix = std::min(s->prefix, n);
+        if (!fold_clear && s->overlap_clear) {  // issued AFTER the mask kernel so that its CTAs only fill what that kernel leaves free
+            GAPA_CUDA_TRY(cudaStreamWaitEvent(set->aux, set->ev_pass_begin, 0));
+            GAPA_LAUNCH(k_pc_clear, clear_grid, kThreads, 0, set->aux, reinterpret_cast<Rec*>(reached), words / kPack);
+            GAPA_CUDA_TRY(cudaEventRecord(set->ev_cleared, set->aux));
+        }
+        GAPA_LAUNCH(k_pc_transpose, dim3((words_per_row + kTransThreads - 1) / kTransThreads, pgroups), kTransThreads,
+                    sizeof(word_t) * kBits * (kTransThreads + 1), stream, set->removed.as<word_t>(), words_per_row, n, crows, alive,
+                    fold_clear ? reached : static_cast<word_t*>(nullptr));
+        if (!fold_clear) {
+            if (s->overlap_clear) GAPA_CUDA_TRY(cudaStreamWaitEvent(stream, set->ev_cleared, 0));
+            else GAPA_LAUNCH(k_pc_clear, clear_grid, kThreads, 0, stream, reinterpret_cast<Rec*>(reached), words / kPack);
+        }
+        if (prefix <= 0)
+            GAPA_LAUNCH(k_pc_source, (crows * 32 + kThreads - 1) / kThreads, kThreads, 0, stream, g_by_degree, n, crows, alive, reached);
+
+        // ---- phase 1 ------------------------------------------------------------------
+        const word_t* alive_rec = alive;
+        Rec* reached_rec = reinterpret_cast<Rec*>(reached);
+        if (prefix > 0) {
+            // measured on B200 (tools/ab_prefix.sh): 8 CTAs per super-group up to 8 groups, 4 at 16-32, 2 at 64;
+            // beyond that every cluster must be resident at once (one CTA of this kernel per SM)
+            int csize = sgroups <= 8 ? kPrefixCluster : 4;
+            while (csize > 1 && sgroups * csize > sm) csize >>= 1;
+            if (s->prefix_cluster > 0) csize = s->prefix_cluster;
+            cudaLaunchConfig_t cfg{};
+            cfg.gridDim = dim3(sgroups * csize);
+            cfg.blockDim = dim3(kPrefixThreads);
+            cfg.stream = stream;
+            cudaLaunchAttribute attr{};
+            attr.id = cudaLaunchAttributeClusterDimension;
+            attr.val.clusterDim.x = csize; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
+            cfg.attrs = &attr; cfg.numAttrs = 1;
+            GAPA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pc_prefix, g_row_ptr, g_col_idx, static_cast<const int4*>(s->nbr4.as<int4>()),
+                                             s->prefix_first4, n, prefix, alive_rec, reached_rec, 1, g_by_degree, crows));
+            g_launches.fetch_add(1, std::memory_order_relaxed);
+        }
+        const int il = std::min(std::max(1, s->interleave / kPack), sgroups);
+        const dim3 grid(((n + kThreads - 1) / kThreads) * il, (sgroups + il - 1) / il);
+        GAPA_TRY(set->block_done.ensure(sizeof(int2) * static_cast<size_t>(sgroups) * ((n + kThreads - 1) / kThreads)));
+        SweepArgs A;
+        A.row_ptr = g_row_ptr; A.col_idx = g_col_idx; A.nbr4 = s->nbr4.as<int4>(); A.n = n; A.sgroups = sgroups; A.interleave = il;
+        A.alive = alive_rec; A.reached = reached_rec; A.unreached = set->unreached.as<int>();
+        A.entry_of = set->entry_of.as<int32_t>(); A.slot0 = slot0; A.counters = counters;
+        A.incomplete = set->block_done.as<int2>(); A.record = 0; A.descending = 0;
+        A.defer_above = static_cast<unsigned>(std::min<size_t>(0xfffffffeu, static_cast<size_t>(sgroups) * n / 16));  // 6 % of the pairs
+        auto sweep = [&](bool final_pass, bool record, bool descending = false, bool local = false) -> int {
+            A.descending = descending ? 1 : 0;
+            A.cap_entries = static_cast<unsigned>(set->cap_entries);  // may have grown after an overflow retry
+            A.cap_slots = static_cast<unsigned>(set->cap_slots);
+            A.left_v = set->left_v.as<int32_t>(); A.left_g = set->left_g.as<int32_t>(); A.left_w = set->left_w.as<word_t>();
+            A.left_base = set->left_base.as<int32_t>(); A.parent = set->parent.as<int32_t>(); A.comp_size = set->comp_size.as<int32_t>();
+            A.record = record ? 1 : 0;
+            if (final_pass) GAPA_LAUNCH(k_pc_record, sm * 4, kThreads, 0, stream, A);
+            else if (local) GAPA_LAUNCH(k_pc_sweep_local, grid, kThreads, 0, stream, A);
+            else GAPA_LAUNCH(k_pc_sweep, grid, kThreads, 0, stream, A);
+            return GAPA_CUDA_OK;
+        };
+        // With the prefix closed, ONE ordered sweep reaches nearly everything on power-law graphs and marks the
+        // 256-vertex chunks that are complete; the recording sweep then only visits the few incomplete chunks, and
+        // phase 2 (exact for any leftover, attaching to the giant through reached neighbours) finishes.  If a lot is
+        // still unreached AND the sweeps were still making progress, more rounds follow first: one sweep in DESCENDING
+        // block order, then an ascending one; from the fifth round on (random graphs converge before that; what is
+        // left has a large diameter) each block iterates its chunk to a local fixpoint (k_pc_sweep_local).  Across
+        // blocks reachability runs any distance along ids in the direction the blocks are scheduled but only one hop
+        // against it: high-diameter graphs (rings, grids) need both directions to converge in a few rounds.
+        const unsigned many = static_cast<unsigned>(std::max<size_t>(8192, words / 512));
+        auto ordinary_sweeps = [&](int round, bool record_last) -> int {
+            const int ordinary = round == 0 ? 1 : 2;
+            for (int i = 0; i < ordinary; ++i) GAPA_TRY(sweep(false, record_last && i + 1 == ordinary, ordinary == 2 && i == 0, round >= 4));
+            return GAPA_CUDA_OK;
+        };
+        Phase2Args P2;
+        auto phase2_args = [&]() {  // the buffers may have grown after an overflow retry
+            P2.row_ptr = g_row_ptr; P2.col_idx = g_col_idx; P2.n = n; P2.alive = alive; P2.reached = reached;
+            P2.entry_of = set->entry_of.as<int32_t>(); P2.left_v = set->left_v.as<int32_t>(); P2.left_g = set->left_g.as<int32_t>();
+            P2.left_w = set->left_w.as<word_t>(); P2.left_base = set->left_base.as<int32_t>(); P2.parent = set->parent.as<int32_t>();
+            P2.comp_size = set->comp_size.as<int32_t>(); P2.slot0 = slot0; P2.pc_extra = set->pc_extra.as<unsigned long long>();
+            P2.mcn_extra = set->mcn_extra.as<int>(); P2.counters = counters;
+        };
+        auto phase2 = [&](unsigned stand_down_above, unsigned entries_hint) -> int {
+            const unsigned blocks = entries_hint ? (entries_hint + kThreads - 1) / kThreads : static_cast<unsigned>(sm * 8);
+            const int pgrid = static_cast<int>(std::max(1u, std::min<unsigned>(blocks, sm * 8)));
+            phase2_args();
+            GAPA_LAUNCH(k_pc_hook, pgrid, kThreads, 0, stream, P2, stand_down_above);
+            GAPA_LAUNCH(k_pc_count, pgrid, kThreads, 0, stream, P2, stand_down_above);
+            GAPA_LAUNCH(k_pc_reduce, pgrid, kThreads, 0, stream, P2, stand_down_above);
+            return GAPA_CUDA_OK;
+        };
+        if (spec_rounds >= 1) {
+            for (int round = 0; round < spec_rounds; ++round) {
+                if (round > 0) GAPA_TRY(reset(0));  // `changed` should tell about the last round only
+                GAPA_TRY(ordinary_sweeps(round, round + 1 == spec_rounds));
+            }
+            GAPA_TRY(sweep(true, false));
+            if (s->phase2_big) GAPA_TRY(phase2(many, 0));
+            phase2_args();
+            // the last kernel: (phase 2,) results, counters to the host, accumulators left clean for the next lane
+            GAPA_LAUNCH(k_pc_final, 1, kFinalThreads, 0, stream, P2, many, kFusedPhase2Entries, s->phase2_big ? 0 : 1, crows, job.task,
+                        set->removed_count.as<int>(), set->unreached.as<int>(), job.out_dev + row0, counters, h_out, pgroups * kBits);
+            set->clean_slots = pgroups * kBits;  // entry slots start right above: a larger lane must reset for itself
+            return GAPA_CUDA_OK;
+        } else {
+            PcCounters h{};
+            for (int round = 0;; ++round) {
+                GAPA_TRY(ordinary_sweeps(round, true));
+                if (round >= 47) A.defer_above = ~0u;  // bounded: the last round records whatever is left
+                GAPA_TRY(sweep(true, false));
+                GAPA_CUDA_TRY(cudaMemcpyAsync(&h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
+                GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
+                if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
+                if (s->trace)
+                    std::fprintf(stderr, "pc_eval round %d: entries %u slots %u overflow %d changed %d incomplete %u deferred %d (cap %zu / %zu)\n",
+                                 round, h.n_entries, h.n_slots, h.overflow, h.changed, h.n_incomplete, h.deferred, set->cap_entries, set->cap_slots);
+                const bool retry_bigger = h.overflow != 0;
+                const bool keep_sweeping = h.deferred || (h.changed && h.n_entries > many && round < 48);
+                if (rounds_used) *rounds_used = round + 1;
+                if (!retry_bigger && !keep_sweeping) break;
+                if (retry_bigger)
+                    GAPA_TRY(ensure_phase2(set, pgroups, std::max<size_t>(set->cap_entries, static_cast<size_t>(h.n_entries) + 1024),
+                                           std::max<size_t>(set->cap_slots, static_cast<size_t>(h.n_slots) + 1024)));
+                GAPA_TRY(reset(0));
+            }
+            if (h.n_entries) GAPA_TRY(phase2(~0u, h.n_entries));
+        }
+    } else if (static_cast<size_t>(crows) * cols) {
+        return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
+    }
+    GAPA_LAUNCH(k_pc_result, (crows + kThreads - 1) / kThreads, kThreads, 0, stream, n, crows, job.task, set->removed_count.as<int>(),
+                set->unreached.as<int>(), set->comp_size.as<int32_t>(), set->pc_extra.as<unsigned long long>(),
+                set->mcn_extra.as<int>(), job.out_dev + row0);
+    return GAPA_CUDA_OK;
+}
+
 int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_dev, cudaStream_t stream, bool trusted,
             const VariationSpec* vary) {
     const int cols = genes.cols;
@@ -1050,6 +1467,16 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         s->mask_chunks = env_int("GAPA_PC_MASK_CHUNKS", 1, 1, 64);
         s->relabel = env_int("GAPA_PC_RELABEL", -1, -1, 1);  // -1 automatic, 0 never, 1 always (tests)
         s->small_path = env_int("GAPA_PC_SMALL", 1, 0, 2);  // 0: never, 1: where it pays, 2: wherever it fits (tests)
+        // individuals per lane.  Measured at C4 (tools/ab_lanes.sh): ONE lane of 4096 is as fast as two of 2048 (1.887 vs
+        // 1.877 ms per generation) and every finer split is slower (1024 x 2 streams 1.97, 512 x 4 2.01, 256 x 8 2.33 ms):
+        // the mask kernel holds a whole SM (125 KB bitmap, 1024 threads x 46 registers), so a second lane's sweeps find no
+        // room beside it, and every lane pays the latency-bound prefix closure again.  Lanes therefore only split
+        // populations beyond 4096 (and whatever the scratch budget forces).
+        s->lane_rows = env_int("GAPA_PC_LANE_ROWS", 4096, 64, 1 << 20) / kBits * kBits;
+        s->lane_streams = env_int("GAPA_PC_LANE_STREAMS", 2, 1, 8);  // lanes in flight
+        s->spec_rounds = env_int("GAPA_PC_SPEC_ROUNDS", 1, 0, 6);    // 0: always the host-driven loop
+        s->phase2_big = env_int("GAPA_PC_PHASE2_BIG", 0, 0, 1) != 0;  // 1: never resolve leftovers inside k_pc_final (tests)
+        s->fold_clear_bytes = static_cast<size_t>(env_int("GAPA_PC_FOLD_CLEAR_MB", 16, 0, 1 << 20)) << 20;
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small<kSmallThreadsFew>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small<kSmallThreadsMany>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         // the shared-memory bitmap may use most of the SM (one CTA per individual)
@@ -1073,15 +1500,20 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         s->overlap_clear = env_int("GAPA_PC_OVERLAP_CLEAR", 1, 0, 1);
         s->trace = env_int("GAPA_PC_TRACE", 0, 0, 1);  // one stderr line per sweep round
         s->prefix_first4 = env_int("GAPA_PC_PREFIX_FIRST4", 1, 0, 1);  // 0: scan whole (bounded) rows in the prefix closure
-        {  // lowest priority: the clear yields to every kernel of the work stream
-            int least = 0, greatest = 0;
-            GAPA_CUDA_TRY(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-            GAPA_CUDA_TRY(cudaStreamCreateWithPriority(&s->aux, cudaStreamNonBlocking, least));
-        }
-        GAPA_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_pass_begin, cudaEventDisableTiming));
-        GAPA_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_cleared, cudaEventDisableTiming));
+        GAPA_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&s->h_counters), sizeof(PcCounters) * kMaxLanes));
+        GAPA_CUDA_TRY(cudaEventCreateWithFlags(&s->ev_fork, cudaEventDisableTiming));
         s->configured = true;
     }
+    auto get_set = [&](int i, PcSet** out) -> int {
+        while (static_cast<int>(s->sets.size()) <= i) {
+            PcSet* fresh = nullptr;
+            const int rc = pc_set_create(&fresh);
+            s->sets.push_back(fresh);  // owned (and freed) by the scratch even when half-built
+            GAPA_TRY(rc);
+        }
+        *out = s->sets[i];
+        return GAPA_CUDA_OK;
+    };
     const int n = ctx->n;
     const int sm = ctx->sm_count;
     // Measured crossover (tools/ab_small.sh): the per-individual kernel wins only where the bit-sliced pipeline
@@ -1091,8 +1523,10 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
     const bool small_pays = n <= 2048 || (n <= 4096 && rows <= 1024);
     if (small_fits && (s->small_path == 2 || (s->small_path == 1 && small_pays))) {
         const size_t smem = sizeof(int32_t) * (2 * static_cast<size_t>(n) + ((n + 31) >> 5) + 1);
-        GAPA_TRY(s->counters.ensure(sizeof(PcCounters)));
-        PcCounters* counters = s->counters.as<PcCounters>();
+        PcSet* set0 = nullptr;
+        GAPA_TRY(get_set(0, &set0));
+        GAPA_TRY(set0->counters.ensure(sizeof(PcCounters)));
+        PcCounters* counters = set0->counters.as<PcCounters>();
         if (!trusted) GAPA_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(PcCounters), stream));  // trusted genes cannot be out of range
         const bool fuse = vary && cols > 0;
         if (vary && !fuse) GAPA_TRY(launch_variation_spec(*vary, cols, rows, stream));
@@ -1112,222 +1546,74 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         return GAPA_CUDA_OK;
     }
     GAPA_TRY(ensure_order(ctx, s));
-    const int32_t* g_row_ptr = s->ord_relabeled ? s->ord_row_ptr.as<int32_t>() : ctx->d_row_ptr;
-    const int32_t* g_col_idx = s->ord_relabeled ? s->ord_col_idx.as<int32_t>() : ctx->d_col_idx;
-    const int32_t* g_gene_map = s->ord_relabeled ? s->ord_gene_map.as<int32_t>() : (ctx->pool_identity ? nullptr : ctx->d_pool_map);
-    const int32_t* g_by_degree = s->ord_relabeled ? nullptr : ctx->d_by_degree;
-    const int words_per_row = std::max(1, (n + 63) / 64);
-    int chunk_bits = std::min(words_per_row * 64, 192 * 1024 * 8);  // <= 192 KB of shared memory
-    if (s->mask_chunks > 1) chunk_bits = std::min(chunk_bits, ((words_per_row + s->mask_chunks - 1) / s->mask_chunks) * 64);
-    const int chunks = (words_per_row * 64 + chunk_bits - 1) / chunk_bits;
-    // groups per pass bounded by a scratch budget: alive + reached + entry_of (20 B) + bitmaps (8 B / 64) per vertex
-    const size_t budget = static_cast<size_t>(env_int("GAPA_SCRATCH_MB", 24 * 1024, 1, 1 << 20)) << 20;  // scratch per pass
+    // Lanes: whole 64-individual groups, at most lane_rows individuals and at most what the scratch budget allows
+    // (alive + reached + entry_of = 20 B per vertex and group, bitmaps 8 B per vertex and group) for every set in flight.
+    const size_t budget = static_cast<size_t>(env_int("GAPA_SCRATCH_MB", 24 * 1024, 1, 1 << 20)) << 20;
     const int all_groups = (rows + kBits - 1) / kBits;
-    const int max_groups = static_cast<int>(std::min<size_t>(1023, std::max<size_t>(1, budget / (28ull * std::max(n, 1)))));
-
-    for (int g0 = 0; g0 < all_groups; g0 += max_groups) {
-        const int groups = std::min(max_groups, all_groups - g0);
-        const int row0 = g0 * kBits;
-        const int crows = std::min(rows - row0, groups * kBits);
-        const int sgroups = (groups + kPack - 1) / kPack;  // 4 groups share one 32-byte vertex record
-        const int pgroups = sgroups * kPack;
-        const size_t words = static_cast<size_t>(pgroups) * std::max(n, 1);
-        GAPA_TRY(s->removed.ensure(sizeof(word_t) * static_cast<size_t>(crows) * words_per_row));
-        GAPA_TRY(s->removed_count.ensure(sizeof(int) * pgroups * kBits));
-        GAPA_TRY(s->alive.ensure(sizeof(word_t) * words));
-        GAPA_TRY(s->reached.ensure(sizeof(word_t) * words));
-        GAPA_TRY(s->entry_of.ensure(sizeof(int32_t) * words));
-        GAPA_TRY(s->unreached.ensure(sizeof(int) * pgroups * kBits));
-        GAPA_TRY(s->pc_extra.ensure(sizeof(unsigned long long) * pgroups * kBits));
-        GAPA_TRY(s->mcn_extra.ensure(sizeof(int) * pgroups * kBits));
-        GAPA_TRY(s->counters.ensure(sizeof(PcCounters)));
-        if (s->cap_entries == 0 || s->parent.cap < sizeof(int32_t) * (static_cast<size_t>(pgroups) * kBits + s->cap_slots))
-            GAPA_TRY(ensure_phase2(s, pgroups, std::max<size_t>(s->cap_entries, 1u << 16),
-                                   std::max<size_t>(s->cap_slots, 1u << 20)));
-        word_t* alive = s->alive.as<word_t>();
-        word_t* reached = s->reached.as<word_t>();
-        PcCounters* counters = s->counters.as<PcCounters>();
-        const int slot0 = pgroups * kBits;
-        const int reset_grid = std::max(1, (pgroups * kBits + kThreads - 1) / kThreads);
-        auto reset = [&](int first) -> int {
-            GAPA_LAUNCH(k_pc_reset, reset_grid, kThreads, 0, stream, pgroups, s->parent.as<int32_t>(),
-                        s->comp_size.as<int32_t>(), s->unreached.as<int>(), s->pc_extra.as<unsigned long long>(),
-                        s->mcn_extra.as<int>(), counters, first);
-            return GAPA_CUDA_OK;
-        };
-        GAPA_TRY(reset(1));
-        GAPA_CUDA_TRY(cudaMemsetAsync(s->removed_count.ptr, 0, sizeof(int) * pgroups * kBits, stream));
-
-        if (n > 0) {
-            // The 0.5 GB clear of the `reached` records depends on nothing this pass computes, only on the
-            // previous user of the buffer being done: it runs on a side stream underneath the mask build,
-            // which is bound by integer issue, not by HBM.
-            if (s->overlap_clear) GAPA_CUDA_TRY(cudaEventRecord(s->ev_pass_begin, stream));
-            // ---- masks ------------------------------------------------------------------
-            // one CTA per individual: as many threads as it has 16-byte gene quads (or bitmap words) to work on, so that
-            // small budgets do not occupy an SM with idle warps (k = 500: 128 threads, 16 CTAs per SM instead of 2)
-            // (k = 5000: 640 threads make two full passes over the 1250 quads where 1024 would idle 40 % of their slots)
-            auto mask_cta = [&](int work) {  // the CTA size whose passes over `work` items waste the fewest thread slots
-                int best = 128;
-                long best_cost = -1;
-                for (int nt = 128; nt <= kMaskThreads; nt += 128) {
-                    const long cost = static_cast<long>((work + nt - 1) / nt) * nt;
-                    if (best_cost < 0 || cost <= best_cost) best = nt, best_cost = cost;
-                }
-                return best;
-            };
-            const bool fused_mask = vary && chunks == 1 && cols > 0;
-            // fused kernel: one 16-byte quad per thread and pass; plain kernel: two 32-byte loads per thread and pass
-            // (with a bitmap that leaves room for only a few CTAs per SM the kernels live on the bytes each CTA keeps in
-            // flight and keep the full 1024 threads: C4 measured 1.93 ms with 1024 against 1.95 ms with 896)
-            const int mask_threads = chunk_bits / 8 > 32 * 1024
-                                         ? kMaskThreads
-                                         : mask_cta(std::max({fused_mask ? cols / 4 : cols / 16, chunk_bits / 512, 1}));
-            if (fused_mask) {
-                VariationSpec pass = *vary;
-                pass.row_first += row0;
-#define GAPA_MASK_VARY(NT)                                                                                                  \
-    GAPA_LAUNCH(k_pc_bitmask_vary<NT>, crows, NT, static_cast<size_t>(chunk_bits) / 8, stream, pass, cols, g_gene_map, n, \
-                words_per_row, s->removed.as<word_t>(), s->removed_count.as<int>())
-                switch (mask_threads) {
-                    case 128: GAPA_MASK_VARY(128); break;
-                    case 256: GAPA_MASK_VARY(256); break;
-                    case 384: GAPA_MASK_VARY(384); break;
-                    case 512: GAPA_MASK_VARY(512); break;
-                    case 640: GAPA_MASK_VARY(640); break;
-                    case 768: GAPA_MASK_VARY(768); break;
-                    case 896: GAPA_MASK_VARY(896); break;
-                    default: GAPA_MASK_VARY(1024); break;
-                }
-#undef GAPA_MASK_VARY
-            } else {
-                if (vary) {
-                    VariationSpec pass = *vary;
-                    pass.row_first += row0;
-                    GAPA_TRY(launch_variation_spec(pass, cols, crows, stream));
-                }
-#define GAPA_MASK(NT)                                                                                                       \
-    GAPA_LAUNCH(k_pc_bitmask<NT>, dim3(chunks, crows), NT, static_cast<size_t>(chunk_bits) / 8, stream, genes.from(row0),  \
-                g_gene_map, ctx->pool_size, n, chunk_bits, words_per_row, s->removed.as<word_t>(),                         \
-                s->removed_count.as<int>(), counters)
-                switch (mask_threads) {
-                    case 128: GAPA_MASK(128); break;
-                    case 256: GAPA_MASK(256); break;
-                    case 384: GAPA_MASK(384); break;
-                    case 512: GAPA_MASK(512); break;
-                    case 640: GAPA_MASK(640); break;
-                    case 768: GAPA_MASK(768); break;
-                    case 896: GAPA_MASK(896); break;
-                    default: GAPA_MASK(1024); break;
-                }
-#undef GAPA_MASK
+    const int budget_groups = static_cast<int>(std::min<size_t>(1023, std::max<size_t>(1, budget / (28ull * std::max(n, 1)))));
+    int lane_groups = std::max(1, std::min(s->lane_rows / kBits, all_groups));
+    int streams = std::min(s->lane_streams, (all_groups + lane_groups - 1) / lane_groups);
+    if (lane_groups * streams > budget_groups) {
+        streams = std::max(1, std::min(streams, budget_groups / lane_groups));
+        lane_groups = std::max(1, std::min(lane_groups, budget_groups / streams));
+    }
+    if (lane_groups >= kPack) lane_groups = lane_groups / kPack * kPack;  // whole 32-byte records
+    const int total_lanes = (all_groups + lane_groups - 1) / lane_groups;
+    PcLaneJob job{task, genes, 0, 0, out_dev, trusted, vary};
+    auto lane_many = [&](int crows) {
+        const int sg = ((crows + kBits - 1) / kBits + kPack - 1) / kPack;
+        return static_cast<unsigned>(std::max<size_t>(8192, static_cast<size_t>(sg) * kPack * std::max(n, 1) / 512));
+    };
+    for (int wave0 = 0; wave0 < total_lanes; wave0 += kMaxLanes) {
+        const int lanes = std::min(kMaxLanes, total_lanes - wave0);
+        const bool forked = lanes > 1 && streams > 1;
+        const int spec = s->spec_rounds;
+        if (forked) {
+            GAPA_CUDA_TRY(cudaEventRecord(s->ev_fork, stream));
+            for (int j = 0; j < std::min(streams, lanes); ++j) {
+                PcSet* set = nullptr;
+                GAPA_TRY(get_set(j, &set));
+                GAPA_CUDA_TRY(cudaStreamWaitEvent(set->stream, s->ev_fork, 0));
             }
-            if (s->overlap_clear) {  // issued AFTER the mask kernel so that its CTAs only fill what that kernel leaves free
-                GAPA_CUDA_TRY(cudaStreamWaitEvent(s->aux, s->ev_pass_begin, 0));
-                GAPA_CUDA_TRY(cudaMemsetAsync(reached, 0, sizeof(word_t) * words, s->aux));
-                GAPA_CUDA_TRY(cudaEventRecord(s->ev_cleared, s->aux));
-            }
-            GAPA_LAUNCH(k_pc_transpose, dim3((words_per_row + kTransThreads - 1) / kTransThreads, pgroups), kTransThreads,
-                        sizeof(word_t) * kBits * (kTransThreads + 1), stream, s->removed.as<word_t>(), words_per_row, n, crows, alive);
-            if (s->overlap_clear) GAPA_CUDA_TRY(cudaStreamWaitEvent(stream, s->ev_cleared, 0));
-            else GAPA_CUDA_TRY(cudaMemsetAsync(reached, 0, sizeof(word_t) * words, stream));
-            GAPA_LAUNCH(k_pc_source, (crows * 32 + kThreads - 1) / kThreads, kThreads, 0, stream, g_by_degree, n,
-                        crows, alive, reached);
-
-            // ---- phase 1 ------------------------------------------------------------------
-            const word_t* alive_rec = alive;
-            Rec* reached_rec = reinterpret_cast<Rec*>(reached);
-            const int prefix = std::min(s->prefix, n);
-            if (prefix > 0) {
-                // measured on B200 (tools/ab_prefix.sh): 8 CTAs per super-group up to 8 groups, 4 at 16-32, 2 at 64;
-                // beyond that every cluster must be resident at once (one CTA of this kernel per SM)
-                int csize = sgroups <= 8 ? kPrefixCluster : 4;
-                while (csize > 1 && sgroups * csize > sm) csize >>= 1;
-                if (s->prefix_cluster > 0) csize = s->prefix_cluster;
-                cudaLaunchConfig_t cfg{};
-                cfg.gridDim = dim3(sgroups * csize);
-                cfg.blockDim = dim3(kPrefixThreads);
-                cfg.stream = stream;
-                cudaLaunchAttribute attr{};
-                attr.id = cudaLaunchAttributeClusterDimension;
-                attr.val.clusterDim.x = csize; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
-                cfg.attrs = &attr; cfg.numAttrs = 1;
-                GAPA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pc_prefix, g_row_ptr, g_col_idx, static_cast<const int4*>(s->nbr4.as<int4>()),
-                                                 s->prefix_first4, n, prefix, alive_rec, reached_rec));
-                g_launches.fetch_add(1, std::memory_order_relaxed);
-            }
-            const int il = std::min(std::max(1, s->interleave / kPack), sgroups);
-            const dim3 grid(((n + kThreads - 1) / kThreads) * il, (sgroups + il - 1) / il);
-            GAPA_TRY(s->block_done.ensure(sizeof(int2) * static_cast<size_t>(sgroups) * ((n + kThreads - 1) / kThreads)));
-            SweepArgs A;
-            A.row_ptr = g_row_ptr; A.col_idx = g_col_idx; A.nbr4 = s->nbr4.as<int4>(); A.n = n; A.sgroups = sgroups; A.interleave = il;
-            A.alive = alive_rec; A.reached = reached_rec; A.unreached = s->unreached.as<int>();
-            A.entry_of = s->entry_of.as<int32_t>(); A.left_v = s->left_v.as<int32_t>(); A.left_g = s->left_g.as<int32_t>();
-            A.left_w = s->left_w.as<word_t>(); A.left_base = s->left_base.as<int32_t>(); A.parent = s->parent.as<int32_t>();
-            A.comp_size = s->comp_size.as<int32_t>(); A.slot0 = slot0; A.counters = counters;
-            A.incomplete = s->block_done.as<int2>(); A.record = 0; A.descending = 0;
-            A.defer_above = static_cast<unsigned>(std::min<size_t>(0xfffffffeu, static_cast<size_t>(sgroups) * n / 16));  // 6 % of the pairs
-            auto sweep = [&](bool final_pass, bool record, bool descending = false, bool local = false) -> int {
-                A.descending = descending ? 1 : 0;
-                A.cap_entries = static_cast<unsigned>(s->cap_entries);  // may have grown after an overflow retry
-                A.cap_slots = static_cast<unsigned>(s->cap_slots);
-                A.left_v = s->left_v.as<int32_t>(); A.left_g = s->left_g.as<int32_t>(); A.left_w = s->left_w.as<word_t>();
-                A.left_base = s->left_base.as<int32_t>(); A.parent = s->parent.as<int32_t>(); A.comp_size = s->comp_size.as<int32_t>();
-                A.record = record ? 1 : 0;
-                if (final_pass) GAPA_LAUNCH(k_pc_record, sm * 4, kThreads, 0, stream, A);
-                else if (local) GAPA_LAUNCH(k_pc_sweep_local, grid, kThreads, 0, stream, A);
-                else GAPA_LAUNCH(k_pc_sweep, grid, kThreads, 0, stream, A);
-                return GAPA_CUDA_OK;
-            };
-            // With the prefix closed, ONE ordered sweep reaches nearly everything on power-law graphs and
-            // marks the 256-vertex chunks that are complete; the recording sweep then only visits the
-            // few incomplete chunks, and phase 2 (exact for any leftover, attaching to the giant through
-            // reached neighbours) finishes.  If a lot is still unreached AND the sweeps were still
-            // making progress, sweep more before phase 2.
-            const unsigned many = static_cast<unsigned>(std::max<size_t>(8192, words / 512));
-            PcCounters h{};
-            for (int round = 0;; ++round) {
-                // extra rounds: one sweep in DESCENDING block order, then an ascending one; from the fifth round on
-                // (random graphs converge before that; what is left has a large diameter) each block iterates its
-                // chunk to a local fixpoint (k_pc_sweep_local).  Across blocks reachability runs any distance along
-                // ids in the direction the blocks are scheduled but only one hop against it: high-diameter graphs
-                // (rings, grids) need both directions to converge in a few rounds.
-                const int ordinary = round == 0 ? 1 : 2;
-                for (int i = 0; i < ordinary; ++i) GAPA_TRY(sweep(false, i + 1 == ordinary, ordinary == 2 && i == 0, round >= 4));
-                if (round >= 47) A.defer_above = ~0u;  // bounded: the last round records whatever is left
-                GAPA_TRY(sweep(true, false));
-                GAPA_CUDA_TRY(cudaMemcpyAsync(&h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
-                GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
-                if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
-                if (s->trace)
-                    std::fprintf(stderr, "pc_eval round %d: entries %u slots %u overflow %d changed %d incomplete %u deferred %d (cap %zu / %zu)\n",
-                                 round, h.n_entries, h.n_slots, h.overflow, h.changed, h.n_incomplete, h.deferred, s->cap_entries, s->cap_slots);
-                const bool retry_bigger = h.overflow != 0;
-                const bool keep_sweeping = h.deferred || (h.changed && h.n_entries > many && round < 48);
-                if (!retry_bigger && !keep_sweeping) break;
-                if (retry_bigger)
-                    GAPA_TRY(ensure_phase2(s, pgroups, std::max<size_t>(s->cap_entries, static_cast<size_t>(h.n_entries) + 1024),
-                                           std::max<size_t>(s->cap_slots, static_cast<size_t>(h.n_slots) + 1024)));
-                GAPA_TRY(reset(0));
-            }
-            // ---- phase 2 ------------------------------------------------------------------
-            if (h.n_entries) {
-                const int pgrid = static_cast<int>(std::min<unsigned>((h.n_entries + kThreads - 1) / kThreads, sm * 8));
-                GAPA_LAUNCH(k_pc_hook, pgrid, kThreads, 0, stream, g_row_ptr, g_col_idx, n, alive, reached,
-                            s->entry_of.as<int32_t>(), s->left_v.as<int32_t>(), s->left_g.as<int32_t>(),
-                            s->left_w.as<word_t>(), s->left_base.as<int32_t>(), s->parent.as<int32_t>(), slot0, counters);
-                GAPA_LAUNCH(k_pc_count, pgrid, kThreads, 0, stream, s->left_w.as<word_t>(), s->left_base.as<int32_t>(),
-                            s->parent.as<int32_t>(), s->comp_size.as<int32_t>(), slot0, counters);
-                GAPA_LAUNCH(k_pc_reduce, pgrid, kThreads, 0, stream, s->left_g.as<int32_t>(), s->left_w.as<word_t>(),
-                            s->left_base.as<int32_t>(), s->parent.as<int32_t>(), s->comp_size.as<int32_t>(), slot0,
-                            s->pc_extra.as<unsigned long long>(), s->mcn_extra.as<int>(), counters);
-            }
-        } else if (static_cast<size_t>(crows) * cols) {
-            return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
         }
-        GAPA_LAUNCH(k_pc_result, (crows + kThreads - 1) / kThreads, kThreads, 0, stream, n, crows, task,
-                    s->removed_count.as<int>(), s->unreached.as<int>(), s->comp_size.as<int32_t>(),
-                    s->pc_extra.as<unsigned long long>(), s->mcn_extra.as<int>(), out_dev + row0);
+        std::vector<int> redo;
+        for (int i = 0; i < lanes; ++i) {
+            PcSet* set = nullptr;
+            GAPA_TRY(get_set(forked ? i % streams : 0, &set));
+            job.row0 = (wave0 + i) * lane_groups * kBits;
+            job.crows = std::min(rows - job.row0, lane_groups * kBits);
+            GAPA_TRY(pc_run_lane(ctx, s, set, job, forked ? set->stream : stream, spec, &s->h_counters[i], nullptr));
+        }
+        if (forked)
+            for (int j = 0; j < std::min(streams, lanes); ++j) {
+                GAPA_CUDA_TRY(cudaEventRecord(s->sets[j]->ev_done, s->sets[j]->stream));
+                GAPA_CUDA_TRY(cudaStreamWaitEvent(stream, s->sets[j]->ev_done, 0));
+            }
+        if (spec == 0) continue;  // the host-driven loop has already seen every lane's counters
+        // ONE host look at the counters per evaluation, after everything has been enqueued
+        GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
+        for (int i = 0; i < lanes; ++i) {
+            const PcCounters& h = s->h_counters[i];
+            const int crows = std::min(rows - (wave0 + i) * lane_groups * kBits, lane_groups * kBits);
+            if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
+            if (s->trace)
+                std::fprintf(stderr, "pc_eval lane %d (speculative, %d round(s)): entries %u slots %u overflow %d changed %d incomplete %u deferred %d\n",
+                             wave0 + i, spec, h.n_entries, h.n_slots, h.overflow, h.changed, h.n_incomplete, h.deferred);
+            if (h.phase2_skipped) s->phase2_big = true;
+            if (h.overflow || h.deferred || h.phase2_skipped || (h.changed && h.n_entries > lane_many(crows))) redo.push_back(i);
+        }
+        // Lanes whose speculative schedule was not enough are redone with the host-driven loop (a later lane may have
+        // reused the set's buffers, so they start over; variation is a pure function of the parents, so rebuilding the
+        // children writes the same genes).  What the loop needed becomes the next evaluations' speculative schedule.
+        for (int i : redo) {
+            PcSet* set = nullptr;
+            GAPA_TRY(get_set(0, &set));
+            job.row0 = (wave0 + i) * lane_groups * kBits;
+            job.crows = std::min(rows - job.row0, lane_groups * kBits);
+            int used = 0;
+            GAPA_TRY(pc_run_lane(ctx, s, set, job, stream, 0, nullptr, &used));
+            s->spec_rounds = used <= 6 ? std::max(s->spec_rounds, used) : 0;
+        }
     }
     return GAPA_CUDA_OK;
 }
@@ -1335,13 +1621,22 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
 void pc_free(gapa_cuda_ctx* ctx) {
     if (!ctx->pc) return;
     PcScratch* s = ctx->pc;
-    for (DevBuf* b : {&s->nbr4, &s->removed, &s->removed_count, &s->alive, &s->reached, &s->entry_of, &s->unreached, &s->counters, &s->block_done,
-                      &s->left_v, &s->left_g, &s->left_w, &s->left_base, &s->parent, &s->comp_size, &s->pc_extra,
-                      &s->mcn_extra})
-        b->release();
-    if (s->aux) cudaStreamDestroy(s->aux);
-    if (s->ev_pass_begin) cudaEventDestroy(s->ev_pass_begin);
-    if (s->ev_cleared) cudaEventDestroy(s->ev_cleared);
+    for (PcSet* set : s->sets) {
+        if (!set) continue;
+        for (DevBuf* b : {&set->removed, &set->removed_count, &set->alive, &set->reached, &set->entry_of, &set->unreached, &set->counters,
+                          &set->block_done, &set->left_v, &set->left_g, &set->left_w, &set->left_base, &set->parent, &set->comp_size,
+                          &set->pc_extra, &set->mcn_extra})
+            b->release();
+        if (set->aux) cudaStreamDestroy(set->aux);
+        if (set->stream) cudaStreamDestroy(set->stream);
+        if (set->ev_pass_begin) cudaEventDestroy(set->ev_pass_begin);
+        if (set->ev_cleared) cudaEventDestroy(set->ev_cleared);
+        if (set->ev_done) cudaEventDestroy(set->ev_done);
+        delete set;
+    }
+    for (DevBuf* b : {&s->nbr4, &s->ord_row_ptr, &s->ord_col_idx, &s->ord_gene_map}) b->release();
+    if (s->h_counters) cudaFreeHost(s->h_counters);
+    if (s->ev_fork) cudaEventDestroy(s->ev_fork);
     delete s;
     ctx->pc = nullptr;
 }

@@ -182,3 +182,40 @@ def test_high_diameter_graphs(gp, oracle, cuda_device, monkeypatch):
         batch = gp.init_population(pool.size(), 70, k, 4) if k else np.zeros((3, 0), np.int32)
         for task, cls in ((0, gp.PairwiseConnectivityObjective), (1, gp.SixDstObjective)):
             assert np.array_equal(cls(g, pool).evaluate_batch(batch), oracle.eval_batch(og, task, batch, threads=8)), (name, task)
+
+
+@pytest.mark.parametrize("env", [
+    {},                                                                  # speculative schedule, one lane, k_pc_final
+    {"GAPA_PC_SPEC_ROUNDS": "0"},                                        # host-driven loop only
+    {"GAPA_PC_PHASE2_BIG": "1"},                                         # full-grid phase 2 inside the speculative schedule
+    {"GAPA_PC_LANE_ROWS": "64", "GAPA_PC_LANE_STREAMS": "3"},            # many lanes on three streams, sets reused
+    {"GAPA_PC_LANE_ROWS": "128", "GAPA_PC_LANE_STREAMS": "2", "GAPA_PC_SPEC_ROUNDS": "3"},
+    {"GAPA_PC_FOLD_CLEAR_MB": "0", "GAPA_PC_PREFIX": "0"},               # clear and source selection as launches of their own
+    {"GAPA_PC_FOLD_CLEAR_MB": "0", "GAPA_PC_OVERLAP_CLEAR": "0"},
+], ids=["default", "host-driven", "phase2-big", "lanes64x3", "lanes128x2-spec3", "noclearfold-noprefix", "noclearfold-inline"])
+def test_every_schedule_gives_the_oracles_integers(gp, oracle, cuda_device, monkeypatch, env):
+    """The lane / speculation / fusion knobs only change HOW the pipeline is scheduled.  One objective is evaluated
+    repeatedly with growing and shrinking batches (the scratch sets are left clean by k_pc_final and reused), on a
+    power-law graph (nothing left for phase 2), on disjoint cliques (everything is phase 2: more entries than
+    k_pc_final takes on, so the schedule learns to use the full-grid kernels) and on a sparse random graph (the
+    speculative schedule stands down, the host-driven loop takes over and teaches it the rounds it needs)."""
+    monkeypatch.setenv("GAPA_PC_SMALL", "0")
+    for key, value in env.items():
+        monkeypatch.setenv(key, value)
+    rng = np.random.default_rng(21)
+    n = 6000
+    cliques = np.array([(b * 6 + i, b * 6 + j) for b in range(n // 6) for i in range(6) for j in range(i + 1, 6)], dtype=np.int32)
+    ne = 30_000
+    er = rng.integers(0, ne, (int(ne * 1.8 / 2), 2)).astype(np.int32)
+    er = er[er[:, 0] != er[:, 1]]
+    er.sort(axis=1)
+    er = np.unique(er, axis=0)
+    ba = gp.barabasi_albert(20_000, 4, 3)
+    for graph in (ba, gp.Graph(n, cliques), gp.Graph(ne, er)):
+        og = oracle.graph_from_edges(graph.n, graph.edges())
+        pool = gp.build_gene_pool(graph, gp.PoolKind.NodeRemoval)
+        pc, mcn = gp.PairwiseConnectivityObjective(graph, pool), gp.SixDstObjective(graph, pool)
+        for rows in (70, 300, 64, 513, 1):
+            batch = gp.init_population(pool.size(), rows, graph.n // 20, rows)
+            assert np.array_equal(pc.evaluate_batch(batch), oracle.eval_batch(og, 0, batch, threads=8)), (graph.n, rows)
+            assert np.array_equal(mcn.evaluate_batch(batch), oracle.eval_batch(og, 1, batch, threads=8)), (graph.n, rows)
