@@ -338,6 +338,24 @@ def run_gpu_arm(args, w):
     e2e_s = time.perf_counter() - t0
     assert np.array_equal(host_out[:hi - lo].numpy(), ga.fit[lo:hi].cpu().numpy()), "e2e result differs from the device path"
 
+    # the same call with a PAGEABLE gene matrix — what the C++ adapter's evaluate_batch(const PopulationMatrix&) passes
+    # (a std::vector): the library stages it through its own pinned ring
+    pageable_genes = host_genes.numpy().copy()
+    pageable_out = np.empty(max(hi - lo, 1), dtype=np.float64)
+
+    def e2e_pageable_once():
+        gp.capi.check(lib.gapa_cuda_eval_batch(obj.dgraph.handle, obj.task, pageable_genes.ctypes.data, hi - lo, k,
+                                               pageable_out.ctypes.data))
+
+    for _ in range(2):
+        e2e_pageable_once()
+    barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        e2e_pageable_once()
+    e2e_pageable_s = time.perf_counter() - t0
+    assert np.array_equal(pageable_out[:hi - lo], ga.fit[lo:hi].cpu().numpy()), "pageable e2e result differs from the device path"
+
     # N > 1: the sharded run must BE the 1-GPU run (test_parallel.cpp:86-104): rank 0 repeats the same generations
     # unsharded with the same seed and compares history and final population bit for bit.
     verify = None
@@ -358,10 +376,11 @@ def run_gpu_arm(args, w):
             del solo
         barrier()
 
-    times = torch.tensor([step_ms_total, e2e_s * 1e3, float(np.mean(pure_ms)), float(np.mean(eval_ms))], dtype=torch.float64, device="cuda")
+    times = torch.tensor([step_ms_total, e2e_s * 1e3, float(np.mean(pure_ms)), float(np.mean(eval_ms)), e2e_pageable_s * 1e3],
+                         dtype=torch.float64, device="cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
-    step_ms_total, e2e_ms_total, eval_ms_mean, fused_ms_mean = (float(x) for x in times.cpu())
+    step_ms_total, e2e_ms_total, eval_ms_mean, fused_ms_mean, e2e_pageable_ms_total = (float(x) for x in times.cpu())
 
     if rank == 0:
         ms_per_step = step_ms_total / args.steps
@@ -408,7 +427,10 @@ def run_gpu_arm(args, w):
             "fitness_evals_per_sec_kernels_only": rows_per_rank * world / (eval_ms_mean * 1e-3),
             "e2e": {"value": e2e_value, "unit": "evals/s", "h2d_bytes_per_step": int(4 * (hi - lo) * k) * world,
                     "d2h_bytes_per_step": int(8 * (hi - lo)) * world,
-                    "path": "gapa_cuda_eval_batch(host genes) -> host fitness (FitnessFunction::evaluate_batch boundary)"},
+                    "path": "gapa_cuda_eval_batch(pinned host genes) -> host fitness (FitnessFunction::evaluate_batch boundary)"},
+            "e2e_pageable": {"value": s * args.steps / (e2e_pageable_ms_total * 1e-3), "unit": "evals/s",
+                             "path": "the same call with a pageable gene matrix (what CudaObjective::evaluate_batch(const "
+                                     "PopulationMatrix&) passes): staged through the library's pinned ring by host threads"},
             "gpu_launches": int(launches),
             "clocks": clocks,
             "comm": {"backend": "nccl" if world > 1 else None, "nranks": world},

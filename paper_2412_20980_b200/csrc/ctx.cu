@@ -39,6 +39,69 @@ static int upload_i32(const std::vector<int32_t>& h, int32_t** d) {
     return GAPA_CUDA_OK;
 }
 
+
+// ---- pinned staging ring for pageable host buffers ---------------------------------------------------------
+// push(): wait until the slot's previous H2D has drained, copy the slice into the slot with all copy threads, enqueue
+// the H2D.  With kSlots slices in flight the host copy of slice i+1 overlaps the DMA of slice i.
+PinnedRing::PinnedRing() {
+    const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
+    const int count = static_cast<int>(std::min(8u, std::max(1u, hw / 2)));
+    for (int t = 0; t < count; ++t) workers.emplace_back([this, t, count] { work(t, count); });
+}
+PinnedRing::~PinnedRing() {
+    {
+        std::lock_guard<std::mutex> lock(mu);
+        stop = true;
+        ++generation;
+    }
+    wake.notify_all();
+    for (std::thread& w : workers) w.join();
+    for (int i = 0; i < kSlots; ++i) {
+        if (done[i]) cudaEventDestroy(done[i]);
+        if (buf[i]) cudaFreeHost(buf[i]);
+    }
+}
+void PinnedRing::work(int index, int count) {
+    uint64_t seen = 0;
+    for (;;) {
+        std::unique_lock<std::mutex> lock(mu);
+        wake.wait(lock, [&] { return generation != seen; });
+        seen = generation;
+        if (stop) return;
+        const char* src = job_src;
+        char* dst = job_dst;
+        const size_t len = job_len;
+        lock.unlock();
+        const size_t part = ((len + count - 1) / count + 4095) & ~size_t{4095};
+        const size_t lo = std::min(len, part * index), hi = std::min(len, lo + part);
+        if (hi > lo) std::memcpy(dst + lo, src + lo, hi - lo);
+        lock.lock();
+        if (++finished == count) idle.notify_one();
+    }
+}
+int PinnedRing::push(void* dst_dev, const void* src_host, size_t len, cudaStream_t copy_stream) {
+    const int slot = next++ % kSlots;
+    if (!buf[slot]) {
+        GAPA_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&buf[slot]), kPinnedSliceBytes));
+        GAPA_CUDA_TRY(cudaEventCreateWithFlags(&done[slot], cudaEventDisableTiming));
+    } else {
+        GAPA_CUDA_TRY(cudaEventSynchronize(done[slot]));
+    }
+    {
+        std::unique_lock<std::mutex> lock(mu);
+        job_src = static_cast<const char*>(src_host);
+        job_dst = buf[slot];
+        job_len = len;
+        finished = 0;
+        ++generation;
+        wake.notify_all();
+        idle.wait(lock, [&] { return finished == static_cast<int>(workers.size()); });
+    }
+    GAPA_CUDA_TRY(cudaMemcpyAsync(dst_dev, buf[slot], len, cudaMemcpyHostToDevice, copy_stream));
+    GAPA_CUDA_TRY(cudaEventRecord(done[slot], copy_stream));
+    return GAPA_CUDA_OK;
+}
+
 // Edge rank of {u, v} in the (u,v)-sorted edge list, or -1.
 static int32_t edge_rank(const gapa_cuda_ctx* c, int32_t u, int32_t v) {
     if (u < 0 || v < 0 || u >= c->n || v >= c->n || u == v) return -1;
@@ -229,6 +292,8 @@ int gapa_cuda_destroy(gapa_cuda_ctx* c) {
     if (c->stream) cudaStreamDestroy(c->stream);
     if (c->copy_stream) cudaStreamDestroy(c->copy_stream);
     for (cudaEvent_t ev : c->copy_events) cudaEventDestroy(ev);
+    for (cudaEvent_t ev : c->chunk_events) cudaEventDestroy(ev);
+    delete c->ring;
     delete c;
     return GAPA_CUDA_OK;
 }
@@ -381,12 +446,14 @@ static int check_task(const gapa_cuda_ctx* c, int task) {
 }
 
 static int eval_rows_locked(gapa_cuda_ctx* c, int task, const GeneRows& genes, int rows, double* out_dev, void* stream,
-                            const VariationSpec* vary = nullptr, bool defer_timing = false) {
+                            const VariationSpec* vary = nullptr, bool defer_timing = false, bool already_locked = false,
+                            cudaEvent_t ev_begin = nullptr, cudaEvent_t ev_end = nullptr) {
     std::unique_lock<std::mutex> lock(c->mu, std::defer_lock);
-    if (stream != static_cast<void*>(c->stream)) lock.lock();  // the host-buffer form already holds it
+    if (!already_locked) lock.lock();  // the host-buffer form already holds it
     GAPA_CUDA_TRY(cudaSetDevice(c->device));
     cudaStream_t s = static_cast<cudaStream_t>(stream);
-    GAPA_CUDA_TRY(cudaEventRecord(c->ev_start, s));
+    if (!ev_begin) ev_begin = c->ev_start, ev_end = c->ev_stop;
+    GAPA_CUDA_TRY(cudaEventRecord(ev_begin, s));
     int rc;
     if (task == GAPA_TASK_PC || task == GAPA_TASK_MCN) {
         rc = pc_eval(c, task, genes, rows, out_dev, s, vary != nullptr, vary);  // builds the children itself
@@ -397,10 +464,10 @@ static int eval_rows_locked(gapa_cuda_ctx* c, int task, const GeneRows& genes, i
                                         : lpa_eval(c, genes, rows, out_dev, s, vary != nullptr);
     }
     if (rc != GAPA_CUDA_OK) return rc;
-    GAPA_CUDA_TRY(cudaEventRecord(c->ev_stop, s));
+    GAPA_CUDA_TRY(cudaEventRecord(ev_end, s));
     if (defer_timing) return GAPA_CUDA_OK;  // the caller synchronises the stream once and reads the events then
-    GAPA_CUDA_TRY(cudaEventSynchronize(c->ev_stop));
-    GAPA_CUDA_TRY(cudaEventElapsedTime(&c->last_eval_ms, c->ev_start, c->ev_stop));
+    GAPA_CUDA_TRY(cudaEventSynchronize(ev_end));
+    GAPA_CUDA_TRY(cudaEventElapsedTime(&c->last_eval_ms, ev_begin, ev_end));
     return GAPA_CUDA_OK;
 }
 
@@ -457,11 +524,11 @@ int gapa_cuda_eval_batch(gapa_cuda_ctx* c, int task, const int32_t* genes_host, 
     const size_t cells = static_cast<size_t>(rows) * cols;
     GAPA_TRY(c->genes_stage.ensure(sizeof(int32_t) * std::max<size_t>(cells, 1)));
     GAPA_TRY(c->out_stage.ensure(sizeof(double) * rows));
-    // Row chunks of ~64 MB (whole 64-individual groups): the H2D copy of chunk i+1 runs on the
-    // copy stream while the kernels of chunk i run on the work stream, so a PCIe-bound call
-    // costs max(copy, compute) instead of their sum.
+    // Row chunks of ~64 MB in whole super-groups of 256 individuals (one 32-byte record of the bit-sliced PC kernels):
+    // the H2D copy of chunk i+1 runs on the copy stream while the kernels of chunk i run on the work stream, so a
+    // PCIe-bound call costs max(copy, compute) instead of their sum.
     const size_t row_bytes = sizeof(int32_t) * static_cast<size_t>(std::max(cols, 1));
-    int chunk_rows = static_cast<int>(std::min<size_t>(rows, std::max<size_t>(64, ((64ull << 20) / row_bytes) & ~size_t{63})));
+    int chunk_rows = static_cast<int>(std::min<size_t>(rows, std::max<size_t>(256, ((64ull << 20) / row_bytes) & ~size_t{255})));
     const int chunks = (rows + chunk_rows - 1) / chunk_rows;
     if (!c->copy_stream) GAPA_CUDA_TRY(cudaStreamCreateWithFlags(&c->copy_stream, cudaStreamNonBlocking));
     while (static_cast<int>(c->copy_events.size()) < chunks) {
@@ -470,25 +537,60 @@ int gapa_cuda_eval_batch(gapa_cuda_ctx* c, int task, const int32_t* genes_host, 
         c->copy_events.push_back(ev);
     }
     int32_t* stage = c->genes_stage.as<int32_t>();
-    if (cells)
+    // A PAGEABLE caller buffer (std::vector of the reference's PopulationMatrix, population.hpp:12-40) would make every
+    // cudaMemcpyAsync a synchronous, driver-staged copy at a few GB/s.  Large pageable batches go through the
+    // library's own pinned ring instead: host threads copy slice i+1 into a pinned buffer while slice i crosses PCIe.
+    bool pageable = false;
+    if (cells * sizeof(int32_t) >= kPinnedRingMinBytes) {
+        cudaPointerAttributes attr{};
+        if (cudaPointerGetAttributes(&attr, genes_host) != cudaSuccess) (void)cudaGetLastError();
+        pageable = attr.type == cudaMemoryTypeUnregistered;
+    }
+    float total_ms = 0.f;
+    while (static_cast<int>(c->chunk_events.size()) < 2 * chunks) {
+        cudaEvent_t ev;
+        GAPA_CUDA_TRY(cudaEventCreate(&ev));
+        c->chunk_events.push_back(ev);
+    }
+    if (cells && !pageable)
         for (int i = 0; i < chunks; ++i) {
             const int r0 = i * chunk_rows, cr = std::min(chunk_rows, rows - r0);
             GAPA_CUDA_TRY(cudaMemcpyAsync(stage + static_cast<size_t>(r0) * cols, genes_host + static_cast<size_t>(r0) * cols,
                                           sizeof(int32_t) * static_cast<size_t>(cr) * cols, cudaMemcpyHostToDevice, c->copy_stream));
             GAPA_CUDA_TRY(cudaEventRecord(c->copy_events[i], c->copy_stream));
         }
-    float total_ms = 0.f;
-    const bool single = chunks == 1;  // small batches: one host synchronisation for kernels + read-back
+    if (pageable && !c->ring) c->ring = new PinnedRing();
+    size_t ring_next = 0;  // bytes of the gene matrix already handed to the ring
+    auto ring_feed = [&](size_t upto_bytes) -> int {  // stage the matrix up to this byte through the pinned ring
+        const char* src = reinterpret_cast<const char*>(genes_host);
+        char* dst = reinterpret_cast<char*>(stage);
+        while (ring_next < upto_bytes) {
+            const size_t len = std::min(kPinnedSliceBytes, upto_bytes - ring_next);
+            GAPA_TRY(c->ring->push(dst + ring_next, src + ring_next, len, c->copy_stream));
+            ring_next += len;
+        }
+        return GAPA_CUDA_OK;
+    };
     for (int i = 0; i < chunks; ++i) {
         const int r0 = i * chunk_rows, cr = std::min(chunk_rows, rows - r0);
+        if (pageable) {
+            // chunk i AND chunk i+1 are on their way before chunk i's kernels are enqueued
+            GAPA_TRY(ring_feed(sizeof(int32_t) * static_cast<size_t>(std::min(rows, r0 + cr)) * cols));
+            GAPA_CUDA_TRY(cudaEventRecord(c->copy_events[i], c->copy_stream));
+        }
         if (cells) GAPA_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_events[i], 0));
+        // every chunk has its own pair of timing events, read once at the end: the host is free to stage the next chunk
         GAPA_TRY(eval_rows_locked(c, task, GeneRows{stage + static_cast<size_t>(r0) * cols, nullptr, cols}, cr,
-                                  c->out_stage.as<double>() + r0, c->stream, nullptr, single));
-        total_ms += c->last_eval_ms;
+                                  c->out_stage.as<double>() + r0, c->stream, nullptr, true, true, c->chunk_events[2 * i],
+                                  c->chunk_events[2 * i + 1]));
     }
     GAPA_CUDA_TRY(cudaMemcpyAsync(out_host, c->out_stage.ptr, sizeof(double) * rows, cudaMemcpyDeviceToHost, c->stream));
     GAPA_CUDA_TRY(cudaStreamSynchronize(c->stream));
-    if (single) GAPA_CUDA_TRY(cudaEventElapsedTime(&total_ms, c->ev_start, c->ev_stop));
+    for (int i = 0; i < chunks; ++i) {
+        float ms = 0.f;
+        GAPA_CUDA_TRY(cudaEventElapsedTime(&ms, c->chunk_events[2 * i], c->chunk_events[2 * i + 1]));
+        total_ms += ms;
+    }
     c->last_eval_ms = total_ms;
     return GAPA_CUDA_OK;
 }

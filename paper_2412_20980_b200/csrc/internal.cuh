@@ -7,7 +7,9 @@
 
 #include <algorithm>
 #include <atomic>
+#include <condition_variable>
 #include <mutex>
+#include <thread>
 #include <utility>
 #include <cstdarg>
 #include <cstdio>
@@ -131,6 +133,29 @@ struct GeneRows {
     }
 };
 
+// ---- pinned staging ring (ctx.cu): pageable host buffers of the host-buffer entry point ----------------------
+static constexpr size_t kPinnedRingMinBytes = 8u << 20;   // smaller pageable batches take the plain copy
+static constexpr size_t kPinnedSliceBytes = 16u << 20;
+struct PinnedRing {
+    static constexpr int kSlots = 4;
+    char* buf[kSlots] = {};
+    cudaEvent_t done[kSlots] = {};
+    int next = 0;
+    std::vector<std::thread> workers;
+    std::mutex mu;
+    std::condition_variable wake, idle;
+    uint64_t generation = 0;
+    int finished = 0;
+    bool stop = false;
+    const char* job_src = nullptr;
+    char* job_dst = nullptr;
+    size_t job_len = 0;
+    PinnedRing();
+    ~PinnedRing();
+    void work(int index, int count);
+    int push(void* dst_dev, const void* src_host, size_t len, cudaStream_t copy_stream);
+};
+
 // ---- context -------------------------------------------------------------------------
 struct PcScratch;   // pc_kernels.cu
 struct LpaScratch;  // lpa_kernels.cu
@@ -170,7 +195,8 @@ struct gapa_cuda_ctx {
     // work stream + timing
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;          // H2D of the host-buffer entry point, overlapped with compute
-    std::vector<cudaEvent_t> copy_events;
+    std::vector<cudaEvent_t> copy_events, chunk_events;
+    gapa_b200::PinnedRing* ring = nullptr;           // created by the first large pageable batch
     cudaEvent_t ev_start = nullptr, ev_stop = nullptr;
     float last_eval_ms = 0.f;
     // FitnessFunction methods are const and called concurrently from worker threads in the

@@ -149,3 +149,30 @@ def test_concurrent_callers_share_one_objective(gp, oracle, cuda_device):
     for t, b in enumerate(batches):
         assert np.array_equal(got[0][t], oracle.eval_batch(og, 0, b))
         assert np.array_equal(got[1][t], oracle.eval_batch(og, 1, b))
+
+
+def test_large_pageable_batches_take_the_pinned_ring(gp, oracle, cuda_device):
+    """evaluate_batch(const PopulationMatrix&) hands the library a pageable std::vector (population.hpp:12-40); batches
+    of 8 MB and more are staged through the library's pinned ring in 16 MB slices by several host threads.  Same
+    fitness as the pinned-buffer call, the device-buffer call and the oracle; ragged last slice and last chunk."""
+    import torch
+    g = gp.barabasi_albert(20_000, 3, 2)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    obj = gp.PairwiseConnectivityObjective(g, pool)
+    rows, k = 9_001, 1_000  # 36 MB: three slices, the last one ragged
+    batch = gp.init_population(pool.size(), rows, k, 11)  # numpy: pageable
+    got = obj.evaluate_batch(batch)
+    pinned = torch.from_numpy(batch).pin_memory()
+    out = torch.empty(rows, dtype=torch.float64).pin_memory()
+    lib = gp.capi.load()
+    gp.capi.check(lib.gapa_cuda_eval_batch(obj.dgraph.handle, obj.task, pinned.data_ptr(), rows, k, out.data_ptr()))
+    assert np.array_equal(got, out.numpy())
+    dev = torch.from_numpy(batch).cuda()
+    dout = torch.empty(rows, dtype=torch.float64, device="cuda")
+    obj.dgraph.eval_batch_device(obj.task, dev.data_ptr(), rows, k, dout.data_ptr(), 0)
+    torch.cuda.synchronize()
+    assert np.array_equal(got, dout.cpu().numpy())
+    pick = np.r_[0:40, 4090:4110, rows - 30:rows]
+    assert np.array_equal(got[pick], oracle.eval_batch(og, 0, batch[pick], threads=8))
+    assert np.array_equal(obj.evaluate_batch(batch), got)  # ring slots reused

@@ -32,6 +32,30 @@ def test_full_size_matches_the_oracle_on_a_sample(gp, oracle, c4):
     assert np.all(c2(got_mcn[:64]) <= got_pc[:64]) and np.all(got_pc[:64] <= c2(got_mcn[:64]) + c2(alive - got_mcn[:64]))
 
 
+def test_full_size_every_row_of_the_bench_population(gp, oracle, c4):
+    """BASELINE configs[3] at its own population: all 4096 individuals of one batch against the oracle (PC), and all
+    1024 of the module's batch for MCN — the numbers bench.py quotes are for exactly this shape."""
+    g, pool, pop = c4
+    og = oracle.graph_from_edges(g.n, g.edges())
+    big = gp.init_population(pool.size(), 4096, K, 2)
+    assert np.array_equal(gp.PairwiseConnectivityObjective(g, pool).evaluate_batch(big), oracle.eval_batch(og, 0, big, threads=16))
+    assert np.array_equal(gp.SixDstObjective(g, pool).evaluate_batch(pop), oracle.eval_batch(og, 1, pop, threads=16))
+
+
+def test_full_size_trajectory_matches_the_oracle(gp, oracle, c4):
+    """Three generations of the C4 GA (population 256) against oracle.run_ga: history best AND mean, final population
+    and fitness bit for bit (test_parallel.cpp:86-104 at n = 1e6); the library loop and the stepwise sharded driver
+    (two ranks in one process, stand-in all-gather) must both reproduce it."""
+    g, pool, _ = c4
+    og = oracle.graph_from_edges(g.n, g.edges())
+    obj = gp.PairwiseConnectivityObjective(g, pool)
+    params = gp.GAParams(pc=0.6, pm=0.2, pop_size=256, budget=K, iterations=3, seed=5)
+    want = oracle.run_ga(og, 0, 0.6, 0.2, 256, K, 3, 5, threads=16)
+    res = gp.run_ga(params, pool, obj)
+    assert np.array_equal(res.history_best, want["best"]) and np.array_equal(res.history_mean, want["mean"])
+    assert np.array_equal(res.final_population, want["population"]) and np.array_equal(res.final_fitness, want["fitness"])
+
+
 def test_full_size_properties(gp, c4):
     g, pool, pop = c4
     pc = gp.PairwiseConnectivityObjective(g, pool)

@@ -118,6 +118,20 @@ def test_cda_more_individuals_than_sms(gp, oracle, cuda_device):
     assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(og, 2, batch, threads=8))
 
 
+def test_cda_config2_whole_population(gp, oracle, cuda_device):
+    """BASELINE configs[1] at its own size: SBM 10 x 500, 5 % edge deletion, all 100 individuals of the population
+    against the oracle, bit-exact FP64."""
+    g = gp.planted_partition(10, 500, 0.02, 0.0005, 1)
+    pool = _edge_pool(gp, g)
+    k = gp.perturbation_budget(g, gp.PoolKind.EdgeRemoval, 0.05)
+    assert (g.edge_count(), k) == (30321, 1517)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    batch = gp.init_population(pool.size(), 100, k, 1)
+    got = gp.ModularityAttackObjective(g, pool).evaluate_batch(batch)
+    assert np.array_equal(got, oracle.eval_batch(og, 2, batch, threads=16))
+    assert len(np.unique(got)) > 90  # the individuals really differ
+
+
 def test_cda_config2_sample(gp, oracle, cuda_device):
     """BASELINE config 2 shape: SBM 10 x 500, 5 % edge deletion (2 individuals vs the oracle)."""
     g = gp.planted_partition(10, 500, 0.02, 0.0005, 1)

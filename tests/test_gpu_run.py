@@ -45,6 +45,38 @@ def test_small_runs_match_oracle(gp, oracle, cuda_device, task):
         _same(res, oracle.run_ga(og, task, 0.8, 0.1, 30, 8, 25, seed, eda_interval=eda))
 
 
+def test_maximize_direction_runs_match_oracle(gp, oracle, cuda_device):
+    """Direction::Maximize (population.hpp:9) through the whole loop — selection weights, roulette, elitism order and the
+    history all flip (ga_ops.cpp:62, :199).  The reference's tasks minimise; its toy objectives maximise."""
+    g = gp.erdos_renyi(120, 0.035, 11)
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    for task, cls, s, eda in ((0, gp.PairwiseConnectivityObjective, 40, 0), (1, gp.SixDstObjective, 700, 4)):
+        params = gp.GAParams(pc=0.7, pm=0.1, pop_size=s, budget=10, iterations=12, seed=9, eda_interval=eda or None,
+                             direction=gp.Direction.Maximize)
+        res = gp.run_ga(params, pool, cls(g, pool))
+        _same(res, oracle.run_ga(og, task, 0.7, 0.1, s, 10, 12, 9, eda_interval=eda, minimize=False, threads=8))
+        assert np.all(np.diff(res.history_best) >= 0) and np.all(np.diff(res.final_fitness) <= 0)  # best first = largest first
+
+
+def test_c5_corner_population_16384(gp, oracle, cuda_device):
+    """BASELINE configs[4] corner: n = 1e5, population 16,384 (four lanes of 4096 on two streams): every 64th row and
+    both ends against the oracle; one generation of the loop keeps history and stored fitness consistent."""
+    g = gp.barabasi_albert(100_000, 5, 1)
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    og = oracle.graph_from_edges(g.n, g.edges())
+    obj = gp.PairwiseConnectivityObjective(g, pool)
+    s, k = 16_384, 5_000
+    pop = gp.init_population(pool.size(), s, k, 3)
+    got = obj.evaluate_batch(pop)
+    pick = np.unique(np.r_[0:16, 0:s:64, 4090:4100, 8190:8194, s - 16:s])
+    assert np.array_equal(got[pick], oracle.eval_batch(og, 0, pop[pick], threads=16))
+    res = gp.run_ga(gp.GAParams(pc=0.6, pm=0.2, pop_size=s, budget=k, iterations=1, seed=3), pool, obj)
+    assert res.history_best[0] == res.final_fitness[0] and np.all(np.diff(res.final_fitness) >= 0)
+    rows = np.r_[0:8, s - 8:s]
+    assert np.array_equal(res.final_fitness[rows], oracle.eval_batch(og, 0, res.final_population[rows], threads=16))
+
+
 def test_large_population_run_matches_oracle(gp, oracle, cuda_device):
     """Large ragged population sizes (multi-block ranking, weight and pick kernels),
     ragged, on a small graph so that fitness ties are everywhere (stable tie-breaks matter)."""
