@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define GAPA_CUDA_ABI_VERSION 2
+#define GAPA_CUDA_ABI_VERSION 3
 
 enum {
     GAPA_CUDA_OK = 0,
@@ -261,6 +261,58 @@ typedef struct gapa_cuda_run_result {
 
 int gapa_cuda_run(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* params, gapa_cuda_allgather_fn exchange,
                   void* exchange_user, gapa_cuda_run_result* result);
+
+/* The same loop as a resumable object: the population stays in HBM between calls, so a host can interleave its own
+ * work (logging, check-pointing, a stop criterion on history_best — modes.cpp:159-175 is a plain for loop) with
+ * blocks of generations.  gapa_cuda_run == create + advance(iterations) + result + destroy.
+ *   create:  validates like gapa_cuda_run; want_stats != 0 collects the GenerationStats timing columns
+ *   advance: runs min(generations, iterations - done) generations; returns when they have finished on the device;
+ *            *device_ms (optional) = device time of the block, CUDA events on the run's stream
+ *   result:  history (zeros beyond the generations done), final population / fitness = the CURRENT parents */
+typedef struct gapa_cuda_ga gapa_cuda_ga;
+int gapa_cuda_ga_create(gapa_cuda_ctx* ctx, const gapa_cuda_run_params* params, gapa_cuda_allgather_fn exchange,
+                        void* exchange_user, int want_stats, gapa_cuda_ga** out);
+int gapa_cuda_ga_advance(gapa_cuda_ga* ga, int generations, float* device_ms);
+int gapa_cuda_ga_generation(const gapa_cuda_ga* ga, int* generations_done);
+int gapa_cuda_ga_result(gapa_cuda_ga* ga, gapa_cuda_run_result* result);
+int gapa_cuda_ga_destroy(gapa_cuda_ga* ga);
+
+/* ---- the exchange of a row-sharded run, shipped with the library (the GPU form of Channel<T>, channel.hpp:12-35) ----
+ * A communicator connects the `world` ranks of one run (one rank per GPU; ranks may be threads of one process or
+ * separate processes on one node).  gapa_cuda_comm_allgather has the gapa_cuda_allgather_fn signature: pass it, with
+ * the communicator as `exchange_user`, to gapa_cuda_run / gapa_cuda_ga_create.
+ *   PEER: mailboxes in HBM that the peers write directly over NVLink / NVSwitch (same process: peer access; other
+ *         processes: CUDA IPC) — one kernel per exchange, no host involvement.  Set-up: every rank calls
+ *         gapa_cuda_comm_create and publishes the GAPA_CUDA_COMM_HANDLE_BYTES it returns to all ranks by any
+ *         out-of-band means (a file, MPI, torch.distributed, a pipe); every rank then calls gapa_cuda_comm_connect
+ *         with the `world` handles in rank order.
+ *   NCCL: ncclAllGather on the caller's stream (libnccl.so.2 is loaded at run time).  Set-up: rank 0 calls
+ *         gapa_cuda_nccl_unique_id and publishes the 128 bytes; every rank calls gapa_cuda_comm_create_nccl
+ *         (collectively, like ncclCommInitRank).
+ * A peer that does not arrive within GAPA_COMM_TIMEOUT_MS (default 20000) turns into GAPA_CUDA_E_CUDA from
+ * gapa_cuda_comm_status / the run, not into a hang. */
+#define GAPA_CUDA_COMM_HANDLE_BYTES 128
+#define GAPA_CUDA_COMM_CTRL_BYTES 256
+enum { GAPA_COMM_PEER = 0, GAPA_COMM_NCCL = 1 };
+typedef struct gapa_cuda_comm gapa_cuda_comm;
+int gapa_cuda_comm_create(gapa_cuda_ctx* ctx, int rank, int world, int pop_size, gapa_cuda_comm** out, void* handle_out);
+int gapa_cuda_comm_connect(gapa_cuda_comm* comm, const void* all_handles);
+int gapa_cuda_nccl_unique_id(void* id128_out);
+int gapa_cuda_comm_create_nccl(gapa_cuda_ctx* ctx, const void* unique_id128, int rank, int world, gapa_cuda_comm** out);
+int gapa_cuda_comm_allgather(void* comm, double* fit_full_dev, int s, int padded_block, void* stream);
+/* host-level all-gather of up to GAPA_CUDA_COMM_CTRL_BYTES bytes per rank through the same transport (blocking):
+ * all_host receives world x bytes in rank order */
+int gapa_cuda_comm_allgather_bytes(gapa_cuda_comm* comm, const void* mine_host, int bytes, void* all_host);
+int gapa_cuda_comm_status(gapa_cuda_comm* comm);
+int gapa_cuda_comm_info(const gapa_cuda_comm* comm, int* transport, int* rank, int* world);
+int gapa_cuda_comm_destroy(gapa_cuda_comm* comm);
+/* run_mode_m for C / C++ hosts (modes.cpp:190-349): ONE process, one host thread per context (normally one context
+ * per GPU), row blocks by partition_rows, the exchange built in (transport = GAPA_COMM_PEER or GAPA_COMM_NCCL).
+ * params->rank / world are ignored; results[r] is rank r's result — every rank ends with the same history and
+ * population (test_parallel.cpp:86-104), so hosts usually fill in results[0] only and leave the others' output
+ * pointers null. */
+int gapa_cuda_run_multi(gapa_cuda_ctx* const* ctxs, int world, const gapa_cuda_run_params* params, int transport,
+                        gapa_cuda_run_result* results);
 
 /* ---- host-side problem setup (CPU, once per experiment — inputs to the path) --------
  * Deterministic generators with the reference's draw sequences (generators.cpp) and

@@ -484,28 +484,114 @@ def overhead_report(result: RunResult) -> str:
     return "".join(lines)
 
 
-def run_ga(params: GAParams, pool: GenePool, fitness: FitnessFunction, rank: int = 0, world: int = 1,
-           exchange=None) -> RunResult:
-    """run_ga for Mode::S (modes.cpp:132-178) on one GPU, or one rank of a sharded run."""
+class _ResultBuffers:
+    """host arrays behind a gapa_cuda_run_result"""
+
+    def __init__(self, params: GAParams, outputs: bool = True):
+        s, k, it = params.pop_size, params.budget, params.iterations
+        self.it = it
+        self.hb, self.hm = np.zeros(it), np.zeros(it)
+        self.fp, self.ff = np.zeros((s, k), dtype=np.int32), np.zeros(s)
+        self.wall, self.comp, self.exch, self.life = (np.zeros(it) for _ in range(4))
+        self.msgs = np.zeros(it, dtype=np.uint64)
+        null_f, null_i = C.cast(None, capi.c_f64p), C.cast(None, capi.c_i32p)
+        if outputs:
+            self.c = capi.RunResult(self.hb.ctypes.data_as(capi.c_f64p), self.hm.ctypes.data_as(capi.c_f64p),
+                                    self.fp.ctypes.data_as(capi.c_i32p), self.ff.ctypes.data_as(capi.c_f64p), 0, 0.0, 0.0,
+                                    self.wall.ctypes.data_as(capi.c_f64p), self.comp.ctypes.data_as(capi.c_f64p),
+                                    self.exch.ctypes.data_as(capi.c_f64p), self.life.ctypes.data_as(capi.c_f64p),
+                                    self.msgs.ctypes.data_as(C.POINTER(C.c_uint64)))
+        else:
+            self.c = capi.RunResult(null_f, null_f, null_i, null_f, 0, 0.0, 0.0, null_f, null_f, null_f, null_f,
+                                    C.cast(None, C.POINTER(C.c_uint64)))
+
+    def result(self) -> "RunResult":
+        history = [GenerationStats(float(self.hb[i]), float(self.hm[i]), float(self.wall[i]), float(self.comp[i]),
+                                   float(self.exch[i]), float(self.life[i]), int(self.msgs[i])) for i in range(self.it)]
+        return RunResult(self.fp, self.ff, self.fp[0].copy(), float(self.ff[0]), self.hb, self.hm,
+                         int(self.c.fitness_batch_calls), float(self.c.total_wall_seconds), float(self.c.eval_seconds), history)
+
+
+def _run_params(params: GAParams, fitness: FitnessFunction, rank: int, world: int) -> "capi.RunParams":
     params.validate()
     if params.iterations < 1:  # modes.cpp:26-29
         raise GapaCudaError(capi.E_INVALID, "iterations must be >= 1")
-    lib = capi.load()
-    s, k, it = params.pop_size, params.budget, params.iterations
-    hb, hm = np.zeros(it), np.zeros(it)
-    fp, ff = np.zeros((s, k), dtype=np.int32), np.zeros(s)
-    p = capi.RunParams(params.pc, params.pm, s, k, it, _minimize(params.direction), params.eda_interval or 0,
-                       fitness.task, params.seed, rank, world)
-    wall, comp, exch, life = (np.zeros(it) for _ in range(4))
-    msgs = np.zeros(it, dtype=np.uint64)
-    r = capi.RunResult(hb.ctypes.data_as(capi.c_f64p), hm.ctypes.data_as(capi.c_f64p),
-                       fp.ctypes.data_as(capi.c_i32p), ff.ctypes.data_as(capi.c_f64p), 0, 0.0, 0.0,
-                       wall.ctypes.data_as(capi.c_f64p), comp.ctypes.data_as(capi.c_f64p),
-                       exch.ctypes.data_as(capi.c_f64p), life.ctypes.data_as(capi.c_f64p),
-                       msgs.ctypes.data_as(C.POINTER(C.c_uint64)))
-    cb = capi.ALLGATHER_FN(exchange) if exchange is not None else C.cast(None, capi.ALLGATHER_FN)
-    check(lib.gapa_cuda_run(fitness.dgraph.handle, C.byref(p), cb, None, C.byref(r)))
-    history = [GenerationStats(float(hb[i]), float(hm[i]), float(wall[i]), float(comp[i]), float(exch[i]), float(life[i]),
-                               int(msgs[i])) for i in range(it)]
-    return RunResult(fp, ff, fp[0].copy(), float(ff[0]), hb, hm, int(r.fitness_batch_calls),
-                     float(r.total_wall_seconds), float(r.eval_seconds), history)
+    return capi.RunParams(params.pc, params.pm, params.pop_size, params.budget, params.iterations, _minimize(params.direction),
+                          params.eda_interval or 0, fitness.task, params.seed, rank, world)
+
+
+def _exchange_args(exchange, comm):
+    """(hook, user) for the C ABI: a Python callable, or the library's own exchange with a Comm"""
+    if comm is not None:
+        return C.cast(capi.load().gapa_cuda_comm_allgather, capi.ALLGATHER_FN), comm.handle
+    if exchange is not None:
+        return capi.ALLGATHER_FN(exchange), None
+    return C.cast(None, capi.ALLGATHER_FN), None
+
+
+def run_ga(params: GAParams, pool: GenePool, fitness: FitnessFunction, rank: int = 0, world: int = 1,
+           exchange=None, comm=None) -> RunResult:
+    """run_ga for Mode::S (modes.cpp:132-178) on one GPU, or one rank of a sharded run (exchange: a Python hook, or
+    comm: a driver.Comm — the library's own peer-mailbox / NCCL exchange)."""
+    p = _run_params(params, fitness, rank, world)
+    buf = _ResultBuffers(params)
+    cb, user = _exchange_args(exchange, comm)
+    check(capi.load().gapa_cuda_run(fitness.dgraph.handle, C.byref(p), cb, user, C.byref(buf.c)))
+    return buf.result()
+
+
+def run_ga_multi(params: GAParams, fitnesses, transport: str = "peer") -> list:
+    """run_mode_m on GPUs from ONE process (gapa_cuda_run_multi): fitnesses[r] is rank r's objective (its own context,
+    normally on its own GPU); returns every rank's RunResult — identical by the determinism contract."""
+    world = len(fitnesses)
+    p = _run_params(params, fitnesses[0], 0, world)
+    bufs = [_ResultBuffers(params) for _ in range(world)]
+    ctxs = (capi.VP * world)(*[f.dgraph.handle for f in fitnesses])
+    results = (capi.RunResult * world)(*[b.c for b in bufs])
+    check(capi.load().gapa_cuda_run_multi(ctxs, world, C.byref(p), {"peer": 0, "nccl": 1}[transport], results))
+    for b, r in zip(bufs, results):
+        b.c = r
+    return [b.result() for b in bufs]
+
+
+class GaLoop:
+    """The in-library generation loop as a resumable object (gapa_cuda_ga_*): the population stays in HBM between
+    advance() calls."""
+
+    def __init__(self, params: GAParams, fitness: FitnessFunction, rank: int = 0, world: int = 1, exchange=None, comm=None,
+                 want_stats: bool = False):
+        self.params, self.fitness = params, fitness
+        p = _run_params(params, fitness, rank, world)
+        self._cb, user = _exchange_args(exchange, comm)  # keep the callback object alive
+        self._comm = comm
+        self.handle = capi.VP()
+        check(capi.load().gapa_cuda_ga_create(fitness.dgraph.handle, C.byref(p), self._cb, user, 1 if want_stats else 0,
+                                              C.byref(self.handle)))
+
+    def advance(self, generations: int) -> float:
+        """runs the next `generations` generations; returns their device time in ms (CUDA events on the run's stream)"""
+        ms = C.c_float(0.0)
+        check(capi.load().gapa_cuda_ga_advance(self.handle, generations, C.byref(ms)))
+        return float(ms.value)
+
+    @property
+    def generation(self) -> int:
+        g = C.c_int(0)
+        check(capi.load().gapa_cuda_ga_generation(self.handle, C.byref(g)))
+        return g.value
+
+    def result(self) -> RunResult:
+        buf = _ResultBuffers(self.params)
+        check(capi.load().gapa_cuda_ga_result(self.handle, C.byref(buf.c)))
+        return buf.result()
+
+    def close(self):
+        if self.handle:
+            capi.load().gapa_cuda_ga_destroy(self.handle)
+            self.handle = capi.VP()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass

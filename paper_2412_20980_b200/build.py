@@ -13,7 +13,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libgapa_cuda.so")
-SOURCES = ["ctx.cu", "pc_kernels.cu", "ga_kernels.cu", "lpa_kernels.cu", "cda_kernels.cu", "run.cu", "host_graph.cu", "slot_kernels.cu", "sixdst_kernels.cu"]
+SOURCES = ["ctx.cu", "pc_kernels.cu", "ga_kernels.cu", "lpa_kernels.cu", "cda_kernels.cu", "run.cu", "host_graph.cu", "slot_kernels.cu", "sixdst_kernels.cu", "comm.cu"]
 HEADERS = [os.path.join(CSRC, "internal.cuh"), os.path.join(CSRC, "variation.cuh"), os.path.join(REPO, "include", "gapa_cuda.h")]
 
 # -fmad=false: the FP64 paths (modularity gain, RA score, AUC) must round exactly like
@@ -57,7 +57,7 @@ def build(force: bool = False, verbose: bool = False) -> str:
             print(out)
         if p.returncode != 0:
             raise RuntimeError(f"nvcc failed on {src}:\n{out}")
-    subprocess.check_call([nvcc(), "-shared", "-o", LIB, *objs, "-gencode", "arch=compute_100a,code=sm_100a"])
+    subprocess.check_call([nvcc(), "-shared", "-o", LIB, *objs, "-gencode", "arch=compute_100a,code=sm_100a", "-ldl", "-lpthread"])
     return LIB
 
 

@@ -89,6 +89,21 @@ SIGNATURES = {
     "gapa_cuda_ga_elitism": (C.c_int, [C.c_int, VP, VP, C.c_int, C.c_int, VP, VP, C.c_int, VP, VP]),
     "gapa_cuda_rng_draws": (C.c_int, [C.c_int, C.c_uint64, C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, VP]),
     "gapa_cuda_run": (C.c_int, [VP, C.POINTER(RunParams), ALLGATHER_FN, VP, C.POINTER(RunResult)]),
+    "gapa_cuda_ga_create": (C.c_int, [VP, C.POINTER(RunParams), ALLGATHER_FN, VP, C.c_int, C.POINTER(VP)]),
+    "gapa_cuda_ga_advance": (C.c_int, [VP, C.c_int, C.POINTER(C.c_float)]),
+    "gapa_cuda_ga_generation": (C.c_int, [VP, C.POINTER(C.c_int)]),
+    "gapa_cuda_ga_result": (C.c_int, [VP, C.POINTER(RunResult)]),
+    "gapa_cuda_ga_destroy": (C.c_int, [VP]),
+    "gapa_cuda_comm_create": (C.c_int, [VP, C.c_int, C.c_int, C.c_int, C.POINTER(VP), VP]),
+    "gapa_cuda_comm_connect": (C.c_int, [VP, VP]),
+    "gapa_cuda_nccl_unique_id": (C.c_int, [VP]),
+    "gapa_cuda_comm_create_nccl": (C.c_int, [VP, VP, C.c_int, C.c_int, C.POINTER(VP)]),
+    "gapa_cuda_comm_allgather": (C.c_int, [VP, VP, C.c_int, C.c_int, VP]),
+    "gapa_cuda_comm_allgather_bytes": (C.c_int, [VP, VP, C.c_int, VP]),
+    "gapa_cuda_comm_status": (C.c_int, [VP]),
+    "gapa_cuda_comm_info": (C.c_int, [VP, C.POINTER(C.c_int), C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "gapa_cuda_comm_destroy": (C.c_int, [VP]),
+    "gapa_cuda_run_multi": (C.c_int, [C.POINTER(VP), C.c_int, C.POINTER(RunParams), C.c_int, C.POINTER(RunResult)]),
     "gapa_host_barabasi_albert": (C.c_int, [C.c_int32, C.c_int32, C.c_uint64, VP, C.c_int64, C.POINTER(C.c_int64)]),
     "gapa_host_erdos_renyi": (C.c_int, [C.c_int32, C.c_double, C.c_uint64, VP, C.c_int64, C.POINTER(C.c_int64)]),
     "gapa_host_planted_partition": (C.c_int, [C.c_int32, C.c_int32, C.c_double, C.c_double, C.c_uint64, VP, C.c_int64,

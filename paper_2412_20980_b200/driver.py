@@ -136,6 +136,62 @@ class CudaOps:
         return t.cpu().numpy()
 
 
+class Comm:
+    """The library's own exchange (include/gapa_cuda.h, gapa_cuda_comm_*): peer mailboxes over NVLink, or NCCL.
+
+    `allgather_bytes(mine: bytes) -> list[bytes]` is any out-of-band all-gather between the ranks (torch.distributed
+    all_gather_object, MPI, files): it carries the 128-byte handles once at set-up."""
+
+    def __init__(self, handle, keep=None):
+        self.handle, self._keep = handle, keep
+
+    @classmethod
+    def peer(cls, fitness: FitnessFunction, rank: int, world: int, pop_size: int, allgather_bytes) -> "Comm":
+        import ctypes as C
+        lib = capi.load()
+        handle = C.c_void_p()
+        mine = C.create_string_buffer(128)
+        check(lib.gapa_cuda_comm_create(fitness.dgraph.handle, rank, world, pop_size, C.byref(handle), mine))
+        everyone = allgather_bytes(mine.raw)
+        if len(everyone) != world:
+            raise GapaCudaError(capi.E_INVALID, "Comm.peer: the out-of-band all-gather must return one handle per rank")
+        check(lib.gapa_cuda_comm_connect(handle, b"".join(everyone)))
+        return cls(handle)
+
+    @classmethod
+    def nccl(cls, fitness: FitnessFunction, rank: int, world: int, broadcast_bytes) -> "Comm":
+        """broadcast_bytes(data_or_None) -> bytes: rank 0 passes the unique id, everyone receives it"""
+        import ctypes as C
+        lib = capi.load()
+        uid = C.create_string_buffer(128)
+        if rank == 0:
+            check(lib.gapa_cuda_nccl_unique_id(uid))
+        data = broadcast_bytes(uid.raw if rank == 0 else None)
+        handle = C.c_void_p()
+        check(lib.gapa_cuda_comm_create_nccl(fitness.dgraph.handle, data, rank, world, C.byref(handle)))
+        return cls(handle)
+
+    def status(self):
+        check(capi.load().gapa_cuda_comm_status(self.handle))
+
+    def close(self):
+        if self.handle:
+            capi.load().gapa_cuda_comm_destroy(self.handle)
+            self.handle = None
+
+
+def torch_bytes_allgather(group=None):
+    """out-of-band all-gather of small byte strings over torch.distributed (any backend)"""
+    import torch.distributed as dist
+
+    def gather(mine: bytes):
+        out = [None] * dist.get_world_size(group)
+        dist.all_gather_object(out, mine, group=group)
+        return out
+
+    return gather
+
+
 def torch_allgather(group=None):
     """In-place all-gather of the padded fitness vector over torch.distributed."""
     import torch.distributed as dist

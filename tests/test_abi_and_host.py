@@ -28,7 +28,7 @@ def test_library_exports_every_declared_symbol(gp):
         assert hasattr(lib, name), f"{name} is declared in include/gapa_cuda.h but not exported"
         assert name in gp.capi.SIGNATURES, f"{name} has no ctypes signature in capi.py"
     assert set(gp.capi.SIGNATURES) == set(declared)
-    assert lib.gapa_cuda_abi_version() == 2
+    assert lib.gapa_cuda_abi_version() == 3
 
 
 def test_library_is_sm100a_cuda_code(gp):
