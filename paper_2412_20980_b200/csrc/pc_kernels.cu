@@ -212,8 +212,13 @@ __global__ void __launch_bounds__(nt) k_pc_bitmask_vary(VariationSpec V, int k, 
     __syncthreads();
     const uint64_t ks = keys[0], kc = keys[1], km = keys[2], ki = keys[3];
     const bool eda = V.partner == nullptr;
-    const int32_t* mine = V.pool + static_cast<size_t>(V.parent[row]) * k;
-    const int32_t* theirs = eda ? mine : V.pool + static_cast<size_t>(V.parent[V.partner[row]]) * k;
+    const int slot_mine = V.parent[row], slot_theirs = eda ? slot_mine : V.parent[V.partner[row]];
+    bool adopt_mine, adopt_theirs;  // the row lives in another rank's HBM: read it there, keep a copy here
+    const int32_t* mine = parent_row(V, slot_mine, k, &adopt_mine);
+    const int32_t* theirs = eda ? mine : parent_row(V, slot_theirs, k, &adopt_theirs);
+    if (eda || slot_theirs == slot_mine) adopt_theirs = false;
+    int32_t* keep_mine = V.pool + static_cast<size_t>(slot_mine) * k;
+    int32_t* keep_theirs = V.pool + static_cast<size_t>(slot_theirs) * k;
     int32_t* dst = V.pool + static_cast<size_t>(V.child[row]) * k;
     auto mark = [&](int gene) {
         const int node = gene_map ? gene_map[gene] : gene;
@@ -235,6 +240,8 @@ __global__ void __launch_bounds__(nt) k_pc_bitmask_vary(VariationSpec V, int k, 
                 a_next = __ldcs(&mine4[q + nt]);
                 b_next = eda ? a_next : __ldcs(&theirs4[q + nt]);
             }
+            if (adopt_mine) reinterpret_cast<int4*>(keep_mine)[q] = a;
+            if (adopt_theirs) reinterpret_cast<int4*>(keep_theirs)[q] = b;
             const int av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
             int r[4];
             uint64_t prod = kCounterStep * (static_cast<uint64_t>(q) * 4 + 1);
@@ -249,7 +256,10 @@ __global__ void __launch_bounds__(nt) k_pc_bitmask_vary(VariationSpec V, int k, 
         }
     } else {
         for (int j = threadIdx.x; j < k; j += nt) {
-            const int gsel = child_gene(V.P, V.pool, V.parent, k, j, mine[j], theirs[j], eda, ks, kc, km, ki,
+            const int a = mine[j], b = theirs[j];
+            if (adopt_mine) keep_mine[j] = a;
+            if (adopt_theirs) keep_theirs[j] = b;
+            const int gsel = child_gene(V.P, V.pool, V.parent, k, j, a, b, eda, ks, kc, km, ki,
                                         kCounterStep * (static_cast<uint64_t>(j) + 1));
             dst[j] = gsel;
             mark(gsel);
@@ -1010,11 +1020,19 @@ __global__ void __launch_bounds__(kSmallThreads) k_pc_small(GeneRows genes,
         __syncthreads();
         const uint64_t ks = vary_keys[0], kc = vary_keys[1], km = vary_keys[2], ki = vary_keys[3];
         const bool eda = V.partner == nullptr;
-        const int32_t* mine = V.pool + static_cast<size_t>(V.parent[vrow]) * cols;
-        const int32_t* theirs = eda ? mine : V.pool + static_cast<size_t>(V.parent[V.partner[vrow]]) * cols;
+        const int slot_mine = V.parent[vrow], slot_theirs = eda ? slot_mine : V.parent[V.partner[vrow]];
+        bool adopt_mine, adopt_theirs;
+        const int32_t* mine = parent_row(V, slot_mine, cols, &adopt_mine);
+        const int32_t* theirs = eda ? mine : parent_row(V, slot_theirs, cols, &adopt_theirs);
+        if (eda || slot_theirs == slot_mine) adopt_theirs = false;
+        int32_t* keep_mine = V.pool + static_cast<size_t>(slot_mine) * cols;
+        int32_t* keep_theirs = V.pool + static_cast<size_t>(slot_theirs) * cols;
         int32_t* dst = V.pool + static_cast<size_t>(V.child[vrow]) * cols;
         for (int j = tid; j < cols; j += kSmallThreads) {
-            const int gene = child_gene(V.P, V.pool, V.parent, cols, j, mine[j], theirs[j], eda, ks, kc, km, ki,
+            const int a = mine[j], b = theirs[j];
+            if (adopt_mine) keep_mine[j] = a;
+            if (adopt_theirs) keep_theirs[j] = b;
+            const int gene = child_gene(V.P, V.pool, V.parent, cols, j, a, b, eda, ks, kc, km, ki,
                                         kCounterStep * (static_cast<uint64_t>(j) + 1));
             dst[j] = gene;
             const int node = pool_map ? pool_map[gene] : gene;

@@ -12,8 +12,11 @@
 // doubles per evaluation is the ONLY exchange.  Surviving mutated rows of other ranks are
 // recomputed from the replicated parents and the keyed streams (bit-identical by
 // construction), so genomes never cross NVLink.
+#include <unistd.h>
+
 #include <chrono>
 #include <cmath>
+#include <cstring>
 
 #include "internal.cuh"
 #include "variation.cuh"
@@ -37,6 +40,9 @@ int launch_elitism_sharded(const int32_t*, const int32_t*, int, int, const int32
                            double, double, uint32_t, uint64_t, uint64_t, int32_t*, double*, int32_t*, int*, cudaStream_t);
 int launch_elitism(const int32_t*, const int32_t*, int, int, const double*, const double*, int, int32_t*, double*, int32_t*,
                    int*, cudaStream_t);
+int launch_home_children(const int32_t*, int, int, int32_t*, cudaStream_t);
+int launch_home_adopt(const int32_t*, const int32_t*, int, int, int, int32_t*, cudaStream_t);
+int launch_fetch_rows(int32_t*, const int32_t* const*, int32_t*, const int32_t*, int, int, int, cudaStream_t);
 
 // record_generation (modes.cpp:35-43): best = front, mean = SEQUENTIAL sum / s so that
 // non-integer fitness reproduces std::accumulate bit for bit.
@@ -202,8 +208,20 @@ struct gapa_cuda_ga {
     std::vector<cudaEvent_t> gen_marks;  // boundaries not yet folded into wall_of_gen
     std::vector<int> marked_gens;        // the generation (1-based) each of them starts
     cudaEvent_t ev_adv0 = nullptr, ev_adv1 = nullptr;
+    // Row-sharded run over PEER memory (the library's peer-mailbox communicator): slot tables are identical on every
+    // rank, a rank holds only the rows it built or has read.  Surviving children of other ranks are neither rebuilt nor
+    // broadcast: whoever needs one as a parent reads it from its builder's HBM over NVLink inside the variation kernel
+    // and keeps a copy (variation.cuh: parent_row).  Safe without further synchronisation: a slot is overwritten only
+    // when its row has left the parent set, the tables are replicated, and no rank can be more than one exchange ahead.
+    bool peer_rows = false;
+    DevBuf home, bases_dev;
+    std::vector<void*> ipc_opened;
+    bool final_fetch_done = false;
 
     ~gapa_cuda_ga() {
+        for (void* mapped : ipc_opened) cudaIpcCloseMemHandle(mapped);
+        home.release();
+        bases_dev.release();
         for (cudaEvent_t e : gen_marks) cudaEventDestroy(e);
         if (ev_adv0) cudaEventDestroy(ev_adv0);
         if (ev_adv1) cudaEventDestroy(ev_adv1);
@@ -262,7 +280,54 @@ struct gapa_cuda_ga {
         return flush_marks();
     }
     int generation(int gen);
+    int setup_peer_rows();
+    int fetch_all_parents() {  // every parent row local (EDA generations, the returned population)
+        return launch_fetch_rows(pool_rows, bases_dev.as<const int32_t*>(), home.as<int32_t>(), parent, s, k, rank, st);
+    }
 };
+
+namespace {
+struct PoolHandle {  // what the ranks tell each other about their population stores
+    int64_t pid;
+    int32_t device;
+    int32_t pad;
+    uint64_t ptr;
+    cudaIpcMemHandle_t ipc;
+};
+static_assert(sizeof(PoolHandle) <= GAPA_CUDA_COMM_CTRL_BYTES, "pool handle does not fit the control exchange");
+}  // namespace
+
+int gapa_cuda_ga::setup_peer_rows() {
+    gapa_cuda_comm* comm = static_cast<gapa_cuda_comm*>(exchange_user);
+    PoolHandle mine{};
+    mine.pid = static_cast<int64_t>(getpid());
+    mine.device = ctx->device;
+    mine.ptr = reinterpret_cast<uint64_t>(pool_rows);
+    if (cudaIpcGetMemHandle(&mine.ipc, pool_rows) != cudaSuccess) (void)cudaGetLastError();  // same-process peers do not need it
+    std::vector<PoolHandle> all(static_cast<size_t>(world));
+    GAPA_TRY(gapa_cuda_comm_allgather_bytes(comm, &mine, static_cast<int>(sizeof(PoolHandle)), all.data()));
+    std::vector<const int32_t*> bases(static_cast<size_t>(world), nullptr);
+    for (int r = 0; r < world; ++r) {
+        const PoolHandle& h = all[static_cast<size_t>(r)];
+        if (r == rank) {
+            bases[static_cast<size_t>(r)] = pool_rows;
+        } else if (h.pid == mine.pid) {
+            bases[static_cast<size_t>(r)] = reinterpret_cast<const int32_t*>(h.ptr);  // peer access was enabled by comm_connect
+        } else {
+            void* mapped = nullptr;
+            GAPA_CUDA_TRY(cudaIpcOpenMemHandle(&mapped, h.ipc, cudaIpcMemLazyEnablePeerAccess));
+            ipc_opened.push_back(mapped);
+            bases[static_cast<size_t>(r)] = static_cast<const int32_t*>(mapped);
+        }
+    }
+    GAPA_TRY(bases_dev.ensure(sizeof(int32_t*) * static_cast<size_t>(world)));
+    GAPA_CUDA_TRY(cudaMemcpy(bases_dev.ptr, bases.data(), sizeof(int32_t*) * static_cast<size_t>(world), cudaMemcpyHostToDevice));
+    GAPA_TRY(home.ensure(sizeof(int32_t) * 2 * static_cast<size_t>(s)));
+    std::vector<int32_t> self(2 * static_cast<size_t>(s), rank);  // init_population builds every parent row on every rank
+    GAPA_CUDA_TRY(cudaMemcpy(home.ptr, self.data(), sizeof(int32_t) * self.size(), cudaMemcpyHostToDevice));
+    peer_rows = true;
+    return GAPA_CUDA_OK;
+}
 
 int gapa_cuda_ga::generation(int gen) {
     current_gen = gen;
@@ -288,7 +353,15 @@ int gapa_cuda_ga::generation(int gen) {
     vary.child = child;
     vary.partner = partner;
     vary.row_first = lo;
+    if (peer_rows) {
+        GAPA_TRY(launch_home_children(child, s, block, home.as<int32_t>(), st));  // who builds which child this generation
+        if (eda_gen) GAPA_TRY(fetch_all_parents());  // eda_sample reads genes of ALL parents (ga_ops.cpp:214-238)
+        vary.bases = bases_dev.as<const int32_t*>();
+        vary.home = home.as<int32_t>();
+        vary.self = rank;
+    }
     GAPA_TRY(evaluate(child, fit_m, &vary));
+    if (peer_rows && !eda_gen) GAPA_TRY(launch_home_adopt(parent, partner, lo, hi, rank, home.as<int32_t>(), st));
     // elitism permutes the slot tables; survivors built by other ranks are rebuilt in place
     // small populations: elitism, the generation's statistics AND the next generation's selection in one launch
     const bool select_next = gen < iters && !(p.eda_interval > 0 && (gen + 1) % p.eda_interval == 0);
@@ -298,11 +371,20 @@ int gapa_cuda_ga::generation(int gen) {
                                             select_next ? 1 : 0, p.seed, g + 1, B.partner.as<int32_t>(), B.weights.as<double>(),
                                             B.cumulative.as<double>(), st));
     else
-        GAPA_TRY(launch_slots_elitism(pool_rows, parent, child, partner, s, k, lo, hi, fit, fit_m, minimize, p.pc, p.pm, pool,
-                                      p.seed, g, next_parent, next_child, fit_next, B.src_of_rank.as<int32_t>(), status, st));
+        GAPA_TRY(launch_slots_elitism(pool_rows, parent, child, partner, s, k, peer_rows ? 0 : lo, peer_rows ? s : hi, fit, fit_m,
+                                      minimize, p.pc, p.pm, pool, p.seed, g, next_parent, next_child, fit_next,
+                                      B.src_of_rank.as<int32_t>(), status, st));  // peer rows: nothing is rebuilt
     std::swap(parent, next_parent);
     std::swap(child, next_child);
     std::swap(fit, fit_next);
+    if (peer_rows && gen == iters) {
+        // the run ends with every parent row local, and nobody leaves (and frees its pool) before everybody has them:
+        // one more exchange as the barrier (fit_next is scratch by now)
+        GAPA_TRY(fetch_all_parents());
+        const int rc = exchange(exchange_user, fit_next, s, block, st);
+        if (rc != 0) return fail(GAPA_CUDA_E_CUDA, "run: exchange hook failed with status %d", rc);
+        final_fetch_done = true;
+    }
     if (!small) GAPA_LAUNCH(k_ga_stats, 1, 1024, 0, st, fit, s, hist + (gen - 1), hist + iters + (gen - 1));
     // NaN / non-finite fitness is an Error in the reference (ga_ops.cpp:56-57, :189-192);
     // the flag is polled every few generations and at the end to keep the loop asynchronous.
@@ -411,6 +493,15 @@ extern "C" int gapa_cuda_ga_create(gapa_cuda_ctx* ctx, const gapa_cuda_run_param
         ga->exchanges_in_gen.assign(static_cast<size_t>(iters), 0);
         GAPA_CUDA_TRY(cudaEventCreate(&ga->ev_adv0));
         GAPA_CUDA_TRY(cudaEventCreate(&ga->ev_adv1));
+        if (world > 1 && exchange == gapa_cuda_comm_allgather) {
+            int transport = -1;
+            GAPA_TRY(gapa_cuda_comm_info(static_cast<gapa_cuda_comm*>(exchange_user), &transport, nullptr, nullptr));
+            const char* knob = std::getenv("GAPA_PEER_ROWS");  // 0: rebuild foreign survivors instead (the NCCL transport's way)
+            if (transport == GAPA_COMM_PEER && !(knob && knob[0] == '0')) {
+                GAPA_CUDA_TRY(cudaStreamSynchronize(ga->st));
+                GAPA_TRY(ga->setup_peer_rows());
+            }
+        }
         return GAPA_CUDA_OK;
     };
     const int rc = body();
@@ -471,6 +562,7 @@ extern "C" int gapa_cuda_ga_result(gapa_cuda_ga* ga, gapa_cuda_run_result* resul
     if (result->history_best) GAPA_CUDA_TRY(cudaMemcpy(result->history_best, ga->hist, sizeof(double) * iters, cudaMemcpyDeviceToHost));
     if (result->history_mean) GAPA_CUDA_TRY(cudaMemcpy(result->history_mean, ga->hist + iters, sizeof(double) * iters, cudaMemcpyDeviceToHost));
     if (result->final_population) {  // RunResult::final_population: the parents in best-first order
+        if (ga->peer_rows && !ga->final_fetch_done) GAPA_TRY(ga->fetch_all_parents());  // mid-run: the peers are still there
         DevBuf dense;
         GAPA_TRY(dense.ensure(sizeof(int32_t) * std::max<size_t>(ga->cells, 1)));
         int rc = launch_slots_gather(ga->pool_rows, ga->parent, s, ga->k, dense.as<int32_t>(), st);

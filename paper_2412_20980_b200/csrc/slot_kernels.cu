@@ -20,17 +20,21 @@ namespace gapa_b200 {
 static constexpr int kSlotThreads = 256;
 // Builds child row `row` into its slot.  Shared by the variation kernel (own rows) and the rebuild
 // kernel (foreign survivors).
-__device__ __forceinline__ void build_child_row(const VariationParams& P, int32_t* __restrict__ pool,
-                                                const int32_t* __restrict__ parent, const int32_t* __restrict__ child,
-                                                const int32_t* __restrict__ partner, int k, int row, uint64_t* keys) {
+__device__ __forceinline__ void build_child_row(const VariationSpec& V, int k, int row, uint64_t* keys) {
+    const VariationParams& P = V.P;
     if (threadIdx.x < 4)
         keys[threadIdx.x] = stream_key(P.seed, P.generation, GAPA_ROLE_SELECT + threadIdx.x, static_cast<uint64_t>(row)) + kGolden;
     __syncthreads();
     const uint64_t ks = keys[0], kc = keys[1], km = keys[2], ki = keys[3];
-    const bool eda = partner == nullptr;
-    const int32_t* mine = pool + static_cast<size_t>(parent[row]) * k;
-    const int32_t* theirs = eda ? mine : pool + static_cast<size_t>(parent[partner[row]]) * k;
-    int32_t* dst = pool + static_cast<size_t>(child[row]) * k;
+    const bool eda = V.partner == nullptr;
+    const int slot_mine = V.parent[row], slot_theirs = eda ? slot_mine : V.parent[V.partner[row]];
+    bool adopt_mine, adopt_theirs;  // rows that live in another rank's HBM are written through to the local slot
+    const int32_t* mine = parent_row(V, slot_mine, k, &adopt_mine);
+    const int32_t* theirs = eda ? mine : parent_row(V, slot_theirs, k, &adopt_theirs);
+    if (eda || slot_theirs == slot_mine) adopt_theirs = false;
+    int32_t* keep_mine = V.pool + static_cast<size_t>(slot_mine) * k;
+    int32_t* keep_theirs = V.pool + static_cast<size_t>(slot_theirs) * k;
+    int32_t* dst = V.pool + static_cast<size_t>(V.child[row]) * k;
     if ((k & 3) == 0) {  // slots are 16-byte aligned when k is a multiple of 4
         const int4* mine4 = reinterpret_cast<const int4*>(mine);
         const int4* theirs4 = reinterpret_cast<const int4*>(theirs);
@@ -38,30 +42,68 @@ __device__ __forceinline__ void build_child_row(const VariationParams& P, int32_
         for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < (k >> 2); q += gridDim.x * blockDim.x) {
             const int4 a = mine4[q];
             const int4 b = eda ? a : theirs4[q];
+            if (adopt_mine) reinterpret_cast<int4*>(keep_mine)[q] = a;
+            if (adopt_theirs) reinterpret_cast<int4*>(keep_theirs)[q] = b;
             const int av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
             int r[4];
             uint64_t prod = kCounterStep * (static_cast<uint64_t>(q) * 4 + 1);
 #pragma unroll
             for (int t = 0; t < 4; ++t) {
-                r[t] = child_gene(P, pool, parent, k, 4 * q + t, av[t], bv[t], eda, ks, kc, km, ki, prod);
+                r[t] = child_gene(P, V.pool, V.parent, k, 4 * q + t, av[t], bv[t], eda, ks, kc, km, ki, prod);
                 prod += kCounterStep;
             }
             dst4[q] = make_int4(r[0], r[1], r[2], r[3]);
         }
     } else {
-        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x)
-            dst[j] = child_gene(P, pool, parent, k, j, mine[j], theirs[j], eda, ks, kc, km, ki,
-                                kCounterStep * (static_cast<uint64_t>(j) + 1));
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) {
+            const int a = mine[j], b = theirs[j];
+            if (adopt_mine) keep_mine[j] = a;
+            if (adopt_theirs) keep_theirs[j] = b;
+            dst[j] = child_gene(P, V.pool, V.parent, k, j, a, b, eda, ks, kc, km, ki, kCounterStep * (static_cast<uint64_t>(j) + 1));
+        }
     }
 }
 
-// children of rows [row_first, row_first + gridDim.y)
-__global__ void __launch_bounds__(kSlotThreads) k_ga_slots_variation(VariationParams P, int32_t* __restrict__ pool,
-                                                                     const int32_t* __restrict__ parent,
-                                                                     const int32_t* __restrict__ child,
-                                                                     const int32_t* __restrict__ partner, int k, int row_first) {
+// children of rows [V.row_first, V.row_first + gridDim.y)
+__global__ void __launch_bounds__(kSlotThreads) k_ga_slots_variation(VariationSpec V, int k) {
     __shared__ uint64_t keys[4];
-    build_child_row(P, pool, parent, child, partner, k, row_first + blockIdx.y, keys);
+    build_child_row(V, k, V.row_first + blockIdx.y, keys);
+}
+
+// ---- row-sharded runs over peer memory (run.cu) ------------------------------------------------------------------
+// home[child[j]] = the rank that builds child row j this generation (partition_rows, modes.cpp:506-516)
+__global__ void __launch_bounds__(kSlotThreads) k_ga_home_children(const int32_t* __restrict__ child, int s, int block, int32_t* home) {
+    const int j = blockIdx.x * blockDim.x + threadIdx.x;
+    if (j < s) home[child[j]] = j / block;
+}
+// after a variation launch: the parent rows it read remotely now have a local copy
+__global__ void __launch_bounds__(kSlotThreads) k_ga_home_adopt(const int32_t* __restrict__ parent, const int32_t* __restrict__ partner,
+                                                                int lo, int hi, int self, int32_t* home) {
+    const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= hi) return;
+    home[parent[i]] = self;
+    if (partner) home[parent[partner[i]]] = self;
+}
+// every parent row that is not local yet is copied from its builder's pool (EDA generations sample ALL parents; the
+// final population is returned whole)
+__global__ void __launch_bounds__(kSlotThreads) k_ga_fetch_rows(int32_t* __restrict__ pool, const int32_t* const* __restrict__ bases,
+                                                                const int32_t* __restrict__ home, const int32_t* __restrict__ parent,
+                                                                int k, int self) {
+    const int slot = parent[blockIdx.y];
+    const int h = home[slot];
+    if (h == self) return;
+    const int32_t* from = bases[h] + static_cast<size_t>(slot) * k;
+    int32_t* to = pool + static_cast<size_t>(slot) * k;
+    if ((k & 3) == 0) {
+        for (int q = blockIdx.x * blockDim.x + threadIdx.x; q < (k >> 2); q += gridDim.x * blockDim.x)
+            reinterpret_cast<int4*>(to)[q] = reinterpret_cast<const int4*>(from)[q];
+    } else {
+        for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) to[j] = from[j];
+    }
+}
+__global__ void __launch_bounds__(kSlotThreads) k_ga_home_all_local(const int32_t* __restrict__ parent, int s, int self, int32_t* home) {
+    const int i = blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < s) home[parent[i]] = self;
 }
 
 // Stable best-first position of every stacked row (parents 0..s-1, children s..2s-1):
@@ -147,7 +189,14 @@ __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_rebuild(VariationPara
     const int x = order[blockIdx.y];  // blockIdx.y = rank < s: a survivor
     const int row = x - s;
     if (x < s || (row >= block_lo && row < block_hi)) return;
-    build_child_row(P, pool, parent, child, partner, k, row, keys);
+    VariationSpec V;
+    V.P = P;
+    V.pool = pool;
+    V.parent = parent;
+    V.child = child;
+    V.partner = partner;
+    V.row_first = 0;
+    build_child_row(V, k, row, keys);
 }
 
 // next parent table = slots of the s best, next child table = slots of the s others (now free)
@@ -318,14 +367,35 @@ int launch_slots_variation(int32_t* pool, const int32_t* parent, const int32_t* 
                            int row_first, int row_count, double pc, double pm, uint32_t pool_size, uint64_t seed,
                            uint64_t generation, cudaStream_t st) {
     if (row_count == 0 || k == 0) return GAPA_CUDA_OK;
-    GAPA_LAUNCH(k_ga_slots_variation, slot_grid((k & 3) ? k : k / 4, row_count), kSlotThreads, 0, st,
-                make_variation_params(pc, pm, pool_size, s, seed, generation), pool, parent, child, partner, k, row_first);
+    VariationSpec V;
+    V.P = make_variation_params(pc, pm, pool_size, s, seed, generation);
+    V.pool = pool;
+    V.parent = parent;
+    V.child = child;
+    V.partner = partner;
+    V.row_first = row_first;
+    GAPA_LAUNCH(k_ga_slots_variation, slot_grid((k & 3) ? k : k / 4, row_count), kSlotThreads, 0, st, V, k);
     return GAPA_CUDA_OK;
 }
 int launch_variation_spec(const VariationSpec& spec, int k, int rows, cudaStream_t st) {
     if (rows == 0 || k == 0) return GAPA_CUDA_OK;
-    GAPA_LAUNCH(k_ga_slots_variation, slot_grid((k & 3) ? k : k / 4, rows), kSlotThreads, 0, st, spec.P, spec.pool, spec.parent,
-                spec.child, spec.partner, k, spec.row_first);
+    GAPA_LAUNCH(k_ga_slots_variation, slot_grid((k & 3) ? k : k / 4, rows), kSlotThreads, 0, st, spec, k);
+    return GAPA_CUDA_OK;
+}
+// launchers of the peer-memory bookkeeping (run.cu)
+int launch_home_children(const int32_t* child, int s, int block, int32_t* home, cudaStream_t st) {
+    GAPA_LAUNCH(k_ga_home_children, (s + kSlotThreads - 1) / kSlotThreads, kSlotThreads, 0, st, child, s, block, home);
+    return GAPA_CUDA_OK;
+}
+int launch_home_adopt(const int32_t* parent, const int32_t* partner, int lo, int hi, int self, int32_t* home, cudaStream_t st) {
+    if (hi <= lo) return GAPA_CUDA_OK;
+    GAPA_LAUNCH(k_ga_home_adopt, (hi - lo + kSlotThreads - 1) / kSlotThreads, kSlotThreads, 0, st, parent, partner, lo, hi, self, home);
+    return GAPA_CUDA_OK;
+}
+int launch_fetch_rows(int32_t* pool, const int32_t* const* bases, int32_t* home, const int32_t* parent, int s, int k, int self,
+                      cudaStream_t st) {
+    if (k > 0) GAPA_LAUNCH(k_ga_fetch_rows, slot_grid((k & 3) ? k : k / 4, s), kSlotThreads, 0, st, pool, bases, home, parent, k, self);
+    GAPA_LAUNCH(k_ga_home_all_local, (s + kSlotThreads - 1) / kSlotThreads, kSlotThreads, 0, st, parent, s, self, home);
     return GAPA_CUDA_OK;
 }
 int launch_slots_elitism(int32_t* pool, const int32_t* parent, const int32_t* child, const int32_t* partner, int s, int k,

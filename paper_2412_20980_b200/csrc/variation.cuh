@@ -70,6 +70,27 @@ struct VariationSpec {
     const int32_t* child;
     const int32_t* partner;  // nullptr = EDA generation
     int row_first;
+    // Row-sharded runs over peer memory (run.cu): slot tables are identical on every rank, but a rank holds only the rows
+    // it built or has read before.  home[slot] = the rank whose pool holds the row (its builder, or this rank once the
+    // row has been adopted); bases[r] = rank r's pool as mapped here (NVLink peer access / CUDA IPC).  A parent row
+    // that lives elsewhere is read straight from its builder's HBM and written through to the local slot on the way.
+    // bases == nullptr: everything is local.
+    const int32_t* const* bases = nullptr;
+    const int32_t* home = nullptr;
+    int self = 0;
 };
+
+// where parent row `slot` is read from; *remote tells the caller to write it through to the local slot
+__device__ __forceinline__ const int32_t* parent_row(const VariationSpec& V, int slot, int k, bool* remote) {
+    *remote = false;
+    if (V.bases) {
+        const int h = V.home[slot];
+        if (h != V.self) {
+            *remote = true;
+            return V.bases[h] + static_cast<size_t>(slot) * k;
+        }
+    }
+    return V.pool + static_cast<size_t>(slot) * k;
+}
 
 }  // namespace gapa_b200

@@ -44,16 +44,18 @@ def test_full_size_every_row_of_the_bench_population(gp, oracle, c4):
 
 def test_full_size_trajectory_matches_the_oracle(gp, oracle, c4):
     """Three generations of the C4 GA (population 256) against oracle.run_ga: history best AND mean, final population
-    and fitness bit for bit (test_parallel.cpp:86-104 at n = 1e6); the library loop and the stepwise sharded driver
-    (two ranks in one process, stand-in all-gather) must both reproduce it."""
+    and fitness bit for bit (test_parallel.cpp:86-104 at n = 1e6) — the one-GPU library loop, and both ranks of a
+    two-rank gapa_cuda_run_multi (peer-mailbox exchange, foreign parents read from the builder's pool)."""
     g, pool, _ = c4
     og = oracle.graph_from_edges(g.n, g.edges())
     obj = gp.PairwiseConnectivityObjective(g, pool)
     params = gp.GAParams(pc=0.6, pm=0.2, pop_size=256, budget=K, iterations=3, seed=5)
     want = oracle.run_ga(og, 0, 0.6, 0.2, 256, K, 3, 5, threads=16)
     res = gp.run_ga(params, pool, obj)
-    assert np.array_equal(res.history_best, want["best"]) and np.array_equal(res.history_mean, want["mean"])
-    assert np.array_equal(res.final_population, want["population"]) and np.array_equal(res.final_fitness, want["fitness"])
+    sharded = gp.run_ga_multi(params, [obj, gp.PairwiseConnectivityObjective(g, pool)], transport="peer")
+    for r in [res] + sharded:
+        assert np.array_equal(r.history_best, want["best"]) and np.array_equal(r.history_mean, want["mean"])
+        assert np.array_equal(r.final_population, want["population"]) and np.array_equal(r.final_fitness, want["fitness"])
 
 
 def test_full_size_properties(gp, c4):

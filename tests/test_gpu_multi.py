@@ -16,10 +16,13 @@ def _same(a, b):
     assert np.array_equal(a.final_population, b.final_population) and np.array_equal(a.final_fitness, b.final_fitness)
 
 
+@pytest.mark.parametrize("peer_rows", ["1", "0"], ids=["peer-rows", "rebuild"])
 @pytest.mark.parametrize("world,eda", [(2, 0), (3, 4), (4, 0)])
-def test_run_multi_threads_equal_the_single_run(gp, oracle, cuda_device, world, eda):
+def test_run_multi_threads_equal_the_single_run(gp, oracle, cuda_device, world, eda, peer_rows, monkeypatch):
     """gapa_cuda_run_multi: `world` contexts on device 0, one host thread each, peer-mailbox exchange (raw pointers inside
-    one process).  Ragged blocks (37 rows over 2 / 3 / 4 ranks), EDA generations included."""
+    one process).  Ragged blocks (37 rows over 2 / 3 / 4 ranks), EDA generations included.  Surviving children of other
+    ranks are read from their builder's pool on demand (default), or rebuilt locally (GAPA_PEER_ROWS=0)."""
+    monkeypatch.setenv("GAPA_PEER_ROWS", peer_rows)
     g = gp.barabasi_albert(600, 2, 4)
     pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
     s, k, iters = 37, 15, 12
