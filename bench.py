@@ -193,7 +193,7 @@ def workload_shape(w: dict) -> dict:
 def config_of(w: dict, s: int, k: int, n: int, m: int, world: int, rows_per_rank: int) -> dict:
     """the `config` object — identical keys and values in both arms"""
     return {"workload": w["name"], "population": s, "budget": k, "n": n, "m": m,
-            "step": "one generation: select -> crossover+mutate -> evaluate(M_POP) -> elitism, population in HBM",
+            "step": "one generation of the in-library loop: select -> crossover+mutate -> evaluate(M_POP) -> elitism, population in HBM",
             "parallelism": f"population rows sharded over {world} GPU(s), graph replicated, 1 fitness all-gather/generation",
             "l2": "inputs larger than L2 (gene matrix %.0f MB + alive/reached words %.0f MB per step vs 126 MB L2)"
                   % (4.0 * s * k / 1e6, 16.0 * n * ((rows_per_rank + 63) // 64) / 1e6)}
@@ -237,7 +237,7 @@ def run_gpu_arm(args, w):
     import torch
     import torch.distributed as dist
     import paper_2412_20980_b200 as gp
-    from paper_2412_20980_b200.driver import CudaOps, Shard, ShardedGa, torch_allgather
+    from paper_2412_20980_b200.driver import Comm, Shard, torch_bytes_allgather
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
@@ -246,10 +246,17 @@ def run_gpu_arm(args, w):
         raise SystemExit("bench.py: no CUDA device — the hot path has no CPU fallback")
     if world != max(args.gpus, 1):
         raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
-    if torch.cuda.device_count() < world:
+    # development aid: all ranks on GPU 0 (separate processes, time-sliced; rendezvous over gloo because NCCL refuses two
+    # ranks on one device) — exercises the N > 1 code path of this script on a one-GPU box; never a benchmark
+    shared_gpu = world > 1 and os.environ.get("GAPA_BENCH_SHARED_GPU") == "1"
+    if shared_gpu:
+        local = 0
+    elif torch.cuda.device_count() < world:
         raise SystemExit(f"bench.py: --gpus {world} but only {torch.cuda.device_count()} CUDA device(s) are visible")
     torch.cuda.set_device(local)
-    if world > 1:
+    if world > 1 and shared_gpu:
+        dist.init_process_group("gloo")
+    elif world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
         if rank == 0:
             print(f"[bench] NCCL communicator: nranks={dist.get_world_size()} backend={dist.get_backend()}", file=sys.stderr, flush=True)
@@ -276,7 +283,6 @@ def run_gpu_arm(args, w):
     s = args.pop or w["pop"]
     params = gp.GAParams(pc=w["pc"], pm=w["pm"], pop_size=s, budget=k, iterations=args.warmup + args.steps + 1, seed=1)
     shard = Shard(rank, world, s)
-    ga = ShardedGa(params, CudaOps(obj, local), shard, torch_allgather())
     lib = gp.capi.load()
 
     def barrier():
@@ -285,42 +291,62 @@ def run_gpu_arm(args, w):
             dist.barrier()
             torch.cuda.synchronize()
 
-    ga.initialize()
-    for _ in range(args.warmup):
-        ga.step()
+    # The generation loop runs inside the library (gapa_cuda_ga_*: what a C++ host's run_ga_cuda executes), one rank per
+    # GPU.  The once-per-generation exchange is the library's own: peer mailboxes over NVLink where every GPU can reach
+    # every other (surviving children of other ranks are then read from their builder's HBM on demand), else NCCL.
+    comm, transport = None, None
+    if world > 1:
+        transport = args.exchange
+        if transport == "auto" and shared_gpu:
+            transport = "peer"
+        if transport == "auto":
+            reach = all(torch.cuda.can_device_access_peer(local, d) for d in range(world) if d != local)
+            flags = [None] * world
+            dist.all_gather_object(flags, bool(reach))
+            transport = "peer" if all(flags) else "nccl"
+        if transport == "peer":
+            comm = Comm.peer(obj, rank, world, s, torch_bytes_allgather())
+        else:
+            def broadcast_bytes(data):
+                box = [data]
+                dist.broadcast_object_list(box, src=0)
+                return box[0]
+            comm = Comm.nccl(obj, rank, world, broadcast_bytes)
+        if rank == 0:
+            print(f"[bench] exchange transport: {transport} (world {world})", file=sys.stderr, flush=True)
+    loop = gp.GaLoop(params, obj, rank=rank, world=world, comm=comm)
+    loop.advance(args.warmup)  # generation 1 carries the initialisation and the first evaluation of the parents
     barrier()
     sampler = ClockSampler(local)
     if rank == 0:
         sampler.start()
+    calls0, eval_s0, _ = loop.counters()
     launches0 = lib.gapa_cuda_launch_count()
-    eval_ms = []
-    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    ev0.record()
-    for _ in range(args.steps):
-        ga.step()
-        eval_ms.append(obj.dgraph.last_eval_ms())
-    ev1.record()
+    step_ms_total = loop.advance(args.steps)  # device time of exactly K generations: CUDA events on the run's stream
     barrier()
-    step_ms_total = ev0.elapsed_time(ev1)
     launches = lib.gapa_cuda_launch_count() - launches0
     clocks = sampler.stop() if rank == 0 else None
+    calls1, eval_s1, _ = loop.counters()
+    eval_ms = [1e3 * (eval_s1 - eval_s0) / max(calls1 - calls0, 1)]  # variation + evaluation of the timed generations
+    mine = loop.result()
 
-    # pure fitness evaluation (no variation fused in), device-resident: this rank's block of the
-    # current parents through the slot table — what the roofline figures are computed from
+    # pure fitness evaluation (no variation fused in), device-resident: this rank's block of the current parents
+    # — what the roofline figures are computed from
     lo, hi = shard.rows
+    block_dev = torch.from_numpy(mine.final_population[lo:hi]).cuda()
+    fit_dev = torch.empty(max(hi - lo, 1), dtype=torch.float64, device="cuda")
     pure_ms = []
-    scratch_fit = ga.ops.zeros_f64(shard.padded)
     for i in range(3 + args.steps):
-        ga.ops.eval_rows(ga.pool, ga.parent, lo, hi, scratch_fit)
+        obj.dgraph.eval_batch_device(obj.task, block_dev.data_ptr(), hi - lo, k, fit_dev.data_ptr(), 0)
         if i >= 3:
             pure_ms.append(obj.dgraph.last_eval_ms())
     torch.cuda.synchronize()
-    assert torch.equal(scratch_fit[lo:hi], ga.fit[lo:hi]), "re-evaluating the parents changed their fitness"
+    assert np.array_equal(fit_dev[:hi - lo].cpu().numpy(), mine.final_fitness[lo:hi]), "re-evaluating the parents changed their fitness"
 
     # e2e: the plugin boundary with HOST buffers — evaluate_batch(host genes) -> host fitness,
     # this rank's block of the current M_POP, pinned memory, copies inside the timed region.
     host_genes = torch.empty((hi - lo, k), dtype=torch.int32, pin_memory=True)
-    host_genes.copy_(ga.population()[lo:hi])  # this rank's block of the current parents; their fitness is ga.fit
+    host_genes.copy_(torch.from_numpy(mine.final_population[lo:hi]))  # this rank's block of the current parents
     host_out = torch.empty(max(hi - lo, 1), dtype=torch.float64, pin_memory=True)
     torch.cuda.synchronize()
 
@@ -336,7 +362,7 @@ def run_gpu_arm(args, w):
         e2e_once()
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    assert np.array_equal(host_out[:hi - lo].numpy(), ga.fit[lo:hi].cpu().numpy()), "e2e result differs from the device path"
+    assert np.array_equal(host_out[:hi - lo].numpy(), mine.final_fitness[lo:hi]), "e2e result differs from the device path"
 
     # the same call with a PAGEABLE gene matrix — what the C++ adapter's evaluate_batch(const PopulationMatrix&) passes
     # (a std::vector): the library stages it through its own pinned ring
@@ -354,30 +380,27 @@ def run_gpu_arm(args, w):
     for _ in range(args.steps):
         e2e_pageable_once()
     e2e_pageable_s = time.perf_counter() - t0
-    assert np.array_equal(pageable_out[:hi - lo], ga.fit[lo:hi].cpu().numpy()), "pageable e2e result differs from the device path"
+    assert np.array_equal(pageable_out[:hi - lo], mine.final_fitness[lo:hi]), "pageable e2e result differs from the device path"
 
     # N > 1: the sharded run must BE the 1-GPU run (test_parallel.cpp:86-104): rank 0 repeats the same generations
     # unsharded with the same seed and compares history and final population bit for bit.
     verify = None
     if world > 1:
-        mine = ga.result()
         if rank == 0:
-            solo = ShardedGa(params, CudaOps(obj, local), Shard(0, 1, s), torch_allgather())
-            solo.initialize()
-            for _ in range(ga.generation):
-                solo.step()
+            solo = gp.GaLoop(params, obj)
+            solo.advance(loop.generation)
             ref = solo.result()
-            g = ga.generation
-            verify = {"generations": g,
+            solo.close()
+            g = loop.generation
+            verify = {"generations": g, "transport": transport,
                       "history_best_equal": bool(np.array_equal(mine.history_best[:g], ref.history_best[:g])),
                       "history_mean_equal": bool(np.array_equal(mine.history_mean[:g], ref.history_mean[:g])),
                       "final_population_equal": bool(np.array_equal(mine.final_population, ref.final_population)),
                       "final_fitness_equal": bool(np.array_equal(mine.final_fitness, ref.final_fitness))}
-            del solo
         barrier()
 
     times = torch.tensor([step_ms_total, e2e_s * 1e3, float(np.mean(pure_ms)), float(np.mean(eval_ms)), e2e_pageable_s * 1e3],
-                         dtype=torch.float64, device="cuda")
+                         dtype=torch.float64, device="cpu" if shared_gpu else "cuda")
     if world > 1:
         dist.all_reduce(times, op=dist.ReduceOp.MAX)
     step_ms_total, e2e_ms_total, eval_ms_mean, fused_ms_mean, e2e_pageable_ms_total = (float(x) for x in times.cpu())
@@ -433,7 +456,7 @@ def run_gpu_arm(args, w):
                                      "PopulationMatrix&) passes): staged through the library's pinned ring by host threads"},
             "gpu_launches": int(launches),
             "clocks": clocks,
-            "comm": {"backend": "nccl" if world > 1 else None, "nranks": world},
+            "comm": {"transport": transport, "bootstrap": "torch.distributed nccl" if world > 1 else None, "nranks": world},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                          "kernel": "fitness evaluation pipeline (k_pc_sweep dominant)" if task in ("pc", "mcn") else f"{task} fitness pipeline",
@@ -449,17 +472,31 @@ def run_gpu_arm(args, w):
         }
         if verify is not None:
             line["verify"] = verify
+        if task == "cda":
+            # the merge phase is on-chip / L2 traffic and serial merge depth, not HBM — report merges/s.
+            # Merges of one detection = n - communities of its partition; estimated from 8 individuals' partitions.
+            from paper_2412_20980_b200.experiment import _detect
+            sample = mine.final_population[np.linspace(0, s - 1, 8).astype(int)]
+            merges = float(np.mean([n - len(np.unique(_detect(obj.dgraph, row))) for row in sample]))
+            line["merges_per_individual"] = merges
+            line["merges_per_sec"] = merges * rows_per_rank * world / (eval_ms_mean * 1e-3)
+            line["roofline"]["note"] += ("; CDA is bound by the serial depth of the greedy merge sequence (one block-wide step per "
+                                         "merge), not by HBM: see merges_per_sec")
         if world == 1:
             # the same generations through the in-library loop (gapa_cuda_run: no host round trip per
             # operator) — what a C++ host gets from run_ga_cuda(); reported beside the stepwise driver
             iters = max(args.steps, 5) if ms_per_step > 1.0 else 200  # short generations: amortise init + the final read-back
-            loop = gp.run_ga(gp.GAParams(pc=w["pc"], pm=w["pm"], pop_size=s, budget=k, iterations=iters, seed=1), pool, obj)
-            line["library_loop"] = {"generations_per_sec": iters / loop.total_wall_seconds, "iterations": iters,
-                                    "evals_per_sec": s * (iters + 1) / loop.total_wall_seconds,
-                                    "eval_ms_per_generation": 1e3 * loop.eval_seconds / (iters + 1)}
+            run = gp.run_ga(gp.GAParams(pc=w["pc"], pm=w["pm"], pop_size=s, budget=k, iterations=iters, seed=1), pool, obj)
+            line["library_loop"] = {"generations_per_sec": iters / run.total_wall_seconds, "iterations": iters,
+                                    "evals_per_sec": s * (iters + 1) / run.total_wall_seconds,
+                                    "eval_ms_per_generation": 1e3 * run.eval_seconds / (iters + 1)}
         if world == 1 and not args.no_cpu_baseline:
             line["cpu_baseline"] = cpu_reference_throughput(w, 12.0, host_threads())
         print(json.dumps(line), flush=True)
+    loop.close()
+    if comm is not None:
+        barrier()
+        comm.close()
     if world > 1:
         dist.destroy_process_group()
 
@@ -473,6 +510,8 @@ def main():
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--pop", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--exchange", default="auto", choices=["auto", "peer", "nccl"],
+                    help="N > 1: the library's exchange transport (auto = peer mailboxes where every GPU reaches every other)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     w = WORKLOADS[args.workload]

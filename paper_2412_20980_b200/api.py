@@ -585,6 +585,12 @@ class GaLoop:
         check(capi.load().gapa_cuda_ga_result(self.handle, C.byref(buf.c)))
         return buf.result()
 
+    def counters(self) -> tuple:
+        """(fitness_batch_calls, eval_seconds, total_wall_seconds) so far, without copying any population"""
+        buf = _ResultBuffers(self.params, outputs=False)
+        check(capi.load().gapa_cuda_ga_result(self.handle, C.byref(buf.c)))
+        return int(buf.c.fitness_batch_calls), float(buf.c.eval_seconds), float(buf.c.total_wall_seconds)
+
     def close(self):
         if self.handle:
             capi.load().gapa_cuda_ga_destroy(self.handle)

@@ -39,7 +39,10 @@
 
 namespace gapa_b200 {
 
-static constexpr int kCdaThreads = 1024;
+#ifndef GAPA_CDA_THREADS
+#define GAPA_CDA_THREADS 1024
+#endif
+static constexpr int kCdaThreads = GAPA_CDA_THREADS;
 static constexpr int kCdaWarps = kCdaThreads / 32;
 #ifndef GAPA_CDA_GROUP
 #define GAPA_CDA_GROUP 8
@@ -437,7 +440,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                 if (lane == 0) warp_cand[warp] = mine;
                 __syncthreads();
                 if (warp == 0) {
-                    Cand x = warp_cand[lane];
+                    Cand x = lane < kCdaWarps ? warp_cand[lane] : Cand{0.0, -1, -1};
                     x = cand_warp_best(x);
                     if (lane == 0) chosen = x;
                 }
@@ -565,7 +568,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             __syncthreads();
             CDA_TICK(6);  // list work (long lists)
             if (warp == 0) {
-                Cand x = warp_cand[lane];
+                Cand x = lane < kCdaWarps ? warp_cand[lane] : Cand{0.0, a, -1};
                 x = cand_warp_best(x);
                 if (lane == 0) { best_gain[a] = x.gain; best_id[a] = x.b; if (hier) dirty[a >> 5] = 1; }
             }

@@ -45,7 +45,11 @@ static int upload_i32(const std::vector<int32_t>& h, int32_t** d) {
 // the H2D.  With kSlots slices in flight the host copy of slice i+1 overlaps the DMA of slice i.
 PinnedRing::PinnedRing() {
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    const int count = static_cast<int>(std::min(8u, std::max(1u, hw / 2)));
+    // measured on the B200 box (16 host cores, tools/probe_pageable.py, 819 MB batch): 1 / 2 / 4 / 8 / 16 copy threads move
+    // 10.2 / 14.5 / 20.2 / 19.1 / 16.8 GB/s — the host's copy bandwidth saturates at four (plain cudaMemcpyAsync from
+    // pageable memory: 10.8 GB/s; the same batch from pinned memory: 54 GB/s, the PCIe rate)
+    int count = static_cast<int>(std::min(4u, std::max(1u, hw / 2)));
+    if (const char* raw = std::getenv("GAPA_PINNED_RING_THREADS")) count = std::max(1, std::min(64, std::atoi(raw)));
     for (int t = 0; t < count; ++t) workers.emplace_back([this, t, count] { work(t, count); });
 }
 PinnedRing::~PinnedRing() {
@@ -545,6 +549,7 @@ int gapa_cuda_eval_batch(gapa_cuda_ctx* c, int task, const int32_t* genes_host, 
         cudaPointerAttributes attr{};
         if (cudaPointerGetAttributes(&attr, genes_host) != cudaSuccess) (void)cudaGetLastError();
         pageable = attr.type == cudaMemoryTypeUnregistered;
+        if (const char* raw = std::getenv("GAPA_PINNED_RING")) pageable = pageable && raw[0] != '0';
     }
     float total_ms = 0.f;
     while (static_cast<int>(c->chunk_events.size()) < 2 * chunks) {

@@ -298,6 +298,18 @@ static_assert(sizeof(PoolHandle) <= GAPA_CUDA_COMM_CTRL_BYTES, "pool handle does
 }  // namespace
 
 int gapa_cuda_ga::setup_peer_rows() {
+    if (exchange != gapa_cuda_comm_allgather) {
+        // GAPA_PEER_ROWS_LOOPBACK (tools/probe_scaling.py): every "peer" pool is this rank's own — the bookkeeping and the
+        // write-through copies of a sharded generation are timed on one GPU; the rows read are not the real ones
+        std::vector<const int32_t*> loop(static_cast<size_t>(world), pool_rows);
+        GAPA_TRY(bases_dev.ensure(sizeof(int32_t*) * static_cast<size_t>(world)));
+        GAPA_CUDA_TRY(cudaMemcpy(bases_dev.ptr, loop.data(), sizeof(int32_t*) * static_cast<size_t>(world), cudaMemcpyHostToDevice));
+        GAPA_TRY(home.ensure(sizeof(int32_t) * 2 * static_cast<size_t>(s)));
+        std::vector<int32_t> own(2 * static_cast<size_t>(s), rank);
+        GAPA_CUDA_TRY(cudaMemcpy(home.ptr, own.data(), sizeof(int32_t) * own.size(), cudaMemcpyHostToDevice));
+        peer_rows = true;
+        return GAPA_CUDA_OK;
+    }
     gapa_cuda_comm* comm = static_cast<gapa_cuda_comm*>(exchange_user);
     PoolHandle mine{};
     mine.pid = static_cast<int64_t>(getpid());
@@ -501,6 +513,8 @@ extern "C" int gapa_cuda_ga_create(gapa_cuda_ctx* ctx, const gapa_cuda_run_param
                 GAPA_CUDA_TRY(cudaStreamSynchronize(ga->st));
                 GAPA_TRY(ga->setup_peer_rows());
             }
+        } else if (world > 1 && std::getenv("GAPA_PEER_ROWS_LOOPBACK")) {
+            GAPA_TRY(ga->setup_peer_rows());
         }
         return GAPA_CUDA_OK;
     };

@@ -1,47 +1,55 @@
-"""Per-rank critical path of the sharded generation at world = N, measured on ONE GPU.
+"""Per-rank critical path of the sharded generation at world = N, measured on ONE GPU (a projection aid, not a scaling
+result: the box has one GPU).
 
-Runs driver.ShardedGa as rank 0 of N with a stand-in for the all-gather that fills the other ranks'
-fitness blocks with a cyclic copy of this rank's block (so the elitism mix of surviving rows is
-realistic).  What it measures is everything a rank does per generation except the NCCL all-gather
-itself (s doubles; latency-bound, ~20-50 us on NVSwitch).  It is a projection aid, not a scaling result."""
-import json, sys
-sys.path.insert(0, ".")
-import torch
-import paper_2412_20980_b200 as gp
-from paper_2412_20980_b200.driver import CudaOps, Shard, ShardedGa
+Runs the in-library loop (gapa_cuda_ga_*) as rank 0 of N with a stand-in exchange that fills the other ranks' fitness
+blocks with a copy of this rank's block, so the elitism mix of surviving rows is realistic.  Two ways of getting the
+surviving children of other ranks:
+  rebuild   every rank recomputes them from the replicated parents (NCCL transport; round 1's only way)
+  peer      they are read from their builder's pool on demand and kept (peer-mailbox transport) — timed here with
+            GAPA_PEER_ROWS_LOOPBACK: the "remote" pool is this GPU's own, so the bookkeeping and the write-through copies
+            are in the number, the NVLink latency of the remote reads is not.
+The exchange itself (one 4 KB-per-rank all-gather per generation: a few microseconds of NVLink stores and a flag per
+peer) is not in either number."""
+import ctypes as C
+import json
+import os
+import sys
 
-n, attach, s, rate = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1_000_000, 5, 4096, 0.05
-g = gp.barabasi_albert(n, attach, 1)
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import torch  # noqa: E402,F401
+
+import paper_2412_20980_b200 as gp  # noqa: E402
+
+n = int(float(sys.argv[1])) if len(sys.argv) > 1 else 1_000_000
+s = int(sys.argv[2]) if len(sys.argv) > 2 else 4096
+weak = len(sys.argv) > 3 and sys.argv[3] == "weak"
+g = gp.barabasi_albert(n, 5, 1)
 pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
-k = gp.perturbation_budget(g, gp.PoolKind.NodeRemoval, rate)
+k = gp.perturbation_budget(g, gp.PoolKind.NodeRemoval, 0.05)
 obj = gp.PairwiseConnectivityObjective(g, pool)
+cudart = C.CDLL("libcudart.so.12")
 out = {}
-for world in (1, 2, 4, 8):
-    shard = Shard(0, world, s)
-    lo, hi = shard.rows
+for mode in os.environ.get("PROBE_MODES", "rebuild,peer").split(","):
+    os.environ.pop("GAPA_PEER_ROWS_LOOPBACK", None)
+    if mode == "peer":
+        os.environ["GAPA_PEER_ROWS_LOOPBACK"] = "1"
+    out[mode] = {}
+    for world in [int(w) for w in os.environ.get("PROBE_WORLDS", "1,2,4,8").split(",")]:
+        pop = s * world if weak else s
+        block = (pop + world - 1) // world
 
-    def gather(fit, shard_):
-        if shard_.world == 1:
-            return
-        block = fit[lo:hi]
-        for r in range(1, shard_.world):
-            fit[r * (hi - lo):(r + 1) * (hi - lo)] = block
+        def exchange(user, fit_dev, s_, padded_block, stream, world=world):  # stand-in all-gather: copies of block 0
+            for r in range(1, world):
+                cudart.cudaMemcpyAsync(C.c_void_p(fit_dev + 8 * r * padded_block), C.c_void_p(fit_dev), C.c_size_t(8 * padded_block),
+                                       C.c_int(3), C.c_void_p(stream))
+            return 0
 
-    params = gp.GAParams(pc=0.6, pm=0.2, pop_size=s, budget=k, iterations=40, seed=1)
-    ga = ShardedGa(params, CudaOps(obj, 0), shard, gather)
-    ga.initialize()
-    for _ in range(3):
-        ga.step()
-    torch.cuda.synchronize()
-    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-    e0.record()
-    steps = 15
-    for _ in range(steps):
-        ga.step()
-    e1.record()
-    torch.cuda.synchronize()
-    out[world] = e0.elapsed_time(e1) / steps
-    del ga
-base = out[1]
-print(json.dumps({"n": n, "pop": s, "k": k, "ms_per_generation_per_rank": out,
-                  "projected_speedup_excluding_allgather": {w: base / t for w, t in out.items()}}))
+        params = gp.GAParams(pc=0.6, pm=0.2, pop_size=pop, budget=k, iterations=40, seed=1)
+        loop = gp.GaLoop(params, obj, rank=0, world=world, exchange=exchange if world > 1 else None)
+        loop.advance(5)
+        out[mode][world] = loop.advance(20) / 20
+        loop.close()
+        del block
+res = {"n": n, "pop": s, "k": k, "scaling": "weak (pop x world)" if weak else "strong", "ms_per_generation_per_rank": out,
+       "projected_speedup_excluding_exchange": {m: {w: (out[m][1] / t) * (w if weak else 1) for w, t in out[m].items()} for m in out if 1 in out[m]}}
+print(json.dumps(res))
