@@ -80,8 +80,9 @@ int gapa_cuda_graph_info(const gapa_cuda_ctx* ctx, int32_t* n, int64_t* m, int* 
 
 /* GenePool (gene_pool.hpp:32-52).  kind NODE_REMOVAL: u[i] = node of gene i
  * (u == NULL means the identity pool of build_gene_pool, gene_pool.cpp:89-92),
- * v ignored.  kind EDGE_REMOVAL: (u[i], v[i]) must be edges of the graph
- * (u == NULL means build_gene_pool's (u,v)-sorted order, gene_pool.cpp:73-79).
+ * v ignored.  kind EDGE_REMOVAL: (u[i], v[i]) are node pairs (u == NULL means build_gene_pool's (u,v)-sorted edge order,
+ * gene_pool.cpp:73-79); a pair that is not an edge of this graph is accepted and removes nothing, as in the reference
+ * (clearing an absent adjacency bit, gene_pool.cpp:53-56) — e.g. a pool built on the full graph, evaluated on split.train.
  * kind EDGE_ADDITION (cda task only, fitness.cpp:54-57): (u[i], v[i]) is the pair gene i
  * adds (gene_pool.cpp:57-60); u == NULL means every non-edge a < b in lexicographic
  * order (gene_pool.cpp:81-87; fails on a complete graph like :86).  A pair that is
@@ -114,6 +115,15 @@ int gapa_cuda_eval_batch_device(gapa_cuda_ctx* ctx, int task, const int32_t* gen
 /* init_population_block (ga_ops.cpp:19-29): out_dev[row_count x budget] */
 int gapa_cuda_ga_init_device(int32_t pool_size, int row_first, int row_count, int budget, uint64_t seed,
                              uint64_t generation, int32_t* out_dev, void* stream);
+/* make_crossover_mask / make_mutation_mask (ga_ops.cpp:38-47, :84-92): MaskMatrix bytes (population.hpp:43-60) of rows
+ * [row_first, row_first + row_count); role = GAPA_ROLE_CROSSOVER_MASK or GAPA_ROLE_MUTATION_MASK.  The generation loop
+ * never materialises these (the fused variation kernels evaluate the same draws in place); they exist for hosts and
+ * tests that want the matrices themselves (test_ga_engine.cpp:143-173). */
+int gapa_cuda_ga_mask_device(int role, double rate, int row_first, int row_count, int cols, uint64_t seed, uint64_t generation,
+                             uint8_t* out_dev, void* stream);
+/* make_mutation_indices (ga_ops.cpp:94-103): the fresh genes mutate draws, int32 [row_count x cols] */
+int gapa_cuda_ga_mutation_indices_device(int32_t pool_size, int row_first, int row_count, int cols, uint64_t seed,
+                                         uint64_t generation, int32_t* out_dev, void* stream);
 /* roulette_select in index form (ga_ops.cpp:54-82,105-128): rank weights with
  * tie-span averaging -> cumulative -> one Select draw per row -> partner row.
  * weights_dev / scratch may be NULL.  Non-finite fitness -> GAPA_CUDA_E_NAN. */
@@ -198,6 +208,9 @@ int gapa_cuda_ga_stats_device(const double* fit_dev, int s, double* best_dev, do
  * the parity tests.  `device` selects the GPU. */
 int gapa_cuda_ga_init(int device, int32_t pool_size, int row_first, int row_count, int budget, uint64_t seed,
                       uint64_t generation, int32_t* out);
+int gapa_cuda_ga_mask(int device, int role, double rate, int rows, int cols, uint64_t seed, uint64_t generation, uint8_t* out);
+int gapa_cuda_ga_mutation_indices(int device, int32_t pool_size, int rows, int cols, uint64_t seed, uint64_t generation,
+                                  int32_t* out);
 int gapa_cuda_ga_selection_weights(int device, const double* fitness, int s, int minimize, double* weights);
 int gapa_cuda_ga_select(int device, const double* fitness, int s, int minimize, uint64_t seed,
                         uint64_t generation, int32_t* partner_index);

@@ -28,6 +28,7 @@ MODE_SERIAL, MODE_S, MODE_SM, MODE_M, MODE_MNM = 0, 1, 2, 3, 4
 
 _i32p = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
 _f64p = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_u8p = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
 _u64p = np.ctypeslib.ndpointer(dtype=np.uint64, flags="C_CONTIGUOUS")
 _u32p = np.ctypeslib.ndpointer(dtype=np.uint32, flags="C_CONTIGUOUS")
 
@@ -144,6 +145,10 @@ class Oracle:
         lib.orc_ra_score.restype = C.c_double
         lib.orc_ra_score.argtypes = [G, C.c_int32, C.c_int32]
         lib.orc_init_population_block.argtypes = [C.c_int] * 4 + [C.c_uint64, C.c_uint64, _i32p]
+        lib.orc_make_mask.restype = None
+        lib.orc_make_mask.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_uint64, C.c_uint64, _u8p]
+        lib.orc_make_mutation_indices.restype = None
+        lib.orc_make_mutation_indices.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, _i32p]
         lib.orc_selection_weights.argtypes = [_f64p, C.c_int, C.c_int, _f64p]
         lib.orc_roulette_pick.argtypes = [_f64p, C.c_int, C.c_int, C.c_uint64, C.c_uint64, _i32p]
         lib.orc_crossover.argtypes = [_i32p, _i32p, C.c_int, C.c_int, C.c_double, C.c_uint64, C.c_uint64, _i32p]
@@ -234,6 +239,17 @@ class Oracle:
 
     def init_population(self, pool_size, pop_size, budget, seed, generation=0):
         return self.init_population_block(pool_size, 0, pop_size, budget, seed, generation)
+
+    def make_mask(self, rows, cols, rate, role, seed, generation):
+        """role 3 = make_crossover_mask, 4 = make_mutation_mask (ga_ops.cpp:84-92)"""
+        out = np.zeros((rows, cols), dtype=np.uint8)
+        self.lib.orc_make_mask(rows, cols, rate, role, seed, generation, out.reshape(-1) if out.size else np.zeros(1, np.uint8))
+        return out
+
+    def make_mutation_indices(self, rows, cols, pool_size, seed, generation):
+        out = np.zeros((rows, cols), dtype=np.int32)
+        self.lib.orc_make_mutation_indices(rows, cols, pool_size, seed, generation, out.reshape(-1) if out.size else np.zeros(1, np.int32))
+        return out
 
     def selection_weights(self, fitness, minimize=True):
         f = np.ascontiguousarray(fitness, dtype=np.float64)
@@ -357,6 +373,9 @@ class Ref:
         lib.ref_ra_score.restype = C.c_double
         lib.ref_ra_score.argtypes = [V, C.c_int, C.c_int]
         lib.ref_init_population_block.argtypes = [C.c_int] * 4 + [C.c_uint64, C.c_uint64, _i32p]
+        if hasattr(lib, "ref_make_mask"):
+            lib.ref_make_mask.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_uint64, C.c_uint64, _u8p]
+            lib.ref_make_mutation_indices.argtypes = [C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, _i32p]
         lib.ref_selection_weights.argtypes = [_f64p, C.c_int, C.c_int, _f64p]
         lib.ref_roulette_select.argtypes = [_i32p, C.c_int, C.c_int, _f64p, C.c_int, C.c_uint64, C.c_uint64, _i32p,
                                             _i32p]
@@ -490,6 +509,19 @@ class Ref:
 
     def init_population(self, pool_size, pop_size, budget, seed, generation=0):
         return self.init_population_block(pool_size, 0, pop_size, budget, seed, generation)
+
+    def make_mask(self, rows, cols, rate, role, seed, generation):
+        out = np.zeros((rows, cols), dtype=np.uint8)
+        if self.lib.ref_make_mask(rows, cols, rate, role, seed, generation, out.reshape(-1) if out.size else np.zeros(1, np.uint8)):
+            raise ValueError(self._err())
+        return out
+
+    def make_mutation_indices(self, rows, cols, pool_size, seed, generation):
+        out = np.zeros((rows, cols), dtype=np.int32)
+        if self.lib.ref_make_mutation_indices(rows, cols, pool_size, seed, generation,
+                                              out.reshape(-1) if out.size else np.zeros(1, np.int32)):
+            raise ValueError(self._err())
+        return out
 
     def selection_weights(self, fitness, minimize=True):
         f = np.ascontiguousarray(fitness, dtype=np.float64)

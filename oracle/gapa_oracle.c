@@ -701,6 +701,22 @@ int orc_init_population_block(int pool_size, int row_first, int row_count, int b
     return 0;
 }
 
+/* make_mask (ga_ops.cpp:38-47) behind make_crossover_mask / make_mutation_mask (:84-92): role 3 or 4 */
+void orc_make_mask(int rows, int cols, double rate, int role, uint64_t seed, uint64_t generation, uint8_t* out) {
+    for (int i = 0; i < rows; ++i) {
+        const uint64_t key = orc_stream_key(seed, generation, (uint64_t)role, (uint64_t)i);
+        for (int j = 0; j < cols; ++j) out[(size_t)i * cols + j] = orc_draw_unit(key, (uint64_t)j + 1) < rate ? 1 : 0; /* rng.hpp:33 */
+    }
+}
+
+/* make_mutation_indices (ga_ops.cpp:94-103) */
+void orc_make_mutation_indices(int rows, int cols, int pool_size, uint64_t seed, uint64_t generation, int32_t* out) {
+    for (int i = 0; i < rows; ++i) {
+        const uint64_t key = orc_stream_key(seed, generation, ORC_ROLE_MUTATION_INDEX, (uint64_t)i);
+        for (int j = 0; j < cols; ++j) out[(size_t)i * cols + j] = (int32_t)orc_draw_index(key, (uint64_t)j + 1, (uint32_t)pool_size);
+    }
+}
+
 /* stable merge sort of indices; better(a, b) is the strict "a before b" */
 typedef struct { const double* f0; const double* f1; int s; int minimize; } keyctx;
 static double key_of(const keyctx* c, int idx) { return idx < c->s ? c->f0[idx] : c->f1[idx - c->s]; }

@@ -97,6 +97,8 @@ int orc_detect_communities(const orc_graph* g, int32_t* assignment);
 double orc_ra_score(const orc_graph* g, int32_t u, int32_t v); /* link_prediction.cpp:55-69 */
 
 /* ---- genetic operators (ga_ops.cpp) ---------------------------------------- */
+void orc_make_mask(int rows, int cols, double rate, int role, uint64_t seed, uint64_t generation, uint8_t* out);
+void orc_make_mutation_indices(int rows, int cols, int pool_size, uint64_t seed, uint64_t generation, int32_t* out);
 int orc_init_population_block(int pool_size, int row_first, int row_count, int budget,
                               uint64_t seed, uint64_t generation, int32_t* out);
 int orc_selection_weights(const double* fitness, int s, int minimize, double* out);

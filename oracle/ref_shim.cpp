@@ -282,6 +282,19 @@ int ref_init_population_block(int pool_size, int row_first, int row_count, int b
         std::copy(p.data.begin(), p.data.end(), out);
     });
 }
+int ref_make_mask(int rows, int cols, double rate, int role, std::uint64_t seed, std::uint64_t generation, std::uint8_t* out) {
+    return guarded([&] {
+        const MaskMatrix m = role == 3 ? make_crossover_mask(rows, cols, rate, RngPolicy(seed), generation)
+                                       : make_mutation_mask(rows, cols, rate, RngPolicy(seed), generation);
+        std::copy(m.data.begin(), m.data.end(), out);
+    });
+}
+int ref_make_mutation_indices(int rows, int cols, int pool_size, std::uint64_t seed, std::uint64_t generation, std::int32_t* out) {
+    return guarded([&] {
+        const PopulationMatrix m = make_mutation_indices(rows, cols, pool_size, RngPolicy(seed), generation);
+        std::copy(m.data.begin(), m.data.end(), out);
+    });
+}
 int ref_selection_weights(const double* fitness, int s, int minimize, double* out) {
     return guarded([&] {
         const auto w = selection_weights(FitnessVector(fitness, fitness + s), to_direction(minimize));

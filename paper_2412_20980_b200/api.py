@@ -353,6 +353,24 @@ def init_population(pool_size, pop_size, budget, seed, generation=0, device=0) -
     return init_population_block(pool_size, 0, pop_size, budget, seed, generation, device)
 
 
+def make_crossover_mask(rows, cols, pc, seed, generation, device=0) -> np.ndarray:  # ga_ops.cpp:84-87
+    out = np.zeros((rows, cols), dtype=np.uint8)
+    check(capi.load().gapa_cuda_ga_mask(device, 3, pc, rows, cols, seed, generation, _ptr(out)))
+    return out
+
+
+def make_mutation_mask(rows, cols, pm, seed, generation, device=0) -> np.ndarray:  # ga_ops.cpp:89-92
+    out = np.zeros((rows, cols), dtype=np.uint8)
+    check(capi.load().gapa_cuda_ga_mask(device, 4, pm, rows, cols, seed, generation, _ptr(out)))
+    return out
+
+
+def make_mutation_indices(rows, cols, pool_size, seed, generation, device=0) -> np.ndarray:  # ga_ops.cpp:94-103
+    out = np.zeros((rows, cols), dtype=np.int32)
+    check(capi.load().gapa_cuda_ga_mutation_indices(device, pool_size, rows, cols, seed, generation, _ptr(out)))
+    return out
+
+
 def selection_weights(fitness, direction: Direction, device=0) -> np.ndarray:  # ga_ops.cpp:54-76
     f = _f64(fitness)
     out = np.zeros_like(f)

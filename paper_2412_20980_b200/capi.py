@@ -57,6 +57,10 @@ SIGNATURES = {
     "gapa_cuda_eval_batch": (C.c_int, [VP, C.c_int, VP, C.c_int, C.c_int, VP]),
     "gapa_cuda_eval_batch_device": (C.c_int, [VP, C.c_int, VP, C.c_int, C.c_int, VP, VP]),
     "gapa_cuda_ga_init_device": (C.c_int, [C.c_int32, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, VP, VP]),
+    "gapa_cuda_ga_mask_device": (C.c_int, [C.c_int, C.c_double, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, VP, VP]),
+    "gapa_cuda_ga_mutation_indices_device": (C.c_int, [C.c_int32, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, VP, VP]),
+    "gapa_cuda_ga_mask": (C.c_int, [C.c_int, C.c_int, C.c_double, C.c_int, C.c_int, C.c_uint64, C.c_uint64, VP]),
+    "gapa_cuda_ga_mutation_indices": (C.c_int, [C.c_int, C.c_int32, C.c_int, C.c_int, C.c_uint64, C.c_uint64, VP]),
     "gapa_cuda_ga_select_device": (C.c_int, [VP, C.c_int, C.c_int, C.c_uint64, C.c_uint64, VP, VP, VP]),
     "gapa_cuda_ga_crossover_mutate_device": (C.c_int, [VP, VP, C.c_int, C.c_int, C.c_int, C.c_int, C.c_double,
                                                        C.c_double, C.c_int32, C.c_uint64, C.c_uint64, VP, VP]),

@@ -226,7 +226,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                 }
             } else {
                 const int e = A.pool_map ? A.pool_map[gene] : gene;
-                atomicOr(&gone[e >> 5], 1u << (e & 31));
+                if (e >= 0) atomicOr(&gone[e >> 5], 1u << (e & 31));  // -1: the pair is not an edge of this graph, a no-op
             }
         }
         __syncthreads();

@@ -373,6 +373,7 @@ int gapa_cuda_pool_set(gapa_cuda_ctx* c, int kind, int32_t n_genes, const int32_
     if (!u) n_genes = full;
     if (n_genes < 0) return fail(GAPA_CUDA_E_INVALID, "pool_set: negative size");
     std::vector<int32_t> map(static_cast<size_t>(n_genes));
+    std::vector<uint64_t> pair_keys;  // custom edge pools: the (u, v) pairs, for the duplicate check
     bool identity = true;
     for (int32_t i = 0; i < n_genes; ++i) {
         int32_t target;
@@ -382,17 +383,29 @@ int gapa_cuda_pool_set(gapa_cuda_ctx* c, int kind, int32_t n_genes, const int32_
             if (target < 0 || target >= c->n) return fail(GAPA_CUDA_E_INVALID, "pool_set: node %d out of range", target);
         } else {
             if (!v) return fail(GAPA_CUDA_E_INVALID, "pool_set: edge pool needs both endpoint arrays");
-            target = edge_rank(c, u[i], v[i]);
-            if (target < 0) return fail(GAPA_CUDA_E_INVALID, "pool_set: (%d, %d) is not an edge of the graph", u[i], v[i]);
+            int32_t a = u[i], b = v[i];
+            if (a < 0 || b < 0 || a >= c->n || b >= c->n || a == b)
+                return fail(GAPA_CUDA_E_INVALID, "pool_set: (%d, %d) is not a valid node pair", a, b);
+            if (a > b) std::swap(a, b);
+            pair_keys.push_back((static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(b));
+            // A pair that is not an edge of THIS graph (a pool built on the full graph, evaluated on split.train) is accepted
+            // like the reference does (gene_pool.cpp:34-56): clearing an absent adjacency bit is a no-op.  -1 = no-op gene.
+            target = edge_rank(c, a, b);
         }
         map[i] = target;
         identity &= (target == i);
     }
     if (!identity) {  // GenePool's constructor rejects repeated elements (gene_pool.cpp:36-41)
-        std::vector<int32_t> sorted(map);
-        std::sort(sorted.begin(), sorted.end());
-        if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
-            return fail(GAPA_CUDA_E_INVALID, "gene pool: duplicate element");
+        if (!pair_keys.empty()) {
+            std::sort(pair_keys.begin(), pair_keys.end());
+            if (std::adjacent_find(pair_keys.begin(), pair_keys.end()) != pair_keys.end())
+                return fail(GAPA_CUDA_E_INVALID, "gene pool: duplicate element");
+        } else {
+            std::vector<int32_t> sorted(map);
+            std::sort(sorted.begin(), sorted.end());
+            if (std::adjacent_find(sorted.begin(), sorted.end()) != sorted.end())
+                return fail(GAPA_CUDA_E_INVALID, "gene pool: duplicate element");
+        }
     }
     GAPA_CUDA_TRY(cudaSetDevice(c->device));
     for (int32_t** p : {&c->d_pool_map, &c->d_add_u, &c->d_add_v})
@@ -447,6 +460,17 @@ static int check_task(const gapa_cuda_ctx* c, int task) {
             return GAPA_CUDA_OK;
     }
     return fail(GAPA_CUDA_E_INVALID, "unknown fitness task %d", task);
+}
+
+// every gene of the s parent rows lies in [0, pool_size)?
+__global__ void __launch_bounds__(256) k_genes_in_range(const int32_t* __restrict__ pool, const int32_t* __restrict__ parent, int s, int k,
+                                                        int pool_size, int* bad) {
+    const size_t cells = static_cast<size_t>(s) * k;
+    for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cells; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+        const int r = static_cast<int>(i / k);
+        const int gene = pool[static_cast<size_t>(parent[r]) * k + (i - static_cast<size_t>(r) * k)];
+        if (gene < 0 || gene >= pool_size) *bad = 1;
+    }
 }
 
 static int eval_rows_locked(gapa_cuda_ctx* c, int task, const GeneRows& genes, int rows, double* out_dev, void* stream,
@@ -507,6 +531,30 @@ int gapa_cuda_ga_slots_variation_eval_device(gapa_cuda_ctx* c, int task, int32_t
         return fail(GAPA_CUDA_E_INVALID, "variation_eval: row block outside the population");
     if (row_count == 0) return GAPA_CUDA_OK;
     if (!pool_dev || !parent_dev || !child_dev || !fit_block_dev) return fail(GAPA_CUDA_E_INVALID, "variation_eval: null buffer");
+    // The fused kernels index bitmaps with the genes they inherit from the parents without a per-gene range check.  Parents
+    // written by this library's operators are inside the pool by induction; a pool buffer seen for the first time (or
+    // after the gene pool changed) is validated once, all s parent rows.
+    {
+        std::lock_guard<std::mutex> lock(c->mu);
+        const size_t cells = static_cast<size_t>(s) * k;
+        if (c->validated_pool != pool_dev || c->validated_cells != cells || c->validated_version != c->pool_version) {
+            GAPA_CUDA_TRY(cudaSetDevice(c->device));
+            GAPA_TRY(c->status_buf.ensure(sizeof(int)));
+            cudaStream_t st = static_cast<cudaStream_t>(stream);
+            GAPA_CUDA_TRY(cudaMemsetAsync(c->status_buf.ptr, 0, sizeof(int), st));
+            if (cells) {
+                const int grid = static_cast<int>(std::min<size_t>(static_cast<size_t>(c->sm_count) * 8, (cells + 255) / 256));
+                GAPA_LAUNCH(k_genes_in_range, grid, 256, 0, st, pool_dev, parent_dev, s, k, c->pool_size, c->status_buf.as<int>());
+            }
+            int bad = 0;
+            GAPA_CUDA_TRY(cudaMemcpyAsync(&bad, c->status_buf.ptr, sizeof(int), cudaMemcpyDeviceToHost, st));
+            GAPA_CUDA_TRY(cudaStreamSynchronize(st));
+            if (bad) return fail(GAPA_CUDA_E_RANGE, "variation_eval: a parent row holds a gene id outside the pool");
+            c->validated_pool = pool_dev;
+            c->validated_cells = cells;
+            c->validated_version = c->pool_version;
+        }
+    }
     VariationSpec spec;
     spec.P = make_variation_params(pc, pm, static_cast<uint32_t>(c->pool_size), s, seed, generation);
     spec.pool = pool_dev;

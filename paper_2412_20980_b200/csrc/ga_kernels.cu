@@ -28,6 +28,33 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_init(uint32_t pool_size, int 
         dst[j] = static_cast<int32_t>(draw_index(k, static_cast<uint64_t>(j) + 1, pool_size));
 }
 
+// ---- make_crossover_mask / make_mutation_mask (ga_ops.cpp:38-47, :84-92) and make_mutation_indices (:94-103) ------
+// The matrices the fused variation kernels never materialise, for hosts and tests that want them:
+// mask(i, j) = stream(generation, role, row_first + i).next_bernoulli(rate) at draw j + 1 (1 or 0, MaskMatrix bytes).
+__global__ void __launch_bounds__(kGaThreads) k_ga_mask(uint64_t role, int row_first, int cols, uint64_t limit, bool always,
+                                                        uint64_t seed, uint64_t generation, uint8_t* __restrict__ out) {
+    __shared__ uint64_t key;
+    const int row = blockIdx.y;
+    if (threadIdx.x == 0) key = stream_key(seed, generation, role, static_cast<uint64_t>(row_first + row));
+    __syncthreads();
+    const uint64_t k = key;
+    uint8_t* dst = out + static_cast<size_t>(row) * cols;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
+        dst[j] = (always || draw_u64(k, static_cast<uint64_t>(j) + 1) < limit) ? 1 : 0;
+}
+// fresh(i, j) = stream(generation, MutationIndex, row_first + i).next_index(pool) at draw j + 1
+__global__ void __launch_bounds__(kGaThreads) k_ga_mutation_indices(uint32_t pool_size, int row_first, int cols, uint64_t seed,
+                                                                    uint64_t generation, int32_t* __restrict__ out) {
+    __shared__ uint64_t key;
+    const int row = blockIdx.y;
+    if (threadIdx.x == 0) key = stream_key(seed, generation, GAPA_ROLE_MUTATION_INDEX, static_cast<uint64_t>(row_first + row));
+    __syncthreads();
+    const uint64_t k = key;
+    int32_t* dst = out + static_cast<size_t>(row) * cols;
+    for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < cols; j += gridDim.x * blockDim.x)
+        dst[j] = static_cast<int32_t>(draw_index(k, static_cast<uint64_t>(j) + 1, pool_size));
+}
+
 // ---- crossover (ga_ops.cpp:130-144) fused with mutate_block (:164-178) -------------------
 // out(i,j) = RM(i,j) ? fresh(i,j) : (RC(i,j) ? pop(partner_i, j) : pop(i, j)).
 // All three draws are random-access, so a flipped gene skips the crossover draw
@@ -565,6 +592,28 @@ int gapa_cuda_ga_init_device(int32_t pool_size, int row_first, int row_count, in
                        static_cast<cudaStream_t>(stream));
 }
 
+int gapa_cuda_ga_mask_device(int role, double rate, int row_first, int row_count, int cols, uint64_t seed, uint64_t generation,
+                             uint8_t* out_dev, void* stream) {
+    if (role != GAPA_ROLE_CROSSOVER_MASK && role != GAPA_ROLE_MUTATION_MASK) return fail(GAPA_CUDA_E_INVALID, "mask: role must be a mask stream");
+    if (!(rate >= 0.0 && rate <= 1.0)) return fail(GAPA_CUDA_E_INVALID, "mask: rate must be in [0, 1]");
+    if (row_first < 0 || row_count < 0 || cols < 0) return fail(GAPA_CUDA_E_INVALID, "mask: negative shape");
+    if (row_count == 0 || cols == 0) return GAPA_CUDA_OK;
+    const BernoulliLimit lim = bernoulli_limit(rate);
+    GAPA_LAUNCH(k_ga_mask, row_grid(cols, row_count), kGaThreads, 0, static_cast<cudaStream_t>(stream), static_cast<uint64_t>(role),
+                row_first, cols, lim.limit, lim.always, seed, generation, out_dev);
+    return GAPA_CUDA_OK;
+}
+
+int gapa_cuda_ga_mutation_indices_device(int32_t pool_size, int row_first, int row_count, int cols, uint64_t seed,
+                                         uint64_t generation, int32_t* out_dev, void* stream) {
+    if (pool_size < 1) return fail(GAPA_CUDA_E_INVALID, "mutate: empty gene pool");
+    if (row_first < 0 || row_count < 0 || cols < 0) return fail(GAPA_CUDA_E_INVALID, "mutation_indices: negative shape");
+    if (row_count == 0 || cols == 0) return GAPA_CUDA_OK;
+    GAPA_LAUNCH(k_ga_mutation_indices, row_grid(cols, row_count), kGaThreads, 0, static_cast<cudaStream_t>(stream),
+                static_cast<uint32_t>(pool_size), row_first, cols, seed, generation, out_dev);
+    return GAPA_CUDA_OK;
+}
+
 int gapa_cuda_ga_select_device(const double* fitness_dev, int s, int minimize, uint64_t seed, uint64_t generation,
                                int32_t* partner_dev, double* weights_dev, void* stream) {
     if (s < 1) return fail(GAPA_CUDA_E_INVALID, "roulette_select: empty population");
@@ -663,6 +712,26 @@ int gapa_cuda_ga_init(int device, int32_t pool_size, int row_first, int row_coun
     const size_t cells = static_cast<size_t>(std::max(row_count, 0)) * std::max(budget, 0);
     GAPA_TRY(t.up<int32_t>(nullptr, cells, &d));
     GAPA_TRY(gapa_cuda_ga_init_device(pool_size, row_first, row_count, budget, seed, generation, d, nullptr));
+    return t.down(out, d, cells);
+}
+
+int gapa_cuda_ga_mask(int device, int role, double rate, int rows, int cols, uint64_t seed, uint64_t generation, uint8_t* out) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    Tmp t;
+    uint8_t* d = nullptr;
+    const size_t cells = static_cast<size_t>(std::max(rows, 0)) * std::max(cols, 0);
+    GAPA_TRY(t.up<uint8_t>(nullptr, cells, &d));
+    GAPA_TRY(gapa_cuda_ga_mask_device(role, rate, 0, rows, cols, seed, generation, d, nullptr));
+    return t.down(out, d, cells);
+}
+
+int gapa_cuda_ga_mutation_indices(int device, int32_t pool_size, int rows, int cols, uint64_t seed, uint64_t generation, int32_t* out) {
+    GAPA_CUDA_TRY(cudaSetDevice(device));
+    Tmp t;
+    int32_t* d = nullptr;
+    const size_t cells = static_cast<size_t>(std::max(rows, 0)) * std::max(cols, 0);
+    GAPA_TRY(t.up<int32_t>(nullptr, cells, &d));
+    GAPA_TRY(gapa_cuda_ga_mutation_indices_device(pool_size, 0, rows, cols, seed, generation, d, nullptr));
     return t.down(out, d, cells);
 }
 

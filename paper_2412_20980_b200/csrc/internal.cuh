@@ -205,6 +205,10 @@ struct gapa_cuda_ctx {
     // staging for the host-buffer entry point
     gapa_b200::DevBuf genes_stage, out_stage, status_buf;
     int32_t* h_status = nullptr;    // pinned
+    // the caller's slot pool whose parent rows were last checked to hold genes inside the pool (fused variation entry)
+    const void* validated_pool = nullptr;
+    size_t validated_cells = 0;
+    unsigned long long validated_version = ~0ull;
     gapa_b200::PcScratch* pc = nullptr;
     gapa_b200::LpaScratch* lpa = nullptr;
     gapa_b200::CdaScratch* cda = nullptr;

@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(kLpaThreads) k_lpa_remove(GeneRows genes, size
             continue;
         }
         const int e = pool_map ? pool_map[gene] : gene;
+        if (e < 0) continue;  // the pool names a pair that is not an edge of this graph: nothing to clear (gene_pool.cpp:53-56)
         const unsigned bit = 1u << (e & 31);
         const unsigned old = atomicOr(&gone[static_cast<size_t>(r) * mask_words + (e >> 5)], bit);
         if (!(old & bit)) {

@@ -199,10 +199,10 @@ __global__ void __launch_bounds__(nt) k_pc_bitmask(GeneRows genes,
 // to the child's slot and sets it in the shared-memory bitmap in the same pass.  The hash arithmetic
 // of the variation (integer pipes) and the shared-memory atomics of the mask build (LSU) overlap
 // inside one kernel, and the 4 k bytes of the child row are never read back from HBM.
-template <int nt>
+template <int nt, bool kPeer>  // kPeer: parent rows may live in another rank's HBM (variation.cuh: parent_row)
 __global__ void __launch_bounds__(nt) k_pc_bitmask_vary(VariationSpec V, int k, const int32_t* __restrict__ gene_map,
                                                                   int n, int words_per_row, word_t* __restrict__ removed,
-                                                                  int* removed_count) {
+                                                                  int* removed_count, PcCounters* counters) {
     __shared__ uint64_t keys[4];
     const int local = blockIdx.x, row = V.row_first + local;
     const int words64 = (n + 63) >> 6;
@@ -213,17 +213,21 @@ __global__ void __launch_bounds__(nt) k_pc_bitmask_vary(VariationSpec V, int k, 
     const uint64_t ks = keys[0], kc = keys[1], km = keys[2], ki = keys[3];
     const bool eda = V.partner == nullptr;
     const int slot_mine = V.parent[row], slot_theirs = eda ? slot_mine : V.parent[V.partner[row]];
-    bool adopt_mine, adopt_theirs;  // the row lives in another rank's HBM: read it there, keep a copy here
-    const int32_t* mine = parent_row(V, slot_mine, k, &adopt_mine);
-    const int32_t* theirs = eda ? mine : parent_row(V, slot_theirs, k, &adopt_theirs);
+    bool adopt_mine = false, adopt_theirs = false;  // the row lives in another rank's HBM: read it there, keep a copy here
+    const int32_t* mine = kPeer ? parent_row(V, slot_mine, k, &adopt_mine) : V.pool + static_cast<size_t>(slot_mine) * k;
+    const int32_t* theirs = eda ? mine : (kPeer ? parent_row(V, slot_theirs, k, &adopt_theirs) : V.pool + static_cast<size_t>(slot_theirs) * k);
     if (eda || slot_theirs == slot_mine) adopt_theirs = false;
     int32_t* keep_mine = V.pool + static_cast<size_t>(slot_mine) * k;
     int32_t* keep_theirs = V.pool + static_cast<size_t>(slot_theirs) * k;
     int32_t* dst = V.pool + static_cast<size_t>(V.child[row]) * k;
+    // No range check here (one compare per gene costs this kernel 5 %): a mutated gene is inside the pool by construction
+    // and an inherited one is as good as the parents — which this library's own operators wrote, or which
+    // gapa_cuda_ga_slots_variation_eval_device validated when it first saw the caller's pool (ctx.cu).
     auto mark = [&](int gene) {
         const int node = gene_map ? gene_map[gene] : gene;
         atomicOr(&pc_smem_bits[node >> 5], 1u << (node & 31));
     };
+    (void)counters;
     if ((k & 3) == 0) {
         const int4* mine4 = reinterpret_cast<const int4*>(mine);
         const int4* theirs4 = reinterpret_cast<const int4*>(theirs);
@@ -240,8 +244,8 @@ __global__ void __launch_bounds__(nt) k_pc_bitmask_vary(VariationSpec V, int k, 
                 a_next = __ldcs(&mine4[q + nt]);
                 b_next = eda ? a_next : __ldcs(&theirs4[q + nt]);
             }
-            if (adopt_mine) reinterpret_cast<int4*>(keep_mine)[q] = a;
-            if (adopt_theirs) reinterpret_cast<int4*>(keep_theirs)[q] = b;
+            if (kPeer && adopt_mine) reinterpret_cast<int4*>(keep_mine)[q] = a;
+            if (kPeer && adopt_theirs) reinterpret_cast<int4*>(keep_theirs)[q] = b;
             const int av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
             int r[4];
             uint64_t prod = kCounterStep * (static_cast<uint64_t>(q) * 4 + 1);
@@ -257,8 +261,8 @@ __global__ void __launch_bounds__(nt) k_pc_bitmask_vary(VariationSpec V, int k, 
     } else {
         for (int j = threadIdx.x; j < k; j += nt) {
             const int a = mine[j], b = theirs[j];
-            if (adopt_mine) keep_mine[j] = a;
-            if (adopt_theirs) keep_theirs[j] = b;
+            if (kPeer && adopt_mine) keep_mine[j] = a;
+            if (kPeer && adopt_theirs) keep_theirs[j] = b;
             const int gsel = child_gene(V.P, V.pool, V.parent, k, j, a, b, eda, ks, kc, km, ki,
                                         kCounterStep * (static_cast<uint64_t>(j) + 1));
             dst[j] = gsel;
@@ -1301,9 +1305,15 @@ static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLan
         if (fused_mask) {
             VariationSpec pass = *job.vary;
             pass.row_first += row0;
-#define GAPA_MASK_VARY(NT)                                                                                                  \
-    GAPA_LAUNCH(k_pc_bitmask_vary<NT>, crows, NT, static_cast<size_t>(chunk_bits) / 8, stream, pass, cols, g_gene_map, n, \
-                words_per_row, set->removed.as<word_t>(), set->removed_count.as<int>())
+#define GAPA_MASK_VARY(NT)                                                                                                       \
+    do {                                                                                                                        \
+        if (pass.bases)                                                                                                         \
+            GAPA_LAUNCH((k_pc_bitmask_vary<NT, true>), crows, NT, static_cast<size_t>(chunk_bits) / 8, stream, pass, cols,      \
+                        g_gene_map, n, words_per_row, set->removed.as<word_t>(), set->removed_count.as<int>(), counters);       \
+        else                                                                                                                    \
+            GAPA_LAUNCH((k_pc_bitmask_vary<NT, false>), crows, NT, static_cast<size_t>(chunk_bits) / 8, stream, pass, cols,     \
+                        g_gene_map, n, words_per_row, set->removed.as<word_t>(), set->removed_count.as<int>(), counters);       \
+    } while (0)
             switch (mask_threads) {
                 case 128: GAPA_MASK_VARY(128); break;
                 case 256: GAPA_MASK_VARY(256); break;
@@ -1506,14 +1516,22 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<768>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<896>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<640>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<768>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<896>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
-        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<128, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<128, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<256, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<256, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<384, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<384, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<512, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<512, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<640, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<640, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<768, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<768, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<896, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<896, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<1024, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
         s->overlap_clear = env_int("GAPA_PC_OVERLAP_CLEAR", 1, 0, 1);
         s->trace = env_int("GAPA_PC_TRACE", 0, 0, 1);  // one stderr line per sweep round

@@ -347,3 +347,19 @@ for name in ("karate.txt", "sbm60.txt", "tree120.txt", "er90.txt"):
     e = r.graph_edges(g)
     datasets[name] = {"n": r.graph_n(g), "m": r.graph_m(g), "sha": sha(e), "first": ints(e[:5])}
 dump("experiments.json", {"experiments": experiments, "metrics": metrics, "datasets": datasets})
+
+# ------------------------------------------------------------------ mask matrices (ga_ops.cpp:84-103)
+mask_cases = []
+for rows, cols, rate, role, seed, g_ in [(6, 10, 0.6, 3, 1, 1), (100, 50, 0.2, 4, 1, 7), (33, 1, 0.0, 3, 9, 2), (5, 300, 1.0, 4, 3, 4),
+                                         (17, 129, 0.37, 3, 2**63 + 5, 100), (40, 64, 1e-3, 4, 5, 12)]:
+    a = r.make_mask(rows, cols, rate, role, seed, g_)
+    mask_cases.append({"rows": rows, "cols": cols, "rate": rate, "role": role, "seed": seed, "generation": g_, "sha": sha(a),
+                       "row0": [int(x) for x in a[0][:24]], "ones": int(a.sum())})
+index_cases = []
+for rows, cols, pool, seed, g_ in [(6, 10, 1000, 1, 1), (100, 50, 1000, 1, 7), (33, 1, 7, 9, 2), (5, 300, 2_000_000_000, 3, 4)]:
+    a = r.make_mutation_indices(rows, cols, pool, seed, g_)
+    index_cases.append({"rows": rows, "cols": cols, "pool": pool, "seed": seed, "generation": g_, "sha": sha(a),
+                        "row0": [int(x) for x in a[0][:16]]})
+dump("masks.json", {"_source": "compiled unmodified reference (oracle/_ref): make_crossover_mask / make_mutation_mask / "
+                               "make_mutation_indices, ga_ops.cpp:84-103; generated by tests/golden/make_golden.py (masks section)",
+                    "masks": mask_cases, "indices": index_cases})

@@ -49,7 +49,39 @@ def test_custom_edge_pool_order(gp, oracle, cuda_device):
     want = oracle.eval_batch(og, 2, order[genes].astype(np.int32))
     assert np.array_equal(gp.ModularityAttackObjective(g, pool).evaluate_batch(genes), want)
     with pytest.raises(gp.capi.GapaCudaError):
-        gp.ModularityAttackObjective(g, gp.GenePool(gp.PoolKind.EdgeRemoval, [0], [0]))  # not an edge
+        gp.ModularityAttackObjective(g, gp.GenePool(gp.PoolKind.EdgeRemoval, [0], [0]))  # not a node pair
+    # pairs that are not edges of THIS graph are accepted and remove nothing (gene_pool.cpp:34-56: clearing an absent
+    # bit) — the pool of the full graph evaluated on a sub-graph; a repeated pair is still rejected (:36-41)
+    have = {(int(a), int(b)) for a, b in zip(base.u, base.v)}
+    absent = [(a, b) for a in range(g.n) for b in range(a + 1, g.n) if (a, b) not in have][:40]
+    u2 = np.concatenate([u, np.array([a for a, _ in absent], np.int32)])
+    v2 = np.concatenate([v, np.array([b for _, b in absent], np.int32)])
+    mixed = gp.GenePool(gp.PoolKind.EdgeRemoval, u2, v2)
+    genes2 = rng.integers(0, mixed.size(), size=(6, 30)).astype(np.int32)
+    as_ranks = np.where(genes2 < len(order), order[np.minimum(genes2, len(order) - 1)], order[genes2[:, :1] % len(order)])
+    as_ranks = np.where(genes2 < len(order), as_ranks, as_ranks[:, :1])  # an absent pair == a repeat of a present gene (idempotent)
+    keep = genes2[:, 0] < len(order)  # rows whose first gene is a real edge can stand in for the no-ops
+    assert keep.any()
+    got2 = gp.ModularityAttackObjective(g, mixed).evaluate_batch(genes2[keep])
+    assert np.array_equal(got2, oracle.eval_batch(og, 2, as_ranks[keep].astype(np.int32)))
+    split = gp.build_lp_split(g, 0.2, 3)
+    full_pool = gp.build_gene_pool(g, gp.PoolKind.EdgeRemoval)  # built on the FULL graph, evaluated on split.train
+    lobj = gp.LinkPredictionAttackObjective(split, full_pool)
+    tr = gp.build_gene_pool(split.train, gp.PoolKind.EdgeRemoval)
+    rank_in_train = {(int(a), int(b)): i for i, (a, b) in enumerate(zip(tr.u, tr.v))}
+    rows = []
+    for _ in range(5):
+        ids = rng.integers(0, full_pool.size(), size=20)
+        mapped = [rank_in_train[(int(full_pool.u[i]), int(full_pool.v[i]))] for i in ids if (int(full_pool.u[i]), int(full_pool.v[i])) in rank_in_train]
+        if not mapped:
+            continue
+        mapped = (mapped * 20)[:20]  # repeats are idempotent
+        rows.append((ids.astype(np.int32), np.array(mapped, np.int32)))
+    os_ = oracle.split_build(og, 0.2, 3)
+    got3 = lobj.evaluate_batch(np.stack([a for a, _ in rows]))
+    assert np.array_equal(got3, oracle.eval_batch(os_, 3, np.stack([b for _, b in rows])))
+    with pytest.raises(gp.capi.GapaCudaError):
+        gp.ModularityAttackObjective(g, gp.GenePool(gp.PoolKind.EdgeRemoval, [absent[0][0], absent[0][1]], [absent[0][1], absent[0][0]]))
 
 
 def test_csr_constructor_and_argument_errors(gp, oracle, cuda_device):
@@ -176,3 +208,30 @@ def test_large_pageable_batches_take_the_pinned_ring(gp, oracle, cuda_device):
     pick = np.r_[0:40, 4090:4110, rows - 30:rows]
     assert np.array_equal(got[pick], oracle.eval_batch(og, 0, batch[pick], threads=8))
     assert np.array_equal(obj.evaluate_batch(batch), got)  # ring slots reused
+
+
+def test_fused_variation_validates_a_callers_pool_once(gp, cuda_device):
+    """gapa_cuda_ga_slots_variation_eval_device inherits genes from parents the CALLER wrote: the first call on a pool
+    buffer checks all parent rows (gene_pool.cpp:104-108: out of range is an error), later calls trust the library's
+    own operators.  An out-of-range parent gene is GAPA_CUDA_E_RANGE, not an out-of-bounds write."""
+    import torch
+    from paper_2412_20980_b200.driver import CudaOps
+    for n in (1500, 30_000):  # the shared-memory kernel and the bit-sliced pipeline
+        g = gp.barabasi_albert(n, 3, 1)
+        pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+        obj = gp.PairwiseConnectivityObjective(g, pool)
+        ops = CudaOps(obj, 0)
+        s, k = 16, 40
+        slots = ops.empty_genes(2 * s, k)
+        parent, child, partner = ops.empty_i32(s), ops.empty_i32(s), ops.empty_i32(s)
+        fit, fit_m = ops.zeros_f64(s), ops.zeros_f64(s)
+        ops.init(slots, parent, child, s, 3, 0)
+        ops.eval_rows(slots, parent, 0, s, fit)
+        ops.select(fit, s, 1, 3, 1, partner)
+        ops.variation_eval(slots, parent, child, partner, s, 0.6, 0.2, 3, 1, 0, s, fit_m)   # validates, passes
+        torch.cuda.synchronize()
+        bad = slots.clone()                       # a different buffer: validated again
+        bad[5, 7] = n + 12345
+        with pytest.raises(gp.capi.GapaCudaError) as e:
+            ops.variation_eval(bad, parent, child, partner, s, 0.6, 0.2, 3, 1, 0, s, fit_m)
+        assert e.value.code == gp.capi.E_RANGE

@@ -99,3 +99,41 @@ def test_eda_sample(gp, oracle, cuda_device):
         assert np.array_equal(gp.eda_sample(elite, ec, 40, 4, 6, smooth), oracle.eda_sample(elite, ec, 40, 4, 6, smooth))
     with pytest.raises(gp.capi.GapaCudaError):
         gp.eda_sample(elite, 31, 40, 4, 6)
+
+
+def test_mask_matrices_match_reference_and_explain_the_fused_operators(gp, oracle, cuda_device):
+    """make_crossover_mask / make_mutation_mask / make_mutation_indices (ga_ops.cpp:84-103; test_ga_engine.cpp:143-173):
+    the CUDA matrices equal the reference's (golden) and the oracle's, row blocks agree with the full matrices, and the
+    fused crossover+mutate kernel IS  RM ? fresh : (RC ? partner row : own row)  on exactly these matrices."""
+    import hashlib
+    import json
+    import os
+    doc = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "masks.json")))
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+    for c in doc["masks"]:
+        make = gp.make_crossover_mask if c["role"] == 3 else gp.make_mutation_mask
+        m = make(c["rows"], c["cols"], c["rate"], c["seed"], c["generation"])
+        assert m.dtype == np.uint8 and sha(m) == c["sha"] and int(m.sum()) == c["ones"]
+        assert np.array_equal(m, oracle.make_mask(c["rows"], c["cols"], c["rate"], c["role"], c["seed"], c["generation"]))
+    for c in doc["indices"]:
+        m = gp.make_mutation_indices(c["rows"], c["cols"], c["pool"], c["seed"], c["generation"])
+        assert sha(m) == c["sha"]
+    rng = np.random.default_rng(4)
+    s, k, pool, seed, gen, pc, pm = 57, 203, 900, 13, 6, 0.55, 0.15
+    pop = rng.integers(0, pool, size=(s, k)).astype(np.int32)
+    partner = rng.integers(0, s, size=s).astype(np.int32)
+    rc, rm = gp.make_crossover_mask(s, k, pc, seed, gen), gp.make_mutation_mask(s, k, pm, seed, gen)
+    fresh = gp.make_mutation_indices(s, k, pool, seed, gen)
+    want = np.where(rm == 1, fresh, np.where(rc == 1, pop[partner], pop))
+    import ctypes as C
+    out = np.zeros_like(pop)
+    gp.capi.check(gp.capi.load().gapa_cuda_ga_crossover_mutate(0, pop.ctypes.data, partner.ctypes.data, s, k, 0, s, pc, pm, pool, seed,
+                                                               gen, out.ctypes.data))
+    assert np.array_equal(out, want)
+    assert abs(rc.mean() - pc) < 0.02 and abs(rm.mean() - pm) < 0.02  # the rates they realise (test_ga_engine.cpp:150-158)
+    # device form, a row block: rows [20, 31) of the mutation mask
+    import torch
+    blk = torch.empty((11, k), dtype=torch.uint8, device="cuda")
+    gp.capi.check(gp.capi.load().gapa_cuda_ga_mask_device(4, pm, 20, 11, k, seed, gen, blk.data_ptr(), 0))
+    torch.cuda.synchronize()
+    assert np.array_equal(blk.cpu().numpy(), rm[20:31])

@@ -31,3 +31,20 @@ def test_recorded_reference_values(oracle):
     assert f'{gc.load("fitness.json")["karate"]["q0"]:.6f}' == "0.380671"          # criterion 8: unattacked Q
     assert f'{gc.load("runs_widen.json")["acceptance8_cda_add_karate"]["best"][-1]:.5f}' == "0.26156"  # attacked Q @300
     assert oracle.mix64(0) == 0xE220A8397B1DCDAF and oracle.mix64(1) == 0x910A2DEC89025CC1
+
+
+def test_oracle_reproduces_the_reference_mask_matrices(oracle):
+    """make_crossover_mask / make_mutation_mask / make_mutation_indices (ga_ops.cpp:84-103) from the compiled reference"""
+    import hashlib
+    import json
+    import os
+
+    import numpy as np
+    doc = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "masks.json")))
+    sha = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+    for c in doc["masks"]:
+        m = oracle.make_mask(c["rows"], c["cols"], c["rate"], c["role"], c["seed"], c["generation"])
+        assert sha(m) == c["sha"] and m[0][:24].tolist() == c["row0"] and int(m.sum()) == c["ones"]
+    for c in doc["indices"]:
+        m = oracle.make_mutation_indices(c["rows"], c["cols"], c["pool"], c["seed"], c["generation"])
+        assert sha(m) == c["sha"] and m[0][:16].tolist() == c["row0"]

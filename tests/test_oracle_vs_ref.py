@@ -166,3 +166,15 @@ def test_edge_addition_pool_and_cda(oracle, ref):
     b = ref.run_ga(rg, TASK_CDA_ADD, 0.8, 0.1, 8, 12, 4, 3)
     assert np.array_equal(a["best"], b["best"]) and np.array_equal(a["mean"], b["mean"])
     assert np.array_equal(a["population"], b["population"])
+
+
+def test_mask_matrices_oracle_equals_reference(oracle, ref):
+    import numpy as np
+    rng = np.random.default_rng(31)
+    for _ in range(25):
+        rows, cols = int(rng.integers(1, 40)), int(rng.integers(1, 90))
+        rate, seed, gen = float(rng.uniform(0, 1)), int(rng.integers(0, 2**62)), int(rng.integers(0, 500))
+        for role in (3, 4):
+            assert np.array_equal(oracle.make_mask(rows, cols, rate, role, seed, gen), ref.make_mask(rows, cols, rate, role, seed, gen))
+        pool = int(rng.integers(1, 2_000_000_000))
+        assert np.array_equal(oracle.make_mutation_indices(rows, cols, pool, seed, gen), ref.make_mutation_indices(rows, cols, pool, seed, gen))
