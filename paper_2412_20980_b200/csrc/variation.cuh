@@ -10,10 +10,41 @@ namespace gapa_b200 {
 static constexpr uint64_t kGolden = 0x9E3779B97F4A7C15ull;
 static constexpr uint64_t kCounterStep = 0x632BE59BD9B4E019ull;  // rng.hpp:21
 
-__device__ __forceinline__ uint64_t hash_tail(uint64_t y) {  // mix64(x) with y = x + kGolden (rng.hpp:8-13)
-    y = (y ^ (y >> 30)) * 0xBF58476D1CE4E5B9ull;
-    y = (y ^ (y >> 27)) * 0x94D049BB133111EBull;
+// Hand-expanded integer arithmetic of the hash, measured at C4 (tools/ab_vary_arith.sh, one generation):
+//   bit 0 — 64 x 64 -> low 64 as three multiply-adds (one wide, two accumulating into the high word) instead of the
+//           compiler's four instructions: 1.78 -> 1.89 ms.  The three-instruction form is one dependent chain, the
+//           compiler's has two independent halves: the kernel is bound by dependent-issue latency, not by issue slots.
+//   bit 1 — next_index as two wide multiply-adds instead of the generic __umul64hi: 1.781 -> 1.775 ms.  Kept.
+#ifndef GAPA_VARY_ARITH
+#define GAPA_VARY_ARITH 2
+#endif
+__device__ __forceinline__ uint64_t mul64_const(uint64_t x, uint64_t c) {
+#if !(GAPA_VARY_ARITH & 1)
+    return x * c;
+#endif
+    const uint32_t xl = static_cast<uint32_t>(x), xh = static_cast<uint32_t>(x >> 32);
+    const uint32_t cl = static_cast<uint32_t>(c), ch = static_cast<uint32_t>(c >> 32);
+    const uint64_t w = static_cast<uint64_t>(xl) * cl;
+    const uint32_t hi = static_cast<uint32_t>(w >> 32) + xl * ch + xh * cl;
+    return (static_cast<uint64_t>(hi) << 32) | static_cast<uint32_t>(w);
+}
+// mix64(x) up to, but not including, its last xor-shift; y = x + kGolden (rng.hpp:8-13)
+__device__ __forceinline__ uint64_t hash_body(uint64_t y) {
+    y = mul64_const(y ^ (y >> 30), 0xBF58476D1CE4E5B9ull);
+    return mul64_const(y ^ (y >> 27), 0x94D049BB133111EBull);
+}
+__device__ __forceinline__ uint64_t hash_tail(uint64_t y) {
+    y = hash_body(y);
     return y ^ (y >> 31);
+}
+// next_index (rng.hpp:28-31): high 64 bits of u64 x u32 in two wide multiply-adds
+__device__ __forceinline__ uint32_t mulhi_u64_u32(uint64_t u, uint32_t bound) {
+#if !(GAPA_VARY_ARITH & 2)
+    return static_cast<uint32_t>(__umul64hi(u, static_cast<uint64_t>(bound)));
+#endif
+    const uint64_t t = static_cast<uint64_t>(static_cast<uint32_t>(u)) * bound;
+    const uint64_t r = static_cast<uint64_t>(static_cast<uint32_t>(u >> 32)) * bound + (t >> 32);
+    return static_cast<uint32_t>(r >> 32);
 }
 
 struct VariationParams {
@@ -39,7 +70,7 @@ __device__ __forceinline__ int32_t child_gene(const VariationParams& P, const in
     const bool flip = P.pm_always || um < P.pm_limit;
     const uint64_t u2 = hash_tail((flip ? ki : (eda ? ks : kc)) + prod);
     const uint32_t bound = flip ? P.pool_size : P.s + P.pool_size;  // next_index bound (rng.hpp:28-31)
-    const uint32_t idx = static_cast<uint32_t>(__umul64hi(u2, static_cast<uint64_t>(bound)));
+    const uint32_t idx = mulhi_u64_u32(u2, bound);
     if (flip) return static_cast<int32_t>(idx);
     if (eda) return idx < P.s ? pool[static_cast<size_t>(parent[idx]) * k + col] : static_cast<int32_t>(idx - P.s);
     return (P.pc_always || u2 < P.pc_limit) ? theirs : mine;
