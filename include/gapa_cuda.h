@@ -53,7 +53,17 @@ enum {
 };
 
 /* PoolKind, gene_pool.hpp:14 (same order) */
-enum { GAPA_POOL_EDGE_REMOVAL = 0, GAPA_POOL_EDGE_ADDITION = 1, GAPA_POOL_NODE_REMOVAL = 2 };
+enum { GAPA_POOL_EDGE_REMOVAL = 0, GAPA_POOL_EDGE_ADDITION = 1, GAPA_POOL_NODE_REMOVAL = 2,
+       /* NOT in the reference (BASELINE.json north_star: "edge flips" for the link-prediction attack; PARITY UNPINNED,
+        * semantics stated in the oracle directory's C restatement): a gene is a node pair a < b; an edge of the graph is removed, a
+        * non-edge is added, relative to the UNPERTURBED graph (repeats are idempotent, like gene_pool.cpp:49-67).
+        * u == NULL in gapa_cuda_pool_set: every pair in lexicographic order, gene id = a n - a(a+1)/2 + (b - a - 1)
+        * (n <= 65536).  Link-prediction task only. */
+       GAPA_POOL_EDGE_FLIP = 3 };
+
+/* link score of the link-prediction task: RA = the reference's resource allocation (link_prediction.cpp:55-69);
+ * CN = common neighbours, |N'(u) & N'(v)| — north_star's "CN/RA link scores"; NOT in the reference, PARITY UNPINNED */
+enum { GAPA_LP_SCORE_RA = 0, GAPA_LP_SCORE_CN = 1 };
 
 /* StreamRole, rng.hpp:41-47 */
 enum { GAPA_ROLE_INIT = 1, GAPA_ROLE_SELECT = 2, GAPA_ROLE_CROSSOVER_MASK = 3,
@@ -95,6 +105,8 @@ int gapa_cuda_pool_info(const gapa_cuda_ctx* ctx, int* kind, int32_t* n_genes);
  * split.train; test_uv / probe_uv are T and P (u,v) pairs. */
 int gapa_cuda_lp_split_set(gapa_cuda_ctx* ctx, int32_t T, const int32_t* test_uv, int32_t P,
                            const int32_t* probe_uv);
+
+int gapa_cuda_lp_score_set(gapa_cuda_ctx* ctx, int score); /* GAPA_LP_SCORE_*; the default is RA */
 
 /* ---- fitness: FitnessFunction::evaluate_batch (fitness.hpp:17-27) ----------------
  * out[i] = fitness of row i, identical to the reference's evaluate_one on

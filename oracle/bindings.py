@@ -145,6 +145,10 @@ class Oracle:
         lib.orc_ra_score.restype = C.c_double
         lib.orc_ra_score.argtypes = [G, C.c_int32, C.c_int32]
         lib.orc_init_population_block.argtypes = [C.c_int] * 4 + [C.c_uint64, C.c_uint64, _i32p]
+        lib.orc_lpa_flip_batch.argtypes = [S, C.c_int, C.c_void_p, C.c_int64, _i32p, C.c_int, C.c_int, _f64p]
+        lib.orc_lpa_scored_batch.argtypes = [S, C.c_int, _i32p, C.c_int, C.c_int, _f64p]
+        lib.orc_flip_unrank.restype = None
+        lib.orc_flip_unrank.argtypes = [C.c_int32, C.c_int64, C.POINTER(C.c_int32), C.POINTER(C.c_int32)]
         lib.orc_make_mask.restype = None
         lib.orc_make_mask.argtypes = [C.c_int, C.c_int, C.c_double, C.c_int, C.c_uint64, C.c_uint64, _u8p]
         lib.orc_make_mutation_indices.restype = None
@@ -220,6 +224,31 @@ class Oracle:
         if rc:
             raise ValueError("oracle: gene id out of range")
         return out[:g.shape[0]]
+
+    # PARITY UNPINNED: CN score / edge-flip pools have no reference implementation (oracle/gapa_oracle.c states the semantics)
+    def lpa_flip_batch(self, split, genes, score=0, pool_uv=None):
+        g = _genes(genes)
+        out = np.zeros(max(g.shape[0], 1), dtype=np.float64)
+        if pool_uv is None:
+            ptr, size = None, 0
+        else:
+            pool_uv = np.ascontiguousarray(pool_uv, dtype=np.int32).reshape(-1, 2)
+            ptr, size = pool_uv.ctypes.data_as(C.c_void_p), len(pool_uv)
+        if self.lib.orc_lpa_flip_batch(split._ptr, score, ptr, size, g if g.size else np.zeros(1, np.int32), g.shape[0], g.shape[1], out):
+            raise ValueError("oracle: gene id out of range")
+        return out[:g.shape[0]]
+
+    def lpa_scored_batch(self, split, genes, score=0):
+        g = _genes(genes)
+        out = np.zeros(max(g.shape[0], 1), dtype=np.float64)
+        if self.lib.orc_lpa_scored_batch(split._ptr, score, g if g.size else np.zeros(1, np.int32), g.shape[0], g.shape[1], out):
+            raise ValueError("oracle: gene id out of range")
+        return out[:g.shape[0]]
+
+    def flip_unrank(self, n, gene_id):
+        a, b = C.c_int32(0), C.c_int32(0)
+        self.lib.orc_flip_unrank(n, gene_id, C.byref(a), C.byref(b))
+        return a.value, b.value
 
     def detect_communities(self, g):
         out = np.zeros(max(g.n, 1), dtype=np.int32)

@@ -639,6 +639,106 @@ int orc_lpa_batch(const orc_split* s, const int32_t* genes, int rows, int cols, 
     return rc;
 }
 
+/* ---- north_star extensions WITHOUT a reference implementation (PARITY UNPINNED) ----------------------------
+ * BASELINE.json's north_star names "CN/RA link scores" and "edge flips" for the link-prediction attack; the reference
+ * has only the RA score with edge-removal pools (link_prediction.cpp:55-69, fitness.cpp:87).  These twins state the
+ * semantics the CUDA path implements, by generalising the reference's own definitions:
+ *   CN score   = |N'(u) & N'(v)| on the perturbed train graph (the RA sum with every term 1 instead of 1/deg'(z));
+ *   flip gene  = a node pair (a < b): an edge of the train graph is removed, a non-edge is added, relative to the
+ *                UNPERTURBED graph, so a repeated gene is idempotent like the reference's set / clear
+ *                (gene_pool.cpp:49-67).  The canonical flip pool enumerates every pair a < b in lexicographic order
+ *                (the order gene_pool.cpp:81-87 uses for non-edges): gene id = a n - a (a + 1) / 2 + (b - a - 1).
+ * AUC exactly as link_prediction.cpp:82-96.  Nothing here is checked against reference outputs — there are none. */
+void orc_flip_unrank(int32_t n, int64_t id, int32_t* a_out, int32_t* b_out) {
+    int64_t a = 0;
+    /* largest a with first(a) = a n - a (a + 1) / 2 <= id */
+    int64_t lo = 0, hi = n - 2;
+    while (lo < hi) {
+        const int64_t mid = (lo + hi + 1) / 2;
+        if (mid * n - mid * (mid + 1) / 2 <= id) lo = mid; else hi = mid - 1;
+    }
+    a = lo;
+    *a_out = (int32_t)a;
+    *b_out = (int32_t)(id - (a * n - a * (a + 1) / 2) + a + 1);
+}
+
+static int base_has_edge(const orc_graph* g, int32_t a, int32_t b) {
+    int32_t lo = g->row_ptr[a], hi = g->row_ptr[a + 1];
+    while (lo < hi) { const int32_t mid = (lo + hi) / 2; if (g->col_idx[mid] < b) lo = mid + 1; else hi = mid; }
+    return lo < g->row_ptr[a + 1] && g->col_idx[lo] == b;
+}
+
+/* score_kind 0 = RA, 1 = CN.  pool_uv == NULL: the canonical all-pairs pool; else pool_size pairs. */
+int orc_lpa_flip_batch(const orc_split* s, int score_kind, const int32_t* pool_uv, int64_t pool_size, const int32_t* genes,
+                       int rows, int cols, double* out) {
+    const orc_graph* g = s->train;
+    const int32_t n = g->n;
+    if (!pool_uv) pool_size = (int64_t)n * (n - 1) / 2;
+    int32_t** nb = (int32_t**)calloc((size_t)n + 1, sizeof(int32_t*));
+    int32_t* len = (int32_t*)malloc(sizeof(int32_t) * ((size_t)n + 1));
+    int32_t* cap = (int32_t*)malloc(sizeof(int32_t) * ((size_t)n + 1));
+    double* ts = (double*)malloc(sizeof(double) * ((size_t)s->T + 1));
+    double* ps = (double*)malloc(sizeof(double) * ((size_t)s->P + 1));
+    int rc = 0;
+    for (int r = 0; r < rows && !rc; ++r) {
+        for (int32_t x = 0; x < n; ++x) {
+            len[x] = g->row_ptr[x + 1] - g->row_ptr[x];
+            cap[x] = len[x] + 4;
+            nb[x] = (int32_t*)malloc(sizeof(int32_t) * (size_t)cap[x]);
+            memcpy(nb[x], g->col_idx + g->row_ptr[x], sizeof(int32_t) * (size_t)len[x]);
+        }
+        for (int j = 0; j < cols && !rc; ++j) {
+            const int64_t id = genes[(size_t)r * cols + j];
+            if (id < 0 || id >= pool_size) { rc = 1; break; }
+            int32_t a, b;
+            if (pool_uv) { a = pool_uv[2 * id]; b = pool_uv[2 * id + 1]; if (a > b) { const int32_t t = a; a = b; b = t; } }
+            else orc_flip_unrank(n, id, &a, &b);
+            const int want = !base_has_edge(g, a, b); /* the state the flip leaves the pair in */
+            for (int side = 0; side < 2; ++side) {
+                const int32_t x = side ? b : a, y = side ? a : b;
+                int32_t pos = -1;
+                for (int32_t t = 0; t < len[x]; ++t) if (nb[x][t] == y) { pos = t; break; }
+                if (want && pos < 0) {
+                    if (len[x] == cap[x]) { cap[x] *= 2; nb[x] = (int32_t*)realloc(nb[x], sizeof(int32_t) * (size_t)cap[x]); }
+                    nb[x][len[x]++] = y;
+                } else if (!want && pos >= 0) {
+                    nb[x][pos] = nb[x][--len[x]];
+                }
+            }
+        }
+        if (!rc) {
+            for (int32_t x = 0; x < n; ++x) qsort(nb[x], (size_t)len[x], sizeof(int32_t), cmp_i32);
+            for (int32_t q = 0; q < s->T + s->P; ++q) {
+                const int32_t* uv = q < s->T ? s->test_uv + 2 * q : s->probe_uv + 2 * (q - s->T);
+                const int32_t u = uv[0], v = uv[1];
+                int32_t i = 0, jj = 0;
+                double score = 0.0;
+                while (i < len[u] && jj < len[v]) { /* common neighbours in ascending z (link_prediction.cpp:59-66) */
+                    const int32_t za = nb[u][i], zb = nb[v][jj];
+                    if (za < zb) ++i;
+                    else if (zb < za) ++jj;
+                    else { if (len[za] > 0) score += score_kind ? 1.0 : 1.0 / (double)len[za]; ++i; ++jj; }
+                }
+                if (q < s->T) ts[q] = score; else ps[q - s->T] = score;
+            }
+            out[r] = auc_of(ts, s->T, ps, s->P);
+        }
+        for (int32_t x = 0; x < n; ++x) free(nb[x]);
+    }
+    free(nb); free(len); free(cap); free(ts); free(ps);
+    return rc;
+}
+
+/* CN / RA with the reference's edge-REMOVAL pools (genes = edge ranks, as orc_lpa_batch) */
+int orc_lpa_scored_batch(const orc_split* s, int score_kind, const int32_t* genes, int rows, int cols, double* out) {
+    const orc_graph* g = s->train;
+    int32_t* uv = (int32_t*)malloc(sizeof(int32_t) * 2 * ((size_t)g->m + 1));
+    for (int64_t e = 0; e < g->m; ++e) { uv[2 * e] = g->pool_u[e]; uv[2 * e + 1] = g->pool_v[e]; }
+    const int rc = orc_lpa_flip_batch(s, score_kind, uv, g->m, genes, rows, cols, out); /* flipping an edge removes it */
+    free(uv);
+    return rc;
+}
+
 /* ============================================================ batch + threads */
 
 void orc_partition_rows(int pop_size, int pn, int32_t* lo_hi) { /* modes.cpp:506-516 */

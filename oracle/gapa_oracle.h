@@ -97,6 +97,11 @@ int orc_detect_communities(const orc_graph* g, int32_t* assignment);
 double orc_ra_score(const orc_graph* g, int32_t u, int32_t v); /* link_prediction.cpp:55-69 */
 
 /* ---- genetic operators (ga_ops.cpp) ---------------------------------------- */
+/* PARITY UNPINNED (no reference implementation): CN score and edge-flip pools for the link-prediction attack */
+void orc_flip_unrank(int32_t n, int64_t id, int32_t* a_out, int32_t* b_out);
+int orc_lpa_flip_batch(const orc_split* s, int score_kind, const int32_t* pool_uv, int64_t pool_size, const int32_t* genes,
+                       int rows, int cols, double* out);
+int orc_lpa_scored_batch(const orc_split* s, int score_kind, const int32_t* genes, int rows, int cols, double* out);
 void orc_make_mask(int rows, int cols, double rate, int role, uint64_t seed, uint64_t generation, uint8_t* out);
 void orc_make_mutation_indices(int rows, int cols, int pool_size, uint64_t seed, uint64_t generation, int32_t* out);
 int orc_init_population_block(int pool_size, int row_first, int row_count, int budget,

@@ -35,6 +35,12 @@ class PoolKind(enum.IntEnum):  # gene_pool.hpp:14
     EdgeRemoval = 0
     EdgeAddition = 1
     NodeRemoval = 2
+    EdgeFlip = 3  # NOT in the reference (north_star's "edge flips"; parity unpinned — include/gapa_cuda.h)
+
+
+class LinkScore(enum.IntEnum):
+    RA = 0  # link_prediction.cpp:55-69
+    CN = 1  # common neighbours: NOT in the reference (north_star's "CN/RA link scores"; parity unpinned)
 
 
 def _ptr(a: np.ndarray | None):
@@ -112,12 +118,13 @@ def planted_partition(blocks: int, block_size: int, p_in: float, p_out: float, s
 class GenePool:
     """gene_pool.hpp:32-52.  `u`, `v` hold the element of every gene id (v = -1 for nodes)."""
 
-    def __init__(self, kind: PoolKind, u, v=None, graph: Graph | None = None, canonical: bool = False):
+    def __init__(self, kind: PoolKind, u, v=None, graph: Graph | None = None, canonical: bool = False, count: int | None = None):
         self._kind = PoolKind(kind)
         self.u = _i32(u, 1)
         self.v = np.full_like(self.u, -1) if v is None else _i32(v, 1)
         self.graph = graph
         self.canonical = canonical  # exactly build_gene_pool(graph, kind): the device side rebuilds it itself
+        self._count = count         # canonical pools that are never enumerated on the host (all node pairs of EdgeFlip)
 
     def gene(self, gene_id: int) -> tuple[int, int]:
         return int(self.u[gene_id]), int(self.v[gene_id])
@@ -126,7 +133,7 @@ class GenePool:
         return self._kind
 
     def size(self) -> int:
-        return len(self.u)
+        return len(self.u) if self._count is None else self._count
 
 
 def build_gene_pool(g: Graph, kind: PoolKind) -> GenePool:  # gene_pool.cpp:69-96
@@ -138,6 +145,10 @@ def build_gene_pool(g: Graph, kind: PoolKind) -> GenePool:  # gene_pool.cpp:69-9
     if kind == PoolKind.EdgeRemoval:
         e = g.sorted_edges()
         return GenePool(kind, e[:, 0], e[:, 1], graph=g)
+    if kind == PoolKind.EdgeFlip:  # every node pair a < b, lexicographic; genes are unranked on the device
+        if g.n > 65536:
+            raise GapaCudaError(capi.E_INVALID, "gene pool: node pairs do not fit int32 gene ids")
+        return GenePool(kind, np.zeros(0, np.int32), np.zeros(0, np.int32), graph=g, canonical=True, count=g.n * (g.n - 1) // 2)
     e = np.ascontiguousarray(g.edges())
     count = C.c_int64(0)
     lib = capi.load()
@@ -190,7 +201,7 @@ class DeviceGraph:
         self.n, self.m = g.n, g.edge_count()
 
     def set_pool(self, pool: GenePool) -> None:
-        if pool.canonical and pool.kind() == PoolKind.EdgeAddition:  # 12.5 M pairs at n = 5000: built on the C side
+        if pool.canonical and pool.kind() in (PoolKind.EdgeAddition, PoolKind.EdgeFlip):  # 12.5 M pairs at n = 5000: built on the C side
             check(self.lib.gapa_cuda_pool_set(self.handle, int(pool.kind()), pool.size(), None, None))
         elif pool.kind() == PoolKind.NodeRemoval:
             check(self.lib.gapa_cuda_pool_set(self.handle, int(pool.kind()), pool.size(), _ptr(pool.u), None))
@@ -279,7 +290,7 @@ class ModularityAttackObjective(FitnessFunction):  # fitness.hpp:79-88
     task = TASK_CDA
 
     def __init__(self, graph: Graph, pool: GenePool, device: int = 0):
-        if pool.kind() == PoolKind.NodeRemoval:
+        if pool.kind() in (PoolKind.NodeRemoval, PoolKind.EdgeFlip):
             raise GapaCudaError(capi.E_INVALID, "ModularityAttackObjective: incompatible gene pool kind")
         super().__init__(DeviceGraph(graph, device), pool)
         self.dgraph.set_pool(pool)
@@ -288,11 +299,13 @@ class ModularityAttackObjective(FitnessFunction):  # fitness.hpp:79-88
 class LinkPredictionAttackObjective(FitnessFunction):  # fitness.hpp:90-101
     task = TASK_LPA
 
-    def __init__(self, split: LinkPredictionSplit, pool: GenePool, device: int = 0):
-        _require_kind(pool, PoolKind.EdgeRemoval, "LinkPredictionAttackObjective")
+    def __init__(self, split: LinkPredictionSplit, pool: GenePool, device: int = 0, score: LinkScore = LinkScore.RA):
+        if pool.kind() != PoolKind.EdgeFlip:  # the reference takes edge-removal pools only (fitness.cpp:87)
+            _require_kind(pool, PoolKind.EdgeRemoval, "LinkPredictionAttackObjective")
         super().__init__(DeviceGraph(split.train, device), pool)
         self.dgraph.set_pool(pool)
         self.dgraph.set_split(split)
+        check(self.dgraph.lib.gapa_cuda_lp_score_set(self.dgraph.handle, int(LinkScore(score))))
 
 
 def pc_fitness(graph: Graph, batch, pool: GenePool, device: int = 0) -> np.ndarray:  # fitness.hpp:38-39

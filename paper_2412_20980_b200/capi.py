@@ -54,6 +54,7 @@ SIGNATURES = {
     "gapa_cuda_pool_set": (C.c_int, [VP, C.c_int, C.c_int32, VP, VP]),
     "gapa_cuda_pool_info": (C.c_int, [VP, C.POINTER(C.c_int), C.POINTER(C.c_int32)]),
     "gapa_cuda_lp_split_set": (C.c_int, [VP, C.c_int32, VP, C.c_int32, VP]),
+    "gapa_cuda_lp_score_set": (C.c_int, [VP, C.c_int]),
     "gapa_cuda_eval_batch": (C.c_int, [VP, C.c_int, VP, C.c_int, C.c_int, VP]),
     "gapa_cuda_eval_batch_device": (C.c_int, [VP, C.c_int, VP, C.c_int, C.c_int, VP, VP]),
     "gapa_cuda_ga_init_device": (C.c_int, [C.c_int32, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_uint64, VP, VP]),

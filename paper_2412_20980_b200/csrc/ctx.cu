@@ -363,12 +363,64 @@ static int pool_set_addition(gapa_cuda_ctx* c, int32_t n_genes, const int32_t* u
     return GAPA_CUDA_OK;
 }
 
+// Edge-flip pools (not in the reference; include/gapa_cuda.h): every pair a < b (u == NULL: nothing is stored, genes are
+// unranked on the device), or the caller's pairs in d_add_u / d_add_v.
+static int pool_set_flip(gapa_cuda_ctx* c, int32_t n_genes, const int32_t* u, const int32_t* v) {
+    std::vector<int32_t> au, av;
+    const int64_t n = c->n;
+    if (!u) {
+        if (n < 2) return fail(GAPA_CUDA_E_INVALID, "gene pool: no node pairs to flip");
+        if (n > 65536) return fail(GAPA_CUDA_E_INVALID, "gene pool: %lld node pairs do not fit int32 gene ids", static_cast<long long>(n * (n - 1) / 2));
+        n_genes = static_cast<int32_t>(n * (n - 1) / 2);
+    } else {
+        if (!v) return fail(GAPA_CUDA_E_INVALID, "pool_set: edge pool needs both endpoint arrays");
+        if (n_genes < 0) return fail(GAPA_CUDA_E_INVALID, "pool_set: negative size");
+        au.resize(static_cast<size_t>(n_genes));
+        av.resize(static_cast<size_t>(n_genes));
+        std::vector<uint64_t> keys(static_cast<size_t>(n_genes));
+        for (int32_t i = 0; i < n_genes; ++i) {
+            int32_t a = u[i], b = v[i];
+            if (a < 0 || b < 0 || a >= c->n || b >= c->n || a == b)
+                return fail(GAPA_CUDA_E_INVALID, "pool_set: (%d, %d) is not a valid node pair", a, b);
+            if (a > b) std::swap(a, b);
+            au[static_cast<size_t>(i)] = a;
+            av[static_cast<size_t>(i)] = b;
+            keys[static_cast<size_t>(i)] = (static_cast<uint64_t>(a) << 32) | static_cast<uint32_t>(b);
+        }
+        std::sort(keys.begin(), keys.end());
+        if (std::adjacent_find(keys.begin(), keys.end()) != keys.end())
+            return fail(GAPA_CUDA_E_INVALID, "gene pool: duplicate element");  // gene_pool.cpp:40
+    }
+    GAPA_CUDA_TRY(cudaSetDevice(c->device));
+    for (int32_t** p : {&c->d_pool_map, &c->d_add_u, &c->d_add_v})
+        if (*p) { cudaFree(*p); *p = nullptr; }
+    if (u) {
+        GAPA_TRY(upload_i32(au, &c->d_add_u));
+        GAPA_TRY(upload_i32(av, &c->d_add_v));
+    }
+    c->pool_kind = GAPA_POOL_EDGE_FLIP;
+    c->pool_size = n_genes;
+    c->pool_identity = true;
+    c->flip_canonical = u == nullptr;
+    c->h_pool_map.clear();
+    ++c->pool_version;
+    return GAPA_CUDA_OK;
+}
+
+int gapa_cuda_lp_score_set(gapa_cuda_ctx* c, int score) {
+    if (!c) return fail(GAPA_CUDA_E_INVALID, "lp_score_set: null context");
+    if (score != GAPA_LP_SCORE_RA && score != GAPA_LP_SCORE_CN) return fail(GAPA_CUDA_E_INVALID, "lp_score_set: unknown score %d", score);
+    c->lp_score = score;
+    return GAPA_CUDA_OK;
+}
+
 int gapa_cuda_pool_set(gapa_cuda_ctx* c, int kind, int32_t n_genes, const int32_t* u, const int32_t* v) {
     if (!c) return fail(GAPA_CUDA_E_INVALID, "pool_set: null context");
-    if (kind != GAPA_POOL_NODE_REMOVAL && kind != GAPA_POOL_EDGE_REMOVAL && kind != GAPA_POOL_EDGE_ADDITION)
+    if (kind != GAPA_POOL_NODE_REMOVAL && kind != GAPA_POOL_EDGE_REMOVAL && kind != GAPA_POOL_EDGE_ADDITION && kind != GAPA_POOL_EDGE_FLIP)
         return fail(GAPA_CUDA_E_INVALID, "pool_set: unknown pool kind %d", kind);
     if (c->n == 0) return fail(GAPA_CUDA_E_INVALID, "gene pool: graph is empty");  // gene_pool.cpp:70
     if (kind == GAPA_POOL_EDGE_ADDITION) return pool_set_addition(c, n_genes, u, v);
+    if (kind == GAPA_POOL_EDGE_FLIP) return pool_set_flip(c, n_genes, u, v);
     const int32_t full = kind == GAPA_POOL_NODE_REMOVAL ? c->n : static_cast<int32_t>(c->m);
     if (!u) n_genes = full;
     if (n_genes < 0) return fail(GAPA_CUDA_E_INVALID, "pool_set: negative size");
@@ -452,10 +504,10 @@ static int check_task(const gapa_cuda_ctx* c, int task) {
                 return fail(GAPA_CUDA_E_INVALID, "%s: incompatible gene pool kind", task == GAPA_TASK_PC ? "pc_fitness" : "sixdst_fitness");
             return GAPA_CUDA_OK;
         case GAPA_TASK_CDA:
-            if (c->pool_kind == GAPA_POOL_NODE_REMOVAL) return fail(GAPA_CUDA_E_INVALID, "cda_fitness: incompatible gene pool kind");
+            if (c->pool_kind == GAPA_POOL_NODE_REMOVAL || c->pool_kind == GAPA_POOL_EDGE_FLIP) return fail(GAPA_CUDA_E_INVALID, "cda_fitness: incompatible gene pool kind");
             return GAPA_CUDA_OK;
         case GAPA_TASK_LPA:
-            if (c->pool_kind != GAPA_POOL_EDGE_REMOVAL) return fail(GAPA_CUDA_E_INVALID, "lpa_fitness: incompatible gene pool kind");
+            if (c->pool_kind != GAPA_POOL_EDGE_REMOVAL && c->pool_kind != GAPA_POOL_EDGE_FLIP) return fail(GAPA_CUDA_E_INVALID, "lpa_fitness: incompatible gene pool kind");
             if (c->T < 1) return fail(GAPA_CUDA_E_INVALID, "lpa_fitness: no link-prediction split set");
             return GAPA_CUDA_OK;
     }

@@ -192,6 +192,8 @@ struct gapa_cuda_ctx {
     // link-prediction split
     int32_t T = 0, P = 0;
     int32_t* d_pairs = nullptr;     // (T + P) x 2, test pairs first
+    int lp_score = 0;               // GAPA_LP_SCORE_RA / _CN
+    bool flip_canonical = false;    // EDGE_FLIP pool over all pairs: genes are unranked on the device (no table)
     // work stream + timing
     cudaStream_t stream = nullptr;
     cudaStream_t copy_stream = nullptr;          // H2D of the host-buffer entry point, overlapped with compute

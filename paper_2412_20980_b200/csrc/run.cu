@@ -438,10 +438,10 @@ extern "C" int gapa_cuda_ga_create(gapa_cuda_ctx* ctx, const gapa_cuda_run_param
             if (ctx->pool_kind != GAPA_POOL_NODE_REMOVAL) return fail(GAPA_CUDA_E_INVALID, "run: incompatible gene pool kind");
             break;
         case GAPA_TASK_CDA:
-            if (ctx->pool_kind == GAPA_POOL_NODE_REMOVAL) return fail(GAPA_CUDA_E_INVALID, "run: incompatible gene pool kind");
+            if (ctx->pool_kind == GAPA_POOL_NODE_REMOVAL || ctx->pool_kind == GAPA_POOL_EDGE_FLIP) return fail(GAPA_CUDA_E_INVALID, "run: incompatible gene pool kind");
             break;
         case GAPA_TASK_LPA:
-            if (ctx->pool_kind != GAPA_POOL_EDGE_REMOVAL || ctx->T < 1) return fail(GAPA_CUDA_E_INVALID, "run: link-prediction task needs an edge-removal pool and a split");
+            if ((ctx->pool_kind != GAPA_POOL_EDGE_REMOVAL && ctx->pool_kind != GAPA_POOL_EDGE_FLIP) || ctx->T < 1) return fail(GAPA_CUDA_E_INVALID, "run: link-prediction task needs an edge-removal pool and a split");
             break;
         default: return fail(GAPA_CUDA_E_INVALID, "unknown fitness task %d", p->task);
     }

@@ -68,7 +68,13 @@ __device__ __forceinline__ int32_t child_gene(const VariationParams& P, const in
     // streams are counter-based, so the unread draw is simply never computed.
     const uint64_t um = hash_tail(km + prod);
     const bool flip = P.pm_always || um < P.pm_limit;
+#if GAPA_VARY_ARITH & 4
+    // speculative: both candidate second draws, three independent chains per gene instead of two dependent ones
+    const uint64_t u2i = hash_tail(ki + prod), u2c = hash_tail((eda ? ks : kc) + prod);
+    const uint64_t u2 = flip ? u2i : u2c;
+#else
     const uint64_t u2 = hash_tail((flip ? ki : (eda ? ks : kc)) + prod);
+#endif
     const uint32_t bound = flip ? P.pool_size : P.s + P.pool_size;  // next_index bound (rng.hpp:28-31)
     const uint32_t idx = mulhi_u64_u32(u2, bound);
     if (flip) return static_cast<int32_t>(idx);

@@ -172,3 +172,62 @@ def test_lpa_probe_set_beyond_shared_memory_uses_the_grid(gp, oracle, cuda_devic
     os_ = oracle.split_build(oracle.graph_from_edges(g.n, g.edges()), 0.4, 4)
     batch = gp.init_population(pool.size(), 2, 2000, 8)
     assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(os_, 3, batch, threads=2))
+
+
+# ---- north_star extensions without a reference implementation: PARITY UNPINNED (twins in oracle/gapa_oracle.c) ----
+def test_cn_score_and_edge_flip_pools_match_their_cpu_twin(gp, oracle, cuda_device):
+    """CN link score and edge-flip pools for the link-prediction attack (BASELINE.json north_star; the reference has RA
+    with edge-removal pools only).  The CUDA path is held to the CPU twin that STATES the semantics — parity unpinned:
+    there is no reference output to pin either against.  What IS pinned: the twin, restricted to what the reference
+    has (RA, removals), equals the reference-pinned oracle bit for bit, and so does the CUDA flip path fed an
+    edges-only flip pool."""
+    rng = np.random.default_rng(8)
+    for n, p, frac in ((400, 0.03, 0.2), (1500, 0.006, 0.1), (90, 0.25, 0.3)):
+        g = gp.erdos_renyi(n, p, 3)
+        split = gp.build_lp_split(g, frac, 4)
+        og = oracle.graph_from_edges(g.n, g.edges())
+        os_ = oracle.split_build(og, frac, 4)
+        rem = gp.build_gene_pool(split.train, gp.PoolKind.EdgeRemoval)
+        k = max(4, rem.size() // 8)
+        rb = rng.integers(0, rem.size(), size=(9, k)).astype(np.int32)
+        # CN with the reference's removal pools
+        cn = gp.LinkPredictionAttackObjective(split, rem, score=gp.LinkScore.CN)
+        assert np.array_equal(cn.evaluate_batch(rb), oracle.lpa_scored_batch(os_, rb, 1))
+        assert np.array_equal(oracle.lpa_scored_batch(os_, rb, 0), oracle.eval_batch(os_, 3, rb))  # the twin == the pinned RA path
+        # the canonical flip pool: every node pair, genes unranked on the device
+        flip = gp.build_gene_pool(split.train, gp.PoolKind.EdgeFlip)
+        assert flip.size() == n * (n - 1) // 2
+        fb = rng.integers(0, flip.size(), size=(9, k)).astype(np.int32)
+        fb[:, :k // 2] = fb[:, k // 2:2 * (k // 2)]  # repeated genes are idempotent
+        edge_ids = np.array([a * n - a * (a + 1) // 2 + (b - a - 1) for a, b in zip(rem.u[:k // 3], rem.v[:k // 3])], np.int32)
+        fb[0, :len(edge_ids)] = edge_ids               # a row that also removes real edges
+        for score in (gp.LinkScore.RA, gp.LinkScore.CN):
+            obj = gp.LinkPredictionAttackObjective(split, flip, score=score)
+            assert np.array_equal(obj.evaluate_batch(fb), oracle.lpa_flip_batch(os_, fb, int(score))), (n, score)
+            assert obj.evaluate_one([]) == oracle.lpa_flip_batch(os_, np.zeros((1, 0), np.int32), int(score))[0]
+        # a custom flip pool that lists exactly the train edges behaves like the reference's removal pool (pinned)
+        edges_only = gp.GenePool(gp.PoolKind.EdgeFlip, rem.u, rem.v)
+        assert np.array_equal(gp.LinkPredictionAttackObjective(split, edges_only).evaluate_batch(rb), oracle.eval_batch(os_, 3, rb))
+        # ... and a mixed custom pool against the twin
+        pairs = np.stack([rng.integers(0, n, 300), rng.integers(0, n, 300)], 1)
+        pairs = np.unique(np.sort(pairs[pairs[:, 0] != pairs[:, 1]], axis=1), axis=0).astype(np.int32)
+        custom = gp.GenePool(gp.PoolKind.EdgeFlip, pairs[:, 0], pairs[:, 1])
+        cb = rng.integers(0, len(pairs), size=(5, 60)).astype(np.int32)
+        assert np.array_equal(gp.LinkPredictionAttackObjective(split, custom).evaluate_batch(cb), oracle.lpa_flip_batch(os_, cb, 0, pairs))
+    with pytest.raises(gp.capi.GapaCudaError):
+        gp.ModularityAttackObjective(g, gp.build_gene_pool(g, gp.PoolKind.EdgeFlip))  # flips are a link-prediction pool
+
+
+def test_edge_flip_ga_run_is_reproducible_and_consistent(gp, oracle, cuda_device):
+    """A GA over the flip pool with the CN score (the configs[2] wording): reproducible, monotone under elitism, and
+    the stored fitness of the final population equals the CPU twin's evaluation of it (parity unpinned)."""
+    g = gp.erdos_renyi(500, 0.03, 1)
+    split = gp.build_lp_split(g, 0.1, 1)
+    os_ = oracle.split_build(oracle.graph_from_edges(g.n, g.edges()), 0.1, 1)
+    pool = gp.build_gene_pool(split.train, gp.PoolKind.EdgeFlip)
+    obj = gp.LinkPredictionAttackObjective(split, pool, score=gp.LinkScore.CN)
+    params = gp.GAParams(pc=0.7, pm=0.1, pop_size=24, budget=40, iterations=6, seed=2, eda_interval=4)
+    a, b = gp.run_ga(params, pool, obj), gp.run_ga(params, pool, obj)
+    assert np.array_equal(a.history_best, b.history_best) and np.array_equal(a.final_population, b.final_population)
+    assert np.all(np.diff(a.history_best) <= 0)
+    assert np.array_equal(a.final_fitness, oracle.lpa_flip_batch(os_, a.final_population, 1))

@@ -48,3 +48,18 @@ def test_oracle_reproduces_the_reference_mask_matrices(oracle):
     for c in doc["indices"]:
         m = oracle.make_mutation_indices(c["rows"], c["cols"], c["pool"], c["seed"], c["generation"])
         assert sha(m) == c["sha"] and m[0][:16].tolist() == c["row0"]
+
+
+def test_unpinned_twins_reduce_to_the_pinned_oracle(oracle):
+    """CN / edge-flip twins (no reference implementation: parity unpinned).  Restricted to what the reference has —
+    RA score, edges removed — the twin must equal the reference-pinned LPA oracle; unranking covers the pair space."""
+    import numpy as np
+    g = oracle.graph_er(300, 0.04, 5)
+    sp = oracle.split_build(g, 0.2, 2)
+    pop = oracle.init_population(sp.train.m, 6, 30, 1)
+    assert np.array_equal(oracle.lpa_scored_batch(sp, pop, 0), oracle.eval_batch(sp, 3, pop))
+    n = 37
+    seen = [oracle.flip_unrank(n, i) for i in range(n * (n - 1) // 2)]
+    assert seen == [(a, b) for a in range(n) for b in range(a + 1, n)]
+    ranks = np.array([[a * 300 - a * (a + 1) // 2 + (b - a - 1) for a, b in zip(sp.train.pool_u[:20], sp.train.pool_v[:20])]], np.int32)
+    assert np.array_equal(oracle.lpa_flip_batch(sp, ranks, 0), oracle.eval_batch(sp, 3, np.arange(20, dtype=np.int32)[None, :]))

@@ -1,6 +1,6 @@
 #!/bin/bash
 # A/B of the hand-expanded integer arithmetic of the variation hash (variation.cuh) on the GPU box: C4 generation
-for v in 0 1 2 3; do
+for v in ${VARIANTS:-0 1 2 3 6}; do
   echo "== GAPA_VARY_ARITH=$v"
   GAPA_NVCC_EXTRA="-DGAPA_VARY_ARITH=$v" python paper_2412_20980_b200/build.py --force > /dev/null 2>&1 || { echo build failed; continue; }
   for i in 1 2; do python bench.py --steps 10 --warmup 3 --no-cpu-baseline 2>/dev/null | python -c "
