@@ -105,6 +105,7 @@ struct PcScratch {
     std::vector<int32_t> perm;  // original vertex -> internal vertex when relabelled
     bool configured = false;
     int overlap_clear = 1;
+    int vary_waves = 1;  // GAPA_PC_VARY_WAVES: CTAs of the fused variation kernel per resident slot (1 = persistent, large = one row per CTA)
 };
 
 // ---------------------------------------------------------------------------------
@@ -194,92 +195,238 @@ __global__ void __launch_bounds__(nt) k_pc_bitmask(GeneRows genes,
     if ((threadIdx.x & 31) == 0 && distinct) atomicAdd(&removed_count[row], distinct);
 }
 
-// Fused variation + mask build for the generation loop: the CTA BUILDS child row
-// `V.row_first + blockIdx.x` (crossover + mutate, or eda + mutate — variation.cuh), stores each gene
+// Fused variation + mask build for the generation loop: a CTA BUILDS child rows
+// `V.row_first + local` (crossover + mutate, or eda + mutate — variation.cuh), stores each gene
 // to the child's slot and sets it in the shared-memory bitmap in the same pass.  The hash arithmetic
 // of the variation (integer pipes) and the shared-memory atomics of the mask build (LSU) overlap
 // inside one kernel, and the 4 k bytes of the child row are never read back from HBM.
+//
+// Round 2: PERSISTENT and software-pipelined over the rows a CTA owns (local = blockIdx.x, + gridDim.x, ...).  With a
+// 125 KB bitmap only one CTA fits an SM, so nothing used to cover a CTA's prologue (three dependent slot-table loads,
+// zeroing the bitmap, the first parent loads) or its epilogue (bitmap write-out): ~5 of every 33 us at C4 with the
+// integer pipes idle.  Now (a) the slot tables, stream keys and first parent quads of the NEXT row are fetched under the
+// current row's hashing, (b) the write-out of a finished bitmap zeroes it in the same pass, (c) the first quad of the
+// next row is hashed between the two barriers of the epilogue — odd warps write out first and hash second, even warps the
+// other way round, so the LSU-bound write-out and the ALU-bound hashing overlap —, and (d) a last partial pass over
+// the quads that would occupy at most a quarter of the threads is done gene-wise by four times as many threads
+// (C4: 12,500 quads = 12 full passes of 1024 + 212 quads -> one pass of 848 single genes instead of a thirteenth pass).
+// Diagnostics for A/B timing only (results are WRONG with any bit set): 1 = no parent loads, 2 = no bitmap marks,
+// 4 = no child stores, 8 = no hashing.  tools/ab_vary_diag.sh
+#ifndef GAPA_VARY_DIAG
+#define GAPA_VARY_DIAG 0
+#endif
+__device__ __forceinline__ int4 vary_ld(const int4* p, int q) {
+#if GAPA_VARY_DIAG & 1
+    return make_int4(4 * q, 4 * q + 1, 4 * q + 2, 4 * q + 3);
+#else
+    return __ldcs(p + q);
+#endif
+}
+// L2 prefetch distance of the parent rows, in passes of nt quads (0 = off).  One CTA per SM keeps only 32 KB of parent
+// loads in flight in registers (two 16-byte loads per thread): 4.7 MB over the chip, ~3.6 TB/s at the latency of a
+// loaded HBM (measured: the kernel WITHOUT hashing, marks and stores still took 0.59 ms).  A bulk L2 prefetch by one thread
+// per pass holds no registers and no scoreboard: DRAM -> L2 runs GAPA_VARY_PREFETCH passes ahead, the register loads hit L2.
+// Measured (tools/ab_vary_prefetch.sh, C4): the loads-only kernel 0.571 -> 0.490 ms at distance 3, but the complete kernel
+// does not move (0.824 / 0.838 / 0.826 / 0.830 ms at distance 0 / 1 / 2 / 3; 0.905 at 4): with the hashing in place the
+// loads are already covered and the kernel is bound by the integer pipes.  Off by default.
+#ifndef GAPA_VARY_PREFETCH
+#define GAPA_VARY_PREFETCH 0
+#endif
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
+struct VaryRow {
+    const int32_t* mine;
+    const int32_t* theirs;
+    int32_t* keep_mine;
+    int32_t* keep_theirs;
+    int32_t* dst;
+    bool adopt_mine, adopt_theirs;
+};
+template <bool kPeer>
+__device__ __forceinline__ VaryRow vary_row(const VariationSpec& V, int k, int row, bool eda) {
+    VaryRow r;
+    const int slot_mine = V.parent[row], slot_theirs = eda ? slot_mine : V.parent[V.partner[row]];
+    r.adopt_mine = r.adopt_theirs = false;  // the row lives in another rank's HBM: read it there, keep a copy here
+    r.mine = kPeer ? parent_row(V, slot_mine, k, &r.adopt_mine) : V.pool + static_cast<size_t>(slot_mine) * k;
+    r.theirs = eda ? r.mine : (kPeer ? parent_row(V, slot_theirs, k, &r.adopt_theirs) : V.pool + static_cast<size_t>(slot_theirs) * k);
+    if (eda || slot_theirs == slot_mine) r.adopt_theirs = false;
+    r.keep_mine = V.pool + static_cast<size_t>(slot_mine) * k;
+    r.keep_theirs = V.pool + static_cast<size_t>(slot_theirs) * k;
+    r.dst = V.pool + static_cast<size_t>(V.child[row]) * k;
+    return r;
+}
+
 template <int nt, bool kPeer>  // kPeer: parent rows may live in another rank's HBM (variation.cuh: parent_row)
 __global__ void __launch_bounds__(nt) k_pc_bitmask_vary(VariationSpec V, int k, const int32_t* __restrict__ gene_map,
                                                                   int n, int words_per_row, word_t* __restrict__ removed,
-                                                                  int* removed_count, PcCounters* counters) {
+                                                                  int* removed_count, int rows) {
     __shared__ uint64_t keys[4];
-    const int local = blockIdx.x, row = V.row_first + local;
+    const int tid = threadIdx.x;
     const int words64 = (n + 63) >> 6;
-    for (int w = threadIdx.x; w < 2 * words64; w += nt) pc_smem_bits[w] = 0u;
-    if (threadIdx.x < 4)
-        keys[threadIdx.x] = stream_key(V.P.seed, V.P.generation, GAPA_ROLE_SELECT + threadIdx.x, static_cast<uint64_t>(row)) + kGolden;
-    __syncthreads();
-    const uint64_t ks = keys[0], kc = keys[1], km = keys[2], ki = keys[3];
+    word_t* bits64 = reinterpret_cast<word_t*>(pc_smem_bits);
     const bool eda = V.partner == nullptr;
-    const int slot_mine = V.parent[row], slot_theirs = eda ? slot_mine : V.parent[V.partner[row]];
-    bool adopt_mine = false, adopt_theirs = false;  // the row lives in another rank's HBM: read it there, keep a copy here
-    const int32_t* mine = kPeer ? parent_row(V, slot_mine, k, &adopt_mine) : V.pool + static_cast<size_t>(slot_mine) * k;
-    const int32_t* theirs = eda ? mine : (kPeer ? parent_row(V, slot_theirs, k, &adopt_theirs) : V.pool + static_cast<size_t>(slot_theirs) * k);
-    if (eda || slot_theirs == slot_mine) adopt_theirs = false;
-    int32_t* keep_mine = V.pool + static_cast<size_t>(slot_mine) * k;
-    int32_t* keep_theirs = V.pool + static_cast<size_t>(slot_theirs) * k;
-    int32_t* dst = V.pool + static_cast<size_t>(V.child[row]) * k;
+    // quads [0, quad_end) are hashed four genes per thread and pass, genes [4 quad_end, k) one per thread and pass
+    const int quads = (k & 3) == 0 ? k >> 2 : 0;
+    const int tail_quads = quads % nt;
+    const int quad_end = tail_quads * 4 > nt ? quads : quads - tail_quads;
+    const int tail0 = 4 * quad_end;
     // No range check here (one compare per gene costs this kernel 5 %): a mutated gene is inside the pool by construction
     // and an inherited one is as good as the parents — which this library's own operators wrote, or which
     // gapa_cuda_ga_slots_variation_eval_device validated when it first saw the caller's pool (ctx.cu).
     auto mark = [&](int gene) {
+#if GAPA_VARY_DIAG & 2
+        if (gene == -12345) pc_smem_bits[0] = 1;
+        return;
+#endif
         const int node = gene_map ? gene_map[gene] : gene;
         atomicOr(&pc_smem_bits[node >> 5], 1u << (node & 31));
     };
-    (void)counters;
-    if ((k & 3) == 0) {
-        const int4* mine4 = reinterpret_cast<const int4*>(mine);
-        const int4* theirs4 = reinterpret_cast<const int4*>(theirs);
-        int4* dst4 = reinterpret_cast<int4*>(dst);
-        const int quads = k >> 2;
-        int4 a_next = make_int4(0, 0, 0, 0), b_next = a_next;
-        if (threadIdx.x < quads) {
-            a_next = __ldcs(&mine4[threadIdx.x]);
-            b_next = eda ? a_next : __ldcs(&theirs4[threadIdx.x]);
-        }
-        for (int q = threadIdx.x; q < quads; q += nt) {
+    int local = blockIdx.x;
+    if (local >= rows) return;
+    // pass j of a row (thread 0): request the bytes that pass j + D will load — of this row, or of the next row's beginning
+    constexpr int kChunkGenes = 4 * nt;
+    const int chunks = quad_end > 0 ? (k + kChunkGenes - 1) / kChunkGenes : 0;
+    const bool use_prefetch = GAPA_VARY_PREFETCH > 0 && chunks >= GAPA_VARY_PREFETCH + 2;
+    auto prefetch_row = [&](const VaryRow& row, int chunk) {
+        const int g0 = chunk * kChunkGenes;
+        const uint32_t bytes = 4u * static_cast<uint32_t>(min(kChunkGenes, k - g0));
+        if (!(kPeer && row.adopt_mine)) prefetch_l2_bulk(row.mine + g0, bytes);
+        if (!eda && row.theirs != row.mine && !(kPeer && row.adopt_theirs)) prefetch_l2_bulk(row.theirs + g0, bytes);
+    };
+    auto prefetch_step = [&](const VaryRow& cur, const VaryRow* nxt, int j) {
+        if (!use_prefetch || tid != 0) return;
+        const int t = j + GAPA_VARY_PREFETCH;
+        if (t < chunks) prefetch_row(cur, t);
+        else if (nxt && t - chunks < chunks) prefetch_row(*nxt, t - chunks);
+    };
+    VaryRow R = vary_row<kPeer>(V, k, V.row_first + local, eda);
+    if (use_prefetch && tid == 0)
+        for (int c = 1; c < GAPA_VARY_PREFETCH; ++c) prefetch_row(R, c);
+    int4 a_next = make_int4(0, 0, 0, 0), b_next = a_next;
+    if (tid < quad_end) {
+        a_next = vary_ld(reinterpret_cast<const int4*>(R.mine), tid);
+        b_next = eda ? a_next : vary_ld(reinterpret_cast<const int4*>(R.theirs), tid);
+    }
+    for (int w = tid; w < words64; w += nt) bits64[w] = 0ull;
+    if (tid < 4) keys[tid] = stream_key(V.P.seed, V.P.generation, GAPA_ROLE_SELECT + tid, static_cast<uint64_t>(V.row_first + local)) + kGolden;
+    __syncthreads();
+    uint64_t ks = keys[0], kc = keys[1], km = keys[2], ki = keys[3];
+    __syncthreads();  // (once per CTA) nobody rewrites the keys before everybody has read them
+    int r0[4] = {0, 0, 0, 0};  // child genes of the row's first quad of this thread: hashed and stored, not yet marked
+    // first quad of a row: hash + store (the marks wait until the bitmap is known to be clear)
+    auto first_quad = [&](const VaryRow& row) {
+        prefetch_step(row, nullptr, 0);
+        if (tid < quad_end) {
             const int4 a = a_next, b = b_next;
-            if (q + nt < quads) {  // next quad's parents are in flight while this one is hashed
-                a_next = __ldcs(&mine4[q + nt]);
-                b_next = eda ? a_next : __ldcs(&theirs4[q + nt]);
-            }
-            if (kPeer && adopt_mine) reinterpret_cast<int4*>(keep_mine)[q] = a;
-            if (kPeer && adopt_theirs) reinterpret_cast<int4*>(keep_theirs)[q] = b;
+            if (kPeer && row.adopt_mine) reinterpret_cast<int4*>(row.keep_mine)[tid] = a;
+            if (kPeer && row.adopt_theirs) reinterpret_cast<int4*>(row.keep_theirs)[tid] = b;
             const int av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
-            int r[4];
-            uint64_t prod = kCounterStep * (static_cast<uint64_t>(q) * 4 + 1);
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                r[t] = child_gene(V.P, V.pool, V.parent, k, 4 * q + t, av[t], bv[t], eda, ks, kc, km, ki, prod);
-                prod += kCounterStep;
-            }
-            dst4[q] = make_int4(r[0], r[1], r[2], r[3]);
-#pragma unroll
-            for (int t = 0; t < 4; ++t) mark(r[t]);
+            for (int t = 0; t < 4; ++t)
+                r0[t] = child_gene(V.P, V.pool, V.parent, k, 4 * tid + t, av[t], bv[t], eda, ks, kc, km, ki, 4u * tid + t + 1u);
+            reinterpret_cast<int4*>(row.dst)[tid] = make_int4(r0[0], r0[1], r0[2], r0[3]);
         }
-    } else {
-        for (int j = threadIdx.x; j < k; j += nt) {
-            const int a = mine[j], b = theirs[j];
-            if (kPeer && adopt_mine) keep_mine[j] = a;
-            if (kPeer && adopt_theirs) keep_theirs[j] = b;
-            const int gsel = child_gene(V.P, V.pool, V.parent, k, j, a, b, eda, ks, kc, km, ki,
-                                        kCounterStep * (static_cast<uint64_t>(j) + 1));
-            dst[j] = gsel;
+    };
+    first_quad(R);
+    for (;;) {
+        const int next = local + static_cast<int>(gridDim.x);
+        const bool has_next = next < rows;
+        VaryRow N = R;
+        if (has_next) N = vary_row<kPeer>(V, k, V.row_first + next, eda);  // three dependent loads, hidden under this row's hashing
+        if (tid < quad_end) {
+#pragma unroll
+            for (int t = 0; t < 4; ++t) mark(r0[t]);
+        }
+        // gene-wise tail: its parents are requested now and used after the quad passes
+        int ta = 0, tb = 0;
+        const int tj = tail0 + tid;
+        if (tj < k) {
+            ta = R.mine[tj];
+            tb = eda ? ta : R.theirs[tj];
+        }
+        int pass = 0;  // passes of this row done so far (thread 0 counts them for the prefetch; its q always runs to quad_end)
+        {
+            const int4* mine4 = reinterpret_cast<const int4*>(R.mine);
+            const int4* theirs4 = reinterpret_cast<const int4*>(R.theirs);
+            int4* dst4 = reinterpret_cast<int4*>(R.dst);
+            int q = tid + nt;
+            if (q < quad_end) {
+                a_next = vary_ld(mine4, q);
+                b_next = eda ? a_next : vary_ld(theirs4, q);
+            }
+            for (; q < quad_end; q += nt) {
+                prefetch_step(R, has_next ? &N : nullptr, ++pass);
+                const int4 a = a_next, b = b_next;
+                if (q + nt < quad_end) {  // next quad's parents are in flight while this one is hashed
+                    a_next = vary_ld(mine4, q + nt);
+                    b_next = eda ? a_next : vary_ld(theirs4, q + nt);
+                }
+                if (kPeer && R.adopt_mine) reinterpret_cast<int4*>(R.keep_mine)[q] = a;
+                if (kPeer && R.adopt_theirs) reinterpret_cast<int4*>(R.keep_theirs)[q] = b;
+                const int av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
+                int r[4];
+#pragma unroll
+                for (int t = 0; t < 4; ++t) {
+#if GAPA_VARY_DIAG & 8
+                    r[t] = (av[t] ^ bv[t]) % 1000000;
+#else
+                    r[t] = child_gene(V.P, V.pool, V.parent, k, 4 * q + t, av[t], bv[t], eda, ks, kc, km, ki, 4u * q + t + 1u);
+#endif
+                }
+#if GAPA_VARY_DIAG & 4
+                if (r[0] == -12345)
+#endif
+                dst4[q] = make_int4(r[0], r[1], r[2], r[3]);
+#pragma unroll
+                for (int t = 0; t < 4; ++t) mark(r[t]);
+            }
+        }
+        while (++pass < chunks) prefetch_step(R, has_next ? &N : nullptr, pass);
+        for (int j = tj; j < k; j += nt) {
+            if (j != tj) {
+                ta = R.mine[j];
+                tb = eda ? ta : R.theirs[j];
+            }
+            if (kPeer && R.adopt_mine) R.keep_mine[j] = ta;
+            if (kPeer && R.adopt_theirs) R.keep_theirs[j] = tb;
+            const int gsel = child_gene(V.P, V.pool, V.parent, k, j, ta, tb, eda, ks, kc, km, ki, static_cast<uint32_t>(j) + 1u);
+            R.dst[j] = gsel;
             mark(gsel);
         }
+        // the next row's first quads are requested before the barrier and hashed between the barriers
+        if (has_next && tid < quad_end) {
+            a_next = vary_ld(reinterpret_cast<const int4*>(N.mine), tid);
+            b_next = eda ? a_next : vary_ld(reinterpret_cast<const int4*>(N.theirs), tid);
+        }
+        if (has_next && tid < 4)  // everybody has read the current keys (before the previous barrier)
+            keys[tid] = stream_key(V.P.seed, V.P.generation, GAPA_ROLE_SELECT + tid, static_cast<uint64_t>(V.row_first + next)) + kGolden;
+        __syncthreads();  // every mark of this row is in the bitmap; the next row's keys are visible
+        if (has_next) ks = keys[0], kc = keys[1], km = keys[2], ki = keys[3];
+        word_t* out = removed + static_cast<size_t>(local) * words_per_row;
+        int distinct = 0;
+        auto write_out = [&]() {  // write the bitmap, count it, clear it for the next row
+            for (int w = tid; w < words64; w += nt) {
+                const word_t x = bits64[w];
+                distinct += __popcll(x);
+                out[w] = x;
+                bits64[w] = 0ull;
+            }
+        };
+        if ((tid >> 5) & 1) {
+            write_out();
+            if (has_next) first_quad(N);
+        } else {
+            if (has_next) first_quad(N);
+            write_out();
+        }
+        for (int off = 16; off; off >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, off);
+        if ((tid & 31) == 0 && distinct) atomicAdd(&removed_count[local], distinct);
+        if (!has_next) break;
+        __syncthreads();  // the bitmap is clear everywhere
+        local = next;
+        R = N;
     }
-    __syncthreads();
-    const word_t* bits64 = reinterpret_cast<const word_t*>(pc_smem_bits);
-    word_t* out = removed + static_cast<size_t>(local) * words_per_row;
-    int distinct = 0;
-    for (int w = threadIdx.x; w < words64; w += nt) {
-        const word_t x = bits64[w];
-        distinct += __popcll(x);
-        out[w] = x;
-    }
-    for (int off = 16; off; off >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, off);
-    if ((threadIdx.x & 31) == 0 && distinct) atomicAdd(&removed_count[local], distinct);
 }
 
 // mask build, step 2: 64 individuals x 64 vertices bit transpose in registers.
@@ -1036,8 +1183,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_pc_small(GeneRows genes,
             const int a = mine[j], b = theirs[j];
             if (adopt_mine) keep_mine[j] = a;
             if (adopt_theirs) keep_theirs[j] = b;
-            const int gene = child_gene(V.P, V.pool, V.parent, cols, j, a, b, eda, ks, kc, km, ki,
-                                        kCounterStep * (static_cast<uint64_t>(j) + 1));
+            const int gene = child_gene(V.P, V.pool, V.parent, cols, j, a, b, eda, ks, kc, km, ki, static_cast<uint32_t>(j) + 1u);
             dst[j] = gene;
             const int node = pool_map ? pool_map[gene] : gene;
             atomicOr(&gone[node >> 5], 1u << (node & 31));
@@ -1305,14 +1451,23 @@ static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLan
         if (fused_mask) {
             VariationSpec pass = *job.vary;
             pass.row_first += row0;
+            // persistent: as many CTAs as are resident at once, each walks rows blockIdx.x, + grid, ...
+            auto vary_grid = [&](auto kernel, int nt) {
+                int per_sm = 0;
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, static_cast<size_t>(chunk_bits) / 8) != cudaSuccess || per_sm < 1)
+                    per_sm = 1;
+                return std::max(1, std::min(crows, sm * per_sm * s->vary_waves));
+            };
 #define GAPA_MASK_VARY(NT)                                                                                                       \
     do {                                                                                                                        \
         if (pass.bases)                                                                                                         \
-            GAPA_LAUNCH((k_pc_bitmask_vary<NT, true>), crows, NT, static_cast<size_t>(chunk_bits) / 8, stream, pass, cols,      \
-                        g_gene_map, n, words_per_row, set->removed.as<word_t>(), set->removed_count.as<int>(), counters);       \
+            GAPA_LAUNCH((k_pc_bitmask_vary<NT, true>), vary_grid((k_pc_bitmask_vary<NT, true>), NT), NT,                        \
+                        static_cast<size_t>(chunk_bits) / 8, stream, pass, cols,                                                \
+                        g_gene_map, n, words_per_row, set->removed.as<word_t>(), set->removed_count.as<int>(), crows);          \
         else                                                                                                                    \
-            GAPA_LAUNCH((k_pc_bitmask_vary<NT, false>), crows, NT, static_cast<size_t>(chunk_bits) / 8, stream, pass, cols,     \
-                        g_gene_map, n, words_per_row, set->removed.as<word_t>(), set->removed_count.as<int>(), counters);       \
+            GAPA_LAUNCH((k_pc_bitmask_vary<NT, false>), vary_grid((k_pc_bitmask_vary<NT, false>), NT), NT,                      \
+                        static_cast<size_t>(chunk_bits) / 8, stream, pass, cols,                                                \
+                        g_gene_map, n, words_per_row, set->removed.as<word_t>(), set->removed_count.as<int>(), crows);          \
     } while (0)
             switch (mask_threads) {
                 case 128: GAPA_MASK_VARY(128); break;
@@ -1534,6 +1689,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_vary<1024, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
         s->overlap_clear = env_int("GAPA_PC_OVERLAP_CLEAR", 1, 0, 1);
+        s->vary_waves = env_int("GAPA_PC_VARY_WAVES", 1, 1, 1 << 20);
         s->trace = env_int("GAPA_PC_TRACE", 0, 0, 1);  // one stderr line per sweep round
         s->prefix_first4 = env_int("GAPA_PC_PREFIX_FIRST4", 1, 0, 1);  // 0: scan whole (bounded) rows in the prefix closure
         GAPA_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&s->h_counters), sizeof(PcCounters) * kMaxLanes));

@@ -46,12 +46,8 @@ __device__ __forceinline__ void build_child_row(const VariationSpec& V, int k, i
             if (adopt_theirs) reinterpret_cast<int4*>(keep_theirs)[q] = b;
             const int av[4] = {a.x, a.y, a.z, a.w}, bv[4] = {b.x, b.y, b.z, b.w};
             int r[4];
-            uint64_t prod = kCounterStep * (static_cast<uint64_t>(q) * 4 + 1);
 #pragma unroll
-            for (int t = 0; t < 4; ++t) {
-                r[t] = child_gene(P, V.pool, V.parent, k, 4 * q + t, av[t], bv[t], eda, ks, kc, km, ki, prod);
-                prod += kCounterStep;
-            }
+            for (int t = 0; t < 4; ++t) r[t] = child_gene(P, V.pool, V.parent, k, 4 * q + t, av[t], bv[t], eda, ks, kc, km, ki, 4u * q + t + 1u);
             dst4[q] = make_int4(r[0], r[1], r[2], r[3]);
         }
     } else {
@@ -59,7 +55,7 @@ __device__ __forceinline__ void build_child_row(const VariationSpec& V, int k, i
             const int a = mine[j], b = theirs[j];
             if (adopt_mine) keep_mine[j] = a;
             if (adopt_theirs) keep_theirs[j] = b;
-            dst[j] = child_gene(P, V.pool, V.parent, k, j, a, b, eda, ks, kc, km, ki, kCounterStep * (static_cast<uint64_t>(j) + 1));
+            dst[j] = child_gene(P, V.pool, V.parent, k, j, a, b, eda, ks, kc, km, ki, static_cast<uint32_t>(j) + 1u);
         }
     }
 }
