@@ -43,12 +43,56 @@ static int upload_i32(const std::vector<int32_t>& h, int32_t** d) {
 // ---- pinned staging ring for pageable host buffers ---------------------------------------------------------
 // push(): wait until the slot's previous H2D has drained, copy the slice into the slot with all copy threads, enqueue
 // the H2D.  With kSlots slices in flight the host copy of slice i+1 overlaps the DMA of slice i.
+// Copy into the pinned slot with non-temporal stores: the destination is only ever read by the DMA engine, so pulling
+// its lines into the cache first (read-for-ownership) is a third of the memory traffic of the copy for nothing.
+// GAPA_PINNED_RING_COPY=memcpy keeps the C library's copy (tools/probe_pageable.py measures both).
+#if defined(__x86_64__)
+#include <immintrin.h>
+__attribute__((target("avx2"))) static void copy_nt_avx2(char* dst, const char* src, size_t len) {
+    size_t head = (32 - (reinterpret_cast<uintptr_t>(dst) & 31)) & 31;
+    if (head > len) head = len;
+    std::memcpy(dst, src, head);
+    dst += head; src += head; len -= head;
+    const size_t blocks = len / 128;
+    for (size_t i = 0; i < blocks; ++i) {
+        const __m256i a = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src));
+        const __m256i b = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + 32));
+        const __m256i c = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + 64));
+        const __m256i d = _mm256_loadu_si256(reinterpret_cast<const __m256i*>(src + 96));
+        _mm_prefetch(src + 1024, _MM_HINT_NTA);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst), a);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + 32), b);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + 64), c);
+        _mm256_stream_si256(reinterpret_cast<__m256i*>(dst + 96), d);
+        src += 128; dst += 128;
+    }
+    _mm_sfence();
+    std::memcpy(dst, src, len - blocks * 128);
+}
+#endif
+static void ring_copy(char* dst, const char* src, size_t len, bool nt) {
+#if defined(__x86_64__)
+    if (nt && len >= 4096 && __builtin_cpu_supports("avx2")) {
+        copy_nt_avx2(dst, src, len);
+        return;
+    }
+#endif
+    (void)nt;
+    std::memcpy(dst, src, len);
+}
+
 PinnedRing::PinnedRing() {
+    if (const char* raw = std::getenv("GAPA_PINNED_RING_COPY")) nt_copy = raw[0] != 'm';
+    if (const char* raw = std::getenv("GAPA_PINNED_SLICE_MB")) slice_bytes = static_cast<size_t>(std::max(1, std::min(256, std::atoi(raw)))) << 20;
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    // measured on the B200 box (16 host cores, tools/probe_pageable.py, 819 MB batch): 1 / 2 / 4 / 8 / 16 copy threads move
-    // 10.2 / 14.5 / 20.2 / 19.1 / 16.8 GB/s — the host's copy bandwidth saturates at four (plain cudaMemcpyAsync from
-    // pageable memory: 10.8 GB/s; the same batch from pinned memory: 54 GB/s, the PCIe rate)
-    int count = static_cast<int>(std::min(4u, std::max(1u, hw / 2)));
+    // measured on the B200 box (16 host cores, one socket; tools/probe_pageable.py, 819 MB batch = C4):
+    //   plain cudaMemcpyAsync from pageable memory 10.8 GB/s; the same batch from pinned memory 54 GB/s (the PCIe rate);
+    //   this ring with the C library's memcpy: 20.4 / 21.6 GB/s at 4 / 8 threads (round 1's default: 4 threads);
+    //   with non-temporal stores: 8.8 / 15.8 / 25.7 / 33.4 / 32.3 GB/s at 1 / 2 / 4 / 8 / 16 threads  -> 8 threads.
+    //   The host alone copies 73 GB/s (8 threads, no DMA running); copy + DMA together move 3 x 819 MB through its memory,
+    //   ~125 GB/s of the ~150 GB/s it has.  Pinning the caller's pages in place instead (cudaHostRegister per slice) manages
+    //   1.6 - 7.7 GB/s (tools/probe_hostregister.py) and is no alternative.
+    int count = static_cast<int>(std::min(8u, std::max(1u, hw / 2)));
     if (const char* raw = std::getenv("GAPA_PINNED_RING_THREADS")) count = std::max(1, std::min(64, std::atoi(raw)));
     for (int t = 0; t < count; ++t) workers.emplace_back([this, t, count] { work(t, count); });
 }
@@ -78,7 +122,7 @@ void PinnedRing::work(int index, int count) {
         lock.unlock();
         const size_t part = ((len + count - 1) / count + 4095) & ~size_t{4095};
         const size_t lo = std::min(len, part * index), hi = std::min(len, lo + part);
-        if (hi > lo) std::memcpy(dst + lo, src + lo, hi - lo);
+        if (hi > lo) ring_copy(dst + lo, src + lo, hi - lo, nt_copy);
         lock.lock();
         if (++finished == count) idle.notify_one();
     }
@@ -86,7 +130,7 @@ void PinnedRing::work(int index, int count) {
 int PinnedRing::push(void* dst_dev, const void* src_host, size_t len, cudaStream_t copy_stream) {
     const int slot = next++ % kSlots;
     if (!buf[slot]) {
-        GAPA_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&buf[slot]), kPinnedSliceBytes));
+        GAPA_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&buf[slot]), slice_bytes));
         GAPA_CUDA_TRY(cudaEventCreateWithFlags(&done[slot], cudaEventDisableTiming));
     } else {
         GAPA_CUDA_TRY(cudaEventSynchronize(done[slot]));
@@ -670,7 +714,7 @@ int gapa_cuda_eval_batch(gapa_cuda_ctx* c, int task, const int32_t* genes_host, 
         const char* src = reinterpret_cast<const char*>(genes_host);
         char* dst = reinterpret_cast<char*>(stage);
         while (ring_next < upto_bytes) {
-            const size_t len = std::min(kPinnedSliceBytes, upto_bytes - ring_next);
+            const size_t len = std::min(c->ring->slice_bytes, upto_bytes - ring_next);
             GAPA_TRY(c->ring->push(dst + ring_next, src + ring_next, len, c->copy_stream));
             ring_next += len;
         }

@@ -135,7 +135,7 @@ struct GeneRows {
 
 // ---- pinned staging ring (ctx.cu): pageable host buffers of the host-buffer entry point ----------------------
 static constexpr size_t kPinnedRingMinBytes = 8u << 20;   // smaller pageable batches take the plain copy
-static constexpr size_t kPinnedSliceBytes = 16u << 20;
+static constexpr size_t kPinnedSliceBytes = 16u << 20;  // default slice; GAPA_PINNED_SLICE_MB overrides (PinnedRing::slice_bytes)
 struct PinnedRing {
     static constexpr int kSlots = 4;
     char* buf[kSlots] = {};
@@ -147,6 +147,8 @@ struct PinnedRing {
     uint64_t generation = 0;
     int finished = 0;
     bool stop = false;
+    size_t slice_bytes = kPinnedSliceBytes;
+    bool nt_copy = true;  // non-temporal stores into the pinned slot (GAPA_PINNED_RING_COPY=memcpy: the C library's copy)
     const char* job_src = nullptr;
     char* job_dst = nullptr;
     size_t job_len = 0;

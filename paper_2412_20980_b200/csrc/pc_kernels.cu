@@ -66,6 +66,7 @@ struct PcCounters {
     int deferred;  // the recording sweep declined to run: too much is still unreached and the sweeps still progress
     unsigned int n_left;  // (vertex, super-group) pairs with unreached individuals after the last ordinary sweep
     int phase2_skipped;   // k_pc_final: more leftover entries than its single CTA takes on (host copy only)
+    int max_source;       // highest vertex id any individual's BFS source was marked at (-1 after a reset): see SweepArgs::fresh_from
 };
 
 // Scratch of ONE lane in flight (a lane = a contiguous block of whole 64-individual groups that goes through the
@@ -105,6 +106,7 @@ struct PcScratch {
     std::vector<int32_t> perm;  // original vertex -> internal vertex when relabelled
     bool configured = false;
     int overlap_clear = 1;
+    int fresh_skip = 0;  // GAPA_PC_FRESH_SKIP: the first sweep does not load records that are known to be clear (SweepArgs::fresh_from)
     int vary_waves = 1;  // GAPA_PC_VARY_WAVES: CTAs of the fused variation kernel per resident slot (1 = persistent, large = one row per CTA)
 };
 
@@ -488,7 +490,7 @@ __device__ __forceinline__ size_t word_index(int g, int n, int v) {
 // becomes the BFS source.  Any alive vertex would be correct; a hub makes
 // phase 1 cover the giant component.
 __global__ void __launch_bounds__(kThreads) k_pc_source(const int32_t* __restrict__ by_degree, int n, int rows,
-                                                        const word_t* __restrict__ alive, word_t* reached) {
+                                                        const word_t* __restrict__ alive, word_t* reached, PcCounters* counters) {
     const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
@@ -499,7 +501,10 @@ __global__ void __launch_bounds__(kThreads) k_pc_source(const int32_t* __restric
         const bool ok = v >= 0 && (alive[static_cast<size_t>(g) * n + v] & bit);
         const unsigned hit = __ballot_sync(0xffffffffu, ok);
         if (hit) {
-            if (lane == __ffs(hit) - 1) atomicOr(&reached[word_index(g, n, v)], bit);
+            if (lane == __ffs(hit) - 1) {
+                atomicOr(&reached[word_index(g, n, v)], bit);
+                if (v > counters->max_source) atomicMax(&counters->max_source, v);
+            }
             return;
         }
     }
@@ -633,7 +638,7 @@ __device__ __forceinline__ Rec gather_first4(const int32_t* __restrict__ row_ptr
 __global__ void __launch_bounds__(kPrefixThreads)
     k_pc_prefix(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx, const int4* __restrict__ nbr4,
                 int first4_only, int n, int prefix, const word_t* __restrict__ alive, Rec* reached, int pick_sources,
-                const int32_t* __restrict__ by_degree, int rows) {
+                const int32_t* __restrict__ by_degree, int rows, PcCounters* counters) {
     cg::cluster_group cluster = cg::this_cluster();
     // the cluster size is a launch attribute: kPrefixCluster CTAs while every super-group's cluster is
     // resident at once, fewer when there are more super-groups than that (waves of idle-heavy clusters cost more)
@@ -656,7 +661,10 @@ __global__ void __launch_bounds__(kPrefixThreads)
                 const bool ok = v >= 0 && (alive[static_cast<size_t>(g) * n + v] & bit);
                 const unsigned hit = __ballot_sync(0xffffffffu, ok);
                 if (hit) {
-                    if (lane == __ffs(hit) - 1) atomicOr(&reinterpret_cast<word_t*>(reached)[word_index(g, n, v)], bit);
+                    if (lane == __ffs(hit) - 1) {
+                        atomicOr(&reinterpret_cast<word_t*>(reached)[word_index(g, n, v)], bit);
+                        if (v > counters->max_source) atomicMax(&counters->max_source, v);
+                    }
                     break;
                 }
             }
@@ -748,6 +756,14 @@ struct SweepArgs {
     int record;        // ordinary sweep: append incomplete chunks to the list
     unsigned defer_above;  // recording sweep: with more (vertex, super-group) pairs left than this (and progress) sweep again instead
     int descending;        // ordinary sweep: blocks walk the vertex chunks from the highest id down
+    // FIRST sweep after the clear of the reached records: a vertex at or above this id (and above every BFS source,
+    // counters->max_source) cannot have been reached yet — only the prefix closure (ids below `prefix`), the source
+    // marks and a vertex's own sweep thread ever write its record — so its own record is known to be zero and is not
+    // loaded: 32 of the ~98 bytes a (vertex, super-group) pair reads.  n = every record is loaded.
+    // MEASURED SLOWER and off by default (GAPA_PC_FRESH_SKIP, tools/ab_fresh.sh): C4 sweep 0.445 -> 0.594 ms, n = 1e5
+    // 0.038 -> 0.070 ms.  The sequential read of a vertex's own record is what brings it into L2 for the threads that
+    // gather it as a NEIGHBOUR shortly afterwards; without it those gathers go to DRAM one random sector at a time.
+    int fresh_from;
 };
 
 template <bool FINAL>
@@ -772,7 +788,8 @@ __device__ __forceinline__ void sweep_chunk(const SweepArgs& A, int sg, int chun
     if (v < n) {
         const size_t base = static_cast<size_t>(sg) * n;
         const int4 first = __ldg(&A.nbr4[v]);  // in flight together with v's own records
-        Rec mine = load_rec(&reached[base + v]);
+        Rec mine{};
+        if (FINAL || v < A.fresh_from || v <= counters->max_source) mine = load_rec(&reached[base + v]);
         const Rec al = load_alive(alive, sg, n, v);
         Rec todo;
 #pragma unroll
@@ -1085,6 +1102,7 @@ __global__ void __launch_bounds__(kFinalThreads) k_pc_final(Phase2Args P, unsign
         c.phase2_skipped = skipped;
         *host_out = c;
         PcCounters zero{};
+        zero.max_source = -1;
         *counters = zero;
     }
     for (int i = tid; i < reset_slots; i += kFinalThreads) {
@@ -1127,6 +1145,7 @@ __global__ void k_pc_reset(int groups, int32_t* parent, int32_t* comp_size, int*
         counters->deferred = 0;
         counters->n_left = 0u;
         if (first) counters->range_error = 0;
+        if (first) counters->max_source = -1;
     }
 }
 
@@ -1518,7 +1537,7 @@ static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLan
             else GAPA_LAUNCH(k_pc_clear, clear_grid, kThreads, 0, stream, reinterpret_cast<Rec*>(reached), words / kPack);
         }
         if (prefix <= 0)
-            GAPA_LAUNCH(k_pc_source, (crows * 32 + kThreads - 1) / kThreads, kThreads, 0, stream, g_by_degree, n, crows, alive, reached);
+            GAPA_LAUNCH(k_pc_source, (crows * 32 + kThreads - 1) / kThreads, kThreads, 0, stream, g_by_degree, n, crows, alive, reached, counters);
 
         // ---- phase 1 ------------------------------------------------------------------
         const word_t* alive_rec = alive;
@@ -1538,7 +1557,7 @@ static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLan
             attr.val.clusterDim.x = csize; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
             cfg.attrs = &attr; cfg.numAttrs = 1;
             GAPA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pc_prefix, g_row_ptr, g_col_idx, static_cast<const int4*>(s->nbr4.as<int4>()),
-                                             s->prefix_first4, n, prefix, alive_rec, reached_rec, 1, g_by_degree, crows));
+                                             s->prefix_first4, n, prefix, alive_rec, reached_rec, 1, g_by_degree, crows, counters));
             g_launches.fetch_add(1, std::memory_order_relaxed);
         }
         const int il = std::min(std::max(1, s->interleave / kPack), sgroups);
@@ -1548,7 +1567,8 @@ static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLan
         A.row_ptr = g_row_ptr; A.col_idx = g_col_idx; A.nbr4 = s->nbr4.as<int4>(); A.n = n; A.sgroups = sgroups; A.interleave = il;
         A.alive = alive_rec; A.reached = reached_rec; A.unreached = set->unreached.as<int>();
         A.entry_of = set->entry_of.as<int32_t>(); A.slot0 = slot0; A.counters = counters;
-        A.incomplete = set->block_done.as<int2>(); A.record = 0; A.descending = 0;
+        A.incomplete = set->block_done.as<int2>(); A.record = 0; A.descending = 0; A.fresh_from = n;
+        bool first_sweep = s->fresh_skip != 0;  // the reached records were cleared for this lane: nothing above the prefix is set
         A.defer_above = static_cast<unsigned>(std::min<size_t>(0xfffffffeu, static_cast<size_t>(sgroups) * n / 16));  // 6 % of the pairs
         auto sweep = [&](bool final_pass, bool record, bool descending = false, bool local = false) -> int {
             A.descending = descending ? 1 : 0;
@@ -1557,6 +1577,8 @@ static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLan
             A.left_v = set->left_v.as<int32_t>(); A.left_g = set->left_g.as<int32_t>(); A.left_w = set->left_w.as<word_t>();
             A.left_base = set->left_base.as<int32_t>(); A.parent = set->parent.as<int32_t>(); A.comp_size = set->comp_size.as<int32_t>();
             A.record = record ? 1 : 0;
+            A.fresh_from = (!final_pass && !local && !descending && first_sweep) ? std::max(prefix, 0) : n;
+            if (!final_pass) first_sweep = false;
             if (final_pass) GAPA_LAUNCH(k_pc_record, sm * 4, kThreads, 0, stream, A);
             else if (local) GAPA_LAUNCH(k_pc_sweep_local, grid, kThreads, 0, stream, A);
             else GAPA_LAUNCH(k_pc_sweep, grid, kThreads, 0, stream, A);
@@ -1690,6 +1712,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_transpose, cudaFuncAttributeMaxDynamicSharedMemorySize, 80 * 1024));
         s->overlap_clear = env_int("GAPA_PC_OVERLAP_CLEAR", 1, 0, 1);
         s->vary_waves = env_int("GAPA_PC_VARY_WAVES", 1, 1, 1 << 20);
+        s->fresh_skip = env_int("GAPA_PC_FRESH_SKIP", 0, 0, 1);
         s->trace = env_int("GAPA_PC_TRACE", 0, 0, 1);  // one stderr line per sweep round
         s->prefix_first4 = env_int("GAPA_PC_PREFIX_FIRST4", 1, 0, 1);  // 0: scan whole (bounded) rows in the prefix closure
         GAPA_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&s->h_counters), sizeof(PcCounters) * kMaxLanes));

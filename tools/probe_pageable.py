@@ -22,9 +22,32 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     for _ in range(5):
         gp.capi.check(lib.gapa_cuda_eval_batch(obj.dgraph.handle, obj.task, genes.ctypes.data, rows, k, out.ctypes.data))
     dt = (time.perf_counter() - t0) / 5
-    print(f"{os.environ.get('GAPA_PINNED_RING', '1')} ring, threads {os.environ.get('GAPA_PINNED_RING_THREADS', 'default')}: "
+    print(f"{os.environ.get('GAPA_PINNED_RING', '1')} ring, slice {os.environ.get('GAPA_PINNED_SLICE_MB', '16')} MB, copy {os.environ.get('GAPA_PINNED_RING_COPY', 'nt')}, threads {os.environ.get('GAPA_PINNED_RING_THREADS', 'default')}: "
           f"{dt * 1e3:.1f} ms per call, {rows / dt:.0f} evals/s, {4 * rows * k / dt / 1e9:.1f} GB/s")
+elif len(sys.argv) > 1 and sys.argv[1] == "host":
+    # the host's own copy ceiling, no GPU involved: N threads memcpy an 819 MB pageable array into another buffer
+    import threading
+    import time
+    import numpy as np
+    src = np.random.default_rng(1).integers(0, 1 << 20, size=4096 * 50_000, dtype=np.int32)
+    dst = np.empty_like(src)
+    for nthreads in (1, 2, 4, 8, 16):
+        parts = np.array_split(np.arange(src.size), nthreads)
+        bounds = [(int(p[0]), int(p[-1]) + 1) for p in parts]
+        def run(lo, hi):
+            np.copyto(dst[lo:hi], src[lo:hi])
+        best = 1e9
+        for _ in range(3):
+            ts = [threading.Thread(target=run, args=b) for b in bounds]
+            t0 = time.perf_counter()
+            [t.start() for t in ts]
+            [t.join() for t in ts]
+            best = min(best, time.perf_counter() - t0)
+        print(f"host copy (numpy.copyto releases the GIL), {nthreads} threads: {src.nbytes / best / 1e9:.1f} GB/s")
 else:
-    for env in ({"GAPA_PINNED_RING": "0"}, {"GAPA_PINNED_RING_THREADS": "1"}, {"GAPA_PINNED_RING_THREADS": "2"}, {"GAPA_PINNED_RING_THREADS": "4"},
+    subprocess.call([sys.executable, __file__, "host"])
+    for env in ({"GAPA_PINNED_RING_COPY": "memcpy", "GAPA_PINNED_RING_THREADS": "4"}, {"GAPA_PINNED_RING_COPY": "memcpy", "GAPA_PINNED_RING_THREADS": "8"},
+                {"GAPA_PINNED_SLICE_MB": "4", "GAPA_PINNED_RING_THREADS": "8"}, {"GAPA_PINNED_SLICE_MB": "8", "GAPA_PINNED_RING_THREADS": "8"},
+                {"GAPA_PINNED_SLICE_MB": "32", "GAPA_PINNED_RING_THREADS": "8"}, {"GAPA_PINNED_SLICE_MB": "64", "GAPA_PINNED_RING_THREADS": "8"},{"GAPA_PINNED_RING": "0"}, {"GAPA_PINNED_RING_THREADS": "1"}, {"GAPA_PINNED_RING_THREADS": "2"}, {"GAPA_PINNED_RING_THREADS": "4"},
                 {"GAPA_PINNED_RING_THREADS": "8"}, {"GAPA_PINNED_RING_THREADS": "12"}, {"GAPA_PINNED_RING_THREADS": "16"}):
         subprocess.call([sys.executable, __file__, "child"], env={**os.environ, **env})
