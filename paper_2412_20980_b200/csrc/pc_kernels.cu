@@ -106,6 +106,7 @@ struct PcScratch {
     std::vector<int32_t> perm;  // original vertex -> internal vertex when relabelled
     bool configured = false;
     int overlap_clear = 1;
+    int sweep_prefetch = 32;  // GAPA_PC_SWEEP_PREFETCH: chunks ahead (SweepArgs::prefetch_chunks); C4 sweep 0.447 / 0.442 / 0.436 / 0.435 / 0.437 / 0.439 / 0.459 ms at 0 / 8 / 16 / 32 / 64 / 128 / 256 (tools/ab_sweep_prefetch.sh)
     int fresh_skip = 0;  // GAPA_PC_FRESH_SKIP: the first sweep does not load records that are known to be clear (SweepArgs::fresh_from)
     int vary_waves = 1;  // GAPA_PC_VARY_WAVES: CTAs of the fused variation kernel per resident slot (1 = persistent, large = one row per CTA)
 };
@@ -115,6 +116,11 @@ struct PcScratch {
 // shared-memory bitmap of one individual (one vertex chunk of it when n is large).
 // Duplicate genes are idempotent.  Bit c of 64-bit word w = vertex 64 w + c removed.
 extern __shared__ __align__(16) unsigned pc_smem_bits[];
+
+// DRAM -> L2 prefetch of a contiguous range by ONE thread (TMA bulk prefetch: no registers, no scoreboard held)
+__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
+}
 
 // eight consecutive int32 with one 256-bit streaming load (sm_100: LDG.E.EF.256); p must be 32-byte aligned
 __device__ __forceinline__ void load8_stream(const int32_t* p, int (&v)[8]) {
@@ -234,9 +240,6 @@ __device__ __forceinline__ int4 vary_ld(const int4* p, int q) {
 #ifndef GAPA_VARY_PREFETCH
 #define GAPA_VARY_PREFETCH 0
 #endif
-__device__ __forceinline__ void prefetch_l2_bulk(const void* p, uint32_t bytes) {
-    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(p), "r"(bytes) : "memory");
-}
 struct VaryRow {
     const int32_t* mine;
     const int32_t* theirs;
@@ -764,6 +767,10 @@ struct SweepArgs {
     // 0.038 -> 0.070 ms.  The sequential read of a vertex's own record is what brings it into L2 for the threads that
     // gather it as a NEIGHBOUR shortly afterwards; without it those gathers go to DRAM one random sector at a time.
     int fresh_from;
+    // ordinary sweep: thread 0 of a block requests the own-vertex data (reached records, alive words) of the chunk this
+    // many chunks AHEAD in block order into L2, so that the first, parallel stage of that block's loads — and the
+    // neighbour gathers that land in it — hit L2 instead of DRAM.  0 = off.
+    int prefetch_chunks;
 };
 
 template <bool FINAL>
@@ -860,8 +867,21 @@ __device__ __forceinline__ void sweep_chunk(const SweepArgs& A, int sg, int chun
 __global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep(SweepArgs A) {
     const int sg = blockIdx.y * A.interleave + (blockIdx.x % A.interleave);
     if (sg >= A.sgroups) return;
-    const int chunk = blockIdx.x / A.interleave;
-    sweep_chunk<false>(A, sg, A.descending ? (A.n + kThreads - 1) / kThreads - 1 - chunk : chunk, nullptr);
+    const int slot = blockIdx.x / A.interleave;
+    const int chunks = (A.n + kThreads - 1) / kThreads;
+    if (A.prefetch_chunks > 0 && threadIdx.x == 0 && slot + A.prefetch_chunks < chunks) {
+        const int ahead = slot + A.prefetch_chunks;
+        const int v0 = (A.descending ? chunks - 1 - ahead : ahead) * kThreads;
+        const int cnt = min(kThreads, A.n - v0);
+        prefetch_l2_bulk(A.reached + static_cast<size_t>(sg) * A.n + v0, static_cast<uint32_t>(cnt) * sizeof(Rec));
+#pragma unroll
+        for (int i = 0; i < kPack; ++i) {
+            const size_t first = (static_cast<size_t>(sg) * kPack + i) * A.n + v0;
+            const size_t lo = first & ~size_t{1};  // 16-byte aligned start
+            prefetch_l2_bulk(A.alive + lo, static_cast<uint32_t>(((first - lo + cnt + 1) & ~size_t{1}) * sizeof(word_t)));
+        }
+    }
+    sweep_chunk<false>(A, sg, A.descending ? chunks - 1 - slot : slot, nullptr);
 }
 
 // Sweep of the EXTRA rounds (one ordered sweep was not enough: no hub core, or a large diameter).  Inside a
@@ -1567,7 +1587,7 @@ static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLan
         A.row_ptr = g_row_ptr; A.col_idx = g_col_idx; A.nbr4 = s->nbr4.as<int4>(); A.n = n; A.sgroups = sgroups; A.interleave = il;
         A.alive = alive_rec; A.reached = reached_rec; A.unreached = set->unreached.as<int>();
         A.entry_of = set->entry_of.as<int32_t>(); A.slot0 = slot0; A.counters = counters;
-        A.incomplete = set->block_done.as<int2>(); A.record = 0; A.descending = 0; A.fresh_from = n;
+        A.incomplete = set->block_done.as<int2>(); A.record = 0; A.descending = 0; A.fresh_from = n; A.prefetch_chunks = s->sweep_prefetch;
         bool first_sweep = s->fresh_skip != 0;  // the reached records were cleared for this lane: nothing above the prefix is set
         A.defer_above = static_cast<unsigned>(std::min<size_t>(0xfffffffeu, static_cast<size_t>(sgroups) * n / 16));  // 6 % of the pairs
         auto sweep = [&](bool final_pass, bool record, bool descending = false, bool local = false) -> int {
@@ -1713,6 +1733,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         s->overlap_clear = env_int("GAPA_PC_OVERLAP_CLEAR", 1, 0, 1);
         s->vary_waves = env_int("GAPA_PC_VARY_WAVES", 1, 1, 1 << 20);
         s->fresh_skip = env_int("GAPA_PC_FRESH_SKIP", 0, 0, 1);
+        s->sweep_prefetch = env_int("GAPA_PC_SWEEP_PREFETCH", 32, 0, 1 << 20);
         s->trace = env_int("GAPA_PC_TRACE", 0, 0, 1);  // one stderr line per sweep round
         s->prefix_first4 = env_int("GAPA_PC_PREFIX_FIRST4", 1, 0, 1);  // 0: scan whole (bounded) rows in the prefix closure
         GAPA_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&s->h_counters), sizeof(PcCounters) * kMaxLanes));
