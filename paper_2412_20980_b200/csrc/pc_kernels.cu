@@ -262,8 +262,23 @@ __device__ __forceinline__ VaryRow vary_row(const VariationSpec& V, int k, int r
     return r;
 }
 
+// Resident CTAs the compiler must leave room for (it caps the registers accordingly).  The kernel wants 64 registers; with
+// CTAs of 640 threads that is ONE CTA per SM (41 K of the 64 K registers), with 48 registers it is two: n = 1e5 (k = 5000,
+// 640 threads) 0.157 -> 0.124 ms, generation 0.390 -> 0.355 ms (tools/ab_vary_regs.sh).  The full-size CTA (1024 threads,
+// 125 KB bitmap: one per SM whatever the registers) keeps its 64: capped at 56 or 48 it is 0.824 -> 0.882 / 0.885 ms.
+#ifndef GAPA_VARY_MAXREG
+#define GAPA_VARY_MAXREG 0
+#endif
+constexpr int vary_min_blocks(int nt) {
+    return nt >= 768 ? 1 : (65536 / (nt * 48) < 2048 / nt ? 65536 / (nt * 48) : 2048 / nt);
+}
+#if GAPA_VARY_MAXREG > 0
+#define GAPA_VARY_BOUNDS __maxnreg__(GAPA_VARY_MAXREG)
+#else
+#define GAPA_VARY_BOUNDS __launch_bounds__(nt, vary_min_blocks(nt))
+#endif
 template <int nt, bool kPeer>  // kPeer: parent rows may live in another rank's HBM (variation.cuh: parent_row)
-__global__ void __launch_bounds__(nt) k_pc_bitmask_vary(VariationSpec V, int k, const int32_t* __restrict__ gene_map,
+__global__ void GAPA_VARY_BOUNDS k_pc_bitmask_vary(VariationSpec V, int k, const int32_t* __restrict__ gene_map,
                                                                   int n, int words_per_row, word_t* __restrict__ removed,
                                                                   int* removed_count, int rows) {
     __shared__ uint64_t keys[4];
