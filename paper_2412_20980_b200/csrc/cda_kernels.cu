@@ -530,39 +530,45 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                 }
                 const bool is_nb = (pos[c] & kNbFlag) != 0;
                 if (is_nb || (c < a && best_id[c] == a)) {
-                    const int q = atomicAdd(&sh_work, 1);
-                    if (q < kCdaWorkQueue) work_queue[q] = i;
-                    else list_work(std::integral_constant<int, 1>{}, c, e, is_nb, a, b, da, 0, 1u << lane);
+                    // long lists are queued for a whole warp, short ones for a group of lanes — decided HERE, so that both
+                    // kinds are worked on at the same time after one barrier (round 1: long lists were found by the
+                    // groups and done in a phase of their own: 2 of a step's 9 us)
+                    bool queued = false;
+                    if (len[c] > kCdaShortList) {
+                        const int ql = atomicAdd(&sh_long, 1);
+                        if (ql < kCdaLongQueue) { long_queue[ql] = i; queued = true; }
+                    }
+                    if (!queued) {
+                        const int q = atomicAdd(&sh_work, 1);
+                        if (q < kCdaWorkQueue) work_queue[q] = i;
+                        else list_work(std::integral_constant<int, 1>{}, c, e, is_nb, a, b, da, 0, 1u << lane);
+                    }
                 }
             }
             __syncthreads();
             CDA_TICK(4);  // scan of list(a)
             const int n_work = min(sh_work, kCdaWorkQueue);
-            {
+            const int n_long = min(sh_long, kCdaLongQueue);
+            // warps [0, long_warps) take the long lists (one warp per list), the others the short ones (a group of lanes per
+            // list); at least a quarter of the warps stay with the short lists
+            const int long_warps = min(n_long, kCdaWarps - kCdaWarps / 4);
+            if (warp < long_warps) {
+                for (int q = warp; q < n_long; q += long_warps) {
+                    const int i = long_queue[q];
+                    const int c = e_id[ha + i];
+                    list_work(std::integral_constant<int, 32>{}, c, e_cnt[ha + i], (pos[c] & kNbFlag) != 0, a, b, da, lane, 0xffffffffu);
+                }
+            } else {
                 const int gl = lane % kCdaGroup;
                 const unsigned gmask = ((1u << kCdaGroup) - 1u) << (lane - gl);
-                for (int w0 = 0; w0 < n_work; w0 += kCdaThreads / kCdaGroup) {
-                    const int w = w0 + tid / kCdaGroup;
-                    if (w >= n_work) continue;  // uniform within a group
+                const int groups = (kCdaWarps - long_warps) * (32 / kCdaGroup);
+                for (int w = (warp - long_warps) * (32 / kCdaGroup) + lane / kCdaGroup; w < n_work; w += groups) {
                     const int i = work_queue[w];
                     const int c = e_id[ha + i];
-                    int queued = 0;
-                    if (gl == 0 && len[c] > kCdaShortList) {
-                        const int q = atomicAdd(&sh_long, 1);
-                        if (q < kCdaLongQueue) { long_queue[q] = i; queued = 1; }
-                    }
-                    if (__shfl_sync(gmask, queued, lane - gl)) continue;
                     list_work(std::integral_constant<int, kCdaGroup>{}, c, e_cnt[ha + i], (pos[c] & kNbFlag) != 0, a, b, da, gl, gmask);
                 }
             }
-            __syncthreads();
-            CDA_TICK(5);  // list work (short lists)
-            const int n_long = min(sh_long, kCdaLongQueue);
-            for (int q = warp; q < n_long; q += kCdaWarps) {
-                const int i = long_queue[q];
-                const int c = e_id[ha + i];
-                list_work(std::integral_constant<int, 32>{}, c, e_cnt[ha + i], (pos[c] & kNbFlag) != 0, a, b, da, lane, 0xffffffffu);
-            }
+            CDA_TICK(5);  // (unused: short and long lists are one phase now)
             best_a = cand_warp_best(best_a);
             if (lane == 0) warp_cand[warp] = best_a;
             __syncthreads();

@@ -1709,10 +1709,12 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         s->small_path = env_int("GAPA_PC_SMALL", 1, 0, 2);  // 0: never, 1: where it pays, 2: wherever it fits (tests)
         // individuals per lane.  Measured at C4 (tools/ab_lanes.sh): ONE lane of 4096 is as fast as two of 2048 (1.887 vs
         // 1.877 ms per generation) and every finer split is slower (1024 x 2 streams 1.97, 512 x 4 2.01, 256 x 8 2.33 ms):
-        // the mask kernel holds a whole SM (125 KB bitmap, 1024 threads x 46 registers), so a second lane's sweeps find no
-        // room beside it, and every lane pays the latency-bound prefix closure again.  Lanes therefore only split
-        // populations beyond 4096 (and whatever the scratch budget forces).
-        s->lane_rows = env_int("GAPA_PC_LANE_ROWS", 4096, 64, 1 << 20) / kBits * kBits;
+        // the mask kernel holds a whole SM (125 KB bitmap, 1024 threads x 64 registers), so a second lane's sweeps find no
+        // room beside it, and every lane pays the latency-bound prefix closure again.  Re-measured at population 16,384 with
+        // the persistent variation kernel (tools/ab_lanes_small.sh; lanes of 4096 / 8192 / one lane): n = 1e4 0.462 / 0.422 /
+        // 0.409 ms per generation, n = 1e5 1.162 / 1.126 / 1.148, n = 1e6 6.64 / 6.67 / 6.50 — lanes no longer pay
+        // anywhere, so a lane is 16,384 individuals (beyond that, and whatever the scratch budget forces, is split).
+        s->lane_rows = env_int("GAPA_PC_LANE_ROWS", 16384, 64, 1 << 20) / kBits * kBits;
         s->lane_streams = env_int("GAPA_PC_LANE_STREAMS", 2, 1, 8);  // lanes in flight
         s->spec_rounds = env_int("GAPA_PC_SPEC_ROUNDS", 1, 0, 6);    // 0: always the host-driven loop
         s->phase2_big = env_int("GAPA_PC_PHASE2_BIG", 0, 0, 1) != 0;  // 1: never resolve leftovers inside k_pc_final (tests)
