@@ -109,6 +109,44 @@ def test_cda_random_instances_exact(gp, oracle, cuda_device, monkeypatch, argmax
         assert np.array_equal(got, want), (trial, np.abs(got - want).max())
 
 
+def test_cda_tie_heavy_graphs_same_partition(gp, oracle, cuda_device):
+    """Regular graphs are all ties: many candidate pairs share one gain, so the reference's scan order (greatest gain, then
+    smallest a, then smallest b) decides every merge.  The detector's PARTITION — the merge order made visible — must equal
+    the oracle's, for the empty perturbation and for random removals."""
+    rng = np.random.default_rng(11)
+    graphs = []
+    for n in (8, 13, 30, 64):  # rings
+        graphs.append((n, [(i, (i + 1) % n) for i in range(n)]))
+    for w, h in ((3, 4), (5, 5), (6, 9)):  # grids
+        e = [(y * w + x, y * w + x + 1) for y in range(h) for x in range(w - 1)] + [(y * w + x, (y + 1) * w + x) for y in range(h - 1) for x in range(w)]
+        graphs.append((w * h, e))
+    for a, b in ((3, 3), (4, 6)):  # complete bipartite
+        graphs.append((a + b, [(i, a + j) for i in range(a) for j in range(b)]))
+    graphs.append((12, [(i, j) for i in range(6) for j in range(i + 1, 6)] + [(6 + i, 6 + j) for i in range(6) for j in range(i + 1, 6)] + [(0, 6)]))  # two cliques
+    for n, edges in graphs:
+        g = gp.Graph(n, np.asarray(edges, np.int32))
+        pool = _edge_pool(gp, g)
+        obj = gp.ModularityAttackObjective(g, pool)
+        og = oracle.graph_from_edges(g.n, g.edges())
+        for trial in range(6):
+            k = 0 if trial == 0 else int(rng.integers(1, max(2, pool.size() // 2)))
+            genes = rng.integers(0, pool.size(), size=k).astype(np.int32)
+            want_q = oracle.eval_batch(og, 2, genes.reshape(1, -1))
+            assert np.array_equal(obj.evaluate_batch(genes.reshape(1, -1)), want_q), (n, trial)
+            from paper_2412_20980_b200.experiment import _detect
+            owner = _detect(obj.dgraph, genes)
+            kept = [e for i, e in enumerate(g.sorted_edges().tolist()) if i not in set(genes.tolist())]
+            want_owner = oracle.detect_communities(oracle.graph_from_edges(g.n, np.asarray(kept, np.int32).reshape(-1, 2)))
+            assert np.array_equal(_first_appearance(owner), _first_appearance(want_owner)), (n, trial)
+
+
+def _first_appearance(owner):
+    seen, out = {}, []
+    for o in np.asarray(owner).tolist():
+        out.append(seen.setdefault(o, len(seen)))
+    return np.asarray(out)
+
+
 def test_cda_more_individuals_than_sms(gp, oracle, cuda_device):
     g = gp.planted_partition(4, 25, 0.3, 0.02, 7)
     pool = _edge_pool(gp, g)
