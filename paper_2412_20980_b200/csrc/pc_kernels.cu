@@ -106,6 +106,7 @@ struct PcScratch {
     std::vector<int32_t> perm;  // original vertex -> internal vertex when relabelled
     bool configured = false;
     int overlap_clear = 1;
+    int mask_rows = 1;  // GAPA_PC_MASK_ROWS: persistent pipelined mask kernel for whole bitmaps (0: one CTA per row and chunk)
     int sweep_prefetch = 32;  // GAPA_PC_SWEEP_PREFETCH: chunks ahead (SweepArgs::prefetch_chunks); C4 sweep 0.447 / 0.442 / 0.436 / 0.435 / 0.437 / 0.439 / 0.459 ms at 0 / 8 / 16 / 32 / 64 / 128 / 256 (tools/ab_sweep_prefetch.sh)
     int fresh_skip = 0;  // GAPA_PC_FRESH_SKIP: the first sweep does not load records that are known to be clear (SweepArgs::fresh_from)
     int vary_waves = 1;  // GAPA_PC_VARY_WAVES: CTAs of the fused variation kernel per resident slot (1 = persistent, large = one row per CTA)
@@ -201,6 +202,83 @@ __global__ void __launch_bounds__(nt) k_pc_bitmask(GeneRows genes,
     }
     for (int off = 16; off; off >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, off);
     if ((threadIdx.x & 31) == 0 && distinct) atomicAdd(&removed_count[row], distinct);
+}
+
+// The same mask build for whole bitmaps (chunks == 1), PERSISTENT and pipelined over the rows a CTA owns (round 2).  With one
+// CTA per SM (125 KB bitmap) nothing covered a CTA's zeroing, its first loads and its bitmap write-out: ~4 of the ~12 us a row
+// took at C4, with the loads that bound the kernel (64 KB in flight per SM) not running.  Here every thread keeps two 32-byte
+// gene loads in flight across row boundaries — the next row's first two passes are requested before the epilogue barrier —,
+// the write-out clears the bitmap in the same pass, and a last partial pass is done gene-wise by eight times as many threads.
+template <int nt>
+__global__ void __launch_bounds__(nt) k_pc_bitmask_rows(GeneRows genes, const int32_t* __restrict__ pool_map, int pool_size, int n,
+                                                                  int words_per_row, word_t* __restrict__ removed, int* removed_count,
+                                                                  PcCounters* counters, int rows) {
+    const int tid = threadIdx.x;
+    const int words64 = (n + 63) >> 6;
+    word_t* bits64 = reinterpret_cast<word_t*>(pc_smem_bits);
+    const int cols = genes.cols;
+    auto mark = [&](int gene) {
+        if (gene < 0 || gene >= pool_size) {
+            counters->range_error = 1;
+            return;
+        }
+        const int node = pool_map ? pool_map[gene] : gene;
+        atomicOr(&pc_smem_bits[node >> 5], 1u << (node & 31));
+    };
+    int local = blockIdx.x;
+    if (local >= rows) return;
+    const int32_t* g = genes.row(local);
+    // octs [0, oct_end) are marked eight genes per thread and pass (the last pass may be partial), genes from 8 oct_end on
+    // one per thread: a partial pass that would occupy at most an eighth of the threads is done gene-wise instead
+    const int octs = cols >> 3, left = octs % nt;
+    const int oct_end_aligned = left * 8 > nt ? octs : octs - left;
+    auto oct_end_of = [&](const int32_t* row) { return (reinterpret_cast<uintptr_t>(row) & 31) == 0 ? oct_end_aligned : 0; };
+    int oct_end = oct_end_of(g);
+    int a[8], b[8];
+    if (tid < oct_end) load8_stream(g + 8 * static_cast<size_t>(tid), a);
+    if (tid + nt < oct_end) load8_stream(g + 8 * static_cast<size_t>(tid + nt), b);
+    for (int w = tid; w < words64; w += nt) bits64[w] = 0ull;
+    __syncthreads();
+    for (;;) {
+        const int next = local + static_cast<int>(gridDim.x);
+        const bool has_next = next < rows;
+        const int32_t* gn = has_next ? genes.row(next) : g;
+        for (int o = tid; o < oct_end; o += 2 * nt) {
+            int t[8];
+#pragma unroll
+            for (int i = 0; i < 8; ++i) t[i] = a[i];
+            if (o + 2 * nt < oct_end) load8_stream(g + 8 * static_cast<size_t>(o + 2 * nt), a);
+#pragma unroll
+            for (int i = 0; i < 8; ++i) mark(t[i]);
+            if (o + nt < oct_end) {
+#pragma unroll
+                for (int i = 0; i < 8; ++i) t[i] = b[i];
+                if (o + 3 * nt < oct_end) load8_stream(g + 8 * static_cast<size_t>(o + 3 * nt), b);
+#pragma unroll
+                for (int i = 0; i < 8; ++i) mark(t[i]);
+            }
+        }
+        const int oct_end_next = has_next ? oct_end_of(gn) : 0;  // the next row's first two passes travel under this row's epilogue
+        if (tid < oct_end_next) load8_stream(gn + 8 * static_cast<size_t>(tid), a);
+        if (tid + nt < oct_end_next) load8_stream(gn + 8 * static_cast<size_t>(tid + nt), b);
+        for (int j = oct_end * 8 + tid; j < cols; j += nt) mark(g[j]);
+        __syncthreads();  // every mark of this row is in the bitmap
+        word_t* out = removed + static_cast<size_t>(local) * words_per_row;
+        int distinct = 0;
+        for (int w = tid; w < words64; w += nt) {
+            const word_t x = bits64[w];
+            distinct += __popcll(x);
+            out[w] = x;
+            bits64[w] = 0ull;
+        }
+        for (int off = 16; off; off >>= 1) distinct += __shfl_down_sync(0xffffffffu, distinct, off);
+        if ((tid & 31) == 0 && distinct) atomicAdd(&removed_count[local], distinct);
+        if (!has_next) break;
+        __syncthreads();  // the bitmap is clear everywhere
+        local = next;
+        g = gn;
+        oct_end = oct_end_next;
+    }
 }
 
 // Fused variation + mask build for the generation loop: a CTA BUILDS child rows
@@ -1540,10 +1618,23 @@ static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLan
                 pass.row_first += row0;
                 GAPA_TRY(launch_variation_spec(pass, cols, crows, stream));
             }
+            auto rows_grid = [&](auto kernel, int nt) {  // persistent: as many CTAs as are resident at once
+                int per_sm = 0;
+                if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, nt, static_cast<size_t>(chunk_bits) / 8) != cudaSuccess || per_sm < 1)
+                    per_sm = 1;
+                return std::max(1, std::min(crows, sm * per_sm));
+            };
 #define GAPA_MASK(NT)                                                                                                          \
-    GAPA_LAUNCH(k_pc_bitmask<NT>, dim3(chunks, crows), NT, static_cast<size_t>(chunk_bits) / 8, stream, job.genes.from(row0), \
-                g_gene_map, ctx->pool_size, n, chunk_bits, words_per_row, set->removed.as<word_t>(),                          \
-                set->removed_count.as<int>(), counters)
+    do {                                                                                                                      \
+        if (chunks == 1 && s->mask_rows)                                                                                      \
+            GAPA_LAUNCH(k_pc_bitmask_rows<NT>, rows_grid(k_pc_bitmask_rows<NT>, NT), NT, static_cast<size_t>(chunk_bits) / 8, \
+                        stream, job.genes.from(row0), g_gene_map, ctx->pool_size, n, words_per_row,                           \
+                        set->removed.as<word_t>(), set->removed_count.as<int>(), counters, crows);                            \
+        else                                                                                                                  \
+            GAPA_LAUNCH(k_pc_bitmask<NT>, dim3(chunks, crows), NT, static_cast<size_t>(chunk_bits) / 8, stream,               \
+                        job.genes.from(row0), g_gene_map, ctx->pool_size, n, chunk_bits, words_per_row,                       \
+                        set->removed.as<word_t>(), set->removed_count.as<int>(), counters);                                   \
+    } while (0)
             switch (mask_threads) {
                 case 128: GAPA_MASK(128); break;
                 case 256: GAPA_MASK(256); break;
@@ -1722,6 +1813,14 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small<kSmallThreadsFew>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_small<kSmallThreadsMany>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         // the shared-memory bitmap may use most of the SM (one CTA per individual)
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_rows<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_rows<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_rows<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_rows<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_rows<640>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_rows<768>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_rows<896>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask_rows<1024>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<128>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_bitmask<384>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
@@ -1750,6 +1849,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         s->overlap_clear = env_int("GAPA_PC_OVERLAP_CLEAR", 1, 0, 1);
         s->vary_waves = env_int("GAPA_PC_VARY_WAVES", 1, 1, 1 << 20);
         s->fresh_skip = env_int("GAPA_PC_FRESH_SKIP", 0, 0, 1);
+        s->mask_rows = env_int("GAPA_PC_MASK_ROWS", 1, 0, 1);
         s->sweep_prefetch = env_int("GAPA_PC_SWEEP_PREFETCH", 32, 0, 1 << 20);
         s->trace = env_int("GAPA_PC_TRACE", 0, 0, 1);  // one stderr line per sweep round
         s->prefix_first4 = env_int("GAPA_PC_PREFIX_FIRST4", 1, 0, 1);  // 0: scan whole (bounded) rows in the prefix closure
