@@ -209,8 +209,16 @@ __global__ void __launch_bounds__(nt) k_pc_bitmask(GeneRows genes,
 // took at C4, with the loads that bound the kernel (64 KB in flight per SM) not running.  Here every thread keeps two 32-byte
 // gene loads in flight across row boundaries — the next row's first two passes are requested before the epilogue barrier —,
 // the write-out clears the bitmap in the same pass, and a last partial pass is done gene-wise by eight times as many threads.
+#ifndef GAPA_MASK_MAXREG
+#define GAPA_MASK_MAXREG 0
+#endif
+#if GAPA_MASK_MAXREG > 0
+#define GAPA_MASK_BOUNDS __maxnreg__(GAPA_MASK_MAXREG)
+#else
+#define GAPA_MASK_BOUNDS __launch_bounds__(nt)
+#endif
 template <int nt>
-__global__ void __launch_bounds__(nt) k_pc_bitmask_rows(GeneRows genes, const int32_t* __restrict__ pool_map, int pool_size, int n,
+__global__ void GAPA_MASK_BOUNDS k_pc_bitmask_rows(GeneRows genes, const int32_t* __restrict__ pool_map, int pool_size, int n,
                                                                   int words_per_row, word_t* __restrict__ removed, int* removed_count,
                                                                   PcCounters* counters, int rows) {
     const int tid = threadIdx.x;
