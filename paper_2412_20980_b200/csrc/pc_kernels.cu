@@ -788,6 +788,10 @@ __global__ void __launch_bounds__(kPrefixThreads)
         for (int pass = 0; pass < 24; ++pass) {
             int any = 0;
             for (int v = lane_in_cluster; v < limit; v += kStride) {
+                // the four lowest neighbours are requested together with the vertex's own words (one dependent round
+                // trip to L2 less for every vertex that still has work)
+                int4 f = make_int4(-1, -1, -1, -1);
+                if (first4_only) f = __ldg(&nbr4[v]);
                 Rec mine = load_rec(&reached_sg[v]);
                 const Rec al = load_alive(alive, sg, n, v);
                 Rec todo;
@@ -803,7 +807,6 @@ __global__ void __launch_bounds__(kPrefixThreads)
                     // the four lowest neighbours only: in a hub-first order these are the vertex's links towards
                     // the core, which is where reachability arrives from; whatever this misses (a vertex reached
                     // only through younger neighbours) is left to the full sweeps and phase 2
-                    const int4 f = __ldg(&nbr4[v]);
                     const int u[4] = {f.x, f.y, f.z, f.w};
 #pragma unroll
                     for (int t = 0; t < 4; ++t)
