@@ -106,6 +106,12 @@ struct PcScratch {
     std::vector<int32_t> perm;  // original vertex -> internal vertex when relabelled
     bool configured = false;
     int overlap_clear = 1;
+    // Which algorithm this context's graph gets on the large path: -1 = not decided (the bit-sliced pipeline runs; the first
+    // evaluation that needs its host-driven loop times both on that batch), 0 = bit-sliced pipeline, 1 = per-individual
+    // union-find (k_pc_uf).  GAPA_PC_UF = 0 / 1 fixes it (tests run every case through both).
+    int uf_mode = -1;
+    DevBuf uf_scratch, uf_out;
+    cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
     int mask_rows = 1;  // GAPA_PC_MASK_ROWS: persistent pipelined mask kernel for whole bitmaps (0: one CTA per row and chunk)
     int sweep_prefetch = 32;  // GAPA_PC_SWEEP_PREFETCH: chunks ahead (SweepArgs::prefetch_chunks); C4 sweep 0.447 / 0.442 / 0.436 / 0.435 / 0.437 / 0.439 / 0.459 ms at 0 / 8 / 16 / 32 / 64 / 128 / 256 (tools/ab_sweep_prefetch.sh)
     int fresh_skip = 0;  // GAPA_PC_FRESH_SKIP: the first sweep does not load records that are known to be clear (SweepArgs::fresh_from)
@@ -1378,6 +1384,109 @@ __global__ void __launch_bounds__(kSmallThreads) k_pc_small(GeneRows genes,
     }
 }
 
+// The same per-individual algorithm for graphs of ANY size, with the union-find arrays in global memory (L2) instead of
+// shared memory (round 2).  The bit-sliced pipeline lives on graphs with a well-connected core: one ordered sweep reaches
+// nearly everything.  On high-diameter graphs (rings, grids, paths: reachability advances a few hops per sweep round, and
+// after removals there is no giant component, so most of the graph ends up in phase 2) it needed up to 48 host-driven rounds
+// — 5-7 ms for 512 individuals at n = 1e5.  A plain lock-free union-find per individual does not care about diameter.
+// PERSISTENT: CTA b walks rows b, b + grid, ... on its own scratch slot (parent[n], size[n]); the removed bitmap is in shared
+// memory.  pc_eval chooses between the two per context by MEASURING both the first time the pipeline needs the host-driven
+// loop (PcScratch::uf_mode).
+template <int kUfThreads>
+__global__ void __launch_bounds__(kUfThreads, 2048 / kUfThreads) k_pc_uf(GeneRows genes, const int32_t* __restrict__ pool_map, int pool_size, int n, int m,
+                                                      const int32_t* __restrict__ edge_u, const int32_t* __restrict__ edge_v, int task,
+                                                      double* __restrict__ out, PcCounters* counters, VariationSpec V, int have_vary,
+                                                      int rows, int32_t* scratch) {
+    extern __shared__ int32_t small_smem[];
+    __shared__ uint64_t vary_keys[4];
+    __shared__ long long warp_pairs[kUfThreads / 32];
+    __shared__ int warp_best[kUfThreads / 32];
+    const int tid = threadIdx.x;
+    int32_t* parent = scratch + static_cast<size_t>(blockIdx.x) * 2 * n;
+    int32_t* size = parent + n;
+    unsigned* gone = reinterpret_cast<unsigned*>(small_smem);
+    const int gone_words = (n + 31) >> 5;
+    const int cols = genes.cols;
+    for (int row = blockIdx.x; row < rows; row += gridDim.x) {
+        for (int w = tid; w < gone_words; w += kUfThreads) gone[w] = 0u;
+        for (int v = tid; v < n; v += kUfThreads) {
+            parent[v] = v;
+            size[v] = 0;
+        }
+        if (have_vary && tid < 4)
+            vary_keys[tid] = stream_key(V.P.seed, V.P.generation, GAPA_ROLE_SELECT + tid, static_cast<uint64_t>(V.row_first + row)) + kGolden;
+        __syncthreads();
+        if (have_vary) {
+            const int vrow = V.row_first + row;
+            const uint64_t ks = vary_keys[0], kc = vary_keys[1], km = vary_keys[2], ki = vary_keys[3];
+            const bool eda = V.partner == nullptr;
+            const int slot_mine = V.parent[vrow], slot_theirs = eda ? slot_mine : V.parent[V.partner[vrow]];
+            bool adopt_mine, adopt_theirs;
+            const int32_t* mine = parent_row(V, slot_mine, cols, &adopt_mine);
+            const int32_t* theirs = eda ? mine : parent_row(V, slot_theirs, cols, &adopt_theirs);
+            if (eda || slot_theirs == slot_mine) adopt_theirs = false;
+            int32_t* keep_mine = V.pool + static_cast<size_t>(slot_mine) * cols;
+            int32_t* keep_theirs = V.pool + static_cast<size_t>(slot_theirs) * cols;
+            int32_t* dst = V.pool + static_cast<size_t>(V.child[vrow]) * cols;
+            for (int j = tid; j < cols; j += kUfThreads) {
+                const int a = mine[j], b = theirs[j];
+                if (adopt_mine) keep_mine[j] = a;
+                if (adopt_theirs) keep_theirs[j] = b;
+                const int gene = child_gene(V.P, V.pool, V.parent, cols, j, a, b, eda, ks, kc, km, ki, static_cast<uint32_t>(j) + 1u);
+                dst[j] = gene;
+                const int node = pool_map ? pool_map[gene] : gene;
+                atomicOr(&gone[node >> 5], 1u << (node & 31));
+            }
+        } else {
+            const int32_t* g = genes.row(row);
+            for (int j = tid; j < cols; j += kUfThreads) {
+                const int gene = g[j];
+                if (gene < 0 || gene >= pool_size) {
+                    counters->range_error = 1;
+                    continue;
+                }
+                const int node = pool_map ? pool_map[gene] : gene;
+                atomicOr(&gone[node >> 5], 1u << (node & 31));
+            }
+        }
+        __syncthreads();
+        for (int e = tid; e < m; e += kUfThreads) {
+            const int u = edge_u[e], v = edge_v[e];
+            if (((gone[u >> 5] >> (u & 31)) | (gone[v >> 5] >> (v & 31))) & 1u) continue;
+            uf_union(parent, u, v);
+        }
+        __syncthreads();
+        for (int v = tid; v < n; v += kUfThreads)
+            if (!((gone[v >> 5] >> (v & 31)) & 1u)) atomicAdd(&size[uf_find(parent, v)], 1);
+        __syncthreads();
+        long long pairs = 0;
+        int best = n > 0 ? 1 : 0;  // removed vertices are singletons
+        for (int v = tid; v < n; v += kUfThreads) {
+            const long long sz = size[v];
+            pairs += sz * (sz - 1) / 2;
+            best = max(best, static_cast<int>(sz));
+        }
+        for (int off = 16; off; off >>= 1) {
+            pairs += __shfl_down_sync(0xffffffffu, pairs, off);
+            best = max(best, __shfl_down_sync(0xffffffffu, best, off));
+        }
+        if ((tid & 31) == 0) {
+            warp_pairs[tid >> 5] = pairs;
+            warp_best[tid >> 5] = best;
+        }
+        __syncthreads();
+        if (tid == 0) {
+            for (int w = 1; w < kUfThreads / 32; ++w) {
+                pairs += warp_pairs[w];
+                best = max(best, warp_best[w]);
+            }
+            out[row] = task == GAPA_TASK_PC ? static_cast<double>(pairs) : static_cast<double>(best);
+        }
+        __syncthreads();  // the next row reuses the bitmap, the scratch slot and the reduction buffers
+    }
+}
+static constexpr int kUfThreads = 512;
+
 // ---------------------------------------------------------------------------------
 static int ensure_phase2(PcSet* s, int groups, size_t entries, size_t slots) {
     const size_t giant = static_cast<size_t>(groups) * kBits;
@@ -1861,6 +1970,10 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         s->vary_waves = env_int("GAPA_PC_VARY_WAVES", 1, 1, 1 << 20);
         s->fresh_skip = env_int("GAPA_PC_FRESH_SKIP", 0, 0, 1);
         s->mask_rows = env_int("GAPA_PC_MASK_ROWS", 1, 0, 1);
+        s->uf_mode = env_int("GAPA_PC_UF", -1, -1, 1);
+        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_uf<kUfThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
+        GAPA_CUDA_TRY(cudaEventCreate(&s->ev_t0));
+        GAPA_CUDA_TRY(cudaEventCreate(&s->ev_t1));
         s->sweep_prefetch = env_int("GAPA_PC_SWEEP_PREFETCH", 32, 0, 1 << 20);
         s->trace = env_int("GAPA_PC_TRACE", 0, 0, 1);  // one stderr line per sweep round
         s->prefix_first4 = env_int("GAPA_PC_PREFIX_FIRST4", 1, 0, 1);  // 0: scan whole (bounded) rows in the prefix closure
@@ -1909,75 +2022,131 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
         return GAPA_CUDA_OK;
     }
-    GAPA_TRY(ensure_order(ctx, s));
-    // Lanes: whole 64-individual groups, at most lane_rows individuals and at most what the scratch budget allows
-    // (alive + reached + entry_of = 20 B per vertex and group, bitmaps 8 B per vertex and group) for every set in flight.
-    const size_t budget = static_cast<size_t>(env_int("GAPA_SCRATCH_MB", 24 * 1024, 1, 1 << 20)) << 20;
-    const int all_groups = (rows + kBits - 1) / kBits;
-    const int budget_groups = static_cast<int>(std::min<size_t>(1023, std::max<size_t>(1, budget / (28ull * std::max(n, 1)))));
-    int lane_groups = std::max(1, std::min(s->lane_rows / kBits, all_groups));
-    int streams = std::min(s->lane_streams, (all_groups + lane_groups - 1) / lane_groups);
-    if (lane_groups * streams > budget_groups) {
-        streams = std::max(1, std::min(streams, budget_groups / lane_groups));
-        lane_groups = std::max(1, std::min(lane_groups, budget_groups / streams));
-    }
-    if (lane_groups >= kPack) lane_groups = lane_groups / kPack * kPack;  // whole 32-byte records
-    const int total_lanes = (all_groups + lane_groups - 1) / lane_groups;
-    PcLaneJob job{task, genes, 0, 0, out_dev, trusted, vary};
-    auto lane_many = [&](int crows) {
-        const int sg = ((crows + kBits - 1) / kBits + kPack - 1) / kPack;
-        return static_cast<unsigned>(std::max<size_t>(8192, static_cast<size_t>(sg) * kPack * std::max(n, 1) / 512));
-    };
-    for (int wave0 = 0; wave0 < total_lanes; wave0 += kMaxLanes) {
-        const int lanes = std::min(kMaxLanes, total_lanes - wave0);
-        const bool forked = lanes > 1 && streams > 1;
-        const int spec = s->spec_rounds;
-        if (forked) {
-            GAPA_CUDA_TRY(cudaEventRecord(s->ev_fork, stream));
-            for (int j = 0; j < std::min(streams, lanes); ++j) {
-                PcSet* set = nullptr;
-                GAPA_TRY(get_set(j, &set));
-                GAPA_CUDA_TRY(cudaStreamWaitEvent(set->stream, s->ev_fork, 0));
-            }
-        }
-        std::vector<int> redo;
-        for (int i = 0; i < lanes; ++i) {
-            PcSet* set = nullptr;
-            GAPA_TRY(get_set(forked ? i % streams : 0, &set));
-            job.row0 = (wave0 + i) * lane_groups * kBits;
-            job.crows = std::min(rows - job.row0, lane_groups * kBits);
-            GAPA_TRY(pc_run_lane(ctx, s, set, job, forked ? set->stream : stream, spec, &s->h_counters[i], nullptr));
-        }
-        if (forked)
-            for (int j = 0; j < std::min(streams, lanes); ++j) {
-                GAPA_CUDA_TRY(cudaEventRecord(s->sets[j]->ev_done, s->sets[j]->stream));
-                GAPA_CUDA_TRY(cudaStreamWaitEvent(stream, s->sets[j]->ev_done, 0));
-            }
-        if (spec == 0) continue;  // the host-driven loop has already seen every lane's counters
-        // ONE host look at the counters per evaluation, after everything has been enqueued
+    // ---- per-individual union-find in global memory (k_pc_uf) -------------------------------------------------------
+    const bool uf_fits = n > 0 && sizeof(unsigned) * (static_cast<size_t>((n + 31) >> 5) + 1) <= 200 * 1024;  // removed bitmap in shared memory
+    auto launch_uf = [&](GeneRows genes, const VariationSpec* vary, double* out_dev, bool trusted) -> int {
+        const size_t smem = sizeof(unsigned) * (static_cast<size_t>((n + 31) >> 5) + 1);
+        int per_sm = 0;
+        if (cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pc_uf<kUfThreads>, kUfThreads, smem) != cudaSuccess || per_sm < 1) per_sm = 1;
+        const int grid = std::max(1, std::min(rows, sm * per_sm));
+        GAPA_TRY(s->uf_scratch.ensure(sizeof(int32_t) * 2 * static_cast<size_t>(n) * grid));
+        PcSet* set0 = nullptr;
+        GAPA_TRY(get_set(0, &set0));
+        GAPA_TRY(set0->counters.ensure(sizeof(PcCounters)));
+        PcCounters* counters = set0->counters.as<PcCounters>();
+        if (!trusted) GAPA_CUDA_TRY(cudaMemsetAsync(counters, 0, sizeof(PcCounters), stream));
+        const bool fuse = vary && cols > 0;
+        if (vary && !fuse) GAPA_TRY(launch_variation_spec(*vary, cols, rows, stream));
+        GAPA_LAUNCH(k_pc_uf<kUfThreads>, grid, kUfThreads, smem, stream, genes, ctx->pool_identity ? nullptr : ctx->d_pool_map,
+                    ctx->pool_size, n, static_cast<int>(ctx->m), ctx->d_edge_u, ctx->d_edge_v, task, out_dev, counters,
+                    fuse ? *vary : VariationSpec{}, fuse ? 1 : 0, rows, s->uf_scratch.as<int32_t>());
+        if (trusted) return GAPA_CUDA_OK;
+        PcCounters h{};
+        GAPA_CUDA_TRY(cudaMemcpyAsync(&h, counters, sizeof(h), cudaMemcpyDeviceToHost, stream));
         GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
-        for (int i = 0; i < lanes; ++i) {
-            const PcCounters& h = s->h_counters[i];
-            const int crows = std::min(rows - (wave0 + i) * lane_groups * kBits, lane_groups * kBits);
-            if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
-            if (s->trace)
-                std::fprintf(stderr, "pc_eval lane %d (speculative, %d round(s)): entries %u slots %u overflow %d changed %d incomplete %u deferred %d\n",
-                             wave0 + i, spec, h.n_entries, h.n_slots, h.overflow, h.changed, h.n_incomplete, h.deferred);
-            if (h.phase2_skipped) s->phase2_big = true;
-            if (h.overflow || h.deferred || h.phase2_skipped || (h.changed && h.n_entries > lane_many(crows))) redo.push_back(i);
+        if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
+        // the clean-slot bookkeeping of the pipeline's speculative schedule does not survive a memset of the counters
+        set0->clean_slots = 0;
+        return GAPA_CUDA_OK;
+    };
+    if (uf_fits && s->uf_mode == 1) return launch_uf(genes, vary, out_dev, trusted);
+
+    // ---- the bit-sliced pipeline ------------------------------------------------------------------------------------
+    auto pipeline = [&](GeneRows genes, const VariationSpec* vary, double* out_dev, bool trusted, bool* slow) -> int {
+        GAPA_TRY(ensure_order(ctx, s));
+        // Lanes: whole 64-individual groups, at most lane_rows individuals and at most what the scratch budget allows
+        // (alive + reached + entry_of = 20 B per vertex and group, bitmaps 8 B per vertex and group) for every set in flight.
+        const size_t budget = static_cast<size_t>(env_int("GAPA_SCRATCH_MB", 24 * 1024, 1, 1 << 20)) << 20;
+        const int all_groups = (rows + kBits - 1) / kBits;
+        const int budget_groups = static_cast<int>(std::min<size_t>(1023, std::max<size_t>(1, budget / (28ull * std::max(n, 1)))));
+        int lane_groups = std::max(1, std::min(s->lane_rows / kBits, all_groups));
+        int streams = std::min(s->lane_streams, (all_groups + lane_groups - 1) / lane_groups);
+        if (lane_groups * streams > budget_groups) {
+            streams = std::max(1, std::min(streams, budget_groups / lane_groups));
+            lane_groups = std::max(1, std::min(lane_groups, budget_groups / streams));
         }
-        // Lanes whose speculative schedule was not enough are redone with the host-driven loop (a later lane may have
-        // reused the set's buffers, so they start over; variation is a pure function of the parents, so rebuilding the
-        // children writes the same genes).  What the loop needed becomes the next evaluations' speculative schedule.
-        for (int i : redo) {
-            PcSet* set = nullptr;
-            GAPA_TRY(get_set(0, &set));
-            job.row0 = (wave0 + i) * lane_groups * kBits;
-            job.crows = std::min(rows - job.row0, lane_groups * kBits);
-            int used = 0;
-            GAPA_TRY(pc_run_lane(ctx, s, set, job, stream, 0, nullptr, &used));
-            s->spec_rounds = used <= 6 ? std::max(s->spec_rounds, used) : 0;
+        if (lane_groups >= kPack) lane_groups = lane_groups / kPack * kPack;  // whole 32-byte records
+        const int total_lanes = (all_groups + lane_groups - 1) / lane_groups;
+        PcLaneJob job{task, genes, 0, 0, out_dev, trusted, vary};
+        auto lane_many = [&](int crows) {
+            const int sg = ((crows + kBits - 1) / kBits + kPack - 1) / kPack;
+            return static_cast<unsigned>(std::max<size_t>(8192, static_cast<size_t>(sg) * kPack * std::max(n, 1) / 512));
+        };
+        for (int wave0 = 0; wave0 < total_lanes; wave0 += kMaxLanes) {
+            const int lanes = std::min(kMaxLanes, total_lanes - wave0);
+            const bool forked = lanes > 1 && streams > 1;
+            const int spec = s->spec_rounds;
+            if (forked) {
+                GAPA_CUDA_TRY(cudaEventRecord(s->ev_fork, stream));
+                for (int j = 0; j < std::min(streams, lanes); ++j) {
+                    PcSet* set = nullptr;
+                    GAPA_TRY(get_set(j, &set));
+                    GAPA_CUDA_TRY(cudaStreamWaitEvent(set->stream, s->ev_fork, 0));
+                }
+            }
+            std::vector<int> redo;
+            for (int i = 0; i < lanes; ++i) {
+                PcSet* set = nullptr;
+                GAPA_TRY(get_set(forked ? i % streams : 0, &set));
+                job.row0 = (wave0 + i) * lane_groups * kBits;
+                job.crows = std::min(rows - job.row0, lane_groups * kBits);
+                GAPA_TRY(pc_run_lane(ctx, s, set, job, forked ? set->stream : stream, spec, &s->h_counters[i], nullptr));
+            }
+            if (forked)
+                for (int j = 0; j < std::min(streams, lanes); ++j) {
+                    GAPA_CUDA_TRY(cudaEventRecord(s->sets[j]->ev_done, s->sets[j]->stream));
+                    GAPA_CUDA_TRY(cudaStreamWaitEvent(stream, s->sets[j]->ev_done, 0));
+                }
+            if (spec == 0) continue;  // the host-driven loop has already seen every lane's counters
+            // ONE host look at the counters per evaluation, after everything has been enqueued
+            GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
+            for (int i = 0; i < lanes; ++i) {
+                const PcCounters& h = s->h_counters[i];
+                const int crows = std::min(rows - (wave0 + i) * lane_groups * kBits, lane_groups * kBits);
+                if (h.range_error) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
+                if (s->trace)
+                    std::fprintf(stderr, "pc_eval lane %d (speculative, %d round(s)): entries %u slots %u overflow %d changed %d incomplete %u deferred %d\n",
+                                 wave0 + i, spec, h.n_entries, h.n_slots, h.overflow, h.changed, h.n_incomplete, h.deferred);
+                if (h.phase2_skipped) s->phase2_big = true;
+                if (h.overflow || h.deferred || h.phase2_skipped || (h.changed && h.n_entries > lane_many(crows))) redo.push_back(i);
+            }
+            // Lanes whose speculative schedule was not enough are redone with the host-driven loop (a later lane may have
+            // reused the set's buffers, so they start over; variation is a pure function of the parents, so rebuilding the
+            // children writes the same genes).  What the loop needed becomes the next evaluations' speculative schedule.
+            if (!redo.empty()) *slow = true;
+            for (int i : redo) {
+                PcSet* set = nullptr;
+                GAPA_TRY(get_set(0, &set));
+                job.row0 = (wave0 + i) * lane_groups * kBits;
+                job.crows = std::min(rows - job.row0, lane_groups * kBits);
+                int used = 0;
+                GAPA_TRY(pc_run_lane(ctx, s, set, job, stream, 0, nullptr, &used));
+                s->spec_rounds = used <= 6 ? std::max(s->spec_rounds, used) : 0;
+            }
         }
+        return GAPA_CUDA_OK;
+    };
+    bool slow = false;
+    GAPA_TRY(pipeline(genes, vary, out_dev, trusted, &slow));
+    if (slow && uf_fits && s->uf_mode < 0 && rows >= 64) {
+        // This graph made the pipeline fall back to its host-driven loop (no hub core, or a large diameter).  Decide ONCE,
+        // by measurement on this very batch (its children exist by now, so no variation is repeated): the pipeline as it
+        // will run from now on (it has just learned its schedule) against the per-individual union-find.
+        GAPA_TRY(s->uf_out.ensure(sizeof(double) * static_cast<size_t>(rows)));
+        float t_pipe = 0.f, t_uf = 0.f;
+        bool again = false;
+        GAPA_CUDA_TRY(cudaEventRecord(s->ev_t0, stream));
+        GAPA_TRY(pipeline(genes, nullptr, s->uf_out.as<double>(), true, &again));
+        GAPA_CUDA_TRY(cudaEventRecord(s->ev_t1, stream));
+        GAPA_CUDA_TRY(cudaEventSynchronize(s->ev_t1));
+        GAPA_CUDA_TRY(cudaEventElapsedTime(&t_pipe, s->ev_t0, s->ev_t1));
+        GAPA_CUDA_TRY(cudaEventRecord(s->ev_t0, stream));
+        GAPA_TRY(launch_uf(genes, nullptr, s->uf_out.as<double>(), true));
+        GAPA_CUDA_TRY(cudaEventRecord(s->ev_t1, stream));
+        GAPA_CUDA_TRY(cudaEventSynchronize(s->ev_t1));
+        GAPA_CUDA_TRY(cudaEventElapsedTime(&t_uf, s->ev_t0, s->ev_t1));
+        s->uf_mode = t_uf < t_pipe ? 1 : 0;
+        if (s->trace) std::fprintf(stderr, "pc_eval: %d rows, pipeline %.3f ms, union-find %.3f ms -> %s\n", rows, t_pipe, t_uf, s->uf_mode ? "union-find" : "pipeline");
     }
     return GAPA_CUDA_OK;
 }
@@ -1998,7 +2167,9 @@ void pc_free(gapa_cuda_ctx* ctx) {
         if (set->ev_done) cudaEventDestroy(set->ev_done);
         delete set;
     }
-    for (DevBuf* b : {&s->nbr4, &s->ord_row_ptr, &s->ord_col_idx, &s->ord_gene_map}) b->release();
+    for (DevBuf* b : {&s->nbr4, &s->ord_row_ptr, &s->ord_col_idx, &s->ord_gene_map, &s->uf_scratch, &s->uf_out}) b->release();
+    if (s->ev_t0) cudaEventDestroy(s->ev_t0);
+    if (s->ev_t1) cudaEventDestroy(s->ev_t1);
     if (s->h_counters) cudaFreeHost(s->h_counters);
     if (s->ev_fork) cudaEventDestroy(s->ev_fork);
     delete s;

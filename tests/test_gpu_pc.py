@@ -7,11 +7,13 @@ import pytest
 pytestmark = pytest.mark.gpu
 
 
-@pytest.fixture(params=["warp-per-individual", "bit-sliced"], autouse=True)
+@pytest.fixture(params=["warp-per-individual", "bit-sliced", "union-find"], autouse=True)
 def pc_path(request, monkeypatch):
-    """Every case runs through both PC implementations: the shared-memory warp kernel that small
-    graphs take by default, and the bit-sliced pipeline (forced here; the default above n = 2048-4096, see pc_kernels.cu small_pays)."""
+    """Every case runs through all three PC implementations: the shared-memory kernel that small graphs take by default, the
+    bit-sliced pipeline (forced here; the default above n = 2048-4096, see pc_kernels.cu small_pays) and the per-individual
+    union-find in global memory (k_pc_uf: what a context switches to, by measurement, on graphs without a hub core)."""
     monkeypatch.setenv("GAPA_PC_SMALL", "2" if request.param == "warp-per-individual" else "0")
+    monkeypatch.setenv("GAPA_PC_UF", "1" if request.param == "union-find" else "0")
     return request.param
 
 
@@ -219,3 +221,19 @@ def test_every_schedule_gives_the_oracles_integers(gp, oracle, cuda_device, monk
             batch = gp.init_population(pool.size(), rows, graph.n // 20, rows)
             assert np.array_equal(pc.evaluate_batch(batch), oracle.eval_batch(og, 0, batch, threads=8)), (graph.n, rows)
             assert np.array_equal(mcn.evaluate_batch(batch), oracle.eval_batch(og, 1, batch, threads=8)), (graph.n, rows)
+
+
+def test_high_diameter_graph_switches_to_union_find(gp, oracle, cuda_device, monkeypatch):
+    """A ring has no hub core: the pipeline's speculative schedule stands down, the context times both algorithms on that
+    batch and keeps the faster one; whichever it is, every evaluation before, during and after the switch equals the oracle."""
+    monkeypatch.setenv("GAPA_PC_SMALL", "0")
+    monkeypatch.delenv("GAPA_PC_UF", raising=False)  # automatic
+    n = 20000
+    ring = np.stack([np.arange(n), (np.arange(n) + 1) % n], 1).astype(np.int32)
+    g = gp.Graph(n, ring)
+    for task in (0, 1):
+        obj, pool = _objective(gp, g, task)
+        og = oracle.graph_from_edges(n, ring)
+        for trial in range(3):
+            batch = gp.init_population(pool.size(), 128, 1000, 10 + trial)
+            assert np.array_equal(obj.evaluate_batch(batch), oracle.eval_batch(og, task, batch)), (task, trial)
