@@ -456,7 +456,7 @@ def run_gpu_arm(args, w):
                                      "PopulationMatrix&) passes): staged through the library's pinned ring by host threads"},
             "gpu_launches": int(launches),
             "clocks": clocks,
-            "comm": {"transport": transport, "bootstrap": "torch.distributed nccl" if world > 1 else None, "nranks": world},
+            "comm": {"transport": transport, "bootstrap": ("torch.distributed gloo (ranks share one GPU: development aid, not a benchmark)" if shared_gpu else "torch.distributed nccl") if world > 1 else None, "nranks": world},
             "roofline": {"bound": "hbm", "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": traffic, "traffic_source": traffic_src, "peak_source": peak_src,
                          "kernel": "fitness evaluation pipeline (k_pc_sweep dominant)" if task in ("pc", "mcn") else f"{task} fitness pipeline",

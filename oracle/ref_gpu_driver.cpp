@@ -8,7 +8,9 @@
 // gapa::FitnessFunction.  Every run must equal the reference's CPU objective bit for bit:
 // history best AND mean, final population, final fitness (the comparison of
 // tests/test_parallel.cpp:43-52).
+#include <chrono>
 #include <cstdio>
+#include <cstdlib>
 #include <string>
 
 #include "gapa/generators.hpp"
@@ -47,7 +49,36 @@ static void compare_modes(const std::string& name, const GAParams& params, const
     expect(same_outputs(want, run_serial(params, pool, gpu)), name + " serial (evaluate_one)");
 }
 
-int main() {
+// `ref_gpu_driver e2e <n> <attach> <pop> <reps>`: the REAL plugin boundary, timed from C++ — the reference's own Graph, GenePool
+// and PopulationMatrix (a pageable std::vector), FitnessFunction::evaluate_batch(const PopulationMatrix&) of the CUDA objective.
+// One JSON line; the first three fitness values let the caller check them against the device path (same init stream).
+static int bench_e2e(int n, int attach, int pop_rows, int reps) {
+    const Graph g = barabasi_albert(n, attach, 1);
+    const GenePool pool = build_gene_pool(g, PoolKind::NodeRemoval);
+    const int k = perturbation_budget(g, PoolKind::NodeRemoval, 0.05);
+    const gapa_b200::CudaPairwiseConnectivityObjective gpu(g, pool);
+    const PopulationMatrix batch = init_population_block(pool.size(), 0, pop_rows, k, RngPolicy(1), 0);
+    FitnessVector fit = gpu.evaluate_batch(batch);  // warm-up: scratch, pinned ring, learned schedule
+    fit = gpu.evaluate_batch(batch);
+    const auto t0 = std::chrono::steady_clock::now();
+    for (int r = 0; r < reps; ++r) fit = gpu.evaluate_batch(batch);
+    const double sec = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count() / reps;
+    std::printf("{\"path\": \"gapa::FitnessFunction::evaluate_batch(const PopulationMatrix&) of CudaPairwiseConnectivityObjective, called from C++ on "
+                "the reference's own types (pageable std::vector)\", \"n\": %d, \"m\": %d, \"k\": %d, \"pop\": %d, \"reps\": %d, "
+                "\"seconds_per_call\": %.6f, \"evals_per_sec\": %.1f, \"h2d_bytes_per_call\": %.0f, \"fitness_head\": [%.1f, %.1f, %.1f]}\n",
+                n, g.edge_count(), k, pop_rows, reps, sec, pop_rows / sec, 4.0 * pop_rows * k, fit[0], fit[1], fit[2]);
+    return 0;
+}
+
+int main(int argc, char** argv) {
+    if (argc >= 6 && std::string(argv[1]) == "e2e") {
+        try {
+            return bench_e2e(std::atoi(argv[2]), std::atoi(argv[3]), std::atoi(argv[4]), std::atoi(argv[5]));
+        } catch (const std::exception& e) {
+            std::printf("DROPIN_EXCEPTION %s\n", e.what());
+            return 2;
+        }
+    }
     try {
         {  // BASELINE config 1
             const Graph g = barabasi_albert(1000, 2, 1);

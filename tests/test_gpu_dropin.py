@@ -26,6 +26,30 @@ def test_reference_run_ga_drives_cuda_objectives(gp, cuda_device):
     assert out.returncode == 0 and "DROPIN_OK" in out.stdout, out.stdout[-3000:] + out.stderr[-2000:]
 
 
+@pytest.mark.gpu
+def test_cxx_plugin_boundary_end_to_end(gp, cuda_device):
+    """The real drop-in call, from C++: the reference's barabasi_albert / build_gene_pool / init_population_block and
+    FitnessFunction::evaluate_batch(const PopulationMatrix&) of the CUDA objective — a pageable std::vector crossing the
+    library's pinned ring.  Values must equal the Python device path on the same init stream; the line it prints (evals/s
+    through the C++ boundary) is what `tools/cxx_e2e.sh` records under profiles/ at the full C4 size."""
+    import json
+    import numpy as np
+    exe = os.path.join(ROOT, "oracle", "_ref", "ref_gpu_driver")
+    if not os.path.exists(exe):
+        pytest.skip("oracle/_ref/ref_gpu_driver was not built (needs /root/reference at build time)")
+    n, attach, rows = 100_000, 5, 1024
+    out = subprocess.run([exe, "e2e", str(n), str(attach), str(rows), "3"], capture_output=True, text=True, timeout=900, env=_env())
+    assert out.returncode == 0, out.stdout[-2000:] + out.stderr[-2000:]
+    line = json.loads(out.stdout.strip().splitlines()[-1])
+    g = gp.barabasi_albert(n, attach, 1)
+    pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
+    k = gp.perturbation_budget(g, gp.PoolKind.NodeRemoval, 0.05)
+    assert (line["k"], line["m"], line["pop"]) == (k, g.edge_count(), rows)
+    want = gp.PairwiseConnectivityObjective(g, pool).evaluate_batch(gp.init_population(pool.size(), rows, k, 1))
+    assert np.array_equal(np.asarray(line["fitness_head"]), want[:3])
+    assert line["evals_per_sec"] > 0
+
+
 def _build_host_test(tmp_path):
     exe = str(tmp_path / "host_adapter_test")
     cmd = ["g++", "-std=c++20", "-O1", "-I", os.path.join(ROOT, "include"), "-I",
