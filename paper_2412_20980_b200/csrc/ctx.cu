@@ -45,7 +45,8 @@ static int upload_i32(const std::vector<int32_t>& h, int32_t** d) {
 // the H2D.  With kSlots slices in flight the host copy of slice i+1 overlaps the DMA of slice i.
 // Copy into the pinned slot with non-temporal stores: the destination is only ever read by the DMA engine, so pulling
 // its lines into the cache first (read-for-ownership) is a third of the memory traffic of the copy for nothing.
-// GAPA_PINNED_RING_COPY=memcpy keeps the C library's copy (tools/probe_pageable.py measures both).
+// GAPA_PINNED_RING_COPY=nt selects it; the default is the C library's copy, which measures the same or better since the
+// workers spin (tools/probe_pageable.py, tools/sweep_ring.py).
 #if defined(__x86_64__)
 #include <immintrin.h>
 __attribute__((target("avx2"))) static void copy_nt_avx2(char* dst, const char* src, size_t len) {
@@ -82,16 +83,20 @@ static void ring_copy(char* dst, const char* src, size_t len, bool nt) {
 }
 
 PinnedRing::PinnedRing() {
-    if (const char* raw = std::getenv("GAPA_PINNED_RING_COPY")) nt_copy = raw[0] != 'm';
+    if (const char* raw = std::getenv("GAPA_PINNED_RING_COPY")) nt_copy = raw[0] == 'n';
     if (const char* raw = std::getenv("GAPA_PINNED_SLICE_MB")) slice_bytes = static_cast<size_t>(std::max(1, std::min(256, std::atoi(raw)))) << 20;
     const unsigned hw = std::max(1u, std::thread::hardware_concurrency());
-    // measured on the B200 box (16 host cores, one socket; tools/probe_pageable.py, 819 MB batch = C4):
+    // measured on the B200 box (16 host cores, one socket; tools/probe_pageable.py, tools/sweep_ring.py; 819 MB batch = C4):
     //   plain cudaMemcpyAsync from pageable memory 10.8 GB/s; the same batch from pinned memory 54 GB/s (the PCIe rate);
-    //   this ring with the C library's memcpy: 20.4 / 21.6 GB/s at 4 / 8 threads (round 1's default: 4 threads);
-    //   with non-temporal stores: 8.8 / 15.8 / 25.7 / 33.4 / 32.3 GB/s at 1 / 2 / 4 / 8 / 16 threads  -> 8 threads.
-    //   The host alone copies 73 GB/s (8 threads, no DMA running); copy + DMA together move 3 x 819 MB through its memory,
-    //   ~125 GB/s of the ~150 GB/s it has.  Pinning the caller's pages in place instead (cudaHostRegister per slice) manages
-    //   1.6 - 7.7 GB/s (tools/probe_hostregister.py) and is no alternative.
+    //   first ring (blocking push per slice, condition variables): memcpy 20.4 / 21.6 GB/s at 4 / 8 threads, non-temporal
+    //   stores 25.7 / 33.4 GB/s;
+    //   this ring (spinning workers, begin/end split so that the next slice is copied while the previous one is submitted
+    //   and the chunk's kernels are enqueued): memcpy 44.5 GB/s at 8 threads and 16 MB slots (18.4 ms per batch = 222 k
+    //   evals/s; 37.8 - 44.7 GB/s over 6 - 12 threads x 8 - 32 MB), non-temporal stores 43.2 GB/s -> the C library's copy,
+    //   8 threads.  16 spinning workers on 16 cores starve the caller and the driver's threads: 4.9 GB/s — hence cores / 2.
+    //   The host alone copies 73 GB/s (8 threads, no DMA running); copy + DMA together move 3 x 819 MB through its memory.
+    //   Pinning the caller's pages in place instead (cudaHostRegister per slice) manages 1.6 - 7.7 GB/s
+    //   (tools/probe_hostregister.py) and is no alternative.
     int count = static_cast<int>(std::min(8u, std::max(1u, hw / 2)));
     if (const char* raw = std::getenv("GAPA_PINNED_RING_THREADS")) count = std::max(1, std::min(64, std::atoi(raw)));
     for (int t = 0; t < count; ++t) workers.emplace_back([this, t, count] { work(t, count); });
@@ -100,7 +105,7 @@ PinnedRing::~PinnedRing() {
     {
         std::lock_guard<std::mutex> lock(mu);
         stop = true;
-        ++generation;
+        generation.fetch_add(1, std::memory_order_release);
     }
     wake.notify_all();
     for (std::thread& w : workers) w.join();
@@ -109,25 +114,43 @@ PinnedRing::~PinnedRing() {
         if (buf[i]) cudaFreeHost(buf[i]);
     }
 }
+// A worker SPINS on the job counter for a short while after each slice (a batch is a few dozen slices a fraction of a
+// millisecond apart: a condition-variable wake-up per slice and thread costs more than the copy it waits for) and goes
+// to sleep on the condition variable when nothing arrives for ~1 ms.
 void PinnedRing::work(int index, int count) {
     uint64_t seen = 0;
     for (;;) {
-        std::unique_lock<std::mutex> lock(mu);
-        wake.wait(lock, [&] { return generation != seen; });
-        seen = generation;
+        bool got = false;
+        for (int spin = 0; spin < 200000 && !got; ++spin) {
+            got = generation.load(std::memory_order_acquire) != seen;
+#if defined(__x86_64__)
+            if (!got) __builtin_ia32_pause();
+#endif
+        }
+        if (!got) {
+            std::unique_lock<std::mutex> lock(mu);
+            wake.wait(lock, [&] { return generation.load(std::memory_order_acquire) != seen; });
+        }
+        seen = generation.load(std::memory_order_acquire);
         if (stop) return;
         const char* src = job_src;
         char* dst = job_dst;
         const size_t len = job_len;
-        lock.unlock();
         const size_t part = ((len + count - 1) / count + 4095) & ~size_t{4095};
         const size_t lo = std::min(len, part * index), hi = std::min(len, lo + part);
         if (hi > lo) ring_copy(dst + lo, src + lo, hi - lo, nt_copy);
-        lock.lock();
-        if (++finished == count) idle.notify_one();
+        finished.fetch_add(1, std::memory_order_release);
     }
 }
-int PinnedRing::push(void* dst_dev, const void* src_host, size_t len, cudaStream_t copy_stream) {
+// begin(): wait until the slot's previous H2D has drained and hand the slice to the copy threads — returns at once;
+// end(): wait for the copy threads, enqueue the H2D.  Between the two the caller enqueues the kernels of the previous chunk
+// and the previous slice's DMA runs: the host copy of slice i+1 overlaps both.
+int PinnedRing::begin(const void* src_host, size_t len) {
+    if (in_flight) {  // a previous call left after an error between begin() and end(): let its copy finish first
+        const int count = static_cast<int>(workers.size());
+        while (finished.load(std::memory_order_acquire) != count) std::this_thread::yield();
+        in_flight = false;
+    }
     const int slot = next++ % kSlots;
     if (!buf[slot]) {
         GAPA_CUDA_TRY(cudaMallocHost(reinterpret_cast<void**>(&buf[slot]), slice_bytes));
@@ -135,18 +158,30 @@ int PinnedRing::push(void* dst_dev, const void* src_host, size_t len, cudaStream
     } else {
         GAPA_CUDA_TRY(cudaEventSynchronize(done[slot]));
     }
+    cur_slot = slot;
+    cur_len = len;
+    job_src = static_cast<const char*>(src_host);
+    job_dst = buf[slot];
+    job_len = len;
+    finished.store(0, std::memory_order_relaxed);
     {
-        std::unique_lock<std::mutex> lock(mu);
-        job_src = static_cast<const char*>(src_host);
-        job_dst = buf[slot];
-        job_len = len;
-        finished = 0;
-        ++generation;
-        wake.notify_all();
-        idle.wait(lock, [&] { return finished == static_cast<int>(workers.size()); });
+        std::lock_guard<std::mutex> lock(mu);  // a worker that is going to sleep sees the new job or gets the notification
+        generation.fetch_add(1, std::memory_order_release);
     }
-    GAPA_CUDA_TRY(cudaMemcpyAsync(dst_dev, buf[slot], len, cudaMemcpyHostToDevice, copy_stream));
-    GAPA_CUDA_TRY(cudaEventRecord(done[slot], copy_stream));
+    wake.notify_all();
+    in_flight = true;
+    return GAPA_CUDA_OK;
+}
+int PinnedRing::end(void* dst_dev, cudaStream_t copy_stream) {
+    const int count = static_cast<int>(workers.size());
+    while (finished.load(std::memory_order_acquire) != count) {
+#if defined(__x86_64__)
+        __builtin_ia32_pause();
+#endif
+    }
+    in_flight = false;
+    GAPA_CUDA_TRY(cudaMemcpyAsync(dst_dev, buf[cur_slot], cur_len, cudaMemcpyHostToDevice, copy_stream));
+    GAPA_CUDA_TRY(cudaEventRecord(done[cur_slot], copy_stream));
     return GAPA_CUDA_OK;
 }
 
@@ -709,29 +744,45 @@ int gapa_cuda_eval_batch(gapa_cuda_ctx* c, int task, const int32_t* genes_host, 
             GAPA_CUDA_TRY(cudaEventRecord(c->copy_events[i], c->copy_stream));
         }
     if (pageable && !c->ring) c->ring = new PinnedRing();
-    size_t ring_next = 0;  // bytes of the gene matrix already handed to the ring
-    auto ring_feed = [&](size_t upto_bytes) -> int {  // stage the matrix up to this byte through the pinned ring
-        const char* src = reinterpret_cast<const char*>(genes_host);
-        char* dst = reinterpret_cast<char*>(stage);
-        while (ring_next < upto_bytes) {
-            const size_t len = std::min(c->ring->slice_bytes, upto_bytes - ring_next);
-            GAPA_TRY(c->ring->push(dst + ring_next, src + ring_next, len, c->copy_stream));
-            ring_next += len;
+    // pageable: the matrix in slices of at most one ring slot that do not straddle a chunk; slice k+1 is being copied into its
+    // slot by the host threads while slice k crosses PCIe and while this thread enqueues the kernels of the chunk slice k ended
+    struct Slice { size_t off, len; int ends_chunk; };
+    std::vector<Slice> slices;
+    if (pageable) {
+        size_t at = 0;
+        for (int i = 0; i < chunks; ++i) {
+            const size_t upto = sizeof(int32_t) * static_cast<size_t>(std::min(rows, (i + 1) * chunk_rows)) * cols;
+            while (at < upto) {
+                const size_t len = std::min(c->ring->slice_bytes, upto - at);
+                slices.push_back(Slice{at, len, at + len == upto ? i : -1});
+                at += len;
+            }
         }
-        return GAPA_CUDA_OK;
-    };
-    for (int i = 0; i < chunks; ++i) {
+    }
+    auto eval_chunk = [&](int i) -> int {
         const int r0 = i * chunk_rows, cr = std::min(chunk_rows, rows - r0);
-        if (pageable) {
-            // chunk i AND chunk i+1 are on their way before chunk i's kernels are enqueued
-            GAPA_TRY(ring_feed(sizeof(int32_t) * static_cast<size_t>(std::min(rows, r0 + cr)) * cols));
-            GAPA_CUDA_TRY(cudaEventRecord(c->copy_events[i], c->copy_stream));
-        }
         if (cells) GAPA_CUDA_TRY(cudaStreamWaitEvent(c->stream, c->copy_events[i], 0));
         // every chunk has its own pair of timing events, read once at the end: the host is free to stage the next chunk
-        GAPA_TRY(eval_rows_locked(c, task, GeneRows{stage + static_cast<size_t>(r0) * cols, nullptr, cols}, cr,
-                                  c->out_stage.as<double>() + r0, c->stream, nullptr, true, true, c->chunk_events[2 * i],
-                                  c->chunk_events[2 * i + 1]));
+        return eval_rows_locked(c, task, GeneRows{stage + static_cast<size_t>(r0) * cols, nullptr, cols}, cr,
+                                c->out_stage.as<double>() + r0, c->stream, nullptr, true, true, c->chunk_events[2 * i],
+                                c->chunk_events[2 * i + 1]);
+    };
+    if (pageable) {
+        const char* src = reinterpret_cast<const char*>(genes_host);
+        char* dst = reinterpret_cast<char*>(stage);
+        if (!slices.empty()) GAPA_TRY(c->ring->begin(src + slices[0].off, slices[0].len));
+        for (size_t k = 0; k < slices.size(); ++k) {
+            GAPA_TRY(c->ring->end(dst + slices[k].off, c->copy_stream));
+            if (k + 1 < slices.size()) GAPA_TRY(c->ring->begin(src + slices[k + 1].off, slices[k + 1].len));
+            if (slices[k].ends_chunk >= 0) {
+                GAPA_CUDA_TRY(cudaEventRecord(c->copy_events[slices[k].ends_chunk], c->copy_stream));
+                GAPA_TRY(eval_chunk(slices[k].ends_chunk));
+            }
+        }
+        if (!cells)
+            for (int i = 0; i < chunks; ++i) GAPA_TRY(eval_chunk(i));  // cols == 0: nothing to stage
+    } else {
+        for (int i = 0; i < chunks; ++i) GAPA_TRY(eval_chunk(i));
     }
     GAPA_CUDA_TRY(cudaMemcpyAsync(out_host, c->out_stage.ptr, sizeof(double) * rows, cudaMemcpyDeviceToHost, c->stream));
     GAPA_CUDA_TRY(cudaStreamSynchronize(c->stream));

@@ -144,18 +144,22 @@ struct PinnedRing {
     std::vector<std::thread> workers;
     std::mutex mu;
     std::condition_variable wake, idle;
-    uint64_t generation = 0;
-    int finished = 0;
+    std::atomic<uint64_t> generation{0};
+    std::atomic<int> finished{0};
+    int cur_slot = 0;
+    size_t cur_len = 0;
+    bool in_flight = false;  // between begin() and end()
     bool stop = false;
     size_t slice_bytes = kPinnedSliceBytes;
-    bool nt_copy = true;  // non-temporal stores into the pinned slot (GAPA_PINNED_RING_COPY=memcpy: the C library's copy)
+    bool nt_copy = false;  // GAPA_PINNED_RING_COPY=nt: non-temporal stores into the pinned slot instead of the C library's copy
     const char* job_src = nullptr;
     char* job_dst = nullptr;
     size_t job_len = 0;
     PinnedRing();
     ~PinnedRing();
     void work(int index, int count);
-    int push(void* dst_dev, const void* src_host, size_t len, cudaStream_t copy_stream);
+    int begin(const void* src_host, size_t len);
+    int end(void* dst_dev, cudaStream_t copy_stream);
 };
 
 // ---- context -------------------------------------------------------------------------

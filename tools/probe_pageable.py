@@ -22,7 +22,7 @@ if len(sys.argv) > 1 and sys.argv[1] == "child":
     for _ in range(5):
         gp.capi.check(lib.gapa_cuda_eval_batch(obj.dgraph.handle, obj.task, genes.ctypes.data, rows, k, out.ctypes.data))
     dt = (time.perf_counter() - t0) / 5
-    print(f"{os.environ.get('GAPA_PINNED_RING', '1')} ring, slice {os.environ.get('GAPA_PINNED_SLICE_MB', '16')} MB, copy {os.environ.get('GAPA_PINNED_RING_COPY', 'nt')}, threads {os.environ.get('GAPA_PINNED_RING_THREADS', 'default')}: "
+    print(f"{os.environ.get('GAPA_PINNED_RING', '1')} ring, slice {os.environ.get('GAPA_PINNED_SLICE_MB', '16')} MB, copy {os.environ.get('GAPA_PINNED_RING_COPY', 'memcpy')}, threads {os.environ.get('GAPA_PINNED_RING_THREADS', 'default')}: "
           f"{dt * 1e3:.1f} ms per call, {rows / dt:.0f} evals/s, {4 * rows * k / dt / 1e9:.1f} GB/s")
 elif len(sys.argv) > 1 and sys.argv[1] == "host":
     # the host's own copy ceiling, no GPU involved: N threads memcpy an 819 MB pageable array into another buffer
