@@ -157,6 +157,8 @@ extern "C" int gapa_cuda_cda_phase_cycles(unsigned long long* out8, int reset) {
 __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows genes, int rows,
                                                         int pos_in_smem, double* __restrict__ out,
                                                         int32_t* __restrict__ owner_out, int hier_off) {
+    griddep_launch();
+    griddep_wait();
     __shared__ Cand warp_cand[kCdaWarps];
     __shared__ Cand chosen;
     __shared__ long long sh_total;

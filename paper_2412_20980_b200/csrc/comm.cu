@@ -87,6 +87,8 @@ __device__ __forceinline__ void wait_flag(const uint32_t* flag, uint32_t seq, un
 enum { kPush = 1, kPull = 2 };
 __global__ void __launch_bounds__(256) k_comm_allgather(CommPeers peers, int rank, size_t cap, uint32_t seq, double* fit_full,
                                                         int block, int* run_status, unsigned long long timeout_ns, int phases) {
+    griddep_launch();
+    griddep_wait();
     const int p = blockIdx.x;
     if (p == rank) return;
     const size_t parity = seq & 1u;
@@ -112,6 +114,8 @@ __global__ void __launch_bounds__(256) k_comm_allgather(CommPeers peers, int ran
 // the same exchange for a few bytes per rank (bootstrap data: IPC handles of the population stores)
 __global__ void __launch_bounds__(kCtrlBytes) k_comm_ctrl(CommPeers peers, int rank, int world, size_t cap, uint32_t seq, const char* mine,
                                                            int bytes, char* all_out, unsigned long long timeout_ns, int phases) {
+    griddep_launch();
+    griddep_wait();
     const int p = blockIdx.x;
     const size_t parity = seq & 1u;
     if (p == rank) {

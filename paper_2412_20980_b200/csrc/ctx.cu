@@ -16,6 +16,14 @@ namespace gapa_b200 {
 
 static thread_local std::string t_error;
 std::atomic<uint64_t> g_launches{0};
+int g_pdl = [] {
+    const char* raw = std::getenv("GAPA_PDL");
+    return raw && raw[0] == '0' ? 0 : 1;
+}();
+long g_pdl_max_ctas = [] {
+    const char* raw = std::getenv("GAPA_PDL_MAX_CTAS");
+    return raw ? std::atol(raw) : 2368L;  // 16 CTAs per SM: measured, tools/ab_pdl_ctas.sh
+}();
 
 int fail(int code, const char* fmt, ...) {
     char buf[512];
@@ -596,6 +604,8 @@ static int check_task(const gapa_cuda_ctx* c, int task) {
 // every gene of the s parent rows lies in [0, pool_size)?
 __global__ void __launch_bounds__(256) k_genes_in_range(const int32_t* __restrict__ pool, const int32_t* __restrict__ parent, int s, int k,
                                                         int pool_size, int* bad) {
+    griddep_launch();
+    griddep_wait();
     const size_t cells = static_cast<size_t>(s) * k;
     for (size_t i = static_cast<size_t>(blockIdx.x) * blockDim.x + threadIdx.x; i < cells; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int r = static_cast<int>(i / k);

@@ -18,6 +18,8 @@ static constexpr int kGaThreads = 256;
 // ---- init_population_block (ga_ops.cpp:19-29) ----------------------------------------
 __global__ void __launch_bounds__(kGaThreads) k_ga_init(uint32_t pool_size, int row_first, int budget, uint64_t seed,
                                                         uint64_t generation, int32_t* __restrict__ out) {
+    griddep_launch();
+    griddep_wait();
     __shared__ uint64_t key;
     const int row = blockIdx.y;
     if (threadIdx.x == 0) key = stream_key(seed, generation, GAPA_ROLE_INIT, static_cast<uint64_t>(row_first + row));
@@ -33,6 +35,8 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_init(uint32_t pool_size, int 
 // mask(i, j) = stream(generation, role, row_first + i).next_bernoulli(rate) at draw j + 1 (1 or 0, MaskMatrix bytes).
 __global__ void __launch_bounds__(kGaThreads) k_ga_mask(uint64_t role, int row_first, int cols, uint64_t limit, bool always,
                                                         uint64_t seed, uint64_t generation, uint8_t* __restrict__ out) {
+    griddep_launch();
+    griddep_wait();
     __shared__ uint64_t key;
     const int row = blockIdx.y;
     if (threadIdx.x == 0) key = stream_key(seed, generation, role, static_cast<uint64_t>(row_first + row));
@@ -45,6 +49,8 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_mask(uint64_t role, int row_f
 // fresh(i, j) = stream(generation, MutationIndex, row_first + i).next_index(pool) at draw j + 1
 __global__ void __launch_bounds__(kGaThreads) k_ga_mutation_indices(uint32_t pool_size, int row_first, int cols, uint64_t seed,
                                                                     uint64_t generation, int32_t* __restrict__ out) {
+    griddep_launch();
+    griddep_wait();
     __shared__ uint64_t key;
     const int row = blockIdx.y;
     if (threadIdx.x == 0) key = stream_key(seed, generation, GAPA_ROLE_MUTATION_INDEX, static_cast<uint64_t>(row_first + row));
@@ -62,6 +68,8 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_mutation_indices(uint32_t poo
 __global__ void __launch_bounds__(kGaThreads) k_ga_crossover_mutate(
     const int32_t* __restrict__ pop, const int32_t* __restrict__ partner, int k, int row_first, uint64_t pc_thr,
     uint64_t pm_thr, uint32_t pool_size, uint64_t seed, uint64_t generation, int32_t* __restrict__ out) {
+    griddep_launch();
+    griddep_wait();
     __shared__ uint64_t keys[3];
     const int row = row_first + blockIdx.y;
     if (threadIdx.x < 3)
@@ -103,6 +111,8 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_crossover_mutate4(
     const int32_t* __restrict__ pop, const int32_t* __restrict__ partner, int k, int row_first, uint64_t pc_limit,
     bool pc_always, uint64_t pm_limit, bool pm_always, uint32_t pool_size, uint64_t seed, uint64_t generation,
     int32_t* __restrict__ out) {
+    griddep_launch();
+    griddep_wait();
     __shared__ uint64_t keys[3];
     const int row = row_first + blockIdx.y;
     if (threadIdx.x < 3)
@@ -136,6 +146,8 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_crossover_mutate4(
 __global__ void __launch_bounds__(kGaThreads) k_ga_mutate(const int32_t* __restrict__ block, int k, int row_offset,
                                                           uint64_t pm_thr, uint32_t pool_size, uint64_t seed,
                                                           uint64_t generation, int32_t* __restrict__ out) {
+    griddep_launch();
+    griddep_wait();
     __shared__ uint64_t keys[2];
     const int row = row_offset + blockIdx.y;
     if (threadIdx.x < 2)
@@ -154,6 +166,8 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_mutate(const int32_t* __restr
 __global__ void __launch_bounds__(kGaThreads) k_ga_eda(const int32_t* __restrict__ elite, int k, uint32_t elite_count,
                                                        uint32_t bound, int row_first, uint64_t seed, uint64_t generation,
                                                        int32_t* __restrict__ out) {
+    griddep_launch();
+    griddep_wait();
     __shared__ uint64_t key;
     const int row = row_first + blockIdx.y;  // out holds rows [row_first, row_first + gridDim.y)
     if (threadIdx.x == 0) key = stream_key(seed, generation, GAPA_ROLE_SELECT, static_cast<uint64_t>(row));
@@ -179,6 +193,8 @@ static constexpr int kPerBlock = kGaThreads / kSplit;
 
 __global__ void __launch_bounds__(kGaThreads) k_ga_weights(const double* __restrict__ fitness, int s, int minimize,
                                                            double* __restrict__ weights, int* status) {
+    griddep_launch();
+    griddep_wait();
     __shared__ unsigned long long tile[kGaThreads];
     const int i = blockIdx.x * kPerBlock + threadIdx.x / kSplit, part = threadIdx.x % kSplit;
     const double mine_f = i < s ? fitness[i] : 0.0;
@@ -233,6 +249,8 @@ static constexpr int kPickSmemRows = 24576;  // 192 KB of running totals
 __global__ void __launch_bounds__(1024) k_ga_pick(const double* __restrict__ weights, int s, uint64_t seed,
                                                   uint64_t generation, double* __restrict__ cumulative,
                                                   int32_t* __restrict__ partner, int in_smem) {
+    griddep_launch();
+    griddep_wait();
     // The running totals live in shared memory when they fit (s <= kPickSmemRows): the s binary searches below are
     // chains of ~log2 s dependent reads, 30 ns each from shared memory against 300+ ns from L2.
     extern __shared__ double pick_cum[];
@@ -289,6 +307,8 @@ __global__ void __launch_bounds__(1024) k_ga_select_small(const double* __restri
                                                           uint64_t generation, double* __restrict__ weights,
                                                           double* __restrict__ cumulative, int32_t* __restrict__ partner,
                                                           int* status) {
+    griddep_launch();
+    griddep_wait();
     __shared__ double f[1024];
     __shared__ double part[1024];
     const int tid = threadIdx.x;
@@ -337,6 +357,8 @@ __global__ void __launch_bounds__(1024) k_ga_select_small(const double* __restri
 __global__ void __launch_bounds__(kGaThreads) k_ga_elite_rank(const double* __restrict__ fit, const double* __restrict__ fit_m,
                                                               int s, int minimize, int32_t* __restrict__ src_of_rank,
                                                               int* status) {
+    griddep_launch();
+    griddep_wait();
     __shared__ unsigned long long tile[kGaThreads];
     const int x = blockIdx.x * kPerBlock + threadIdx.x / kSplit, part = threadIdx.x % kSplit;
     const int total = 2 * s;
@@ -365,6 +387,8 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_elite_gather(const int32_t* _
                                                                 const double* __restrict__ fit_m, int s, int k,
                                                                 const int32_t* __restrict__ src_of_rank,
                                                                 int32_t* __restrict__ next, double* __restrict__ next_fit) {
+    griddep_launch();
+    griddep_wait();
     const int r = blockIdx.y;
     const int src = src_of_rank[r];
     const int32_t* from = src < s ? pop + static_cast<size_t>(src) * k : m_pop + static_cast<size_t>(src - s) * k;
@@ -380,6 +404,8 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_elite_gather(const int32_t* _
 }
 
 __global__ void k_rng_draws(uint64_t seed, uint64_t generation, uint64_t role, uint64_t row, int count, uint64_t* out) {
+    griddep_launch();
+    griddep_wait();
     const uint64_t key = stream_key(seed, generation, role, row);
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < count; j += gridDim.x * blockDim.x)
         out[j] = draw_u64(key, static_cast<uint64_t>(j) + 1);
@@ -460,6 +486,8 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_elite_gather_sharded(
     const int32_t* __restrict__ partner, const double* __restrict__ fit, const double* __restrict__ fit_m, int s, int k,
     uint64_t pc_thr, uint64_t pm_thr, uint32_t pool_size, uint64_t seed, uint64_t generation,
     const int32_t* __restrict__ src_of_rank, int32_t* __restrict__ next, double* __restrict__ next_fit) {
+    griddep_launch();
+    griddep_wait();
     __shared__ uint64_t keys[4];
     const int r = blockIdx.y;
     const int src = src_of_rank[r];

@@ -30,6 +30,8 @@ struct LpaScratch {
 
 __global__ void __launch_bounds__(kLpaThreads) k_lpa_init(const int32_t* __restrict__ row_ptr, int n, int rows,
                                                           int32_t* __restrict__ deg) {
+    griddep_launch();
+    griddep_wait();
     const size_t total = static_cast<size_t>(rows) * n;
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
@@ -44,6 +46,8 @@ __global__ void __launch_bounds__(kLpaThreads) k_lpa_remove(GeneRows genes, size
                                                             const int32_t* __restrict__ edge_u,
                                                             const int32_t* __restrict__ edge_v, int n, int mask_words,
                                                             unsigned* gone, int32_t* deg, int* status) {
+    griddep_launch();
+    griddep_wait();
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < cells;
          i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int r = static_cast<int>(i / genes.cols);
@@ -70,6 +74,8 @@ __global__ void __launch_bounds__(kLpaThreads) k_lpa_scores(const int32_t* __res
                                                             const int32_t* __restrict__ pairs, int n_pairs, int n,
                                                             int mask_words, const unsigned* __restrict__ gone,
                                                             const int32_t* __restrict__ deg, double* __restrict__ scores, int cn) {
+    griddep_launch();
+    griddep_wait();
     const int r = blockIdx.y;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n_pairs) return;
@@ -109,6 +115,8 @@ __global__ void __launch_bounds__(kLpaThreads) k_lpa_scores(const int32_t* __res
 // 2 * wins over the T x P grid (link_prediction.cpp:87-94), exact integers
 __global__ void __launch_bounds__(kLpaThreads) k_lpa_auc(const double* __restrict__ scores, int T, int P,
                                                          unsigned long long* twice) {
+    griddep_launch();
+    griddep_wait();
     __shared__ double tile[kLpaThreads];
     __shared__ unsigned long long block_sum;
     const int r = blockIdx.y;
@@ -154,6 +162,8 @@ __device__ __forceinline__ unsigned long long score_key(double x) {
 
 __global__ void __launch_bounds__(kLpaSortThreads) k_lpa_auc_sorted(const double* __restrict__ scores, int T, int P, int P2,
                                                                     double* __restrict__ out) {
+    griddep_launch();
+    griddep_wait();
     const int all_probes = P;
     __shared__ unsigned long long warp_sum[kLpaSortThreads / 32];
     __shared__ int n_nonzero;
@@ -248,6 +258,8 @@ __global__ void __launch_bounds__(kLpaThreads) k_lpa_flip_classify(GeneRows gene
                                                                    const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx,
                                                                    const int32_t* __restrict__ edge_id, int mask_words, unsigned* gone,
                                                                    int32_t* deg, unsigned long long* add_keys, int* add_count, int* status) {
+    griddep_launch();
+    griddep_wait();
     for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < cells; i += static_cast<size_t>(gridDim.x) * blockDim.x) {
         const int r = static_cast<int>(i / genes.cols);
         const int gene = genes.row(r)[i - static_cast<size_t>(r) * genes.cols];
@@ -281,6 +293,8 @@ __global__ void __launch_bounds__(kLpaThreads) k_lpa_flip_classify(GeneRows gene
 // One CTA per individual: sort the candidate pairs (bitonic, shared memory), drop repeats, raise the degrees of the
 // endpoints, leave the distinct pairs sorted in add_keys[r][0 .. add_count[r]).
 __global__ void __launch_bounds__(kLpaSortThreads) k_lpa_flip_unique(int cols, int n, unsigned long long* add_keys, int* add_count, int32_t* deg) {
+    griddep_launch();
+    griddep_wait();
     __shared__ int kept;
     const int r = blockIdx.x, tid = threadIdx.x;
     const int c = add_count[r];
@@ -339,6 +353,8 @@ __global__ void __launch_bounds__(kLpaSortThreads) k_lpa_flip_build(const int32_
                                                                     const unsigned* __restrict__ gone, const int32_t* __restrict__ deg,
                                                                     const unsigned long long* __restrict__ add_keys, const int* __restrict__ add_count,
                                                                     int cols, size_t col2_stride, int32_t* row_ptr2, int32_t* col2, int32_t* base_cnt) {
+    griddep_launch();
+    griddep_wait();
     __shared__ int sh_scan[kLpaSortThreads];
     const int r = blockIdx.x, tid = threadIdx.x;
     const unsigned* mask = gone + static_cast<size_t>(r) * mask_words;
@@ -407,6 +423,8 @@ __global__ void __launch_bounds__(kLpaSortThreads) k_lpa_flip_build(const int32_
 __global__ void __launch_bounds__(kLpaThreads) k_lpa_scores_plain(const int32_t* __restrict__ row_ptr2, const int32_t* __restrict__ col2,
                                                                   size_t col2_stride, const int32_t* __restrict__ pairs, int n_pairs, int n,
                                                                   double* __restrict__ scores, int cn) {
+    griddep_launch();
+    griddep_wait();
     const int r = blockIdx.y;
     const int q = blockIdx.x * blockDim.x + threadIdx.x;
     if (q >= n_pairs) return;
@@ -431,6 +449,8 @@ __global__ void __launch_bounds__(kLpaThreads) k_lpa_scores_plain(const int32_t*
 }
 
 __global__ void k_lpa_final(const unsigned long long* __restrict__ twice, int rows, int T, int P, double* out) {
+    griddep_launch();
+    griddep_wait();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
     const double wins = static_cast<double>(twice[r]) / 2.0;

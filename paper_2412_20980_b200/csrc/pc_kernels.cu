@@ -141,6 +141,8 @@ __global__ void __launch_bounds__(nt) k_pc_bitmask(GeneRows genes,
                                                              const int32_t* __restrict__ pool_map, int pool_size, int n,
                                                              int chunk_bits, int words_per_row, word_t* __restrict__ removed,
                                                              int* removed_count, PcCounters* counters) {
+    griddep_launch();
+    griddep_wait();
     const int row = blockIdx.y;  // the chunks of one individual are adjacent blocks: its genes are re-read from L2
     const int v0 = blockIdx.x * chunk_bits;
     const int v1 = min(n, v0 + chunk_bits);
@@ -227,6 +229,8 @@ template <int nt>
 __global__ void GAPA_MASK_BOUNDS k_pc_bitmask_rows(GeneRows genes, const int32_t* __restrict__ pool_map, int pool_size, int n,
                                                                   int words_per_row, word_t* __restrict__ removed, int* removed_count,
                                                                   PcCounters* counters, int rows) {
+    griddep_launch();
+    griddep_wait();
     const int tid = threadIdx.x;
     const int words64 = (n + 63) >> 6;
     word_t* bits64 = reinterpret_cast<word_t*>(pc_smem_bits);
@@ -373,6 +377,8 @@ template <int nt, bool kPeer>  // kPeer: parent rows may live in another rank's 
 __global__ void GAPA_VARY_BOUNDS k_pc_bitmask_vary(VariationSpec V, int k, const int32_t* __restrict__ gene_map,
                                                                   int n, int words_per_row, word_t* __restrict__ removed,
                                                                   int* removed_count, int rows) {
+    griddep_launch();
+    griddep_wait();
     __shared__ uint64_t keys[4];
     const int tid = threadIdx.x;
     const int words64 = (n + 63) >> 6;
@@ -553,6 +559,8 @@ __global__ void GAPA_VARY_BOUNDS k_pc_bitmask_vary(VariationSpec V, int k, const
 __global__ void __launch_bounds__(kTransThreads) k_pc_transpose(const word_t* __restrict__ removed, int words_per_row,
                                                                 int n, int rows, word_t* __restrict__ alive,
                                                                 word_t* __restrict__ clear_reached) {
+    griddep_launch();
+    griddep_wait();
     word_t* tile = reinterpret_cast<word_t*>(pc_smem_bits);  // kBits x (kTransThreads + 1) words, padded against bank conflicts
     const int g = blockIdx.y;
     const int vb0 = blockIdx.x * kTransThreads;
@@ -601,6 +609,8 @@ __device__ __forceinline__ size_t word_index(int g, int n, int v) {
 // phase 1 cover the giant component.
 __global__ void __launch_bounds__(kThreads) k_pc_source(const int32_t* __restrict__ by_degree, int n, int rows,
                                                         const word_t* __restrict__ alive, word_t* reached, PcCounters* counters) {
+    griddep_launch();
+    griddep_wait();
     const int row = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (row >= rows) return;
@@ -749,6 +759,8 @@ __global__ void __launch_bounds__(kPrefixThreads)
     k_pc_prefix(const int32_t* __restrict__ row_ptr, const int32_t* __restrict__ col_idx, const int4* __restrict__ nbr4,
                 int first4_only, int n, int prefix, const word_t* __restrict__ alive, Rec* reached, int pick_sources,
                 const int32_t* __restrict__ by_degree, int rows, PcCounters* counters) {
+    griddep_launch();
+    griddep_wait();
     cg::cluster_group cluster = cg::this_cluster();
     // the cluster size is a launch attribute: kPrefixCluster CTAs while every super-group's cluster is
     // resident at once, fewer when there are more super-groups than that (waves of idle-heavy clusters cost more)
@@ -975,6 +987,8 @@ __device__ __forceinline__ void sweep_chunk(const SweepArgs& A, int sg, int chun
 
 // ordinary sweep: blocks in ascending vertex order, `interleave` super-groups share blockIdx.x
 __global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep(SweepArgs A) {
+    griddep_launch();
+    griddep_wait();
     const int sg = blockIdx.y * A.interleave + (blockIdx.x % A.interleave);
     if (sg >= A.sgroups) return;
     const int slot = blockIdx.x / A.interleave;
@@ -1000,6 +1014,8 @@ __global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep(Sw
 // their records in registers and only re-gather what is still missing), which lets a chain of any length
 // inside a chunk close in one launch.  Rings and grids: 48 rounds -> a few.
 __global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep_local(SweepArgs A) {
+    griddep_launch();
+    griddep_wait();
     const int sg = blockIdx.y * A.interleave + (blockIdx.x % A.interleave);
     if (sg >= A.sgroups) return;
     const int slot = blockIdx.x / A.interleave;
@@ -1042,6 +1058,8 @@ __global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_sweep_lo
 
 // recording sweep: a persistent grid walks the list of incomplete chunks
 __global__ void __launch_bounds__(kThreads, GAPA_SWEEP_MIN_BLOCKS) k_pc_record(SweepArgs A) {
+    griddep_launch();
+    griddep_wait();
     __shared__ int hist[kPack * kBits];
     const unsigned total = A.counters->n_incomplete;
     // Recording is for the last few percent: per leftover vertex it costs a shared-memory atomic per unreached
@@ -1169,14 +1187,20 @@ __device__ __forceinline__ void pc_reduce_body(const Phase2Args& P, unsigned fir
 }
 
 __global__ void __launch_bounds__(kThreads) k_pc_hook(Phase2Args P, unsigned many) {
+    griddep_launch();
+    griddep_wait();
     if (pc_stand_down(P.counters, many)) return;
     pc_hook_body(P, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, P.counters->n_entries);
 }
 __global__ void __launch_bounds__(kThreads) k_pc_count(Phase2Args P, unsigned many) {
+    griddep_launch();
+    griddep_wait();
     if (pc_stand_down(P.counters, many)) return;
     pc_count_body(P, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, P.counters->n_entries);
 }
 __global__ void __launch_bounds__(kThreads) k_pc_reduce(Phase2Args P, unsigned many) {
+    griddep_launch();
+    griddep_wait();
     if (pc_stand_down(P.counters, many)) return;
     pc_reduce_body(P, blockIdx.x * blockDim.x + threadIdx.x, gridDim.x * blockDim.x, P.counters->n_entries);
 }
@@ -1202,6 +1226,8 @@ static constexpr int kFinalThreads = 1024;
 __global__ void __launch_bounds__(kFinalThreads) k_pc_final(Phase2Args P, unsigned many, unsigned fused_limit, int do_phase2, int rows,
                                                             int task, int* removed_count, int* unreached, double* out,
                                                             PcCounters* counters, PcCounters* host_out, int reset_slots) {
+    griddep_launch();
+    griddep_wait();
     __shared__ PcCounters c;
     __shared__ int skipped;
     const unsigned tid = threadIdx.x;
@@ -1250,6 +1276,8 @@ __global__ void __launch_bounds__(kThreads) k_pc_result(int n, int rows, int tas
                                                         const int32_t* __restrict__ comp_size,
                                                         const unsigned long long* __restrict__ pc_extra,
                                                         const int* __restrict__ mcn_extra, double* out) {
+    griddep_launch();
+    griddep_wait();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= rows) return;
     out[r] = pc_result_of(n, task, removed_count[r], unreached[r], comp_size[r], pc_extra[r], mcn_extra[r]);
@@ -1258,6 +1286,8 @@ __global__ void __launch_bounds__(kThreads) k_pc_result(int n, int rows, int tas
 // reset of everything the final sweep / phase 2 accumulate into
 __global__ void k_pc_reset(int groups, int32_t* parent, int32_t* comp_size, int* unreached,
                            unsigned long long* pc_extra, int* mcn_extra, PcCounters* counters, int first) {
+    griddep_launch();
+    griddep_wait();
     const int total = groups * kBits;
     for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < total; i += gridDim.x * blockDim.x) {
         parent[i] = i;
@@ -1300,6 +1330,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_pc_small(GeneRows genes,
     __shared__ long long warp_pairs[kSmallThreads / 32];
     __shared__ int warp_best[kSmallThreads / 32];
     const int tid = threadIdx.x, row = blockIdx.x;
+    griddep_launch();  // the next launch on the stream may become resident now (it waits for this one where it must)
     int32_t* parent = small_smem;
     int32_t* size = parent + n;
     unsigned* gone = reinterpret_cast<unsigned*>(size + n);
@@ -1309,6 +1340,7 @@ __global__ void __launch_bounds__(kSmallThreads) k_pc_small(GeneRows genes,
         parent[v] = v;
         size[v] = 0;
     }
+    griddep_wait();  // everything above is this CTA's own shared memory; from here on the predecessor's results are read
     __syncthreads();
     const int cols = genes.cols;
     if (have_vary) {
@@ -1397,6 +1429,8 @@ __global__ void __launch_bounds__(kUfThreads, 2048 / kUfThreads) k_pc_uf(GeneRow
                                                       const int32_t* __restrict__ edge_u, const int32_t* __restrict__ edge_v, int task,
                                                       double* __restrict__ out, PcCounters* counters, VariationSpec V, int have_vary,
                                                       int rows, int32_t* scratch) {
+    griddep_launch();
+    griddep_wait();
     extern __shared__ int32_t small_smem[];
     __shared__ uint64_t vary_keys[4];
     __shared__ long long warp_pairs[kUfThreads / 32];
@@ -1582,6 +1616,8 @@ static int ensure_order(gapa_cuda_ctx* ctx, PcScratch* s) {
 
 // clear of the reached records (a kernel rather than cudaMemsetAsync so that profilers list it with its DRAM bytes)
 __global__ void __launch_bounds__(kThreads) k_pc_clear(Rec* __restrict__ recs, size_t count) {
+    griddep_launch();
+    griddep_wait();
     const Rec zero{};
     for (size_t i = static_cast<size_t>(blockIdx.x) * kThreads + threadIdx.x; i < count; i += static_cast<size_t>(gridDim.x) * kThreads)
         store_rec(&recs[i], zero);
@@ -1798,10 +1834,12 @@ static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLan
             cfg.gridDim = dim3(sgroups * csize);
             cfg.blockDim = dim3(kPrefixThreads);
             cfg.stream = stream;
-            cudaLaunchAttribute attr{};
-            attr.id = cudaLaunchAttributeClusterDimension;
-            attr.val.clusterDim.x = csize; attr.val.clusterDim.y = 1; attr.val.clusterDim.z = 1;
-            cfg.attrs = &attr; cfg.numAttrs = 1;
+            cudaLaunchAttribute attr[2]{};
+            attr[0].id = cudaLaunchAttributeClusterDimension;
+            attr[0].val.clusterDim.x = csize; attr[0].val.clusterDim.y = 1; attr[0].val.clusterDim.z = 1;
+            attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+            attr[1].val.programmaticStreamSerializationAllowed = 1;
+            cfg.attrs = attr; cfg.numAttrs = pdl_allowed(cfg.gridDim) ? 2 : 1;
             GAPA_CUDA_TRY(cudaLaunchKernelEx(&cfg, k_pc_prefix, g_row_ptr, g_col_idx, static_cast<const int4*>(s->nbr4.as<int4>()),
                                              s->prefix_first4, n, prefix, alive_rec, reached_rec, 1, g_by_degree, crows, counters));
             g_launches.fetch_add(1, std::memory_order_relaxed);
@@ -2008,11 +2046,11 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         const bool fuse = vary && cols > 0;
         if (vary && !fuse) GAPA_TRY(launch_variation_spec(*vary, cols, rows, stream));
         if (rows <= 2 * sm)  // 100 rows at n = 1000: 0.03 ms with 512 threads per row, 0.05 ms with 128 (tools/ab_build.sh)
-            GAPA_LAUNCH(k_pc_small<kSmallThreadsFew>, rows, kSmallThreadsFew, smem, stream, genes,
+            GAPA_LAUNCH_PDL(k_pc_small<kSmallThreadsFew>, rows, kSmallThreadsFew, smem, stream, genes,
                         ctx->pool_identity ? nullptr : ctx->d_pool_map, ctx->pool_size, n, static_cast<int>(ctx->m), ctx->d_edge_u,
                         ctx->d_edge_v, task, out_dev, counters, fuse ? *vary : VariationSpec{}, fuse ? 1 : 0);
         else
-            GAPA_LAUNCH(k_pc_small<kSmallThreadsMany>, rows, kSmallThreadsMany, smem, stream, genes,
+            GAPA_LAUNCH_PDL(k_pc_small<kSmallThreadsMany>, rows, kSmallThreadsMany, smem, stream, genes,
                         ctx->pool_identity ? nullptr : ctx->d_pool_map, ctx->pool_size, n, static_cast<int>(ctx->m), ctx->d_edge_u,
                         ctx->d_edge_v, task, out_dev, counters, fuse ? *vary : VariationSpec{}, fuse ? 1 : 0);
         if (trusted) return GAPA_CUDA_OK;

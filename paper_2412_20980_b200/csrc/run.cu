@@ -47,6 +47,8 @@ int launch_fetch_rows(int32_t*, const int32_t* const*, int32_t*, const int32_t*,
 // record_generation (modes.cpp:35-43): best = front, mean = SEQUENTIAL sum / s so that
 // non-integer fitness reproduces std::accumulate bit for bit.
 __global__ void __launch_bounds__(1024) k_ga_stats(const double* __restrict__ fit, int s, double* best, double* mean) {
+    griddep_launch();
+    griddep_wait();
     __shared__ double stage[4096];
     __shared__ double warp_sum[32];
     __shared__ int not_exact;
@@ -93,6 +95,8 @@ __global__ void __launch_bounds__(1024) k_ga_stats(const double* __restrict__ fi
 }
 
 __global__ void k_check_nan(const double* __restrict__ fit, int s, int* status) {
+    griddep_launch();
+    griddep_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < s && isnan(fit[i])) *status = GAPA_CUDA_E_NAN;
 }

@@ -35,6 +35,8 @@ __global__ void __launch_bounds__(kSixThreads, 1) k_sixdst(const int32_t* __rest
                                                            const int32_t* __restrict__ pool_map, int pool_size, int rows,
                                                            word_t* scratch, int in_smem, double* __restrict__ out,
                                                            int* status) {
+    griddep_launch();
+    griddep_wait();
     __shared__ int counts[64];
     __shared__ int warp_best[kSixThreads / 32];
     const int tid = threadIdx.x;

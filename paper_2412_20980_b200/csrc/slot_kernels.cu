@@ -62,6 +62,8 @@ __device__ __forceinline__ void build_child_row(const VariationSpec& V, int k, i
 
 // children of rows [V.row_first, V.row_first + gridDim.y)
 __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_variation(VariationSpec V, int k) {
+    griddep_launch();
+    griddep_wait();
     __shared__ uint64_t keys[4];
     build_child_row(V, k, V.row_first + blockIdx.y, keys);
 }
@@ -69,12 +71,16 @@ __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_variation(VariationSp
 // ---- row-sharded runs over peer memory (run.cu) ------------------------------------------------------------------
 // home[child[j]] = the rank that builds child row j this generation (partition_rows, modes.cpp:506-516)
 __global__ void __launch_bounds__(kSlotThreads) k_ga_home_children(const int32_t* __restrict__ child, int s, int block, int32_t* home) {
+    griddep_launch();
+    griddep_wait();
     const int j = blockIdx.x * blockDim.x + threadIdx.x;
     if (j < s) home[child[j]] = j / block;
 }
 // after a variation launch: the parent rows it read remotely now have a local copy
 __global__ void __launch_bounds__(kSlotThreads) k_ga_home_adopt(const int32_t* __restrict__ parent, const int32_t* __restrict__ partner,
                                                                 int lo, int hi, int self, int32_t* home) {
+    griddep_launch();
+    griddep_wait();
     const int i = lo + blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= hi) return;
     home[parent[i]] = self;
@@ -85,6 +91,8 @@ __global__ void __launch_bounds__(kSlotThreads) k_ga_home_adopt(const int32_t* _
 __global__ void __launch_bounds__(kSlotThreads) k_ga_fetch_rows(int32_t* __restrict__ pool, const int32_t* const* __restrict__ bases,
                                                                 const int32_t* __restrict__ home, const int32_t* __restrict__ parent,
                                                                 int k, int self) {
+    griddep_launch();
+    griddep_wait();
     const int slot = parent[blockIdx.y];
     const int h = home[slot];
     if (h == self) return;
@@ -98,6 +106,8 @@ __global__ void __launch_bounds__(kSlotThreads) k_ga_fetch_rows(int32_t* __restr
     }
 }
 __global__ void __launch_bounds__(kSlotThreads) k_ga_home_all_local(const int32_t* __restrict__ parent, int s, int self, int32_t* home) {
+    griddep_launch();
+    griddep_wait();
     const int i = blockIdx.x * blockDim.x + threadIdx.x;
     if (i < s) home[parent[i]] = self;
 }
@@ -107,6 +117,8 @@ __global__ void __launch_bounds__(kSlotThreads) k_ga_home_all_local(const int32_
 static constexpr int kSplit = 8;
 __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_rank(const double* __restrict__ fit, const double* __restrict__ fit_m,
                                                                 int s, int minimize, int32_t* __restrict__ order, int* status) {
+    griddep_launch();
+    griddep_wait();
     __shared__ unsigned long long tile[kSlotThreads];
     const int x = blockIdx.x * (kSlotThreads / kSplit) + threadIdx.x / kSplit, part = threadIdx.x % kSplit;
     const int total = 2 * s;
@@ -181,6 +193,8 @@ __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_rebuild(VariationPara
                                                                    const int32_t* __restrict__ child,
                                                                    const int32_t* __restrict__ partner, int k, int s,
                                                                    const int32_t* __restrict__ order, int block_lo, int block_hi) {
+    griddep_launch();
+    griddep_wait();
     __shared__ uint64_t keys[4];
     const int x = order[blockIdx.y];  // blockIdx.y = rank < s: a survivor
     const int row = x - s;
@@ -200,6 +214,8 @@ __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_commit(const int32_t*
                                                                   const double* __restrict__ fit, const double* __restrict__ fit_m, int s,
                                                                   const int32_t* __restrict__ order, int32_t* __restrict__ next_parent,
                                                                   int32_t* __restrict__ next_child, double* __restrict__ next_fit) {
+    griddep_launch();
+    griddep_wait();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r >= s) return;
     const int keep = order[r], drop = order[s + r];
@@ -226,6 +242,8 @@ __global__ void __launch_bounds__(1024) k_ga_slots_elitism_small(const int32_t* 
     __shared__ double warp_sum[32];
     __shared__ int not_exact;
     const int tid = threadIdx.x, total = 2 * s;
+    griddep_launch();
+    griddep_wait();  // the evaluation that wrote fit_m
     const double mine = tid < total ? (tid < s ? fit[tid] : fit_m[tid - s]) : 0.0;
     if (tid < total) {
         f[tid] = mine;
@@ -334,6 +352,8 @@ __global__ void __launch_bounds__(1024) k_ga_slots_elitism_small(const int32_t* 
 }
 
 __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_identity(int s, int32_t* parent, int32_t* child) {
+    griddep_launch();
+    griddep_wait();
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
     if (r < s) {
         parent[r] = r;
@@ -344,6 +364,8 @@ __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_identity(int s, int32
 // dense row-major copy of the rows a table names (population.hpp:12-40)
 __global__ void __launch_bounds__(kSlotThreads) k_ga_slots_gather(const int32_t* __restrict__ pool, const int32_t* __restrict__ table,
                                                                   int k, int32_t* __restrict__ out) {
+    griddep_launch();
+    griddep_wait();
     const int32_t* from = pool + static_cast<size_t>(table[blockIdx.y]) * k;
     int32_t* to = out + static_cast<size_t>(blockIdx.y) * k;
     for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < k; j += gridDim.x * blockDim.x) to[j] = from[j];
@@ -412,7 +434,7 @@ int launch_slots_elitism_small(const int32_t* parent, const int32_t* child, int 
                                int32_t* next_parent, int32_t* next_child, double* next_fit, int32_t* order, int* status,
                                double* hist_best, double* hist_mean, int select_next, uint64_t seed, uint64_t next_generation,
                                int32_t* partner, double* weights, double* cumulative, cudaStream_t st) {
-    GAPA_LAUNCH(k_ga_slots_elitism_small, 1, 1024, 0, st, parent, child, fit, fit_m, s, minimize, order, next_parent, next_child,
+    GAPA_LAUNCH_PDL(k_ga_slots_elitism_small, 1, 1024, 0, st, parent, child, fit, fit_m, s, minimize, order, next_parent, next_child,
                 next_fit, status, hist_best, hist_mean, select_next, seed, next_generation, partner, weights, cumulative);
     return GAPA_CUDA_OK;
 }
