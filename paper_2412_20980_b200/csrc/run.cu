@@ -404,7 +404,8 @@ int gapa_cuda_ga::generation(int gen) {
     if (!small) GAPA_LAUNCH(k_ga_stats, 1, 1024, 0, st, fit, s, hist + (gen - 1), hist + iters + (gen - 1));
     // NaN / non-finite fitness is an Error in the reference (ga_ops.cpp:56-57, :189-192);
     // the flag is polled every few generations and at the end to keep the loop asynchronous.
-    if ((gen & 15) == 0 || gen == iters) {
+    // (every 16 generations; every 64 where a generation is two launches of ~10 us and the drain of a poll is a whole generation)
+    if ((gen & (small ? 63 : 15)) == 0 || gen == iters) {
         GAPA_TRY(poll_status("elitism: NaN fitness"));
         if (stride == 1 && world == 1 && timer.last_ms >= 0.f && timer.last_ms < kSampleBelowMs) {
             // A timing event between two kernels costs ~5 us of device time: short evaluations switch to SAMPLED marks
