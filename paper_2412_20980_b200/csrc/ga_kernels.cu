@@ -548,6 +548,15 @@ struct OpScratch {
     DevBuf a, b, c;
     int* status = nullptr;
     int* h_status = nullptr;  // pinned
+    OpScratch() = default;
+    OpScratch(const OpScratch&) = delete;
+    OpScratch& operator=(const OpScratch&) = delete;
+    ~OpScratch() {  // the owning thread ends, or the pool is trimmed (cudaFree waits for work that still uses the buffers)
+        a.release();
+        b.release();
+        c.release();
+        if (h_status) cudaFreeHost(h_status);
+    }
     int init(cudaStream_t st) {
         GAPA_TRY(c.ensure(sizeof(int)));
         status = c.as<int>();
@@ -572,7 +581,11 @@ static OpScratch& op_scratch(cudaStream_t st) {
     static thread_local std::map<Key, OpScratch> pool;
     int device = 0;
     cudaGetDevice(&device);
-    return pool[Key{device, st}];
+    const Key key{device, st};
+    // streams come and go in a long-lived host thread: entries of streams that no longer exist are dropped wholesale once
+    // the pool has grown past what any live set of streams needs (they are re-created on demand)
+    if (pool.size() >= 64 && pool.find(key) == pool.end()) pool.clear();
+    return pool[key];
 }
 
 }  // namespace gapa_b200
