@@ -77,13 +77,17 @@ def test_c5_corner_population_16384(gp, oracle, cuda_device):
     assert np.array_equal(res.final_fitness[rows], oracle.eval_batch(og, 0, res.final_population[rows], threads=16))
 
 
-def test_large_population_run_matches_oracle(gp, oracle, cuda_device):
+@pytest.mark.parametrize("ranking", ["default", "sorted-tiles", "counting"])
+def test_large_population_run_matches_oracle(gp, oracle, cuda_device, monkeypatch, ranking):
     """Large ragged population sizes (multi-block ranking, weight and pick kernels),
-    ragged, on a small graph so that fitness ties are everywhere (stable tie-breaks matter)."""
+    ragged, on a small graph so that fitness ties are everywhere (stable tie-breaks matter).  Both elitism rankings: binary
+    searches over sorted tiles of 1024 (the default from 2048 individuals on) and the counting kernel."""
+    if ranking != "default":
+        monkeypatch.setenv("GAPA_RANK_TILES_MIN", "1" if ranking == "sorted-tiles" else "100000000")
     g = gp.erdos_renyi(80, 0.05, 7)
     pool = gp.build_gene_pool(g, gp.PoolKind.NodeRemoval)
     og = oracle.graph_from_edges(g.n, g.edges())
-    for s, eda in [(4100, 0), (9001, 2)]:
+    for s, eda in [(4100, 0), (9001, 2), (700, 0), (1024, 3)]:
         params = gp.GAParams(pc=0.7, pm=0.15, pop_size=s, budget=6, iterations=4, seed=21, eda_interval=eda or None)
         res = gp.run_ga(params, pool, gp.PairwiseConnectivityObjective(g, pool))
         _same(res, oracle.run_ga(og, 0, 0.7, 0.15, s, 6, 4, 21, eda_interval=eda, threads=8))
