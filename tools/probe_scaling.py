@@ -48,6 +48,14 @@ for mode in os.environ.get("PROBE_MODES", "rebuild,peer").split(","):
         loop = gp.GaLoop(params, obj, rank=0, world=world, exchange=exchange if world > 1 else None)
         loop.advance(5)
         out[mode][world] = loop.advance(20) / 20
+        if os.environ.get("PROBE_PROFILE"):  # per-kernel device time of a generation at this world size (stderr)
+            from torch.profiler import ProfilerActivity, profile
+            with profile(activities=[ProfilerActivity.CUDA]) as prof:
+                loop.advance(5)
+                torch.cuda.synchronize()
+            rows = sorted(((e.key, e.device_time_total / 5 / 1000.0) for e in prof.key_averages()), key=lambda r: -r[1])
+            print(f"[{mode} world {world}] " + "; ".join(f"{k_.split('(')[0].replace('void gapa_b200::', '')[:26]} {t:.4f}" for k_, t in rows[:14]),
+                  file=sys.stderr)
         loop.close()
         del block
 res = {"n": n, "pop": s, "k": k, "scaling": "weak (pop x world)" if weak else "strong", "ms_per_generation_per_rank": out,
