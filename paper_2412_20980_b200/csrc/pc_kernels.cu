@@ -112,6 +112,7 @@ struct PcScratch {
     int uf_mode = -1;
     DevBuf uf_scratch, uf_out;
     cudaEvent_t ev_t0 = nullptr, ev_t1 = nullptr;
+    int mask_threads_forced = 0;  // GAPA_PC_MASK_THREADS: CTA size of the mask kernels (multiple of 128; 0 = by the genes per row)
     int mask_rows = 1;  // GAPA_PC_MASK_ROWS: persistent pipelined mask kernel for whole bitmaps (0: one CTA per row and chunk)
     int sweep_prefetch = 32;  // GAPA_PC_SWEEP_PREFETCH: chunks ahead (SweepArgs::prefetch_chunks); C4 sweep 0.447 / 0.442 / 0.436 / 0.435 / 0.437 / 0.439 / 0.459 ms at 0 / 8 / 16 / 32 / 64 / 128 / 256 (tools/ab_sweep_prefetch.sh)
     int fresh_skip = 0;  // GAPA_PC_FRESH_SKIP: the first sweep does not load records that are known to be clear (SweepArgs::fresh_from)
@@ -1733,9 +1734,15 @@ static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLan
         // fused kernel: one 16-byte quad per thread and pass; plain kernel: two 32-byte loads per thread and pass
         // (with a bitmap that leaves room for only a few CTAs per SM the kernels live on the bytes each CTA keeps in
         // flight and keep the full 1024 threads: C4 measured 1.93 ms with 1024 against 1.95 ms with 896)
-        const int mask_threads = chunk_bits / 8 > 32 * 1024
-                                     ? kMaskThreads
-                                     : mask_cta(std::max({fused_mask ? cols / 4 : cols / 16, chunk_bits / 512, 1}));
+        int mask_threads = chunk_bits / 8 > 32 * 1024
+                               ? kMaskThreads
+                               : mask_cta(std::max({fused_mask ? cols / 4 : cols / 16, chunk_bits / 512, 1}));
+        // The PERSISTENT fused kernel prefers many small CTAs per SM where the bitmap allows it (their prologues and epilogues
+        // overlap each other's hashing) as soon as there are rows enough to fill them: n = 1e5 (k = 5000, 12.5 KB bitmap),
+        // 128 instead of 640 threads: 4096 rows 0.356 -> 0.310 ms per generation, 16,384 rows 1.032 -> 0.893, 1024 rows
+        // 0.214 -> 0.203; 256 rows 0.129 -> 0.132 (kept at the old rule).  tools: GAPA_PC_MASK_THREADS.
+        if (fused_mask && chunk_bits / 8 <= 32 * 1024 && crows >= 4 * sm) mask_threads = 128;
+        if (s->mask_threads_forced > 0) mask_threads = s->mask_threads_forced;  // GAPA_PC_MASK_THREADS (A/B)
         if (fused_mask) {
             VariationSpec pass = *job.vary;
             pass.row_first += row0;
@@ -2008,6 +2015,7 @@ int pc_eval(gapa_cuda_ctx* ctx, int task, GeneRows genes, int rows, double* out_
         s->vary_waves = env_int("GAPA_PC_VARY_WAVES", 1, 1, 1 << 20);
         s->fresh_skip = env_int("GAPA_PC_FRESH_SKIP", 0, 0, 1);
         s->mask_rows = env_int("GAPA_PC_MASK_ROWS", 1, 0, 1);
+        s->mask_threads_forced = env_int("GAPA_PC_MASK_THREADS", 0, 0, 1024) / 128 * 128;
         s->uf_mode = env_int("GAPA_PC_UF", -1, -1, 1);
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_pc_uf<kUfThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, 200 * 1024));
         GAPA_CUDA_TRY(cudaEventCreate(&s->ev_t0));
