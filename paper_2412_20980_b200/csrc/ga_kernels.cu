@@ -248,9 +248,12 @@ __global__ void __launch_bounds__(kGaThreads) k_ga_weights(const double* __restr
 static constexpr int kPickSmemRows = 24576;  // 192 KB of running totals
 __global__ void __launch_bounds__(1024) k_ga_pick(const double* __restrict__ weights, int s, uint64_t seed,
                                                   uint64_t generation, double* __restrict__ cumulative,
-                                                  int32_t* __restrict__ partner, int in_smem) {
+                                                  int32_t* __restrict__ partner, int in_smem, int phase) {
     griddep_launch();
     griddep_wait();
+    // phase 0: scan + picks in one launch (the totals fit shared memory: every block redoes the scan and picks its 1024
+    // rows).  Populations beyond that: phase 1 = one block scans into `cumulative`, phase 2 = every block picks its rows
+    // from it (searches in L2) — instead of one block doing all s searches (s = 32,768: 0.18 ms).
     // The running totals live in shared memory when they fit (s <= kPickSmemRows): the s binary searches below are
     // chains of ~log2 s dependent reads, 30 ns each from shared memory against 300+ ns from L2.
     extern __shared__ double pick_cum[];
@@ -259,6 +262,7 @@ __global__ void __launch_bounds__(1024) k_ga_pick(const double* __restrict__ wei
     const int tid = threadIdx.x, lane = tid & 31, wid = tid >> 5;
     if (tid == 0) carry_s = 0.0;
     __syncthreads();
+    if (phase != 2)
     for (int t0 = 0; t0 < s; t0 += 1024) {  // tile-wise inclusive scan: warp shuffles, warp totals, running carry
         const int i = t0 + tid;
         double v = i < s ? weights[i] : 0.0;
@@ -286,7 +290,8 @@ __global__ void __launch_bounds__(1024) k_ga_pick(const double* __restrict__ wei
         if (tid == 1023) carry_s = v;
     }
     __syncthreads();
-    const double total = carry_s;
+    if (phase == 1) return;
+    const double total = phase == 2 ? cumulative[s - 1] : carry_s;
     const double* cum = in_smem ? pick_cum : cumulative;
     // the picks are chains of dependent instructions (four mix64 for the stream key, log2 s search steps): with the
     // totals in shared memory every block redoes the scan and then picks for its own 1024 rows, one row per thread
@@ -434,7 +439,12 @@ int launch_select(const double* fitness, int s, int minimize, uint64_t seed, uin
     const size_t pick_smem = in_smem ? sizeof(double) * static_cast<size_t>(s) : 0;
     if (pick_smem > 48 * 1024)  // per device and cheap: set whenever the launch needs it
         GAPA_CUDA_TRY(cudaFuncSetAttribute(k_ga_pick, cudaFuncAttributeMaxDynamicSharedMemorySize, sizeof(double) * kPickSmemRows));
-    GAPA_LAUNCH(k_ga_pick, in_smem ? (s + 1023) / 1024 : 1, 1024, pick_smem, st, weights, s, seed, generation, cumulative, partner, in_smem);
+    if (in_smem) {
+        GAPA_LAUNCH(k_ga_pick, (s + 1023) / 1024, 1024, pick_smem, st, weights, s, seed, generation, cumulative, partner, 1, 0);
+    } else {
+        GAPA_LAUNCH(k_ga_pick, 1, 1024, 0, st, weights, s, seed, generation, cumulative, partner, 0, 1);
+        GAPA_LAUNCH(k_ga_pick, (s + 1023) / 1024, 1024, 0, st, weights, s, seed, generation, cumulative, partner, 0, 2);
+    }
     return GAPA_CUDA_OK;
 }
 int launch_crossover_mutate(const int32_t* pop, const int32_t* partner, int k, int row_first, int row_count, double pc,
