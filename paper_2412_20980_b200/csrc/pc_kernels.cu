@@ -1690,7 +1690,12 @@ static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLan
     GAPA_TRY(set->unreached.ensure(sizeof(int) * pgroups * kBits));
     GAPA_TRY(set->pc_extra.ensure(sizeof(unsigned long long) * pgroups * kBits));
     GAPA_TRY(set->mcn_extra.ensure(sizeof(int) * pgroups * kBits));
-    GAPA_TRY(set->counters.ensure(sizeof(PcCounters)));
+    {
+        const size_t before = set->counters.cap;
+        GAPA_TRY(set->counters.ensure(sizeof(PcCounters)));
+        // a fresh block: k_pc_final copies the whole struct, including the field only the host copy uses (initcheck)
+        if (set->counters.cap != before) GAPA_CUDA_TRY(cudaMemsetAsync(set->counters.ptr, 0, set->counters.cap, stream));
+    }
     if (set->cap_entries == 0 || set->parent.cap < sizeof(int32_t) * (static_cast<size_t>(pgroups) * kBits + set->cap_slots))
         GAPA_TRY(ensure_phase2(set, pgroups, std::max<size_t>(set->cap_entries, 1u << 16), std::max<size_t>(set->cap_slots, 1u << 20)));
     word_t* alive = set->alive.as<word_t>();
