@@ -301,6 +301,7 @@ int gapa_cuda_comm_connect(gapa_cuda_comm* c, const void* all_handles) {
         }
     }
     GAPA_TRY(c->ctrl_stage.ensure(static_cast<size_t>(kCtrlBytes) * (c->world + 1)));
+    cudaMemset(c->ctrl_stage.ptr, 0, c->ctrl_stage.cap);  // slots are copied back whole; only `bytes` of each are written (initcheck)
     {   // ranks of this process that share a device meet on the host before every exchange (see HostBarrier)
         bool shared_device = false, one_process = true;
         CommHandle first{};
@@ -355,6 +356,7 @@ int gapa_cuda_comm_create_nccl(gapa_cuda_ctx* ctx, const void* unique_id128, int
         delete c;
         return GAPA_CUDA_E_NOMEM;
     }
+    cudaMemset(c->ctrl_stage.ptr, 0, c->ctrl_stage.cap);
     c->connected = true;
     *out = c;
     return GAPA_CUDA_OK;

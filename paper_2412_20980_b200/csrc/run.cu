@@ -495,6 +495,7 @@ extern "C" int gapa_cuda_ga_create(gapa_cuda_ctx* ctx, const gapa_cuda_run_param
         GAPA_CUDA_TRY(cudaMemsetAsync(ga->status, 0, sizeof(int), ga->st));
         GAPA_CUDA_TRY(cudaMemsetAsync(ga->fit, 0, sizeof(double) * ga->padded, ga->st));
         GAPA_CUDA_TRY(cudaMemsetAsync(ga->fit_m, 0, sizeof(double) * ga->padded, ga->st));
+        GAPA_CUDA_TRY(cudaMemsetAsync(ga->fit_next, 0, sizeof(double) * ga->padded, ga->st));  // exchanged whole, padding included
         GAPA_CUDA_TRY(cudaMemsetAsync(ga->hist, 0, sizeof(double) * 2 * iters, ga->st));
         // GenerationStats timing (modes.hpp:63-71): generation boundaries and the exchange hook are bracketed by events.
         // A small population's generation is two launches of 10-15 us, so there the marks are SAMPLED from generation 2
