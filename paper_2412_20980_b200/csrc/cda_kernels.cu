@@ -408,7 +408,9 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         for (;;) {
             if (hier) {
                 for (int g2 = warp; g2 < n_groups; g2 += kCdaWarps) {
-                    if (!dirty[g2]) continue;  // uniform within the warp
+                    const int is_dirty = dirty[g2];  // uniform within the warp
+                    __syncwarp();                    // every lane has read the flag before lane 0 clears it below
+                    if (!is_dirty) continue;
                     const int c = g2 * 32 + lane;
                     Cand x{0.0, c, -1};
                     if (c < n) {
