@@ -51,6 +51,8 @@ WORKLOADS = {
                  name="C5 point: CND-PC, BA n=1e5 attach=5, k=5000, pop 4096"),
     "n1e4": dict(task="pc", graph=("ba", 10_000, 5, 1), rate=0.05, pop=4096, pc=0.6, pm=0.2,
                  name="C5 point: CND-PC, BA n=1e4 attach=5, k=500, pop 4096"),
+    "n5e5": dict(task="pc", graph=("ba", 500_000, 5, 1), rate=0.05, pop=4096, pc=0.6, pm=0.2,
+                 name="between the C5 points: CND-PC, BA n=5e5 attach=5, k=25,000, pop 4096"),
 }
 TASK_ID = {"pc": 0, "mcn": 1, "cda": 2, "lpa": 3}
 

@@ -1747,6 +1747,9 @@ static int pc_run_lane(gapa_cuda_ctx* ctx, PcScratch* s, PcSet* set, const PcLan
         // 128 instead of 640 threads: 4096 rows 0.356 -> 0.310 ms per generation, 16,384 rows 1.032 -> 0.893, 1024 rows
         // 0.214 -> 0.203; 256 rows 0.129 -> 0.132 (kept at the old rule).  tools: GAPA_PC_MASK_THREADS.
         if (fused_mask && chunk_bits / 8 <= 32 * 1024 && crows >= 4 * sm) mask_threads = 128;
+        // bitmaps of which two still fit an SM (n = 5e5: 62.5 KB): two CTAs of 640 threads instead of one of 1024 —
+        // generation 0.951 -> 0.907 ms (256 / 384 / 512 / 640 / 768 threads: 0.923 / 0.912 / 0.916 / 0.907 / 0.973)
+        else if (fused_mask && chunk_bits / 8 <= 64 * 1024 && crows >= 4 * sm) mask_threads = 640;
         if (s->mask_threads_forced > 0) mask_threads = s->mask_threads_forced;  // GAPA_PC_MASK_THREADS (A/B)
         if (fused_mask) {
             VariationSpec pass = *job.vary;
