@@ -218,7 +218,7 @@ def run_reference_arm(args, w):
             rows.append(base["rows"])
     value = float(np.sum(rows) / np.sum(secs))
     base["value"] = value
-    s = args.pop or w["pop"]
+    s = (args.pop or w["pop"]) * (max(args.gpus, 1) if args.scaling == "weak" else 1)  # weak: the workload's population PER GPU
     world = max(args.gpus, 1)
     shape = workload_shape(w)
     # A step of this arm is a BOUNDED SAMPLE of the workload's step (rows_per_step individuals of the population,
@@ -226,7 +226,7 @@ def run_reference_arm(args, w):
     line = {"impl": "reference", "metric": "fitness_evals_per_sec", "value": value, "unit": "evals/s", "n_gpus": args.gpus,
             "steps": steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(secs)), "rows_per_step": int(np.mean(rows)),
             "step_is_sample": True, "ms_per_full_step_extrapolated": 1e3 * s / value,
-            "higher_is_better": True, "scaling": "strong", "vs_baseline": None,
+            "higher_is_better": True, "scaling": args.scaling, "vs_baseline": None,
             "dtype": "int64" if w["task"] in ("pc", "mcn") else "f64", "data": "synthetic",
             "config": config_of(w, s, shape["budget"], shape["n"], shape["m"], world, (s + world - 1) // world),
             "cpu_baseline": base,
@@ -282,7 +282,7 @@ def run_gpu_arm(args, w):
         base_graph = graph
     n, m = base_graph.node_count(), base_graph.edge_count()
     k = gp.perturbation_budget(base_graph, pool.kind(), w["rate"])
-    s = args.pop or w["pop"]
+    s = (args.pop or w["pop"]) * (max(args.gpus, 1) if args.scaling == "weak" else 1)  # weak: the workload's population PER GPU
     params = gp.GAParams(pc=w["pc"], pm=w["pm"], pop_size=s, budget=k, iterations=args.warmup + args.steps + 1, seed=1)
     shard = Shard(rank, world, s)
     lib = gp.capi.load()
@@ -443,7 +443,7 @@ def run_gpu_arm(args, w):
         actual = traffic * (rows_per_rank / s) / (eval_ms_mean * 1e-3) / 1e9 if traffic else None
         line = {
             "metric": "fitness_evals_per_sec", "value": value, "unit": "evals/s", "n_gpus": world, "steps": args.steps,
-            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": "strong",
+            "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True, "scaling": args.scaling,
             "vs_baseline": None, "dtype": "int64" if task in ("pc", "mcn") else "f64", "data": "synthetic",
             "config": config_of(w, s, k, n, m, world, rows_per_rank),
             "generations_per_sec": 1e3 / ms_per_step,
@@ -512,6 +512,8 @@ def main():
     ap.add_argument("--workload", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--pop", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--scaling", default="strong", choices=["strong", "weak"],
+                    help="N > 1: strong = the workload's population sharded over the GPUs (north_star's C4); weak = that population per GPU")
     ap.add_argument("--exchange", default="auto", choices=["auto", "peer", "nccl"],
                     help="N > 1: the library's exchange transport (auto = peer mailboxes where every GPU reaches every other)")
     args = ap.parse_args()
