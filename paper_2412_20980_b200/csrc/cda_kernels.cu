@@ -154,17 +154,18 @@ extern "C" int gapa_cuda_cda_phase_cycles(unsigned long long* out8, int reset) {
 #define CDA_TICK(k) do { } while (0)
 #endif
 
-__global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows genes, int rows,
+template <int kT>  // threads per CTA: 512 for graphs up to 8192 vertices, 1024 beyond (measured, cda_eval)
+__global__ void __launch_bounds__(kT, 1) k_cda(CdaArgs A, GeneRows genes, int rows,
                                                         int pos_in_smem, double* __restrict__ out,
                                                         int32_t* __restrict__ owner_out, int hier_off) {
     griddep_launch();
     griddep_wait();
-    __shared__ Cand warp_cand[kCdaWarps];
+    __shared__ Cand warp_cand[(kT / 32)];
     __shared__ Cand chosen;
     __shared__ long long sh_total;
     __shared__ long long sh_pool_top;
     __shared__ int sh_len, sh_pb, sh_new_head, sh_abort, sh_count;
-    __shared__ int sh_scan[kCdaThreads];
+    __shared__ int sh_scan[kT];
     __shared__ int long_queue[kCdaLongQueue];
     __shared__ int work_queue[kCdaWorkQueue];
     __shared__ int sh_long, sh_work;
@@ -208,14 +209,14 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         // EdgeRemoval: bit per edge rank.  EdgeAddition: bit per pool gene, so that a repeated gene
         // adds its pair once; merged_into[] doubles as the per-vertex count of added edges.
         const bool adding = A.add_u != nullptr;
-        for (int w = tid; w < A.mask_words; w += kCdaThreads) gone[w] = 0u;
+        for (int w = tid; w < A.mask_words; w += kT) gone[w] = 0u;
         if (adding)
-            for (int u = tid; u < n; u += kCdaThreads) merged_into[u] = 0;
+            for (int u = tid; u < n; u += kT) merged_into[u] = 0;
         if (tid == 0) { sh_total = 0; sh_abort = 0; }
         __syncthreads();
         const int cols = genes.cols;
         const int32_t* g = genes.row(r);
-        for (int j = tid; j < cols; j += kCdaThreads) {
+        for (int j = tid; j < cols; j += kT) {
             const int gene = g[j];
             if (gene < 0 || gene >= A.pool_size) { A.status[0] = GAPA_CUDA_E_RANGE; sh_abort = 1; continue; }
             if (adding) {
@@ -237,7 +238,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         // ---- singleton communities: list(u) = perturbed adjacency row ------------------
         long long my_deg = 0;
         if (!adding) {  // surviving CSR row, in place
-            for (int u = tid; u < n; u += kCdaThreads) {
+            for (int u = tid; u < n; u += kT) {
                 const int off = A.row_ptr[u], end = A.row_ptr[u + 1];
                 int cnt = 0;
                 for (int i = off; i < end; ++i) {
@@ -253,13 +254,13 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                 my_deg += cnt;
             }
         } else {  // CSR row followed by room for the added pairs: heads by a block-wide prefix sum
-            const int per = (n + kCdaThreads - 1) / kCdaThreads;
+            const int per = (n + kT - 1) / kT;
             const int u_lo = min(tid * per, n), u_hi = min(u_lo + per, n);
             int want = 0;
             for (int u = u_lo; u < u_hi; ++u) want += A.row_ptr[u + 1] - A.row_ptr[u] + merged_into[u];
             sh_scan[tid] = want;
             __syncthreads();
-            for (int off = 1; off < kCdaThreads; off <<= 1) {
+            for (int off = 1; off < kT; off <<= 1) {
                 const int add = tid >= off ? sh_scan[tid - off] : 0;
                 __syncthreads();
                 sh_scan[tid] += add;
@@ -278,7 +279,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             }
             my_deg = want;
             __syncthreads();
-            for (int j = tid; j < cols; j += kCdaThreads) {  // the thread that clears a gene's bit appends its pair
+            for (int j = tid; j < cols; j += kT) {  // the thread that clears a gene's bit appends its pair
                 const int gene = g[j];
                 const int a = A.add_u[gene];
                 if (a < 0) continue;
@@ -308,9 +309,9 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         if (tid == 0) sh_pool_top = adding ? total_degree : A.csr_slots;
 
         if (hier)
-            for (int g2 = tid; g2 < n_groups; g2 += kCdaThreads) dirty[g2] = 1;
+            for (int g2 = tid; g2 < n_groups; g2 += kT) dirty[g2] = 1;
         // initial cached bests
-        for (int u = tid; u < n; u += kCdaThreads) {
+        for (int u = tid; u < n; u += kT) {
             const int h = head[u], l = len[u], du = cdeg[u];
             Cand best{0.0, u, -1};
             for (int i = 0; i < l; ++i) {
@@ -407,7 +408,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
 #endif
         for (;;) {
             if (hier) {
-                for (int g2 = warp; g2 < n_groups; g2 += kCdaWarps) {
+                for (int g2 = warp; g2 < n_groups; g2 += (kT / 32)) {
                     const int is_dirty = dirty[g2];  // uniform within the warp
                     __syncwarp();                    // every lane has read the flag before lane 0 clears it below
                     if (!is_dirty) continue;
@@ -433,7 +434,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                 __syncthreads();
             } else {
                 Cand mine{0.0, -1, -1};
-                for (int c = tid; c < n; c += kCdaThreads) {
+                for (int c = tid; c < n; c += kT) {
                     const int b = best_id[c];
                     if (b >= 0) {
                         const Cand x{best_gain[c], c, b};
@@ -444,7 +445,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                 if (lane == 0) warp_cand[warp] = mine;
                 __syncthreads();
                 if (warp == 0) {
-                    Cand x = lane < kCdaWarps ? warp_cand[lane] : Cand{0.0, -1, -1};
+                    Cand x = lane < (kT / 32) ? warp_cand[lane] : Cand{0.0, -1, -1};
                     x = cand_warp_best(x);
                     if (lane == 0) chosen = x;
                 }
@@ -467,19 +468,19 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
                 __syncthreads();
                 if (sh_abort) break;
                 const int nh = sh_new_head;
-                for (int i = tid; i < la; i += kCdaThreads) { e_id[nh + i] = e_id[ha + i]; e_cnt[nh + i] = e_cnt[ha + i]; }
+                for (int i = tid; i < la; i += kT) { e_id[nh + i] = e_id[ha + i]; e_cnt[nh + i] = e_cnt[ha + i]; }
                 __syncthreads();
                 if (tid == 0) { head[a] = nh; cap[a] = 2 * (la + lb); }
                 ha = nh;
             }
             // positions of list(a) in the map
-            for (int i = tid; i < la; i += kCdaThreads) pos[e_id[ha + i]] = i;
+            for (int i = tid; i < la; i += kT) pos[e_id[ha + i]] = i;
             if (tid == 0) sh_len = la;
             __syncthreads();
             CDA_TICK(1);  // room + mark positions
             if (tid == 0) sh_pb = pos[b];
             // fold list(b) into list(a); every neighbour of b ends up in the map, flagged
-            for (int j = tid; j < lb; j += kCdaThreads) {
+            for (int j = tid; j < lb; j += kT) {
                 const int c = e_id[hb + j];
                 if (c == a) continue;
                 const int e = e_cnt[hb + j];
@@ -523,7 +524,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             // whose list needs work — the neighbours of b, and neighbours whose cached best was a (their pair with
             // a only got worse).  A full queue makes the finder do the work itself.
             Cand best_a{0.0, a, -1};
-            for (int i = tid; i < la2; i += kCdaThreads) {
+            for (int i = tid; i < la2; i += kT) {
                 const int c = e_id[ha + i], e = e_cnt[ha + i];
                 if (c > a) {
                     const double gn = merge_gain(e, da, cdeg[c], m, den);
@@ -555,7 +556,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             const int n_long = min(sh_long, kCdaLongQueue);
             // warps [0, long_warps) take the long lists (one warp per list), the others the short ones (a group of lanes per
             // list); at least a quarter of the warps stay with the short lists
-            const int long_warps = min(n_long, kCdaWarps - kCdaWarps / 4);
+            const int long_warps = min(n_long, (kT / 32) - (kT / 32) / 4);
             if (warp < long_warps) {
                 for (int q = warp; q < n_long; q += long_warps) {
                     const int i = long_queue[q];
@@ -565,7 +566,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             } else {
                 const int gl = lane % kCdaGroup;
                 const unsigned gmask = ((1u << kCdaGroup) - 1u) << (lane - gl);
-                const int groups = (kCdaWarps - long_warps) * (32 / kCdaGroup);
+                const int groups = ((kT / 32) - long_warps) * (32 / kCdaGroup);
                 for (int w = (warp - long_warps) * (32 / kCdaGroup) + lane / kCdaGroup; w < n_work; w += groups) {
                     const int i = work_queue[w];
                     const int c = e_id[ha + i];
@@ -578,11 +579,11 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
             __syncthreads();
             CDA_TICK(6);  // list work (long lists)
             if (warp == 0) {
-                Cand x = lane < kCdaWarps ? warp_cand[lane] : Cand{0.0, a, -1};
+                Cand x = lane < (kT / 32) ? warp_cand[lane] : Cand{0.0, a, -1};
                 x = cand_warp_best(x);
                 if (lane == 0) { best_gain[a] = x.gain; best_id[a] = x.b; if (hier) dirty[a >> 5] = 1; }
             }
-            for (int i = tid; i < la2; i += kCdaThreads) pos[e_id[ha + i]] = -1;  // the map is empty again
+            for (int i = tid; i < la2; i += kT) pos[e_id[ha + i]] = -1;  // the map is empty again
             __syncthreads();
             CDA_TICK(7);  // best of the merged community + map reset
         }
@@ -591,7 +592,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         // detect_communities' partition (community.cpp:28-91) for the reporting path: the owner of
         // u is the root of its merge chain == the smallest member of its community.
         if (owner_out) {
-            for (int u = tid; u < n; u += kCdaThreads) {
+            for (int u = tid; u < n; u += kT) {
                 int root = u;
                 while (merged_into[root] != -1) root = merged_into[root];
                 owner_out[static_cast<size_t>(r) * n + u] = root;
@@ -602,7 +603,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         // Live communities in ascending id == first-appearance order.  A term that is
         // exactly zero cannot change the running sum, so only non-zero terms are queued.
         const double two_m = static_cast<double>(total_degree);
-        const int per = (n + kCdaThreads - 1) / kCdaThreads;
+        const int per = (n + kT - 1) / kT;
         const int c_lo = min(tid * per, n), c_hi = min(c_lo + per, n);
         int queued = 0;
         for (int c = c_lo; c < c_hi; ++c) {
@@ -620,7 +621,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         }
         sh_scan[tid] = queued;
         __syncthreads();
-        for (int off = 1; off < kCdaThreads; off <<= 1) {
+        for (int off = 1; off < kT; off <<= 1) {
             const int add = tid >= off ? sh_scan[tid - off] : 0;
             __syncthreads();
             sh_scan[tid] += add;
@@ -629,7 +630,7 @@ __global__ void __launch_bounds__(kCdaThreads, 1) k_cda(CdaArgs A, GeneRows gene
         int write = sh_scan[tid] - queued;
         for (int c = c_lo; c < c_hi; ++c)
             if (merged_into[c] == -1 && best_id[c]) head[write++] = c;  // head[] is free now: ordered queue
-        if (tid == kCdaThreads - 1) sh_count = sh_scan[tid];
+        if (tid == kT - 1) sh_count = sh_scan[tid];
         __syncthreads();
         if (tid == 0) {
             double q = 0.0;
@@ -688,9 +689,17 @@ int cda_eval(gapa_cuda_ctx* ctx, GeneRows genes, int rows, double* out_dev, cuda
         const size_t hier_bytes = n_groups * (sizeof(double) + 3 * sizeof(int32_t));
         const bool hier = s->hier_argmax && hier_at + hier_bytes <= 209 * 1024;  // 227 KB minus the kernel's static shared memory
         const size_t smem = hier ? hier_at + hier_bytes : base_smem;
-        GAPA_CUDA_TRY(cudaFuncSetAttribute(k_cda, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
-        GAPA_LAUNCH(k_cda, slots, kCdaThreads, smem, stream, A, genes, rows, pos_in_smem, out_dev, owner_out_dev,
-                    hier ? static_cast<int>(hier_at) : -1);
+        // CTA size: a merge step is a chain of barriers and dependent L2 round trips, cheaper with 16 warps than with 32 while
+        // the lists are short — C2 (n = 5000) 42.1 -> 40.4 ms with 512 threads, but n = 20,000 300 -> 348 ms (768: 41.1 / 319)
+        if (n <= 8192 && kCdaThreads == 1024) {
+            GAPA_CUDA_TRY(cudaFuncSetAttribute(k_cda<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            GAPA_LAUNCH(k_cda<512>, slots, 512, smem, stream, A, genes, rows, pos_in_smem, out_dev, owner_out_dev,
+                        hier ? static_cast<int>(hier_at) : -1);
+        } else {
+            GAPA_CUDA_TRY(cudaFuncSetAttribute(k_cda<kCdaThreads>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem)));
+            GAPA_LAUNCH(k_cda<kCdaThreads>, slots, kCdaThreads, smem, stream, A, genes, rows, pos_in_smem, out_dev, owner_out_dev,
+                        hier ? static_cast<int>(hier_at) : -1);
+        }
         GAPA_CUDA_TRY(cudaMemcpyAsync(ctx->h_status, s->status.ptr, 2 * sizeof(int), cudaMemcpyDeviceToHost, stream));
         GAPA_CUDA_TRY(cudaStreamSynchronize(stream));
         if (ctx->h_status[0] == GAPA_CUDA_E_RANGE) return fail(GAPA_CUDA_E_RANGE, "perturbation: gene id out of range");
