@@ -493,7 +493,7 @@ def run_gpu_arm(args, w):
                                     "evals_per_sec": s * (iters + 1) / run.total_wall_seconds,
                                     "eval_ms_per_generation": 1e3 * run.eval_seconds / (iters + 1)}
         if world == 1 and not args.no_cpu_baseline:
-            line["cpu_baseline"] = cpu_reference_throughput(w, 12.0, host_threads())
+            line["cpu_baseline"] = cpu_reference_throughput(w, 30.0, host_threads())
         print(json.dumps(line), flush=True)
     loop.close()
     if comm is not None:
