@@ -192,10 +192,17 @@ static constexpr int kSplit = 8;
 static constexpr int kPerBlock = kGaThreads / kSplit;
 
 __global__ void __launch_bounds__(kGaThreads) k_ga_weights(const double* __restrict__ fitness, int s, int minimize,
-                                                           double* __restrict__ weights, int* status) {
+                                                           double* __restrict__ weights, int* status, double* stats_best,
+                                                           double* stats_mean) {
     griddep_launch();
     griddep_wait();
     __shared__ unsigned long long tile[kGaThreads];
+    if (stats_best && blockIdx.x == gridDim.x - 1) {
+        // one extra block: best / mean of this population for the run's history (run.cu defers them to this launch)
+        __shared__ GaStatsSmem stats_sm;
+        ga_stats_block(fitness, s, stats_best, stats_mean, stats_sm);
+        return;
+    }
     const int i = blockIdx.x * kPerBlock + threadIdx.x / kSplit, part = threadIdx.x % kSplit;
     const double mine_f = i < s ? fitness[i] : 0.0;
     if (i < s && !isfinite(mine_f)) *status = GAPA_CUDA_E_NAN;
@@ -429,12 +436,15 @@ int launch_init(uint32_t pool_size, int row_first, int row_count, int budget, ui
     return GAPA_CUDA_OK;
 }
 int launch_select(const double* fitness, int s, int minimize, uint64_t seed, uint64_t generation, int32_t* partner,
-                  double* weights, double* cumulative, int* status, cudaStream_t st) {
+                  double* weights, double* cumulative, int* status, cudaStream_t st, double* stats_best = nullptr,
+                  double* stats_mean = nullptr) {
     if (s <= 1024) {
+        if (stats_best) return fail(GAPA_CUDA_E_INVALID, "select: statistics ride only on the multi-block selection");
         GAPA_LAUNCH(k_ga_select_small, 1, 1024, 0, st, fitness, s, minimize, seed, generation, weights, cumulative, partner, status);
         return GAPA_CUDA_OK;
     }
-    GAPA_LAUNCH(k_ga_weights, (s + kPerBlock - 1) / kPerBlock, kGaThreads, 0, st, fitness, s, minimize, weights, status);
+    GAPA_LAUNCH(k_ga_weights, (s + kPerBlock - 1) / kPerBlock + (stats_best ? 1 : 0), kGaThreads, 0, st, fitness, s, minimize, weights, status,
+                stats_best, stats_mean);
     const int in_smem = s <= kPickSmemRows ? 1 : 0;
     const size_t pick_smem = in_smem ? sizeof(double) * static_cast<size_t>(s) : 0;
     if (pick_smem > 48 * 1024)  // per device and cheap: set whenever the launch needs it

@@ -138,6 +138,57 @@ __device__ __forceinline__ bool draw_bernoulli(uint64_t key, uint64_t j, uint64_
 // in), key(x) == key(y) <=> x == y (-0.0 and +0.0 share a key).  The O(s^2) counting kernels of selection and
 // elitism compare these integers instead of doubles (two integer instructions per compare instead of FP64
 // set-predicates and a direction select).  NaN is reported separately and never ranked.
+// record_generation (modes.cpp:35-43) by ONE block of any size: best = front, mean = SEQUENTIAL sum / s so that non-integer
+// fitness reproduces std::accumulate bit for bit.  Shared by k_ga_stats (run.cu) and the statistics block of
+// k_ga_weights (ga_kernels.cu: the previous generation's statistics ride on the next generation's selection launch).
+struct GaStatsSmem {
+    double stage[4096];
+    double warp_sum[32];
+    int not_exact;
+};
+__device__ __forceinline__ void ga_stats_block(const double* __restrict__ fit, int s, double* best, double* mean, GaStatsSmem& sm) {
+    const int tid = threadIdx.x, nt = blockDim.x;
+    if (tid == 0) sm.not_exact = 0;
+    __syncthreads();
+    // Integer-valued fitness whose running sums stay below 2^53 (PC, MCN) adds exactly in any order.
+    double local = 0.0;
+    const double bound = 9007199254740992.0 / static_cast<double>(s);
+    for (int i = tid; i < s; i += nt) {
+        const double x = fit[i];
+        if (!(x == floor(x)) || !(fabs(x) < bound)) sm.not_exact = 1;
+        local += x;
+    }
+    __syncthreads();
+    if (!sm.not_exact) {
+        for (int off = 16; off; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
+        if ((tid & 31) == 0) sm.warp_sum[tid >> 5] = local;
+        __syncthreads();
+        if (tid < 32) {
+            double v = tid < (nt >> 5) ? sm.warp_sum[tid] : 0.0;
+            for (int off = 16; off; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
+            if (tid == 0) {
+                *best = fit[0];
+                *mean = v / static_cast<double>(s);
+            }
+        }
+        return;
+    }
+    // general FP64 fitness: the reference's left-to-right std::accumulate, staged through shared memory
+    double sum = 0.0;
+    for (int base = 0; base < s; base += 4096) {
+        const int lim = min(4096, s - base);
+        for (int i = tid; i < lim; i += nt) sm.stage[i] = fit[base + i];
+        __syncthreads();
+        if (tid == 0)
+            for (int i = 0; i < lim; ++i) sum += sm.stage[i];
+        __syncthreads();
+    }
+    if (tid == 0) {
+        *best = fit[0];
+        *mean = sum / static_cast<double>(s);
+    }
+}
+
 __device__ __forceinline__ unsigned long long order_key(double x, int minimize) {
     if (x == 0.0) x = 0.0;
     const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));

@@ -23,7 +23,8 @@
 
 namespace gapa_b200 {
 int launch_init(uint32_t, int, int, int, uint64_t, uint64_t, int32_t*, cudaStream_t);
-int launch_select(const double*, int, int, uint64_t, uint64_t, int32_t*, double*, double*, int*, cudaStream_t);
+int launch_select(const double*, int, int, uint64_t, uint64_t, int32_t*, double*, double*, int*, cudaStream_t, double* stats_best = nullptr,
+                  double* stats_mean = nullptr);
 int launch_crossover_mutate(const int32_t*, const int32_t*, int, int, int, double, double, uint32_t, uint64_t, uint64_t,
                             int32_t*, cudaStream_t);
 int launch_mutate(const int32_t*, int, int, int, double, uint32_t, uint64_t, uint64_t, int32_t*, cudaStream_t);
@@ -49,49 +50,8 @@ int launch_fetch_rows(int32_t*, const int32_t* const*, int32_t*, const int32_t*,
 __global__ void __launch_bounds__(1024) k_ga_stats(const double* __restrict__ fit, int s, double* best, double* mean) {
     griddep_launch();
     griddep_wait();
-    __shared__ double stage[4096];
-    __shared__ double warp_sum[32];
-    __shared__ int not_exact;
-    const int tid = threadIdx.x;
-    if (tid == 0) not_exact = 0;
-    __syncthreads();
-    // Integer-valued fitness whose running sums stay below 2^53 (PC, MCN) adds exactly in any order.
-    double local = 0.0;
-    const double bound = 9007199254740992.0 / static_cast<double>(s);
-    for (int i = tid; i < s; i += blockDim.x) {
-        const double x = fit[i];
-        if (!(x == floor(x)) || !(fabs(x) < bound)) not_exact = 1;
-        local += x;
-    }
-    __syncthreads();
-    if (!not_exact) {
-        for (int off = 16; off; off >>= 1) local += __shfl_down_sync(0xffffffffu, local, off);
-        if ((tid & 31) == 0) warp_sum[tid >> 5] = local;
-        __syncthreads();
-        if (tid < 32) {
-            double v = tid < (blockDim.x >> 5) ? warp_sum[tid] : 0.0;
-            for (int off = 16; off; off >>= 1) v += __shfl_down_sync(0xffffffffu, v, off);
-            if (tid == 0) {
-                *best = fit[0];
-                *mean = v / static_cast<double>(s);
-            }
-        }
-        return;
-    }
-    // general FP64 fitness: the reference's left-to-right std::accumulate, staged through shared memory
-    double sum = 0.0;
-    for (int base = 0; base < s; base += 4096) {
-        const int lim = min(4096, s - base);
-        for (int i = tid; i < lim; i += blockDim.x) stage[i] = fit[base + i];
-        __syncthreads();
-        if (tid == 0)
-            for (int i = 0; i < lim; ++i) sum += stage[i];
-        __syncthreads();
-    }
-    if (tid == 0) {
-        *best = fit[0];
-        *mean = sum / static_cast<double>(s);
-    }
+    __shared__ GaStatsSmem sm;
+    ga_stats_block(fit, s, best, mean, sm);
 }
 
 __global__ void k_check_nan(const double* __restrict__ fit, int s, int* status) {
@@ -284,6 +244,9 @@ struct gapa_cuda_ga {
         return flush_marks();
     }
     int generation(int gen);
+    int stats_pending_gen = 0;  // generation whose history entry has not been written yet (0 = none)
+    bool defer_stats = true;
+    int flush_stats(int gen);
     int setup_peer_rows();
     int fetch_all_parents() {  // every parent row local (EDA generations, the returned population)
         return launch_fetch_rows(pool_rows, bases_dev.as<const int32_t*>(), home.as<int32_t>(), parent, s, k, rank, st);
@@ -360,8 +323,13 @@ int gapa_cuda_ga::generation(int gen) {
     const bool eda_gen = p.eda_interval > 0 && gen % p.eda_interval == 0;  // modes.cpp:31-33,167-168
     const int32_t* partner = eda_gen ? nullptr : B.partner.as<int32_t>();
     if (!eda_gen && !(small && gen > 1))  // small populations: selected by the previous generation's elitism launch
+    {
+        // the previous generation's statistics, if they were deferred, ride on this selection's first launch (a block of their own)
+        const int sg = stats_pending_gen;
+        stats_pending_gen = 0;
         GAPA_TRY(launch_select(fit, s, minimize, p.seed, g, B.partner.as<int32_t>(), B.weights.as<double>(),
-                               B.cumulative.as<double>(), status, st));
+                               B.cumulative.as<double>(), status, st, sg ? hist + (sg - 1) : nullptr, sg ? hist + iters + (sg - 1) : nullptr));
+    }
     VariationSpec vary;  // the evaluation builds the children of rows [lo, hi) into their slots first
     vary.P = make_variation_params(p.pc, p.pm, pool, s, p.seed, g);
     vary.pool = pool_rows;
@@ -401,7 +369,14 @@ int gapa_cuda_ga::generation(int gen) {
         if (rc != 0) return fail(GAPA_CUDA_E_CUDA, "run: exchange hook failed with status %d", rc);
         final_fetch_done = true;
     }
-    if (!small) GAPA_LAUNCH(k_ga_stats, 1, 1024, 0, st, fit, s, hist + (gen - 1), hist + iters + (gen - 1));
+    if (!small) {
+        // Statistics of this generation (they read the new parents' fitness, like the next selection): a launch of their own
+        // is ~5 us on the critical path of a generation, so where the next generation starts with the multi-block selection
+        // they are deferred to an extra block of its first kernel (k_ga_weights); gapa_cuda_ga_result flushes a pending one.
+        const bool next_selects = gen < iters && !(p.eda_interval > 0 && (gen + 1) % p.eda_interval == 0) && s > 1024;
+        if (next_selects && defer_stats) stats_pending_gen = gen;
+        else GAPA_TRY(flush_stats(gen));
+    }
     // NaN / non-finite fitness is an Error in the reference (ga_ops.cpp:56-57, :189-192);
     // the flag is polled every few generations and at the end to keep the loop asynchronous.
     // (every 16 generations; every 64 where a generation is two launches of ~10 us and the drain of a poll is a whole generation)
@@ -414,6 +389,11 @@ int gapa_cuda_ga::generation(int gen) {
         }
     }
     gen_done = gen;
+    return GAPA_CUDA_OK;
+}
+
+int gapa_cuda_ga::flush_stats(int gen) {
+    GAPA_LAUNCH(k_ga_stats, 1, 1024, 0, st, fit, s, hist + (gen - 1), hist + iters + (gen - 1));
     return GAPA_CUDA_OK;
 }
 
@@ -504,6 +484,7 @@ extern "C" int gapa_cuda_ga_create(gapa_cuda_ctx* ctx, const gapa_cuda_run_param
         // switch to sampling at the first status poll (generation 16) if an evaluation takes less than kSampleBelowMs.
         ga->want_stats = want_stats != 0;
         ga->small = world == 1 && 2 * s <= 1024;
+        if (const char* raw = std::getenv("GAPA_DEFER_STATS")) ga->defer_stats = raw[0] != '0';
         ga->stride = ga->small ? kTimingStride : 1;
         ga->timer.pool = ga->first_timer.pool = ga->exchange_marks.pool = &ga->events;
         ga->exchange_of_gen.assign(static_cast<size_t>(iters), 0.0);
@@ -564,6 +545,10 @@ extern "C" int gapa_cuda_ga_result(gapa_cuda_ga* ga, gapa_cuda_run_result* resul
     const int iters = ga->iters, s = ga->s;
     if (ga->want_stats && ga->gen_done > 0 && (ga->marked_gens.empty() || ga->marked_gens.back() != ga->gen_done + 1))
         GAPA_TRY(ga->mark_generation(ga->gen_done + 1));  // closes the last block of generations
+    if (ga->stats_pending_gen) {  // fit still holds that generation's parents: nothing ran since
+        GAPA_TRY(ga->flush_stats(ga->stats_pending_gen));
+        ga->stats_pending_gen = 0;
+    }
     GAPA_CUDA_TRY(cudaStreamSynchronize(st));
     GAPA_TRY(ga->flush_marks());
     result->fitness_batch_calls = ga->fitness_batch_calls;

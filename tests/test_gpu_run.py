@@ -252,3 +252,28 @@ def test_sampled_timing_marks_keep_results_and_columns(gp, oracle, cuda_device):
         if s <= 512:  # always sampled; larger populations only when an evaluation is short (not under a sanitizer)
             assert len(set(walls[20:26])) <= 2  # generations between two marks share their mean
         assert res.fitness_batch_calls == iters + 1
+
+
+@pytest.mark.parametrize("defer", ["1", "0"])
+def test_deferred_statistics_fp64_and_midrun_result(gp, oracle, cuda_device, monkeypatch, defer):
+    """Populations beyond 1024: a generation's best / mean ride on the NEXT generation's selection launch (an extra block of
+    k_ga_weights, run.cu) unless that generation is an EDA one or the run ends.  Non-integer fitness (AUC) takes the
+    sequential-sum path of that block; a result() in the middle of a run flushes the pending entry and the run goes on."""
+    monkeypatch.setenv("GAPA_DEFER_STATS", defer)
+    g = gp.erdos_renyi(60, 0.12, 3)
+    split = gp.build_lp_split(g, 0.2, 5)
+    pool = gp.build_gene_pool(split.train, gp.PoolKind.EdgeRemoval)
+    os_ = oracle.split_build(oracle.graph_from_edges(g.n, g.edges()), 0.2, 5)
+    for s, eda in [(1100, 0), (1300, 3)]:
+        params = gp.GAParams(pc=0.7, pm=0.1, pop_size=s, budget=8, iterations=7, seed=13, eda_interval=eda or None)
+        want = oracle.run_ga(os_, 3, 0.7, 0.1, s, 8, 7, 13, eda_interval=eda, threads=8)
+        obj = gp.LinkPredictionAttackObjective(split, pool)
+        _same(gp.run_ga(params, pool, obj), want)
+        loop = gp.GaLoop(params, obj)
+        loop.advance(4)
+        mid = loop.result()  # generation 4's statistics were pending (generation 5 selects) unless it is an EDA one
+        assert np.array_equal(mid.history_best[:4], want["best"][:4]) and np.array_equal(mid.history_mean[:4], want["mean"][:4])
+        assert np.all(mid.history_best[4:] == 0)
+        loop.advance(100)
+        _same(loop.result(), want)
+        loop.close()
